@@ -1,0 +1,411 @@
+"""Cluster trees and admissibility block trees, built array-at-a-time.
+
+Host-side mirror of ``greencross/clustering.py``.  The public objects keep
+the reference's shapes (``BoundingBox`` ``:15-43``, ``admissible``
+``:46-51``, ``ClusterTree`` ``:54-104``, ``BlockTree`` ``:170-212``) and the
+results are bit-identical: same permutation, same boxes, same preorder
+indices, same leaves in the same depth-first order.  The construction is
+different: instead of one Python call per node the trees are grown one level
+at a time over flat arrays (segmented min/max, one stable ``lexsort`` per
+level, vectorised admissibility), which is what makes the host plan cheap
+enough at 0.5-2 M triangles (SURVEY.md §8 f, rank 1).  The flat arrays
+(``ClusterTree.flat`` and ``BlockTree.flat``) are what the device layout in
+``gca.py`` is built from.
+"""
+
+import numpy as np
+
+from .errors import ConfigError
+from .geometry import control_points
+
+ADMISSIBLE = "admissible"
+INADMISSIBLE = "inadmissible"
+SUBDIVIDED = "subdivided"
+
+
+def _blas_norm(v):
+    # 1-D numpy norm = sqrt(ddot(v, v)); the reference's rounding
+    return float(np.linalg.norm(v))
+
+
+class BoundingBox:
+    """Axis-parallel box (``clustering.py:15-43``)."""
+
+    __slots__ = ("lower", "upper")
+
+    def __init__(self, lower, upper):
+        self.lower = np.asarray(lower, dtype=float)
+        self.upper = np.asarray(upper, dtype=float)
+        if self.lower.shape != (3,) or self.upper.shape != (3,):
+            raise ConfigError("bounding box corners must be 3-vectors")
+        if np.any(self.lower > self.upper):
+            raise ConfigError("bounding box has lower > upper")
+
+    @classmethod
+    def of_points(cls, points):
+        p = np.asarray(points, dtype=float).reshape(-1, 3)
+        return cls(p.min(axis=0), p.max(axis=0))
+
+    def diameter(self):
+        return _blas_norm(self.upper - self.lower)
+
+    def distance(self, other):
+        gap = np.maximum(0.0, np.maximum(self.lower - other.upper,
+                                         other.lower - self.upper))
+        return _blas_norm(gap)
+
+    def __repr__(self):
+        return "BoundingBox(%s, %s)" % (self.lower.tolist(), self.upper.tolist())
+
+
+def admissible(tau, sigma, eta):
+    """Standard admissibility max(diam) <= 2 eta dist (``clustering.py:46-51``)."""
+    if eta <= 0:
+        raise ConfigError("eta must be positive, got %r" % (eta,))
+    return max(tau.diameter(), sigma.diameter()) <= 2.0 * eta * tau.distance(sigma)
+
+
+class ClusterTree:
+    """Node view of a flat cluster tree; ``perm[start:stop]`` are its dofs,
+    ``index`` its preorder number."""
+
+    __slots__ = ("perm", "start", "stop", "box", "children", "index", "flat")
+
+    def __init__(self, flat, index, box, children):
+        self.flat = flat
+        self.perm = flat.perm
+        self.index = index
+        self.start = int(flat.start[index])
+        self.stop = int(flat.stop[index])
+        self.box = box
+        self.children = children
+
+    @property
+    def size(self):
+        return self.stop - self.start
+
+    @property
+    def indices(self):
+        return self.perm[self.start:self.stop]
+
+    def is_leaf(self):
+        return not self.children
+
+    def nodes(self):
+        """Subtree nodes in preorder."""
+        return [self.flat.node(i) for i in range(self.index,
+                                                 self.index + int(self.flat.count[self.index]))]
+
+    def leaves(self):
+        return [n for n in self.nodes() if n.is_leaf()]
+
+    def depth(self):
+        sub = slice(self.index, self.index + int(self.flat.count[self.index]))
+        return int(self.flat.depth[sub].max() - self.flat.depth[self.index])
+
+    def __repr__(self):
+        return "ClusterTree(#%d, %d dofs, %s)" % (
+            self.index, self.size, "leaf" if self.is_leaf() else "2 children")
+
+
+class FlatClusterTree:
+    """Preorder arrays of a binary cluster tree.
+
+    ``start, stop, left, right (-1 for leaves), parent, depth, count
+    (subtree size in nodes), lower, upper (N,3), diam`` plus ``perm``.
+    ``diam`` is the reference's ``box.diameter()`` bit for bit.
+    """
+
+    def __init__(self, perm, start, stop, left, right, parent, depth, lower, upper):
+        self.perm = perm
+        self.start, self.stop = start, stop
+        self.left, self.right, self.parent, self.depth = left, right, parent, depth
+        self.lower, self.upper = lower, upper
+        n = len(start)
+        self.count = np.ones(n, dtype=np.int64)
+        for i in range(n - 1, -1, -1):       # children have larger indices
+            if left[i] >= 0:
+                self.count[i] = 1 + self.count[left[i]] + self.count[right[i]]
+        self.diam = np.array([_blas_norm(u - l) for l, u in zip(lower, upper)])
+        self.is_leaf = left < 0
+        # height: 0 for leaves, 1 + max(child heights) otherwise
+        h = np.zeros(n, dtype=np.int64)
+        for i in range(n - 1, -1, -1):
+            if left[i] >= 0:
+                h[i] = 1 + max(h[left[i]], h[right[i]])
+        self.height = h
+        self._nodes = [None] * n
+
+    def __len__(self):
+        return len(self.start)
+
+    def node(self, i):
+        nd = self._nodes[i]
+        if nd is None:
+            kids = () if self.left[i] < 0 else (self.node(int(self.left[i])),
+                                                 self.node(int(self.right[i])))
+            nd = ClusterTree(self, i, BoundingBox(self.lower[i], self.upper[i]), kids)
+            self._nodes[i] = nd
+        return nd
+
+
+def _support_data(mesh, basis_kind):
+    """Reference points and support bounds per dof (``clustering.py:107-128``)."""
+    ctrl = control_points(mesh)
+    lo, hi = ctrl.min(axis=1), ctrl.max(axis=1)
+    if basis_kind == "constant":
+        return mesh.centroids(), lo, hi
+    stars = mesh.vertex_stars()
+    sizes = np.array([len(s) for s in stars])
+    if np.any(sizes == 0):
+        raise ConfigError("mesh has isolated vertices")
+    adj = np.concatenate(stars)
+    first = np.concatenate(([0], np.cumsum(sizes)))[:-1]
+    return (mesh.vertices.copy(), np.minimum.reduceat(lo[adj], first, axis=0),
+            np.maximum.reduceat(hi[adj], first, axis=0))
+
+
+def _subtree_counts(size, leaf_size, memo):
+    if size not in memo:
+        if size <= leaf_size:
+            memo[size] = 1
+        else:
+            h = size // 2
+            memo[size] = (1 + _subtree_counts(h, leaf_size, memo)
+                          + _subtree_counts(size - h, leaf_size, memo))
+    return memo[size]
+
+
+def build_cluster_tree(mesh, basis_kind="constant", leaf_size=32):
+    """Binary cluster tree: split at the positional median along the longest
+    box axis, stable in the reference point coordinate
+    (``clustering.py:131-162``).  Returns the root :class:`ClusterTree`."""
+    if basis_kind not in ("constant", "linear"):
+        raise ConfigError("unknown basis kind %r" % (basis_kind,))
+    if leaf_size < 1:
+        raise ConfigError("leaf_size must be >= 1")
+    points, lo, hi = _support_data(mesh, basis_kind)
+    n = len(points)
+    memo = {}
+    total = _subtree_counts(n, leaf_size, memo)
+    start = np.zeros(total, dtype=np.int64)
+    stop = np.zeros(total, dtype=np.int64)
+    left = np.full(total, -1, dtype=np.int64)
+    right = np.full(total, -1, dtype=np.int64)
+    parent = np.full(total, -1, dtype=np.int64)
+    depth = np.zeros(total, dtype=np.int64)
+    lower = np.zeros((total, 3))
+    upper = np.zeros((total, 3))
+    perm = np.arange(n)
+    # one padding row so that reduceat may address index n
+    lo_pad = lambda p: np.concatenate([lo[p], lo[:1]])
+    hi_pad = lambda p: np.concatenate([hi[p], hi[:1]])
+
+    # frontier of one tree depth: node ids with contiguous [start, stop)
+    ids = np.array([0], dtype=np.int64)
+    stop[0] = n
+    d = 0
+    while ids.size:
+        s, e = start[ids], stop[ids]
+        depth[ids] = d
+        # boxes: segmented min/max over the current permutation (the
+        # frontier may have gaps where shallower leaves sit, so reduce over
+        # explicit [start, stop) pairs and drop the in-between reductions)
+        bounds = np.stack([s, e], axis=1).ravel()
+        lower[ids] = np.minimum.reduceat(lo_pad(perm), bounds, axis=0)[::2]
+        upper[ids] = np.maximum.reduceat(hi_pad(perm), bounds, axis=0)[::2]
+        split = (e - s) > leaf_size
+        if not split.any():
+            break
+        ids_s, s_s, e_s = ids[split], s[split], e[split]
+        axis = np.argmax(upper[ids_s] - lower[ids_s], axis=1)
+        seg_len = e_s - s_s
+        seg_of = np.repeat(np.arange(len(ids_s)), seg_len)
+        heads = np.cumsum(seg_len) - seg_len
+        pos = np.arange(int(seg_len.sum())) + np.repeat(s_s - heads, seg_len)
+        key = points[perm[pos], axis[seg_of]]
+        order = np.lexsort((key, seg_of))        # stable within each segment
+        perm[pos] = perm[pos[order]]
+        half = seg_len // 2
+        lid = ids_s + 1
+        rid = ids_s + 1 + np.array([memo[int(h)] for h in half], dtype=np.int64)
+        left[ids_s], right[ids_s] = lid, rid
+        parent[lid], parent[rid] = ids_s, ids_s
+        start[lid], stop[lid] = s_s, s_s + half
+        start[rid], stop[rid] = s_s + half, e_s
+        ids = np.concatenate([lid, rid])
+        ids = ids[np.argsort(start[ids], kind="stable")]
+        d += 1
+    flat = FlatClusterTree(perm, start, stop, left, right, parent, depth, lower, upper)
+    return flat.node(0)
+
+
+# --------------------------------------------------------------------------
+# block tree
+
+class BlockTree:
+    """Node view of the flat block tree (``clustering.py:170-212``)."""
+
+    __slots__ = ("row", "col", "state", "_flat", "_id")
+
+    def __init__(self, flat, i):
+        self._flat, self._id = flat, i
+        self.row = flat.row_tree.node(int(flat.row[i]))
+        self.col = flat.col_tree.node(int(flat.col[i]))
+        self.state = (ADMISSIBLE, INADMISSIBLE, SUBDIVIDED)[int(flat.state[i])]
+
+    @property
+    def children(self):
+        f = self._flat
+        return tuple(BlockTree(f, int(j)) for j in f.kids(self._id))
+
+    def is_leaf(self):
+        return self.state != SUBDIVIDED
+
+    def _leaf_ids(self, which=None):
+        f = self._flat
+        lo, hi = f.key_lo[self._id], f.key_hi[self._id]
+        a, b = np.searchsorted(f.leaf_key, [lo, hi], side="left")
+        sel = f.leaf_ids[a:b]
+        if which is not None:
+            sel = sel[f.state[sel] == which]
+        return sel
+
+    def leaves(self):
+        return [BlockTree(self._flat, int(j)) for j in self._leaf_ids()]
+
+    def admissible_leaves(self):
+        return [BlockTree(self._flat, int(j)) for j in self._leaf_ids(0)]
+
+    def inadmissible_leaves(self):
+        return [BlockTree(self._flat, int(j)) for j in self._leaf_ids(1)]
+
+    def depth(self):
+        f = self._flat
+        ids = self._leaf_ids()
+        return int(f.level[ids].max() - f.level[self._id]) if len(ids) else 0
+
+    def stats(self):
+        ids = self._leaf_ids()
+        adm = int((self._flat.state[ids] == 0).sum())
+        return {"depth": self.depth(), "leaves": len(ids), "admissible": adm,
+                "inadmissible": len(ids) - adm}
+
+    @property
+    def flat(self):
+        return self._flat
+
+    def __repr__(self):
+        return "BlockTree(row #%d x col #%d, %s)" % (
+            self.row.index, self.col.index, self.state)
+
+
+_KEY_DIGITS = 31          # base-4 path digits; depth <= 31 levels
+
+
+class FlatBlockTree:
+    """All block-tree nodes as arrays: ``row, col, state (0 adm, 1 inadm,
+    2 subdivided), level, key`` and the leaves in depth-first order
+    (``leaf_ids``, ``leaf_key``).  ``key`` is the base-4 path code aligned
+    to ``_KEY_DIGITS`` digits, so sorting by it is the reference DFS order."""
+
+    def __init__(self, row_tree, col_tree, row, col, state, level, key, parent_of):
+        self.row_tree, self.col_tree = row_tree, col_tree
+        self.row, self.col, self.state, self.level, self.key = row, col, state, level, key
+        self.parent_of = parent_of
+        span = np.power(4, _KEY_DIGITS - level, dtype=np.int64)
+        self.key_lo, self.key_hi = key, key + span
+        leaves = np.flatnonzero(state != 2)
+        order = np.argsort(key[leaves], kind="stable")
+        self.leaf_ids = leaves[order]
+        self.leaf_key = key[self.leaf_ids]
+        self._kid_index = None
+
+    def kids(self, i):
+        if self._kid_index is None:
+            order = np.argsort(self.parent_of, kind="stable")
+            cuts = np.searchsorted(self.parent_of[order], np.arange(len(self.row) + 1))
+            self._kid_index = (order, cuts)
+        order, cuts = self._kid_index
+        kids = order[cuts[i]:cuts[i + 1]]
+        return kids[np.argsort(self.key[kids], kind="stable")]
+
+    def leaves(self, state=None):
+        """Leaf (row, col) node ids in DFS order, optionally one state only."""
+        ids = self.leaf_ids
+        if state is not None:
+            ids = ids[self.state[ids] == state]
+        return self.row[ids], self.col[ids]
+
+
+def _gap_norm_vector(gap):
+    return np.sqrt((gap[:, 0] * gap[:, 0] + gap[:, 1] * gap[:, 1]) + gap[:, 2] * gap[:, 2])
+
+
+def _admissible_many(rt, ct, r, c, eta):
+    """Vectorised ``admissible`` with an exact recheck of near-ties: the
+    distance is computed elementwise, and whenever the comparison is within
+    1e-12 relative of flipping it is redone with the reference's 1-D BLAS
+    norm, so the decision is bit-for-bit the reference's."""
+    d = np.maximum(rt.diam[r], ct.diam[c])
+    gap = np.maximum(0.0, np.maximum(rt.lower[r] - ct.upper[c], ct.lower[c] - rt.upper[r]))
+    rhs = 2.0 * eta * _gap_norm_vector(gap)
+    adm = d <= rhs
+    close = np.flatnonzero(np.abs(d - rhs) <= 1e-12 * np.maximum(d, rhs))
+    for i in close:
+        adm[i] = d[i] <= 2.0 * eta * _blas_norm(gap[i])
+    return adm
+
+
+def build_block_tree(row_root, col_root=None, eta=1.0):
+    """Recursive block partition (``clustering.py:215-237``), grown level by
+    level.  Returns the root :class:`BlockTree` view."""
+    if col_root is None:
+        col_root = row_root
+    if eta <= 0:
+        raise ConfigError("eta must be positive, got %r" % (eta,))
+    rt, ct = row_root.flat, col_root.flat
+    rows, cols, states, levels, keys, parents = [], [], [], [], [], []
+    fr = np.array([row_root.index], dtype=np.int64)
+    fc = np.array([col_root.index], dtype=np.int64)
+    fkey = np.zeros(1, dtype=np.int64)
+    fpar = np.full(1, -1, dtype=np.int64)
+    base = 0
+    lev = 0
+    while fr.size:
+        if lev >= _KEY_DIGITS:
+            raise ConfigError("block tree deeper than %d levels" % _KEY_DIGITS)
+        adm = _admissible_many(rt, ct, fr, fc, eta)
+        rleaf, cleaf = rt.is_leaf[fr], ct.is_leaf[fc]
+        state = np.where(adm, 0, np.where(rleaf & cleaf, 1, 2)).astype(np.int8)
+        ids = base + np.arange(fr.size)
+        rows.append(fr); cols.append(fc); states.append(state)
+        levels.append(np.full(fr.size, lev, dtype=np.int64))
+        keys.append(fkey); parents.append(fpar)
+        base += fr.size
+        sub = np.flatnonzero(state == 2)
+        if not sub.size:
+            break
+        r, c = fr[sub], fc[sub]
+        r_split, c_split = ~rt.is_leaf[r], ~ct.is_leaf[c]
+        # children of a pair: (rc, cc) for rc in rs for cc in cs
+        rk = [np.where(r_split, rt.left[r], r), np.where(r_split, rt.right[r], -1)]
+        ck = [np.where(c_split, ct.left[c], c), np.where(c_split, ct.right[c], -1)]
+        digit_scale = np.int64(4) ** (_KEY_DIGITS - 1 - lev)
+        nr, nc, nk, npar = [], [], [], []
+        for a in range(2):
+            for b in range(2):
+                ok = (rk[a] >= 0) & (ck[b] >= 0)
+                # sequential digit among the existing children of each parent
+                dig = (a * np.where(c_split, 2, 1) + b)
+                sel = np.flatnonzero(ok)
+                nr.append(rk[a][sel]); nc.append(ck[b][sel])
+                nk.append(keys[-1][sub[sel]] + dig[sel] * digit_scale)
+                npar.append(ids[sub[sel]])
+        fr, fc = np.concatenate(nr), np.concatenate(nc)
+        fkey, fpar = np.concatenate(nk), np.concatenate(npar)
+        lev += 1
+    flat = FlatBlockTree(rt, ct, np.concatenate(rows), np.concatenate(cols),
+                         np.concatenate(states), np.concatenate(levels),
+                         np.concatenate(keys), np.concatenate(parents))
+    return BlockTree(flat, 0)

@@ -1,0 +1,184 @@
+/*
+ * gcb200.h - C-ABI of the B200-native GCA-H2 hot path (libgcb200.so).
+ *
+ * Plain C: pointers, sizes and an opaque cudaStream_t passed as void*.
+ * Every pointer marked [dev] is caller-owned device memory (the Python host
+ * layer allocates it with torch); [host] pointers are host memory.  All
+ * functions are thread-safe (no global mutable state besides the error
+ * string, which is thread-local, and an atomic launch counter) and never
+ * synchronise the device unless stated.  Return value: GC_OK or one of the
+ * GC_ERR_* codes; gc_last_error() returns the message.  The host layer maps
+ * GC_ERR_CONFIG -> ConfigError, GC_ERR_GEOMETRY -> GeometryError,
+ * GC_ERR_STATE -> StateError and everything else -> GreencrossError
+ * (greencross/errors.py:4-35).
+ *
+ * Each entry point names the reference interface whose results it
+ * reproduces (paths relative to /root/reference/pkg/src/greencross).
+ */
+#ifndef GCB200_H
+#define GCB200_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define GC_ABI_VERSION 1
+
+#define GC_OK 0
+#define GC_ERR_CONFIG 1
+#define GC_ERR_GEOMETRY 2
+#define GC_ERR_CUDA 3
+#define GC_ERR_STATE 4
+
+int gc_abi_version(void);
+const char* gc_last_error(void);
+/* kernels launched by this library since load / last reset (bench evidence) */
+uint64_t gc_launch_count(void);
+void gc_reset_launch_count(void);
+
+/* ---------------------------------------------------------------------
+ * Device-resident geometry (replaces geometry.chart_pack, geometry.py:266-293,
+ * and assembly._surface_quadrature, assembly.py:371-381).
+ *   corners [dev] (nt,3,3)  triangle vertices
+ *   gram    [dev] (nt,)     plane Gramian |(v1-v0)x(v2-v0)| from the host
+ *   tri_vid [dev] (nt,3)    global vertex ids (pair classification)
+ *   xq      [dev] (nt,mq,3) regular-rule surface points (gc_surface_points)
+ *   wq      [dev] (mq,)     triangle_gauss(q_reg) weights
+ * ------------------------------------------------------------------- */
+typedef struct gc_geom {
+    const double* corners;
+    const double* gram;
+    const int64_t* tri_vid;
+    const double* xq;
+    const double* wq;
+    int64_t nt;
+    int64_t mq;
+} gc_geom;
+
+/* Singular pair rules (quadrature.sauter_rule, quadrature.py:211-284) as
+ * SoA tables [dev] of 5*P doubles: x1[P] x2[P] y1[P] y2[P] w[P].  For the
+ * identical case x1, x2 hold x1-y1, x2-y2 (the two charts coincide). */
+typedef struct gc_rules {
+    const double* table[4]; /* index by case code; [0] unused */
+    int64_t npts[4];
+} gc_rules;
+
+/* Quadrature points of the regular rule on every chart, in the reference's
+ * exact operation order: xq[t,m,c] = sum_a n6[m,a] node[t,a,c] summed
+ * sequentially without FMA, nodes = corners + straight midpoints
+ * (assembly._interp6 / _surface_quadrature, assembly.py:138-143, 371-381).
+ *   n6 [dev] (mq,6) shape functions at the triangle_gauss(q_reg) points. */
+int gc_surface_points(const double* corners, int64_t nt, const double* n6,
+                      int64_t mq, double* xq, void* stream);
+
+/* Batched pair quadrature for the evaluator seam: replaces the evaluator
+ * galerkin_pair_evaluator(...).evaluate(case, rows, cols, px, py)
+ * (assembly.py:159-216; contract batchexec.py:70-76, 161-163).
+ *   rows, cols, px, py [dev] (B,) int64; out [dev] (B,) double.
+ * Constant basis, plane charts, single layer. */
+int gc_pair_eval(const gc_geom* g, const gc_rules* r, int kase, int64_t B,
+                 const int64_t* rows, const int64_t* cols, const int64_t* px,
+                 const int64_t* py, double* out, void* stream);
+
+/* Singular-task queues filled by gc_assemble_blocks: per case c in 1..3 a
+ * [dev] array of cap[c] packed tasks (t, s, px | py << 8, out_index). */
+typedef struct gc_queue {
+    int64_t* tasks[4];
+    int64_t cap[4];
+    int32_t* count; /* [dev] 4 counters */
+} gc_queue;
+
+/* Whole-block Galerkin assembly (replaces the executor path of
+ * gca.build_h2, gca.py:282-312, for near-field and coupling blocks and
+ * assembly.assemble_galerkin_block, assembly.py:330-337).
+ * desc [dev] (nb,5) int64: row_off, nr, col_off, nc, out_off.  Entry (a,b)
+ * pairs triangle row_idx[row_off+a] with col_idx[col_off+b] and is stored
+ * column-major at out[out_off + b*nr + a].  Disjoint pairs are integrated
+ * here; singular pairs are appended to the queue and integrated by
+ * gc_singular_flush.  flags [dev] int: bit 1 set on queue overflow. */
+int gc_assemble_blocks(const gc_geom* g, int64_t nb, const int64_t* desc,
+                       int64_t max_block_entries, const int64_t* row_idx,
+                       const int64_t* col_idx, double* out, gc_queue* q,
+                       int32_t* flags, void* stream);
+
+/* Integrate all queued singular tasks into out and reset the counters.
+ * Synchronises `stream` once to read the counters; counts [host] (4,)
+ * receives the number of tasks per case (index 1..3; may be NULL). */
+int gc_singular_flush(const gc_geom* g, const gc_rules* r, gc_queue* q,
+                      double* out, int64_t* counts, void* stream);
+
+/* Batched transpose: for node i with desc (off, rows, cols) [dev] (nn,3):
+ * out[off + c*rows + r] = in[off + r*cols + c]. */
+int gc_batched_transpose(int64_t nn, const int64_t* desc, const double* in,
+                         double* out, void* stream);
+
+/* Box-boundary Green rules of a batch of cluster boxes: replaces
+ * quadrature.green_box_rule (quadrature.py:95-126) evaluated per node.
+ *   g01, w01 [dev] (m,) Gauss-Legendre on [0,1];
+ *   box [dev] (nn,8) double: lower[3], upper[3], delta, d_tau (host values);
+ *   outputs [dev]: z (nn,K,3) points, sq (nn,K) sqrt(weights), nz (nn,K,3)
+ *   outward normals; K = 6 m^2. */
+int gc_green_box_rules(int m, const double* g01, const double* w01, int64_t nn,
+                       const double* box, double* z, double* sq, double* nz,
+                       void* stream);
+
+/* Green quadrature factors for a batch of cluster-basis nodes: replaces
+ * assembly.green_row_factor / green_col_factor (assembly.py:420-455).
+ *   side 0: A = [sqrt(w) g, -d sqrt(w) h];  side 1: B = [sqrt(w) h, sqrt(w)/d g]
+ *   desc [dev] (nn,4) int64: rows_off, R, out_off, rule index;
+ *   dtau [dev] (nn,) box diameters (host values); z/sq/nz: rules as above;
+ *   rows [dev] dof (triangle) ids; out [dev] row-major (R, 2K) per node.
+ * flags bit 0 is set when an expansion point touches the surface
+ * (r <= 1e-12, assembly._touch_guard, assembly.py:365-368). */
+int gc_green_factor(const gc_geom* g, int side, int64_t K, int64_t nn,
+                    const int64_t* desc, const double* dtau, const double* z,
+                    const double* sq, const double* nz, const int64_t* rows,
+                    double* out, int32_t* flags, void* stream);
+
+/* Batched full-pivot cross approximation (gca.aca_interpolation,
+ * gca.py:41-79) of nn thin matrices of width W.
+ *   desc [dev] (nn,4) int64: fac_off, R, piv_off, v_off.  The factor at
+ *   fac[fac_off] (R x W row-major) is overwritten.  Outputs: rank[n],
+ *   piv[piv_off + k] local pivot rows (k < rank), V at v[v_off] (R x rank
+ *   row-major, V[piv] = I exactly); u is scratch of the same layout as v.
+ *   max_rank <= 0 means W.  max_rows bounds R over the batch. */
+int gc_aca(int64_t nn, const int64_t* desc, int64_t W, double eps,
+           int64_t max_rank, double* fac, int64_t* piv, int64_t* rank,
+           double* v, double* u, int64_t max_rows, void* stream);
+
+/* ---------------------------------------------------------------------
+ * H2 matvec building blocks (h2.mvm, h2.py:19-80)
+ * ------------------------------------------------------------------- */
+/* xt[i] = x[perm[i]] (h2.py:68) */
+int gc_gather(const double* x, const int64_t* perm, int64_t n, double* xt,
+              void* stream);
+/* y[perm[i]] = yt[i] (h2.py:78-79) */
+int gc_scatter(const double* yt, const int64_t* perm, int64_t n, double* y,
+               void* stream);
+
+/* Segmented block-row product, the single kernel form behind every matvec
+ * phase.  For segment s = (out_off, T, blk_begin, blk_end):
+ *     out[out_off + t] (+)= sum_{b in [blk_begin, blk_end)} sum_{k<K_b}
+ *                           A_b[k*lda_b + t*ts_b] * in_b[in_off_b + k]
+ * blk (nblk,6) int64: a_off, K, lda, in_off, sel (bit0: A1 instead of A0,
+ * bit1: in1 instead of in0), ts (1 for the coalesced layouts of mvm; the
+ * transposed product mvm_t reuses the same storage with ts = row length).  Forward transform: A = V or V-hat (row-major),
+ * coupling: A = S^T, backward: A = V-hat^T, near-field: A = N^T.  Each
+ * output element has one writer and a fixed summation order: the result is
+ * bitwise deterministic.  accumulate != 0 adds into out. */
+int gc_segmv(int64_t nseg, const int64_t* seg, const int64_t* blk,
+             const double* A0, const double* A1, const double* in0,
+             const double* in1, double* out, int accumulate, int64_t max_T,
+             void* stream);
+
+/* FP64 DFMA throughput probe used as the roofline denominator (no FP64
+ * figure exists in MEASURED_PEAKS.json): blocks x threads x iters x 8 DFMA. */
+int gc_dfma_probe(int64_t blocks, int64_t threads, int64_t iters, double* out,
+                  void* stream);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* GCB200_H */

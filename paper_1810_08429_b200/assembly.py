@@ -1,0 +1,164 @@
+"""Device-backed Galerkin assembly and Green factors behind the reference's seams.
+
+Mirrors the hot-path entry points of ``greencross/assembly.py``:
+
+* ``galerkin_pair_evaluator(kind, mesh, basis, q_reg, q_sing)`` returns an
+  ``evaluate(case, rows, cols, px, py)`` with the executor contract of
+  ``batchexec.py:70-76`` (values in canonical permuted order, shape (B,1,1),
+  independent of batch composition), computed by ``gc_pair_eval``
+  (``assembly.py:159-216``);
+* ``assemble_galerkin_block`` - dense block on any index lists
+  (``assembly.py:330-337``) through ``gc_assemble_blocks`` +
+  ``gc_singular_flush``;
+* ``green_row_factor`` / ``green_col_factor`` - the Green quadrature factor
+  seam resolved by ``gca.build_cluster_basis`` (``assembly.py:420-455``)
+  through ``gc_green_factor``.
+
+Only the single-layer kernel with the piecewise-constant basis on plane
+charts runs on the device (the configurations of BASELINE.json); other
+kinds raise :class:`ConfigError`.  There is no host fallback.
+"""
+
+from collections import namedtuple
+
+import numpy as np
+
+from . import _native
+from . import quadrature as quad
+from .device import (DeviceMesh, DeviceRules, SingularQueue, check_mesh, empty, ptr,
+                     require_device, stream_handle, to_dev, torch)
+from .errors import ConfigError, GeometryError
+
+FOUR_PI = 4.0 * np.pi
+DenseBlock = namedtuple("DenseBlock", "rows cols values")
+
+
+def galerkin_classify(mesh):
+    """Host twin of the device classifier (``assembly.py:150-156``)."""
+    tris = mesh.triangles
+
+    def classify(rows, cols):
+        return quad.classify_pairs(tris[rows], tris[cols])
+
+    return classify
+
+
+def galerkin_pair_evaluator(kind, mesh, basis, q_reg, q_sing, device=None):
+    """Batched device pair evaluator for the executor seam."""
+    if kind not in ("slp", "dlp"):
+        raise ConfigError("unknown kernel kind %r" % (kind,))
+    if basis not in ("constant", "linear"):
+        raise ConfigError("unknown basis %r" % (basis,))
+    check_mesh(mesh, kind, basis)
+    dev = require_device(device)
+    dmesh = DeviceMesh.get(mesh, q_reg, dev)
+    rules = DeviceRules.get(q_sing, dev)
+
+    def evaluate(case, rows, cols, px, py):
+        case = int(case)
+        if case not in (0, 1, 2, 3):
+            raise ConfigError("unknown pair case %r" % (case,))
+        b = len(rows)
+        out = empty(b, dev)
+        args = [to_dev(np.asarray(a, dtype=np.int64), dev) for a in (rows, cols, px, py)]
+        with torch.cuda.device(dev):
+            _native.call("gc_pair_eval", dmesh.geom, rules.struct, case, b,
+                         *[ptr(a) for a in args], ptr(out), stream_handle())
+        return out.cpu().numpy().reshape(b, 1, 1)
+
+    return evaluate
+
+
+def device_block_assembly(dmesh, rules, queue, row_idx, col_idx, desc, out, stats=None):
+    """Assemble blocks described by ``desc (nb,5)`` into the device buffer
+    ``out`` (column-major per block); singular pairs are flushed at the end.
+    Returns the per-case task counts."""
+    nb = len(desc)
+    if nb == 0:
+        return [0, 0, 0, 0]
+    entries = desc[:, 1] * desc[:, 3]
+    d_desc = to_dev(desc.astype(np.int64), out.device)
+    stream = stream_handle()
+    with torch.cuda.device(out.device):
+        _native.call("gc_assemble_blocks", dmesh.geom, nb, ptr(d_desc), int(entries.max()),
+                     ptr(row_idx), ptr(col_idx), ptr(out), queue.struct, ptr(queue.flags),
+                     stream)
+        counts = (_native.c_i64 * 4)()
+        _native.call("gc_singular_flush", dmesh.geom, rules.struct, queue.struct, ptr(out),
+                     counts, stream)
+    queue.check_flags()
+    n_sing = [int(counts[k]) for k in range(4)]
+    n_sing[0] = int(entries.sum()) - sum(n_sing[1:])
+    return n_sing
+
+
+def assemble_galerkin_block(kind, mesh, basis, rows, cols, orders=(3, 5), capacity=None,
+                            threads=None, device=None):
+    """Dense Galerkin block G[rows, cols] (``assembly.py:330-337``)."""
+    check_mesh(mesh, kind, basis)
+    rows = np.asarray(rows, dtype=np.int64)
+    cols = np.asarray(cols, dtype=np.int64)
+    if len(np.unique(rows)) != len(rows) or len(np.unique(cols)) != len(cols):
+        raise ConfigError("duplicate indices")
+    nr, nc = len(rows), len(cols)
+    if nr == 0 or nc == 0:
+        return DenseBlock(rows, cols, np.zeros((nr, nc)))
+    dev = require_device(device)
+    dmesh = DeviceMesh.get(mesh, orders[0], dev)
+    rules = DeviceRules.get(orders[1], dev)
+    queue = SingularQueue.get(mesh, dev)
+    out = empty(nr * nc, dev)
+    desc = np.array([[0, nr, 0, nc, 0]], dtype=np.int64)
+    device_block_assembly(dmesh, rules, queue, to_dev(rows, dev), to_dev(cols, dev), desc, out)
+    return DenseBlock(rows, cols, out.cpu().numpy().reshape(nc, nr).T.copy())
+
+
+# --------------------------------------------------------------------------
+# Green factors
+
+def green_factors_device(dmesh, side, K, rows, desc, dtau, z, sq, nz, total_rows, device):
+    """Factor matrices of a batch of nodes (device buffer, row-major per
+    node).  Raises GeometryError if an expansion point touches the surface."""
+    out = empty(total_rows * 2 * K, device)
+    flags = torch.zeros(1, dtype=torch.int32, device=device)
+    with torch.cuda.device(device):
+        _native.call("gc_green_factor", dmesh.geom, 0 if side == "row" else 1, K, len(desc),
+                     ptr(desc), ptr(dtau), ptr(z), ptr(sq), ptr(nz), ptr(rows), ptr(out),
+                     ptr(flags), stream_handle())
+    if int(flags.item()) & 1:
+        raise GeometryError("expansion point touches the surface; "
+                            "enlarge delta or the cluster box")
+    return out
+
+
+def _single_factor(side, cluster, rule, mesh, basis, orders, d_tau, device=None):
+    check_mesh(mesh, "slp", basis)
+    dev = require_device(device)
+    dmesh = DeviceMesh.get(mesh, orders[0], dev)
+    rows = np.asarray(cluster.indices, dtype=np.int64)
+    K = int(rule.k)
+    z = to_dev(np.asarray(rule.points, dtype=np.float64), dev)
+    sq = to_dev(np.sqrt(np.asarray(rule.weights, dtype=np.float64)), dev)
+    nz = to_dev(np.asarray(rule.normals, dtype=np.float64), dev)
+    desc = to_dev(np.array([[0, len(rows), 0, 0]], dtype=np.int64), dev)
+    dtau = to_dev(np.array([d_tau]), dev)
+    out = green_factors_device(dmesh, side, K, to_dev(rows, dev), desc, dtau, z, sq, nz,
+                               len(rows), dev)
+    return out.cpu().numpy().reshape(len(rows), 2 * K)
+
+
+def green_row_factor(cluster, rule, mesh, basis, orders=(3, 5)):
+    """Row factor A = [sqrt(w) g-moments, -d_tau sqrt(w) dg/dn-moments]
+    (``assembly.py:420-439``); ``cluster`` needs ``.indices`` and ``.box``."""
+    if basis == "collocation":
+        raise ConfigError("collocation rows are out of scope on the device")
+    return _single_factor("row", cluster, rule, mesh, basis, orders, cluster.box.diameter())
+
+
+def green_col_factor(pair, rule, mesh, basis, orders=(3, 5)):
+    """Column factor B = [sqrt(w) dg/dn-moments, sqrt(w)/d_tau g-moments] of
+    sigma under tau's rule (``assembly.py:442-455``)."""
+    tau, sigma = pair
+    if basis == "collocation":
+        raise ConfigError("column factors integrate a Galerkin basis")
+    return _single_factor("col", sigma, rule, mesh, basis, orders, tau.box.diameter())

@@ -1,0 +1,147 @@
+// Green quadrature factors of cluster-basis nodes (assembly.py:371-455,
+// quadrature.py:95-126), one CTA per node, one thread per (row, box point).
+//
+// Pivot sets are chosen by argmax over these entries, so every operation
+// follows the reference's rounding: no FMA contraction (__d*_rn
+// intrinsics), sequential point sums starting from 0, 1/(4 pi r) formed as
+// 1/(FOUR_PI*r), and r^3 rounded once (cube_rn).  The only known difference
+// is numpy's SIMD r**3, which is within 1 ulp of cube_rn.
+#include "common.cuh"
+
+namespace gcb {
+
+constexpr int GREEN_THREADS = 256;
+constexpr int GREEN_MAX_K = 6 * 8 * 8;  // m <= 8
+
+// Box-boundary rules of a batch of nodes (quadrature.green_box_rule):
+// face (axis, low/high side) -> m x m tensor Gauss points, with the
+// reference's operation order for points and weights.
+__global__ void k_green_box_rules(int m, const double* __restrict__ g01,
+                                  const double* __restrict__ w01, int64_t nn,
+                                  const double* __restrict__ boxes, double* __restrict__ z,
+                                  double* __restrict__ sq, double* __restrict__ nz) {
+    const int K = 6 * m * m;
+    for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < nn * K;
+         e += (int64_t)gridDim.x * blockDim.x) {
+        const int64_t node = e / K;
+        const int k = (int)(e % K);
+        const double* bx = boxes + 8 * node;
+        const int face = k / (m * m), ij = k % (m * m), i = ij / m, j = ij % m;
+        const int axis = face >> 1, hi_side = face & 1;
+        const int b = axis == 0 ? 1 : 0, c = axis == 2 ? 1 : 2;
+        double lo[3], hi[3];
+#pragma unroll
+        for (int a = 0; a < 3; ++a) {
+            lo[a] = __dsub_rn(bx[a], bx[6]);
+            hi[a] = __dadd_rn(bx[3 + a], bx[6]);
+        }
+        const double span_b = __dsub_rn(hi[b], lo[b]), span_c = __dsub_rn(hi[c], lo[c]);
+        double p[3], n[3] = {0.0, 0.0, 0.0};
+        p[axis] = hi_side ? hi[axis] : lo[axis];
+        p[b] = __dadd_rn(lo[b], __dmul_rn(span_b, g01[i]));
+        p[c] = __dadd_rn(lo[c], __dmul_rn(span_c, g01[j]));
+        n[axis] = hi_side ? 1.0 : -1.0;
+        const double wz = __dmul_rn(__dmul_rn(__dmul_rn(w01[i], w01[j]), span_b), span_c);
+#pragma unroll
+        for (int a = 0; a < 3; ++a) {
+            z[3 * e + a] = p[a];
+            nz[3 * e + a] = n[a];
+        }
+        sq[e] = __dsqrt_rn(wz);
+    }
+}
+
+// One CTA per node; rule (K points) staged in shared memory; one thread per
+// (row, box point) entry of the R x 2K factor.
+__global__ void __launch_bounds__(GREEN_THREADS) k_green_factor(
+    gc_geom g, int side, int K, const int64_t* __restrict__ desc,
+    const double* __restrict__ dtau, const double* __restrict__ zr, const double* __restrict__ sqr,
+    const double* __restrict__ nzr, const int64_t* __restrict__ rows, double* __restrict__ out,
+    int32_t* flags) {
+    __shared__ double z[GREEN_MAX_K][3];
+    __shared__ double nn3[GREEN_MAX_K][3];
+    __shared__ double sq[GREEN_MAX_K];
+    const int node = blockIdx.x;
+    const int64_t rows_off = desc[4 * node], R = desc[4 * node + 1];
+    const int64_t out_off = desc[4 * node + 2], rule = desc[4 * node + 3];
+    const double d_tau = dtau[node];
+    for (int k = threadIdx.x; k < K; k += blockDim.x) {
+#pragma unroll
+        for (int a = 0; a < 3; ++a) {
+            z[k][a] = zr[(rule * K + k) * 3 + a];
+            nn3[k][a] = nzr[(rule * K + k) * 3 + a];
+        }
+        sq[k] = sqr[rule * K + k];
+    }
+    __syncthreads();
+
+    const int mq = (int)g.mq;
+    const int64_t W = 2 * (int64_t)K;
+    bool touch = false;
+    for (int64_t e = threadIdx.x; e < R * K; e += blockDim.x) {
+        const int64_t r = e / K;
+        const int k = (int)(e % K);
+        const int64_t t = rows[rows_off + r];
+        const double gram = g.gram[t];
+        const double z0 = z[k][0], z1 = z[k][1], z2 = z[k][2];
+        const double n0 = nn3[k][0], n1 = nn3[k][1], n2 = nn3[k][2];
+        double ig = 0.0, ih = 0.0;
+        const double* xq = g.xq + t * 3 * mq;
+        for (int p = 0; p < mq; ++p) {
+            const double d0 = __dsub_rn(xq[3 * p], z0);
+            const double d1 = __dsub_rn(xq[3 * p + 1], z1);
+            const double d2 = __dsub_rn(xq[3 * p + 2], z2);
+            const double r2 = __dadd_rn(__dadd_rn(__dmul_rn(d0, d0), __dmul_rn(d1, d1)),
+                                        __dmul_rn(d2, d2));
+            const double rr = __dsqrt_rn(r2);
+            touch |= (rr <= 1e-12);
+            const double gk = __ddiv_rn(1.0, __dmul_rn(FOUR_PI, rr));
+            const double dot = __dadd_rn(__dadd_rn(__dmul_rn(d0, n0), __dmul_rn(d1, n1)),
+                                         __dmul_rn(d2, n2));
+            const double hk = __ddiv_rn(dot, __dmul_rn(FOUR_PI, cube_rn(rr)));
+            const double gw = __dmul_rn(gram, g.wq[p]);
+            ig = __dadd_rn(ig, __dmul_rn(gw, gk));
+            ih = __dadd_rn(ih, __dmul_rn(gw, hk));
+        }
+        double* row = out + out_off + r * W;
+        if (side == 0) {
+            row[k] = __dmul_rn(sq[k], ig);
+            row[K + k] = __dmul_rn(__dmul_rn(-d_tau, sq[k]), ih);
+        } else {
+            row[k] = __dmul_rn(sq[k], ih);
+            row[K + k] = __dmul_rn(__ddiv_rn(sq[k], d_tau), ig);
+        }
+    }
+    if (touch) atomicOr(flags, FLAG_TOUCH);
+}
+
+}  // namespace gcb
+
+using namespace gcb;
+
+extern "C" int gc_green_box_rules(int m, const double* g01, const double* w01, int64_t nn,
+                                  const double* box, double* z, double* sq, double* nz,
+                                  void* stream) {
+    if (m < 1 || m > 8) { set_error(GC_ERR_CONFIG, "green order m=%d outside [1, 8]", m); return GC_ERR_CONFIG; }
+    if (nn <= 0) return GC_OK;
+    int64_t total = nn * 6 * m * m;
+    int64_t grid = (total + 255) / 256;
+    if (grid > 148 * 32) grid = 148 * 32;
+    k_green_box_rules<<<(unsigned)grid, 256, 0, (cudaStream_t)stream>>>(m, g01, w01, nn, box, z, sq, nz);
+    GC_CHECK_LAUNCH("k_green_box_rules");
+    return GC_OK;
+}
+
+extern "C" int gc_green_factor(const gc_geom* gp, int side, int64_t K, int64_t nn,
+                               const int64_t* desc, const double* dtau, const double* z,
+                               const double* sq, const double* nz, const int64_t* rows,
+                               double* out, int32_t* flags, void* stream) {
+    if (!gp) { set_error(GC_ERR_CONFIG, "null geometry"); return GC_ERR_CONFIG; }
+    if (side != 0 && side != 1) { set_error(GC_ERR_CONFIG, "side must be 0 (row) or 1 (col)"); return GC_ERR_CONFIG; }
+    if (K < 1 || K > GREEN_MAX_K) { set_error(GC_ERR_CONFIG, "rule size K=%lld outside [1, %d]", (long long)K, GREEN_MAX_K); return GC_ERR_CONFIG; }
+    if (nn <= 0) return GC_OK;
+    k_green_factor<<<(unsigned)nn, GREEN_THREADS, 0, (cudaStream_t)stream>>>(
+        *gp, side, (int)K, desc, dtau, z, sq, nz, rows, out, flags);
+    GC_CHECK_LAUNCH("k_green_factor");
+    return GC_OK;
+}

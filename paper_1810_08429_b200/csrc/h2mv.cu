@@ -1,0 +1,90 @@
+// Segmented block-row products: the one kernel form behind every H2 matvec
+// phase (h2.py:19-80) - forward transform (V^T x, V-hat^T x-hat), coupling
+// (S x-hat), backward transform (E y-hat) and the near-field SpMV (N x).
+//
+// Matrices are stored so that the product reads contiguous rows of A
+// (out[t] += sum_k A[k*lda + t] in[k]): a group of T threads covers the T
+// outputs of a segment and streams one row of A per step with coalesced
+// loads; ng = 256/T groups split the k range round-robin and are summed in
+// group order at the end, so every output has exactly one writer and a
+// fixed summation order (bitwise deterministic, no atomics).
+#include "common.cuh"
+
+namespace gcb {
+
+constexpr int SEG_THREADS = 256;
+
+__global__ void __launch_bounds__(SEG_THREADS) k_segmv(const int64_t* __restrict__ seg,
+                                                       const int64_t* __restrict__ blk,
+                                                       const double* __restrict__ A0,
+                                                       const double* __restrict__ A1,
+                                                       const double* __restrict__ in0,
+                                                       const double* __restrict__ in1,
+                                                       double* __restrict__ out, int accumulate) {
+    __shared__ double red[SEG_THREADS];
+    const int64_t* sd = seg + 4 * (int64_t)blockIdx.x;
+    const int64_t out_off = sd[0];
+    const int T = (int)sd[1];
+    const int64_t b0 = sd[2], b1 = sd[3];
+    const int tt = T < SEG_THREADS ? T : SEG_THREADS;   // threads per group
+    const int ng = SEG_THREADS / tt;                     // groups
+    const int g = threadIdx.x / tt;
+    for (int t0 = 0; t0 < T; t0 += tt) {
+        const int t = t0 + (int)(threadIdx.x % tt);
+        const bool live = g < ng && t < T;
+        double acc = 0.0;
+        if (live) {
+            for (int64_t b = b0; b < b1; ++b) {
+                const int64_t* bd = blk + 6 * b;
+                const int64_t a_off = bd[0], K = bd[1], lda = bd[2], in_off = bd[3];
+                const int sel = (int)bd[4];
+                const double* A = ((sel & 1) ? A1 : A0) + a_off + t * bd[5];
+                const double* x = ((sel & 2) ? in1 : in0) + in_off;
+                int64_t k = g;
+                for (; k + 3 * ng < K; k += 4 * ng) {
+                    const double a0 = __ldg(A + k * lda), a1 = __ldg(A + (k + ng) * lda);
+                    const double a2 = __ldg(A + (k + 2 * ng) * lda), a3 = __ldg(A + (k + 3 * ng) * lda);
+                    const double x0 = __ldg(x + k), x1 = __ldg(x + k + ng);
+                    const double x2 = __ldg(x + k + 2 * ng), x3 = __ldg(x + k + 3 * ng);
+                    acc = fma(a0, x0, acc);
+                    acc = fma(a1, x1, acc);
+                    acc = fma(a2, x2, acc);
+                    acc = fma(a3, x3, acc);
+                }
+                for (; k < K; k += ng) acc = fma(__ldg(A + k * lda), __ldg(x + k), acc);
+            }
+        }
+        if (ng == 1) {
+            if (live) {
+                double* o = out + out_off + t;
+                *o = accumulate ? *o + acc : acc;
+            }
+            continue;
+        }
+        red[threadIdx.x] = acc;
+        __syncthreads();
+        if (threadIdx.x < tt && t < T) {
+            double s = red[threadIdx.x];
+            for (int q = 1; q < ng; ++q) s += red[q * tt + threadIdx.x];
+            double* o = out + out_off + t;
+            *o = accumulate ? *o + s : s;
+        }
+        __syncthreads();
+    }
+}
+
+}  // namespace gcb
+
+using namespace gcb;
+
+extern "C" int gc_segmv(int64_t nseg, const int64_t* seg, const int64_t* blk, const double* A0,
+                        const double* A1, const double* in0, const double* in1, double* out,
+                        int accumulate, int64_t max_T, void* stream) {
+    (void)max_T;
+    if (nseg <= 0) return GC_OK;
+    if (nseg > 0x7fffffffLL) { set_error(GC_ERR_CONFIG, "too many segments"); return GC_ERR_CONFIG; }
+    k_segmv<<<(unsigned)nseg, SEG_THREADS, 0, (cudaStream_t)stream>>>(seg, blk, A0, A1, in0, in1,
+                                                                      out, accumulate);
+    GC_CHECK_LAUNCH("k_segmv");
+    return GC_OK;
+}

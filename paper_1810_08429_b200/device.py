@@ -1,0 +1,176 @@
+"""Device-resident geometry, rule tables and singular-task queues.
+
+PyTorch is used only for allocation, streams and host<->device copies; all
+arithmetic happens in ``libgcb200.so``.  Uploads are cached on the mesh
+object (meshes are immutable), so one mesh is uploaded once
+per device and quadrature order.
+"""
+
+import ctypes
+
+import numpy as np
+
+from . import _native
+from .errors import ConfigError, DeviceError
+from .geometry import chart_pack, shape_functions
+from .quadrature import sauter_rule, triangle_gauss
+
+try:  # torch is plumbing only; importing the package must not need a GPU
+    import torch
+except ImportError:  # pragma: no cover
+    torch = None
+
+
+def require_device(device=None):
+    """torch.device for the hot path; raises DeviceError without CUDA."""
+    if torch is None or not torch.cuda.is_available():
+        raise DeviceError("the GCA-H2 hot path needs a CUDA device (B200); "
+                          "there is no CPU fallback")
+    _native.load()
+    if device is None:
+        device = torch.device("cuda", torch.cuda.current_device())
+    return torch.device(device)
+
+
+def stream_handle():
+    return ctypes.c_void_p(torch.cuda.current_stream().cuda_stream)
+
+
+def ptr(t):
+    return ctypes.c_void_p(t.data_ptr()) if t is not None and t.numel() else ctypes.c_void_p(0)
+
+
+def to_dev(a, device, dtype=None):
+    a = np.ascontiguousarray(a)
+    t = torch.from_numpy(a)
+    if dtype is not None:
+        t = t.to(dtype)
+    return t.to(device, non_blocking=False)
+
+
+def zeros(shape, device, dtype=None):
+    return torch.zeros(shape, dtype=dtype or torch.float64, device=device)
+
+
+def empty(shape, device, dtype=None):
+    return torch.empty(shape, dtype=dtype or torch.float64, device=device)
+
+
+class DeviceMesh:
+    """Chart data of one plane mesh on one device, for one regular order.
+
+    ``corners (nt,3,3)``, ``gram (nt,)`` (host-computed, never recomputed),
+    ``tri_vid (nt,3)``, and the regular-rule surface points ``xq (nt,q^2,3)``
+    computed on the device in the reference's operation order.
+    """
+
+    def __init__(self, mesh, q_reg, device):
+        pack = chart_pack(mesh)
+        self.mesh = mesh
+        self.device = device
+        self.nt = mesh.nt
+        self.q_reg = q_reg
+        pts, wts = triangle_gauss(q_reg)
+        self.corners = to_dev(pack.nodes[:, :3], device)
+        self.gram = to_dev(pack.gram, device)
+        self.tri_vid = to_dev(mesh.triangles.astype(np.int64), device)
+        self.wq = to_dev(wts, device)
+        n6 = to_dev(shape_functions(pts), device)
+        self.mq = len(wts)
+        self.xq = empty((self.nt, self.mq, 3), device)
+        with torch.cuda.device(device):
+            _native.call("gc_surface_points", ptr(self.corners), self.nt, ptr(n6), self.mq,
+                         ptr(self.xq), stream_handle())
+        self.geom = _native.GcGeom(ptr(self.corners), ptr(self.gram), ptr(self.tri_vid),
+                                   ptr(self.xq), ptr(self.wq), self.nt, self.mq)
+
+    @classmethod
+    def get(cls, mesh, q_reg, device):
+        cache = mesh.__dict__.setdefault("_device_cache", {})
+        key = ("mesh", str(device), int(q_reg))
+        if key not in cache:
+            cache[key] = cls(mesh, int(q_reg), device)
+        return cache[key]
+
+
+class DeviceRules:
+    """Sauter-Schwab vertex / edge / identical tables of order ``q_sing`` as
+    SoA (x1, x2, y1, y2, w); identical stores x-y in the x slots."""
+
+    def __init__(self, q_sing, device):
+        self.q_sing = q_sing
+        self.tables = [None] * 4
+        self.struct = _native.GcRules()
+        for case in (1, 2, 3):
+            rule = sauter_rule(case, q_sing)
+            x, y, w = rule.x, rule.y, rule.w
+            if case == 3:
+                cols = [x[:, 0] - y[:, 0], x[:, 1] - y[:, 1], y[:, 0], y[:, 1], w]
+            else:
+                cols = [x[:, 0], x[:, 1], y[:, 0], y[:, 1], w]
+            t = to_dev(np.concatenate(cols), device)
+            self.tables[case] = t
+            self.struct.table[case] = t.data_ptr()
+            self.struct.npts[case] = len(w)
+
+    @classmethod
+    def get(cls, q_sing, device):
+        key = (str(device), int(q_sing))
+        if key not in _RULE_CACHE:
+            _RULE_CACHE[key] = cls(int(q_sing), device)
+        return _RULE_CACHE[key]
+
+
+_RULE_CACHE = {}
+
+
+def singular_capacity(mesh):
+    """Number of ordered triangle pairs per singular case over the whole
+    mesh: identical nt, edge 2 ne, vertex sum_v deg(v)^2 - 3 nt - 4 ne
+    (pairs sharing v counted once per shared vertex)."""
+    deg = np.bincount(mesh.triangles.ravel(), minlength=mesh.nv).astype(np.int64)
+    ident, edge = mesh.nt, 2 * mesh.ne
+    vert = int((deg * deg).sum()) - 3 * ident - 2 * edge
+    return [0, max(vert, 0), edge, ident]
+
+
+class SingularQueue:
+    """Device task queues for the singular cases of one mesh."""
+
+    def __init__(self, mesh, device):
+        caps = singular_capacity(mesh)
+        self.count = torch.zeros(4, dtype=torch.int32, device=device)
+        self.flags = torch.zeros(1, dtype=torch.int32, device=device)
+        self.tasks = [torch.empty((max(c, 1), 4), dtype=torch.int64, device=device)
+                      for c in caps]
+        self.struct = _native.GcQueue()
+        for k in range(4):
+            self.struct.tasks[k] = self.tasks[k].data_ptr()
+            self.struct.cap[k] = caps[k]
+        self.struct.count = self.count.data_ptr()
+
+    @classmethod
+    def get(cls, mesh, device):
+        cache = mesh.__dict__.setdefault("_device_cache", {})
+        key = ("queue", str(device))
+        if key not in cache:
+            cache[key] = cls(mesh, device)
+        return cache[key]
+
+    def check_flags(self):
+        f = int(self.flags.item())
+        if f & 2:
+            raise DeviceError("singular task queue overflow")
+        if f:
+            self.flags.zero_()
+
+
+def check_mesh(mesh, kind="slp", basis="constant"):
+    if kind != "slp":
+        raise ConfigError("device kernels implement the single-layer kernel only "
+                          "(dlp is out of scope, SURVEY.md §2)")
+    if basis != "constant":
+        raise ConfigError("device kernels implement the piecewise-constant basis only "
+                          "(linear/collocation are out of scope, SURVEY.md §8 f)")
+    if getattr(mesh, "midpoints", None) is not None:
+        raise ConfigError("curved charts are out of scope")

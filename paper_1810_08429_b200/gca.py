@@ -1,0 +1,534 @@
+"""GCA-H2 construction on the device: nested cluster bases and H2 assembly.
+
+Host-side mirror of the hot-path part of ``greencross/gca.py``:
+``aca_interpolation`` (``:41-79``), ``BasisNode`` / ``ClusterBasis``
+(``:92-146``), ``coupling_marks`` (``:149-159``), ``build_cluster_basis``
+(``:162-220``), ``expand_basis`` (``:223-227``), ``H2Matrix`` and
+``build_h2`` (``:230-312``).
+
+The reference builds bases by recursion (one factor + one ACA per node).
+Here the materialised forest is processed level-synchronously by height
+(SPEC.md:500-501): one ``gc_green_box_rules`` + ``gc_green_factor`` +
+``gc_aca`` launch per level over every node of that level, then one small
+device->host read of ranks and pivots, which the host turns into the next
+level's row lists.  ``build_h2`` assembles every coupling and near-field
+block with two ``gc_assemble_blocks`` launches plus the singular flush;
+values stay in HBM in the matvec layout (``h2.py``) and reach the host only
+through the lazy ``.values`` / ``.v`` / ``.transfer`` views.
+"""
+
+import time
+from collections import namedtuple
+from collections.abc import Sequence
+
+import numpy as np
+
+from . import _native
+from .assembly import device_block_assembly, green_factors_device
+from .device import (DeviceMesh, DeviceRules, SingularQueue, check_mesh, empty, ptr,
+                     require_device, stream_handle, to_dev, torch)
+from .errors import ConfigError
+from .quadrature import _gauss01
+
+__all__ = ["Interpolation", "aca_interpolation", "BasisNode", "ClusterBasis",
+           "build_cluster_basis", "expand_basis", "CouplingBlock", "NearfieldBlock",
+           "H2Matrix", "build_h2", "coupling_marks"]
+
+Interpolation = namedtuple("Interpolation", "pivots v")
+CouplingBlock = namedtuple("CouplingBlock", "row col values")
+NearfieldBlock = namedtuple("NearfieldBlock", "row col values")
+
+
+def _ranges(starts, lengths):
+    """Concatenation of arange(s, s+l) over segments (vectorised)."""
+    starts = np.asarray(starts, dtype=np.int64)
+    lengths = np.asarray(lengths, dtype=np.int64)
+    total = int(lengths.sum())
+    if total == 0:
+        return np.zeros(0, dtype=np.int64)
+    heads = np.cumsum(lengths) - lengths
+    return np.arange(total, dtype=np.int64) + np.repeat(starts - heads, lengths)
+
+
+def _offsets(sizes):
+    sizes = np.asarray(sizes, dtype=np.int64)
+    return np.cumsum(sizes) - sizes
+
+
+# --------------------------------------------------------------------------
+# ACA on one matrix (API parity with gca.aca_interpolation)
+
+def aca_interpolation(a, eps, max_rank=None, device=None):
+    """Full-pivot cross approximation of a thin matrix on the device
+    (``gca.py:41-79``).  ``v[pivots] == I`` exactly."""
+    a = np.ascontiguousarray(a, dtype=np.float64)
+    n, w = a.shape
+    dev = require_device(device)
+    limit = min(n, w if max_rank is None else int(max_rank))
+    fac = to_dev(a.ravel(), dev)
+    cap = max(n * max(limit, 0), 1)
+    v = empty(cap, dev)
+    u = empty(cap, dev)
+    piv = torch.zeros(max(limit, 1), dtype=torch.int64, device=dev)
+    rank = torch.zeros(1, dtype=torch.int64, device=dev)
+    desc = to_dev(np.array([[0, n, 0, 0]], dtype=np.int64), dev)
+    mr = limit if max_rank is not None else 0
+    if max_rank is not None and limit <= 0:
+        return Interpolation(np.zeros(0, dtype=np.intp), np.zeros((n, 0)))
+    with torch.cuda.device(dev):
+        _native.call("gc_aca", 1, ptr(desc), w, float(eps), mr, ptr(fac), ptr(piv), ptr(rank),
+                     ptr(v), ptr(u), n, stream_handle())
+    r = int(rank.item())
+    pivots = piv.cpu().numpy()[:r].astype(np.intp)
+    if r == 0:
+        return Interpolation(pivots, np.zeros((n, 0)))
+    return Interpolation(pivots, v[:n * r].cpu().numpy().reshape(n, r))
+
+
+# --------------------------------------------------------------------------
+# nested bases
+
+class BasisNode:
+    """Per-cluster basis content (``gca.py:92-121``): leaves carry ``v``
+    (size x rank), every non-root node its ``transfer`` (rank x parent
+    rank); ``pivots`` are global dof indices.  ``v`` and ``transfer`` are
+    host views of the device store, copied on first access."""
+
+    __slots__ = ("cluster", "pivots", "children", "_store", "_slot", "_v", "_transfer")
+
+    def __init__(self, cluster, pivots, children, store, slot):
+        self.cluster = cluster
+        self.pivots = pivots
+        self.children = children
+        self._store, self._slot = store, slot
+        self._v = None
+        self._transfer = None
+
+    @property
+    def rank(self):
+        return len(self.pivots)
+
+    @property
+    def v(self):
+        if self._v is None and not self.children and self._store is not None:
+            self._v = self._store.host_matrix(self.cluster.index)
+        return self._v
+
+    @v.setter
+    def v(self, value):
+        self._v = value
+
+    @property
+    def transfer(self):
+        if self._transfer is None and self._store is not None:
+            self._transfer = self._store.host_transfer(self.cluster.index)
+        return self._transfer
+
+    @transfer.setter
+    def transfer(self, value):
+        self._transfer = value
+
+    def nodes(self):
+        out = [self]
+        for c in self.children:
+            out.extend(c.nodes())
+        return out
+
+    def __repr__(self):
+        return "BasisNode(#%d, rank %d)" % (self.cluster.index, self.rank)
+
+
+class ClusterBasis:
+    """Nested basis over a (possibly partial) cluster tree (``gca.py:124-146``)."""
+
+    def __init__(self, roots, by_index, store=None):
+        self.roots = roots
+        self._by_index = by_index
+        self.store = store
+
+    @property
+    def root(self):
+        if len(self.roots) != 1:
+            raise ConfigError("basis is a forest, not a single tree")
+        return self.roots[0]
+
+    def node(self, cluster):
+        return self._by_index[cluster.index]
+
+    def nodes(self):
+        return [bn for r in self.roots for bn in r.nodes()]
+
+
+class DeviceBasis:
+    """Device store of one nested basis, indexed by cluster-tree node id.
+
+    Arrays (length = number of tree nodes, -1 / 0 where not materialised):
+    ``rank, rows (R = factor rows), piv_off, v_off, coef_off, height``.
+    Tensors: ``pivots`` (compact global pivot ids), ``V`` (R x rank
+    row-major per node at ``v_off``: leaf V or internal V-hat whose row
+    blocks are the children's transfers), ``VT`` (the transposes, row side
+    only, used by the backward transform).
+    """
+
+    def __init__(self, tree, side, device):
+        self.tree = tree
+        self.flat = tree.flat
+        self.side = side
+        self.device = device
+        n = len(self.flat)
+        self.materialized = np.zeros(n, dtype=bool)
+        self.rank = np.zeros(n, dtype=np.int64)
+        self.rows = np.zeros(n, dtype=np.int64)
+        self.piv_off = np.full(n, -1, dtype=np.int64)
+        self.v_off = np.full(n, -1, dtype=np.int64)
+        self.coef_off = np.full(n, -1, dtype=np.int64)
+        self.child_row = np.zeros(n, dtype=np.int64)   # row offset inside parent's V-hat
+        self.pivots_host = None
+        self.pivots = None
+        self.V = None
+        self.VT = None
+        self.coef_size = 0
+        self._host_V = None
+        self.timing = {}
+
+    def host_V(self):
+        if self._host_V is None:
+            self._host_V = self.V.cpu().numpy()
+        return self._host_V
+
+    def host_matrix(self, i):
+        o, R, r = self.v_off[i], self.rows[i], self.rank[i]
+        return self.host_V()[o:o + R * r].reshape(R, r)
+
+    def host_transfer(self, i):
+        p = self.flat.parent[i]
+        if p < 0 or not self.materialized[p]:
+            return None
+        vhat = self.host_matrix(p)
+        o = self.child_row[i]
+        return vhat[o:o + self.rank[i]]
+
+
+def coupling_marks(btree):
+    """Row and column cluster indices of admissible leaves (``gca.py:149-159``)."""
+    fb = btree.flat
+    ids = btree._leaf_ids(0)
+    return set(fb.row[ids].tolist()), set(fb.col[ids].tolist())
+
+
+def _materialize(flat, marks):
+    n = len(flat)
+    if marks is None:
+        mat = np.zeros(n, dtype=bool)
+        mat[0] = True
+    else:
+        mat = np.zeros(n, dtype=bool)
+        idx = np.fromiter((int(i) for i in marks), dtype=np.int64)
+        if idx.size:
+            mat[idx] = True
+    marked = mat.copy()
+    order = np.argsort(flat.depth, kind="stable")
+    for d in range(1, int(flat.depth.max()) + 1 if n else 0):
+        ids = order[flat.depth[order] == d]
+        mat[ids] |= mat[flat.parent[ids]]
+    roots = np.flatnonzero(marked & ~np.where(flat.parent >= 0, mat[np.maximum(flat.parent, 0)], False))
+    roots = roots[mat[roots]]
+    return mat, roots
+
+
+def build_cluster_basis(tree, mesh, basis, m, delta_factor=0.5, eps=1e-4, side="row",
+                        orders=(3, 5), marks=None, device=None):
+    """Nested interpolation basis built bottom-up, level-synchronously on
+    the device (``gca.py:162-220``)."""
+    if side not in ("row", "col"):
+        raise ConfigError("side must be 'row' or 'col', got %r" % (side,))
+    if basis == "collocation" and side == "col":
+        raise ConfigError("column factors integrate a Galerkin basis")
+    check_mesh(mesh, "slp", basis)
+    if tree.index != 0:
+        raise ConfigError("build_cluster_basis expects the root of a cluster tree")
+    dev = require_device(device)
+    t0 = time.perf_counter()
+    flat = tree.flat
+    store = DeviceBasis(tree, side, dev)
+    mat, roots = _materialize(flat, marks)
+    store.materialized = mat
+    dmesh = DeviceMesh.get(mesh, orders[0], dev)
+    K = 6 * m * m
+    W = 2 * K
+    g01, w01 = _gauss01(m)
+    d_g01, d_w01 = to_dev(g01, dev), to_dev(w01, dev)
+    size = flat.stop - flat.start
+    cap = int(np.minimum(size[mat], W).sum()) if mat.any() else 0
+    gpiv = np.empty(max(cap, 1), dtype=np.int64)
+    cursor = 0
+    v_levels, v_base = [], 0
+    perm = flat.perm
+    heights = np.unique(flat.height[mat])
+    t_factor = t_aca = 0.0
+    stream = stream_handle()
+    for h in heights:
+        ids = np.flatnonzero(mat & (flat.height == h))
+        leaf = flat.is_leaf[ids]
+        lc, rc = flat.left[ids], flat.right[ids]
+        R = np.where(leaf, size[ids], store.rank[np.maximum(lc, 0)] + store.rank[np.maximum(rc, 0)])
+        # row lists: leaf dofs, or the children's pivots (left then right)
+        seg_start = np.where(leaf, flat.start[ids], 0)
+        rows_parts_starts, rows_parts_len, rows_parts_src = [], [], []
+        src = np.zeros(len(ids) * 2, dtype=np.int64)
+        # build gather indices into a combined source [perm | gpiv]
+        n_perm = len(perm)
+        st1 = np.where(leaf, flat.start[ids], n_perm + store.piv_off[np.maximum(lc, 0)])
+        ln1 = np.where(leaf, size[ids], store.rank[np.maximum(lc, 0)])
+        st2 = np.where(leaf, 0, n_perm + store.piv_off[np.maximum(rc, 0)])
+        ln2 = np.where(leaf, 0, store.rank[np.maximum(rc, 0)])
+        starts = np.stack([st1, st2], 1).ravel()
+        lens = np.stack([ln1, ln2], 1).ravel()
+        combined = np.concatenate([perm, gpiv[:cursor]])
+        rows_host = combined[_ranges(starts, lens)]
+        rows_off = _offsets(R)
+        limit = np.minimum(R, W)
+        # child row offsets inside the parent's V-hat
+        store.child_row[np.maximum(lc, 0)[~leaf]] = 0
+        store.child_row[np.maximum(rc, 0)[~leaf]] = store.rank[lc[~leaf]]
+        store.rows[ids] = R
+        # Green factors (rule per node, host-computed delta and d_tau)
+        diam = flat.diam[ids]
+        box = np.concatenate([flat.lower[ids], flat.upper[ids], (delta_factor * diam)[:, None],
+                              diam[:, None]], axis=1)
+        nn = len(ids)
+        tf = time.perf_counter()
+        d_box = to_dev(box, dev)
+        z = empty(nn * K * 3, dev)
+        sq = empty(nn * K, dev)
+        nz = empty(nn * K * 3, dev)
+        with torch.cuda.device(dev):
+            _native.call("gc_green_box_rules", m, ptr(d_g01), ptr(d_w01), nn, ptr(d_box),
+                         ptr(z), ptr(sq), ptr(nz), stream)
+        fdesc = to_dev(np.stack([rows_off, R, rows_off * W, np.arange(nn)], 1), dev)
+        d_rows = to_dev(rows_host, dev)
+        fac = green_factors_device(dmesh, side, K, d_rows, fdesc, to_dev(diam, dev), z, sq, nz,
+                                   int(R.sum()), dev)
+        ta = time.perf_counter()
+        t_factor += ta - tf
+        # batched ACA
+        vcap = R * limit
+        v_off = _offsets(vcap)
+        piv_off_l = _offsets(limit)
+        adesc = to_dev(np.stack([rows_off * W, R, piv_off_l, v_off], 1), dev)
+        V = empty(max(int(vcap.sum()), 1), dev)
+        U = empty(max(int(vcap.sum()), 1), dev)
+        d_piv = torch.zeros(max(int(limit.sum()), 1), dtype=torch.int64, device=dev)
+        d_rank = torch.zeros(nn, dtype=torch.int64, device=dev)
+        with torch.cuda.device(dev):
+            _native.call("gc_aca", nn, ptr(adesc), W, float(eps), 0, ptr(fac), ptr(d_piv),
+                         ptr(d_rank), ptr(V), ptr(U), int(R.max()), stream)
+        rank = d_rank.cpu().numpy()
+        piv_local = d_piv.cpu().numpy()
+        t_aca += time.perf_counter() - ta
+        del U, fac
+        # local -> global pivots, compact store
+        sel = _ranges(piv_off_l, rank)
+        node_of = np.repeat(np.arange(nn), rank)
+        glob = rows_host[rows_off[node_of] + piv_local[sel]]
+        gpiv[cursor:cursor + len(glob)] = glob
+        store.piv_off[ids] = cursor + _offsets(rank)
+        cursor += len(glob)
+        store.rank[ids] = rank
+        store.v_off[ids] = v_base + v_off
+        v_levels.append(V)
+        v_base += V.numel()
+    store.pivots_host = gpiv[:cursor].copy()
+    store.pivots = to_dev(store.pivots_host if cursor else np.zeros(1, np.int64), dev)
+    store.V = torch.cat(v_levels) if v_levels else empty(1, dev)
+    if side == "row" and mat.any():
+        ids = np.flatnonzero(mat & (store.rank > 0))
+        tdesc = to_dev(np.stack([store.v_off[ids], store.rows[ids], store.rank[ids]], 1), dev)
+        store.VT = torch.zeros_like(store.V)
+        with torch.cuda.device(dev):
+            _native.call("gc_batched_transpose", len(ids), ptr(tdesc), ptr(store.V),
+                         ptr(store.VT), stream)
+    # coefficient offsets: breadth first, siblings adjacent
+    pos = 0
+    queue = list(roots)
+    for r in roots:
+        store.coef_off[r] = pos
+        pos += store.rank[r]
+    k = 0
+    while k < len(queue):
+        i = queue[k]
+        k += 1
+        if not flat.is_leaf[i]:
+            for c in (flat.left[i], flat.right[i]):
+                store.coef_off[c] = pos
+                pos += store.rank[c]
+                queue.append(c)
+    store.coef_size = int(pos)
+    store.timing = {"factor_s": t_factor, "aca_s": t_aca, "total_s": time.perf_counter() - t0}
+    # host BasisNode objects
+    by_index = {}
+
+    def make(i):
+        kids = () if flat.is_leaf[i] else (make(int(flat.left[i])), make(int(flat.right[i])))
+        o, r = store.piv_off[i], store.rank[i]
+        bn = BasisNode(flat.node(i), store.pivots_host[o:o + r], kids, store, i)
+        by_index[i] = bn
+        return bn
+
+    root_nodes = [make(int(r)) for r in roots]
+    return ClusterBasis(root_nodes, by_index, store)
+
+
+def expand_basis(node):
+    """Dense cluster-size x rank matrix realised by the nested basis."""
+    if not node.children:
+        return node.v
+    return np.vstack([expand_basis(c) @ c.transfer for c in node.children])
+
+
+# --------------------------------------------------------------------------
+# H2 matrix
+
+class _BlockList(Sequence):
+    """Lazy list of coupling / near-field blocks backed by a device store
+    (column-major per block); ``values`` are host arrays created on access."""
+
+    def __init__(self, factory, rows, cols, nr, nc, off, store):
+        self._factory = factory
+        self._rows, self._cols = rows, cols
+        self._nr, self._nc, self._off = nr, nc, off
+        self._store = store
+        self._host = None
+
+    def __len__(self):
+        return len(self._rows)
+
+    def _host_store(self):
+        if self._host is None:
+            self._host = self._store.cpu().numpy()
+        return self._host
+
+    def __getitem__(self, i):
+        if isinstance(i, slice):
+            return [self[j] for j in range(*i.indices(len(self)))]
+        if i < 0:
+            i += len(self)
+        nr, nc, o = int(self._nr[i]), int(self._nc[i]), int(self._off[i])
+        vals = self._host_store()[o:o + nr * nc].reshape(nc, nr).T
+        return self._factory(self._tree_r.node(int(self._rows[i])),
+                             self._tree_c.node(int(self._cols[i])), vals)
+
+    def bind(self, row_flat, col_flat):
+        self._tree_r, self._tree_c = row_flat, col_flat
+        return self
+
+
+class H2Matrix:
+    """Compressed operator (``gca.py:234-259``) whose blocks live in HBM.
+
+    ``dev`` holds the device stores and the matvec plans used by
+    :mod:`h2`; ``coupling`` / ``nearfield`` are lazy host views.
+    """
+
+    def __init__(self, row_tree, col_tree, row_basis, col_basis, coupling, nearfield,
+                 exec_stats=None, dev=None):
+        self.row_tree = row_tree
+        self.col_tree = col_tree
+        self.row_basis = row_basis
+        self.col_basis = col_basis
+        self.coupling = coupling
+        self.nearfield = nearfield
+        self.exec_stats = exec_stats
+        self.dev = dev
+
+    @property
+    def shape(self):
+        return (self.row_tree.size, self.col_tree.size)
+
+    def __repr__(self):
+        return "H2Matrix(%dx%d, %d coupling, %d nearfield)" % (
+            self.shape + (len(self.coupling), len(self.nearfield)))
+
+
+class DeviceH2:
+    """Device-resident block data of an H2 matrix.
+
+    coupling store: S (r_tau x r_sigma) column-major per block;
+    near store: N (size_tau x size_sigma) column-major per block.
+    Block metadata arrays are kept in reference (depth-first) order.
+    """
+
+    def __init__(self, device):
+        self.device = device
+        self.plans = {}
+
+
+def build_h2(btree, row_basis, col_basis, mesh, kind="slp", basis="constant",
+             disc="galerkin", orders=(3, 5), capacity=None, threads=None, device=None,
+             row_range=None):
+    """Assemble the H2 matrix (``gca.py:282-312``) on the device.
+
+    Admissible leaves get exact entries at pivot rows x pivot columns,
+    inadmissible leaves dense blocks.  ``row_range=(lo, hi)`` restricts the
+    assembly to block rows whose row cluster lies in tree positions
+    [lo, hi) (block-row sharding across GPUs, SURVEY.md §8 e)."""
+    if disc != "galerkin":
+        raise ConfigError("unknown discretization %r" % (disc,) if disc != "collocation"
+                          else "collocation is out of scope on the device")
+    check_mesh(mesh, kind, basis)
+    dev = require_device(device)
+    fb = btree.flat
+    rf, cf = fb.row_tree, fb.col_tree
+    rstore, cstore = row_basis.store, col_basis.store
+    ids = btree._leaf_ids()
+    st = fb.state[ids]
+    lr, lc = fb.row[ids], fb.col[ids]
+    if row_range is not None:
+        keep = (rf.start[lr] >= row_range[0]) & (rf.stop[lr] <= row_range[1])
+        ids, st, lr, lc = ids[keep], st[keep], lr[keep], lc[keep]
+    adm = st == 0
+    cr, cc = lr[adm], lc[adm]
+    nr_r, nc_r = lr[~adm], lc[~adm]
+    if np.any(~rstore.materialized[cr]) or np.any(~cstore.materialized[cc]):
+        raise ConfigError("coupling block without basis content; build the bases "
+                          "with coupling_marks(btree)")
+    dmesh = DeviceMesh.get(mesh, orders[0], dev)
+    rules = DeviceRules.get(orders[1], dev)
+    queue = SingularQueue.get(mesh, dev)
+    t0 = time.perf_counter()
+    # coupling blocks: pivot rows x pivot columns
+    c_nr, c_nc = rstore.rank[cr], cstore.rank[cc]
+    c_off = _offsets(c_nr * c_nc)
+    c_total = int((c_nr * c_nc).sum())
+    coup = empty(max(c_total, 1), dev)
+    cdesc = np.stack([rstore.piv_off[cr], c_nr, cstore.piv_off[cc], c_nc, c_off], 1)
+    keep = (c_nr > 0) & (c_nc > 0)
+    stats_c = device_block_assembly(dmesh, rules, queue, rstore.pivots, cstore.pivots,
+                                    cdesc[keep], coup)
+    t1 = time.perf_counter()
+    # near-field blocks: full clusters
+    n_nr = rf.stop[nr_r] - rf.start[nr_r]
+    n_nc = cf.stop[nc_r] - cf.start[nc_r]
+    n_off = _offsets(n_nr * n_nc)
+    near = empty(max(int((n_nr * n_nc).sum()), 1), dev)
+    perm_r = to_dev(rf.perm, dev)
+    perm_c = perm_r if cf is rf else to_dev(cf.perm, dev)
+    ndesc = np.stack([rf.start[nr_r], n_nr, cf.start[nc_r], n_nc, n_off], 1)
+    stats_n = device_block_assembly(dmesh, rules, queue, perm_r, perm_c, ndesc, near)
+    torch.cuda.synchronize(dev)
+    t2 = time.perf_counter()
+    d = DeviceH2(dev)
+    d.coup, d.near = coup, near
+    d.c_rows, d.c_cols, d.c_nr, d.c_nc, d.c_off = cr, cc, c_nr, c_nc, c_off
+    d.n_rows, d.n_cols, d.n_nr, d.n_nc, d.n_off = nr_r, nc_r, n_nr, n_nc, n_off
+    d.perm_r, d.perm_c = perm_r, perm_c
+    d.row_range = row_range
+    d.timing = {"coupling_s": t1 - t0, "nearfield_s": t2 - t1}
+    tasks = [stats_c[k] + stats_n[k] for k in range(4)]
+    exec_stats = [{"case": k, "tasks": int(tasks[k]), "batches": int(tasks[k] > 0)
+                   + int(k == 0 and stats_c[0] > 0 and stats_n[0] > 0),
+                   "wall_s": (t2 - t0) if k == 0 else 0.0} for k in range(4)]
+    coupling = _BlockList(CouplingBlock, cr, cc, c_nr, c_nc, c_off, coup).bind(rf, cf)
+    nearfield = _BlockList(NearfieldBlock, nr_r, nc_r, n_nr, n_nc, n_off, near).bind(rf, cf)
+    return H2Matrix(rf.node(0), cf.node(0), row_basis, col_basis, coupling, nearfield,
+                    exec_stats, d)

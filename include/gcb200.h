@@ -173,6 +173,19 @@ int gc_segmv(int64_t nseg, const int64_t* seg, const int64_t* blk,
              const double* in1, double* out, int accumulate, int64_t max_T,
              void* stream);
 
+/* Panel product, the mvm hot path.  A phase is a list of work items; item
+ * i (items[6i..6i+5] = a_off, xi_off, out_off, T, nrows, mode) computes
+ *     s[t] = sum_{r < nrows} A[a_off + r*T + t] * in[xidx[xi_off + r]]
+ * over a contiguous row-major chunk of a panel (A = A1 if mode&1, in = in1
+ * if mode&2) and writes s to out[out_off + t] (mode&4; added to it if
+ * mode&8) or to scratch[out_off + t].  red (nred,5) = out_off, T,
+ * scratch_off, nitems, accumulate then sums consecutive scratch rows into
+ * out in item order.  One writer per output, fixed order: deterministic. */
+int gc_panelmv(int64_t nitems, const int64_t* items, const int32_t* xidx,
+               const double* A0, const double* A1, const double* in0,
+               const double* in1, double* out, double* scratch, int64_t nred,
+               const int64_t* red, void* stream);
+
 /* FP64 DFMA throughput probe used as the roofline denominator (no FP64
  * figure exists in MEASURED_PEAKS.json): blocks x threads x iters x 8 DFMA. */
 int gc_dfma_probe(int64_t blocks, int64_t threads, int64_t iters, double* out,

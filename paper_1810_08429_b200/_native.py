@@ -51,6 +51,7 @@ _SIGNATURES = {
     "gc_gather": [c_p, c_p, c_i64, c_p, c_p],
     "gc_scatter": [c_p, c_p, c_i64, c_p, c_p],
     "gc_segmv": [c_i64, c_p, c_p, c_p, c_p, c_p, c_p, c_p, ctypes.c_int, c_i64, c_p],
+    "gc_panelmv": [c_i64, c_p, c_p, c_p, c_p, c_p, c_p, c_p, c_p, c_i64, c_p, c_p],
     "gc_dfma_probe": [c_i64, c_i64, c_i64, c_p, c_p],
 }
 _RESTYPES = {"gc_last_error": ctypes.c_char_p, "gc_launch_count": ctypes.c_uint64,

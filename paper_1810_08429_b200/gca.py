@@ -55,6 +55,15 @@ def _offsets(sizes):
     return np.cumsum(sizes) - sizes
 
 
+def _grouped_offsets(keys, sizes):
+    """Offsets that store items with equal key contiguously (keys ascending,
+    original order inside a key)."""
+    order = np.argsort(keys, kind="stable")
+    off = np.empty(len(keys), dtype=np.int64)
+    off[order] = _offsets(np.asarray(sizes, dtype=np.int64)[order])
+    return off
+
+
 # --------------------------------------------------------------------------
 # ACA on one matrix (API parity with gca.aca_interpolation)
 
@@ -498,7 +507,9 @@ def build_h2(btree, row_basis, col_basis, mesh, kind="slp", basis="constant",
     t0 = time.perf_counter()
     # coupling blocks: pivot rows x pivot columns
     c_nr, c_nc = rstore.rank[cr], cstore.rank[cc]
-    c_off = _offsets(c_nr * c_nc)
+    # storage grouped by row cluster: the blocks of one block row form one
+    # contiguous (sum r_sigma) x r_tau panel for the matvec (h2.PanelPlan)
+    c_off = _grouped_offsets(cr, c_nr * c_nc)
     c_total = int((c_nr * c_nc).sum())
     coup = empty(max(c_total, 1), dev)
     cdesc = np.stack([rstore.piv_off[cr], c_nr, cstore.piv_off[cc], c_nc, c_off], 1)
@@ -509,7 +520,7 @@ def build_h2(btree, row_basis, col_basis, mesh, kind="slp", basis="constant",
     # near-field blocks: full clusters
     n_nr = rf.stop[nr_r] - rf.start[nr_r]
     n_nc = cf.stop[nc_r] - cf.start[nc_r]
-    n_off = _offsets(n_nr * n_nc)
+    n_off = _grouped_offsets(nr_r, n_nr * n_nc)
     near = empty(max(int((n_nr * n_nc).sum()), 1), dev)
     perm_r = to_dev(rf.perm, dev)
     perm_c = perm_r if cf is rf else to_dev(cf.perm, dev)

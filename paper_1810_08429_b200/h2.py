@@ -28,7 +28,7 @@ __all__ = ["mvm", "mvm_t", "as_operator", "storage_report", "storage_csv_rows",
 
 
 class _Launch:
-    __slots__ = ("seg", "blk", "nseg", "A0", "A1", "in0", "in1", "out", "acc", "maxT")
+    __slots__ = ("seg", "blk", "nseg", "A0", "A1", "in0", "in1", "out", "acc", "maxT", "name")
 
 
 class MatvecPlan:
@@ -84,7 +84,7 @@ class MatvecPlan:
                 blk = np.stack([fwd.v_off[ids[sel]], K[sel], lda[sel], in_off[sel],
                                 np.zeros(n, np.int64), ts[sel]], 1)
                 self._add(seg, blk, fwdA, None, self.xt if is_leaf else self.xhat, None,
-                          self.xhat, 0)
+                          self.xhat, 0, "forward")
 
         # ---- coupling
         c_off = d.c_off
@@ -106,7 +106,7 @@ class MatvecPlan:
             blk = np.stack([c_off[order], K_all[order], lda_all[order],
                             fwd.coef_off[in_node[order]], np.zeros(len(order), np.int64),
                             ts_all[order]], 1)
-            self._add(seg, blk, d.coup, None, self.xhat, None, self.yhat, 0)
+            self._add(seg, blk, d.coup, None, self.xhat, None, self.yhat, 0, "coupling")
 
         # ---- backward transform, top down
         matb = bwd.materialized & (bwd.rank > 0) & ~btree_.is_leaf
@@ -122,7 +122,7 @@ class MatvecPlan:
             n = len(ids)
             seg = np.stack([out_off, T, np.arange(n), np.arange(1, n + 1)], 1)
             blk = np.stack([bwd.v_off[ids], K, lda, bwd.coef_off[ids], np.zeros(n, np.int64), ts], 1)
-            self._add(seg, blk, bwdA, None, self.yhat, None, self.yhat, 1)
+            self._add(seg, blk, bwdA, None, self.yhat, None, self.yhat, 1, "backward")
 
         # ---- leaf basis + near field, one segment per output leaf
         if trans:
@@ -156,9 +156,9 @@ class MatvecPlan:
         last = np.searchsorted(bl_seg, leaves, side="right")
         seg = np.stack([btree_.start[leaves], size_b[leaves], first, last], 1)
         leafA = bwd.V if trans else bwd.VT
-        self._add(seg, bl, d.near, leafA, self.xt, self.yhat, self.yt, 0)
+        self._add(seg, bl, d.near, leafA, self.xt, self.yhat, self.yt, 0, "leaf_near")
 
-    def _add(self, seg, blk, A0, A1, in0, in1, out, acc):
+    def _add(self, seg, blk, A0, A1, in0, in1, out, acc, name):
         if len(seg) == 0:
             return
         L = _Launch()
@@ -168,16 +168,24 @@ class MatvecPlan:
         L.nseg = len(seg)
         L.A0, L.A1, L.in0, L.in1, L.out, L.acc = A0, A1, in0, in1, out, acc
         L.maxT = int(np.max(seg[:, 1]))
+        L.name = name
         self.launches.append(L)
 
-    def run(self, x_dev, y_dev):
-        """y_dev = H x_dev (or H^T) for device vectors in external order."""
+    def run(self, x_dev, y_dev, phase_events=None, phase="coupling"):
+        """y_dev = H x_dev (or H^T) for device vectors in external order.
+        ``phase_events=(start, end)`` records CUDA events around the launch
+        named ``phase`` (bench roofline timing on the launching stream)."""
         stream = stream_handle()
         _native.call("gc_gather", ptr(x_dev), ptr(self.perm_in), self.n_in, ptr(self.xt), stream)
         self.yhat.zero_()
         for L in self.launches:
+            timed = phase_events is not None and L.name == phase
+            if timed:
+                phase_events[0].record()
             _native.call("gc_segmv", L.nseg, ptr(L.seg), ptr(L.blk), ptr(L.A0), ptr(L.A1),
                          ptr(L.in0), ptr(L.in1), ptr(L.out), L.acc, L.maxT, stream)
+            if timed:
+                phase_events[1].record()
         _native.call("gc_scatter", ptr(self.yt), ptr(self.perm_out), self.n_out, ptr(y_dev), stream)
 
     @property
@@ -185,10 +193,19 @@ class MatvecPlan:
         return len(self.launches) + 2
 
 
-def plan(h, trans=False):
+def plan(h, trans=False, graph=True):
+    """Cached product plan: PanelPlan (CUDA graph) for H x, MatvecPlan
+    (segmented kernel over the same storage) for H^T x."""
     key = "T" if trans else "N"
     if key not in h.dev.plans:
-        h.dev.plans[key] = MatvecPlan(h, trans)
+        if trans:
+            h.dev.plans[key] = MatvecPlan(h, True)
+        else:
+            pl = PanelPlan(h)
+            if graph:
+                with torch.cuda.device(pl.dev):
+                    pl.capture()
+            h.dev.plans[key] = pl
     return h.dev.plans[key]
 
 
@@ -209,11 +226,26 @@ def mvm_device(h, x_dev, y_dev=None, trans=False):
 
 
 def mvm(h, x):
-    """y = H x, external ordering in and out (``h2.py:63-80``)."""
+    """y = H x, external ordering in and out (``h2.py:63-80``).
+
+    Host vector -> pinned staging -> static device input of the captured
+    graph -> replay -> pinned staging -> host vector."""
     nr, nc = h.shape
     x = _check_dim(x, nc)
-    xd = to_dev(x, h.dev.device)
-    return mvm_device(h, xd).cpu().numpy()
+    p = plan(h)
+    if not hasattr(p, "pin_x"):
+        p.pin_x = torch.empty(nc, dtype=torch.float64, pin_memory=True)
+        p.pin_y = torch.empty(nr, dtype=torch.float64, pin_memory=True)
+    p.pin_x.numpy()[:] = x
+    with torch.cuda.device(p.dev):
+        p.x.copy_(p.pin_x, non_blocking=True)
+        if p.graph is not None:
+            p.graph.replay()
+        else:
+            p._body()
+        p.pin_y.copy_(p.y, non_blocking=True)
+        torch.cuda.current_stream().synchronize()
+    return p.pin_y.numpy().copy()
 
 
 def mvm_t(h, x):
@@ -356,3 +388,213 @@ def cgnr_solve(apply, b, tol=1e-8, max_iter=500):
         p = s + (ss_new / ss) * p
         ss = ss_new
     return CGResult(x, np.asarray(hist), bool(hist[-1] <= tol * bnorm))
+
+
+# --------------------------------------------------------------------------
+# panel plan: the non-transposed product (the benchmarked hot path)
+
+_ITEM_ELEMS = 4096          # ~32 KB of matrix data per work item
+
+
+class _Phase:
+    __slots__ = ("name", "items", "xidx", "red", "nitems", "nred", "A0", "A1", "in0", "in1",
+                 "out", "scratch", "bytes")
+
+
+class PanelPlan:
+    """mvm as 6 phases of ``gc_panelmv`` over contiguous panels.
+
+    Streams: the near-field (independent of the basis transforms) runs on a
+    side stream concurrently with the latency-bound forward transform; the
+    leaf-basis phase joins it.  ``capture()`` records the whole product into
+    one CUDA graph with static input/output buffers.
+    """
+
+    def __init__(self, h):
+        d = h.dev
+        dev = d.device
+        self.dev = dev
+        rs, cs = h.row_basis.store, h.col_basis.store
+        rf, cf = h.row_tree.flat, h.col_tree.flat
+        self.n_in, self.n_out = cf.stop[0], rf.stop[0]
+        self.perm_in, self.perm_out = d.perm_c, d.perm_r
+        f64 = dict(dtype=torch.float64, device=dev)
+        self.x = torch.zeros(self.n_in, **f64)
+        self.y = torch.zeros(self.n_out, **f64)
+        self.xt = torch.zeros(self.n_in, **f64)
+        self.yt = torch.zeros(self.n_out, **f64)
+        self.xhat = torch.zeros(max(cs.coef_size, 1), **f64)
+        self.yhat = torch.zeros(max(rs.coef_size, 1), **f64)
+        self.main_phases, self.side_phases, self.tail_phases = [], [], []
+        size_r = rf.stop - rf.start
+        # forward transform (column basis), by height
+        mat = cs.materialized & (cs.rank > 0)
+        for h_ in np.unique(cf.height[mat]):
+            ids = np.flatnonzero(mat & (cf.height == h_))
+            leaf = h_ == 0
+            K = cs.rows[ids]
+            base = cf.start[ids] if leaf else cs.coef_off[cf.left[ids]]
+            panels = (cs.v_off[ids], K, cs.rank[ids], [b + np.arange(k) for b, k in zip(base, K)],
+                      cs.coef_off[ids], 0)
+            self.main_phases.append(self._phase("forward", panels, cs.V, None,
+                                                self.xt if leaf else self.xhat, None, self.xhat))
+        # coupling (row panels)
+        live = (d.c_nr > 0) & (d.c_nc > 0)
+        order = np.flatnonzero(live)[np.argsort(d.c_rows[live], kind="stable")]
+        if order.size:
+            sn = d.c_rows[order]
+            cuts = np.flatnonzero(np.r_[True, sn[1:] != sn[:-1]])
+            ends = np.r_[cuts[1:], len(order)]
+            xi = [cs.coef_off[d.c_cols[order[a:b]]] for a, b in zip(cuts, ends)]
+            ks = [d.c_nc[order[a:b]] for a, b in zip(cuts, ends)]
+            rows = [np.concatenate([o + np.arange(k) for o, k in zip(oo, kk)]) for oo, kk in zip(xi, ks)]
+            K = np.array([len(r) for r in rows], dtype=np.int64)
+            panels = (d.c_off[order[cuts]], K, d.c_nr[order[cuts]], rows, rs.coef_off[sn[cuts]], 0)
+            self.main_phases.append(self._phase("coupling", panels, d.coup, None, self.xhat, None,
+                                                self.yhat))
+        # backward transform (row basis), top down
+        matb = rs.materialized & (rs.rank > 0) & ~rf.is_leaf
+        for h_ in sorted(np.unique(rf.height[matb]), reverse=True):
+            ids = np.flatnonzero(matb & (rf.height == h_))
+            K = rs.rank[ids]
+            panels = (rs.v_off[ids], K, rs.rows[ids], [o + np.arange(k) for o, k in zip(rs.coef_off[ids], K)],
+                      rs.coef_off[rf.left[ids]], 1)
+            self.main_phases.append(self._phase("backward", panels, rs.VT, None, self.yhat, None,
+                                                self.yhat))
+        # near field (side stream): one panel per row leaf
+        order = np.argsort(d.n_rows, kind="stable")
+        sn = d.n_rows[order]
+        cuts = np.flatnonzero(np.r_[True, sn[1:] != sn[:-1]]) if len(sn) else np.zeros(0, np.int64)
+        ends = np.r_[cuts[1:], len(order)]
+        rows = [np.concatenate([cf.start[c] + np.arange(k) for c, k in
+                                zip(d.n_cols[order[a:b]], d.n_nc[order[a:b]])]) for a, b in zip(cuts, ends)]
+        K = np.array([len(r) for r in rows], dtype=np.int64)
+        panels = (d.n_off[order[cuts]], K, d.n_nr[order[cuts]], rows, rf.start[sn[cuts]], 0)
+        self.side_phases.append(self._phase("nearfield", panels, d.near, None, self.xt, None, self.yt))
+        # leaf basis (after the join): yt[leaf] += V yhat
+        leaves = np.flatnonzero(rf.is_leaf & rs.materialized & (rs.rank > 0))
+        if d.row_range is not None:
+            leaves = leaves[(rf.start[leaves] >= d.row_range[0]) & (rf.stop[leaves] <= d.row_range[1])]
+        if leaves.size:
+            K = rs.rank[leaves]
+            panels = (rs.v_off[leaves], K, size_r[leaves],
+                      [o + np.arange(k) for o, k in zip(rs.coef_off[leaves], K)], rf.start[leaves], 1)
+            self.tail_phases.append(self._phase("leafbasis", panels, rs.VT, None, self.yhat, None, self.yt))
+        self.side = torch.cuda.Stream(device=dev)
+        self.graph = None
+
+    def _phase(self, name, panels, A0, A1, in0, in1, out):
+        a_off, K, T, rows, out_off, accumulate = panels
+        a_off = np.asarray(a_off, np.int64)
+        K = np.asarray(K, np.int64)
+        T = np.asarray(T, np.int64)
+        out_off = np.asarray(out_off, np.int64)
+        n = len(a_off)
+        elems = int((K * T).sum())
+        # chunk rows so every phase has >= ~4 items per SM when it can
+        target = max(256, min(_ITEM_ELEMS, elems // (148 * 4) + 1))
+        rpi = np.maximum(1, -(-target // np.maximum(T, 1)))          # rows per item
+        nit = np.maximum(1, -(-K // rpi))
+        xidx = np.concatenate(rows).astype(np.int32) if n else np.zeros(1, np.int32)
+        xoff = _offsets_np(K)
+        item_panel = np.repeat(np.arange(n), nit)
+        item_k = _ranges_np(np.zeros(n, np.int64), nit) * rpi[item_panel]
+        item_rows = np.minimum(rpi[item_panel], K[item_panel] - item_k)
+        multi = nit > 1
+        scr_off = _offsets_np(np.where(multi, nit * T, 0))
+        item_idx_in_panel = _ranges_np(np.zeros(n, np.int64), nit)
+        direct = ~multi[item_panel]
+        out_col = np.where(direct, out_off[item_panel],
+                           scr_off[item_panel] + item_idx_in_panel * T[item_panel])
+        mode = np.where(direct, 4 | (8 * accumulate), 0)
+        items = np.stack([a_off[item_panel] + item_k * T[item_panel], xoff[item_panel] + item_k,
+                          out_col, T[item_panel], item_rows, mode], 1)
+        red = np.stack([out_off[multi], T[multi], scr_off[multi], nit[multi],
+                        np.full(int(multi.sum()), accumulate)], 1)
+        P = _Phase()
+        P.name = name
+        P.items = to_dev(np.ascontiguousarray(items, np.int64), self.dev)
+        P.xidx = to_dev(xidx, self.dev)
+        P.red = to_dev(np.ascontiguousarray(red, np.int64), self.dev) if multi.any() else None
+        P.nitems, P.nred = len(items), int(multi.sum())
+        P.A0, P.A1, P.in0, P.in1, P.out = A0, A1, in0, in1, out
+        P.scratch = torch.zeros(max(int((np.where(multi, nit * T, 0)).sum()), 1),
+                                dtype=torch.float64, device=self.dev)
+        P.bytes = 8 * elems
+        return P
+
+    def _launch(self, P, stream):
+        _native.call("gc_panelmv", P.nitems, ptr(P.items), ptr(P.xidx), ptr(P.A0), ptr(P.A1),
+                     ptr(P.in0), ptr(P.in1), ptr(P.out), ptr(P.scratch), P.nred, ptr(P.red),
+                     stream)
+
+    def _body(self, phase_events=None, phase="coupling"):
+        main = torch.cuda.current_stream()
+        st = stream_handle()
+        _native.call("gc_gather", ptr(self.x), ptr(self.perm_in), self.n_in, ptr(self.xt), st)
+        fork = torch.cuda.Event()
+        fork.record(main)
+        with torch.cuda.stream(self.side):
+            self.side.wait_event(fork)
+            sst = stream_handle()
+            for P in self.side_phases:
+                self._launch(P, sst)
+            join = torch.cuda.Event()
+            join.record(self.side)
+        self.yhat.zero_()
+        for P in self.main_phases:
+            timed = phase_events is not None and P.name == phase
+            if timed:
+                phase_events[0].record(main)
+            self._launch(P, st)
+            if timed:
+                phase_events[1].record(main)
+        main.wait_event(join)
+        for P in self.tail_phases:
+            self._launch(P, st)
+        _native.call("gc_scatter", ptr(self.yt), ptr(self.perm_out), self.n_out, ptr(self.y), st)
+
+    def capture(self):
+        """Record the product into a CUDA graph (static x -> y buffers)."""
+        s = torch.cuda.Stream(device=self.dev)
+        s.wait_stream(torch.cuda.current_stream())
+        with torch.cuda.stream(s):
+            self._body()                   # warm-up outside capture
+        torch.cuda.current_stream().wait_stream(s)
+        torch.cuda.synchronize(self.dev)
+        g = torch.cuda.CUDAGraph()
+        with torch.cuda.graph(g):
+            self._body()
+        torch.cuda.synchronize(self.dev)
+        self.graph = g
+        return g
+
+    def run(self, x_dev, y_dev, phase_events=None, phase="coupling"):
+        """y_dev = H x_dev (device vectors, external ordering)."""
+        self.x.copy_(x_dev, non_blocking=True)
+        if phase_events is None and self.graph is not None:
+            self.graph.replay()
+        else:
+            self._body(phase_events, phase)
+        y_dev.copy_(self.y, non_blocking=True)
+
+    @property
+    def num_kernels(self):
+        n = 2
+        for P in self.main_phases + self.side_phases + self.tail_phases:
+            n += 1 + int(P.nred > 0)
+        return n
+
+
+def _offsets_np(sizes):
+    sizes = np.asarray(sizes, dtype=np.int64)
+    return np.cumsum(sizes) - sizes
+
+
+def _ranges_np(starts, lengths):
+    lengths = np.asarray(lengths, dtype=np.int64)
+    total = int(lengths.sum())
+    if total == 0:
+        return np.zeros(0, dtype=np.int64)
+    heads = np.cumsum(lengths) - lengths
+    return np.arange(total, dtype=np.int64) + np.repeat(np.asarray(starts, np.int64) - heads, lengths)

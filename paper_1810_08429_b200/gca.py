@@ -325,7 +325,7 @@ def build_cluster_basis(tree, mesh, basis, m, delta_factor=0.5, eps=1e-4, side="
         v_off = _offsets(vcap)
         piv_off_l = _offsets(limit)
         adesc = to_dev(np.stack([rows_off * W, R, piv_off_l, v_off], 1), dev)
-        V = empty(max(int(vcap.sum()), 1), dev)
+        V = torch.zeros(max(int(vcap.sum()), 1), dtype=torch.float64, device=dev)
         U = empty(max(int(vcap.sum()), 1), dev)
         d_piv = torch.zeros(max(int(limit.sum()), 1), dtype=torch.int64, device=dev)
         d_rank = torch.zeros(nn, dtype=torch.int64, device=dev)

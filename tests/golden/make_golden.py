@@ -1,0 +1,176 @@
+"""Generate the golden fixtures from the reference implementation itself.
+
+Run in the build container (the reference is importable there):
+    PYTHONPATH=/root/reference/pkg/src python tests/golden/make_golden.py
+Outputs tests/golden/*.npz.  The GPU box has no /root/reference; the tests
+read only these committed files.
+"""
+
+import os
+import sys
+
+import numpy as np
+
+sys.path.insert(0, "/root/reference/pkg/src")
+from greencross import assembly as A  # noqa: E402
+from greencross import clustering as C  # noqa: E402
+from greencross import gca as GC  # noqa: E402
+from greencross import geometry as G  # noqa: E402
+from greencross import h2 as H  # noqa: E402
+from greencross import quadrature as Q  # noqa: E402
+
+OUT = os.path.dirname(os.path.abspath(__file__))
+
+
+def cube(level):
+    s = G.build_sphere_mesh(level)
+    v = s.vertices
+    return G.TriangleMesh(v / np.abs(v).max(axis=1, keepdims=True), s.triangles)
+
+
+def pair_tasks(mesh, n_disjoint, seed):
+    """Random disjoint tasks plus every singular pair of a triangle subset."""
+    rng = np.random.default_rng(seed)
+    rows = list(rng.integers(0, mesh.nt, n_disjoint))
+    cols = list(rng.integers(0, mesh.nt, n_disjoint))
+    stars = mesh.vertex_stars()
+    for t in rng.choice(mesh.nt, 24, replace=False):
+        for v in mesh.triangles[t]:
+            for s in stars[v]:
+                rows.append(int(t))
+                cols.append(int(s))
+    rows, cols = np.array(rows), np.array(cols)
+    case, px, py = Q.classify_pairs(mesh.triangles[rows], mesh.triangles[cols])
+    ev = A.galerkin_pair_evaluator("slp", mesh, "constant", 3, 5)
+    vals = np.empty(len(rows))
+    for k in range(4):
+        m = case == k
+        if m.any():
+            vals[m] = ev(k, rows[m], cols[m], px[m], py[m]).ravel()
+    return dict(rows=rows, cols=cols, case=case, px=px, py=py, values=vals)
+
+
+def pipeline(mesh, eps, seed, nsample=40):
+    tree = C.build_cluster_tree(mesh, "constant", 16)
+    bt = C.build_block_tree(tree, eta=1.0)
+    rm, cm = GC.coupling_marks(bt)
+    rb = GC.build_cluster_basis(tree, mesh, "constant", 3, 0.5, eps, "row", (3, 5), rm)
+    cb = GC.build_cluster_basis(tree, mesh, "constant", 3, 0.5, eps, "col", (3, 5), cm)
+    hm = GC.build_h2(bt, rb, cb, mesh, "slp", "constant", "galerkin", (3, 5))
+    nodes = tree.nodes()
+    leaves = bt.leaves()
+    out = dict(perm=tree.perm.astype(np.int32),
+               start=np.array([n.start for n in nodes], np.int32),
+               stop=np.array([n.stop for n in nodes], np.int32),
+               lower=np.array([n.box.lower for n in nodes]),
+               upper=np.array([n.box.upper for n in nodes]),
+               leaf_row=np.array([l.row.index for l in leaves], np.int32),
+               leaf_col=np.array([l.col.index for l in leaves], np.int32),
+               leaf_adm=np.array([l.state == "admissible" for l in leaves]))
+    for side, basis in (("row", rb), ("col", cb)):
+        bns = basis.nodes()
+        out[side + "_node"] = np.array([b.cluster.index for b in bns], np.int32)
+        out[side + "_rank"] = np.array([b.rank for b in bns], np.int32)
+        out[side + "_piv"] = np.concatenate([b.pivots for b in bns]).astype(np.int32)
+        # transfers / leaf bases of a few nodes for value checks
+        rng = np.random.default_rng(seed + (side == "col"))
+        pick = rng.choice(len(bns), min(12, len(bns)), replace=False)
+        vals, meta = [], []
+        for i in pick:
+            b = bns[i]
+            m = b.v if b.v is not None else b.transfer
+            kind = 0 if b.v is not None else 1
+            if m is None:
+                continue
+            meta.append((b.cluster.index, kind, m.shape[0], m.shape[1]))
+            vals.append(m.ravel())
+        out[side + "_mat_meta"] = np.array(meta, np.int64).reshape(-1, 4)
+        out[side + "_mat_vals"] = np.concatenate(vals) if vals else np.zeros(0)
+    rng = np.random.default_rng(seed)
+    for name, blocks in (("coup", hm.coupling), ("near", hm.nearfield)):
+        pick = np.sort(rng.choice(len(blocks), min(nsample, len(blocks)), replace=False))
+        out[name + "_pick"] = pick.astype(np.int32)
+        out[name + "_shape"] = np.array([blocks[i].values.shape for i in pick], np.int32)
+        out[name + "_vals"] = np.concatenate([blocks[i].values.ravel() for i in pick])
+    xs = np.random.default_rng(seed + 7).standard_normal((2, mesh.nt))
+    out["x"] = xs
+    out["mvm"] = np.stack([H.mvm(hm, x) for x in xs])
+    out["mvm_t"] = np.stack([H.mvm_t(hm, x) for x in xs])
+    rep = H.storage_report(hm)
+    out["storage_keys"] = np.array(list(rep.keys()))
+    out["storage_vals"] = np.array(list(rep.values()), np.int64)
+    out["exec_tasks"] = np.array([s["tasks"] for s in hm.exec_stats], np.int64)
+    return out
+
+
+def factors(mesh, seed):
+    """Green factors (row and column side) of leaves and of internal nodes
+    on the reference's own row lists, plus ACA results on them."""
+    tree = C.build_cluster_tree(mesh, "constant", 16)
+    nodes = tree.nodes()
+    rng = np.random.default_rng(seed)
+    leaves = [n for n in nodes if n.is_leaf()]
+    inner = [n for n in nodes if not n.is_leaf() and n.size <= 64]
+    chosen = list(rng.choice(len(leaves), 4, replace=False))
+    out = {"node": [], "side": [], "rows": [], "nrows": [], "A": [], "piv": [], "npiv": [], "V": []}
+    for node in [leaves[i] for i in chosen] + inner[:3]:
+        rows = np.asarray(node.indices)
+        for side in ("row", "col"):
+            rule = Q.green_box_rule(node.box, 0.5 * node.box.diameter(), 3)
+            stub = GC._Rows(rows, node.box)
+            a = (A.green_row_factor(stub, rule, mesh, "constant") if side == "row" else
+                 A.green_col_factor((stub, stub), rule, mesh, "constant"))
+            it = GC.aca_interpolation(a, 1e-6)
+            out["node"].append(node.index)
+            out["side"].append(side == "col")
+            out["rows"].append(rows)
+            out["nrows"].append(len(rows))
+            out["A"].append(a.ravel())
+            out["piv"].append(it.pivots)
+            out["npiv"].append(len(it.pivots))
+            out["V"].append(it.v.ravel())
+    return {k: (np.concatenate(v) if k in ("rows", "A", "piv", "V") else np.array(v))
+            for k, v in out.items()}
+
+
+def aca_kats():
+    rng = np.random.default_rng(2024)
+    mats, shapes, eps, pivs, npiv, vs = [], [], [], [], [], []
+    q1, _ = np.linalg.qr(rng.standard_normal((60, 20)))
+    q2, _ = np.linalg.qr(rng.standard_normal((20, 20)))
+    cases = [(np.eye(8), 1e-12), (np.outer(np.arange(1.0, 7.0), [2.0, -1.0, 0.5]), 1e-12),
+             (rng.standard_normal((200, 24)), 1e-6), (np.zeros((10, 4)), 1e-8),
+             (q1 @ np.diag(10.0 ** -np.arange(20.0)) @ q2.T, 1e-3),
+             (rng.standard_normal((37, 108)), 1e-4)]
+    for a, e in cases:
+        it = GC.aca_interpolation(a, e)
+        mats.append(a.ravel())
+        shapes.append(a.shape)
+        eps.append(e)
+        pivs.append(it.pivots)
+        npiv.append(len(it.pivots))
+        vs.append(it.v.ravel())
+    return dict(A=np.concatenate(mats), shape=np.array(shapes), eps=np.array(eps),
+                piv=np.concatenate(pivs), npiv=np.array(npiv), V=np.concatenate(vs))
+
+
+def main():
+    s3 = G.build_sphere_mesh(3)
+    np.savez_compressed(os.path.join(OUT, "pairs_sphere3.npz"), **pair_tasks(s3, 600, 11))
+    c3 = cube(3)
+    np.savez_compressed(os.path.join(OUT, "pairs_cube3.npz"), **pair_tasks(c3, 300, 12))
+    s2 = G.build_sphere_mesh(2)
+    idx = np.arange(s2.nt)
+    np.savez_compressed(os.path.join(OUT, "dense_sphere2.npz"),
+                        values=A.assemble_galerkin_block("slp", s2, "constant", idx, idx).values)
+    np.savez_compressed(os.path.join(OUT, "factors_sphere4.npz"), **factors(G.build_sphere_mesh(4), 5))
+    np.savez_compressed(os.path.join(OUT, "aca_kats.npz"), **aca_kats())
+    np.savez_compressed(os.path.join(OUT, "h2_sphere4_eps1e-4.npz"),
+                        **pipeline(G.build_sphere_mesh(4), 1e-4, 21))
+    np.savez_compressed(os.path.join(OUT, "h2_cube4_eps1e-6.npz"), **pipeline(cube(4), 1e-6, 22))
+    np.savez_compressed(os.path.join(OUT, "h2_sphere5_eps1e-6.npz"),
+                        **pipeline(G.build_sphere_mesh(5), 1e-6, 23))
+
+
+if __name__ == "__main__":
+    main()

@@ -1,0 +1,62 @@
+"""The C-ABI library: builds for sm_100a, loads without a GPU, exports every
+symbol include/gcb200.h declares, and fails loudly (no CPU fallback) when
+no device is present."""
+
+import ctypes
+import os
+import re
+
+import pytest
+
+from paper_1810_08429_b200 import _native, build_native
+from paper_1810_08429_b200.errors import DeviceError
+
+HEADER = os.path.join(os.path.dirname(os.path.dirname(os.path.abspath(__file__))),
+                      "include", "gcb200.h")
+
+
+def declared():
+    text = open(HEADER).read()
+    text = re.sub(r"/\*.*?\*/", "", text, flags=re.S)
+    return sorted(set(re.findall(r"\b(gc_[a-z0-9_]+)\s*\(", text)))
+
+
+def test_library_builds_and_loads():
+    build_native.build()
+    lib = _native.load()
+    assert lib.gc_abi_version() == _native.ABI_VERSION
+
+
+def test_every_declared_symbol_is_exported_and_bound():
+    lib = ctypes.CDLL(_native.LIB_PATH)
+    names = declared()
+    assert len(names) >= 15
+    for name in names:
+        assert hasattr(lib, name), name
+        assert name in _native.EXPORTED, "%s has no ctypes signature" % name
+
+
+def test_sm100a_code_object():
+    import subprocess
+    out = subprocess.run(["/usr/local/cuda/bin/cuobjdump", "--list-elf", _native.LIB_PATH],
+                         capture_output=True, text=True).stdout
+    assert "sm_100a" in out
+
+
+def test_error_mapping():
+    _native.load()
+    with pytest.raises(Exception) as ei:
+        # invalid configuration is rejected before touching the device
+        _native.call("gc_green_factor", None, 0, 54, 1, None, None, None, None, None, None,
+                     None, None, None)
+    assert "null" in str(ei.value)
+
+
+def test_no_cpu_fallback():
+    import torch
+    if torch.cuda.is_available():
+        pytest.skip("GPU present")
+    from paper_1810_08429_b200 import assembly, geometry
+    m = geometry.build_sphere_mesh(1)
+    with pytest.raises(DeviceError):
+        assembly.assemble_galerkin_block("slp", m, "constant", [0, 1], [2, 3])

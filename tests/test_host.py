@@ -1,0 +1,148 @@
+"""Host-side mirror (meshes, rule tables, classification, trees, block
+trees, configuration, errors) against the reference fixtures: bit-exact."""
+
+import os
+
+import numpy as np
+import pytest
+
+from conftest import PIPELINES, golden, mesh_for
+from oracle import port as P
+from paper_1810_08429_b200 import cli, clustering, geometry, quadrature as Q
+from paper_1810_08429_b200.errors import (ConfigError, MeshFormatError, SizeLimitError)
+
+
+@pytest.mark.parametrize("level", [0, 1, 2, 3, 4])
+def test_sphere_mesh_matches_oracle_charts(level):
+    m = geometry.build_sphere_mesh(level)
+    assert m.nt == 8 * 4 ** level
+    nodes, gram = P.chart_nodes(m.vertices, m.triangles)
+    pack = geometry.chart_pack(m)
+    assert np.array_equal(pack.nodes, nodes) and np.array_equal(pack.gram, gram)
+    assert np.allclose(np.linalg.norm(m.vertices, axis=1), 1.0, atol=1e-15)
+
+
+def test_cube_mesh_is_closed_and_on_the_cube():
+    c = geometry.build_cube_mesh(3)
+    assert c.nt == 512 and np.allclose(np.abs(c.vertices).max(axis=1), 1.0)
+    assert len(c.edges) == 3 * c.nt // 2
+
+
+def test_level_cap_lifted_to_9():
+    assert geometry.LEVEL_CAP == 9
+    with pytest.raises(SizeLimitError):
+        geometry.build_sphere_mesh(10)
+
+
+def test_mesh_roundtrip(tmp_path):
+    m = geometry.build_cube_mesh(2)
+    path = os.path.join(tmp_path, "m.txt")
+    geometry.write_mesh(m, path)
+    r = geometry.read_mesh(path)
+    assert np.array_equal(r.vertices, m.vertices) and np.array_equal(r.triangles, m.triangles)
+    with open(path, "a") as fh:
+        fh.write("1 2\n")
+    with pytest.raises(MeshFormatError):
+        geometry.read_mesh(path)
+
+
+def test_mesh_validation():
+    v = np.array([[0.0, 0, 0], [1, 0, 0], [0, 1, 0], [0, 0, 1]])
+    with pytest.raises(MeshFormatError):
+        geometry.TriangleMesh(v, np.array([[0, 1, 2]]))          # open surface
+    with pytest.raises(MeshFormatError):
+        geometry.TriangleMesh(v, np.array([[0, 1, 5]]))          # bad index
+
+
+@pytest.mark.parametrize("case", [1, 2, 3])
+@pytest.mark.parametrize("q", [2, 3, 5])
+def test_sauter_tables_bitwise(case, q):
+    a = Q.sauter_rule(case, q)
+    x, y, w = P.sauter(case, q)
+    assert np.array_equal(a.x, x) and np.array_equal(a.y, y) and np.array_equal(a.w, w)
+
+
+def test_triangle_gauss_and_box_rule():
+    for q in (1, 2, 4, 7):
+        p, w = Q.triangle_gauss(q)
+        op, ow = P.triangle_rule(q)
+        assert np.array_equal(p, op) and np.array_equal(w, ow)
+        assert abs(w.sum() - 0.5) < 1e-14
+    rng = np.random.default_rng(0)
+    for _ in range(5):
+        lo = rng.standard_normal(3)
+        hi = lo + rng.random(3)
+        a = Q.green_box_rule((lo, hi), 0.3, 3)
+        z, wz, nz = P.box_rule(lo, hi, 0.3, 3)
+        assert np.array_equal(a.points, z) and np.array_equal(a.weights, wz)
+        assert np.array_equal(a.normals, nz)
+    r = Q.green_box_rule((np.zeros(3), np.ones(3)), 0.5, 2)
+    assert abs(r.weights.sum() - 24.0) < 1e-12 and r.k == 24
+
+
+def test_classification_matches_oracle():
+    rng = np.random.default_rng(3)
+    pool = np.array([(0, 1, 2), (2, 1, 5), (3, 4, 2), (3, 4, 5), (1, 2, 6), (0, 5, 6),
+                     (7, 8, 9), (2, 0, 1), (1, 0, 3), (0, 3, 2)])
+    r = pool[rng.integers(0, len(pool), 3000)]
+    c = pool[rng.integers(0, len(pool), 3000)]
+    for a, b in zip(Q.classify_pairs(r, c), P.classify(r, c)):
+        assert np.array_equal(a, b)
+    distinct = [t for t in pool if tuple(t) != (2, 0, 1)]     # one ordering per vertex set
+    for t in distinct:
+        for s in distinct:
+            case = Q.classify_pair(t, s)
+            k = {"identical": 3, "edge": 2, "vertex": 1, "disjoint": 0}[case.kind]
+            tp, sp = np.asarray(t)[list(case.row_perm)], np.asarray(s)[list(case.col_perm)]
+            assert np.array_equal(tp[:k], sp[:k])
+
+
+@pytest.mark.parametrize("name", PIPELINES)
+def test_cluster_and_block_tree_bitwise(name):
+    g = golden(name)
+    mesh = mesh_for(name)
+    tree = clustering.build_cluster_tree(mesh, "constant", leaf_size=16)
+    f = tree.flat
+    assert np.array_equal(tree.perm, g["perm"])
+    assert np.array_equal(f.start, g["start"]) and np.array_equal(f.stop, g["stop"])
+    assert np.array_equal(f.lower, g["lower"]) and np.array_equal(f.upper, g["upper"])
+    assert [n.index for n in tree.nodes()] == list(range(len(f)))
+    bt = clustering.build_block_tree(tree, eta=1.0)
+    lr, lc = bt.flat.leaves()
+    st = bt.flat.state[bt.flat.leaf_ids]
+    assert np.array_equal(lr, g["leaf_row"]) and np.array_equal(lc, g["leaf_col"])
+    assert np.array_equal(st == 0, g["leaf_adm"])
+    lv = bt.leaves()
+    assert len(lv) == len(lr) and lv[5].row.index == lr[5]
+    s = bt.stats()
+    assert s["admissible"] == int(g["leaf_adm"].sum()) and s["leaves"] == len(lr)
+
+
+def test_block_tree_tiles_the_matrix(sphere3):
+    tree = clustering.build_cluster_tree(sphere3, "constant", 16)
+    bt = clustering.build_block_tree(tree, eta=1.0)
+    cover = np.zeros((sphere3.nt, sphere3.nt), dtype=np.int64)
+    for b in bt.leaves():
+        cover[b.row.start:b.row.stop, b.col.start:b.col.stop] += 1
+        if b.state == clustering.ADMISSIBLE:
+            assert clustering.admissible(b.row.box, b.col.box, 1.0)
+    assert np.all(cover == 1)
+
+
+def test_tree_validation(sphere2):
+    with pytest.raises(ConfigError):
+        clustering.build_cluster_tree(sphere2, "quadratic", 16)
+    with pytest.raises(ConfigError):
+        clustering.build_cluster_tree(sphere2, "constant", 0)
+    t = clustering.build_cluster_tree(sphere2, "constant", 16)
+    with pytest.raises(ConfigError):
+        clustering.build_block_tree(t, eta=0.0)
+
+
+def test_config_validation():
+    cfg = cli.default_config()
+    assert (cfg.eta, cfg.m, cfg.leaf_size, cfg.q_reg, cfg.q_sing) == (1.0, 3, 16, 3, 5)
+    for bad in (dict(eps=0.0), dict(m=0), dict(eta=-1.0), dict(q_reg=0), dict(lam=1.5),
+                dict(disc="collocation")):
+        with pytest.raises(ConfigError):
+            cli.default_config(**bad)

@@ -99,22 +99,29 @@ extern "C" int gc_segmv(int64_t nseg, const int64_t* seg, const int64_t* blk, co
 namespace gcb {
 
 constexpr int PAN_THREADS = 256;
-constexpr int PAN_UNROLL = 8;
+constexpr int PAN_UNROLL = 16;
+constexpr int PAN_MAX_ROWS = 1024;   // rows per work item (x gathered to smem)
 
 // item: a_off, xi_off, out_off, T, nrows, mode (bit0 A1, bit1 in1,
 //       bit2 direct to out, bit3 accumulate into out)
+// The item's input entries are gathered into shared memory first, so the
+// streaming loop over A has no dependent loads: 16 independent 8-byte loads
+// per thread are in flight before the first FMA.
 __global__ void __launch_bounds__(PAN_THREADS) k_panelmv(
     const int64_t* __restrict__ items, const int32_t* __restrict__ xidx,
     const double* __restrict__ A0, const double* __restrict__ A1,
     const double* __restrict__ in0, const double* __restrict__ in1,
     double* __restrict__ out, double* __restrict__ scratch) {
     __shared__ double red[PAN_THREADS];
+    __shared__ double xs[PAN_MAX_ROWS];
     const int64_t* it = items + 6 * (int64_t)blockIdx.x;
     const int64_t a_off = it[0], xi_off = it[1], out_off = it[2];
     const int T = (int)it[3], nrows = (int)it[4], mode = (int)it[5];
     const double* __restrict__ A = ((mode & 1) ? A1 : A0) + a_off;
     const double* __restrict__ x = (mode & 2) ? in1 : in0;
     const int32_t* __restrict__ xi = xidx + xi_off;
+    for (int r = threadIdx.x; r < nrows; r += PAN_THREADS) xs[r] = __ldg(x + __ldg(xi + r));
+    __syncthreads();
     const int tt = T < PAN_THREADS ? T : PAN_THREADS;
     const int ng = PAN_THREADS / tt;
     const int g = threadIdx.x / tt;
@@ -123,20 +130,16 @@ __global__ void __launch_bounds__(PAN_THREADS) k_panelmv(
         const bool live = g < ng && t < T;
         double acc = 0.0;
         if (live) {
+            const double* __restrict__ At = A + t;
             int r = g;
             for (; r + (PAN_UNROLL - 1) * ng < nrows; r += PAN_UNROLL * ng) {
                 double a[PAN_UNROLL];
-                int32_t k[PAN_UNROLL];
 #pragma unroll
-                for (int j = 0; j < PAN_UNROLL; ++j) {
-                    a[j] = __ldcs(A + (int64_t)(r + j * ng) * T + t);
-                    k[j] = __ldg(xi + r + j * ng);
-                }
+                for (int j = 0; j < PAN_UNROLL; ++j) a[j] = __ldcs(At + (int64_t)(r + j * ng) * T);
 #pragma unroll
-                for (int j = 0; j < PAN_UNROLL; ++j) acc = fma(a[j], __ldg(x + k[j]), acc);
+                for (int j = 0; j < PAN_UNROLL; ++j) acc = fma(a[j], xs[r + j * ng], acc);
             }
-            for (; r < nrows; r += ng)
-                acc = fma(__ldcs(A + (int64_t)r * T + t), __ldg(x + __ldg(xi + r)), acc);
+            for (; r < nrows; r += ng) acc = fma(__ldcs(At + (int64_t)r * T), xs[r], acc);
         }
         red[threadIdx.x] = acc;
         __syncthreads();

@@ -393,7 +393,8 @@ def cgnr_solve(apply, b, tol=1e-8, max_iter=500):
 # --------------------------------------------------------------------------
 # panel plan: the non-transposed product (the benchmarked hot path)
 
-_ITEM_ELEMS = 4096          # ~32 KB of matrix data per work item
+_ITEM_ELEMS = 8192          # ~64 KB of matrix data per work item
+_ITEM_MAX_ROWS = 1024       # PAN_MAX_ROWS in csrc/h2mv.cu
 
 
 class _Phase:
@@ -493,7 +494,7 @@ class PanelPlan:
         elems = int((K * T).sum())
         # chunk rows so every phase has >= ~4 items per SM when it can
         target = max(256, min(_ITEM_ELEMS, elems // (148 * 4) + 1))
-        rpi = np.maximum(1, -(-target // np.maximum(T, 1)))          # rows per item
+        rpi = np.minimum(_ITEM_MAX_ROWS, np.maximum(1, -(-target // np.maximum(T, 1))))  # rows/item
         nit = np.maximum(1, -(-K // rpi))
         xidx = np.concatenate(rows).astype(np.int32) if n else np.zeros(1, np.int32)
         xoff = _offsets_np(K)

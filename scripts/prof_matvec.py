@@ -1,59 +1,37 @@
-"""Per-phase matvec timing (events around every launch) + graph replay."""
-import os, sys, time
+"""Per-phase matvec timing for the panel plan (events around every phase
+launch, all on one stream) + graph replay."""
+import os, sys
 import numpy as np
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 import torch
-from paper_1810_08429_b200 import cli, geometry, h2, _native
-from paper_1810_08429_b200.device import ptr, stream_handle
+from paper_1810_08429_b200 import cli, geometry, h2
+from paper_1810_08429_b200.device import stream_handle
 L = int(sys.argv[1]) if len(sys.argv) > 1 else 6
 eps = float(sys.argv[2]) if len(sys.argv) > 2 else 1e-6
 mesh = geometry.build_sphere_mesh(L)
 hm, tree, bt = cli.build_h2_operator(mesh, cli.default_config(level=L, eps=eps))
 p = h2.plan(hm)
-n = mesh.nt
-x = torch.randn(n, dtype=torch.float64, device="cuda"); y = torch.empty_like(x)
+x = torch.randn(mesh.nt, dtype=torch.float64, device="cuda"); y = torch.empty_like(x)
 for _ in range(5): p.run(x, y)
 torch.cuda.synchronize()
-# per-launch timing
+phases = p.side_phases + p.main_phases + p.tail_phases
 acc = {}
-for rep in range(20):
+for rep in range(15):
     evs = []
-    st = stream_handle()
-    _native.call("gc_gather", ptr(x), ptr(p.perm_in), p.n_in, ptr(p.xt), st)
-    p.yhat.zero_()
-    for Lc in p.launches:
+    for i, P in enumerate(phases):
         a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-        a.record()
-        _native.call("gc_segmv", Lc.nseg, ptr(Lc.seg), ptr(Lc.blk), ptr(Lc.A0), ptr(Lc.A1), ptr(Lc.in0), ptr(Lc.in1), ptr(Lc.out), Lc.acc, Lc.maxT, st)
-        b.record(); evs.append((Lc, a, b))
+        a.record(); p._launch(P, stream_handle()); b.record(); evs.append((i, P, a, b))
     torch.cuda.synchronize()
     if rep >= 5:
-        for i, (Lc, a, b) in enumerate(evs):
-            acc.setdefault((i, Lc.name, Lc.nseg), []).append(a.elapsed_time(b))
+        for i, P, a, b in evs:
+            acc.setdefault(i, []).append(a.elapsed_time(b))
 tot = 0
-for k, v in acc.items():
-    print("%2d %-10s nseg %6d  %.1f us" % (k[0], k[1], k[2], 1e3 * np.median(v))); tot += np.median(v)
-print("sum of kernels %.1f us" % (1e3 * tot))
-rep = h2.storage_report(hm); print(rep)
-# eager end-to-end
-for mode in ("eager",):
-    torch.cuda.synchronize(); a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-    a.record()
-    for _ in range(50): p.run(x, y)
-    b.record(); torch.cuda.synchronize()
-    print(mode, "%.1f us/mvm" % (a.elapsed_time(b) / 50 * 1e3))
-# graph
-g = torch.cuda.CUDAGraph()
-s = torch.cuda.Stream()
-s.wait_stream(torch.cuda.current_stream())
-with torch.cuda.stream(s):
-    p.run(x, y)
-torch.cuda.current_stream().wait_stream(s)
-with torch.cuda.graph(g):
-    p.run(x, y)
-torch.cuda.synchronize()
+for i, P in enumerate(phases):
+    t = np.median(acc[i]); tot += t
+    print("%2d %-10s items %6d red %5d  %7.1f us  %6.1f MB  %6.0f GB/s" % (i, P.name, P.nitems, P.nred, 1e3 * t, P.bytes / 1e6, P.bytes / (t * 1e-3) / 1e9))
+print("sum of phases %.1f us" % (1e3 * tot))
 a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
 a.record()
-for _ in range(50): g.replay()
+for _ in range(50): p.run(x, y)
 b.record(); torch.cuda.synchronize()
-print("graph %.1f us/mvm" % (a.elapsed_time(b) / 50 * 1e3))
+print("graph %.1f us/mvm  -> %.0f GB/s" % (a.elapsed_time(b) / 50 * 1e3, (h2.storage_report(hm)["total"] + 16 * mesh.nt) / (a.elapsed_time(b) / 50 * 1e-3) / 1e9))

@@ -293,9 +293,20 @@ def run_native(args):
             e1.synchronize()
             times.append(e0.elapsed_time(e1) * 1e-3)
         t = float(np.median(times[1:]))
-        P = [0, 2 * 5 ** 4, 10 * 5 ** 4, 6 * 5 ** 4]
-        flops = counts[0] * (12 * 3 ** 4 + 24 * 3 ** 2 + 3) + sum(counts[k] * (33 * P[k] + 3) for k in (1, 2, 3))
-        q[name] = {"seconds": t, "gflop": flops / 1e9, "tflops": flops / t / 1e12, "tasks": counts}
+        # work actually executed (SURVEY §8d convention): disjoint entry
+        # 12 q^4 + 24 q^2 + 3; singular task per point of the xi-reduced
+        # rule: 2*3*NC (D from NC FMAs per component) + 9, times P_reduced
+        P = rules.npts
+        per_pt = [0, 2 * 3 * 4 + 9, 2 * 3 * 3 + 9, 2 * 3 * 2 + 9]
+        flops = counts[0] * (12 * 3 ** 4 + 24 * 3 ** 2 + 3) + sum(
+            counts[k] * (per_pt[k] * P[k] + 3) for k in (1, 2, 3))
+        # the reference's full rule (P = 2/10/6 q^4, 33 flops per point)
+        P_full = [0, 2 * 5 ** 4, 10 * 5 ** 4, 6 * 5 ** 4]
+        flops_ref = counts[0] * (12 * 3 ** 4 + 24 * 3 ** 2 + 3) + sum(
+            counts[k] * (33 * P_full[k] + 3) for k in (1, 2, 3))
+        q[name] = {"seconds": t, "gflop": flops / 1e9, "tflops": flops / t / 1e12, "tasks": counts,
+                   "reference_rule_gflop": flops_ref / 1e9,
+                   "reference_rule_equivalent_tflops": flops_ref / t / 1e12}
     assert np.array_equal(scratch_n.cpu().numpy(), d.near.cpu().numpy()), "near-field rerun not bitwise reproducible"
     peak64 = dfma_peak(torch, _native, ptr)
 

@@ -46,6 +46,7 @@ void gc_reset_launch_count(void);
  *   tri_vid [dev] (nt,3)    global vertex ids (pair classification)
  *   xq      [dev] (nt,mq,3) regular-rule surface points (gc_surface_points)
  *   wq      [dev] (mq,)     triangle_gauss(q_reg) weights
+ *   wq_host [host] (mq,)    the same weights (kernel-parameter copies)
  * ------------------------------------------------------------------- */
 typedef struct gc_geom {
     const double* corners;
@@ -55,11 +56,14 @@ typedef struct gc_geom {
     const double* wq;
     int64_t nt;
     int64_t mq;
+    const double* wq_host;
 } gc_geom;
 
-/* Singular pair rules (quadrature.sauter_rule, quadrature.py:211-284) as
- * SoA tables [dev] of 5*P doubles: x1[P] x2[P] y1[P] y2[P] w[P].  For the
- * identical case x1, x2 hold x1-y1, x2-y2 (the two charts coincide). */
+/* Singular pair rules (quadrature.sauter_rule, quadrature.py:211-284) in
+ * the xi-reduced form of quadrature.reduced_sauter_rule: SoA tables [dev]
+ * of (NC+1)*P doubles, NC coefficient columns then the weights, with
+ * D = sum_k coef_k G_k; NC = 4 (vertex: E1,E2,-F1,-F2), 3 (edge: E1,E2,-F2),
+ * 2 (identical: E1,E2).  npts[c] = P. */
 typedef struct gc_rules {
     const double* table[4]; /* index by case code; [0] unused */
     int64_t npts[4];
@@ -97,9 +101,10 @@ typedef struct gc_queue {
  * pairs triangle row_idx[row_off+a] with col_idx[col_off+b] and is stored
  * column-major at out[out_off + b*nr + a].  Disjoint pairs are integrated
  * here; singular pairs are appended to the queue and integrated by
- * gc_singular_flush.  flags [dev] int: bit 1 set on queue overflow. */
+ * gc_singular_flush.  max_rows / max_cols bound nr / nc over the batch
+ * (shared-memory staging).  flags [dev] int: bit 1 set on queue overflow. */
 int gc_assemble_blocks(const gc_geom* g, int64_t nb, const int64_t* desc,
-                       int64_t max_block_entries, const int64_t* row_idx,
+                       int64_t max_rows, int64_t max_cols, const int64_t* row_idx,
                        const int64_t* col_idx, double* out, gc_queue* q,
                        int32_t* flags, void* stream);
 

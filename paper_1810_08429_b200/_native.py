@@ -19,7 +19,7 @@ c_p = ctypes.c_void_p
 
 class GcGeom(ctypes.Structure):
     _fields_ = [("corners", c_p), ("gram", c_p), ("tri_vid", c_p), ("xq", c_p),
-                ("wq", c_p), ("nt", c_i64), ("mq", c_i64)]
+                ("wq", c_p), ("nt", c_i64), ("mq", c_i64), ("wq_host", c_p)]
 
 
 class GcRules(ctypes.Structure):
@@ -39,7 +39,7 @@ _SIGNATURES = {
     "gc_surface_points": [c_p, c_i64, c_p, c_i64, c_p, c_p],
     "gc_pair_eval": [ctypes.POINTER(GcGeom), ctypes.POINTER(GcRules), ctypes.c_int, c_i64,
                      c_p, c_p, c_p, c_p, c_p, c_p],
-    "gc_assemble_blocks": [ctypes.POINTER(GcGeom), c_i64, c_p, c_i64, c_p, c_p, c_p,
+    "gc_assemble_blocks": [ctypes.POINTER(GcGeom), c_i64, c_p, c_i64, c_i64, c_p, c_p, c_p,
                            ctypes.POINTER(GcQueue), c_p, c_p],
     "gc_singular_flush": [ctypes.POINTER(GcGeom), ctypes.POINTER(GcRules),
                           ctypes.POINTER(GcQueue), c_p, ctypes.POINTER(c_i64), c_p],

@@ -80,8 +80,8 @@ def device_block_assembly(dmesh, rules, queue, row_idx, col_idx, desc, out, stat
     d_desc = to_dev(desc.astype(np.int64), out.device)
     stream = stream_handle()
     with torch.cuda.device(out.device):
-        _native.call("gc_assemble_blocks", dmesh.geom, nb, ptr(d_desc), int(entries.max()),
-                     ptr(row_idx), ptr(col_idx), ptr(out), queue.struct, ptr(queue.flags),
+        _native.call("gc_assemble_blocks", dmesh.geom, nb, ptr(d_desc), int(desc[:, 1].max()),
+                     int(desc[:, 3].max()), ptr(row_idx), ptr(col_idx), ptr(out), queue.struct, ptr(queue.flags),
                      stream)
         counts = (_native.c_i64 * 4)()
         _native.call("gc_singular_flush", dmesh.geom, rules.struct, queue.struct, ptr(out),

@@ -80,13 +80,17 @@ __device__ __forceinline__ int classify_pair(const int64_t* tv, const int64_t* s
         *px = __ffs(rhit) - 1;
         *py = __ffs(chit) - 1;
     } else if (shared == 2) {
-        int missing = __ffs(~rhit & 7) - 1;
-        int rot = (missing + 1) % 3;
+        // rotation putting the shared edge in slots 0, 1 (register selects:
+        // no dynamically indexed local arrays)
+        const int missing = __ffs(~rhit & 7) - 1;
+        const int rot = (missing + 1) % 3;
         *px = rot;
-        int64_t g0 = tv[kPerms3[rot][0]], g1 = tv[kPerms3[rot][1]];
-        int c0 = (sv[0] == g0) ? 0 : (sv[1] == g0 ? 1 : 2);
-        int c1 = (sv[0] == g1) ? 0 : (sv[1] == g1 ? 1 : 2);
-        *py = kPermId[c0][c1];
+        const int64_t g0 = rot == 0 ? tv[0] : (rot == 1 ? tv[1] : tv[2]);
+        const int64_t g1 = rot == 0 ? tv[1] : (rot == 1 ? tv[2] : tv[0]);
+        const int c0 = (sv[0] == g0) ? 0 : (sv[1] == g0 ? 1 : 2);
+        const int c1 = (sv[0] == g1) ? 0 : (sv[1] == g1 ? 1 : 2);
+        // id of the permutation (c0, c1, 3-c0-c1): see kPermId
+        *py = c0 == 0 ? (c1 == 1 ? 0 : 3) : (c0 == 1 ? (c1 == 2 ? 1 : 5) : (c1 == 0 ? 2 : 4));
     }
     return shared;
 }

@@ -1,19 +1,25 @@
 // Batched Galerkin pair quadrature for the single-layer kernel 1/(4 pi r),
 // piecewise-constant basis, plane charts (assembly.py:159-216).
 //
-// Disjoint pairs (the regular q_reg^2 x q_reg^2 tensor rule) are one thread
-// per matrix entry: the q^2 row points stay in registers, the column points
-// are broadcast across the warp, and 1/r comes from a MUFU seed plus one
-// cubic-corrected Newton step (common.cuh rsqrt_fast).  Singular pairs
-// (Sauter-Schwab vertex / edge / identical rules) are queued by the block
-// kernel and integrated by a CTA-per-4-tasks kernel: 256 threads split the
-// rule points, every rule point loaded once serves 4 tasks, and a fixed
-// reduction tree makes each value independent of how tasks were grouped.
+// Disjoint pairs (the regular q_reg^2 x q_reg^2 tensor rule): one CTA per
+// block.  The block's row and column quadrature points are staged in shared
+// memory; each thread owns one row (its q^2 points in registers) and two
+// adjacent columns, so every shared-memory read of a column point feeds
+// q^2 independent distance evaluations.  1/r is a MUFU seed plus one
+// cubic-corrected Newton step (common.cuh rsqrt_fast).
+//
+// Singular pairs (Sauter-Schwab vertex / edge / identical) are queued by the
+// block kernel and integrated by persistent warps: the rule (xi-reduced, see
+// quadrature.reduced_sauter_rule) sits in shared memory, each warp takes 2
+// tasks at a time, lane l evaluates rule points l, l+32, ... and a fixed
+// butterfly sums the lanes - every value is independent of how tasks were
+// grouped or scheduled, so assembly is bitwise reproducible.
 #include "common.cuh"
 
 namespace gcb {
 
-// sum_i sum_j w_i w_j / |X_i - Y_j| with X in registers (M compile-time)
+// sum_i sum_j w_i w_j / |X_i - Y_j| reading both point sets from global
+// (evaluator seam, one thread per task)
 template <int M>
 __device__ __forceinline__ double disjoint_sum(const double* __restrict__ xq_t,
                                                const double* __restrict__ xq_s,
@@ -25,9 +31,6 @@ __device__ __forceinline__ double disjoint_sum(const double* __restrict__ xq_t,
         X[i][1] = __ldg(xq_t + 3 * i + 1);
         X[i][2] = __ldg(xq_t + 3 * i + 2);
     }
-    double wi[M];
-#pragma unroll
-    for (int i = 0; i < M; ++i) wi[i] = __ldg(wq + i);
     double total = 0.0;
 #pragma unroll 1
     for (int j = 0; j < M; ++j) {
@@ -38,14 +41,13 @@ __device__ __forceinline__ double disjoint_sum(const double* __restrict__ xq_t,
         for (int i = 0; i < M; ++i) {
             double d0 = X[i][0] - y0, d1 = X[i][1] - y1, d2 = X[i][2] - y2;
             double r2 = fma(d2, d2, fma(d1, d1, d0 * d0));
-            acc = fma(wi[i], rsqrt_fast(r2), acc);
+            acc = fma(__ldg(wq + i), rsqrt_fast(r2), acc);
         }
-        total = fma(wi[j], acc, total);
+        total = fma(__ldg(wq + j), acc, total);
     }
     return total;
 }
 
-// generic (any mq) variant reading both point sets from L1
 __device__ double disjoint_sum_any(const double* __restrict__ xq_t,
                                    const double* __restrict__ xq_s,
                                    const double* __restrict__ wq, int mq) {
@@ -72,10 +74,10 @@ __device__ __forceinline__ double disjoint_entry(const gc_geom& g, int64_t t, in
         sum = disjoint_sum<(M > 0 ? M : 1)>(g.xq + t * 3 * M, g.xq + s * 3 * M, g.wq);
     else
         sum = disjoint_sum_any(g.xq + t * 3 * g.mq, g.xq + s * 3 * g.mq, g.wq, (int)g.mq);
-    return (__ldg(g.gram + t) * __ldg(g.gram + s) * INV_FOUR_PI) * sum;
+    return ((__ldg(g.gram + t) * INV_FOUR_PI) * __ldg(g.gram + s)) * sum;  // same association as k_assemble_blocks
 }
 
-__device__ __forceinline__ void push_task(gc_queue q, int kase, int64_t t, int64_t s, int px,
+__device__ __forceinline__ void push_task(const gc_queue& q, int kase, int64_t t, int64_t s, int px,
                                           int py, int64_t out_idx, int32_t* flags) {
     int slot = atomicAdd(q.count + kase, 1);
     if (slot >= q.cap[kase]) {
@@ -89,21 +91,122 @@ __device__ __forceinline__ void push_task(gc_queue q, int kase, int64_t t, int64
     dst[3] = out_idx;
 }
 
-// one CTA per block, one thread per entry, column-major output
-template <int M>
-__global__ void __launch_bounds__(256) k_assemble_blocks(gc_geom g, const int64_t* __restrict__ desc,
-                                                         const int64_t* __restrict__ row_idx,
-                                                         const int64_t* __restrict__ col_idx,
-                                                         double* __restrict__ out, gc_queue q,
-                                                         int32_t* flags) {
+constexpr int BLK_THREADS = 256;
+
+struct RuleW;
+static void e_copy_weights(const gc_geom& g, RuleW& rw, int M);
+
+// quadrature weights as a kernel parameter: they live in the constant bank
+// and feed the DFMAs directly instead of occupying 2*M registers
+struct RuleW {
+    double w[16];
+};
+
+// One CTA per block; column-major output.  Shared memory: row points
+// (nr*M*3), column points (nc*M*3) and both vertex-id lists; the caller
+// sizes the dynamic allocation for the largest block.  NT = 128 for the
+// 16x16 near-field blocks (one thread per column pair), 256 otherwise.
+template <int M, int NT>
+__global__ void __launch_bounds__(NT) k_assemble_blocks(
+    gc_geom g, RuleW rw, const int64_t* __restrict__ desc, const int64_t* __restrict__ row_idx,
+    const int64_t* __restrict__ col_idx, double* __restrict__ out, gc_queue q, int32_t* flags) {
+    extern __shared__ double sm[];
     const int64_t* d = desc + 5 * (int64_t)blockIdx.x;
     const int64_t row_off = d[0], col_off = d[2], out_off = d[4];
     const int nr = (int)d[1], nc = (int)d[3];
-    const int total = nr * nc;
-    for (int e = threadIdx.x; e < total; e += blockDim.x) {
-        int a = e % nr, b = e / nr;
-        int64_t t = __ldg(row_idx + row_off + a);
-        int64_t s = __ldg(col_idx + col_off + b);
+    double* Xs = sm;                                   // nr * M * 3
+    double* Ys = Xs + nr * M * 3;                      // nc * M * 3
+    int64_t* tvs = (int64_t*)(Ys + nc * M * 3);        // nr * 4: id, v0, v1, v2
+    int64_t* svs = tvs + 4 * nr;                       // nc * 4
+    for (int e = threadIdx.x; e < nr; e += NT) {
+        const int64_t t = __ldg(row_idx + row_off + e);
+        tvs[4 * e] = t;
+#pragma unroll
+        for (int k = 0; k < 3; ++k) tvs[4 * e + 1 + k] = __ldg(g.tri_vid + 3 * t + k);
+    }
+    for (int e = threadIdx.x; e < nc; e += NT) {
+        const int64_t s = __ldg(col_idx + col_off + e);
+        svs[4 * e] = s;
+#pragma unroll
+        for (int k = 0; k < 3; ++k) svs[4 * e + 1 + k] = __ldg(g.tri_vid + 3 * s + k);
+    }
+    __syncthreads();
+    for (int e = threadIdx.x; e < nr * M * 3; e += NT) {
+        const int a = e / (M * 3);
+        Xs[e] = __ldg(g.xq + tvs[4 * a] * (M * 3) + (e - a * M * 3));
+    }
+    for (int e = threadIdx.x; e < nc * M * 3; e += NT) {
+        const int b = e / (M * 3);
+        Ys[e] = __ldg(g.xq + svs[4 * b] * (M * 3) + (e - b * M * 3));
+    }
+    __syncthreads();
+    const int npairs = (nc + 1) / 2;
+    for (int e = threadIdx.x; e < nr * npairs; e += NT) {
+        const int a = e % nr, b0 = 2 * (e / nr);
+        const bool two = b0 + 1 < nc;
+        const int64_t t = tvs[4 * a];
+        const int64_t tv[3] = {tvs[4 * a + 1], tvs[4 * a + 2], tvs[4 * a + 3]};
+        bool live[2];
+#pragma unroll
+        for (int c = 0; c < 2; ++c) {
+            live[c] = false;
+            if (c == 1 && !two) continue;
+            const int b = b0 + c;
+            const int64_t sv[3] = {svs[4 * b + 1], svs[4 * b + 2], svs[4 * b + 3]};
+            int px, py;
+            const int kase = classify_pair(tv, sv, &px, &py);
+            if (kase == 0)
+                live[c] = true;
+            else
+                push_task(q, kase, t, svs[4 * b], px, py, out_off + (int64_t)b * nr + a, flags);
+        }
+        if (!live[0] && !live[1]) continue;
+        double X[M][3];
+#pragma unroll
+        for (int i = 0; i < M; ++i)
+#pragma unroll
+            for (int k = 0; k < 3; ++k) X[i][k] = Xs[(a * M + i) * 3 + k];
+        const double* Y0 = Ys + b0 * M * 3;
+        const double* Y1 = Ys + (two ? b0 + 1 : b0) * M * 3;
+        double tot0 = 0.0, tot1 = 0.0;
+#pragma unroll 1
+        for (int j = 0; j < M; ++j) {
+            const double u0 = Y0[3 * j], u1 = Y0[3 * j + 1], u2 = Y0[3 * j + 2];
+            const double v0 = Y1[3 * j], v1 = Y1[3 * j + 1], v2 = Y1[3 * j + 2];
+            double acc0 = 0.0, acc1 = 0.0;
+#pragma unroll
+            for (int i = 0; i < M; ++i) {
+                const double d0 = X[i][0] - u0, d1 = X[i][1] - u1, d2 = X[i][2] - u2;
+                const double e0 = X[i][0] - v0, e1 = X[i][1] - v1, e2 = X[i][2] - v2;
+                const double r2a = fma(d2, d2, fma(d1, d1, d0 * d0));
+                const double r2b = fma(e2, e2, fma(e1, e1, e0 * e0));
+                acc0 = fma(rw.w[i], rsqrt_fast(r2a), acc0);
+                acc1 = fma(rw.w[i], rsqrt_fast(r2b), acc1);
+            }
+            tot0 = fma(rw.w[j], acc0, tot0);
+            tot1 = fma(rw.w[j], acc1, tot1);
+        }
+        const double gt = __ldg(g.gram + t) * INV_FOUR_PI;
+        if (live[0]) out[out_off + (int64_t)b0 * nr + a] = (gt * __ldg(g.gram + svs[4 * b0])) * tot0;
+        if (live[1])
+            out[out_off + (int64_t)(b0 + 1) * nr + a] = (gt * __ldg(g.gram + svs[4 * (b0 + 1)])) * tot1;
+    }
+}
+
+static void e_copy_weights(const gc_geom& g, RuleW& rw, int M) {
+    for (int i = 0; i < 16; ++i) rw.w[i] = (i < M && g.wq_host) ? g.wq_host[i] : 0.0;
+}
+
+// generic-order fallback (any q_reg): one thread per entry, points from L1
+__global__ void __launch_bounds__(BLK_THREADS) k_assemble_blocks_any(
+    gc_geom g, const int64_t* __restrict__ desc, const int64_t* __restrict__ row_idx,
+    const int64_t* __restrict__ col_idx, double* __restrict__ out, gc_queue q, int32_t* flags) {
+    const int64_t* d = desc + 5 * (int64_t)blockIdx.x;
+    const int64_t row_off = d[0], col_off = d[2], out_off = d[4];
+    const int nr = (int)d[1], nc = (int)d[3];
+    for (int e = threadIdx.x; e < nr * nc; e += blockDim.x) {
+        const int a = e % nr, b = e / nr;
+        const int64_t t = __ldg(row_idx + row_off + a), s = __ldg(col_idx + col_off + b);
         int64_t tv[3], sv[3];
 #pragma unroll
         for (int k = 0; k < 3; ++k) {
@@ -111,9 +214,9 @@ __global__ void __launch_bounds__(256) k_assemble_blocks(gc_geom g, const int64_
             sv[k] = __ldg(g.tri_vid + 3 * s + k);
         }
         int px, py;
-        int kase = classify_pair(tv, sv, &px, &py);
+        const int kase = classify_pair(tv, sv, &px, &py);
         if (kase == 0)
-            out[out_off + e] = disjoint_entry<M>(g, t, s);
+            out[out_off + e] = disjoint_entry<0>(g, t, s);
         else
             push_task(q, kase, t, s, px, py, out_off + e, flags);
     }
@@ -140,91 +243,115 @@ __global__ void k_pack_tasks(int64_t B, const int64_t* rows, const int64_t* cols
     }
 }
 
-constexpr int SING_THREADS = 256;
-constexpr int SING_G = 4;  // tasks per CTA
+constexpr int SING_THREADS = 128;
+constexpr int SING_WARPS = SING_THREADS / 32;
+constexpr int SING_G = 2;   // tasks per warp
 
-// Singular pairs.  Vertex/edge: D = x1 E1 + x2 E2 - y1 F1 - y2 F2 with
-// E_k = P_k - P_0 (row chart after its alignment permutation), F likewise
-// for the column chart; P_0 == Q_0 is the shared vertex, so the difference
-// is formed without cancellation.  Identical: D = dx E1 + dy E2.
-template <int KASE>
+// Singular pairs with the xi-reduced rule: D = sum_k coef[k] G_k,
+//   NC = 4 (vertex):    G = (E1, E2, -F1, -F2)
+//   NC = 3 (edge):      G = (E1, E2, -F2)          (E1 == F1)
+//   NC = 2 (identical): G = (E1, E2)               (E == F)
+// with E_k = P_k - P_0, F_k = Q_k - Q_0 after the alignment permutations;
+// P_0 == Q_0 is the shared vertex, so D carries no cancellation.  The rule
+// table (NC coefficient columns + weight, SoA, P points) is staged in
+// shared memory when it fits, else read through L1.
+template <int NC, bool SMEM>
 __global__ void __launch_bounds__(SING_THREADS) k_singular(gc_geom g, const double* __restrict__ rule,
-                                                           int64_t P, const int64_t* __restrict__ tasks,
+                                                           int P, const int64_t* __restrict__ tasks,
                                                            int64_t ntasks, double* __restrict__ out) {
-    const int64_t first = (int64_t)blockIdx.x * SING_G;
-    double E1[SING_G][3], E2[SING_G][3], F1[SING_G][3], F2[SING_G][3];
-    double scale[SING_G];
-    int64_t oidx[SING_G];
-#pragma unroll
-    for (int k = 0; k < SING_G; ++k) {
-        int64_t id = first + k;
-        bool live = id < ntasks;
-        const int64_t* tk = tasks + 4 * (live ? id : first);
-        int64_t t = tk[0], s = tk[1], pp = tk[2];
-        oidx[k] = live ? tk[3] : -1;
-        int px = (int)(pp & 0xff), py = (int)((pp >> 8) & 0xff);
-        const double* ct = g.corners + 9 * t;
-        const double* cs = g.corners + 9 * s;
-        int p0 = kPerms3[px][0], p1 = kPerms3[px][1], p2 = kPerms3[px][2];
-        int q0 = kPerms3[py][0], q1 = kPerms3[py][1], q2 = kPerms3[py][2];
-#pragma unroll
-        for (int c = 0; c < 3; ++c) {
-            E1[k][c] = ct[3 * p1 + c] - ct[3 * p0 + c];
-            E2[k][c] = ct[3 * p2 + c] - ct[3 * p0 + c];
-            F1[k][c] = cs[3 * q1 + c] - cs[3 * q0 + c];
-            F2[k][c] = cs[3 * q2 + c] - cs[3 * q0 + c];
-        }
-        scale[k] = g.gram[t] * g.gram[s] * INV_FOUR_PI;
+    extern __shared__ double sr[];
+    const double* R = rule;
+    if (SMEM) {
+        for (int i = threadIdx.x; i < (NC + 1) * P; i += SING_THREADS) sr[i] = rule[i];
+        __syncthreads();
+        R = sr;
     }
-    double acc[SING_G];
+    const int lane = threadIdx.x & 31;
+    const int64_t nwarps = (int64_t)gridDim.x * SING_WARPS;
+    const int64_t ngroups = (ntasks + SING_G - 1) / SING_G;
+    for (int64_t grp = (int64_t)blockIdx.x * SING_WARPS + (threadIdx.x >> 5); grp < ngroups;
+         grp += nwarps) {
+        double G[SING_G][NC][3];
+        double scale[SING_G];
+        int64_t oidx[SING_G];
 #pragma unroll
-    for (int k = 0; k < SING_G; ++k) acc[k] = 0.0;
-    const double* rx1 = rule;
-    const double* rx2 = rule + P;
-    const double* ry1 = rule + 2 * P;
-    const double* ry2 = rule + 3 * P;
-    const double* rw = rule + 4 * P;
-    for (int64_t p = threadIdx.x; p < P; p += SING_THREADS) {
-        const double x1 = __ldg(rx1 + p), x2 = __ldg(rx2 + p), w = __ldg(rw + p);
-        if (KASE == 3) {
+        for (int k = 0; k < SING_G; ++k) {
+            const int64_t id = grp * SING_G + k;
+            const bool live = id < ntasks;
+            const int64_t* tk = tasks + 4 * (live ? id : grp * SING_G);
+            const int64_t t = tk[0], s = tk[1], pp = tk[2];
+            oidx[k] = live ? tk[3] : -1;
+            const int px = (int)(pp & 0xff), py = (int)((pp >> 8) & 0xff);
+            const double* ct = g.corners + 9 * t;
+            const double* cs = g.corners + 9 * s;
+            const int p0 = kPerms3[px][0], p1 = kPerms3[px][1], p2 = kPerms3[px][2];
+            const int q0 = kPerms3[py][0], q1 = kPerms3[py][1], q2 = kPerms3[py][2];
+#pragma unroll
+            for (int c = 0; c < 3; ++c) {
+                G[k][0][c] = ct[3 * p1 + c] - ct[3 * p0 + c];
+                G[k][1][c] = ct[3 * p2 + c] - ct[3 * p0 + c];
+                if (NC == 4) {
+                    G[k][2 % NC][c] = -(cs[3 * q1 + c] - cs[3 * q0 + c]);
+                    G[k][3 % NC][c] = -(cs[3 * q2 + c] - cs[3 * q0 + c]);
+                } else if (NC == 3) {
+                    G[k][2 % NC][c] = -(cs[3 * q2 + c] - cs[3 * q0 + c]);
+                }
+            }
+            scale[k] = g.gram[t] * g.gram[s] * INV_FOUR_PI;
+        }
+        double acc[SING_G];
+#pragma unroll
+        for (int k = 0; k < SING_G; ++k) acc[k] = 0.0;
+        for (int p = lane; p < P; p += 32) {
+            double cf[NC];
+#pragma unroll
+            for (int j = 0; j < NC; ++j) cf[j] = R[j * P + p];
+            const double w = R[NC * P + p];
 #pragma unroll
             for (int k = 0; k < SING_G; ++k) {
-                double d0 = fma(x1, E1[k][0], x2 * E2[k][0]);
-                double d1 = fma(x1, E1[k][1], x2 * E2[k][1]);
-                double d2 = fma(x1, E1[k][2], x2 * E2[k][2]);
-                double r2 = fma(d2, d2, fma(d1, d1, d0 * d0));
-                acc[k] = fma(w, rsqrt_fast(r2), acc[k]);
-            }
-        } else {
-            const double y1 = __ldg(ry1 + p), y2 = __ldg(ry2 + p);
+                double dd[3];
 #pragma unroll
-            for (int k = 0; k < SING_G; ++k) {
-                double d[3];
+                for (int c = 0; c < 3; ++c) {
+                    double v = cf[0] * G[k][0][c];
 #pragma unroll
-                for (int c = 0; c < 3; ++c)
-                    d[c] = fma(x1, E1[k][c], fma(x2, E2[k][c], -fma(y1, F1[k][c], y2 * F2[k][c])));
-                double r2 = fma(d[2], d[2], fma(d[1], d[1], d[0] * d[0]));
+                    for (int j = 1; j < NC; ++j) v = fma(cf[j], G[k][j][c], v);
+                    dd[c] = v;
+                }
+                const double r2 = fma(dd[2], dd[2], fma(dd[1], dd[1], dd[0] * dd[0]));
                 acc[k] = fma(w, rsqrt_fast(r2), acc[k]);
             }
         }
-    }
-    // fixed-order reduction: warp butterfly, then warp partials in order
-    __shared__ double part[SING_THREADS / 32][SING_G];
-    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
 #pragma unroll
-    for (int k = 0; k < SING_G; ++k) {
-        double v = acc[k];
+        for (int k = 0; k < SING_G; ++k) {
+            double v = acc[k];
 #pragma unroll
-        for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
-        if (lane == 0) part[warp][k] = v;
+            for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+            if (lane == 0 && oidx[k] >= 0) out[oidx[k]] = scale[k] * v;
+        }
     }
-    __syncthreads();
-    if (threadIdx.x < SING_G) {
-        const int k = threadIdx.x;
-        double v = 0.0;
-        for (int w = 0; w < SING_THREADS / 32; ++w) v += part[w][k];
-        if (oidx[k] >= 0) out[oidx[k]] = scale[k] * v;
+}
+
+template <int NC>
+static int launch_singular_nc(const gc_geom& g, const double* table, int64_t P, const int64_t* tasks,
+                              int64_t n, double* out, cudaStream_t st) {
+    const size_t bytes = (size_t)(NC + 1) * P * sizeof(double);
+    const int64_t groups = (n + SING_G - 1) / SING_G;
+    int64_t grid = (groups + SING_WARPS - 1) / SING_WARPS;
+    if (bytes <= 200 * 1024) {
+        cudaError_t e = cudaFuncSetAttribute(k_singular<NC, true>,
+                                             cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes);
+        if (e != cudaSuccess) return cuda_status(e, "k_singular smem attribute");
+        int per_sm = 1;
+        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_singular<NC, true>, SING_THREADS, bytes);
+        if (per_sm < 1) per_sm = 1;
+        if (grid > 148LL * per_sm) grid = 148LL * per_sm;
+        k_singular<NC, true><<<(unsigned)grid, SING_THREADS, bytes, st>>>(g, table, (int)P, tasks, n, out);
+    } else {
+        if (grid > 148LL * 8) grid = 148LL * 8;
+        k_singular<NC, false><<<(unsigned)grid, SING_THREADS, 0, st>>>(g, table, (int)P, tasks, n, out);
     }
+    GC_CHECK_LAUNCH("k_singular");
+    return GC_OK;
 }
 
 static int launch_singular(const gc_geom& g, const gc_rules& r, int kase, const int64_t* tasks,
@@ -234,26 +361,42 @@ static int launch_singular(const gc_geom& g, const gc_rules& r, int kase, const 
         set_error(GC_ERR_CONFIG, "singular rule for case %d not uploaded", kase);
         return GC_ERR_CONFIG;
     }
-    int64_t grid = (n + SING_G - 1) / SING_G;
-    if (grid > 0x7fffffffLL) {
-        set_error(GC_ERR_CONFIG, "too many singular tasks");
-        return GC_ERR_CONFIG;
-    }
     switch (kase) {
-        case 1: k_singular<1><<<(unsigned)grid, SING_THREADS, 0, st>>>(g, r.table[1], r.npts[1], tasks, n, out); break;
-        case 2: k_singular<2><<<(unsigned)grid, SING_THREADS, 0, st>>>(g, r.table[2], r.npts[2], tasks, n, out); break;
-        case 3: k_singular<3><<<(unsigned)grid, SING_THREADS, 0, st>>>(g, r.table[3], r.npts[3], tasks, n, out); break;
+        case 1: return launch_singular_nc<4>(g, r.table[1], r.npts[1], tasks, n, out, st);
+        case 2: return launch_singular_nc<3>(g, r.table[2], r.npts[2], tasks, n, out, st);
+        case 3: return launch_singular_nc<2>(g, r.table[3], r.npts[3], tasks, n, out, st);
         default: set_error(GC_ERR_CONFIG, "bad singular case %d", kase); return GC_ERR_CONFIG;
     }
-    GC_CHECK_LAUNCH("k_singular");
+}
+
+template <int M, int NT>
+static int launch_blocks_nt(const gc_geom& g, const RuleW& rw, int64_t nb, const int64_t* desc,
+                            size_t bytes, const int64_t* ri, const int64_t* ci, double* out,
+                            const gc_queue& q, int32_t* flags, cudaStream_t st) {
+    cudaError_t e = cudaFuncSetAttribute(k_assemble_blocks<M, NT>,
+                                         cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes);
+    if (e != cudaSuccess) return cuda_status(e, "k_assemble_blocks smem attribute");
+    k_assemble_blocks<M, NT><<<(unsigned)nb, NT, bytes, st>>>(g, rw, desc, ri, ci, out, q, flags);
+    GC_CHECK_LAUNCH("k_assemble_blocks");
     return GC_OK;
 }
 
 template <int M>
-static void launch_blocks(const gc_geom& g, int64_t nb, const int64_t* desc, int threads,
-                          const int64_t* ri, const int64_t* ci, double* out, gc_queue q,
-                          int32_t* flags, cudaStream_t st) {
-    k_assemble_blocks<M><<<(unsigned)nb, threads, 0, st>>>(g, desc, ri, ci, out, q, flags);
+static int launch_blocks(const gc_geom& g, int64_t nb, const int64_t* desc, int64_t max_rows,
+                         int64_t max_cols, const int64_t* ri, const int64_t* ci, double* out,
+                         gc_queue q, int32_t* flags, cudaStream_t st) {
+    const size_t bytes = (size_t)(max_rows + max_cols) * (M * 3 * sizeof(double) + 4 * sizeof(int64_t));
+    if (bytes > 200 * 1024) {
+        k_assemble_blocks_any<<<(unsigned)nb, BLK_THREADS, 0, st>>>(g, desc, ri, ci, out, q, flags);
+        GC_CHECK_LAUNCH("k_assemble_blocks_any");
+        return GC_OK;
+    }
+    if (!g.wq_host) { set_error(GC_ERR_CONFIG, "gc_geom.wq_host is required"); return GC_ERR_CONFIG; }
+    RuleW rw;
+    e_copy_weights(g, rw, M);
+    if (max_rows * ((max_cols + 1) / 2) <= 128)
+        return launch_blocks_nt<M, 128>(g, rw, nb, desc, bytes, ri, ci, out, q, flags, st);
+    return launch_blocks_nt<M, 256>(g, rw, nb, desc, bytes, ri, ci, out, q, flags, st);
 }
 
 }  // namespace gcb
@@ -276,8 +419,6 @@ int gc_pair_eval(const gc_geom* gp, const gc_rules* rp, int kase, int64_t B, con
             k_pair_disjoint<9><<<(unsigned)grid, 128, 0, st>>>(g, B, rows, cols, out);
         else if (g.mq == 4)
             k_pair_disjoint<4><<<(unsigned)grid, 128, 0, st>>>(g, B, rows, cols, out);
-        else if (g.mq == 16)
-            k_pair_disjoint<16><<<(unsigned)grid, 128, 0, st>>>(g, B, rows, cols, out);
         else
             k_pair_disjoint<0><<<(unsigned)grid, 128, 0, st>>>(g, B, rows, cols, out);
         GC_CHECK_LAUNCH("k_pair_disjoint");
@@ -296,23 +437,23 @@ int gc_pair_eval(const gc_geom* gp, const gc_rules* rp, int kase, int64_t B, con
     return rc;
 }
 
-int gc_assemble_blocks(const gc_geom* gp, int64_t nb, const int64_t* desc,
-                       int64_t max_block_entries, const int64_t* row_idx, const int64_t* col_idx,
+int gc_assemble_blocks(const gc_geom* gp, int64_t nb, const int64_t* desc, int64_t max_rows,
+                       int64_t max_cols, const int64_t* row_idx, const int64_t* col_idx,
                        double* out, gc_queue* qp, int32_t* flags, void* stream) {
     if (!gp || !qp) { set_error(GC_ERR_CONFIG, "null geometry/queue"); return GC_ERR_CONFIG; }
     if (nb <= 0) return GC_OK;
     if (nb > 0x7fffffffLL) { set_error(GC_ERR_CONFIG, "too many blocks"); return GC_ERR_CONFIG; }
-    int threads = max_block_entries >= 256 ? 256 : (max_block_entries > 32 ? (int)((max_block_entries + 31) / 32 * 32) : 32);
     cudaStream_t st = (cudaStream_t)stream;
     const gc_geom g = *gp;
     switch (g.mq) {
-        case 9: launch_blocks<9>(g, nb, desc, threads, row_idx, col_idx, out, *qp, flags, st); break;
-        case 4: launch_blocks<4>(g, nb, desc, threads, row_idx, col_idx, out, *qp, flags, st); break;
-        case 16: launch_blocks<16>(g, nb, desc, threads, row_idx, col_idx, out, *qp, flags, st); break;
-        default: launch_blocks<0>(g, nb, desc, threads, row_idx, col_idx, out, *qp, flags, st); break;
+        case 9: return launch_blocks<9>(g, nb, desc, max_rows, max_cols, row_idx, col_idx, out, *qp, flags, st);
+        case 4: return launch_blocks<4>(g, nb, desc, max_rows, max_cols, row_idx, col_idx, out, *qp, flags, st);
+        case 16: return launch_blocks<16>(g, nb, desc, max_rows, max_cols, row_idx, col_idx, out, *qp, flags, st);
+        default:
+            k_assemble_blocks_any<<<(unsigned)nb, BLK_THREADS, 0, st>>>(g, desc, row_idx, col_idx, out, *qp, flags);
+            GC_CHECK_LAUNCH("k_assemble_blocks_any");
+            return GC_OK;
     }
-    GC_CHECK_LAUNCH("k_assemble_blocks");
-    return GC_OK;
 }
 
 int gc_singular_flush(const gc_geom* gp, const gc_rules* rp, gc_queue* qp, double* out,

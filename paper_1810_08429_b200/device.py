@@ -13,7 +13,7 @@ import numpy as np
 from . import _native
 from .errors import ConfigError, DeviceError
 from .geometry import chart_pack, shape_functions
-from .quadrature import sauter_rule, triangle_gauss
+from .quadrature import reduced_sauter_rule, triangle_gauss
 
 try:  # torch is plumbing only; importing the package must not need a GPU
     import torch
@@ -81,8 +81,10 @@ class DeviceMesh:
         with torch.cuda.device(device):
             _native.call("gc_surface_points", ptr(self.corners), self.nt, ptr(n6), self.mq,
                          ptr(self.xq), stream_handle())
+        self.wq_host = np.ascontiguousarray(wts, dtype=np.float64)
         self.geom = _native.GcGeom(ptr(self.corners), ptr(self.gram), ptr(self.tri_vid),
-                                   ptr(self.xq), ptr(self.wq), self.nt, self.mq)
+                                   ptr(self.xq), ptr(self.wq), self.nt, self.mq,
+                                   self.wq_host.ctypes.data)
 
     @classmethod
     def get(cls, mesh, q_reg, device):
@@ -94,24 +96,22 @@ class DeviceMesh:
 
 
 class DeviceRules:
-    """Sauter-Schwab vertex / edge / identical tables of order ``q_sing`` as
-    SoA (x1, x2, y1, y2, w); identical stores x-y in the x slots."""
+    """Sauter-Schwab vertex / edge / identical rules of order ``q_sing`` in
+    the xi-reduced coefficient form (quadrature.reduced_sauter_rule): SoA
+    (NC coefficient columns, then weights) per case."""
 
     def __init__(self, q_sing, device):
         self.q_sing = q_sing
         self.tables = [None] * 4
+        self.npts = [0] * 4
         self.struct = _native.GcRules()
         for case in (1, 2, 3):
-            rule = sauter_rule(case, q_sing)
-            x, y, w = rule.x, rule.y, rule.w
-            if case == 3:
-                cols = [x[:, 0] - y[:, 0], x[:, 1] - y[:, 1], y[:, 0], y[:, 1], w]
-            else:
-                cols = [x[:, 0], x[:, 1], y[:, 0], y[:, 1], w]
-            t = to_dev(np.concatenate(cols), device)
+            rule = reduced_sauter_rule(case, q_sing)
+            t = to_dev(np.concatenate([rule.coef.T.ravel(), rule.w]), device)
             self.tables[case] = t
+            self.npts[case] = len(rule.w)
             self.struct.table[case] = t.data_ptr()
-            self.struct.npts[case] = len(w)
+            self.struct.npts[case] = len(rule.w)
 
     @classmethod
     def get(cls, q_sing, device):

@@ -222,3 +222,54 @@ def sauter_rule(kind, q):
         x, y = np.concatenate([x, flip(y)]), np.concatenate([y, flip(x)])
         w = np.concatenate([0.5 * w, 0.5 * w])
     return PairRule(x, y, w)
+
+
+ReducedRule = namedtuple("ReducedRule", "coef w ncoef")
+
+
+@lru_cache(maxsize=None)
+def reduced_sauter_rule(kind, q):
+    """The Sauter-Schwab rule of ``sauter_rule(kind, q)`` with the xi
+    (radial) sum done exactly.
+
+    In every subdomain all four relative coordinates carry the factor xi and
+    the Jacobian carries xi^3 (quadrature.py:246-271), so the pair distance
+    is xi * rhat(eta) and the 1/(4 pi r) integrand times the Jacobian is
+    xi^2 * j(eta) / (4 pi rhat(eta)).  The xi sum therefore factors out as
+    S2 = sum_xi w_xi xi^2 (= 1/3 for q >= 2) and the rule keeps q^3 points
+    per subdomain (2/10/6 q^3) - the same quadrature sum, 5x fewer kernel
+    evaluations at q = 5.
+
+    Points are returned as coefficients of the aligned chart edge vectors,
+    ``D = x - y = sum_k coef[k] * G_k`` with
+      vertex:    G = (E1, E2, -F1, -F2)        (4 coefficients)
+      edge:      G = (E1, E2, -F2), E1 == F1   (3)
+      identical: G = (E1, E2), E == F          (2)
+    where E_k = P_k - P_0 and F_k = Q_k - Q_0 after the alignment
+    permutations (P_0 = Q_0 is a shared vertex).
+    """
+    code = KIND_CODES[kind] if isinstance(kind, str) else int(kind)
+    if code not in (VERTEX, EDGE, IDENTICAL):
+        raise ValueError("reduced rules exist for the singular cases only")
+    g, w = _gauss01(q)
+    s2 = float(np.sum(w * g * g))
+    e1, e2, e3 = (a.ravel() for a in np.meshgrid(g, g, g, indexing="ij"))
+    w3 = np.einsum("i,j,k->ijk", w, w, w).ravel()
+    one = np.ones_like(e1)
+    builder = {IDENTICAL: _identical_parts, VERTEX: _vertex_parts, EDGE: _edge_parts}[code]
+    parts = builder(one, e1, e2, e3)
+    x = np.concatenate([np.column_stack([a - b, b]) for a, b, _, _, _ in parts])
+    y = np.concatenate([np.column_stack([c - d, d]) for _, _, c, d, _ in parts])
+    wt = np.concatenate([w3 * j * s2 for *_, j in parts])
+    if code == VERTEX:
+        coef = np.column_stack([x[:, 0], x[:, 1], y[:, 0], y[:, 1]])
+    elif code == IDENTICAL:
+        coef = np.column_stack([x[:, 0] - y[:, 0], x[:, 1] - y[:, 1]])
+    else:
+        # D = x1 E1 + x2 E2 - y1 F1 - y2 F2 with F1 = E1; the mirrored half
+        # (x, y) -> (S y, S x) gives (x1+x2-y1-y2) E1 + y2 E2 - x2 F2
+        direct = np.column_stack([x[:, 0] - y[:, 0], x[:, 1], y[:, 1]])
+        mirror = np.column_stack([x[:, 0] + x[:, 1] - y[:, 0] - y[:, 1], y[:, 1], x[:, 1]])
+        coef = np.concatenate([direct, mirror])
+        wt = np.concatenate([0.5 * wt, 0.5 * wt])
+    return ReducedRule(np.ascontiguousarray(coef), wt, coef.shape[1])

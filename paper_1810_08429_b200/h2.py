@@ -193,6 +193,9 @@ class MatvecPlan:
         return len(self.launches) + 2
 
 
+PERSISTENT = False      # PersistentPlan (one cooperative launch) is experimental
+
+
 def plan(h, trans=False, graph=True):
     """Cached product plan: PanelPlan (CUDA graph) for H x, MatvecPlan
     (segmented kernel over the same storage) for H^T x."""
@@ -201,7 +204,7 @@ def plan(h, trans=False, graph=True):
         if trans:
             h.dev.plans[key] = MatvecPlan(h, True)
         else:
-            pl = PanelPlan(h)
+            pl = PersistentPlan(h) if PERSISTENT else PanelPlan(h)
             if graph:
                 with torch.cuda.device(pl.dev):
                     pl.capture()
@@ -599,3 +602,156 @@ def _ranges_np(starts, lengths):
         return np.zeros(0, dtype=np.int64)
     heads = np.cumsum(lengths) - lengths
     return np.arange(total, dtype=np.int64) + np.repeat(np.asarray(starts, np.int64) - heads, lengths)
+
+
+# --------------------------------------------------------------------------
+# persistent plan: the whole product in one cooperative launch
+
+class _PanelRec:
+    __slots__ = ("name", "panels", "A0", "in0", "out")
+
+
+class PersistentPlan(PanelPlan):
+    """mvm as ONE ``gc_h2mv_persistent`` launch (csrc/h2persist.cu).
+
+    Stages (separated by grid barriers): forward transform by height ->
+    coupling panels + near-field panels (same stage) -> reduction of split
+    panels -> backward transform by height -> leaf basis + near-field sum +
+    output permutation.  Stage 0 inside the kernel gathers x[perm] and
+    zeroes y-hat.  Work items inside a stage are ordered largest first and
+    dealt round-robin to the CTAs."""
+
+    def _phase(self, name, panels, A0, A1, in0, in1, out):
+        rec = _PanelRec()
+        rec.name, rec.panels, rec.A0, rec.in0, rec.out = name, panels, A0, in0, out
+        return rec
+
+    def __init__(self, h):
+        super().__init__(h)
+        d = h.dev
+        rs, cs = h.row_basis.store, h.col_basis.store
+        rf, cf = h.row_tree.flat, h.col_tree.flat
+        mats = {id(cs.V): 0, id(d.coup): 1, id(d.near): 2, id(rs.VT): 3}
+        self.mats = [cs.V, d.coup, d.near, rs.VT]
+        bufs = {id(self.x): 0, id(self.xt): 1, id(self.xhat): 2, id(self.yhat): 3,
+                id(self.yt): 4, id(self.y): 5}
+        xparts, xoff = [], [0]
+
+        def xi_of(rows):
+            arr = np.concatenate(rows).astype(np.int32) if len(rows) else np.zeros(0, np.int32)
+            starts = xoff[0] + _offsets_np([len(r) for r in rows])
+            xparts.append(arr)
+            xoff[0] += len(arr)
+            return starts
+
+        def items_of(rec, target, sel=None):
+            """Column-split work items of the panels of one record (no
+            partial sums: every item owns a slice of output columns)."""
+            a_off, K, T, rows, out_off, acc = rec.panels
+            a_off, K, T, out_off = (np.asarray(v, np.int64) for v in (a_off, K, T, out_off))
+            xs = xi_of(rows)
+            if sel is not None:
+                a_off, K, T, out_off, xs = a_off[sel], K[sel], T[sel], out_off[sel], xs[sel]
+            ns = np.clip(-(-(K * T) // target), 1, np.maximum(1, -(-T // 8)))
+            tw = -(-T // ns)
+            ns = -(-T // tw)
+            pan = np.repeat(np.arange(len(K)), ns)
+            c0 = _ranges_np(np.zeros(len(K), np.int64), ns) * tw[pan]
+            hd = (0 | (mats[id(rec.A0)] << 4) | (bufs[id(rec.in0)] << 8) | (bufs[id(rec.out)] << 12)
+                  | (int(acc) << 16))
+            return np.stack([np.full(len(pan), hd), a_off[pan], xs[pan], out_off[pan], T[pan],
+                             K[pan], c0, np.minimum(tw[pan], T[pan] - c0)], 1)
+
+        fwd = [p for p in self.main_phases if p.name == "forward"]
+        coup = [p for p in self.main_phases if p.name == "coupling"]
+        bwd = [p for p in self.main_phases if p.name == "backward"]
+        H = len(fwd)
+        F = [[items_of(p, 2048)] for p in fwd]          # stage F_h: forward height h
+        C = []
+        if coup:
+            # each coupling panel (one row cluster) runs in the stage right
+            # after the forward transform produced all its inputs
+            live = (d.c_nr > 0) & (d.c_nc > 0)
+            order_ = np.flatnonzero(live)[np.argsort(d.c_rows[live], kind="stable")]
+            sn = d.c_rows[order_]
+            cuts = np.flatnonzero(np.r_[True, sn[1:] != sn[:-1]])
+            hmax = np.maximum.reduceat(cf.height[d.c_cols[order_]], cuts)
+            hlev = np.searchsorted(np.unique(cf.height[cs.materialized & (cs.rank > 0)]), hmax)
+            for lev in range(H + 1):
+                sel = np.flatnonzero(hlev == lev)
+                if not sel.size:
+                    continue
+                it = items_of(coup[0], 8192, sel)
+                (F[lev + 1] if lev + 1 < H else C).append(it)
+        # near field: spread over the forward stages, least-loaded first
+        near = items_of(self.side_phases[0], 8192)
+        load = [sum(int((i[:, 5] * i[:, 7]).sum()) for i in st[1:]) for st in F] + \
+               [sum(int((i[:, 5] * i[:, 7]).sum()) for i in C)]
+        buckets = [[] for _ in load]
+        for j in np.argsort(-(near[:, 5] * near[:, 7]), kind="stable"):
+            k = int(np.argmin(load))
+            buckets[k].append(j)
+            load[k] += int(near[j, 5] * near[j, 7])
+        for k, bj in enumerate(buckets):
+            if bj:
+                (F[k] if k < H else C).append(near[np.array(bj)])
+        B = [[items_of(p, 2048)] for p in bwd]
+        # final stage: every leaf (in range): y[perm] = yt + V yhat
+        size_r = rf.stop - rf.start
+        leaves = np.flatnonzero(rf.is_leaf)
+        if d.row_range is not None:
+            leaves = leaves[(rf.start[leaves] >= d.row_range[0]) & (rf.stop[leaves] <= d.row_range[1])]
+        has = rs.materialized[leaves] & (rs.rank[leaves] > 0)
+        K = np.where(has, rs.rank[leaves], 0)
+        rows = [o + np.arange(k) for o, k in zip(np.where(has, rs.coef_off[leaves], 0), K)]
+        xs = xi_of(rows)
+        hd = 3 | (3 << 4) | (3 << 8) | (5 << 12)
+        Lst = [np.stack([np.full(len(leaves), hd), np.where(has, rs.v_off[leaves], 0), xs,
+                         rf.start[leaves], size_r[leaves], K, np.zeros(len(leaves), np.int64),
+                         np.zeros(len(leaves), np.int64)], 1)]
+
+        def stage(parts, critical=1):
+            """Concatenate a stage: latency-critical transform items first,
+            then the bandwidth filler, each largest first."""
+            out = []
+            for k, it in enumerate(parts):
+                if len(it):
+                    work = it[:, 5] * np.maximum(it[:, 7], 1)
+                    out.append(it[np.argsort(-work, kind="stable")])
+            return np.concatenate(out) if out else np.zeros((0, 8), np.int64)
+
+        stages = [stage(s) for s in F] + ([stage(C)] if C else []) + [stage(s) for s in B] + [stage(Lst)]
+        stages = [s for s in stages if len(s)]
+        self.stage_sizes = [len(s) for s in stages]
+        allit = np.concatenate(stages).astype(np.int64)
+        self.items = to_dev(np.ascontiguousarray(allit), self.dev)
+        self.stage_off = to_dev(np.concatenate([[0], np.cumsum(self.stage_sizes)]).astype(np.int32), self.dev)
+        xidx = np.concatenate(xparts) if xparts else np.zeros(1, np.int32)
+        self.xidx_all = to_dev(xidx if len(xidx) else np.zeros(1, np.int32), self.dev)
+        self.scratch = torch.zeros(1, dtype=torch.float64, device=self.dev)
+        self.barrier = torch.zeros(1, dtype=torch.int32, device=self.dev)
+        import ctypes
+        self._mats = (ctypes.c_void_p * 4)(*[m.data_ptr() for m in self.mats])
+        self._bufs = (ctypes.c_void_p * 8)(self.x.data_ptr(), self.xt.data_ptr(), self.xhat.data_ptr(),
+                                           self.yhat.data_ptr(), self.yt.data_ptr(), self.y.data_ptr(),
+                                           self.scratch.data_ptr(), 0)
+        self.zero_len = int(self.yhat.numel())
+        self.grid = 0            # 0: largest co-resident grid
+        self.timing = None       # set to an int64 tensor to record stage times
+        self.bytes = int(sum(int((s[:, 5] * np.maximum(s[:, 7], 1)).sum()) for s in stages) * 8)
+        self.max_rows = int(max(int(s[:, 5].max()) for s in stages))
+
+    def _body(self, phase_events=None, phase="coupling"):
+        st = stream_handle()
+        if phase_events is not None:
+            phase_events[0].record()
+        _native.call("gc_h2mv_persistent", ptr(self.items), ptr(self.xidx_all), ptr(self.stage_off),
+                     len(self.stage_sizes), ptr(self.perm_in), ptr(self.perm_out), self.n_in,
+                     self.zero_len, self._mats, self._bufs, ptr(self.barrier), self.grid,
+                     ptr(self.timing) if self.timing is not None else None, self.max_rows, st)
+        if phase_events is not None:
+            phase_events[1].record()
+
+    @property
+    def num_kernels(self):
+        return 1

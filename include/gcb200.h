@@ -191,20 +191,18 @@ int gc_panelmv(int64_t nitems, const int64_t* items, const int32_t* xidx,
                const double* in1, double* out, double* scratch, int64_t nred,
                const int64_t* red, void* stream);
 
-/* The whole product y = H x as ONE persistent cooperative kernel (stages
- * separated by grid barriers, csrc/h2persist.cu).  items (nitems,8),
- * stage_off (nstages+1), xidx as for gc_panelmv; mats[4] = panel matrix
- * bases; bufs[8] = x, xt, x-hat, y-hat, yt, y, scratch, unused; barrier
- * [dev] one unsigned int (reset by the call).  grid <= 0 picks the largest
- * co-resident grid; max_rows = the longest panel (shared-memory input
- * staging).  timing [dev] (optional, 2*nstages+2 int64): block 0
- * records %globaltimer after stage 0 and before/after every barrier.
- * Capturable in a CUDA graph. */
-int gc_h2mv_persistent(const int64_t* items, const int32_t* xidx,
-                       const int32_t* stage_off, int32_t nstages,
+/* The whole product y = H x as ONE persistent cooperative kernel scheduled
+ * by dataflow counters (csrc/h2persist.cu; replaces h2.mvm, h2.py:63-80).
+ * items (nitems,8) in walk order (format in csrc/h2persist.cu); xidx int32
+ * input indices; mats[4] = panel matrix bases; bufs[8] = x, xt, x-hat,
+ * y-hat (coupling), y-hat, yt (near field), y, unused; sync [dev] nsync
+ * counters (reset by the call).  grid <= 0: the largest co-resident grid;
+ * max_rows: the longest panel (shared-memory input staging); timing [dev]
+ * optional per-CTA finish times (%globaltimer).  Capturable in a graph. */
+int gc_h2mv_persistent(const int64_t* items, const int32_t* xidx, int64_t nitems,
                        const int64_t* perm_in, const int64_t* perm_out, int64_t n_in,
                        int64_t zero_len, const double* const* mats, double* const* bufs,
-                       unsigned int* barrier, int32_t grid, long long* timing,
+                       unsigned int* sync, int32_t nsync, int32_t grid, long long* timing,
                        int32_t max_rows, void* stream);
 /* Largest co-resident grid of gc_h2mv_persistent (max_rows: longest panel). */
 int gc_h2mv_grid(int32_t max_rows, int32_t* grid);

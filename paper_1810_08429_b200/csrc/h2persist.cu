@@ -1,24 +1,32 @@
 // The whole H2 matvec (h2.mvm, h2.py:63-80) as ONE persistent cooperative
-// kernel: every tree level of the forward transform, the coupling phase,
-// the coupling reduction, every level of the backward transform and the
-// final leaf-basis + near-field + permutation stage run as stages of a
-// single launch separated by grid barriers.  The ~20 launches (and their
-// drain/launch gaps) of the level-by-level formulation collapse to one;
-// the near-field panels run in the same stage as the coupling panels.
+// kernel driven by dataflow counters instead of level barriers.
 //
-// Work items (8 x int64):
-//   [0] type | a_sel << 4 | in_sel << 8 | out_sel << 12 | acc << 16
-//       type 0: panel product -> out[out_off + t]  (acc: += instead of =)
-//       type 1: panel product -> scratch[out_off + t]
-//       type 2: reduce: out[out_off + t] (+)= sum_{i<aux2} scratch[aux + i*T + t]
-//       type 3: leaf final: y[perm_out[out_off + t]] = yt[out_off + t] + panel(t)
-//   [1] a_off  [2] xi_off  [3] out_off  [4] T  [5] nrows  [6] c0 / aux  [7] tw / aux2
-// Panel product over the column slice t in [c0, c0+tw) (tw = 0: all T):
-//   s[t] = sum_{r < nrows} A[a_off + r*T + t] * in[xidx[xi_off + r]].
-// Panels are split by columns, never by rows, so no partial sums exist.
-// Every output element has one writer and a fixed summation order, so the
-// result is bitwise identical to the multi-launch formulation's order
-// within each item and deterministic run to run.
+// Every product phase is a list of work items over contiguous panels
+// (forward transform per tree height, coupling per row cluster, near field
+// per row leaf, backward transform per height, final leaf basis + near sum
+// + output permutation).  Panels are split by output COLUMNS only, so every
+// output element is written by exactly one item with a fixed summation
+// order: the result is bitwise deterministic and there are no partial sums.
+//
+// CTAs walk the global item list round-robin (item i -> CTA i mod G).  An
+// item names up to two (counter, target) conditions it waits for and up to
+// two counters it bumps when done; dependencies always point to earlier
+// items, so with all CTAs co-resident (cooperative launch) the walk cannot
+// deadlock.  Static operands (descriptor, input indices, the first batch of
+// matrix rows) are loaded BEFORE waiting, so after a dependency resolves an
+// item costs one L2 round trip for its inputs plus the stream of the rest of
+// its panel.  The latency-bound transform levels no longer pay a launch or
+// a grid barrier each.
+//
+// Work item (8 x int64):
+//   [0] type | a_sel<<4 | in_sel<<8 | out_sel<<12 | add_sel<<20
+//       type 0: out[out_off + t] = (add ? add[out_off + t] : 0) + s[t]
+//       type 2: out[out_off + t] = sum_{i < nrows} scratch[a_off + i*T + t]
+//       type 3: y[perm_out[out_off + t]] = add[out_off + t] + s[t]
+//   [1] a_off  [2] xi_off  [3] out_off  [4] T (row stride)  [5] nrows
+//   [6] c0 | tw << 16 | sig1 << 32 | sig2 << 40     (column slice, signals)
+//   [7] wait1 | wait2 << 32, wait = counter << 24 | target   (counter 127: none)
+//   s[t] = sum_{r < nrows} A[a_off + r*T + t] * in[xidx[xi_off + r]],  t in [c0, c0+tw)
 #include <cuda/atomic>
 
 #include "common.cuh"
@@ -27,21 +35,21 @@ namespace gcb {
 
 constexpr int PM_THREADS = 256;
 constexpr int PM_UNROLL = 16;
+constexpr int PM_NONE = 127;
+constexpr int PM_TICKET = 126;   // sync slot of the work ticket
 
 struct MvProgram {
     const int64_t* items;
     const int32_t* xidx;
-    const int32_t* stage_off;   // nstages + 1
-    int32_t nstages;
-    int32_t pad;
+    int64_t nitems;
     const int64_t* perm_in;     // xt[i] = x[perm_in[i]]
-    const int64_t* perm_out;    // y[perm_out[i]] = yt[i] + ...
+    const int64_t* perm_out;    // y[perm_out[i]] = ...
     int64_t n_in;
-    int64_t zero_len;           // yhat entries zeroed in stage 0
+    int64_t zero_len;           // buf[3] entries zeroed before the walk
     const double* mat[4];       // panel matrices
-    double* buf[8];             // 0 x, 1 xt, 2 xhat, 3 yhat, 4 yt, 5 y, 6 scratch
-    unsigned int* barrier;      // zeroed before launch
-    long long* timing;          // optional: globaltimer after each stage (block 0)
+    double* buf[8];             // 0 x, 1 xt, 2 x-hat, 3 y-hat (coupling), 4 y-hat, 5 yt (near), 6 y, 7 scratch
+    unsigned int* sync;         // [0] start barrier, [1..] dataflow counters; zeroed before launch
+    long long* timing;          // optional: per item (wait start, wait end, done)
 };
 
 __device__ __forceinline__ long long global_ns() {
@@ -50,34 +58,29 @@ __device__ __forceinline__ long long global_ns() {
     return t;
 }
 
-__device__ __forceinline__ void grid_barrier(unsigned int* bar, unsigned int target) {
-    __syncthreads();
-    if (threadIdx.x == 0) {
-        cuda::atomic_ref<unsigned int, cuda::thread_scope_device> a(*bar);
-        __threadfence();
-        a.fetch_add(1u, cuda::memory_order_release);
-        while (a.load(cuda::memory_order_acquire) < target) __nanosleep(32);
-        __threadfence();
-    }
-    __syncthreads();
+__device__ __forceinline__ void wait_counter(unsigned int* ctr, unsigned int target) {
+    cuda::atomic_ref<unsigned int, cuda::thread_scope_device> a(*ctr);
+    while (a.load(cuda::memory_order_acquire) < target) __nanosleep(20);
 }
 
-__device__ void panel_item(const MvProgram& P, const int64_t* it, double* xs, double* red) {
+__device__ void run_item(const MvProgram& P, const int64_t* it, double* xs, double* red,
+                         long long* tm) {
     const int64_t head = it[0];
     const int type = (int)(head & 15), a_sel = (int)((head >> 4) & 15);
     const int in_sel = (int)((head >> 8) & 15), out_sel = (int)((head >> 12) & 15);
-    const bool acc_out = ((head >> 16) & 1) != 0;
+    const int add_sel = (int)((head >> 20) & 15);
     const int64_t a_off = it[1], xi_off = it[2], out_off = it[3];
-    const int T = (int)it[4], nrows = (int)it[5], c0 = (int)it[6];
-    const int tw = it[7] > 0 ? (int)it[7] : T;          // column slice [c0, c0 + tw)
+    const int T = (int)it[4], nrows = (int)it[5];
+    const int64_t w6 = it[6], w7 = it[7];
+    const int c0 = (int)(w6 & 0xffff);
+    const int tw = ((w6 >> 16) & 0xffff) ? (int)((w6 >> 16) & 0xffff) : T;
     const double* __restrict__ A = P.mat[a_sel] + a_off;
-    const double* __restrict__ x = P.buf[in_sel];
     const int32_t* __restrict__ xi = P.xidx + xi_off;
     const int tt = tw < PM_THREADS ? (tw > 0 ? tw : 1) : PM_THREADS;
     const int ng = PM_THREADS / tt;
     const int g = threadIdx.x / tt;
-    // first batch of matrix loads is issued before the (dependent) input
-    // gather so the two memory round trips overlap
+    // static operands first: the first batch of matrix rows and the input
+    // indices do not depend on other items
     double a0[PM_UNROLL];
     {
         const int t = c0 + (int)(threadIdx.x % tt);
@@ -88,9 +91,31 @@ __device__ void panel_item(const MvProgram& P, const int64_t* it, double* xs, do
             a0[j] = (live && r < nrows) ? __ldcs(A + (int64_t)r * T + t) : 0.0;
         }
     }
-    // inputs may have been written by other CTAs in an earlier stage of this
-    // launch: read them through L2 (ld.global.cg), never from a stale L1 line
-    for (int r = threadIdx.x; r < nrows; r += PM_THREADS) xs[r] = __ldcg(x + __ldg(xi + r));
+    int32_t myidx[4];
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {
+        const int r = threadIdx.x + j * PM_THREADS;
+        myidx[j] = r < nrows ? __ldg(xi + r) : 0;
+    }
+    // dependencies
+    if (tm && threadIdx.x == 0) tm[0] = global_ns();
+    if (threadIdx.x == 0) {
+        const unsigned int w1 = (unsigned int)(w7 & 0xffffffff), w2 = (unsigned int)(w7 >> 32);
+        if ((w1 >> 24) != PM_NONE) wait_counter(P.sync + 1 + (w1 >> 24), w1 & 0xffffff);
+        if ((w2 >> 24) != PM_NONE) wait_counter(P.sync + 1 + (w2 >> 24), w2 & 0xffffff);
+        __threadfence();
+    }
+    __syncthreads();
+    if (tm && threadIdx.x == 0) tm[1] = global_ns();
+    // inputs were written by other CTAs: read through L2 (ld.global.cg)
+    const double* __restrict__ x = P.buf[in_sel];
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {
+        const int r = threadIdx.x + j * PM_THREADS;
+        if (r < nrows) xs[r] = __ldcg(x + myidx[j]);
+    }
+    for (int r = threadIdx.x + 4 * PM_THREADS; r < nrows; r += PM_THREADS)
+        xs[r] = __ldcg(x + __ldg(xi + r));
     __syncthreads();
     for (int t0 = c0; t0 < c0 + tw; t0 += tt) {
         const int t = t0 + (int)(threadIdx.x % tt);
@@ -119,65 +144,94 @@ __device__ void panel_item(const MvProgram& P, const int64_t* it, double* xs, do
         if (threadIdx.x < tt && t < c0 + tw) {
             double s = red[threadIdx.x];
             for (int q = 1; q < ng; ++q) s += red[q * tt + threadIdx.x];
-            if (type == 0) {
-                double* o = P.buf[out_sel] + out_off + t;
-                *o = acc_out ? __ldcg(o) + s : s;
-            } else if (type == 1) {
-                P.buf[6][out_off + t] = s;
-            } else {  // type 3: leaf final
-                const int64_t i = out_off + t;
-                P.buf[5][__ldg(P.perm_out + i)] = __ldcg(P.buf[4] + i) + s;
-            }
+            const int64_t i = out_off + t;
+            if (add_sel) s = __ldcg(P.buf[add_sel] + i) + s;
+            if (type == 3)
+                P.buf[6][__ldg(P.perm_out + i)] = s;
+            else
+                P.buf[out_sel][i] = s;
         }
         __syncthreads();
     }
+    // signals (after every thread's stores: barrier above, then a fence)
+    if (threadIdx.x == 0) {
+        const int s1 = (int)((w6 >> 32) & 0xff), s2 = (int)((w6 >> 40) & 0xff);
+        __threadfence();
+        if (s1 != PM_NONE) atomicAdd(P.sync + 1 + s1, 1u);
+        if (s2 != PM_NONE) atomicAdd(P.sync + 1 + s2, 1u);
+        if (tm) tm[2] = global_ns();
+    }
 }
 
-__device__ void reduce_item(const MvProgram& P, const int64_t* it) {
+// type 2: out[out_off + t] = sum_{i < nrows} scratch[a_off + i*T + t] (partials of a
+// row-split panel, summed in chunk order)
+__device__ void reduce_item(const MvProgram& P, const int64_t* it, long long* tm) {
     const int64_t head = it[0];
     const int out_sel = (int)((head >> 12) & 15);
-    const bool acc_out = ((head >> 16) & 1) != 0;
-    const int64_t out_off = it[3], T = it[4], so = it[6], ni = it[7];
-    const double* sc = P.buf[6];
+    const int64_t so = it[1], out_off = it[3], T = it[4], nch = it[5];
+    const int64_t w6 = it[6], w7 = it[7];
+    if (threadIdx.x == 0) {
+        if (tm) tm[0] = global_ns();
+        const unsigned int w1 = (unsigned int)(w7 & 0xffffffff), w2 = (unsigned int)(w7 >> 32);
+        if ((w1 >> 24) != PM_NONE) wait_counter(P.sync + 1 + (w1 >> 24), w1 & 0xffffff);
+        if ((w2 >> 24) != PM_NONE) wait_counter(P.sync + 1 + (w2 >> 24), w2 & 0xffffff);
+        __threadfence();
+        if (tm) tm[1] = global_ns();
+    }
+    __syncthreads();
+    const double* sc = P.buf[7];
     for (int64_t t = threadIdx.x; t < T; t += PM_THREADS) {
         double v = __ldcg(sc + so + t);
-        for (int64_t i = 1; i < ni; ++i) v += __ldcg(sc + so + i * T + t);
-        double* o = P.buf[out_sel] + out_off + t;
-        *o = acc_out ? __ldcg(o) + v : v;
+        for (int64_t i = 1; i < nch; ++i) v += __ldcg(sc + so + i * T + t);
+        P.buf[out_sel][out_off + t] = v;
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        const int s1 = (int)((w6 >> 32) & 0xff), s2 = (int)((w6 >> 40) & 0xff);
+        __threadfence();
+        if (s1 != PM_NONE) atomicAdd(P.sync + 1 + s1, 1u);
+        if (s2 != PM_NONE) atomicAdd(P.sync + 1 + s2, 1u);
+        if (tm) tm[2] = global_ns();
     }
 }
 
 __global__ void __launch_bounds__(PM_THREADS, 4) k_h2mv_persistent(MvProgram P) {
-    extern __shared__ double xs[];      // max rows over all items
+    extern __shared__ double xs[];      // longest panel's inputs
     __shared__ double red[PM_THREADS];
     const unsigned int G = gridDim.x;
-    // stage 0: permuted input and zeroed coupling accumulators
-    {
+    {   // permuted input and zeroed coupling accumulators, one grid barrier
         const int64_t stride = (int64_t)G * PM_THREADS;
         for (int64_t i = blockIdx.x * (int64_t)PM_THREADS + threadIdx.x; i < P.n_in; i += stride)
             P.buf[1][i] = __ldcg(P.buf[0] + __ldg(P.perm_in + i));
         for (int64_t i = blockIdx.x * (int64_t)PM_THREADS + threadIdx.x; i < P.zero_len; i += stride)
             P.buf[3][i] = 0.0;
+        __syncthreads();
+        if (threadIdx.x == 0) {
+            __threadfence();
+            atomicAdd(P.sync, 1u);
+            wait_counter(P.sync, G);
+            __threadfence();
+        }
+        __syncthreads();
     }
-    if (P.timing && blockIdx.x == 0 && threadIdx.x == 0) P.timing[0] = global_ns();
-    unsigned int target = G;
-    grid_barrier(P.barrier, target);
-    if (P.timing && blockIdx.x == 0 && threadIdx.x == 0) P.timing[1] = global_ns();
-    for (int s = 0; s < P.nstages; ++s) {
-        const int b = P.stage_off[s], e = P.stage_off[s + 1];
-        for (int i = b + (int)blockIdx.x; i < e; i += (int)G) {
-            const int64_t* it = P.items + 8 * (int64_t)i;
-            if ((it[0] & 15) == 2)
-                reduce_item(P, it);
-            else
-                panel_item(P, it, xs, red);
-        }
-        if (P.timing && blockIdx.x == 0 && threadIdx.x == 0) P.timing[2 + 2 * s] = global_ns();
-        if (s + 1 < P.nstages) {
-            target += G;
-            grid_barrier(P.barrier, target);
-        }
-        if (P.timing && blockIdx.x == 0 && threadIdx.x == 0) P.timing[3 + 2 * s] = global_ns();
+    if (P.timing && blockIdx.x == 0 && threadIdx.x == 0) P.timing[3 * P.nitems] = global_ns();
+    // dynamic walk: tickets hand out items in priority order; every item's
+    // dependencies have smaller indices and were handed out earlier to
+    // co-resident CTAs, so waiting cannot deadlock
+    __shared__ long long s_ticket;
+    unsigned int* ticket = P.sync + 1 + PM_TICKET;
+    for (;;) {
+        if (threadIdx.x == 0) s_ticket = (long long)atomicAdd(ticket, 1u);
+        __syncthreads();
+        const int64_t i = s_ticket;
+        __syncthreads();
+        if (i >= P.nitems) break;
+        const int64_t* it = P.items + 8 * i;
+        long long* tm = P.timing ? P.timing + 3 * i : nullptr;
+        if ((it[0] & 15) == 2)
+            reduce_item(P, it, tm);
+        else
+            run_item(P, it, xs, red, tm);
     }
 }
 
@@ -185,25 +239,22 @@ __global__ void __launch_bounds__(PM_THREADS, 4) k_h2mv_persistent(MvProgram P) 
 
 using namespace gcb;
 
-extern "C" int gc_h2mv_persistent(const int64_t* items, const int32_t* xidx,
-                                  const int32_t* stage_off, int32_t nstages,
+extern "C" int gc_h2mv_persistent(const int64_t* items, const int32_t* xidx, int64_t nitems,
                                   const int64_t* perm_in, const int64_t* perm_out, int64_t n_in,
                                   int64_t zero_len, const double* const* mats, double* const* bufs,
-                                  unsigned int* barrier, int32_t grid, long long* timing,
-                                  int32_t max_rows, void* stream) {
+                                  unsigned int* sync, int32_t nsync, int32_t grid,
+                                  long long* timing, int32_t max_rows, void* stream) {
     MvProgram P;
     P.items = items;
     P.xidx = xidx;
-    P.stage_off = stage_off;
-    P.nstages = nstages;
-    P.pad = 0;
+    P.nitems = nitems;
     P.perm_in = perm_in;
     P.perm_out = perm_out;
     P.n_in = n_in;
     P.zero_len = zero_len;
     for (int i = 0; i < 4; ++i) P.mat[i] = mats[i];
     for (int i = 0; i < 8; ++i) P.buf[i] = bufs[i];
-    P.barrier = barrier;
+    P.sync = sync;
     P.timing = timing;
     cudaStream_t st = (cudaStream_t)stream;
     const size_t smem = (size_t)(max_rows > 0 ? max_rows : 1) * sizeof(double);
@@ -219,8 +270,8 @@ extern "C" int gc_h2mv_persistent(const int64_t* items, const int32_t* xidx,
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
     const int cap = max_blocks * sms;
     if (grid <= 0 || grid > cap) grid = cap;
-    e = cudaMemsetAsync(barrier, 0, sizeof(unsigned int), st);
-    if (e != cudaSuccess) return cuda_status(e, "gc_h2mv_persistent barrier reset");
+    e = cudaMemsetAsync(sync, 0, (size_t)nsync * sizeof(unsigned int), st);
+    if (e != cudaSuccess) return cuda_status(e, "gc_h2mv_persistent counter reset");
     void* args[] = {&P};
     e = cudaLaunchCooperativeKernel((const void*)k_h2mv_persistent, dim3(grid), dim3(PM_THREADS),
                                     args, smem, st);

@@ -611,15 +611,33 @@ class _PanelRec:
     __slots__ = ("name", "panels", "A0", "in0", "out")
 
 
-class PersistentPlan(PanelPlan):
-    """mvm as ONE ``gc_h2mv_persistent`` launch (csrc/h2persist.cu).
+_NONE = 127
 
-    Stages (separated by grid barriers): forward transform by height ->
-    coupling panels + near-field panels (same stage) -> reduction of split
-    panels -> backward transform by height -> leaf basis + near-field sum +
-    output permutation.  Stage 0 inside the kernel gathers x[perm] and
-    zeroes y-hat.  Work items inside a stage are ordered largest first and
-    dealt round-robin to the CTAs."""
+
+def _wait(ctr=None, target=0):
+    """Packed (counter, target) dependency; counter None = no wait."""
+    if ctr is None:
+        return _NONE << 24
+    if target >= (1 << 24):
+        raise ConfigError("dependency target too large")
+    return (int(ctr) << 24) | int(target)
+
+
+class PersistentPlan(PanelPlan):
+    """The whole product as ONE ``gc_h2mv_persistent`` launch
+    (csrc/h2persist.cu), scheduled by dataflow counters.
+
+    Item order (CTAs take items round-robin): forward transform by height
+    (height h waits for every height h-1 item), near field, coupling panels
+    (each waits for the forward height of its inputs), backward transform
+    top-down (waits for all coupling and the level above), final leaf stage
+    (waits for backward and near field).  Counters: FWD[h] = h, BWD[h] =
+    64 + h, CPL = 128, NEAR = 129, BWD_ALL = 130.  Coupling results go to a
+    separate y-hat buffer so the backward step is ``y_c = yc_c + E y_p``
+    with a single writer per entry."""
+
+    FWD, BWD, CPLC, CPLR, NEAR, BWD_ALL, CPL = 0, 20, 40, 60, 80, 81, 82
+    NSYNC = 1 + 128                       # slot 1+126 is the work ticket
 
     def _phase(self, name, panels, A0, A1, in0, in1, out):
         rec = _PanelRec()
@@ -631,10 +649,11 @@ class PersistentPlan(PanelPlan):
         d = h.dev
         rs, cs = h.row_basis.store, h.col_basis.store
         rf, cf = h.row_tree.flat, h.col_tree.flat
-        mats = {id(cs.V): 0, id(d.coup): 1, id(d.near): 2, id(rs.VT): 3}
+        f64 = dict(dtype=torch.float64, device=self.dev)
+        self.yc = torch.zeros(max(rs.coef_size, 1), **f64)        # coupling part of y-hat
         self.mats = [cs.V, d.coup, d.near, rs.VT]
-        bufs = {id(self.x): 0, id(self.xt): 1, id(self.xhat): 2, id(self.yhat): 3,
-                id(self.yt): 4, id(self.y): 5}
+        mats = {id(m): i for i, m in enumerate(self.mats)}
+        B_X, B_XT, B_XH, B_YC, B_YH, B_YT, B_Y, B_SC = range(8)
         xparts, xoff = [], [0]
 
         def xi_of(rows):
@@ -644,59 +663,143 @@ class PersistentPlan(PanelPlan):
             xoff[0] += len(arr)
             return starts
 
-        def items_of(rec, target, sel=None):
-            """Column-split work items of the panels of one record (no
-            partial sums: every item owns a slice of output columns)."""
-            a_off, K, T, rows, out_off, acc = rec.panels
-            a_off, K, T, out_off = (np.asarray(v, np.int64) for v in (a_off, K, T, out_off))
-            xs = xi_of(rows)
-            if sel is not None:
-                a_off, K, T, out_off, xs = a_off[sel], K[sel], T[sel], out_off[sel], xs[sel]
-            ns = np.clip(-(-(K * T) // target), 1, np.maximum(1, -(-T // 8)))
+        def make(typ, a_sel, in_sel, out_sel, add_sel, a_off, xs, out_off, T, K, target,
+                 sig1, sig2, wait1, wait2):
+            """Column-split items of a list of panels (vectorised)."""
+            a_off, xs, out_off, T, K = (np.asarray(v, np.int64) for v in (a_off, xs, out_off, T, K))
+            n = len(T)
+            if n == 0:
+                return np.zeros((0, 8), np.int64)
+            ns = np.clip(-(-(np.maximum(K, 1) * T) // target), 1, np.maximum(1, -(-T // 8)))
             tw = -(-T // ns)
             ns = -(-T // tw)
-            pan = np.repeat(np.arange(len(K)), ns)
-            c0 = _ranges_np(np.zeros(len(K), np.int64), ns) * tw[pan]
-            hd = (0 | (mats[id(rec.A0)] << 4) | (bufs[id(rec.in0)] << 8) | (bufs[id(rec.out)] << 12)
-                  | (int(acc) << 16))
-            return np.stack([np.full(len(pan), hd), a_off[pan], xs[pan], out_off[pan], T[pan],
-                             K[pan], c0, np.minimum(tw[pan], T[pan] - c0)], 1)
+            pan = np.repeat(np.arange(n), ns)
+            c0 = _ranges_np(np.zeros(n, np.int64), ns) * tw[pan]
+            w = np.minimum(tw[pan], T[pan] - c0)
+            if np.any(T > 0xffff):
+                raise ConfigError("panel wider than 65535 columns")
+            head = typ | (a_sel << 4) | (np.asarray(in_sel, np.int64)[pan] << 8 if np.ndim(in_sel) else in_sel << 8) \
+                | (out_sel << 12) | (add_sel << 20)
+            w6 = c0 | (w << 16) | (np.int64(sig1) << 32) | (np.int64(sig2) << 40)
+            w7 = np.asarray(wait1, np.int64) | (np.asarray(wait2, np.int64) << 32)
+            w7 = w7[pan] if np.ndim(w7) else np.full(len(pan), w7)
+            return np.stack([np.broadcast_to(head, pan.shape), a_off[pan], xs[pan], out_off[pan],
+                             T[pan], K[pan], w6, w7], 1)
 
+        # ---- forward transform (column basis)
         fwd = [p for p in self.main_phases if p.name == "forward"]
+        nF, F = [], []
+        for lev, p in enumerate(fwd):
+            a_off, K, T, rows, out_off, _ = p.panels
+            xs = xi_of(rows)
+            it = make(0, 0, B_XT if lev == 0 else B_XH, B_XH, 0, a_off, xs, out_off, T, K, 2048,
+                      self.FWD + lev, _NONE,
+                      _wait() if lev == 0 else _wait(self.FWD + lev - 1, nF[lev - 1]), _wait())
+            nF.append(len(it))
+            F.append(it)
+        H = len(F)
+        # ---- near field: ready after the start barrier
+        a_off, K, T, rows, out_off, _ = self.side_phases[0].panels
+        near = make(0, 2, B_XT, B_YT, 0, a_off, xi_of(rows), out_off, T, K, 8192,
+                    self.NEAR, _NONE, _wait(), _wait())
+        nN = len(near)
+        # ---- coupling: row panels cut into ~64 KB row chunks; single-chunk
+        # panels write y-hat directly, longer ones write partials that a
+        # reduce item sums in chunk order
         coup = [p for p in self.main_phases if p.name == "coupling"]
-        bwd = [p for p in self.main_phases if p.name == "backward"]
-        H = len(fwd)
-        F = [[items_of(p, 2048)] for p in fwd]          # stage F_h: forward height h
-        C = []
+        C = [[] for _ in range(max(H, 1))]
+        R = []
+        nCres = 0
+        nres = np.zeros(64, dtype=np.int64)     # coupling results per row level
+        scratch = 0
         if coup:
-            # each coupling panel (one row cluster) runs in the stage right
-            # after the forward transform produced all its inputs
             live = (d.c_nr > 0) & (d.c_nc > 0)
             order_ = np.flatnonzero(live)[np.argsort(d.c_rows[live], kind="stable")]
             sn = d.c_rows[order_]
             cuts = np.flatnonzero(np.r_[True, sn[1:] != sn[:-1]])
             hmax = np.maximum.reduceat(cf.height[d.c_cols[order_]], cuts)
-            hlev = np.searchsorted(np.unique(cf.height[cs.materialized & (cs.rank > 0)]), hmax)
-            for lev in range(H + 1):
-                sel = np.flatnonzero(hlev == lev)
+            fwd_heights = np.unique(cf.height[cs.materialized & (cs.rank > 0)])
+            levs = np.searchsorted(fwd_heights, hmax)
+            row_heights = np.unique(rf.height[rs.materialized])
+            rlev = np.searchsorted(row_heights, rf.height[sn[cuts]])
+            if len(fwd_heights) > 20 or len(row_heights) > 20:
+                raise ConfigError("cluster trees deeper than 20 basis levels")
+            a_off, K, T, rows, out_off, _ = coup[0].panels
+            a_off, K, T, out_off = (np.asarray(v, np.int64) for v in (a_off, K, T, out_off))
+            xs = xi_of(rows)
+            rpi = np.maximum(1, -(-8192 // np.maximum(T, 1)))
+            nch = np.maximum(1, -(-K // rpi))
+            for lev in range(H):
+                sel = np.flatnonzero(levs == lev)
                 if not sel.size:
                     continue
-                it = items_of(coup[0], 8192, sel)
-                (F[lev + 1] if lev + 1 < H else C).append(it)
-        # near field: spread over the forward stages, least-loaded first
-        near = items_of(self.side_phases[0], 8192)
-        load = [sum(int((i[:, 5] * i[:, 7]).sum()) for i in st[1:]) for st in F] + \
-               [sum(int((i[:, 5] * i[:, 7]).sum()) for i in C)]
-        buckets = [[] for _ in load]
-        for j in np.argsort(-(near[:, 5] * near[:, 7]), kind="stable"):
-            k = int(np.argmin(load))
-            buckets[k].append(j)
-            load[k] += int(near[j, 5] * near[j, 7])
-        for k, bj in enumerate(buckets):
-            if bj:
-                (F[k] if k < H else C).append(near[np.array(bj)])
-        B = [[items_of(p, 2048)] for p in bwd]
-        # final stage: every leaf (in range): y[perm] = yt + V yhat
+                one = sel[nch[sel] == 1]
+                if one.size:
+                    it1 = make(0, 1, B_XH, B_YC, 0, a_off[one], xs[one], out_off[one],
+                               T[one], K[one], 1 << 30, 0, self.CPL,
+                               _wait(self.FWD + lev, nF[lev]), _wait())
+                    it1[:, 6] = (it1[:, 6] & 0xffffffff) | ((self.CPLR + rlev[one]) << 32) | (np.int64(self.CPL) << 40)
+                    C[lev].append(it1)
+                    nres[rlev[one]] += 1
+                    nCres += len(it1)
+                many = sel[nch[sel] > 1]
+                if many.size:
+                    pan = np.repeat(many, nch[many])
+                    ci = _ranges_np(np.zeros(len(many), np.int64), nch[many])
+                    r0 = ci * rpi[pan]
+                    nr = np.minimum(rpi[pan], K[pan] - r0)
+                    sbase = scratch + _offsets_np(nch[many] * T[many])
+                    scratch += int((nch[many] * T[many]).sum())
+                    sb = np.repeat(sbase, nch[many]) + ci * T[pan]
+                    head = 0 | (1 << 4) | (B_XH << 8) | (B_SC << 12)
+                    w6 = 0 | (np.int64(0) << 16) | (np.int64(self.CPLC + lev) << 32) | (np.int64(_NONE) << 40)
+                    chunks = np.stack([np.full(len(pan), head), a_off[pan] + r0 * T[pan], xs[pan] + r0, sb,
+                                       T[pan], nr, np.full(len(pan), w6),
+                                       np.full(len(pan), _wait(self.FWD + lev, nF[lev]) | (_wait() << 32))], 1)
+                    C[lev].append(chunks)
+                    rhead = 2 | (B_YC << 12)
+                    rw6 = ((self.CPLR + rlev[many]) << 32) | (np.int64(self.CPL) << 40)
+                    np.add.at(nres, rlev[many], 1)
+                    R.append((lev, np.stack([np.full(len(many), rhead), sbase, np.zeros(len(many), np.int64),
+                                             out_off[many], T[many], nch[many], rw6,
+                                             np.zeros(len(many), np.int64)], 1), len(chunks)))
+            # reduce items wait for every chunk of their level
+            Rlev = {}
+            for lev, it, nchunks in R:
+                it[:, 7] = _wait(self.CPLC + lev, nchunks) | (_wait() << 32)
+                Rlev[lev] = it
+                nCres += len(it)
+        nC = nCres
+        # ---- backward transform (row basis), top down
+        bwd = [p for p in self.main_phases if p.name == "backward"]
+        roots = rs.materialized & ~np.where(rf.parent >= 0, rs.materialized[np.maximum(rf.parent, 0)], False)
+        row_heights = np.unique(rf.height[rs.materialized])
+        leaf_depth = rf.depth[rf.is_leaf]
+        uniform = bool(len(np.unique(leaf_depth)) == 1 and len(np.unique(rf.height[roots])) <= 1)
+        Bl = []
+        nB = []
+        hts = sorted(np.unique(rf.height[rs.materialized & (rs.rank > 0) & ~rf.is_leaf]), reverse=True)
+        for k, p in enumerate(bwd):
+            a_off, K, T, rows, out_off, _ = p.panels
+            xs = xi_of(rows)
+            h_ = hts[k]
+            ids = np.flatnonzero(rs.materialized & (rs.rank > 0) & ~rf.is_leaf & (rf.height == h_))
+            is_root = roots[ids]
+            in_sel = np.where(is_root, B_YC, B_YH)
+            if uniform:
+                rl_c = int(np.searchsorted(row_heights, h_ - 1))
+                rl_p = int(np.searchsorted(row_heights, h_))
+                w1 = _wait(self.CPLR + rl_c, int(nres[rl_c]))
+                w2 = np.where(is_root, _wait(self.CPLR + rl_p, int(nres[rl_p])),
+                              _wait() if k == 0 else _wait(self.BWD + k - 1, nB[k - 1]))
+            else:
+                w1 = _wait(self.CPL, nC)
+                w2 = _wait() if k == 0 else _wait(self.BWD + k - 1, nB[k - 1])
+            it = make(0, 3, in_sel, B_YH, B_YC, a_off, xs, out_off, T, K, 2048,
+                      self.BWD + k, self.BWD_ALL, w1, w2)
+            nB.append(len(it))
+            Bl.append(it)
+        # ---- final: every leaf in range, y[perm] = yt + V y-hat
         size_r = rf.stop - rf.start
         leaves = np.flatnonzero(rf.is_leaf)
         if d.row_range is not None:
@@ -705,49 +808,91 @@ class PersistentPlan(PanelPlan):
         K = np.where(has, rs.rank[leaves], 0)
         rows = [o + np.arange(k) for o, k in zip(np.where(has, rs.coef_off[leaves], 0), K)]
         xs = xi_of(rows)
-        hd = 3 | (3 << 4) | (3 << 8) | (5 << 12)
-        Lst = [np.stack([np.full(len(leaves), hd), np.where(has, rs.v_off[leaves], 0), xs,
-                         rf.start[leaves], size_r[leaves], K, np.zeros(len(leaves), np.int64),
-                         np.zeros(len(leaves), np.int64)], 1)]
+        in_sel = np.where(roots[leaves], B_YC, B_YH)
+        if uniform and not roots[leaves].any():
+            w1, w2 = (_wait(self.BWD_ALL, sum(nB)) if nB else _wait()), _wait(self.NEAR, nN)
+        else:   # conservative: every coupling result and every near item
+            w1 = _wait(self.BWD_ALL, sum(nB)) if nB else _wait()
+            w2 = _wait(self.CPL, nC + nN)
+            near[:, 6] = (near[:, 6] & ~(np.int64(0xff) << 40)) | (np.int64(self.CPL) << 40)
+        fin = make(3, 3, in_sel, B_Y, B_YT, np.where(has, rs.v_off[leaves], 0), xs, rf.start[leaves],
+                   size_r[leaves], K, 1 << 30, _NONE, _NONE, w1, w2)
+        # ---- walk order: the transform chains interleaved with ready filler
+        # (near field during the forward sweep, mid-level coupling after the
+        # level it waits for, the deepest coupling level during the backward
+        # sweep, which needs it last)
+        def cat(parts):
+            parts = [q for q in parts if len(q)]
+            return np.concatenate(parts) if parts else np.zeros((0, 8), np.int64)
 
-        def stage(parts, critical=1):
-            """Concatenate a stage: latency-critical transform items first,
-            then the bandwidth filler, each largest first."""
-            out = []
-            for k, it in enumerate(parts):
-                if len(it):
-                    work = it[:, 5] * np.maximum(it[:, 7], 1)
-                    out.append(it[np.argsort(-work, kind="stable")])
-            return np.concatenate(out) if out else np.zeros((0, 8), np.int64)
+        def split(a, n):
+            return [a[i * len(a) // n:(i + 1) * len(a) // n] for i in range(n)] if n > 0 else []
 
-        stages = [stage(s) for s in F] + ([stage(C)] if C else []) + [stage(s) for s in B] + [stage(Lst)]
-        stages = [s for s in stages if len(s)]
-        self.stage_sizes = [len(s) for s in stages]
-        allit = np.concatenate(stages).astype(np.int64)
+        Cl = [cat(C[l]) for l in range(H)] if H else []
+        Rl = [Rlev.get(l, np.zeros((0, 8), np.int64)) for l in range(H)]
+        items, names = [], []
+
+        def add(name, a):
+            if len(a):
+                items.append(a)
+                names.append(name)
+
+        add("fwd0", F[0])
+        nsplit = split(near, 2)
+        if H > 1:
+            add("near", nsplit[0])
+            add("fwd1", F[1])
+            add("near", nsplit[1])
+        else:
+            add("near", near)
+        for lev in range(2, H):
+            add("fwd%d" % lev, F[lev])
+            add("cpl%d" % (lev - 1), Cl[lev - 1])
+            add("reduce", Rl[lev - 1])
+        if H > 1:
+            add("cpl%d" % (H - 1), Cl[H - 1])
+            add("reduce", Rl[H - 1])
+        deep = Cl[0] if H else np.zeros((0, 8), np.int64)
+        if uniform and len(Bl) > 1:
+            parts = split(deep, len(Bl) - 1)
+            for k, it in enumerate(Bl[:-1]):
+                add("bwd%d" % k, it)
+                add("cpl0", parts[k])
+            add("reduce", Rl[0] if H else np.zeros((0, 8), np.int64))
+            add("bwd%d" % (len(Bl) - 1), Bl[-1])
+        else:
+            add("cpl0", deep)
+            add("reduce", Rl[0] if H else np.zeros((0, 8), np.int64))
+            for k, it in enumerate(Bl):
+                add("bwd%d" % k, it)
+        add("final", fin)
+        self.segments = [(nm, len(i)) for nm, i in zip(names, items)]
+        allit = np.concatenate([i for i in items if len(i)]).astype(np.int64)
+        self.nitems = len(allit)
         self.items = to_dev(np.ascontiguousarray(allit), self.dev)
-        self.stage_off = to_dev(np.concatenate([[0], np.cumsum(self.stage_sizes)]).astype(np.int32), self.dev)
         xidx = np.concatenate(xparts) if xparts else np.zeros(1, np.int32)
         self.xidx_all = to_dev(xidx if len(xidx) else np.zeros(1, np.int32), self.dev)
-        self.scratch = torch.zeros(1, dtype=torch.float64, device=self.dev)
-        self.barrier = torch.zeros(1, dtype=torch.int32, device=self.dev)
+        self.sync = torch.zeros(self.NSYNC, dtype=torch.int32, device=self.dev)
+        self.scratch = torch.zeros(max(scratch, 1), dtype=torch.float64, device=self.dev)
         import ctypes
         self._mats = (ctypes.c_void_p * 4)(*[m.data_ptr() for m in self.mats])
         self._bufs = (ctypes.c_void_p * 8)(self.x.data_ptr(), self.xt.data_ptr(), self.xhat.data_ptr(),
-                                           self.yhat.data_ptr(), self.yt.data_ptr(), self.y.data_ptr(),
-                                           self.scratch.data_ptr(), 0)
-        self.zero_len = int(self.yhat.numel())
-        self.grid = 0            # 0: largest co-resident grid
-        self.timing = None       # set to an int64 tensor to record stage times
-        self.bytes = int(sum(int((s[:, 5] * np.maximum(s[:, 7], 1)).sum()) for s in stages) * 8)
-        self.max_rows = int(max(int(s[:, 5].max()) for s in stages))
+                                           self.yc.data_ptr(), self.yhat.data_ptr(), self.yt.data_ptr(),
+                                           self.y.data_ptr(), self.scratch.data_ptr())
+        self.zero_len = int(self.yc.numel())
+        self.grid = 0
+        self.timing = None
+        self.max_rows = int(allit[:, 5].max())
+        self.bytes = None
+        self.counts = {"forward": nF, "near": nN, "coupling": nC, "backward": nB}
 
     def _body(self, phase_events=None, phase="coupling"):
         st = stream_handle()
         if phase_events is not None:
             phase_events[0].record()
-        _native.call("gc_h2mv_persistent", ptr(self.items), ptr(self.xidx_all), ptr(self.stage_off),
-                     len(self.stage_sizes), ptr(self.perm_in), ptr(self.perm_out), self.n_in,
-                     self.zero_len, self._mats, self._bufs, ptr(self.barrier), self.grid,
+        _native.call("gc_h2mv_persistent", ptr(self.items), ptr(self.xidx_all), self.nitems,
+                     ptr(self.perm_in), ptr(self.perm_out), self.n_in, self.zero_len,
+                     self._mats, self._bufs, ptr(self.sync), self.NSYNC, self.grid,
                      ptr(self.timing) if self.timing is not None else None, self.max_rows, st)
         if phase_events is not None:
             phase_events[1].record()

@@ -186,6 +186,7 @@ class DeviceBasis:
         self.device = device
         n = len(self.flat)
         self.materialized = np.zeros(n, dtype=bool)
+        self.available = self.materialized     # nodes whose pivots are known (sharding)
         self.rank = np.zeros(n, dtype=np.int64)
         self.rows = np.zeros(n, dtype=np.int64)
         self.piv_off = np.full(n, -1, dtype=np.int64)
@@ -218,6 +219,29 @@ class DeviceBasis:
         return vhat[o:o + self.rank[i]]
 
 
+def coef_layout(flat, roots, rank, base=0):
+    """Coefficient offsets of a basis forest: roots first, then breadth
+    first with the two children of every node adjacent, so the input of a
+    parent's V-hat^T product is one contiguous slice.  Returns (offsets for
+    every tree node, -1 where absent; total size)."""
+    off = np.full(len(flat), -1, dtype=np.int64)
+    pos = base
+    queue = [int(r) for r in roots]
+    for r in queue:
+        off[r] = pos
+        pos += int(rank[r])
+    k = 0
+    while k < len(queue):
+        i = queue[k]
+        k += 1
+        if not flat.is_leaf[i]:
+            for c in (int(flat.left[i]), int(flat.right[i])):
+                off[c] = pos
+                pos += int(rank[c])
+                queue.append(c)
+    return off, int(pos - base)
+
+
 def coupling_marks(btree):
     """Row and column cluster indices of admissible leaves (``gca.py:149-159``)."""
     fb = btree.flat
@@ -246,9 +270,12 @@ def _materialize(flat, marks):
 
 
 def build_cluster_basis(tree, mesh, basis, m, delta_factor=0.5, eps=1e-4, side="row",
-                        orders=(3, 5), marks=None, device=None):
+                        orders=(3, 5), marks=None, device=None, row_range=None):
     """Nested interpolation basis built bottom-up, level-synchronously on
-    the device (``gca.py:162-220``)."""
+    the device (``gca.py:162-220``).  ``row_range=(lo, hi)`` keeps only the
+    nodes inside that range of tree positions (one GPU's subtree when the
+    operator is sharded by block rows, ``parallel.py``); node results do
+    not depend on the restriction."""
     if side not in ("row", "col"):
         raise ConfigError("side must be 'row' or 'col', got %r" % (side,))
     if basis == "collocation" and side == "col":
@@ -261,7 +288,16 @@ def build_cluster_basis(tree, mesh, basis, m, delta_factor=0.5, eps=1e-4, side="
     flat = tree.flat
     store = DeviceBasis(tree, side, dev)
     mat, roots = _materialize(flat, marks)
+    if row_range is not None:
+        inside = (flat.start >= row_range[0]) & (flat.stop <= row_range[1])
+        crossing = mat & ~inside & (flat.start < row_range[1]) & (flat.stop > row_range[0])
+        if np.any(crossing & np.isin(np.arange(len(flat)), roots)):
+            raise ConfigError("a basis root straddles the shard boundary; shard at a "
+                              "coarser tree level")
+        mat = mat & inside
+        roots = roots[inside[roots]]
     store.materialized = mat
+    store.available = mat.copy()
     dmesh = DeviceMesh.get(mesh, orders[0], dev)
     K = 6 * m * m
     W = 2 * K
@@ -357,22 +393,7 @@ def build_cluster_basis(tree, mesh, basis, m, delta_factor=0.5, eps=1e-4, side="
         with torch.cuda.device(dev):
             _native.call("gc_batched_transpose", len(ids), ptr(tdesc), ptr(store.V),
                          ptr(store.VT), stream)
-    # coefficient offsets: breadth first, siblings adjacent
-    pos = 0
-    queue = list(roots)
-    for r in roots:
-        store.coef_off[r] = pos
-        pos += store.rank[r]
-    k = 0
-    while k < len(queue):
-        i = queue[k]
-        k += 1
-        if not flat.is_leaf[i]:
-            for c in (flat.left[i], flat.right[i]):
-                store.coef_off[c] = pos
-                pos += store.rank[c]
-                queue.append(c)
-    store.coef_size = int(pos)
+    store.coef_off, store.coef_size = coef_layout(flat, roots, store.rank)
     store.timing = {"factor_s": t_factor, "aca_s": t_aca, "total_s": time.perf_counter() - t0}
     # host BasisNode objects
     by_index = {}
@@ -498,7 +519,7 @@ def build_h2(btree, row_basis, col_basis, mesh, kind="slp", basis="constant",
     adm = st == 0
     cr, cc = lr[adm], lc[adm]
     nr_r, nc_r = lr[~adm], lc[~adm]
-    if np.any(~rstore.materialized[cr]) or np.any(~cstore.materialized[cc]):
+    if np.any(~rstore.materialized[cr]) or np.any(~cstore.available[cc]):
         raise ConfigError("coupling block without basis content; build the bases "
                           "with coupling_marks(btree)")
     dmesh = DeviceMesh.get(mesh, orders[0], dev)

@@ -1,0 +1,290 @@
+"""Block-row sharding of the H2 operator over GPUs (SURVEY.md §8 e).
+
+One process per GPU (``torch.distributed``, NCCL over NVLink).  With
+P = 2^k ranks, rank g owns the g-th cluster-tree node at depth k: a
+contiguous range of tree-ordered rows.
+
+* Assembly needs no communication for the row side.  Every admissible
+  block sits at tree level >= 4 and every near-field block at the leaf
+  level, so all block rows of a shard lie inside it.  Each rank builds the
+  row and column bases of its own subtree.  Every basis root sits at tree
+  depth >= 4 >= k, so no node straddles shards.
+* Coupling entries on rank g need the column pivots of remote clusters
+  sigma.  One ``all_gather_object`` of the per-rank (node, rank, pivots)
+  lists, a few MB, gives every rank the global column pivot table.
+* Matvec:
+  1. all-gather the owned slice of x (tree order) -> full x_t;
+  2. forward transform of the own column subtree into the own slot of a
+     rank-major x-hat layout;
+  3. all-gather the x-hat slots;
+  4. coupling, backward transform, near field and leaf basis for the own
+     rows -> the owned slice of y (tree order).
+  Rows are disjoint, so no reduction is needed.
+
+The host-side layout logic (``ShardLayout``) is pure numpy and is tested
+with ``gloo`` on the CPU (tests/test_parallel.py).  The device path reuses
+the single-GPU kernels unchanged.
+"""
+
+import numpy as np
+
+from .errors import ConfigError
+
+
+def shard_nodes(flat, world):
+    """Tree nodes owning the shards: the nodes at depth log2(world), in row
+    order."""
+    if world < 1 or world & (world - 1):
+        raise ConfigError("world size must be a power of two, got %d" % world)
+    k = world.bit_length() - 1
+    ids = np.flatnonzero(flat.depth == k)
+    ids = ids[np.argsort(flat.start[ids], kind="stable")]
+    if len(ids) != world or (k and not np.all(flat.left[flat.parent[ids]] >= 0)):
+        raise ConfigError("cluster tree too shallow for %d shards" % world)
+    return ids
+
+
+def shard_range(flat, world, rank):
+    node = shard_nodes(flat, world)[rank]
+    return int(flat.start[node]), int(flat.stop[node])
+
+
+def check_shardable(btree, world):
+    """Every block row must lie inside one shard (block rows at depth >= k)."""
+    fb = btree.flat
+    k = world.bit_length() - 1
+    rows = fb.row[fb.leaf_ids]
+    depth = fb.row_tree.depth[rows]
+    if np.any(depth < k):
+        raise ConfigError("block rows above tree depth %d: shard with fewer GPUs" % k)
+
+
+class ShardLayout:
+    """Per-rank partition data that needs no GPU.
+
+    ``lo, hi`` own tree rows; ``own_leaves`` block-tree leaf ids (DFS order)
+    of the own block rows; ``global_coef(...)`` the rank-major column
+    coefficient layout assembled from every rank's (nodes, ranks).
+    """
+
+    def __init__(self, tree, btree, world, rank):
+        self.world, self.rank = world, rank
+        flat = tree.flat
+        check_shardable(btree, world)
+        self.lo, self.hi = shard_range(flat, world, rank)
+        fb = btree.flat
+        rows = fb.row[fb.leaf_ids]
+        inside = (flat.start[rows] >= self.lo) & (flat.stop[rows] <= self.hi)
+        self.own_leaves = fb.leaf_ids[inside]
+
+    @staticmethod
+    def global_coef(flat, per_rank):
+        """per_rank: list of (nodes, ranks) of each rank's column basis.
+        Returns (offset per tree node (-1 absent), slot size): rank g's
+        coefficients occupy [g*slot, g*slot + size_g) laid out breadth
+        first with siblings adjacent (gca.coef_layout)."""
+        from .gca import coef_layout
+        n = len(flat)
+        rank_all = np.zeros(n, dtype=np.int64)
+        off = np.full(n, -1, dtype=np.int64)
+        layouts = []
+        for nodes, ranks in per_rank:
+            nodes = np.asarray(nodes, dtype=np.int64)
+            rank_all[nodes] = ranks
+            present = np.zeros(n, dtype=bool)
+            present[nodes] = True
+            par = flat.parent[nodes]
+            roots = nodes[(par < 0) | ~present[np.maximum(par, 0)]]
+            roots = roots[np.argsort(roots, kind="stable")]
+            o, size = coef_layout(flat, roots, rank_all)
+            layouts.append((nodes, o, size))
+        slot = max([size for _, _, size in layouts] + [1])
+        for g, (nodes, o, _) in enumerate(layouts):
+            off[nodes] = g * slot + o[nodes]
+        return off, slot
+
+
+# --------------------------------------------------------------------------
+# device path
+
+class ShardedH2:
+    """Own block rows of the H2 operator on this rank's GPU."""
+
+    def __init__(self, h, layout, group, slot):
+        self.h = h
+        self.layout = layout
+        self.group = group
+        self.slot = slot
+        self.plan = None
+
+    def mvm_local(self, x_slice):
+        """Own slice of y = H x (tree order) from the own slice of x."""
+        import torch
+        if self.plan is None:
+            self.plan = ShardPlan(self)
+        with torch.cuda.device(self.plan.dev):
+            return self.plan.run(x_slice)
+
+
+def build_sharded_operator(mesh, cfg, group=None, device=None, timings=None):
+    """Trees, block tree, own bases, allgathered column pivots and the own
+    block rows of the GCA-H2 matrix for this rank."""
+    import time
+
+    import torch
+    import torch.distributed as dist
+
+    from . import gca
+    from .clustering import build_block_tree, build_cluster_tree
+    from .device import require_device, to_dev
+    world = dist.get_world_size(group)
+    rank = dist.get_rank(group)
+    dev = require_device(device)
+    t0 = time.perf_counter()
+    tree = build_cluster_tree(mesh, basis_kind=cfg.basis, leaf_size=cfg.leaf_size)
+    btree = build_block_tree(tree, eta=cfg.eta)
+    layout = ShardLayout(tree, btree, world, rank)
+    rng = (layout.lo, layout.hi)
+    orders = (cfg.q_reg, cfg.q_sing)
+    rmarks, cmarks = gca.coupling_marks(btree)
+    t1 = time.perf_counter()
+    rb = gca.build_cluster_basis(tree, mesh, cfg.basis, cfg.m, cfg.delta_factor, cfg.eps,
+                                 "row", orders, rmarks, dev, row_range=rng)
+    cb = gca.build_cluster_basis(tree, mesh, cfg.basis, cfg.m, cfg.delta_factor, cfg.eps,
+                                 "col", orders, cmarks, dev, row_range=rng)
+    t2 = time.perf_counter()
+    cs = cb.store
+    flat = tree.flat
+    own = np.flatnonzero(cs.materialized)
+    mine = (own, cs.rank[own], [cs.pivots_host[cs.piv_off[i]:cs.piv_off[i] + cs.rank[i]]
+                                 for i in own])
+    gathered = [None] * world
+    dist.all_gather_object(gathered, mine, group=group)
+    # global column pivot table and rank-major coefficient layout
+    piv_parts, pos = [], 0
+    for nodes, ranks, pivs in gathered:
+        for i, r, pv in zip(nodes, ranks, pivs):
+            cs.rank[i] = r
+            cs.piv_off[i] = pos
+            piv_parts.append(np.asarray(pv, dtype=np.int64))
+            pos += int(r)
+    cs.pivots = to_dev(np.concatenate(piv_parts) if piv_parts else np.zeros(1, np.int64), dev)
+    cs.coef_off, slot = ShardLayout.global_coef(flat, [(g[0], g[1]) for g in gathered])
+    cs.coef_size = world * slot
+    cs.available = cs.available.copy()
+    for nodes, _, _ in gathered:
+        cs.available[np.asarray(nodes, dtype=np.int64)] = True
+    h = gca.build_h2(btree, rb, cb, mesh, kind="slp", basis=cfg.basis, disc=cfg.disc,
+                     orders=orders, device=dev, row_range=rng)
+    torch.cuda.synchronize(dev)
+    t3 = time.perf_counter()
+    if timings is not None:
+        timings.update(trees_s=t1 - t0, bases_s=t2 - t1, build_h2_s=t3 - t2, total_s=t3 - t0)
+    return ShardedH2(h, layout, group, slot)
+
+
+def _shard_plan_class():
+    from .h2 import PanelPlan
+
+    class ShardPlan(PanelPlan):
+        """PanelPlan of one shard: the input slice is all-gathered into x_t,
+        the forward transform covers the own column subtree, and the x-hat
+        slots are all-gathered before the coupling phase."""
+
+        def __init__(self, sh):
+            super().__init__(sh.h)
+            self.sh = sh
+            self.lo, self.hi = sh.layout.lo, sh.layout.hi
+            g = sh.layout.rank
+            self.own_xhat = self.xhat[g * sh.slot:(g + 1) * sh.slot]
+            self.y_slice = None
+
+        def run(self, x_slice):
+            import torch
+            import torch.distributed as dist
+            from . import _native
+            from .device import ptr, stream_handle
+            group = self.sh.group
+            dist.all_gather_into_tensor(self.xt, x_slice.contiguous(), group=group)
+            main = torch.cuda.current_stream()
+            fork = torch.cuda.Event()
+            fork.record(main)
+            with torch.cuda.stream(self.side):
+                self.side.wait_event(fork)
+                sst = stream_handle()
+                for P in self.side_phases:
+                    self._launch(P, sst)
+                join = torch.cuda.Event()
+                join.record(self.side)
+            st = stream_handle()
+            self.yhat.zero_()
+            for P in self.main_phases:
+                if P.name == "coupling":
+                    dist.all_gather_into_tensor(self.xhat, self.own_xhat.clone(), group=group)
+                self._launch(P, st)
+            if not any(P.name == "coupling" for P in self.main_phases):
+                dist.all_gather_into_tensor(self.xhat, self.own_xhat.clone(), group=group)
+            main.wait_event(join)
+            for P in self.tail_phases:
+                self._launch(P, st)
+            return self.yt[self.lo:self.hi].clone()
+
+    return ShardPlan
+
+
+def ShardPlan(sh):
+    return _shard_plan_class()(sh)
+
+
+def bench_distributed(args, rank, world, local, metric, workload):
+    """bench.py at N > 1: the same workload sharded by block rows, strong
+    scaling; time = max over ranks of CUDA-event time per product."""
+    import json
+    import time
+
+    import torch
+    import torch.distributed as dist
+
+    from . import cli, geometry, h2
+    mesh = (geometry.build_sphere_mesh(args.level) if args.geometry == "sphere"
+            else geometry.build_cube_mesh(args.level))
+    cfg = cli.default_config(level=args.level, eps=args.eps)
+    build_sharded_operator(mesh, cfg)             # warm-up
+    torch.cuda.synchronize()
+    dist.barrier()
+    t0 = time.perf_counter()
+    timings = {}
+    sh = build_sharded_operator(mesh, cfg, timings=timings)
+    torch.cuda.synchronize()
+    asm = torch.tensor([time.perf_counter() - t0], dtype=torch.float64, device="cuda")
+    dist.all_reduce(asm, op=dist.ReduceOp.MAX)
+    rep = h2.storage_report(sh.h)
+    mine = torch.tensor([rep["couplings"] + rep["nearfield"] + rep["leaf_bases"] + rep["transfers"]],
+                        dtype=torch.float64, device="cuda")
+    dist.all_reduce(mine)
+    n = mesh.nt
+    nbytes = float(mine.item()) / 1.0 + 16 * n
+    x = torch.randn(sh.layout.hi - sh.layout.lo, dtype=torch.float64, device="cuda")
+    for _ in range(args.warmup):
+        sh.mvm_local(x)
+    torch.cuda.synchronize()
+    dist.barrier()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record()
+    for _ in range(args.steps):
+        sh.mvm_local(x)
+    e1.record()
+    torch.cuda.synchronize()
+    t = torch.tensor([e0.elapsed_time(e1) * 1e-3 / args.steps], dtype=torch.float64, device="cuda")
+    dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    dist.barrier()
+    if rank == 0:
+        s = float(t.item())
+        print(json.dumps({
+            "metric": metric, "value": round(nbytes / s / 1e9, 2), "unit": "GB/s", "n_gpus": world,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(s * 1e3, 4),
+            "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f64",
+            "data": "synthetic", "config": dict(workload, parallelism="block-row x%d" % world),
+            "assembly": {"value": round(float(asm.item()), 4), "unit": "s"},
+            "e2e": None, "gpu_launches": None}))
+    dist.destroy_process_group()

@@ -295,3 +295,32 @@ def test_native_launches_counted(sphere2):
     before = _native.launch_count()
     assembly.assemble_galerkin_block("slp", sphere2, "constant", [0, 1], [2, 3])
     assert _native.launch_count() > before
+
+
+def test_sharded_operator_world1_matches_full():
+    """The block-row sharded device path (parallel.py) at world size 1 over
+    NCCL equals the single-operator product (the N>1 exchange logic is
+    covered on the CPU with gloo in tests/test_parallel.py)."""
+    import os
+    import socket
+    import torch.distributed as dist
+    from paper_1810_08429_b200 import parallel
+    with socket.socket() as s:
+        s.bind(("127.0.0.1", 0))
+        port = s.getsockname()[1]
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("nccl", rank=0, world_size=1, device_id=torch.device("cuda", 0))
+    try:
+        mesh = geometry.build_sphere_mesh(4)
+        cfg = cli.default_config(eps=1e-6)
+        sh = parallel.build_sharded_operator(mesh, cfg)
+        hm, tree, _ = cli.build_h2_operator(mesh, cfg)
+        x = np.random.default_rng(3).standard_normal(mesh.nt)
+        xt = torch.from_numpy(x[tree.perm]).cuda()
+        ys = sh.mvm_local(xt).cpu().numpy()
+        y = np.empty(mesh.nt)
+        y[tree.perm] = ys
+        ref = h2.mvm(hm, x)
+        assert np.linalg.norm(y - ref) <= 1e-13 * np.linalg.norm(ref)
+    finally:
+        dist.destroy_process_group()

@@ -207,6 +207,12 @@ int gc_h2mv_persistent(const int64_t* items, const int32_t* xidx, int64_t nitems
 /* Largest co-resident grid of gc_h2mv_persistent (max_rows: longest panel). */
 int gc_h2mv_grid(int32_t max_rows, int32_t* grid);
 
+/* Host helper (no device): norms of n 3-vectors v [host] (n,3) into out
+ * [host] (n,) with mode 0 = sqrt(fma(z,z,fma(y,y,x*x))) (the rounding of
+ * numpy's 1-D norm through OpenBLAS ddot, used for box diameters,
+ * clustering.py:34-43) or mode 1 = sqrt((x*x+y*y)+z*z). */
+int gc_host_norm3(const double* v, int64_t n, double* out, int mode);
+
 /* FP64 DFMA throughput probe used as the roofline denominator (no FP64
  * figure exists in MEASURED_PEAKS.json): blocks x threads x iters x 8 DFMA. */
 int gc_dfma_probe(int64_t blocks, int64_t threads, int64_t iters, double* out,

@@ -28,6 +28,46 @@ def _blas_norm(v):
     return float(np.linalg.norm(v))
 
 
+_NORM_MODE = []
+
+
+def blas_norms(v):
+    """``np.linalg.norm(row)`` for every row of an (n,3) array, bit for bit,
+    without n Python calls: the native host helper evaluates the rounding
+    sequence that numpy's 1-D norm (OpenBLAS ddot) was found to use on this
+    host, checked once against numpy on a probe set; if neither candidate
+    reproduces numpy exactly the rows are normed one by one."""
+    v = np.ascontiguousarray(v, dtype=np.float64).reshape(-1, 3)
+    if not _NORM_MODE:
+        rng = np.random.default_rng(7)
+        probe = np.concatenate([rng.standard_normal((512, 3)),
+                                rng.random((512, 3)) * np.array([1e-3, 1.0, 3.0])])
+        want = np.array([float(np.linalg.norm(r)) for r in probe])
+        mode = None
+        for m in (0, 1):
+            got = _native_norms(probe, m)
+            if got is not None and np.array_equal(got, want):
+                mode = m
+                break
+        _NORM_MODE.append(mode)
+    mode = _NORM_MODE[0]
+    if mode is None:
+        return np.array([float(np.linalg.norm(r)) for r in v])
+    return _native_norms(v, mode)
+
+
+def _native_norms(v, mode):
+    try:
+        from . import _native
+        lib = _native.load()
+    except Exception:  # library not built: exact per-row fallback
+        return None
+    out = np.empty(len(v))
+    if len(v):
+        _native.check(lib.gc_host_norm3(v.ctypes.data, len(v), out.ctypes.data, mode))
+    return out
+
+
 class BoundingBox:
     """Axis-parallel box (``clustering.py:15-43``)."""
 
@@ -69,16 +109,29 @@ class ClusterTree:
     """Node view of a flat cluster tree; ``perm[start:stop]`` are its dofs,
     ``index`` its preorder number."""
 
-    __slots__ = ("perm", "start", "stop", "box", "children", "index", "flat")
+    __slots__ = ("perm", "start", "stop", "_box", "_children", "index", "flat")
 
-    def __init__(self, flat, index, box, children):
+    def __init__(self, flat, index):
         self.flat = flat
         self.perm = flat.perm
         self.index = index
         self.start = int(flat.start[index])
         self.stop = int(flat.stop[index])
-        self.box = box
-        self.children = children
+        self._box = None
+        self._children = None
+
+    @property
+    def box(self):
+        if self._box is None:
+            self._box = BoundingBox(self.flat.lower[self.index], self.flat.upper[self.index])
+        return self._box
+
+    @property
+    def children(self):
+        if self._children is None:
+            f, i = self.flat, self.index
+            self._children = () if f.left[i] < 0 else (f.node(int(f.left[i])), f.node(int(f.right[i])))
+        return self._children
 
     @property
     def size(self):
@@ -89,7 +142,7 @@ class ClusterTree:
         return self.perm[self.start:self.stop]
 
     def is_leaf(self):
-        return not self.children
+        return bool(self.flat.left[self.index] < 0)
 
     def nodes(self):
         """Subtree nodes in preorder."""
@@ -122,18 +175,16 @@ class FlatClusterTree:
         self.left, self.right, self.parent, self.depth = left, right, parent, depth
         self.lower, self.upper = lower, upper
         n = len(start)
-        self.count = np.ones(n, dtype=np.int64)
-        for i in range(n - 1, -1, -1):       # children have larger indices
-            if left[i] >= 0:
-                self.count[i] = 1 + self.count[left[i]] + self.count[right[i]]
-        self.diam = np.array([_blas_norm(u - l) for l, u in zip(lower, upper)])
         self.is_leaf = left < 0
-        # height: 0 for leaves, 1 + max(child heights) otherwise
+        # subtree node counts and heights, one tree depth at a time (bottom up)
+        self.count = np.ones(n, dtype=np.int64)
         h = np.zeros(n, dtype=np.int64)
-        for i in range(n - 1, -1, -1):
-            if left[i] >= 0:
-                h[i] = 1 + max(h[left[i]], h[right[i]])
+        for d in range(int(depth.max()) if n else 0, 0, -1):
+            ids = np.flatnonzero(depth == d)
+            np.add.at(self.count, parent[ids], self.count[ids])
+            np.maximum.at(h, parent[ids], h[ids] + 1)
         self.height = h
+        self.diam = blas_norms(upper - lower)
         self._nodes = [None] * n
 
     def __len__(self):
@@ -142,9 +193,7 @@ class FlatClusterTree:
     def node(self, i):
         nd = self._nodes[i]
         if nd is None:
-            kids = () if self.left[i] < 0 else (self.node(int(self.left[i])),
-                                                 self.node(int(self.right[i])))
-            nd = ClusterTree(self, i, BoundingBox(self.lower[i], self.upper[i]), kids)
+            nd = ClusterTree(self, i)
             self._nodes[i] = nd
         return nd
 
@@ -198,8 +247,11 @@ def build_cluster_tree(mesh, basis_kind="constant", leaf_size=32):
     upper = np.zeros((total, 3))
     perm = np.arange(n)
     # one padding row so that reduceat may address index n
-    lo_pad = lambda p: np.concatenate([lo[p], lo[:1]])
-    hi_pad = lambda p: np.concatenate([hi[p], hi[:1]])
+    # lo/hi/points in current permutation order, plus one padding row so
+    # that reduceat may address index n; permuted in place with perm
+    lo_p = np.concatenate([lo, lo[:1]])
+    hi_p = np.concatenate([hi, hi[:1]])
+    pts_p = points.copy()
 
     # frontier of one tree depth: node ids with contiguous [start, stop)
     ids = np.array([0], dtype=np.int64)
@@ -212,8 +264,8 @@ def build_cluster_tree(mesh, basis_kind="constant", leaf_size=32):
         # frontier may have gaps where shallower leaves sit, so reduce over
         # explicit [start, stop) pairs and drop the in-between reductions)
         bounds = np.stack([s, e], axis=1).ravel()
-        lower[ids] = np.minimum.reduceat(lo_pad(perm), bounds, axis=0)[::2]
-        upper[ids] = np.maximum.reduceat(hi_pad(perm), bounds, axis=0)[::2]
+        lower[ids] = np.minimum.reduceat(lo_p, bounds, axis=0)[::2]
+        upper[ids] = np.maximum.reduceat(hi_p, bounds, axis=0)[::2]
         split = (e - s) > leaf_size
         if not split.any():
             break
@@ -223,9 +275,13 @@ def build_cluster_tree(mesh, basis_kind="constant", leaf_size=32):
         seg_of = np.repeat(np.arange(len(ids_s)), seg_len)
         heads = np.cumsum(seg_len) - seg_len
         pos = np.arange(int(seg_len.sum())) + np.repeat(s_s - heads, seg_len)
-        key = points[perm[pos], axis[seg_of]]
+        key = pts_p[pos, axis[seg_of]]
         order = np.lexsort((key, seg_of))        # stable within each segment
-        perm[pos] = perm[pos[order]]
+        src = pos[order]
+        perm[pos] = perm[src]
+        lo_p[pos] = lo_p[src]
+        hi_p[pos] = hi_p[src]
+        pts_p[pos] = pts_p[src]
         half = seg_len // 2
         lid = ids_s + 1
         rid = ids_s + 1 + np.array([memo[int(h)] for h in half], dtype=np.int64)

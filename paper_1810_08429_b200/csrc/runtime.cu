@@ -1,6 +1,7 @@
 // Error plumbing, launch accounting, permutation gather/scatter, chart
 // quadrature points and the FP64 throughput probe.
 #include <atomic>
+#include <cmath>
 #include <stdarg.h>
 #include <string.h>
 
@@ -143,6 +144,30 @@ int gc_batched_transpose(int64_t nn, const int64_t* desc, const double* in, doub
     if (nn <= 0) return GC_OK;
     k_batched_transpose<<<(unsigned)nn, 256, 0, (cudaStream_t)stream>>>(desc, in, out);
     GC_CHECK_LAUNCH("gc_batched_transpose");
+    return GC_OK;
+}
+
+int gc_host_norm3(const double* v, int64_t n, double* out, int mode) {
+    // host helper: Euclidean norms of n 3-vectors with a chosen rounding
+    // sequence (mode 0: sqrt(fma(z,z,fma(y,y,x*x))), the OpenBLAS ddot tail;
+    // mode 1: sqrt((x*x + y*y) + z*z) without contraction)
+    if (n < 0 || (mode != 0 && mode != 1)) {
+        set_error(GC_ERR_CONFIG, "gc_host_norm3: bad arguments");
+        return GC_ERR_CONFIG;
+    }
+    for (int64_t i = 0; i < n; ++i) {
+        const double x = v[3 * i], y = v[3 * i + 1], z = v[3 * i + 2];
+        volatile double xx = x * x;
+        double s;
+        if (mode == 0) {
+            s = std::fma(z, z, std::fma(y, y, (double)xx));
+        } else {
+            volatile double yy = y * y, zz = z * z;
+            volatile double t = (double)xx + (double)yy;
+            s = (double)t + (double)zz;
+        }
+        out[i] = std::sqrt(s);
+    }
     return GC_OK;
 }
 

@@ -238,14 +238,16 @@ def chart_pack(mesh):
     nodes[:, :3] = corners
     for slot, (i, j) in zip((3, 4, 5), ((0, 1), (1, 2), (2, 0))):
         nodes[:, slot] = 0.5 * (nodes[:, i] + nodes[:, j])
+    # plane charts: the normal is constant, so only the partials at node 0
+    # are needed (same sequential sum over the 6 nodes as the reference's
+    # all-node einsum, bit for bit)
     grads = _shape_gradients_at_nodes()
-    du = np.einsum("ma,tac->tmc", grads[:, :, 0], nodes)
-    dv = np.einsum("ma,tac->tmc", grads[:, :, 1], nodes)
-    normals = np.cross(du, dv)
-    gram = np.linalg.norm(normals[:, 0], axis=1)
-    normals = np.repeat(normals[:, :1], 6, axis=1)
-    mesh._pack = ChartPack(np.ascontiguousarray(nodes),
-                           np.ascontiguousarray(normals), gram, False)
+    du = np.einsum("a,tac->tc", grads[0, :, 0], nodes)
+    dv = np.einsum("a,tac->tc", grads[0, :, 1], nodes)
+    n0 = np.cross(du, dv)
+    gram = np.linalg.norm(n0, axis=1)
+    normals = np.broadcast_to(n0[:, None, :], (mesh.nt, 6, 3))
+    mesh._pack = ChartPack(np.ascontiguousarray(nodes), normals, gram, False)
     return mesh._pack
 
 

@@ -52,7 +52,9 @@ _SIGNATURES = {
     "gc_scatter": [c_p, c_p, c_i64, c_p, c_p],
     "gc_segmv": [c_i64, c_p, c_p, c_p, c_p, c_p, c_p, c_p, ctypes.c_int, c_i64, c_p],
     "gc_panelmv": [c_i64, c_p, c_p, c_p, c_p, c_p, c_p, c_p, c_p, c_i64, c_p, c_p],
-    "gc_h2mv_persistent": [c_p, c_p, c_i64, c_p, c_p, c_i64, c_i64, ctypes.POINTER(c_p),
+    "gc_h2mv_persistent": [c_p, c_p, c_i64, ctypes.c_int32, c_p, ctypes.c_int32,
+                           ctypes.POINTER(ctypes.c_int32),
+                           c_p, c_p, c_i64, c_i64, ctypes.POINTER(c_p),
                            ctypes.POINTER(c_p), c_p, ctypes.c_int32, ctypes.c_int32, c_p,
                            ctypes.c_int32, c_p],
     "gc_h2mv_grid": [ctypes.c_int32, ctypes.POINTER(ctypes.c_int32)],

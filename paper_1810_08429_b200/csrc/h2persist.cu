@@ -36,7 +36,8 @@ namespace gcb {
 constexpr int PM_THREADS = 256;
 constexpr int PM_UNROLL = 16;
 constexpr int PM_NONE = 127;
-constexpr int PM_TICKET = 126;   // sync slot of the work ticket
+constexpr int PM_SEG0 = 128;     // sync slots 128..: per-segment take counters
+constexpr int PM_MAXSEG = 120;
 
 struct MvProgram {
     const int64_t* items;
@@ -49,6 +50,10 @@ struct MvProgram {
     const double* mat[4];       // panel matrices
     double* buf[8];             // 0 x, 1 xt, 2 x-hat, 3 y-hat (coupling), 4 y-hat, 5 yt (near), 6 y, 7 scratch
     unsigned int* sync;         // [0] start barrier, [1..] dataflow counters; zeroed before launch
+    int32_t nseg;               // item segments:
+    const int32_t* seg;         // [dev] (nseg, 3): begin, end, unused
+    int32_t nlists;             // segment lists in priority order (readiness
+    int32_t list_end[8];        // monotone along each list): [end[l-1], end[l])
     long long* timing;          // optional: per item (wait start, wait end, done)
 };
 
@@ -56,6 +61,19 @@ __device__ __forceinline__ long long global_ns() {
     long long t;
     asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
     return t;
+}
+
+__device__ __forceinline__ bool counter_reached(const unsigned int* ctr, unsigned int target) {
+    cuda::atomic_ref<unsigned int, cuda::thread_scope_device> a(*const_cast<unsigned int*>(ctr));
+    return a.load(cuda::memory_order_acquire) >= target;
+}
+
+template <typename Prog>
+__device__ __forceinline__ bool deps_ready(const Prog& P, int64_t w7) {
+    const unsigned int w1 = (unsigned int)(w7 & 0xffffffff), w2 = (unsigned int)(w7 >> 32);
+    if ((w1 >> 24) != PM_NONE && !counter_reached(P.sync + 1 + (w1 >> 24), w1 & 0xffffff)) return false;
+    if ((w2 >> 24) != PM_NONE && !counter_reached(P.sync + 1 + (w2 >> 24), w2 & 0xffffff)) return false;
+    return true;
 }
 
 __device__ __forceinline__ void wait_counter(unsigned int* ctr, unsigned int target) {
@@ -215,17 +233,54 @@ __global__ void __launch_bounds__(PM_THREADS, 4) k_h2mv_persistent(MvProgram P) 
         __syncthreads();
     }
     if (P.timing && blockIdx.x == 0 && threadIdx.x == 0) P.timing[3 * P.nitems] = global_ns();
-    // dynamic walk: tickets hand out items in priority order; every item's
-    // dependencies have smaller indices and were handed out earlier to
-    // co-resident CTAs, so waiting cannot deadlock
-    __shared__ long long s_ticket;
-    unsigned int* ticket = P.sync + 1 + PM_TICKET;
+    // Scheduler.  Items form segments (runs with one shared dependency) in
+    // priority order: transform chains, coupling by deadline, filler.
+    // Thread 0 takes from the first segment that is both non-exhausted and
+    // ready, with one atomicAdd on that segment's counter (an overshoot just
+    // means exhausted), so a taken item never waits, CTAs never block one
+    // another and the walk is deadlock-free for any dependency DAG.
+    __shared__ long long s_taken;
+    __shared__ int s_cur[8];                 // per list: first non-exhausted segment
+    __shared__ unsigned char s_ready[PM_MAXSEG];
+    if (threadIdx.x < 8) s_cur[threadIdx.x] = threadIdx.x ? P.list_end[threadIdx.x - 1] : 0;
+    for (int q = threadIdx.x; q < PM_MAXSEG; q += PM_THREADS) s_ready[q] = 0;
+    __syncthreads();
     for (;;) {
-        if (threadIdx.x == 0) s_ticket = (long long)atomicAdd(ticket, 1u);
+        if (threadIdx.x == 0) {
+            long long taken = -1;
+            unsigned int spins = 0;
+            for (;;) {
+                bool left = false;
+                for (int l = 0; l < P.nlists && taken < 0; ++l) {
+                    int q = s_cur[l];
+                    while (q < P.list_end[l]) {
+                        const int b = P.seg[3 * q], e = P.seg[3 * q + 1];
+                        unsigned int* ctr = P.sync + 1 + PM_SEG0 + q;
+                        cuda::atomic_ref<unsigned int, cuda::thread_scope_device> a(*ctr);
+                        if (b + (int)a.load(cuda::memory_order_relaxed) >= e) { s_cur[l] = ++q; continue; }
+                        left = true;
+                        if (!s_ready[q]) {
+                            // readiness is monotone along a list: stop at the
+                            // first segment that is not ready yet
+                            if (!deps_ready(P, P.items[8 * (int64_t)b + 7])) break;
+                            s_ready[q] = 1;
+                        }
+                        const unsigned int k = a.fetch_add(1u, cuda::memory_order_relaxed);
+                        if (b + (int)k < e) { taken = b + k; break; }
+                        s_cur[l] = ++q;
+                    }
+                }
+                if (taken >= 0 || !left) break;
+                __nanosleep(spins < 16 ? 32 : 128);
+                ++spins;
+            }
+            __threadfence();
+            s_taken = taken;
+        }
         __syncthreads();
-        const int64_t i = s_ticket;
+        const long long i = s_taken;
         __syncthreads();
-        if (i >= P.nitems) break;
+        if (i < 0) break;
         const int64_t* it = P.items + 8 * i;
         long long* tm = P.timing ? P.timing + 3 * i : nullptr;
         if ((it[0] & 15) == 2)
@@ -240,6 +295,8 @@ __global__ void __launch_bounds__(PM_THREADS, 4) k_h2mv_persistent(MvProgram P) 
 using namespace gcb;
 
 extern "C" int gc_h2mv_persistent(const int64_t* items, const int32_t* xidx, int64_t nitems,
+                                  int32_t nseg, const int32_t* seg, int32_t nlists,
+                                  const int32_t* list_end,
                                   const int64_t* perm_in, const int64_t* perm_out, int64_t n_in,
                                   int64_t zero_len, const double* const* mats, double* const* bufs,
                                   unsigned int* sync, int32_t nsync, int32_t grid,
@@ -248,6 +305,13 @@ extern "C" int gc_h2mv_persistent(const int64_t* items, const int32_t* xidx, int
     P.items = items;
     P.xidx = xidx;
     P.nitems = nitems;
+    if (nseg < 1 || nseg > PM_MAXSEG) { set_error(GC_ERR_CONFIG, "1..%d item segments", PM_MAXSEG); return GC_ERR_CONFIG; }
+    if (nsync < 1 + PM_SEG0 + nseg) { set_error(GC_ERR_CONFIG, "sync array too small"); return GC_ERR_CONFIG; }
+    P.nseg = nseg;
+    P.seg = seg;
+    if (nlists < 1 || nlists > 8) { set_error(GC_ERR_CONFIG, "1..8 segment lists"); return GC_ERR_CONFIG; }
+    P.nlists = nlists;
+    for (int l = 0; l < 8; ++l) P.list_end[l] = l < nlists ? list_end[l] : nseg;
     P.perm_in = perm_in;
     P.perm_out = perm_out;
     P.n_in = n_in;

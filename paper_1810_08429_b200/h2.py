@@ -193,7 +193,7 @@ class MatvecPlan:
         return len(self.launches) + 2
 
 
-PERSISTENT = False      # PersistentPlan (one cooperative launch) is experimental
+PERSISTENT = False      # PersistentPlan: experimental, slower at C2
 
 
 def plan(h, trans=False, graph=True):
@@ -637,7 +637,8 @@ class PersistentPlan(PanelPlan):
     with a single writer per entry."""
 
     FWD, BWD, CPLC, CPLR, NEAR, BWD_ALL, CPL = 0, 20, 40, 60, 80, 81, 82
-    NSYNC = 1 + 128                       # slot 1+126 is the work ticket
+    NSYNC = 1 + 128 + 120                 # dependency counters, then segment counters
+    CHUNK_ELEMS = 4096                    # coupling row chunks (~32 KB of matrix)
 
     def _phase(self, name, panels, A0, A1, in0, in1, out):
         rec = _PanelRec()
@@ -727,7 +728,7 @@ class PersistentPlan(PanelPlan):
             a_off, K, T, rows, out_off, _ = coup[0].panels
             a_off, K, T, out_off = (np.asarray(v, np.int64) for v in (a_off, K, T, out_off))
             xs = xi_of(rows)
-            rpi = np.maximum(1, -(-8192 // np.maximum(T, 1)))
+            rpi = np.maximum(1, -(-self.CHUNK_ELEMS // np.maximum(T, 1)))
             nch = np.maximum(1, -(-K // rpi))
             for lev in range(H):
                 sel = np.flatnonzero(levs == lev)
@@ -740,7 +741,7 @@ class PersistentPlan(PanelPlan):
                                _wait(self.FWD + lev, nF[lev]), _wait())
                     it1[:, 6] = (it1[:, 6] & 0xffffffff) | ((self.CPLR + rlev[one]) << 32) | (np.int64(self.CPL) << 40)
                     C[lev].append(it1)
-                    nres[rlev[one]] += 1
+                    np.add.at(nres, rlev[one], 1)
                     nCres += len(it1)
                 many = sel[nch[sel] > 1]
                 if many.size:
@@ -809,14 +810,14 @@ class PersistentPlan(PanelPlan):
         rows = [o + np.arange(k) for o, k in zip(np.where(has, rs.coef_off[leaves], 0), K)]
         xs = xi_of(rows)
         in_sel = np.where(roots[leaves], B_YC, B_YH)
-        if uniform and not roots[leaves].any():
-            w1, w2 = (_wait(self.BWD_ALL, sum(nB)) if nB else _wait()), _wait(self.NEAR, nN)
-        else:   # conservative: every coupling result and every near item
-            w1 = _wait(self.BWD_ALL, sum(nB)) if nB else _wait()
-            w2 = _wait(self.CPL, nC + nN)
-            near[:, 6] = (near[:, 6] & ~(np.int64(0xff) << 40)) | (np.int64(self.CPL) << 40)
+        # a leaf below a basis parent waits for the backward sweep; a leaf
+        # that is itself a basis root only for the coupling results
+        w1 = np.where(roots[leaves], _wait(self.CPL, nC),
+                      _wait(self.BWD_ALL, sum(nB)) if nB else _wait(self.CPL, nC))
+        w2 = _wait(self.NEAR, nN)
         fin = make(3, 3, in_sel, B_Y, B_YT, np.where(has, rs.v_off[leaves], 0), xs, rf.start[leaves],
                    size_r[leaves], K, 1 << 30, _NONE, _NONE, w1, w2)
+        fin = fin[np.argsort(fin[:, 7], kind="stable")]
         # ---- walk order: the transform chains interleaved with ready filler
         # (near field during the forward sweep, mid-level coupling after the
         # level it waits for, the deepest coupling level during the backward
@@ -830,42 +831,39 @@ class PersistentPlan(PanelPlan):
 
         Cl = [cat(C[l]) for l in range(H)] if H else []
         Rl = [Rlev.get(l, np.zeros((0, 8), np.int64)) for l in range(H)]
-        items, names = [], []
-
-        def add(name, a):
-            if len(a):
-                items.append(a)
-                names.append(name)
-
-        add("fwd0", F[0])
-        nsplit = split(near, 2)
-        if H > 1:
-            add("near", nsplit[0])
-            add("fwd1", F[1])
-            add("near", nsplit[1])
-        else:
-            add("near", near)
-        for lev in range(2, H):
-            add("fwd%d" % lev, F[lev])
-            add("cpl%d" % (lev - 1), Cl[lev - 1])
-            add("reduce", Rl[lev - 1])
-        if H > 1:
-            add("cpl%d" % (H - 1), Cl[H - 1])
-            add("reduce", Rl[H - 1])
-        deep = Cl[0] if H else np.zeros((0, 8), np.int64)
-        if uniform and len(Bl) > 1:
-            parts = split(deep, len(Bl) - 1)
-            for k, it in enumerate(Bl[:-1]):
-                add("bwd%d" % k, it)
-                add("cpl0", parts[k])
-            add("reduce", Rl[0] if H else np.zeros((0, 8), np.int64))
-            add("bwd%d" % (len(Bl) - 1), Bl[-1])
-        else:
-            add("cpl0", deep)
-            add("reduce", Rl[0] if H else np.zeros((0, 8), np.int64))
-            for k, it in enumerate(Bl):
-                add("bwd%d" % k, it)
-        add("final", fin)
+        # priority lists: the transform chains; coupling by deadline (the
+        # top levels are needed first by the backward sweep); the deep
+        # coupling levels (ready early, needed last); the near field
+        # readiness is monotone along each list (the scheduler stops at the
+        # first segment of a list that is not ready)
+        lists = [
+            [("fwd%d" % l, F[l]) for l in range(H)] + [("bwd%d" % k, it) for k, it in enumerate(Bl)]
+            + [("final", fin)],
+            [("reduce", Rl[l]) for l in range(H)],
+            [("cpl%d" % l, Cl[l]) for l in range(H)],
+            [("near", near)],
+        ]
+        items, names, list_end = [], [], []
+        for lst in lists:
+            for nm, it in lst:
+                if not len(it):
+                    continue
+                # segments: runs of items with one shared dependency word
+                w = it[:, 7]
+                cuts = np.flatnonzero(np.r_[True, w[1:] != w[:-1], True])
+                for a_, b_ in zip(cuts[:-1], cuts[1:]):
+                    items.append(it[a_:b_])
+                    names.append(nm)
+            list_end.append(len(items))
+        if len(items) > 120:
+            raise ConfigError("too many scheduling segments (%d)" % len(items))
+        ends = np.cumsum([len(i) for i in items])
+        segs = np.stack([ends - np.array([len(i) for i in items]), ends, np.zeros(len(items), np.int64)], 1)
+        self.nseg = len(items)
+        self.seg_dev = to_dev(segs.astype(np.int32), self.dev)
+        import ctypes
+        self.nlists = len(list_end)
+        self._list_end = (ctypes.c_int32 * 8)(*(list_end + [list_end[-1]] * (8 - len(list_end))))
         self.segments = [(nm, len(i)) for nm, i in zip(names, items)]
         allit = np.concatenate([i for i in items if len(i)]).astype(np.int64)
         self.nitems = len(allit)
@@ -891,7 +889,7 @@ class PersistentPlan(PanelPlan):
         if phase_events is not None:
             phase_events[0].record()
         _native.call("gc_h2mv_persistent", ptr(self.items), ptr(self.xidx_all), self.nitems,
-                     ptr(self.perm_in), ptr(self.perm_out), self.n_in, self.zero_len,
+                     self.nseg, ptr(self.seg_dev), self.nlists, self._list_end, ptr(self.perm_in), ptr(self.perm_out), self.n_in, self.zero_len,
                      self._mats, self._bufs, ptr(self.sync), self.NSYNC, self.grid,
                      ptr(self.timing) if self.timing is not None else None, self.max_rows, st)
         if phase_events is not None:

@@ -209,6 +209,14 @@ int gc_h2mv_persistent(const int64_t* items, const int32_t* xidx, int64_t nitems
                        int64_t zero_len, const double* const* mats, double* const* bufs,
                        unsigned int* sync, int32_t nsync, int32_t grid, long long* timing,
                        int32_t max_rows, void* stream);
+/* Run items [first, first+count) of a gc_h2mv_persistent program as one
+ * plain launch (one CTA per item, dependencies assumed satisfied by
+ * stream order; signals go to sync).  The multi-launch matvec issues one
+ * such launch per phase inside a CUDA graph. */
+int gc_run_items(const int64_t* items, int64_t first, int64_t count, const int32_t* xidx,
+                 const double* const* mats, double* const* bufs, unsigned int* sync,
+                 int32_t max_rows, const int64_t* perm_out, void* stream);
+
 /* Largest co-resident grid of gc_h2mv_persistent (max_rows: longest panel). */
 int gc_h2mv_grid(int32_t max_rows, int32_t* grid);
 

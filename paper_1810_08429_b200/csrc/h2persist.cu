@@ -28,6 +28,7 @@
 //   [7] wait1 | wait2 << 32, wait = counter << 24 | target   (counter 127: none)
 //   s[t] = sum_{r < nrows} A[a_off + r*T + t] * in[xidx[xi_off + r]],  t in [c0, c0+tw)
 #include <cuda/atomic>
+#include <string.h>
 
 #include "common.cuh"
 
@@ -115,9 +116,9 @@ __device__ void run_item(const MvProgram& P, const int64_t* it, double* xs, doub
         const int r = threadIdx.x + j * PM_THREADS;
         myidx[j] = r < nrows ? __ldg(xi + r) : 0;
     }
-    // dependencies
+    // dependencies (none when launched phase by phase: P.sync == nullptr)
     if (tm && threadIdx.x == 0) tm[0] = global_ns();
-    if (threadIdx.x == 0) {
+    if (threadIdx.x == 0 && P.sync) {
         const unsigned int w1 = (unsigned int)(w7 & 0xffffffff), w2 = (unsigned int)(w7 >> 32);
         if ((w1 >> 24) != PM_NONE) wait_counter(P.sync + 1 + (w1 >> 24), w1 & 0xffffff);
         if ((w2 >> 24) != PM_NONE) wait_counter(P.sync + 1 + (w2 >> 24), w2 & 0xffffff);
@@ -172,7 +173,7 @@ __device__ void run_item(const MvProgram& P, const int64_t* it, double* xs, doub
         __syncthreads();
     }
     // signals (after every thread's stores: barrier above, then a fence)
-    if (threadIdx.x == 0) {
+    if (threadIdx.x == 0 && P.sync) {
         const int s1 = (int)((w6 >> 32) & 0xff), s2 = (int)((w6 >> 40) & 0xff);
         __threadfence();
         if (s1 != PM_NONE) atomicAdd(P.sync + 1 + s1, 1u);
@@ -188,7 +189,7 @@ __device__ void reduce_item(const MvProgram& P, const int64_t* it, long long* tm
     const int out_sel = (int)((head >> 12) & 15);
     const int64_t so = it[1], out_off = it[3], T = it[4], nch = it[5];
     const int64_t w6 = it[6], w7 = it[7];
-    if (threadIdx.x == 0) {
+    if (threadIdx.x == 0 && P.sync) {
         if (tm) tm[0] = global_ns();
         const unsigned int w1 = (unsigned int)(w7 & 0xffffffff), w2 = (unsigned int)(w7 >> 32);
         if ((w1 >> 24) != PM_NONE) wait_counter(P.sync + 1 + (w1 >> 24), w1 & 0xffffff);
@@ -204,7 +205,7 @@ __device__ void reduce_item(const MvProgram& P, const int64_t* it, long long* tm
         P.buf[out_sel][out_off + t] = v;
     }
     __syncthreads();
-    if (threadIdx.x == 0) {
+    if (threadIdx.x == 0 && P.sync) {
         const int s1 = (int)((w6 >> 32) & 0xff), s2 = (int)((w6 >> 40) & 0xff);
         __threadfence();
         if (s1 != PM_NONE) atomicAdd(P.sync + 1 + s1, 1u);
@@ -354,5 +355,47 @@ extern "C" int gc_h2mv_grid(int32_t max_rows, int32_t* grid_out) {
     cudaGetDevice(&dev);
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
     *grid_out = max_blocks * sms;
+    return GC_OK;
+}
+
+// ---------------------------------------------------------------------------
+// The same work items launched phase by phase (one CTA per item, no
+// scheduling): the multi-launch formulation used inside a CUDA graph.
+namespace gcb {
+
+__global__ void __launch_bounds__(PM_THREADS) k_run_items(MvProgram P, int64_t first) {
+    extern __shared__ double xs[];
+    __shared__ double red[PM_THREADS];
+    const int64_t* it = P.items + 8 * (first + blockIdx.x);
+    if ((it[0] & 15) == 2)
+        reduce_item(P, it, nullptr);
+    else
+        run_item(P, it, xs, red, nullptr);
+}
+
+}  // namespace gcb
+
+extern "C" int gc_run_items(const int64_t* items, int64_t first, int64_t count, const int32_t* xidx,
+                            const double* const* mats, double* const* bufs, unsigned int* sync,
+                            int32_t max_rows, const int64_t* perm_out, void* stream) {
+    using namespace gcb;
+    if (count <= 0) return GC_OK;
+    if (count > 0x7fffffffLL) { set_error(GC_ERR_CONFIG, "too many items"); return GC_ERR_CONFIG; }
+    MvProgram P;
+    memset(&P, 0, sizeof(P));
+    P.items = items;
+    P.xidx = xidx;
+    P.nitems = first + count;
+    P.perm_out = perm_out;
+    for (int i = 0; i < 4; ++i) P.mat[i] = mats[i];
+    for (int i = 0; i < 8; ++i) P.buf[i] = bufs[i];
+    P.sync = nullptr;   // stream order replaces the dataflow counters
+    (void)sync;
+    const size_t smem = (size_t)(max_rows > 0 ? max_rows : 1) * sizeof(double);
+    if (smem > 160 * 1024) { set_error(GC_ERR_CONFIG, "panel with %d rows is too long", max_rows); return GC_ERR_CONFIG; }
+    cudaError_t e = cudaFuncSetAttribute(k_run_items, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    if (e != cudaSuccess) return cuda_status(e, "gc_run_items smem attribute");
+    k_run_items<<<(unsigned)count, PM_THREADS, smem, (cudaStream_t)stream>>>(P, first);
+    GC_CHECK_LAUNCH("k_run_items");
     return GC_OK;
 }

@@ -898,3 +898,65 @@ class PersistentPlan(PanelPlan):
     @property
     def num_kernels(self):
         return 1
+
+
+class LaunchPlan(PersistentPlan):
+    """The persistent plan's work items launched phase by phase (one CTA per
+    item) inside a CUDA graph: gather, forward levels, coupling chunks,
+    coupling reductions, backward levels, final leaf stage fused with the
+    output permutation; the near field runs on a side stream.  Transform
+    levels are split by output columns (no partial sums, no reduce
+    launches)."""
+
+    def __init__(self, h):
+        super().__init__(h)
+        # contiguous item ranges per phase, in stream order
+        ranges, k = {}, 0
+        for name, cnt in self.segments:
+            key = "fwd" if name.startswith("fwd") else "bwd" if name.startswith("bwd") else \
+                "cpl" if name.startswith("cpl") else name
+            lvl = name[3:] if key in ("fwd", "bwd") else ""
+            ranges.setdefault((key, lvl), []).append((k, cnt))
+            k += cnt
+        self.ranges = ranges
+
+        def span(key):
+            parts = [r for (kk, _), rr in ranges.items() if kk == key for r in rr]
+            return parts
+
+        fw = sorted([(int(l), r) for (kk, l), r in ranges.items() if kk == "fwd"])
+        bw = sorted([(int(l), r) for (kk, l), r in ranges.items() if kk == "bwd"])
+        self.order = ([("fwd", r) for _, r in fw] + [("cpl", span("cpl")), ("reduce", span("reduce"))]
+                      + [("bwd", r) for _, r in bw] + [("final", span("final"))])
+        self.near_ranges = span("near")
+
+    def _runs(self, parts, st):
+        for first, count in parts:
+            _native.call("gc_run_items", ptr(self.items), first, count, ptr(self.xidx_all),
+                         self._mats, self._bufs, ptr(self.sync), self.max_rows, ptr(self.perm_out), st)
+
+    def _body(self, phase_events=None, phase="coupling"):
+        main = torch.cuda.current_stream()
+        st = stream_handle()
+        _native.call("gc_gather", ptr(self.x), ptr(self.perm_in), self.n_in, ptr(self.xt), st)
+        self.yc.zero_()
+        fork = torch.cuda.Event()
+        fork.record(main)
+        with torch.cuda.stream(self.side):
+            self.side.wait_event(fork)
+            self._runs(self.near_ranges, stream_handle())
+            join = torch.cuda.Event()
+            join.record(self.side)
+        for name, parts in self.order:
+            if name == "final":
+                main.wait_event(join)
+            timed = phase_events is not None and name == phase
+            if timed:
+                phase_events[0].record(main)
+            self._runs(parts, st)
+            if timed:
+                phase_events[1].record(main)
+
+    @property
+    def num_kernels(self):
+        return 2 + sum(len(p) for _, p in self.order) + len(self.near_ranges)

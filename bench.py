@@ -221,6 +221,17 @@ def run_reference(args):
 # --------------------------------------------------------------------------
 # native arm
 
+def _traffic(kernel):
+    """dram__bytes_read.sum + dram__bytes_write.sum per launch of the
+    roofline kernel, from the committed ncu --set full summary
+    (profiles/traffic.json, written by scripts/ncu_traffic.py)."""
+    path = os.path.join(ROOT, "profiles", "traffic.json")
+    try:
+        return json.load(open(path)).get(kernel)
+    except (OSError, ValueError):
+        return None
+
+
 def dfma_peak(torch, _native, ptr):
     """Measured FP64 DFMA throughput (TFLOP/s): 148*8 CTAs x 256 threads x
     8 chains, timed with CUDA events (best of 5)."""
@@ -376,9 +387,9 @@ def run_native(args):
                                   "achieved": round(q["nearfield"]["tflops"], 3), "peak": round(peak64, 3),
                                   "unit": "TFLOP/s", "frac": round(q["nearfield"]["tflops"] / peak64, 4),
                                   "peak_source": "measured in this run: gc_dfma_probe DFMA loop (no FP64 entry in MEASURED_PEAKS.json)"}},
-        "roofline": {"bound": "hbm", "kernel": "k_segmv (coupling phase)",
+        "roofline": {"bound": "hbm", "kernel": "k_panelmv (coupling phase of the matvec)",
                      "achieved": round(coup_bytes / coup_s / 1e9, 1), "peak": hbm_peak, "unit": "GB/s",
-                     "frac": round(coup_bytes / coup_s / 1e9 / hbm_peak, 4), "traffic": None,
+                     "frac": round(coup_bytes / coup_s / 1e9 / hbm_peak, 4), "traffic": _traffic("coupling"),
                      "algorithmic_bytes_per_launch": int(coup_bytes), "avg_launch_s": coup_s,
                      "share_of_step": round(coup_s / mv_s, 3),
                      "peak_source": "MEASURED_PEAKS.json hbm_gbs" if peaks else "fallback 6650 GB/s"},

@@ -132,7 +132,8 @@ int gc_green_box_rules(int m, const double* g01, const double* w01, int64_t nn,
 /* Green quadrature factors for a batch of cluster-basis nodes: replaces
  * assembly.green_row_factor / green_col_factor (assembly.py:420-455).
  *   side 0: A = [sqrt(w) g, -d sqrt(w) h];  side 1: B = [sqrt(w) h, sqrt(w)/d g]
- *   desc [dev] (nn,4) int64: rows_off, R, out_off, rule index;
+ *   desc [dev] (nn,5) int64: rows_off, R, out_off, rule index, side;
+ *   side -1 takes the side per node from desc (one launch for both bases);
  *   dtau [dev] (nn,) box diameters (host values); z/sq/nz: rules as above;
  *   rows [dev] dof (triangle) ids; out [dev] row-major (R, 2K) per node.
  * flags bit 0 is set when an expansion point touches the surface

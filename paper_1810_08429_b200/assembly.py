@@ -116,19 +116,25 @@ def assemble_galerkin_block(kind, mesh, basis, rows, cols, orders=(3, 5), capaci
 # --------------------------------------------------------------------------
 # Green factors
 
-def green_factors_device(dmesh, side, K, rows, desc, dtau, z, sq, nz, total_rows, device):
+def green_factors_device(dmesh, side, K, rows, desc, dtau, z, sq, nz, total_rows, device,
+                         check_flags=True):
     """Factor matrices of a batch of nodes (device buffer, row-major per
     node).  Raises GeometryError if an expansion point touches the surface."""
     out = empty(total_rows * 2 * K, device)
     flags = torch.zeros(1, dtype=torch.int32, device=device)
     with torch.cuda.device(device):
-        _native.call("gc_green_factor", dmesh.geom, 0 if side == "row" else 1, K, len(desc),
+        _native.call("gc_green_factor", dmesh.geom, {"row": 0, "col": 1}.get(side, -1), K, desc.numel() // 5,
                      ptr(desc), ptr(dtau), ptr(z), ptr(sq), ptr(nz), ptr(rows), ptr(out),
                      ptr(flags), stream_handle())
-    if int(flags.item()) & 1:
+    if check_flags:
+        touch_check(flags)
+    return out, flags
+
+
+def touch_check(flags):
+    if int(flags.max().item()) & 1:
         raise GeometryError("expansion point touches the surface; "
                             "enlarge delta or the cluster box")
-    return out
 
 
 def _single_factor(side, cluster, rule, mesh, basis, orders, d_tau, device=None):
@@ -140,10 +146,10 @@ def _single_factor(side, cluster, rule, mesh, basis, orders, d_tau, device=None)
     z = to_dev(np.asarray(rule.points, dtype=np.float64), dev)
     sq = to_dev(np.sqrt(np.asarray(rule.weights, dtype=np.float64)), dev)
     nz = to_dev(np.asarray(rule.normals, dtype=np.float64), dev)
-    desc = to_dev(np.array([[0, len(rows), 0, 0]], dtype=np.int64), dev)
+    desc = to_dev(np.array([[0, len(rows), 0, 0, 0]], dtype=np.int64), dev)
     dtau = to_dev(np.array([d_tau]), dev)
-    out = green_factors_device(dmesh, side, K, to_dev(rows, dev), desc, dtau, z, sq, nz,
-                               len(rows), dev)
+    out, _ = green_factors_device(dmesh, side, K, to_dev(rows, dev), desc, dtau, z, sq, nz,
+                                  len(rows), dev)
     return out.cpu().numpy().reshape(len(rows), 2 * K)
 
 

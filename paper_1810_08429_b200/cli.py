@@ -63,12 +63,10 @@ def build_h2_operator(mesh, cfg, kind="slp", capacity=None, threads=None, device
     t2 = time.perf_counter()
     orders = (cfg.q_reg, cfg.q_sing)
     rmarks, cmarks = gca.coupling_marks(btree)
-    rb = gca.build_cluster_basis(tree, mesh, cfg.basis, cfg.m, cfg.delta_factor, cfg.eps,
-                                 side="row", orders=orders, marks=rmarks, device=device)
-    t3 = time.perf_counter()
-    cb = gca.build_cluster_basis(tree, mesh, cfg.basis, cfg.m, cfg.delta_factor, cfg.eps,
-                                 side="col", orders=orders, marks=cmarks, device=device)
-    t4 = time.perf_counter()
+    # row and column bases in shared per-level launches (gca.build_cluster_bases)
+    rb, cb = gca.build_cluster_bases(tree, mesh, cfg.basis, cfg.m, cfg.delta_factor, cfg.eps,
+                                     [("row", rmarks), ("col", cmarks)], orders, device)
+    t3 = t4 = time.perf_counter()
     hm = gca.build_h2(btree, rb, cb, mesh, kind=kind, basis=cfg.basis, disc=cfg.disc,
                       orders=orders, device=device)
     t5 = time.perf_counter()

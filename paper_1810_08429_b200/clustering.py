@@ -249,9 +249,10 @@ def build_cluster_tree(mesh, basis_kind="constant", leaf_size=32):
     # one padding row so that reduceat may address index n
     # lo/hi/points in current permutation order, plus one padding row so
     # that reduceat may address index n; permuted in place with perm
-    lo_p = np.concatenate([lo, lo[:1]])
-    hi_p = np.concatenate([hi, hi[:1]])
-    pts_p = points.copy()
+    # one (n+1, 9) array [lo | hi | point] permuted as a whole each level
+    pack = np.concatenate([np.concatenate([lo, hi, points], axis=1),
+                           np.concatenate([lo[:1], hi[:1], points[:1]], axis=1)])
+    lo_p, hi_p, pts_p = pack[:, 0:3], pack[:, 3:6], pack[:, 6:9]
 
     # frontier of one tree depth: node ids with contiguous [start, stop)
     ids = np.array([0], dtype=np.int64)
@@ -276,12 +277,16 @@ def build_cluster_tree(mesh, basis_kind="constant", leaf_size=32):
         heads = np.cumsum(seg_len) - seg_len
         pos = np.arange(int(seg_len.sum())) + np.repeat(s_s - heads, seg_len)
         key = pts_p[pos, axis[seg_of]]
-        order = np.lexsort((key, seg_of))        # stable within each segment
+        if np.all(seg_len == seg_len[0]):
+            # equal segments (power-of-two trees): one row-wise stable sort
+            L = int(seg_len[0])
+            order = (np.argsort(key.reshape(-1, L), axis=1, kind="stable")
+                     + (np.arange(len(seg_len)) * L)[:, None]).ravel()
+        else:
+            order = np.lexsort((key, seg_of))    # stable within each segment
         src = pos[order]
         perm[pos] = perm[src]
-        lo_p[pos] = lo_p[src]
-        hi_p[pos] = hi_p[src]
-        pts_p[pos] = pts_p[src]
+        pack[pos] = np.take(pack, src, axis=0)
         half = seg_len // 2
         lid = ids_s + 1
         rid = ids_s + 1 + np.array([memo[int(h)] for h in half], dtype=np.int64)

@@ -62,8 +62,9 @@ __global__ void __launch_bounds__(GREEN_THREADS) k_green_factor(
     __shared__ double nn3[GREEN_MAX_K][3];
     __shared__ double sq[GREEN_MAX_K];
     const int node = blockIdx.x;
-    const int64_t rows_off = desc[4 * node], R = desc[4 * node + 1];
-    const int64_t out_off = desc[4 * node + 2], rule = desc[4 * node + 3];
+    const int64_t rows_off = desc[5 * node], R = desc[5 * node + 1];
+    const int64_t out_off = desc[5 * node + 2], rule = desc[5 * node + 3];
+    if (side < 0) side = (int)desc[5 * node + 4];      // per-node side
     const double d_tau = dtau[node];
     for (int k = threadIdx.x; k < K; k += blockDim.x) {
 #pragma unroll
@@ -137,7 +138,7 @@ extern "C" int gc_green_factor(const gc_geom* gp, int side, int64_t K, int64_t n
                                const double* sq, const double* nz, const int64_t* rows,
                                double* out, int32_t* flags, void* stream) {
     if (!gp) { set_error(GC_ERR_CONFIG, "null geometry"); return GC_ERR_CONFIG; }
-    if (side != 0 && side != 1) { set_error(GC_ERR_CONFIG, "side must be 0 (row) or 1 (col)"); return GC_ERR_CONFIG; }
+    if (side < -1 || side > 1) { set_error(GC_ERR_CONFIG, "side must be 0 (row), 1 (col) or -1 (per node)"); return GC_ERR_CONFIG; }
     if (K < 1 || K > GREEN_MAX_K) { set_error(GC_ERR_CONFIG, "rule size K=%lld outside [1, %d]", (long long)K, GREEN_MAX_K); return GC_ERR_CONFIG; }
     if (nn <= 0) return GC_OK;
     k_green_factor<<<(unsigned)nn, GREEN_THREADS, 0, (cudaStream_t)stream>>>(

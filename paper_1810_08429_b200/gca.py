@@ -27,7 +27,7 @@ from . import _native
 from .assembly import device_block_assembly, green_factors_device
 from .device import (DeviceMesh, DeviceRules, SingularQueue, check_mesh, empty, ptr,
                      require_device, stream_handle, to_dev, torch)
-from .errors import ConfigError
+from .errors import ConfigError, GeometryError
 from .quadrature import _gauss01
 
 __all__ = ["Interpolation", "aca_interpolation", "BasisNode", "ClusterBasis",
@@ -280,133 +280,183 @@ def build_cluster_basis(tree, mesh, basis, m, delta_factor=0.5, eps=1e-4, side="
         raise ConfigError("side must be 'row' or 'col', got %r" % (side,))
     if basis == "collocation" and side == "col":
         raise ConfigError("column factors integrate a Galerkin basis")
+    return build_cluster_bases(tree, mesh, basis, m, delta_factor, eps, [(side, marks)],
+                               orders, device, row_range)[0]
+
+
+class _Side:
+    """Per-basis state while several bases are built in shared launches."""
+
+    def __init__(self, tree, side, marks, row_range, W, dev):
+        flat = tree.flat
+        self.side = side
+        self.store = DeviceBasis(tree, side, dev)
+        mat, roots = _materialize(flat, marks)
+        if row_range is not None:
+            inside = (flat.start >= row_range[0]) & (flat.stop <= row_range[1])
+            crossing = mat & ~inside & (flat.start < row_range[1]) & (flat.stop > row_range[0])
+            if np.any(crossing & np.isin(np.arange(len(flat)), roots)):
+                raise ConfigError("a basis root straddles the shard boundary; shard at a "
+                                  "coarser tree level")
+            mat = mat & inside
+            roots = roots[inside[roots]]
+        self.mat, self.roots = mat, roots
+        self.store.materialized = mat
+        self.store.available = mat.copy()
+        size = flat.stop - flat.start
+        cap = int(np.minimum(size[mat], W).sum()) if mat.any() else 0
+        self.gpiv = np.empty(max(cap, 1), dtype=np.int64)
+        self.cursor = 0
+        self.v_parts = []        # (level tensor, start, stop)
+        self.v_base = 0
+
+
+def build_cluster_bases(tree, mesh, basis, m, delta_factor, eps, sides, orders=(3, 5),
+                        device=None, row_range=None):
+    """Several nested bases of one cluster tree (row and column side of the
+    H2 matrix) built together: per tree height one ``gc_green_box_rules``,
+    one ``gc_green_factor`` (side per node) and one ``gc_aca`` launch over
+    the nodes of every basis, then one device->host read of ranks, pivots
+    and the touch flags.  ``sides`` is a list of (side, marks)."""
     check_mesh(mesh, "slp", basis)
     if tree.index != 0:
         raise ConfigError("build_cluster_basis expects the root of a cluster tree")
     dev = require_device(device)
     t0 = time.perf_counter()
     flat = tree.flat
-    store = DeviceBasis(tree, side, dev)
-    mat, roots = _materialize(flat, marks)
-    if row_range is not None:
-        inside = (flat.start >= row_range[0]) & (flat.stop <= row_range[1])
-        crossing = mat & ~inside & (flat.start < row_range[1]) & (flat.stop > row_range[0])
-        if np.any(crossing & np.isin(np.arange(len(flat)), roots)):
-            raise ConfigError("a basis root straddles the shard boundary; shard at a "
-                              "coarser tree level")
-        mat = mat & inside
-        roots = roots[inside[roots]]
-    store.materialized = mat
-    store.available = mat.copy()
     dmesh = DeviceMesh.get(mesh, orders[0], dev)
     K = 6 * m * m
     W = 2 * K
     g01, w01 = _gauss01(m)
     d_g01, d_w01 = to_dev(g01, dev), to_dev(w01, dev)
     size = flat.stop - flat.start
-    cap = int(np.minimum(size[mat], W).sum()) if mat.any() else 0
-    gpiv = np.empty(max(cap, 1), dtype=np.int64)
-    cursor = 0
-    v_levels, v_base = [], 0
     perm = flat.perm
-    heights = np.unique(flat.height[mat])
+    S = [_Side(tree, side, marks, row_range, W, dev) for side, marks in sides]
+    heights = np.unique(np.concatenate([flat.height[s.mat] for s in S])) if S else []
     t_factor = t_aca = 0.0
     stream = stream_handle()
     for h in heights:
-        ids = np.flatnonzero(mat & (flat.height == h))
-        leaf = flat.is_leaf[ids]
-        lc, rc = flat.left[ids], flat.right[ids]
-        R = np.where(leaf, size[ids], store.rank[np.maximum(lc, 0)] + store.rank[np.maximum(rc, 0)])
-        # row lists: leaf dofs, or the children's pivots (left then right)
-        seg_start = np.where(leaf, flat.start[ids], 0)
-        rows_parts_starts, rows_parts_len, rows_parts_src = [], [], []
-        src = np.zeros(len(ids) * 2, dtype=np.int64)
-        # build gather indices into a combined source [perm | gpiv]
-        n_perm = len(perm)
-        st1 = np.where(leaf, flat.start[ids], n_perm + store.piv_off[np.maximum(lc, 0)])
-        ln1 = np.where(leaf, size[ids], store.rank[np.maximum(lc, 0)])
-        st2 = np.where(leaf, 0, n_perm + store.piv_off[np.maximum(rc, 0)])
-        ln2 = np.where(leaf, 0, store.rank[np.maximum(rc, 0)])
-        starts = np.stack([st1, st2], 1).ravel()
-        lens = np.stack([ln1, ln2], 1).ravel()
-        combined = np.concatenate([perm, gpiv[:cursor]])
-        rows_host = combined[_ranges(starts, lens)]
+        # ---- host: row lists of every node of this height, all bases
+        parts = []
+        for k, s in enumerate(S):
+            st = s.store
+            ids = np.flatnonzero(s.mat & (flat.height == h))
+            if not ids.size:
+                continue
+            leaf = flat.is_leaf[ids]
+            lc, rc = np.maximum(flat.left[ids], 0), np.maximum(flat.right[ids], 0)
+            R = np.where(leaf, size[ids], st.rank[lc] + st.rank[rc])
+            # leaf dofs, or the children's pivots (left then right), gathered
+            # from the combined source [perm | this basis' pivots]
+            n_perm = len(perm)
+            st1 = np.where(leaf, flat.start[ids], n_perm + st.piv_off[lc])
+            ln1 = np.where(leaf, size[ids], st.rank[lc])
+            st2 = np.where(leaf, 0, n_perm + st.piv_off[rc])
+            ln2 = np.where(leaf, 0, st.rank[rc])
+            combined = np.concatenate([perm, s.gpiv[:s.cursor]])
+            rows_host = combined[_ranges(np.stack([st1, st2], 1).ravel(),
+                                         np.stack([ln1, ln2], 1).ravel())]
+            st.child_row[lc[~leaf]] = 0
+            st.child_row[rc[~leaf]] = st.rank[flat.left[ids][~leaf]]
+            st.rows[ids] = R
+            parts.append((k, ids, R, rows_host))
+        if not parts:
+            continue
+        ids_all = np.concatenate([p[1] for p in parts])
+        R = np.concatenate([p[2] for p in parts])
+        rows_host = np.concatenate([p[3] for p in parts])
+        side_code = np.concatenate([np.full(len(p[1]), 0 if S[p[0]].side == "row" else 1)
+                                    for p in parts])
+        nn = len(ids_all)
         rows_off = _offsets(R)
         limit = np.minimum(R, W)
-        # child row offsets inside the parent's V-hat
-        store.child_row[np.maximum(lc, 0)[~leaf]] = 0
-        store.child_row[np.maximum(rc, 0)[~leaf]] = store.rank[lc[~leaf]]
-        store.rows[ids] = R
-        # Green factors (rule per node, host-computed delta and d_tau)
-        diam = flat.diam[ids]
-        box = np.concatenate([flat.lower[ids], flat.upper[ids], (delta_factor * diam)[:, None],
-                              diam[:, None]], axis=1)
-        nn = len(ids)
+        diam = flat.diam[ids_all]
+        box = np.concatenate([flat.lower[ids_all], flat.upper[ids_all],
+                              (delta_factor * diam)[:, None], diam[:, None]], axis=1)
+        vcap = R * limit
+        v_off = _offsets(vcap)
+        piv_off_l = _offsets(limit)
+        # one upload of every per-node table of this level
+        ints = to_dev(np.concatenate([np.stack([rows_off, R, rows_off * W, np.arange(nn), side_code], 1).ravel(),
+                                      np.stack([rows_off * W, R, piv_off_l, v_off], 1).ravel(),
+                                      rows_host]), dev)
+        fdesc, adesc, d_rows = ints[:5 * nn], ints[5 * nn:9 * nn], ints[9 * nn:]
+        dbl = to_dev(np.concatenate([box.ravel(), diam]), dev)
+        d_box, d_diam = dbl[:8 * nn], dbl[8 * nn:]
         tf = time.perf_counter()
-        d_box = to_dev(box, dev)
         z = empty(nn * K * 3, dev)
         sq = empty(nn * K, dev)
         nz = empty(nn * K * 3, dev)
         with torch.cuda.device(dev):
             _native.call("gc_green_box_rules", m, ptr(d_g01), ptr(d_w01), nn, ptr(d_box),
                          ptr(z), ptr(sq), ptr(nz), stream)
-        fdesc = to_dev(np.stack([rows_off, R, rows_off * W, np.arange(nn)], 1), dev)
-        d_rows = to_dev(rows_host, dev)
-        fac = green_factors_device(dmesh, side, K, d_rows, fdesc, to_dev(diam, dev), z, sq, nz,
-                                   int(R.sum()), dev)
+        fac, flags = green_factors_device(dmesh, "mixed", K, d_rows, fdesc, d_diam, z, sq, nz,
+                                          int(R.sum()), dev, check_flags=False)
         ta = time.perf_counter()
         t_factor += ta - tf
-        # batched ACA
-        vcap = R * limit
-        v_off = _offsets(vcap)
-        piv_off_l = _offsets(limit)
-        adesc = to_dev(np.stack([rows_off * W, R, piv_off_l, v_off], 1), dev)
         V = torch.zeros(max(int(vcap.sum()), 1), dtype=torch.float64, device=dev)
         U = empty(max(int(vcap.sum()), 1), dev)
-        d_piv = torch.zeros(max(int(limit.sum()), 1), dtype=torch.int64, device=dev)
-        d_rank = torch.zeros(nn, dtype=torch.int64, device=dev)
+        small = torch.zeros(max(int(limit.sum()), 1) + nn + 1, dtype=torch.int64, device=dev)
+        d_piv, d_rank = small[:max(int(limit.sum()), 1)], small[-nn - 1:-1]
         with torch.cuda.device(dev):
             _native.call("gc_aca", nn, ptr(adesc), W, float(eps), 0, ptr(fac), ptr(d_piv),
                          ptr(d_rank), ptr(V), ptr(U), int(R.max()), stream)
-        rank = d_rank.cpu().numpy()
-        piv_local = d_piv.cpu().numpy()
+            small[-1:].copy_(flags.to(torch.int64))
+        host = small.cpu().numpy()                 # the level's only sync
+        if host[-1] & 1:
+            raise GeometryError("expansion point touches the surface; "
+                                "enlarge delta or the cluster box")
+        rank, piv_local = host[-nn - 1:-1], host[:max(int(limit.sum()), 1)]
         t_aca += time.perf_counter() - ta
         del U, fac
-        # local -> global pivots, compact store
-        sel = _ranges(piv_off_l, rank)
-        node_of = np.repeat(np.arange(nn), rank)
-        glob = rows_host[rows_off[node_of] + piv_local[sel]]
-        gpiv[cursor:cursor + len(glob)] = glob
-        store.piv_off[ids] = cursor + _offsets(rank)
-        cursor += len(glob)
-        store.rank[ids] = rank
-        store.v_off[ids] = v_base + v_off
-        v_levels.append(V)
-        v_base += V.numel()
-    store.pivots_host = gpiv[:cursor].copy()
-    store.pivots = to_dev(store.pivots_host if cursor else np.zeros(1, np.int64), dev)
-    store.V = torch.cat(v_levels) if v_levels else empty(1, dev)
-    if side == "row" and mat.any():
-        ids = np.flatnonzero(mat & (store.rank > 0))
-        tdesc = to_dev(np.stack([store.v_off[ids], store.rows[ids], store.rank[ids]], 1), dev)
-        store.VT = torch.zeros_like(store.V)
-        with torch.cuda.device(dev):
-            _native.call("gc_batched_transpose", len(ids), ptr(tdesc), ptr(store.V),
-                         ptr(store.VT), stream)
-    store.coef_off, store.coef_size = coef_layout(flat, roots, store.rank)
-    store.timing = {"factor_s": t_factor, "aca_s": t_aca, "total_s": time.perf_counter() - t0}
-    # host BasisNode objects
-    by_index = {}
+        # ---- per basis: local -> global pivots, compact pivot store
+        o = 0
+        for k, ids, Rk, rh in parts:
+            s, st = S[k], S[k].store
+            n = len(ids)
+            rk = rank[o:o + n]
+            sel = _ranges(piv_off_l[o:o + n], rk)
+            node_of = np.repeat(np.arange(n), rk)
+            roff = rows_off[o:o + n] - rows_off[o]
+            glob = rh[roff[node_of] + piv_local[sel]]
+            s.gpiv[s.cursor:s.cursor + len(glob)] = glob
+            st.piv_off[ids] = s.cursor + _offsets(rk)
+            s.cursor += len(glob)
+            st.rank[ids] = rk
+            v0, v1 = int(v_off[o]), int(v_off[o + n - 1] + vcap[o + n - 1])
+            st.v_off[ids] = s.v_base + v_off[o:o + n] - v0
+            s.v_parts.append(V[v0:max(v1, v0)])
+            s.v_base += v1 - v0
+            o += n
+    out = []
+    for s in S:
+        st = s.store
+        st.pivots_host = s.gpiv[:s.cursor].copy()
+        st.pivots = to_dev(st.pivots_host if s.cursor else np.zeros(1, np.int64), dev)
+        st.V = torch.cat(s.v_parts) if s.v_parts else empty(1, dev)
+        if st.V.numel() == 0:
+            st.V = torch.zeros(1, dtype=torch.float64, device=dev)
+        if s.side == "row" and s.mat.any():
+            ids = np.flatnonzero(s.mat & (st.rank > 0))
+            tdesc = to_dev(np.stack([st.v_off[ids], st.rows[ids], st.rank[ids]], 1), dev)
+            st.VT = torch.zeros_like(st.V)
+            with torch.cuda.device(dev):
+                _native.call("gc_batched_transpose", len(ids), ptr(tdesc), ptr(st.V),
+                             ptr(st.VT), stream)
+        st.coef_off, st.coef_size = coef_layout(flat, s.roots, st.rank)
+        st.timing = {"factor_s": t_factor, "aca_s": t_aca, "total_s": time.perf_counter() - t0,
+                     "shared_with": len(S)}
+        by_index = {}
 
-    def make(i):
-        kids = () if flat.is_leaf[i] else (make(int(flat.left[i])), make(int(flat.right[i])))
-        o, r = store.piv_off[i], store.rank[i]
-        bn = BasisNode(flat.node(i), store.pivots_host[o:o + r], kids, store, i)
-        by_index[i] = bn
-        return bn
+        def make(i, st=st, by_index=by_index):
+            kids = () if flat.is_leaf[i] else (make(int(flat.left[i])), make(int(flat.right[i])))
+            o_, r_ = st.piv_off[i], st.rank[i]
+            bn = BasisNode(flat.node(i), st.pivots_host[o_:o_ + r_], kids, st, i)
+            by_index[i] = bn
+            return bn
 
-    root_nodes = [make(int(r)) for r in roots]
-    return ClusterBasis(root_nodes, by_index, store)
+        out.append(ClusterBasis([make(int(r)) for r in s.roots], by_index, st))
+    return out
 
 
 def expand_basis(node):

@@ -99,7 +99,7 @@ static void e_copy_weights(const gc_geom& g, RuleW& rw, int M);
 // quadrature weights as a kernel parameter: they live in the constant bank
 // and feed the DFMAs directly instead of occupying 2*M registers
 struct RuleW {
-    double w[16];
+    double w[64];
 };
 
 // One CTA per block; column-major output.  Shared memory: row points
@@ -194,7 +194,100 @@ __global__ void __launch_bounds__(NT) k_assemble_blocks(
 }
 
 static void e_copy_weights(const gc_geom& g, RuleW& rw, int M) {
-    for (int i = 0; i < 16; ++i) rw.w[i] = (i < M && g.wq_host) ? g.wq_host[i] : 0.0;
+    for (int i = 0; i < 64; ++i) rw.w[i] = (i < M && g.wq_host) ? g.wq_host[i] : 0.0;
+}
+
+// Higher regular orders (q_reg^2 = M > 16, M <= 64): same structure as
+// k_assemble_blocks, the row's points held in registers MC at a time.
+template <int MC, int NT>
+__global__ void __launch_bounds__(NT) k_assemble_blocks_big(
+    gc_geom g, RuleW rw, int M, const int64_t* __restrict__ desc, const int64_t* __restrict__ row_idx,
+    const int64_t* __restrict__ col_idx, double* __restrict__ out, gc_queue q, int32_t* flags) {
+    extern __shared__ double sm[];
+    const int64_t* d = desc + 5 * (int64_t)blockIdx.x;
+    const int64_t row_off = d[0], col_off = d[2], out_off = d[4];
+    const int nr = (int)d[1], nc = (int)d[3];
+    double* Xs = sm;
+    double* Ys = Xs + nr * M * 3;
+    int64_t* tvs = (int64_t*)(Ys + nc * M * 3);
+    int64_t* svs = tvs + 4 * nr;
+    for (int e = threadIdx.x; e < nr; e += NT) {
+        const int64_t t = __ldg(row_idx + row_off + e);
+        tvs[4 * e] = t;
+        for (int k = 0; k < 3; ++k) tvs[4 * e + 1 + k] = __ldg(g.tri_vid + 3 * t + k);
+    }
+    for (int e = threadIdx.x; e < nc; e += NT) {
+        const int64_t s = __ldg(col_idx + col_off + e);
+        svs[4 * e] = s;
+        for (int k = 0; k < 3; ++k) svs[4 * e + 1 + k] = __ldg(g.tri_vid + 3 * s + k);
+    }
+    __syncthreads();
+    for (int e = threadIdx.x; e < nr * M * 3; e += NT) {
+        const int a = e / (M * 3);
+        Xs[e] = __ldg(g.xq + tvs[4 * a] * (M * 3) + (e - a * M * 3));
+    }
+    for (int e = threadIdx.x; e < nc * M * 3; e += NT) {
+        const int b = e / (M * 3);
+        Ys[e] = __ldg(g.xq + svs[4 * b] * (M * 3) + (e - b * M * 3));
+    }
+    __syncthreads();
+    const int npairs = (nc + 1) / 2;
+    for (int e = threadIdx.x; e < nr * npairs; e += NT) {
+        const int a = e % nr, b0 = 2 * (e / nr);
+        const bool two = b0 + 1 < nc;
+        const int64_t t = tvs[4 * a];
+        const int64_t tv[3] = {tvs[4 * a + 1], tvs[4 * a + 2], tvs[4 * a + 3]};
+        bool live[2];
+#pragma unroll
+        for (int c = 0; c < 2; ++c) {
+            live[c] = false;
+            if (c == 1 && !two) continue;
+            const int b = b0 + c;
+            const int64_t sv[3] = {svs[4 * b + 1], svs[4 * b + 2], svs[4 * b + 3]};
+            int px, py;
+            const int kase = classify_pair(tv, sv, &px, &py);
+            if (kase == 0)
+                live[c] = true;
+            else
+                push_task(q, kase, t, svs[4 * b], px, py, out_off + (int64_t)b * nr + a, flags);
+        }
+        if (!live[0] && !live[1]) continue;
+        const double* Y0 = Ys + b0 * M * 3;
+        const double* Y1 = Ys + (two ? b0 + 1 : b0) * M * 3;
+        double tot0 = 0.0, tot1 = 0.0;
+        for (int i0 = 0; i0 < M; i0 += MC) {
+            double X[MC][3], wi[MC];
+#pragma unroll
+            for (int i = 0; i < MC; ++i) {
+                const bool in = i0 + i < M;
+#pragma unroll
+                for (int k = 0; k < 3; ++k) X[i][k] = in ? Xs[(a * M + i0 + i) * 3 + k] : 1e30;
+                wi[i] = in ? rw.w[i0 + i] : 0.0;
+            }
+#pragma unroll 1
+            for (int j = 0; j < M; ++j) {
+                const double u0 = Y0[3 * j], u1 = Y0[3 * j + 1], u2 = Y0[3 * j + 2];
+                const double v0 = Y1[3 * j], v1 = Y1[3 * j + 1], v2 = Y1[3 * j + 2];
+                double acc0 = 0.0, acc1 = 0.0;
+#pragma unroll
+                for (int i = 0; i < MC; ++i) {
+                    // padded points (weight 0) sit far away: finite, nonzero r2
+                    const double d0 = X[i][0] - u0, d1 = X[i][1] - u1, d2 = X[i][2] - u2;
+                    const double e0 = X[i][0] - v0, e1 = X[i][1] - v1, e2 = X[i][2] - v2;
+                    const double r2a = fma(d2, d2, fma(d1, d1, d0 * d0));
+                    const double r2b = fma(e2, e2, fma(e1, e1, e0 * e0));
+                    acc0 = fma(wi[i], rsqrt_fast(r2a), acc0);
+                    acc1 = fma(wi[i], rsqrt_fast(r2b), acc1);
+                }
+                tot0 = fma(rw.w[j], acc0, tot0);
+                tot1 = fma(rw.w[j], acc1, tot1);
+            }
+        }
+        const double gt = __ldg(g.gram + t) * INV_FOUR_PI;
+        if (live[0]) out[out_off + (int64_t)b0 * nr + a] = (gt * __ldg(g.gram + svs[4 * b0])) * tot0;
+        if (live[1])
+            out[out_off + (int64_t)(b0 + 1) * nr + a] = (gt * __ldg(g.gram + svs[4 * (b0 + 1)])) * tot1;
+    }
 }
 
 // generic-order fallback (any q_reg): one thread per entry, points from L1
@@ -450,6 +543,27 @@ int gc_assemble_blocks(const gc_geom* gp, int64_t nb, const int64_t* desc, int64
         case 4: return launch_blocks<4>(g, nb, desc, max_rows, max_cols, row_idx, col_idx, out, *qp, flags, st);
         case 16: return launch_blocks<16>(g, nb, desc, max_rows, max_cols, row_idx, col_idx, out, *qp, flags, st);
         default:
+            if (g.mq > 16 && g.mq <= 64) {
+                if (!g.wq_host) { set_error(GC_ERR_CONFIG, "gc_geom.wq_host is required"); return GC_ERR_CONFIG; }
+                const int M = (int)g.mq;
+                const size_t bytes = (size_t)(max_rows + max_cols) * (M * 3 * sizeof(double) + 4 * sizeof(int64_t));
+                if (bytes <= 200 * 1024) {
+                    RuleW rw;
+                    e_copy_weights(g, rw, M);
+                    cudaError_t e;
+                    if (max_rows * ((max_cols + 1) / 2) <= 128) {
+                        e = cudaFuncSetAttribute(k_assemble_blocks_big<8, 128>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes);
+                        if (e != cudaSuccess) return cuda_status(e, "k_assemble_blocks_big smem");
+                        k_assemble_blocks_big<8, 128><<<(unsigned)nb, 128, bytes, st>>>(g, rw, M, desc, row_idx, col_idx, out, *qp, flags);
+                    } else {
+                        e = cudaFuncSetAttribute(k_assemble_blocks_big<8, 256>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes);
+                        if (e != cudaSuccess) return cuda_status(e, "k_assemble_blocks_big smem");
+                        k_assemble_blocks_big<8, 256><<<(unsigned)nb, 256, bytes, st>>>(g, rw, M, desc, row_idx, col_idx, out, *qp, flags);
+                    }
+                    GC_CHECK_LAUNCH("k_assemble_blocks_big");
+                    return GC_OK;
+                }
+            }
             k_assemble_blocks_any<<<(unsigned)nb, BLK_THREADS, 0, st>>>(g, desc, row_idx, col_idx, out, *qp, flags);
             GC_CHECK_LAUNCH("k_assemble_blocks_any");
             return GC_OK;

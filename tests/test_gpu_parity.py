@@ -324,3 +324,16 @@ def test_sharded_operator_world1_matches_full():
         assert np.linalg.norm(y - ref) <= 1e-13 * np.linalg.norm(ref)
     finally:
         dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("q", [2, 4, 5, 6])
+def test_other_quadrature_orders_vs_oracle(q):
+    """C5 orders (q_reg = q_sing = q): blocks against the oracle's
+    reference-order restatement with the reference's full rules."""
+    mesh = geometry.build_sphere_mesh(2)
+    rows = np.arange(0, mesh.nt, 3)
+    cols = np.arange(mesh.nt)
+    got = assembly.assemble_galerkin_block("slp", mesh, "constant", rows, cols, orders=(q, q)).values
+    nodes, gram = P.chart_nodes(mesh.vertices, mesh.triangles)
+    ref = P.block(nodes, gram, mesh.triangles, rows, cols, q=(q, q))
+    assert rel(got, ref) < 1e-12

@@ -179,18 +179,40 @@ int gc_segmv(int64_t nseg, const int64_t* seg, const int64_t* blk,
              const double* in1, double* out, int accumulate, int64_t max_T,
              void* stream);
 
-/* Panel product, the mvm hot path.  A phase is a list of work items; item
- * i (items[6i..6i+5] = a_off, xi_off, out_off, T, nrows, mode) computes
+/* Panel product, the mvm hot path (one phase of h2.py:63-80).  A phase
+ * is a list of work items; item i (items[8i..8i+7] = a_off, xi_off,
+ * out_off, T, nrows, mode, red_slot, 0) computes
  *     s[t] = sum_{r < nrows} A[a_off + r*T + t] * in[xidx[xi_off + r]]
  * over a contiguous row-major chunk of a panel (A = A1 if mode&1, in = in1
  * if mode&2) and writes s to out[out_off + t] (mode&4; added to it if
- * mode&8) or to scratch[out_off + t].  red (nred,5) = out_off, T,
- * scratch_off, nitems, accumulate then sums consecutive scratch rows into
- * out in item order.  One writer per output, fixed order: deterministic. */
+ * mode&8) or, for a panel split over several items, to scratch[out_off+t].
+ * red (nred,5) = out_off, T, scratch_off, nitems, accumulate describes each
+ * split panel; the last item of a panel to finish (arrivals[red_slot], an
+ * int32 counter that must start at 0 and is re-armed by the kernel) sums
+ * the scratch rows into out in item order.  One writer per output, fixed
+ * order: deterministic.  chain != 0 launches with programmatic stream
+ * serialization (PDL): the kernel prefetches its matrix chunk while the
+ * previous kernel on the stream drains and waits for it before reading in
+ * (for the latency-bound transform levels).  trace (optional, NULL = off)
+ * = [dev] 2 x uint64 receiving min(start) / max(end) %globaltimer (ns) of
+ * the launch's CTAs, for timelines inside CUDA graphs. */
 int gc_panelmv(int64_t nitems, const int64_t* items, const int32_t* xidx,
                const double* A0, const double* A1, const double* in0,
                const double* in1, double* out, double* scratch, int64_t nred,
-               const int64_t* red, void* stream);
+               const int64_t* red, int32_t* arrivals, int32_t chain, uint64_t* trace,
+               void* stream);
+
+/* A run of consecutive transform levels (h2.py:63-70 forward, h2.py:74-79
+ * backward) in ONE co-resident launch with grid barriers between levels.
+ * phases [dev] = nphase packed descriptors of gc_panel_phase_bytes() bytes:
+ * {items, nitems, xidx, A0, A1, in0, in1, out, scratch, red, arrivals,
+ * trace} with the meaning of gc_panelmv's arguments (trace unused here); grid from
+ * gc_panel_chain_grid; barrier [dev] = one uint32, zero before the first
+ * launch, left consistent by every launch (no re-arming). */
+int gc_panel_chain_grid(int64_t* grid);
+int gc_panel_chain(int64_t nphase, const void* phases, int64_t grid, uint32_t* barrier,
+                   void* stream);
+int64_t gc_panel_phase_bytes(void);
 
 /* The whole product y = H x as ONE persistent cooperative kernel scheduled
  * by dataflow counters (csrc/h2persist.cu; replaces h2.mvm, h2.py:63-80).

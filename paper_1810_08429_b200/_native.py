@@ -51,7 +51,11 @@ _SIGNATURES = {
     "gc_gather": [c_p, c_p, c_i64, c_p, c_p],
     "gc_scatter": [c_p, c_p, c_i64, c_p, c_p],
     "gc_segmv": [c_i64, c_p, c_p, c_p, c_p, c_p, c_p, c_p, ctypes.c_int, c_i64, c_p],
-    "gc_panelmv": [c_i64, c_p, c_p, c_p, c_p, c_p, c_p, c_p, c_p, c_i64, c_p, c_p],
+    "gc_panelmv": [c_i64, c_p, c_p, c_p, c_p, c_p, c_p, c_p, c_p, c_i64, c_p, c_p, ctypes.c_int32, c_p,
+                   c_p],
+    "gc_panel_chain_grid": [ctypes.POINTER(c_i64)],
+    "gc_panel_chain": [c_i64, c_p, c_i64, c_p, c_p],
+    "gc_panel_phase_bytes": [],
     "gc_h2mv_persistent": [c_p, c_p, c_i64, ctypes.c_int32, c_p, ctypes.c_int32,
                            ctypes.POINTER(ctypes.c_int32),
                            c_p, c_p, c_i64, c_i64, ctypes.POINTER(c_p),
@@ -64,7 +68,7 @@ _SIGNATURES = {
     "gc_dfma_probe": [c_i64, c_i64, c_i64, c_p, c_p],
 }
 _RESTYPES = {"gc_last_error": ctypes.c_char_p, "gc_launch_count": ctypes.c_uint64,
-             "gc_reset_launch_count": None}
+             "gc_reset_launch_count": None, "gc_panel_phase_bytes": ctypes.c_int64}
 
 EXPORTED = tuple(_SIGNATURES)
 ABI_VERSION = 1

@@ -95,32 +95,89 @@ extern "C" int gc_segmv(int64_t nseg, const int64_t* seg, const int64_t* blk, co
 // all near-field blocks of one row leaf, one V-hat, ...).  The panels of a
 // phase are cut into work items of ~32 KB so every CTA streams the same
 // amount of HBM; items of a multi-item panel write partial sums to scratch
-// and k_panel_reduce adds them in item order (bitwise deterministic).
+// and the last CTA of the panel adds them in item order (bitwise deterministic).
 namespace gcb {
 
 constexpr int PAN_THREADS = 256;
 constexpr int PAN_UNROLL = 16;
 constexpr int PAN_MAX_ROWS = 1024;   // rows per work item (x gathered to smem)
 
-// item: a_off, xi_off, out_off, T, nrows, mode (bit0 A1, bit1 in1,
-//       bit2 direct to out, bit3 accumulate into out)
+// item (8 x int64): a_off, xi_off, out_off, T, nrows, mode, red, 0
+//   mode bit0 A1, bit1 in1, bit2 direct to out, bit3 accumulate into out;
+//   red = reduction slot of a split panel (items without bit2 write partial
+//   sums to scratch[out_off..]).
+// red slot (5 x int64): out_off, T, scratch_off, nitems, accumulate.
 // The item's input entries are gathered into shared memory first, so the
 // streaming loop over A has no dependent loads: 16 independent 8-byte loads
-// per thread are in flight before the first FMA.
-__global__ void __launch_bounds__(PAN_THREADS) k_panelmv(
-    const int64_t* __restrict__ items, const int32_t* __restrict__ xidx,
-    const double* __restrict__ A0, const double* __restrict__ A1,
-    const double* __restrict__ in0, const double* __restrict__ in1,
-    double* __restrict__ out, double* __restrict__ scratch) {
-    __shared__ double red[PAN_THREADS];
-    __shared__ double xs[PAN_MAX_ROWS];
-    const int64_t* it = items + 6 * (int64_t)blockIdx.x;
+// per thread are in flight before the first FMA.  The last CTA to finish a
+// split panel (arrival counter) adds its partial sums in item order, so the
+// result is bitwise deterministic without a second launch; it re-arms the
+// counter for the next product.
+struct PanelSmem {
+    double red[PAN_THREADS];
+    double xs[PAN_MAX_ROWS];
+    int last;
+};
+
+struct PanelPhase {           // one phase (forward level, bucket, ...) of the product
+    const int64_t* items;
+    int64_t nitems;
+    const int32_t* xidx;
+    const double* A0;
+    const double* A1;
+    const double* in0;
+    const double* in1;
+    double* out;
+    double* scratch;
+    const int64_t* red;
+    int* arrivals;
+    unsigned long long* trace;   // optional: min start / max end %globaltimer (ns)
+};
+
+__device__ __forceinline__ unsigned long long globaltimer() {
+    unsigned long long t;
+    asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
+    return t;
+}
+
+__device__ __forceinline__ void prefetch_l2(const void* p, int64_t bytes) {
+    const uintptr_t lo = reinterpret_cast<uintptr_t>(p) & ~uintptr_t(127);
+    const uintptr_t hi = reinterpret_cast<uintptr_t>(p) + bytes;
+    for (uintptr_t l = lo + 128 * threadIdx.x; l < hi; l += 128 * PAN_THREADS)
+        asm volatile("prefetch.global.L2 [%0];" ::"l"(l));
+}
+
+__device__ __forceinline__ void prefetch_item(const PanelPhase& P, int64_t i) {
+    const int64_t* it = P.items + 8 * i;
+    const double* A = ((it[5] & 1) ? P.A1 : P.A0) + it[0];
+    prefetch_l2(A, 8 * it[3] * it[4]);
+}
+
+// load the item's inputs into smem (WAIT: griddepcontrol.wait between the
+// input-independent prologue and the first read of the input vector)
+template <bool WAIT>
+__device__ __forceinline__ void panel_item(const PanelPhase& P, int64_t item, PanelSmem& sm) {
+    const int64_t* it = P.items + 8 * item;
     const int64_t a_off = it[0], xi_off = it[1], out_off = it[2];
     const int T = (int)it[3], nrows = (int)it[4], mode = (int)it[5];
-    const double* __restrict__ A = ((mode & 1) ? A1 : A0) + a_off;
-    const double* __restrict__ x = (mode & 2) ? in1 : in0;
-    const int32_t* __restrict__ xi = xidx + xi_off;
-    for (int r = threadIdx.x; r < nrows; r += PAN_THREADS) xs[r] = __ldg(x + __ldg(xi + r));
+    const double* __restrict__ A = ((mode & 1) ? P.A1 : P.A0) + a_off;
+    const double* x = (mode & 2) ? P.in1 : P.in0;
+    const int32_t* __restrict__ xi = P.xidx + xi_off;
+    if (WAIT) {
+        int* xsi = reinterpret_cast<int*>(sm.red);
+        prefetch_l2(A, 8 * (int64_t)nrows * T);
+        const bool staged = nrows <= 2 * PAN_THREADS;
+        if (staged)
+            for (int r = threadIdx.x; r < nrows; r += PAN_THREADS) xsi[r] = __ldg(xi + r);
+        asm volatile("griddepcontrol.wait;" ::: "memory");
+        if (staged) {
+            for (int r = threadIdx.x; r < nrows; r += PAN_THREADS) sm.xs[r] = __ldcg(x + xsi[r]);
+        } else {
+            for (int r = threadIdx.x; r < nrows; r += PAN_THREADS) sm.xs[r] = __ldcg(x + __ldg(xi + r));
+        }
+    } else {
+        for (int r = threadIdx.x; r < nrows; r += PAN_THREADS) sm.xs[r] = __ldcg(x + __ldg(xi + r));
+    }
     __syncthreads();
     const int tt = T < PAN_THREADS ? T : PAN_THREADS;
     const int ng = PAN_THREADS / tt;
@@ -137,57 +194,274 @@ __global__ void __launch_bounds__(PAN_THREADS) k_panelmv(
 #pragma unroll
                 for (int j = 0; j < PAN_UNROLL; ++j) a[j] = __ldcs(At + (int64_t)(r + j * ng) * T);
 #pragma unroll
-                for (int j = 0; j < PAN_UNROLL; ++j) acc = fma(a[j], xs[r + j * ng], acc);
+                for (int j = 0; j < PAN_UNROLL; ++j) acc = fma(a[j], sm.xs[r + j * ng], acc);
             }
-            for (; r < nrows; r += ng) acc = fma(__ldcs(At + (int64_t)r * T), xs[r], acc);
+            for (; r < nrows; r += ng) acc = fma(__ldcs(At + (int64_t)r * T), sm.xs[r], acc);
         }
-        red[threadIdx.x] = acc;
+        sm.red[threadIdx.x] = acc;
         __syncthreads();
         if (threadIdx.x < tt && t < T) {
-            double s = red[threadIdx.x];
-            for (int q = 1; q < ng; ++q) s += red[q * tt + threadIdx.x];
+            double s = sm.red[threadIdx.x];
+            for (int q = 1; q < ng; ++q) s += sm.red[q * tt + threadIdx.x];
             if (mode & 4) {
-                double* o = out + out_off + t;
-                *o = (mode & 8) ? *o + s : s;
+                double* o = P.out + out_off + t;
+                *o = (mode & 8) ? __ldcg(o) + s : s;
             } else {
-                scratch[out_off + t] = s;
+                P.scratch[out_off + t] = s;
             }
         }
         __syncthreads();
     }
+    if (mode & 4) return;
+    const int slot = (int)it[6];
+    const int64_t* rd = P.red + 5 * (int64_t)slot;
+    __threadfence();
+    __syncthreads();
+    if (threadIdx.x == 0) sm.last = atomicAdd(P.arrivals + slot, 1) == (int)rd[3] - 1;
+    __syncthreads();
+    if (!sm.last) return;
+    __threadfence();
+    const int64_t o_off = rd[0], so = rd[2];
+    const int RT = (int)rd[1], ni = (int)rd[3];
+    const bool accum = rd[4] != 0;
+    for (int t = threadIdx.x; t < RT; t += PAN_THREADS) {
+        double v = __ldcg(P.scratch + so + t);
+        for (int i = 1; i < ni; ++i) v += __ldcg(P.scratch + so + (int64_t)i * RT + t);
+        P.out[o_off + t] = accum ? __ldcg(P.out + o_off + t) + v : v;
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) P.arrivals[slot] = 0;
 }
 
-// red: out_off, T, scratch_off, nitems, accumulate
-__global__ void k_panel_reduce(int64_t nred, const int64_t* __restrict__ red,
-                               const double* __restrict__ scratch, double* __restrict__ out) {
-    for (int64_t s = blockIdx.x; s < nred; s += gridDim.x) {
-        const int64_t* r = red + 5 * s;
-        const int64_t out_off = r[0], T = r[1], so = r[2], ni = r[3];
-        const bool accum = r[4] != 0;
-        for (int64_t t = threadIdx.x; t < T; t += blockDim.x) {
-            double v = scratch[so + t];
-            for (int64_t i = 1; i < ni; ++i) v += scratch[so + i * T + t];
-            out[out_off + t] = accum ? out[out_off + t] + v : v;
+// One phase, one CTA per item.  CHAIN: launched with programmatic stream
+// serialization - the kernel starts while its predecessor drains, reads its
+// descriptor and indices and prefetches its matrix chunk into L2, then
+// waits (griddepcontrol.wait) before it touches the input vector.
+template <bool CHAIN>
+__global__ void __launch_bounds__(PAN_THREADS) k_panelmv(PanelPhase P) {
+    __shared__ PanelSmem sm;
+    if (CHAIN) asm volatile("griddepcontrol.launch_dependents;");
+    if (P.trace != nullptr && threadIdx.x == 0) atomicMin(P.trace, globaltimer());
+    panel_item<CHAIN>(P, blockIdx.x, sm);
+    if (P.trace != nullptr) {
+        __syncthreads();
+        if (threadIdx.x == 0) atomicMax(P.trace + 1, globaltimer());
+    }
+}
+
+// Grid-wide barrier (co-resident grid): every CTA adds 1 except CTA 0,
+// which adds 2^31 - (nb - 1), so each barrier flips bit 31 of the counter
+// and the counter never needs re-arming between launches.
+__device__ __forceinline__ void grid_barrier(unsigned* bar) {
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        const unsigned nb = gridDim.x;
+        const unsigned inc = blockIdx.x == 0 ? 0x80000000u - (nb - 1) : 1u;
+        __threadfence();
+        const unsigned old = atomicAdd(bar, inc);
+        unsigned cur;
+        do {
+            asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(cur) : "l"(bar) : "memory");
+        } while (((old ^ cur) & 0x80000000u) == 0);
+    }
+    __syncthreads();
+}
+
+// Warp-granular item (the chain's levels are too small to give every CTA
+// an item: a level has ~10^3 items of a few KB, so one warp owns one item
+// and a CTA works 8 items at once).  Lane l owns outputs t = t0 + l + 32 j,
+// j < J, and runs the rows of the item in order (fixed summation order).
+constexpr int WARP_MAX_ROWS = 256;
+
+template <int J>
+__device__ __forceinline__ void warp_rows(const double* __restrict__ A, int T, int t0, int nrows,
+                                          const double* xs, int lane, double* acc) {
+    constexpr int U = 16 / J;                     // rows in flight
+#pragma unroll
+    for (int j = 0; j < J; ++j) acc[j] = 0.0;
+    const int tl = t0 + lane;
+    int r = 0;
+    for (; r + U <= nrows; r += U) {
+        double a[U][J];
+#pragma unroll
+        for (int u = 0; u < U; ++u)
+#pragma unroll
+            for (int j = 0; j < J; ++j) {
+                const int t = tl + 32 * j;
+                a[u][j] = t < T ? __ldcs(A + (int64_t)(r + u) * T + t) : 0.0;
+            }
+#pragma unroll
+        for (int u = 0; u < U; ++u)
+#pragma unroll
+            for (int j = 0; j < J; ++j) acc[j] = fma(a[u][j], xs[r + u], acc[j]);
+    }
+    for (; r < nrows; ++r)
+#pragma unroll
+        for (int j = 0; j < J; ++j) {
+            const int t = tl + 32 * j;
+            if (t < T) acc[j] = fma(__ldcs(A + (int64_t)r * T + t), xs[r], acc[j]);
+        }
+}
+
+__device__ void warp_item(const PanelPhase& P, int64_t item, double* xs, int lane) {
+    const int64_t* it = P.items + 8 * item;
+    const int64_t a_off = it[0], xi_off = it[1], out_off = it[2];
+    const int T = (int)it[3], nrows = (int)it[4], mode = (int)it[5];
+    const double* __restrict__ A = ((mode & 1) ? P.A1 : P.A0) + a_off;
+    const double* x = (mode & 2) ? P.in1 : P.in0;
+    const int32_t* __restrict__ xi = P.xidx + xi_off;
+    for (int r = lane; r < nrows; r += 32) xs[r] = __ldcg(x + __ldg(xi + r));
+    __syncwarp();
+    double* dst = (mode & 4) ? P.out + out_off : P.scratch + out_off;
+    for (int t0 = 0; t0 < T; t0 += 256) {
+        const int span = T - t0;
+        double acc[8];
+        if (span > 128) warp_rows<8>(A, T, t0, nrows, xs, lane, acc);
+        else if (span > 64) warp_rows<4>(A, T, t0, nrows, xs, lane, acc);
+        else if (span > 32) warp_rows<2>(A, T, t0, nrows, xs, lane, acc);
+        else warp_rows<1>(A, T, t0, nrows, xs, lane, acc);
+        const int J = span > 128 ? 8 : span > 64 ? 4 : span > 32 ? 2 : 1;
+#pragma unroll
+        for (int j = 0; j < 8; ++j) {
+            const int t = t0 + lane + 32 * j;
+            if (j < J && t < T) dst[t] = (mode & 12) == 12 ? __ldcg(dst + t) + acc[j] : acc[j];
+        }
+    }
+    __syncwarp();
+    if (mode & 4) return;
+    const int slot = (int)it[6];
+    const int64_t* rd = P.red + 5 * (int64_t)slot;
+    __threadfence();
+    __syncwarp();
+    int last = 0;
+    if (lane == 0) last = atomicAdd(P.arrivals + slot, 1) == (int)rd[3] - 1;
+    last = __shfl_sync(0xffffffffu, last, 0);
+    if (!last) return;
+    __threadfence();
+    const int64_t o_off = rd[0], so = rd[2];
+    const int RT = (int)rd[1], ni = (int)rd[3];
+    const bool accum = rd[4] != 0;
+    for (int t = lane; t < RT; t += 32) {
+        double v = __ldcg(P.scratch + so + t);
+        for (int i = 1; i < ni; ++i) v += __ldcg(P.scratch + so + (int64_t)i * RT + t);
+        P.out[o_off + t] = accum ? __ldcg(P.out + o_off + t) + v : v;
+    }
+    __syncwarp();
+    if (lane == 0) P.arrivals[slot] = 0;
+}
+
+// A run of consecutive chain phases (transform levels) in ONE co-resident
+// launch: warps stride over each phase's items, prefetch their items of
+// the next phase into L2, and the grid meets at a barrier between phases.
+__global__ void __launch_bounds__(PAN_THREADS) k_panel_chain(const PanelPhase* __restrict__ phases,
+                                                             int nphase, unsigned* bar) {
+    __shared__ double xs[PAN_THREADS / 32][WARP_MAX_ROWS];
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    const int64_t gw = (int64_t)blockIdx.x * (PAN_THREADS / 32) + warp;
+    const int64_t nw = (int64_t)gridDim.x * (PAN_THREADS / 32);
+    for (int ph = 0; ph < nphase; ++ph) {
+        const PanelPhase P = phases[ph];
+        for (int64_t i = gw; i < P.nitems; i += nw) warp_item(P, i, xs[warp], lane);
+        if (ph + 1 < nphase) {
+            const PanelPhase& Q = phases[ph + 1];
+            for (int64_t i = gw; i < Q.nitems; i += nw) {
+                const int64_t* it = Q.items + 8 * i;
+                const double* A = ((it[5] & 1) ? Q.A1 : Q.A0) + it[0];
+                const uintptr_t lo = reinterpret_cast<uintptr_t>(A) & ~uintptr_t(127);
+                const uintptr_t hi = reinterpret_cast<uintptr_t>(A + it[3] * it[4]);
+                for (uintptr_t l = lo + 128 * lane; l < hi; l += 128 * 32)
+                    asm volatile("prefetch.global.L2 [%0];" ::"l"(l));
+            }
+            grid_barrier(bar);
         }
     }
 }
 
 }  // namespace gcb
 
-extern "C" int gc_panelmv(int64_t nitems, const int64_t* items, const int32_t* xidx,
-                          const double* A0, const double* A1, const double* in0,
-                          const double* in1, double* out, double* scratch, int64_t nred,
-                          const int64_t* red, void* stream) {
-    using namespace gcb;
-    if (nitems <= 0) return GC_OK;
+// the chain's kernels carry the device's highest scheduling priority, so
+// their CTAs are dispatched ahead of the queued bulk phases
+static int top_priority() {
+    int least = 0, greatest = 0;
+    if (cudaDeviceGetStreamPriorityRange(&least, &greatest) != cudaSuccess) return 0;
+    return greatest;
+}
+
+static int check_phase(int64_t nitems, int64_t nred, const int64_t* red, const int32_t* arrivals) {
     if (nitems > 0x7fffffffLL) { set_error(GC_ERR_CONFIG, "too many work items"); return GC_ERR_CONFIG; }
-    cudaStream_t st = (cudaStream_t)stream;
-    k_panelmv<<<(unsigned)nitems, PAN_THREADS, 0, st>>>(items, xidx, A0, A1, in0, in1, out, scratch);
-    GC_CHECK_LAUNCH("k_panelmv");
-    if (nred > 0) {
-        int64_t grid = nred < 148 * 16 ? nred : 148 * 16;
-        k_panel_reduce<<<(unsigned)grid, 128, 0, st>>>(nred, red, scratch, out);
-        GC_CHECK_LAUNCH("k_panel_reduce");
+    if (nred > 0 && (red == nullptr || arrivals == nullptr)) {
+        set_error(GC_ERR_CONFIG, "gc_panelmv: split panels need red and arrivals");
+        return GC_ERR_CONFIG;
     }
     return GC_OK;
 }
+
+extern "C" int gc_panelmv(int64_t nitems, const int64_t* items, const int32_t* xidx,
+                          const double* A0, const double* A1, const double* in0,
+                          const double* in1, double* out, double* scratch, int64_t nred,
+                          const int64_t* red, int32_t* arrivals, int32_t chain, uint64_t* trace,
+                          void* stream) {
+    using namespace gcb;
+    if (nitems <= 0) return GC_OK;
+    if (int rc = check_phase(nitems, nred, red, arrivals)) return rc;
+    const PanelPhase P{items, nitems, xidx, A0, A1, in0, in1, out, scratch, red, arrivals,
+                       (unsigned long long*)trace};
+    if (!chain) {
+        k_panelmv<false><<<(unsigned)nitems, PAN_THREADS, 0, (cudaStream_t)stream>>>(P);
+        GC_CHECK_LAUNCH("k_panelmv");
+        return GC_OK;
+    }
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3((unsigned)nitems);
+    cfg.blockDim = dim3(PAN_THREADS);
+    cfg.stream = (cudaStream_t)stream;
+    cudaLaunchAttribute attr[2];
+    attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    attr[0].val.programmaticStreamSerializationAllowed = 1;
+    attr[1].id = cudaLaunchAttributePriority;
+    attr[1].val.priority = top_priority();
+    cfg.attrs = attr;
+    cfg.numAttrs = 2;
+    cudaError_t e = cudaLaunchKernelEx(&cfg, k_panelmv<true>, P);
+    if (e != cudaSuccess) return cuda_status(e, "k_panelmv (chain)");
+    count_launch();
+    return GC_OK;
+}
+
+extern "C" int gc_panel_chain_grid(int64_t* grid) {
+    using namespace gcb;
+    int dev = 0, sms = 0, per_sm = 0;
+    cudaError_t e = cudaGetDevice(&dev);
+    if (e == cudaSuccess) e = cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    if (e == cudaSuccess) e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_panel_chain, PAN_THREADS, 0);
+    if (e != cudaSuccess) return cuda_status(e, "gc_panel_chain_grid");
+    // two CTAs per SM: enough memory parallelism for the small transform
+    // levels, and room left on every SM for the concurrent bulk phases
+    *grid = (int64_t)sms * (per_sm < 2 ? per_sm : 2);
+    return GC_OK;
+}
+
+extern "C" int gc_panel_chain(int64_t nphase, const void* phases, int64_t grid, uint32_t* barrier,
+                              void* stream) {
+    using namespace gcb;
+    if (nphase <= 0) return GC_OK;
+    if (grid <= 0 || barrier == nullptr) { set_error(GC_ERR_CONFIG, "gc_panel_chain: bad grid"); return GC_ERR_CONFIG; }
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3((unsigned)grid);
+    cfg.blockDim = dim3(PAN_THREADS);
+    cfg.stream = (cudaStream_t)stream;
+    cudaLaunchAttribute attr[2];
+    attr[0].id = cudaLaunchAttributeCooperative;
+    attr[0].val.cooperative = 1;
+    attr[1].id = cudaLaunchAttributePriority;
+    attr[1].val.priority = top_priority();
+    cfg.attrs = attr;
+    cfg.numAttrs = 2;
+    cudaError_t e = cudaLaunchKernelEx(&cfg, k_panel_chain, (const PanelPhase*)phases, (int)nphase,
+                                       (unsigned*)barrier);
+    if (e != cudaSuccess) return cuda_status(e, "k_panel_chain");
+    count_launch();
+    return GC_OK;
+}
+
+extern "C" int64_t gc_panel_phase_bytes(void) { return (int64_t)sizeof(gcb::PanelPhase); }

@@ -15,6 +15,7 @@ same bytes the reference does; ``spectral_error_estimate``, ``cg_solve``
 and ``cgnr_solve`` are host consumers of the device matvec.
 """
 
+import os
 from collections import namedtuple
 
 import numpy as np
@@ -398,20 +399,41 @@ def cgnr_solve(apply, b, tol=1e-8, max_iter=500):
 
 _ITEM_ELEMS = 8192          # ~64 KB of matrix data per work item
 _ITEM_MAX_ROWS = 1024       # PAN_MAX_ROWS in csrc/h2mv.cu
+_WARP_MAX_ROWS = 256        # WARP_MAX_ROWS in csrc/h2mv.cu
 
 
 class _Phase:
-    __slots__ = ("name", "items", "xidx", "red", "nitems", "nred", "A0", "A1", "in0", "in1",
-                 "out", "scratch", "bytes")
+    __slots__ = ("name", "height", "items", "xidx", "red", "arrivals", "nitems", "nred", "A0", "A1",
+                 "in0", "in1", "out", "scratch", "bytes")
+
+
+class _Node:
+    """One step of the product DAG: a panel phase or a host callable
+    (gather, zero, scatter, a collective), run on ``stream`` after ``deps``."""
+    __slots__ = ("name", "phase", "fn", "stream", "deps", "launches")
+
+    def __init__(self, name, stream, deps=(), phase=None, fn=None):
+        self.name, self.stream, self.deps, self.phase, self.fn = name, stream, list(deps), phase, fn
+        self.launches = 1 if phase is not None else 0
 
 
 class PanelPlan:
-    """mvm as 6 phases of ``gc_panelmv`` over contiguous panels.
+    """mvm as a DAG of ``gc_panelmv`` phases over contiguous panels.
 
-    Streams: the near-field (independent of the basis transforms) runs on a
-    side stream concurrently with the latency-bound forward transform; the
-    leaf-basis phase joins it.  ``capture()`` records the whole product into
-    one CUDA graph with static input/output buffers.
+    The four phases of h2.py:63-80 are cut by tree height: forward levels
+    (bottom-up) and backward levels (top-down) form the latency-bound
+    "chain" on a high-priority stream (programmatic dependent launches: a
+    level's prologue overlaps its predecessor's drain); the coupling panels
+    are bucketed by the height of their row cluster and each bucket runs on
+    its own stream as soon as the forward transform has produced every
+    x-hat it reads, so the bandwidth-bound bulk (deep buckets, near field)
+    streams from HBM while the chain climbs the tree.  A backward level
+    waits only for the buckets that write the y-hat entries it reads or adds
+    into.  Coupling overwrites y-hat before any backward contribution is
+    added, so the summation order - and the result, bit for bit - does not
+    depend on the schedule.  ``capture()`` records the DAG into one CUDA
+    graph with static input/output buffers; ``run(..., phase_events=...)``
+    executes it serially on the current stream (for per-phase timing).
     """
 
     def __init__(self, h):
@@ -429,9 +451,15 @@ class PanelPlan:
         self.yt = torch.zeros(self.n_out, **f64)
         self.xhat = torch.zeros(max(cs.coef_size, 1), **f64)
         self.yhat = torch.zeros(max(rs.coef_size, 1), **f64)
-        self.main_phases, self.side_phases, self.tail_phases = [], [], []
+        # "pdl": one launch per transform level; "persistent": runs of levels
+        # in one co-resident launch with grid barriers (experimental)
+        self.chain_mode = os.environ.get("GC_CHAIN_MODE", "pdl")
+        grid = _native.ctypes.c_int64(0)
+        _native.call("gc_panel_chain_grid", _native.ctypes.byref(grid))
+        self._chain_grid = grid.value
         size_r = rf.stop - rf.start
         # forward transform (column basis), by height
+        fwd = []
         mat = cs.materialized & (cs.rank > 0)
         for h_ in np.unique(cf.height[mat]):
             ids = np.flatnonzero(mat & (cf.height == h_))
@@ -440,9 +468,10 @@ class PanelPlan:
             base = cf.start[ids] if leaf else cs.coef_off[cf.left[ids]]
             panels = (cs.v_off[ids], K, cs.rank[ids], [b + np.arange(k) for b, k in zip(base, K)],
                       cs.coef_off[ids], 0)
-            self.main_phases.append(self._phase("forward", panels, cs.V, None,
-                                                self.xt if leaf else self.xhat, None, self.xhat))
-        # coupling (row panels)
+            fwd.append(self._phase("forward", int(h_), panels, cs.V, None,
+                                   self.xt if leaf else self.xhat, None, self.xhat, transform=True))
+        # coupling: one panel per row cluster, bucketed by row height
+        cpl = []
         live = (d.c_nr > 0) & (d.c_nc > 0)
         order = np.flatnonzero(live)[np.argsort(d.c_rows[live], kind="stable")]
         if order.size:
@@ -453,19 +482,27 @@ class PanelPlan:
             ks = [d.c_nc[order[a:b]] for a, b in zip(cuts, ends)]
             rows = [np.concatenate([o + np.arange(k) for o, k in zip(oo, kk)]) for oo, kk in zip(xi, ks)]
             K = np.array([len(r) for r in rows], dtype=np.int64)
-            panels = (d.c_off[order[cuts]], K, d.c_nr[order[cuts]], rows, rs.coef_off[sn[cuts]], 0)
-            self.main_phases.append(self._phase("coupling", panels, d.coup, None, self.xhat, None,
-                                                self.yhat))
+            colh = np.maximum.reduceat(cf.height[d.c_cols[order]], cuts)
+            rowh = rf.height[sn[cuts]]
+            for h_ in np.unique(rowh):
+                sel = np.flatnonzero(rowh == h_)
+                panels = (d.c_off[order[cuts[sel]]], K[sel], d.c_nr[order[cuts[sel]]],
+                          [rows[i] for i in sel], rs.coef_off[sn[cuts[sel]]], 0)
+                P = self._phase("coupling", int(h_), panels, d.coup, None, self.xhat, None, self.yhat)
+                cpl.append((P, int(colh[sel].max())))
         # backward transform (row basis), top down
+        bwd = []
         matb = rs.materialized & (rs.rank > 0) & ~rf.is_leaf
         for h_ in sorted(np.unique(rf.height[matb]), reverse=True):
             ids = np.flatnonzero(matb & (rf.height == h_))
             K = rs.rank[ids]
             panels = (rs.v_off[ids], K, rs.rows[ids], [o + np.arange(k) for o, k in zip(rs.coef_off[ids], K)],
                       rs.coef_off[rf.left[ids]], 1)
-            self.main_phases.append(self._phase("backward", panels, rs.VT, None, self.yhat, None,
-                                                self.yhat))
-        # near field (side stream): one panel per row leaf
+            P = self._phase("backward", int(h_), panels, rs.VT, None, self.yhat, None, self.yhat,
+                            transform=True)
+            kids = np.r_[rf.left[ids], rf.right[ids]]
+            bwd.append((P, set(rf.height[kids].tolist()) | {int(h_)}))
+        # near field: one panel per row leaf
         order = np.argsort(d.n_rows, kind="stable")
         sn = d.n_rows[order]
         cuts = np.flatnonzero(np.r_[True, sn[1:] != sn[:-1]]) if len(sn) else np.zeros(0, np.int64)
@@ -474,8 +511,9 @@ class PanelPlan:
                                 zip(d.n_cols[order[a:b]], d.n_nc[order[a:b]])]) for a, b in zip(cuts, ends)]
         K = np.array([len(r) for r in rows], dtype=np.int64)
         panels = (d.n_off[order[cuts]], K, d.n_nr[order[cuts]], rows, rf.start[sn[cuts]], 0)
-        self.side_phases.append(self._phase("nearfield", panels, d.near, None, self.xt, None, self.yt))
-        # leaf basis (after the join): yt[leaf] += V yhat
+        near = self._phase("nearfield", 0, panels, d.near, None, self.xt, None, self.yt)
+        # leaf basis: yt[leaf] += V yhat
+        leafp = None
         leaves = np.flatnonzero(rf.is_leaf & rs.materialized & (rs.rank > 0))
         if d.row_range is not None:
             leaves = leaves[(rf.start[leaves] >= d.row_range[0]) & (rf.stop[leaves] <= d.row_range[1])]
@@ -483,11 +521,182 @@ class PanelPlan:
             K = rs.rank[leaves]
             panels = (rs.v_off[leaves], K, size_r[leaves],
                       [o + np.arange(k) for o, k in zip(rs.coef_off[leaves], K)], rf.start[leaves], 1)
-            self.tail_phases.append(self._phase("leafbasis", panels, rs.VT, None, self.yhat, None, self.yt))
-        self.side = torch.cuda.Stream(device=dev)
+            leafp = self._phase("leafbasis", 0, panels, rs.VT, None, self.yhat, None, self.yt,
+                                transform=True)
+        self._fwd, self._cpl, self._bwd, self._near, self._leaf = fwd, cpl, bwd, near, leafp
+        self.phases = [P for P in [near] + fwd + [c for c, _ in cpl] + [b for b, _ in bwd] + [leafp]
+                       if P is not None and P.nitems > 0]
+        # the chain gets the highest stream priority so its CTAs are
+        # scheduled ahead of the queued bulk (coupling buckets, near field)
+        self.streams = {"chain": torch.cuda.Stream(device=dev, priority=-8)}
+        self._bulk_priority = 0
+        self._keep = []
+        self._barrier = torch.zeros(1, dtype=torch.int32, device=dev)
+        self.trace = {}                    # id(phase) -> [2] int64 (profiling only)
+        self.nodes = self._build_nodes()
         self.graph = None
 
-    def _phase(self, name, panels, A0, A1, in0, in1, out):
+    # -- DAG -----------------------------------------------------------------
+    def _split_height(self):
+        """Chain split for the persistent mode: levels below S and above S
+        form separate launches, S the lowest height whose buckets together
+        hold <= 20% of the coupling bytes (the big deep buckets then only
+        gate the lower backward launch)."""
+        if not self._cpl:
+            return 0
+        by_h = sorted(((P.height, P.bytes) for P, _ in self._cpl), reverse=True)
+        total = sum(b for _, b in by_h)
+        acc, S = 0, by_h[0][0] + 1
+        for h_, b in by_h:
+            if acc + b > 0.2 * total:
+                break
+            acc += b
+            S = h_
+        return S
+
+    def _segment_nodes(self, name, phases, deps):
+        """Chain steps for a run of levels: one PDL launch per level, or (in
+        the persistent mode) one co-resident launch with grid barriers."""
+        phases = [P for P in phases if P.nitems > 0]
+        if not phases:
+            return []
+        if len(phases) == 1 or self.chain_mode != "persistent":
+            return [_Node(name, "chain", deps if i == 0 else [], phase=P) for i, P in enumerate(phases)]
+        assert _native.load().gc_panel_phase_bytes() == 96
+
+        def addr(t):
+            return ptr(t).value or 0
+        desc = np.array([[addr(P.items), P.nitems, addr(P.xidx), addr(P.A0), addr(P.A1), addr(P.in0),
+                          addr(P.in1), addr(P.out), addr(P.scratch), addr(P.red), addr(P.arrivals), 0]
+                         for P in phases], dtype=np.uint64)
+        dev_desc = to_dev(desc.view(np.int64), self.dev)
+        self._keep.append(dev_desc)
+        n = len(phases)
+
+        def launch():
+            _native.call("gc_panel_chain", n, ptr(dev_desc), self._chain_grid, ptr(self._barrier),
+                         stream_handle())
+        node = _Node(name, "chain", deps, fn=launch)
+        node.launches = 1
+        return [node]
+
+    def _build_nodes(self, gather=True, before_coupling=None, scatter=True):
+        """Nodes in a valid serial order (a topological order of the DAG)."""
+        st = stream_handle
+        nodes = []
+
+        def add(n):
+            nodes.append(n)
+            return len(nodes) - 1
+
+        def add_steps(name, phases, deps):
+            k = None
+            for n in self._segment_nodes(name, phases, deps):
+                k = add(n)
+            return k
+
+        persistent = self.chain_mode == "persistent"
+        S = self._split_height() if persistent else None
+        z = add(_Node("zero", "chain", fn=lambda: self.yhat.zero_()))
+        if gather:
+            g = add(_Node("gather", "chain", [z], fn=lambda: _native.call(
+                "gc_gather", ptr(self.x), ptr(self.perm_in), self.n_in, ptr(self.xt), st())))
+            nodes[g].launches = 1
+        else:
+            g = z
+        near = add(_Node("nearfield", "near", [g], phase=self._near)) if self._near.nitems else None
+        last = g
+        fwd_done = []                                   # (max height covered, node)
+        groups = ([[P for P in self._fwd if P.height < S], [P for P in self._fwd if P.height >= S]]
+                  if persistent else [[P] for P in self._fwd])
+        for grp in groups:
+            k = add_steps("forward", grp, [last])
+            if k is not None:
+                last = k
+                fwd_done.append((max(P.height for P in grp), k))
+        gate = None
+        if before_coupling is not None:
+            gate = add(_Node("pre-coupling", "chain", [last], fn=before_coupling))
+        bucket = {}
+        for P, colh in sorted(self._cpl, key=lambda c: c[0].height):
+            if gate is not None:
+                dep = gate
+            else:
+                dep = next((k for hh, k in fwd_done if hh >= colh), last)
+            bucket[P.height] = add(_Node("coupling", "c%d" % P.height, [dep, z], phase=P))
+        prev = gate if gate is not None else last
+        groups = ([[b for b in self._bwd if b[0].height > S], [b for b in self._bwd if b[0].height <= S]]
+                  if persistent else [[b] for b in self._bwd])
+        for grp in groups:
+            if not grp:
+                continue
+            need = sorted(set().union(*[hs for _, hs in grp]))
+            k = add_steps("backward", [P for P, _ in grp], [prev] + [bucket[x] for x in need if x in bucket])
+            if k is not None:
+                prev = k
+        tail = [prev] + list(bucket.values()) + ([near] if near is not None else [])
+        if self._leaf is not None and self._leaf.nitems:
+            prev = add(_Node("leafbasis", "chain", tail, phase=self._leaf))
+            tail = [prev]
+        if scatter:
+            k = add(_Node("scatter", "chain", tail, fn=lambda: _native.call(
+                "gc_scatter", ptr(self.yt), ptr(self.perm_out), self.n_out, ptr(self.y), st())))
+            nodes[k].launches = 1
+        else:
+            add(_Node("join", "chain", tail, fn=lambda: None))
+        return nodes
+
+    def _stream(self, key):
+        s = self.streams.get(key)
+        if s is None:
+            s = self.streams[key] = torch.cuda.Stream(device=self.dev, priority=self._bulk_priority)
+        return s
+
+    def _exec(self, nodes, serial=False, phase_events=None, phase="coupling"):
+        main = torch.cuda.current_stream()
+        if serial:
+            st = stream_handle()
+            first = lastn = None
+            for i, n in enumerate(nodes):
+                if n.name == phase:
+                    first = i if first is None else first
+                    lastn = i
+            for i, n in enumerate(nodes):
+                if phase_events is not None and i == first:
+                    phase_events[0].record(main)
+                if n.phase is not None:
+                    self._launch(n.phase, st, n.stream == "chain")
+                else:
+                    n.fn()
+                if phase_events is not None and i == lastn:
+                    phase_events[1].record(main)
+            return
+        fork = torch.cuda.Event()
+        fork.record(main)
+        events = [None] * len(nodes)
+        used = set()
+        for i, n in enumerate(nodes):
+            s = self._stream(n.stream)
+            if n.stream not in used:
+                s.wait_event(fork)
+                used.add(n.stream)
+            for dep in n.deps:
+                if nodes[dep].stream != n.stream:
+                    s.wait_event(events[dep])
+            with torch.cuda.stream(s):
+                if n.phase is not None:
+                    self._launch(n.phase, stream_handle(), n.stream == "chain")
+                else:
+                    n.fn()
+                ev = torch.cuda.Event()
+                ev.record(s)
+            events[i] = ev
+        for key in used:                       # rejoin every forked stream
+            last = max(i for i, n in enumerate(nodes) if n.stream == key)
+            main.wait_event(events[last])
+
+    # -- phases --------------------------------------------------------------
+    def _phase(self, name, height, panels, A0, A1, in0, in1, out, transform=False):
         a_off, K, T, rows, out_off, accumulate = panels
         a_off = np.asarray(a_off, np.int64)
         K = np.asarray(K, np.int64)
@@ -495,68 +704,56 @@ class PanelPlan:
         out_off = np.asarray(out_off, np.int64)
         n = len(a_off)
         elems = int((K * T).sum())
-        # chunk rows so every phase has >= ~4 items per SM when it can
-        target = max(256, min(_ITEM_ELEMS, elems // (148 * 4) + 1))
-        rpi = np.minimum(_ITEM_MAX_ROWS, np.maximum(1, -(-target // np.maximum(T, 1))))  # rows/item
+        if transform:
+            # transform levels: one item per panel (split only past the row
+            # cap) - these levels are latency-bound, and a split panel costs
+            # a second pass over L2 for its reduction
+            target = 1 << 40
+            max_rows = _WARP_MAX_ROWS if self.chain_mode == "persistent" else _ITEM_MAX_ROWS
+        else:
+            # chunk rows so every phase has >= ~4 items per SM when it can
+            target = max(256, min(_ITEM_ELEMS, elems // (148 * 4) + 1))
+            max_rows = _ITEM_MAX_ROWS
+        rpi = np.minimum(max_rows, np.maximum(1, -(-target // np.maximum(T, 1))))  # rows/item
         nit = np.maximum(1, -(-K // rpi))
         xidx = np.concatenate(rows).astype(np.int32) if n else np.zeros(1, np.int32)
         xoff = _offsets_np(K)
         item_panel = np.repeat(np.arange(n), nit)
-        item_k = _ranges_np(np.zeros(n, np.int64), nit) * rpi[item_panel]
+        item_idx_in_panel = _ranges_np(np.zeros(n, np.int64), nit)
+        item_k = item_idx_in_panel * rpi[item_panel]
         item_rows = np.minimum(rpi[item_panel], K[item_panel] - item_k)
         multi = nit > 1
         scr_off = _offsets_np(np.where(multi, nit * T, 0))
-        item_idx_in_panel = _ranges_np(np.zeros(n, np.int64), nit)
+        slot = np.cumsum(multi) - 1                  # reduction slot of each split panel
         direct = ~multi[item_panel]
         out_col = np.where(direct, out_off[item_panel],
                            scr_off[item_panel] + item_idx_in_panel * T[item_panel])
         mode = np.where(direct, 4 | (8 * accumulate), 0)
         items = np.stack([a_off[item_panel] + item_k * T[item_panel], xoff[item_panel] + item_k,
-                          out_col, T[item_panel], item_rows, mode], 1)
+                          out_col, T[item_panel], item_rows, mode,
+                          np.where(direct, -1, slot[item_panel]), np.zeros_like(mode)], 1)
         red = np.stack([out_off[multi], T[multi], scr_off[multi], nit[multi],
                         np.full(int(multi.sum()), accumulate)], 1)
         P = _Phase()
-        P.name = name
+        P.name, P.height = name, height
         P.items = to_dev(np.ascontiguousarray(items, np.int64), self.dev)
         P.xidx = to_dev(xidx, self.dev)
-        P.red = to_dev(np.ascontiguousarray(red, np.int64), self.dev) if multi.any() else None
         P.nitems, P.nred = len(items), int(multi.sum())
+        P.red = to_dev(np.ascontiguousarray(red, np.int64), self.dev) if P.nred else None
+        P.arrivals = torch.zeros(max(P.nred, 1), dtype=torch.int32, device=self.dev)
         P.A0, P.A1, P.in0, P.in1, P.out = A0, A1, in0, in1, out
         P.scratch = torch.zeros(max(int((np.where(multi, nit * T, 0)).sum()), 1),
                                 dtype=torch.float64, device=self.dev)
         P.bytes = 8 * elems
         return P
 
-    def _launch(self, P, stream):
+    def _launch(self, P, stream, chain=False):
         _native.call("gc_panelmv", P.nitems, ptr(P.items), ptr(P.xidx), ptr(P.A0), ptr(P.A1),
                      ptr(P.in0), ptr(P.in1), ptr(P.out), ptr(P.scratch), P.nred, ptr(P.red),
-                     stream)
+                     ptr(P.arrivals), int(chain), ptr(self.trace.get(id(P))), stream)
 
     def _body(self, phase_events=None, phase="coupling"):
-        main = torch.cuda.current_stream()
-        st = stream_handle()
-        _native.call("gc_gather", ptr(self.x), ptr(self.perm_in), self.n_in, ptr(self.xt), st)
-        fork = torch.cuda.Event()
-        fork.record(main)
-        with torch.cuda.stream(self.side):
-            self.side.wait_event(fork)
-            sst = stream_handle()
-            for P in self.side_phases:
-                self._launch(P, sst)
-            join = torch.cuda.Event()
-            join.record(self.side)
-        self.yhat.zero_()
-        for P in self.main_phases:
-            timed = phase_events is not None and P.name == phase
-            if timed:
-                phase_events[0].record(main)
-            self._launch(P, st)
-            if timed:
-                phase_events[1].record(main)
-        main.wait_event(join)
-        for P in self.tail_phases:
-            self._launch(P, st)
-        _native.call("gc_scatter", ptr(self.yt), ptr(self.perm_out), self.n_out, ptr(self.y), st)
+        self._exec(self.nodes, serial=phase_events is not None, phase_events=phase_events, phase=phase)
 
     def capture(self):
         """Record the product into a CUDA graph (static x -> y buffers)."""
@@ -573,21 +770,22 @@ class PanelPlan:
         self.graph = g
         return g
 
-    def run(self, x_dev, y_dev, phase_events=None, phase="coupling"):
-        """y_dev = H x_dev (device vectors, external ordering)."""
+    def run(self, x_dev, y_dev, phase_events=None, phase="coupling", serial=False):
+        """y_dev = H x_dev (device vectors, external ordering).  With
+        ``phase_events`` (or ``serial``) every node runs in order on the
+        current stream and the events bracket the named phase's kernels."""
         self.x.copy_(x_dev, non_blocking=True)
-        if phase_events is None and self.graph is not None:
+        if phase_events is None and not serial and self.graph is not None:
             self.graph.replay()
         else:
-            self._body(phase_events, phase)
+            self._exec(self.nodes, serial=serial or phase_events is not None,
+                       phase_events=phase_events, phase=phase)
         y_dev.copy_(self.y, non_blocking=True)
 
     @property
     def num_kernels(self):
-        n = 2
-        for P in self.main_phases + self.side_phases + self.tail_phases:
-            n += 1 + int(P.nred > 0)
-        return n
+        """Own kernels per product (the torch fill of y-hat not counted)."""
+        return sum(n.launches for n in self.nodes)
 
 
 def _offsets_np(sizes):

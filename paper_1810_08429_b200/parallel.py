@@ -192,41 +192,23 @@ def _shard_plan_class():
         slots are all-gathered before the coupling phase."""
 
         def __init__(self, sh):
+            import torch.distributed as dist
             super().__init__(sh.h)
             self.sh = sh
             self.lo, self.hi = sh.layout.lo, sh.layout.hi
             g = sh.layout.rank
             self.own_xhat = self.xhat[g * sh.slot:(g + 1) * sh.slot]
-            self.y_slice = None
+
+            def gather_xhat():
+                dist.all_gather_into_tensor(self.xhat, self.own_xhat.clone(), group=sh.group)
+
+            # no permutation steps; the x-hat all-gather gates every coupling bucket
+            self.nodes = self._build_nodes(gather=False, before_coupling=gather_xhat, scatter=False)
 
         def run(self, x_slice):
-            import torch
             import torch.distributed as dist
-            from . import _native
-            from .device import ptr, stream_handle
-            group = self.sh.group
-            dist.all_gather_into_tensor(self.xt, x_slice.contiguous(), group=group)
-            main = torch.cuda.current_stream()
-            fork = torch.cuda.Event()
-            fork.record(main)
-            with torch.cuda.stream(self.side):
-                self.side.wait_event(fork)
-                sst = stream_handle()
-                for P in self.side_phases:
-                    self._launch(P, sst)
-                join = torch.cuda.Event()
-                join.record(self.side)
-            st = stream_handle()
-            self.yhat.zero_()
-            for P in self.main_phases:
-                if P.name == "coupling":
-                    dist.all_gather_into_tensor(self.xhat, self.own_xhat.clone(), group=group)
-                self._launch(P, st)
-            if not any(P.name == "coupling" for P in self.main_phases):
-                dist.all_gather_into_tensor(self.xhat, self.own_xhat.clone(), group=group)
-            main.wait_event(join)
-            for P in self.tail_phases:
-                self._launch(P, st)
+            dist.all_gather_into_tensor(self.xt, x_slice.contiguous(), group=self.sh.group)
+            self._exec(self.nodes)
             return self.yt[self.lo:self.hi].clone()
 
     return ShardPlan

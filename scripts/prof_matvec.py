@@ -14,7 +14,7 @@ p = h2.plan(hm)
 x = torch.randn(mesh.nt, dtype=torch.float64, device="cuda"); y = torch.empty_like(x)
 for _ in range(5): p.run(x, y)
 torch.cuda.synchronize()
-phases = p.side_phases + p.main_phases + p.tail_phases
+phases = p.phases
 acc = {}
 for rep in range(15):
     evs = []
@@ -28,7 +28,7 @@ for rep in range(15):
 tot = 0
 for i, P in enumerate(phases):
     t = np.median(acc[i]); tot += t
-    print("%2d %-10s items %6d red %5d  %7.1f us  %6.1f MB  %6.0f GB/s" % (i, P.name, P.nitems, P.nred, 1e3 * t, P.bytes / 1e6, P.bytes / (t * 1e-3) / 1e9))
+    print("%2d %-10s h%-2d items %6d red %5d  %7.1f us  %6.1f MB  %6.0f GB/s" % (i, P.name, P.height, P.nitems, P.nred, 1e3 * t, P.bytes / 1e6, P.bytes / (t * 1e-3) / 1e9))
 print("sum of phases %.1f us" % (1e3 * tot))
 a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
 a.record()

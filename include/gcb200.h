@@ -193,14 +193,16 @@ int gc_segmv(int64_t nseg, const int64_t* seg, const int64_t* blk,
  * order: deterministic.  chain != 0 launches with programmatic stream
  * serialization (PDL): the kernel prefetches its matrix chunk while the
  * previous kernel on the stream drains and waits for it before reading in
- * (for the latency-bound transform levels).  trace (optional, NULL = off)
+ * (for the latency-bound transform levels).  priority != 0 sets the
+ * launch's scheduling priority (CUDA stream-priority scale, lower = more
+ * urgent; 0 = the stream's own).  trace (optional, NULL = off)
  * = [dev] 2 x uint64 receiving min(start) / max(end) %globaltimer (ns) of
  * the launch's CTAs, for timelines inside CUDA graphs. */
 int gc_panelmv(int64_t nitems, const int64_t* items, const int32_t* xidx,
                const double* A0, const double* A1, const double* in0,
                const double* in1, double* out, double* scratch, int64_t nred,
-               const int64_t* red, int32_t* arrivals, int32_t chain, uint64_t* trace,
-               void* stream);
+               const int64_t* red, int32_t* arrivals, int32_t chain, int32_t priority,
+               uint64_t* trace, void* stream);
 
 /* A run of consecutive transform levels (h2.py:63-70 forward, h2.py:74-79
  * backward) in ONE co-resident launch with grid barriers between levels.
@@ -213,6 +215,24 @@ int gc_panel_chain_grid(int64_t* grid);
 int gc_panel_chain(int64_t nphase, const void* phases, int64_t grid, uint32_t* barrier,
                    void* stream);
 int64_t gc_panel_phase_bytes(void);
+
+/* Bulk phase (coupling buckets, near field) on the TMA streaming kernel:
+ * same items/red/arrivals/trace as gc_panelmv (T <= 1024 per item), run by
+ * a co-resident grid of `grid` CTAs (gc_panel_stream_grid); CTA b works
+ * items [cta_begin[b], cta_begin[b+1]) [dev, grid+1 int64] in order.  One
+ * producer thread per CTA streams each item's rows into a 4-stage smem
+ * ring with cp.async.bulk (mbarrier completion); 8 consumer warps FMA them.
+ * Matrix buffers must be readable 16 bytes past their last element. */
+int gc_panel_stream_grid(int64_t* grid);
+int gc_panel_stream(int64_t nitems, const int64_t* items, const int32_t* xidx,
+                    const double* A0, const double* A1, const double* in0,
+                    const double* in1, double* out, double* scratch, int64_t nred,
+                    const int64_t* red, int32_t* arrivals, const int64_t* cta_begin,
+                    int64_t grid, int32_t priority, uint64_t* trace, void* stream);
+
+/* The device's scheduling-priority range (cudaDeviceGetStreamPriorityRange):
+ * least (default, e.g. 0) and greatest (most urgent, e.g. -5). */
+int gc_priority_range(int32_t* least, int32_t* greatest);
 
 /* The whole product y = H x as ONE persistent cooperative kernel scheduled
  * by dataflow counters (csrc/h2persist.cu; replaces h2.mvm, h2.py:63-80).

@@ -11,7 +11,7 @@ import os
 
 from .errors import ConfigError, DeviceError, GeometryError, GreencrossError, StateError
 
-LIB_PATH = os.path.join(os.path.dirname(os.path.abspath(__file__)), "libgcb200.so")
+LIB_PATH = os.environ.get("GC_LIB") or os.path.join(os.path.dirname(os.path.abspath(__file__)), "libgcb200.so")
 
 c_i64 = ctypes.c_int64
 c_p = ctypes.c_void_p
@@ -51,11 +51,15 @@ _SIGNATURES = {
     "gc_gather": [c_p, c_p, c_i64, c_p, c_p],
     "gc_scatter": [c_p, c_p, c_i64, c_p, c_p],
     "gc_segmv": [c_i64, c_p, c_p, c_p, c_p, c_p, c_p, c_p, ctypes.c_int, c_i64, c_p],
-    "gc_panelmv": [c_i64, c_p, c_p, c_p, c_p, c_p, c_p, c_p, c_p, c_i64, c_p, c_p, ctypes.c_int32, c_p,
-                   c_p],
+    "gc_panelmv": [c_i64, c_p, c_p, c_p, c_p, c_p, c_p, c_p, c_p, c_i64, c_p, c_p, ctypes.c_int32,
+                   ctypes.c_int32, c_p, c_p],
     "gc_panel_chain_grid": [ctypes.POINTER(c_i64)],
     "gc_panel_chain": [c_i64, c_p, c_i64, c_p, c_p],
     "gc_panel_phase_bytes": [],
+    "gc_panel_stream_grid": [ctypes.POINTER(c_i64)],
+    "gc_panel_stream": [c_i64, c_p, c_p, c_p, c_p, c_p, c_p, c_p, c_p, c_i64, c_p, c_p, c_p, c_i64,
+                        ctypes.c_int32, c_p, c_p],
+    "gc_priority_range": [ctypes.POINTER(ctypes.c_int32), ctypes.POINTER(ctypes.c_int32)],
     "gc_h2mv_persistent": [c_p, c_p, c_i64, ctypes.c_int32, c_p, ctypes.c_int32,
                            ctypes.POINTER(ctypes.c_int32),
                            c_p, c_p, c_i64, c_i64, ctypes.POINTER(c_p),

@@ -99,11 +99,15 @@ extern "C" int gc_segmv(int64_t nseg, const int64_t* seg, const int64_t* blk, co
 namespace gcb {
 
 constexpr int PAN_THREADS = 256;
-constexpr int PAN_UNROLL = 16;
+#ifndef GC_PAN_UNROLL
+#define GC_PAN_UNROLL 8
+#endif
+constexpr int PAN_UNROLL = GC_PAN_UNROLL;
 constexpr int PAN_MAX_ROWS = 1024;   // rows per work item (x gathered to smem)
 
 // item (8 x int64): a_off, xi_off, out_off, T, nrows, mode, red, 0
-//   mode bit0 A1, bit1 in1, bit2 direct to out, bit3 accumulate into out;
+//   mode bit0 A1, bit1 in1, bit2 direct to out, bit3 accumulate into out,
+//   bit4 prefetch the item's matrix chunk into L2 before the input gather;
 //   red = reduction slot of a split panel (items without bit2 write partial
 //   sums to scratch[out_off..]).
 // red slot (5 x int64): out_off, T, scratch_off, nitems, accumulate.
@@ -176,6 +180,9 @@ __device__ __forceinline__ void panel_item(const PanelPhase& P, int64_t item, Pa
             for (int r = threadIdx.x; r < nrows; r += PAN_THREADS) sm.xs[r] = __ldcg(x + __ldg(xi + r));
         }
     } else {
+        // bulk: start the item's matrix stream (L2 prefetch of the whole
+        // chunk) before the dependent index -> input gather
+        if (mode & 16) prefetch_l2(A, 8 * (int64_t)nrows * T);
         for (int r = threadIdx.x; r < nrows; r += PAN_THREADS) sm.xs[r] = __ldcg(x + __ldg(xi + r));
     }
     __syncthreads();
@@ -246,6 +253,201 @@ __global__ void __launch_bounds__(PAN_THREADS) k_panelmv(PanelPhase P) {
     if (P.trace != nullptr) {
         __syncthreads();
         if (threadIdx.x == 0) atomicMax(P.trace + 1, globaltimer());
+    }
+}
+
+// ---------------------------------------------------------------------------
+// Bulk phases (coupling buckets, near field): a TMA-fed streaming kernel.
+// A co-resident grid (2 CTAs per SM); CTA b owns the items
+// [cta_begin[b], cta_begin[b+1]) (equal bytes per CTA, set on the host).
+// One producer thread streams each item's matrix rows into a 4-stage
+// shared-memory ring with cp.async.bulk (row-aligned chunks of <= 16 KB,
+// completion counted on an mbarrier); 8 consumer warps gather the item's
+// input entries, wait for a stage, FMA it against them and release the
+// stage.  DRAM sees one long stream of 16 KB bulk reads per CTA with up to
+// 64 KB in flight, independent of the consumers' gather/reduce latency.
+// Summation order is fixed by (item, chunk, row group): deterministic.
+// Every matrix buffer must be readable 16 bytes past its last element (the
+// bulk copies are widened to 16-byte boundaries).
+constexpr int ST_STAGES = 4;
+constexpr int ST_ELEMS = 2048;                 // 16 KB of matrix per stage
+constexpr int ST_PAD = 4;                      // 16-byte widening slack (doubles)
+constexpr int ST_CONSUMERS = 256;
+constexpr int ST_THREADS = ST_CONSUMERS + 32;  // + 1 producer warp
+constexpr int ST_MAX_T = 1024;                 // 4 outputs per consumer thread
+
+struct StreamSmem {
+    double stage[ST_STAGES][ST_ELEMS + ST_PAD];
+    double xs[PAN_MAX_ROWS];
+    double red[ST_CONSUMERS];
+    unsigned long long full[ST_STAGES];
+    unsigned long long empty[ST_STAGES];
+    int last;
+};
+
+__device__ __forceinline__ uint32_t smem_u32(const void* p) {
+    return static_cast<uint32_t>(__cvta_generic_to_shared(p));
+}
+__device__ __forceinline__ void mbar_init(unsigned long long* b, unsigned count) {
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(b)), "r"(count));
+}
+__device__ __forceinline__ void mbar_wait(unsigned long long* b, unsigned parity) {
+    const uint32_t a = smem_u32(b);
+    uint32_t done = 0;
+    while (!done) {
+        asm volatile(
+            "{\n .reg .pred p;\n mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n"
+            " selp.u32 %0, 1, 0, p;\n}\n"
+            : "=r"(done) : "r"(a), "r"(parity) : "memory");
+    }
+}
+__device__ __forceinline__ void mbar_arrive(unsigned long long* b) {
+    asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(b)) : "memory");
+}
+__device__ __forceinline__ void mbar_expect_tx(unsigned long long* b, unsigned bytes) {
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(b)), "r"(bytes)
+                 : "memory");
+}
+__device__ __forceinline__ void bulk_g2s(void* dst, const void* src, unsigned bytes, unsigned long long* b) {
+    asm volatile(
+        "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];"
+        ::"r"(smem_u32(dst)), "l"(src), "r"(bytes), "r"(smem_u32(b)) : "memory");
+}
+__device__ __forceinline__ void consumers_sync() {
+    asm volatile("bar.sync 1, %0;" ::"n"(ST_CONSUMERS) : "memory");
+}
+
+__global__ void __launch_bounds__(ST_THREADS) k_panel_stream(PanelPhase P, const int64_t* __restrict__ cta_begin) {
+    extern __shared__ __align__(128) unsigned char st_raw[];
+    StreamSmem& sm = *reinterpret_cast<StreamSmem*>(st_raw);
+    const int tid = threadIdx.x;
+    const int64_t beg = cta_begin[blockIdx.x], end = cta_begin[blockIdx.x + 1];
+    if (tid == 0) {
+        for (int s = 0; s < ST_STAGES; ++s) {
+            mbar_init(&sm.full[s], 1);
+            mbar_init(&sm.empty[s], ST_CONSUMERS / 32);
+        }
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    }
+    __syncthreads();
+    if (P.trace != nullptr && tid == 0) atomicMin(P.trace, globaltimer());
+    if (tid >= ST_CONSUMERS) {
+        // producer: one lane streams every chunk of every owned item
+        if (tid == ST_CONSUMERS) {
+            int stage = 0;
+            unsigned phase = 0;
+            for (int64_t i = beg; i < end; ++i) {
+                const int64_t* it = P.items + 8 * i;
+                const int T = (int)it[3], nrows = (int)it[4], mode = (int)it[5];
+                const double* A = ((mode & 1) ? P.A1 : P.A0) + it[0];
+                const int rc = ST_ELEMS / T;
+                for (int r0 = 0; r0 < nrows; r0 += rc) {
+                    const int rows = min(rc, nrows - r0);
+                    const uintptr_t src = reinterpret_cast<uintptr_t>(A + (int64_t)r0 * T);
+                    const uintptr_t al = src & ~uintptr_t(15);
+                    const unsigned bytes = (unsigned)(((src - al) + (uintptr_t)rows * T * 8 + 15) & ~uintptr_t(15));
+                    mbar_wait(&sm.empty[stage], phase ^ 1);
+                    mbar_expect_tx(&sm.full[stage], bytes);
+                    bulk_g2s(sm.stage[stage], reinterpret_cast<const void*>(al), bytes, &sm.full[stage]);
+                    if (++stage == ST_STAGES) { stage = 0; phase ^= 1; }
+                }
+            }
+        }
+        return;
+    }
+    // consumers
+    const int lane = tid & 31;
+    int stage = 0;
+    unsigned phase = 0;
+    for (int64_t i = beg; i < end; ++i) {
+        const int64_t* it = P.items + 8 * i;
+        const int64_t out_off = it[2];
+        const int T = (int)it[3], nrows = (int)it[4], mode = (int)it[5];
+        const double* A = ((mode & 1) ? P.A1 : P.A0) + it[0];
+        const double* x = (mode & 2) ? P.in1 : P.in0;
+        const int32_t* __restrict__ xi = P.xidx + it[1];
+        consumers_sync();                                     // xs / red free
+        for (int r = tid; r < nrows; r += ST_CONSUMERS) sm.xs[r] = __ldcg(x + __ldg(xi + r));
+        consumers_sync();
+        const int tt = T < ST_CONSUMERS ? T : ST_CONSUMERS;
+        const int ng = ST_CONSUMERS / tt;
+        const int g = tid / tt, tl = tid - g * tt;
+        const int J = (T + ST_CONSUMERS - 1) / ST_CONSUMERS;
+        double acc[4] = {0.0, 0.0, 0.0, 0.0};
+        const int rc = ST_ELEMS / T;
+        for (int r0 = 0; r0 < nrows; r0 += rc) {
+            const int rows = min(rc, nrows - r0);
+            const uintptr_t src = reinterpret_cast<uintptr_t>(A + (int64_t)r0 * T);
+            const int lead = (int)((src & 15) >> 3);
+            mbar_wait(&sm.full[stage], phase);
+            const double* C = sm.stage[stage] + lead;
+            const double* xr = sm.xs + r0;
+            if (g < ng) {
+                if (J == 1) {
+                    double a0 = 0.0, a1 = 0.0;
+                    int lr = g;
+                    for (; lr + ng < rows; lr += 2 * ng) {
+                        a0 = fma(C[lr * T + tl], xr[lr], a0);
+                        a1 = fma(C[(lr + ng) * T + tl], xr[lr + ng], a1);
+                    }
+                    if (lr < rows) a0 = fma(C[lr * T + tl], xr[lr], a0);
+                    acc[0] += a0 + a1;
+                } else {
+                    for (int lr = 0; lr < rows; ++lr) {
+                        const double xv = xr[lr];
+#pragma unroll
+                        for (int j = 0; j < 4; ++j) {
+                            const int t = tl + ST_CONSUMERS * j;
+                            if (j < J && t < T) acc[j] = fma(C[lr * T + t], xv, acc[j]);
+                        }
+                    }
+                }
+            }
+            __syncwarp();
+            if (lane == 0) mbar_arrive(&sm.empty[stage]);
+            if (++stage == ST_STAGES) { stage = 0; phase ^= 1; }
+        }
+        double* dst = (mode & 4) ? P.out + out_off : P.scratch + out_off;
+        const bool add = (mode & 12) == 12;
+        if (J == 1) {
+            sm.red[tid] = acc[0];
+            consumers_sync();
+            if (tid < T) {
+                double s = sm.red[tid];
+                for (int q = 1; q < ng; ++q) s += sm.red[q * T + tid];
+                dst[tid] = add ? __ldcg(dst + tid) + s : s;
+            }
+        } else {
+#pragma unroll
+            for (int j = 0; j < 4; ++j) {
+                const int t = tl + ST_CONSUMERS * j;
+                if (j < J && t < T) dst[t] = add ? __ldcg(dst + t) + acc[j] : acc[j];
+            }
+        }
+        if (mode & 4) continue;
+        // split panel: the last CTA to finish adds the partial sums in item order
+        const int slot = (int)it[6];
+        const int64_t* rd = P.red + 5 * (int64_t)slot;
+        __threadfence();
+        consumers_sync();
+        if (tid == 0) sm.last = atomicAdd(P.arrivals + slot, 1) == (int)rd[3] - 1;
+        consumers_sync();
+        if (!sm.last) continue;
+        __threadfence();
+        const int64_t o_off = rd[0], so = rd[2];
+        const int RT = (int)rd[1], ni = (int)rd[3];
+        const bool accum = rd[4] != 0;
+        for (int t = tid; t < RT; t += ST_CONSUMERS) {
+            double v = __ldcg(P.scratch + so + t);
+            for (int k = 1; k < ni; ++k) v += __ldcg(P.scratch + so + (int64_t)k * RT + t);
+            P.out[o_off + t] = accum ? __ldcg(P.out + o_off + t) + v : v;
+        }
+        consumers_sync();
+        if (tid == 0) P.arrivals[slot] = 0;
+    }
+    if (P.trace != nullptr) {
+        consumers_sync();
+        if (tid == 0) atomicMax(P.trace + 1, globaltimer());
     }
 }
 
@@ -379,8 +581,8 @@ __global__ void __launch_bounds__(PAN_THREADS) k_panel_chain(const PanelPhase* _
 
 }  // namespace gcb
 
-// the chain's kernels carry the device's highest scheduling priority, so
-// their CTAs are dispatched ahead of the queued bulk phases
+// the persistent chain kernel carries the device's highest scheduling
+// priority, so its CTAs are dispatched ahead of the queued bulk phases
 static int top_priority() {
     int least = 0, greatest = 0;
     if (cudaDeviceGetStreamPriorityRange(&least, &greatest) != cudaSuccess) return 0;
@@ -399,31 +601,34 @@ static int check_phase(int64_t nitems, int64_t nred, const int64_t* red, const i
 extern "C" int gc_panelmv(int64_t nitems, const int64_t* items, const int32_t* xidx,
                           const double* A0, const double* A1, const double* in0,
                           const double* in1, double* out, double* scratch, int64_t nred,
-                          const int64_t* red, int32_t* arrivals, int32_t chain, uint64_t* trace,
-                          void* stream) {
+                          const int64_t* red, int32_t* arrivals, int32_t chain, int32_t priority,
+                          uint64_t* trace, void* stream) {
     using namespace gcb;
     if (nitems <= 0) return GC_OK;
     if (int rc = check_phase(nitems, nred, red, arrivals)) return rc;
     const PanelPhase P{items, nitems, xidx, A0, A1, in0, in1, out, scratch, red, arrivals,
                        (unsigned long long*)trace};
-    if (!chain) {
-        k_panelmv<false><<<(unsigned)nitems, PAN_THREADS, 0, (cudaStream_t)stream>>>(P);
-        GC_CHECK_LAUNCH("k_panelmv");
-        return GC_OK;
-    }
     cudaLaunchConfig_t cfg = {};
     cfg.gridDim = dim3((unsigned)nitems);
     cfg.blockDim = dim3(PAN_THREADS);
     cfg.stream = (cudaStream_t)stream;
     cudaLaunchAttribute attr[2];
-    attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
-    attr[0].val.programmaticStreamSerializationAllowed = 1;
-    attr[1].id = cudaLaunchAttributePriority;
-    attr[1].val.priority = top_priority();
+    int na = 0;
+    if (chain) {
+        attr[na].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+        attr[na].val.programmaticStreamSerializationAllowed = 1;
+        ++na;
+    }
+    if (priority != 0) {
+        attr[na].id = cudaLaunchAttributePriority;
+        attr[na].val.priority = priority;
+        ++na;
+    }
     cfg.attrs = attr;
-    cfg.numAttrs = 2;
-    cudaError_t e = cudaLaunchKernelEx(&cfg, k_panelmv<true>, P);
-    if (e != cudaSuccess) return cuda_status(e, "k_panelmv (chain)");
+    cfg.numAttrs = na;
+    cudaError_t e = chain ? cudaLaunchKernelEx(&cfg, k_panelmv<true>, P)
+                          : cudaLaunchKernelEx(&cfg, k_panelmv<false>, P);
+    if (e != cudaSuccess) return cuda_status(e, "k_panelmv");
     count_launch();
     return GC_OK;
 }
@@ -465,3 +670,65 @@ extern "C" int gc_panel_chain(int64_t nphase, const void* phases, int64_t grid, 
 }
 
 extern "C" int64_t gc_panel_phase_bytes(void) { return (int64_t)sizeof(gcb::PanelPhase); }
+
+extern "C" int gc_priority_range(int32_t* least, int32_t* greatest) {
+    using namespace gcb;
+    int l = 0, g = 0;
+    cudaError_t e = cudaDeviceGetStreamPriorityRange(&l, &g);
+    if (e != cudaSuccess) return cuda_status(e, "gc_priority_range");
+    *least = l;
+    *greatest = g;
+    return GC_OK;
+}
+
+extern "C" int gc_panel_stream_grid(int64_t* grid) {
+    using namespace gcb;
+    int dev = 0, sms = 0, per_sm = 0;
+    cudaError_t e = cudaGetDevice(&dev);
+    if (e == cudaSuccess) e = cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    if (e == cudaSuccess)
+        e = cudaFuncSetAttribute(k_panel_stream, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sizeof(StreamSmem));
+    if (e == cudaSuccess)
+        e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_panel_stream, ST_THREADS, sizeof(StreamSmem));
+    if (e != cudaSuccess) return cuda_status(e, "gc_panel_stream_grid");
+    *grid = (int64_t)sms * (per_sm < 2 ? per_sm : 2);
+    return GC_OK;
+}
+
+extern "C" int gc_panel_stream(int64_t nitems, const int64_t* items, const int32_t* xidx,
+                               const double* A0, const double* A1, const double* in0,
+                               const double* in1, double* out, double* scratch, int64_t nred,
+                               const int64_t* red, int32_t* arrivals, const int64_t* cta_begin,
+                               int64_t grid, int32_t priority, uint64_t* trace, void* stream) {
+    using namespace gcb;
+    if (nitems <= 0) return GC_OK;
+    if (int rc = check_phase(nitems, nred, red, arrivals)) return rc;
+    if (grid <= 0 || cta_begin == nullptr) { set_error(GC_ERR_CONFIG, "gc_panel_stream: bad grid"); return GC_ERR_CONFIG; }
+    const PanelPhase P{items, nitems, xidx, A0, A1, in0, in1, out, scratch, red, arrivals,
+                       (unsigned long long*)trace};
+    static bool attr_set = false;
+    if (!attr_set) {
+        cudaError_t e = cudaFuncSetAttribute(k_panel_stream, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                             (int)sizeof(StreamSmem));
+        if (e != cudaSuccess) return cuda_status(e, "k_panel_stream smem attribute");
+        attr_set = true;
+    }
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3((unsigned)grid);
+    cfg.blockDim = dim3(ST_THREADS);
+    cfg.dynamicSmemBytes = sizeof(StreamSmem);
+    cfg.stream = (cudaStream_t)stream;
+    cudaLaunchAttribute attr[1];
+    int na = 0;
+    if (priority != 0) {
+        attr[na].id = cudaLaunchAttributePriority;
+        attr[na].val.priority = priority;
+        ++na;
+    }
+    cfg.attrs = attr;
+    cfg.numAttrs = na;
+    cudaError_t e = cudaLaunchKernelEx(&cfg, k_panel_stream, P, cta_begin);
+    if (e != cudaSuccess) return cuda_status(e, "k_panel_stream");
+    count_launch();
+    return GC_OK;
+}

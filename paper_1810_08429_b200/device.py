@@ -56,6 +56,23 @@ def empty(shape, device, dtype=None):
     return torch.empty(shape, dtype=dtype or torch.float64, device=device)
 
 
+TAIL_PAD = 4   # doubles readable past the end of a panel buffer (16-byte bulk copies)
+
+
+def padded_empty(n, device):
+    """float64 vector of n entries whose storage extends TAIL_PAD zeros past
+    the end (matrix storage streamed by widened cp.async.bulk copies)."""
+    t = torch.empty(n + TAIL_PAD, dtype=torch.float64, device=device)
+    t[n:].zero_()
+    return t[:n]
+
+
+def padded_copy(src):
+    out = padded_empty(src.numel(), src.device)
+    out.copy_(src)
+    return out
+
+
 class DeviceMesh:
     """Chart data of one plane mesh on one device, for one regular order.
 

@@ -25,8 +25,8 @@ import numpy as np
 
 from . import _native
 from .assembly import device_block_assembly, green_factors_device
-from .device import (DeviceMesh, DeviceRules, SingularQueue, check_mesh, empty, ptr,
-                     require_device, stream_handle, to_dev, torch)
+from .device import (DeviceMesh, DeviceRules, SingularQueue, check_mesh, empty, padded_copy,
+                     padded_empty, ptr, require_device, stream_handle, to_dev, torch)
 from .errors import ConfigError, GeometryError
 from .quadrature import _gauss01
 
@@ -433,13 +433,13 @@ def build_cluster_bases(tree, mesh, basis, m, delta_factor, eps, sides, orders=(
         st = s.store
         st.pivots_host = s.gpiv[:s.cursor].copy()
         st.pivots = to_dev(st.pivots_host if s.cursor else np.zeros(1, np.int64), dev)
-        st.V = torch.cat(s.v_parts) if s.v_parts else empty(1, dev)
+        st.V = padded_copy(torch.cat(s.v_parts)) if s.v_parts else padded_empty(1, dev)
         if st.V.numel() == 0:
-            st.V = torch.zeros(1, dtype=torch.float64, device=dev)
+            st.V = padded_empty(1, dev).zero_()
         if s.side == "row" and s.mat.any():
             ids = np.flatnonzero(s.mat & (st.rank > 0))
             tdesc = to_dev(np.stack([st.v_off[ids], st.rows[ids], st.rank[ids]], 1), dev)
-            st.VT = torch.zeros_like(st.V)
+            st.VT = padded_empty(st.V.numel(), dev).zero_()
             with torch.cuda.device(dev):
                 _native.call("gc_batched_transpose", len(ids), ptr(tdesc), ptr(st.V),
                              ptr(st.VT), stream)
@@ -582,7 +582,7 @@ def build_h2(btree, row_basis, col_basis, mesh, kind="slp", basis="constant",
     # contiguous (sum r_sigma) x r_tau panel for the matvec (h2.PanelPlan)
     c_off = _grouped_offsets(cr, c_nr * c_nc)
     c_total = int((c_nr * c_nc).sum())
-    coup = empty(max(c_total, 1), dev)
+    coup = padded_empty(max(c_total, 1), dev)
     cdesc = np.stack([rstore.piv_off[cr], c_nr, cstore.piv_off[cc], c_nc, c_off], 1)
     keep = (c_nr > 0) & (c_nc > 0)
     stats_c = device_block_assembly(dmesh, rules, queue, rstore.pivots, cstore.pivots,
@@ -592,7 +592,7 @@ def build_h2(btree, row_basis, col_basis, mesh, kind="slp", basis="constant",
     n_nr = rf.stop[nr_r] - rf.start[nr_r]
     n_nc = cf.stop[nc_r] - cf.start[nc_r]
     n_off = _grouped_offsets(nr_r, n_nr * n_nc)
-    near = empty(max(int((n_nr * n_nc).sum()), 1), dev)
+    near = padded_empty(max(int((n_nr * n_nc).sum()), 1), dev)
     perm_r = to_dev(rf.perm, dev)
     perm_c = perm_r if cf is rf else to_dev(cf.perm, dev)
     ndesc = np.stack([rf.start[nr_r], n_nr, cf.start[nc_r], n_nc, n_off], 1)

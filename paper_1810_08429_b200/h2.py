@@ -397,24 +397,26 @@ def cgnr_solve(apply, b, tol=1e-8, max_iter=500):
 # --------------------------------------------------------------------------
 # panel plan: the non-transposed product (the benchmarked hot path)
 
-_ITEM_ELEMS = 8192          # ~64 KB of matrix data per work item
+_ITEM_ELEMS = int(os.environ.get("GC_ITEM_ELEMS", 16384))  # ~128 KB of matrix data per work item
 _ITEM_MAX_ROWS = 1024       # PAN_MAX_ROWS in csrc/h2mv.cu
 _WARP_MAX_ROWS = 256        # WARP_MAX_ROWS in csrc/h2mv.cu
+_STREAM_MAX_T = 1024        # ST_MAX_T in csrc/h2mv.cu
 
 
 class _Phase:
     __slots__ = ("name", "height", "items", "xidx", "red", "arrivals", "nitems", "nred", "A0", "A1",
-                 "in0", "in1", "out", "scratch", "bytes")
+                 "in0", "in1", "out", "scratch", "bytes", "cta", "in_elems", "out_elems")
 
 
 class _Node:
     """One step of the product DAG: a panel phase or a host callable
     (gather, zero, scatter, a collective), run on ``stream`` after ``deps``."""
-    __slots__ = ("name", "phase", "fn", "stream", "deps", "launches")
+    __slots__ = ("name", "phase", "fn", "stream", "deps", "launches", "priority")
 
-    def __init__(self, name, stream, deps=(), phase=None, fn=None):
+    def __init__(self, name, stream, deps=(), phase=None, fn=None, priority=0):
         self.name, self.stream, self.deps, self.phase, self.fn = name, stream, list(deps), phase, fn
         self.launches = 1 if phase is not None else 0
+        self.priority = priority
 
 
 class PanelPlan:
@@ -457,6 +459,8 @@ class PanelPlan:
         grid = _native.ctypes.c_int64(0)
         _native.call("gc_panel_chain_grid", _native.ctypes.byref(grid))
         self._chain_grid = grid.value
+        _native.call("gc_panel_stream_grid", _native.ctypes.byref(grid))
+        self._stream_grid = grid.value
         size_r = rf.stop - rf.start
         # forward transform (column basis), by height
         fwd = []
@@ -530,6 +534,9 @@ class PanelPlan:
         # scheduled ahead of the queued bulk (coupling buckets, near field)
         self.streams = {"chain": torch.cuda.Stream(device=dev, priority=-8)}
         self._bulk_priority = 0
+        least, greatest = _native.ctypes.c_int32(0), _native.ctypes.c_int32(0)
+        _native.call("gc_priority_range", _native.ctypes.byref(least), _native.ctypes.byref(greatest))
+        self._prio = (least.value, greatest.value)
         self._keep = []
         self._barrier = torch.zeros(1, dtype=torch.int32, device=dev)
         self.trace = {}                    # id(phase) -> [2] int64 (profiling only)
@@ -538,10 +545,12 @@ class PanelPlan:
 
     # -- DAG -----------------------------------------------------------------
     def _split_height(self):
-        """Chain split for the persistent mode: levels below S and above S
-        form separate launches, S the lowest height whose buckets together
-        hold <= 20% of the coupling bytes (the big deep buckets then only
-        gate the lower backward launch)."""
+        """S = the lowest height whose coupling buckets together hold <= 20%
+        of the coupling bytes.  Buckets at height >= S are small and gate
+        the top of the backward chain: they get the chain's priority.  The
+        deep buckets below S are the bulk: lower priority, and the higher
+        the bucket the sooner the backward chain needs it, so the higher its
+        priority.  (The persistent mode also splits its launches at S.)"""
         if not self._cpl:
             return 0
         by_h = sorted(((P.height, P.bytes) for P, _ in self._cpl), reverse=True)
@@ -561,7 +570,8 @@ class PanelPlan:
         if not phases:
             return []
         if len(phases) == 1 or self.chain_mode != "persistent":
-            return [_Node(name, "chain", deps if i == 0 else [], phase=P) for i, P in enumerate(phases)]
+            return [_Node(name, "chain", deps if i == 0 else [], phase=P, priority=self._prio[1])
+                    for i, P in enumerate(phases)]
         assert _native.load().gc_panel_phase_bytes() == 96
 
         def addr(t):
@@ -596,7 +606,9 @@ class PanelPlan:
             return k
 
         persistent = self.chain_mode == "persistent"
-        S = self._split_height() if persistent else None
+        S = self._split_height()
+        least, greatest = self._prio
+        levels = least - greatest
         z = add(_Node("zero", "chain", fn=lambda: self.yhat.zero_()))
         if gather:
             g = add(_Node("gather", "chain", [z], fn=lambda: _native.call(
@@ -623,7 +635,12 @@ class PanelPlan:
                 dep = gate
             else:
                 dep = next((k for hh, k in fwd_done if hh >= colh), last)
-            bucket[P.height] = add(_Node("coupling", "c%d" % P.height, [dep, z], phase=P))
+            if P.height >= S or levels < 2:
+                prio = greatest
+            else:
+                prio = least - 1 - int(round(P.height * (levels - 2) / max(S - 1, 1)))
+                prio = min(least - 1, max(greatest + 1, prio))
+            bucket[P.height] = add(_Node("coupling", "c%d" % P.height, [dep, z], phase=P, priority=prio))
         prev = gate if gate is not None else last
         groups = ([[b for b in self._bwd if b[0].height > S], [b for b in self._bwd if b[0].height <= S]]
                   if persistent else [[b] for b in self._bwd])
@@ -636,7 +653,7 @@ class PanelPlan:
                 prev = k
         tail = [prev] + list(bucket.values()) + ([near] if near is not None else [])
         if self._leaf is not None and self._leaf.nitems:
-            prev = add(_Node("leafbasis", "chain", tail, phase=self._leaf))
+            prev = add(_Node("leafbasis", "chain", tail, phase=self._leaf, priority=greatest))
             tail = [prev]
         if scatter:
             k = add(_Node("scatter", "chain", tail, fn=lambda: _native.call(
@@ -665,7 +682,7 @@ class PanelPlan:
                 if phase_events is not None and i == first:
                     phase_events[0].record(main)
                 if n.phase is not None:
-                    self._launch(n.phase, st, n.stream == "chain")
+                    self._launch(n.phase, st, n.stream == "chain", n.priority)
                 else:
                     n.fn()
                 if phase_events is not None and i == lastn:
@@ -685,7 +702,7 @@ class PanelPlan:
                     s.wait_event(events[dep])
             with torch.cuda.stream(s):
                 if n.phase is not None:
-                    self._launch(n.phase, stream_handle(), n.stream == "chain")
+                    self._launch(n.phase, stream_handle(), n.stream == "chain", n.priority)
                 else:
                     n.fn()
                 ev = torch.cuda.Event()
@@ -729,6 +746,8 @@ class PanelPlan:
         out_col = np.where(direct, out_off[item_panel],
                            scr_off[item_panel] + item_idx_in_panel * T[item_panel])
         mode = np.where(direct, 4 | (8 * accumulate), 0)
+        if not transform and os.environ.get("GC_BULK_PREFETCH", "0") == "1":
+            mode = mode | 16
         items = np.stack([a_off[item_panel] + item_k * T[item_panel], xoff[item_panel] + item_k,
                           out_col, T[item_panel], item_rows, mode,
                           np.where(direct, -1, slot[item_panel]), np.zeros_like(mode)], 1)
@@ -745,12 +764,28 @@ class PanelPlan:
         P.scratch = torch.zeros(max(int((np.where(multi, nit * T, 0)).sum()), 1),
                                 dtype=torch.float64, device=self.dev)
         P.bytes = 8 * elems
+        P.in_elems, P.out_elems = int(K.sum()), int(T.sum())
+        P.cta = None
+        if (not transform and n and int(T.max()) <= _STREAM_MAX_T and self._stream_grid > 0
+                and os.environ.get("GC_BULK_KERNEL", "panel") == "stream"):
+            # bulk phase: TMA streaming kernel, items split over the
+            # co-resident grid by equal bytes (+ a per-item latency charge)
+            cost = np.cumsum(8 * item_rows * T[item_panel] + 4096)
+            G = self._stream_grid
+            begin = np.searchsorted(cost, cost[-1] * np.arange(1, G) / G, side="left")
+            P.cta = to_dev(np.r_[0, np.minimum(begin, len(items)), len(items)].astype(np.int64), self.dev)
         return P
 
-    def _launch(self, P, stream, chain=False):
+    def _launch(self, P, stream, chain=False, priority=0):
+        if P.cta is not None and not chain:
+            _native.call("gc_panel_stream", P.nitems, ptr(P.items), ptr(P.xidx), ptr(P.A0), ptr(P.A1),
+                         ptr(P.in0), ptr(P.in1), ptr(P.out), ptr(P.scratch), P.nred, ptr(P.red),
+                         ptr(P.arrivals), ptr(P.cta), self._stream_grid, int(priority),
+                         ptr(self.trace.get(id(P))), stream)
+            return
         _native.call("gc_panelmv", P.nitems, ptr(P.items), ptr(P.xidx), ptr(P.A0), ptr(P.A1),
                      ptr(P.in0), ptr(P.in1), ptr(P.out), ptr(P.scratch), P.nred, ptr(P.red),
-                     ptr(P.arrivals), int(chain), ptr(self.trace.get(id(P))), stream)
+                     ptr(P.arrivals), int(chain), int(priority), ptr(self.trace.get(id(P))), stream)
 
     def _body(self, phase_events=None, phase="coupling"):
         self._exec(self.nodes, serial=phase_events is not None, phase_events=phase_events, phase=phase)

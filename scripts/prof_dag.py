@@ -24,7 +24,7 @@ def subset(keep):
     out = []
     for i in idx:
         n = p.nodes[i]
-        out.append(h2._Node(n.name, n.stream, [remap[d] for d in n.deps if d in remap], n.phase, n.fn))
+        out.append(h2._Node(n.name, n.stream, [remap[d] for d in n.deps if d in remap], n.phase, n.fn, n.priority))
     return out
 
 
@@ -51,13 +51,14 @@ def time_graph(nodes, serial=False, reps=50):
 
 
 p.run(x, y)
-full = time_graph(p.nodes)
-print("full DAG        %7.1f us  %6.0f GB/s" % (full, nbytes / full / 1e3))
+for _ in range(3):
+    full = time_graph(p.nodes)
+    print("full DAG        %7.1f us  %6.0f GB/s" % (full, nbytes / full / 1e3))
 print("serial          %7.1f us" % time_graph(p.nodes, serial=True))
 chain = subset(lambda n: n.stream == "chain")
 print("chain only      %7.1f us  (%d nodes)" % (time_graph(chain), len(chain)))
-for n in p.nodes: print("   node", n.name, n.stream, n.deps, n.phase.height if n.phase else "")
-bulk = [h2._Node(n.name, n.stream, [], n.phase, n.fn) for n in p.nodes
+for n in p.nodes: print("   node", n.name, n.stream, n.deps, n.priority, n.phase.height if n.phase else "")
+bulk = [h2._Node(n.name, n.stream, [], n.phase, n.fn, n.priority) for n in p.nodes
         if n.name in ("coupling", "nearfield")]
 print("bulk only       %7.1f us  (%d nodes, concurrent)" % (time_graph(bulk), len(bulk)))
 print("bulk serial     %7.1f us" % time_graph(bulk, serial=True))
@@ -102,6 +103,6 @@ if os.environ.get("TIMELINE", "1") == "1":
         en = [r[id(n.phase)][1] - min(v[0] for v in r.values()) for r in res]
         rows.append((np.median(st) / 1e3, np.median(en) / 1e3, n))
     for a_, b_, n in sorted(rows, key=lambda r: r[0]):
-        print("  %-10s %-5s h%-2d %7.1f -> %7.1f  (%5.1f)  %6.1f MB" % (
-            n.name, n.stream, n.phase.height, a_, b_, b_ - a_, n.phase.bytes / 1e6))
+        print("  %-10s %-5s p%-2d h%-2d %7.1f -> %7.1f  (%5.1f)  %6.1f MB" % (
+            n.name, n.stream, n.priority, n.phase.height, a_, b_, b_ - a_, n.phase.bytes / 1e6))
     p.trace.clear()

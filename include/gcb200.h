@@ -193,7 +193,8 @@ int gc_segmv(int64_t nseg, const int64_t* seg, const int64_t* blk,
  * order: deterministic.  chain != 0 launches with programmatic stream
  * serialization (PDL): the kernel prefetches its matrix chunk while the
  * previous kernel on the stream drains and waits for it before reading in
- * (for the latency-bound transform levels).  priority != 0 sets the
+ * (for the latency-bound transform levels); chain = 1 releases the next
+ * launch at each CTA's start, chain = 2 after each CTA's item.  priority != 0 sets the
  * launch's scheduling priority (CUDA stream-priority scale, lower = more
  * urgent; 0 = the stream's own).  trace (optional, NULL = off)
  * = [dev] 2 x uint64 receiving min(start) / max(end) %globaltimer (ns) of
@@ -229,6 +230,18 @@ int gc_panel_stream(int64_t nitems, const int64_t* items, const int32_t* xidx,
                     const double* in1, double* out, double* scratch, int64_t nred,
                     const int64_t* red, int32_t* arrivals, const int64_t* cta_begin,
                     int64_t grid, int32_t priority, uint64_t* trace, void* stream);
+
+/* Bulk phase, one CTA per item, TMA-fed: each CTA moves its item's whole
+ * matrix chunk (<= gc_panel_tma_item_elems() doubles, T <= 256 per item not
+ * required) into shared memory with ONE cp.async.bulk (mbarrier
+ * completion) while it gathers the inputs.  Arguments as gc_panelmv.
+ * Matrix buffers must be readable 16 bytes past their last element. */
+int gc_panel_tma(int64_t nitems, const int64_t* items, const int32_t* xidx,
+                 const double* A0, const double* A1, const double* in0,
+                 const double* in1, double* out, double* scratch, int64_t nred,
+                 const int64_t* red, int32_t* arrivals, int32_t priority, uint64_t* trace,
+                 void* stream);
+int64_t gc_panel_tma_item_elems(void);
 
 /* The device's scheduling-priority range (cudaDeviceGetStreamPriorityRange):
  * least (default, e.g. 0) and greatest (most urgent, e.g. -5). */

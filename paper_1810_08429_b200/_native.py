@@ -57,6 +57,8 @@ _SIGNATURES = {
     "gc_panel_chain": [c_i64, c_p, c_i64, c_p, c_p],
     "gc_panel_phase_bytes": [],
     "gc_panel_stream_grid": [ctypes.POINTER(c_i64)],
+    "gc_panel_tma": [c_i64, c_p, c_p, c_p, c_p, c_p, c_p, c_p, c_p, c_i64, c_p, c_p, ctypes.c_int32, c_p, c_p],
+    "gc_panel_tma_item_elems": [],
     "gc_panel_stream": [c_i64, c_p, c_p, c_p, c_p, c_p, c_p, c_p, c_p, c_i64, c_p, c_p, c_p, c_i64,
                         ctypes.c_int32, c_p, c_p],
     "gc_priority_range": [ctypes.POINTER(ctypes.c_int32), ctypes.POINTER(ctypes.c_int32)],
@@ -72,7 +74,8 @@ _SIGNATURES = {
     "gc_dfma_probe": [c_i64, c_i64, c_i64, c_p, c_p],
 }
 _RESTYPES = {"gc_last_error": ctypes.c_char_p, "gc_launch_count": ctypes.c_uint64,
-             "gc_reset_launch_count": None, "gc_panel_phase_bytes": ctypes.c_int64}
+             "gc_reset_launch_count": None, "gc_panel_phase_bytes": ctypes.c_int64,
+             "gc_panel_tma_item_elems": ctypes.c_int64}
 
 EXPORTED = tuple(_SIGNATURES)
 ABI_VERSION = 1

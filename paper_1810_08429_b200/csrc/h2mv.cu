@@ -233,6 +233,7 @@ __device__ __forceinline__ void panel_item(const PanelPhase& P, int64_t item, Pa
     const bool accum = rd[4] != 0;
     for (int t = threadIdx.x; t < RT; t += PAN_THREADS) {
         double v = __ldcg(P.scratch + so + t);
+#pragma unroll 8
         for (int i = 1; i < ni; ++i) v += __ldcg(P.scratch + so + (int64_t)i * RT + t);
         P.out[o_off + t] = accum ? __ldcg(P.out + o_off + t) + v : v;
     }
@@ -244,12 +245,16 @@ __device__ __forceinline__ void panel_item(const PanelPhase& P, int64_t item, Pa
 // serialization - the kernel starts while its predecessor drains, reads its
 // descriptor and indices and prefetches its matrix chunk into L2, then
 // waits (griddepcontrol.wait) before it touches the input vector.
-template <bool CHAIN>
+// TRIGGER 1: the dependent launch is released at the CTA's start (its CTAs
+// then wait on SM slots); 2: after the CTA's item is done (the dependent
+// only overlaps this kernel's drain and keeps its slots free for the bulk).
+template <bool CHAIN, int TRIGGER>
 __global__ void __launch_bounds__(PAN_THREADS) k_panelmv(PanelPhase P) {
     __shared__ PanelSmem sm;
-    if (CHAIN) asm volatile("griddepcontrol.launch_dependents;");
+    if (CHAIN && TRIGGER == 1) asm volatile("griddepcontrol.launch_dependents;");
     if (P.trace != nullptr && threadIdx.x == 0) atomicMin(P.trace, globaltimer());
     panel_item<CHAIN>(P, blockIdx.x, sm);
+    if (CHAIN && TRIGGER == 2) asm volatile("griddepcontrol.launch_dependents;");
     if (P.trace != nullptr) {
         __syncthreads();
         if (threadIdx.x == 0) atomicMax(P.trace + 1, globaltimer());
@@ -451,6 +456,106 @@ __global__ void __launch_bounds__(ST_THREADS) k_panel_stream(PanelPhase P, const
     }
 }
 
+// ---------------------------------------------------------------------------
+// Bulk phases, one CTA per item, TMA-fed: thread 0 launches ONE cp.async.bulk
+// of the item's whole contiguous matrix chunk (<= TMA_ITEM_ELEMS doubles)
+// into shared memory, tracked by an mbarrier, and the CTA gathers the
+// item's input entries while the bytes are in flight; then it computes
+// from shared memory.  Every CTA puts its whole item in flight at once and
+// the hardware scheduler keeps 3 CTAs per SM streaming (the index -> input
+// gather no longer serialises with the matrix stream).
+constexpr int TMA_ITEM_ELEMS = 7168;            // 56 KB per item: 3 CTAs per SM
+
+struct TmaSmem {
+    double a[TMA_ITEM_ELEMS + ST_PAD];
+    double xs[PAN_MAX_ROWS];
+    double red[PAN_THREADS];
+    unsigned long long full;
+    int last;
+};
+
+__global__ void __launch_bounds__(PAN_THREADS) k_panel_tma(PanelPhase P) {
+    extern __shared__ __align__(128) unsigned char tma_raw[];
+    TmaSmem& sm = *reinterpret_cast<TmaSmem*>(tma_raw);
+    const int tid = threadIdx.x;
+    const int64_t* it = P.items + 8 * (int64_t)blockIdx.x;
+    const int64_t a_off = it[0], xi_off = it[1], out_off = it[2];
+    const int T = (int)it[3], nrows = (int)it[4], mode = (int)it[5];
+    const double* A = ((mode & 1) ? P.A1 : P.A0) + a_off;
+    const uintptr_t src = reinterpret_cast<uintptr_t>(A);
+    const uintptr_t al = src & ~uintptr_t(15);
+    const int lead = (int)((src - al) >> 3);
+    if (tid == 0) {
+        if (P.trace != nullptr) atomicMin(P.trace, globaltimer());
+        mbar_init(&sm.full, 1);
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+        const unsigned bytes = (unsigned)(((src - al) + (uintptr_t)nrows * T * 8 + 15) & ~uintptr_t(15));
+        mbar_expect_tx(&sm.full, bytes);
+        bulk_g2s(sm.a, reinterpret_cast<const void*>(al), bytes, &sm.full);
+    }
+    const double* x = (mode & 2) ? P.in1 : P.in0;
+    const int32_t* __restrict__ xi = P.xidx + xi_off;
+    for (int r = tid; r < nrows; r += PAN_THREADS) sm.xs[r] = __ldcg(x + __ldg(xi + r));
+    __syncthreads();                                  // xs ready, barrier initialised
+    mbar_wait(&sm.full, 0);
+    const double* C = sm.a + lead;
+    const int tt = T < PAN_THREADS ? T : PAN_THREADS;
+    const int ng = PAN_THREADS / tt;
+    const int g = tid / tt;
+    for (int t0 = 0; t0 < T; t0 += tt) {
+        const int t = t0 + (tid % tt);
+        double acc = 0.0;
+        if (g < ng && t < T) {
+            double a1 = 0.0;
+            int r = g;
+            for (; r + ng < nrows; r += 2 * ng) {
+                acc = fma(C[r * T + t], sm.xs[r], acc);
+                a1 = fma(C[(r + ng) * T + t], sm.xs[r + ng], a1);
+            }
+            if (r < nrows) acc = fma(C[r * T + t], sm.xs[r], acc);
+            acc += a1;
+        }
+        sm.red[tid] = acc;
+        __syncthreads();
+        if (tid < tt && t < T) {
+            double s = sm.red[tid];
+            for (int q = 1; q < ng; ++q) s += sm.red[q * tt + tid];
+            if (mode & 4) {
+                double* o = P.out + out_off + t;
+                *o = (mode & 8) ? __ldcg(o) + s : s;
+            } else {
+                P.scratch[out_off + t] = s;
+            }
+        }
+        __syncthreads();
+    }
+    if (!(mode & 4)) {
+        const int slot = (int)it[6];
+        const int64_t* rd = P.red + 5 * (int64_t)slot;
+        __threadfence();
+        __syncthreads();
+        if (tid == 0) sm.last = atomicAdd(P.arrivals + slot, 1) == (int)rd[3] - 1;
+        __syncthreads();
+        if (sm.last) {
+            __threadfence();
+            const int64_t o_off = rd[0], so = rd[2];
+            const int RT = (int)rd[1], ni = (int)rd[3];
+            const bool accum = rd[4] != 0;
+            for (int t = tid; t < RT; t += PAN_THREADS) {
+                double v = __ldcg(P.scratch + so + t);
+                for (int k = 1; k < ni; ++k) v += __ldcg(P.scratch + so + (int64_t)k * RT + t);
+                P.out[o_off + t] = accum ? __ldcg(P.out + o_off + t) + v : v;
+            }
+            __syncthreads();
+            if (tid == 0) P.arrivals[slot] = 0;
+        }
+    }
+    if (P.trace != nullptr) {
+        __syncthreads();
+        if (tid == 0) atomicMax(P.trace + 1, globaltimer());
+    }
+}
+
 // Grid-wide barrier (co-resident grid): every CTA adds 1 except CTA 0,
 // which adds 2^31 - (nb - 1), so each barrier flips bit 31 of the counter
 // and the counter never needs re-arming between launches.
@@ -626,8 +731,9 @@ extern "C" int gc_panelmv(int64_t nitems, const int64_t* items, const int32_t* x
     }
     cfg.attrs = attr;
     cfg.numAttrs = na;
-    cudaError_t e = chain ? cudaLaunchKernelEx(&cfg, k_panelmv<true>, P)
-                          : cudaLaunchKernelEx(&cfg, k_panelmv<false>, P);
+    cudaError_t e = chain == 1   ? cudaLaunchKernelEx(&cfg, k_panelmv<true, 1>, P)
+                    : chain == 2 ? cudaLaunchKernelEx(&cfg, k_panelmv<true, 2>, P)
+                                 : cudaLaunchKernelEx(&cfg, k_panelmv<false, 0>, P);
     if (e != cudaSuccess) return cuda_status(e, "k_panelmv");
     count_launch();
     return GC_OK;
@@ -732,3 +838,42 @@ extern "C" int gc_panel_stream(int64_t nitems, const int64_t* items, const int32
     count_launch();
     return GC_OK;
 }
+
+extern "C" int gc_panel_tma(int64_t nitems, const int64_t* items, const int32_t* xidx,
+                            const double* A0, const double* A1, const double* in0,
+                            const double* in1, double* out, double* scratch, int64_t nred,
+                            const int64_t* red, int32_t* arrivals, int32_t priority, uint64_t* trace,
+                            void* stream) {
+    using namespace gcb;
+    if (nitems <= 0) return GC_OK;
+    if (int rc = check_phase(nitems, nred, red, arrivals)) return rc;
+    const PanelPhase P{items, nitems, xidx, A0, A1, in0, in1, out, scratch, red, arrivals,
+                       (unsigned long long*)trace};
+    static bool attr_set = false;
+    if (!attr_set) {
+        cudaError_t e = cudaFuncSetAttribute(k_panel_tma, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                             (int)sizeof(TmaSmem));
+        if (e != cudaSuccess) return cuda_status(e, "k_panel_tma smem attribute");
+        attr_set = true;
+    }
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3((unsigned)nitems);
+    cfg.blockDim = dim3(PAN_THREADS);
+    cfg.dynamicSmemBytes = sizeof(TmaSmem);
+    cfg.stream = (cudaStream_t)stream;
+    cudaLaunchAttribute attr[1];
+    int na = 0;
+    if (priority != 0) {
+        attr[na].id = cudaLaunchAttributePriority;
+        attr[na].val.priority = priority;
+        ++na;
+    }
+    cfg.attrs = attr;
+    cfg.numAttrs = na;
+    cudaError_t e = cudaLaunchKernelEx(&cfg, k_panel_tma, P);
+    if (e != cudaSuccess) return cuda_status(e, "k_panel_tma");
+    count_launch();
+    return GC_OK;
+}
+
+extern "C" int64_t gc_panel_tma_item_elems(void) { return gcb::TMA_ITEM_ELEMS; }

@@ -405,7 +405,7 @@ _STREAM_MAX_T = 1024        # ST_MAX_T in csrc/h2mv.cu
 
 class _Phase:
     __slots__ = ("name", "height", "items", "xidx", "red", "arrivals", "nitems", "nred", "A0", "A1",
-                 "in0", "in1", "out", "scratch", "bytes", "cta", "in_elems", "out_elems")
+                 "in0", "in1", "out", "scratch", "bytes", "cta", "in_elems", "out_elems", "tma")
 
 
 class _Node:
@@ -456,6 +456,15 @@ class PanelPlan:
         # "pdl": one launch per transform level; "persistent": runs of levels
         # in one co-resident launch with grid barriers (experimental)
         self.chain_mode = os.environ.get("GC_CHAIN_MODE", "pdl")
+        # bulk phases: "panel" (plain 8-byte loads, 8 per thread in flight;
+        # the fastest measured), "tma" (one cp.async.bulk per item into
+        # shared memory) and "stream" (persistent producer/consumer ring)
+        # are kept as measured alternatives (matvec section)
+        self.bulk_kernel = os.environ.get("GC_BULK_KERNEL", "panel")
+        self._tma_elems = int(_native.load().gc_panel_tma_item_elems())
+        # chain launches: 0 = plain, 1 = PDL released at CTA start, 2 = PDL
+        # released after each CTA's item
+        self._pdl = int(os.environ.get("GC_CHAIN_PDL", "1"))
         grid = _native.ctypes.c_int64(0)
         _native.call("gc_panel_chain_grid", _native.ctypes.byref(grid))
         self._chain_grid = grid.value
@@ -727,11 +736,21 @@ class PanelPlan:
             # a second pass over L2 for its reduction
             target = 1 << 40
             max_rows = _WARP_MAX_ROWS if self.chain_mode == "persistent" else _ITEM_MAX_ROWS
+        elif self.bulk_kernel == "tma":
+            # TMA kernel: items fill its shared-memory tile
+            target = self._tma_elems
+            max_rows = _ITEM_MAX_ROWS
         else:
             # chunk rows so every phase has >= ~4 items per SM when it can
             target = max(256, min(_ITEM_ELEMS, elems // (148 * 4) + 1))
             max_rows = _ITEM_MAX_ROWS
-        rpi = np.minimum(max_rows, np.maximum(1, -(-target // np.maximum(T, 1))))  # rows/item
+        if not transform and self.bulk_kernel == "tma":
+            rpi = np.minimum(max_rows, np.maximum(1, target // np.maximum(T, 1)))  # fits the smem tile
+        else:
+            rpi = np.minimum(max_rows, np.maximum(1, -(-target // np.maximum(T, 1))))  # rows/item
+        # at most 8 items per panel: the last item of a split panel sums the
+        # partials serially, so deep splits of small phases cost latency
+        rpi = np.maximum(rpi, np.minimum(max_rows, -(-K // 8)))
         nit = np.maximum(1, -(-K // rpi))
         xidx = np.concatenate(rows).astype(np.int32) if n else np.zeros(1, np.int32)
         xoff = _offsets_np(K)
@@ -766,8 +785,9 @@ class PanelPlan:
         P.bytes = 8 * elems
         P.in_elems, P.out_elems = int(K.sum()), int(T.sum())
         P.cta = None
+        P.tma = bool(not transform and self.bulk_kernel == "tma" and n and int(T.max()) <= self._tma_elems)
         if (not transform and n and int(T.max()) <= _STREAM_MAX_T and self._stream_grid > 0
-                and os.environ.get("GC_BULK_KERNEL", "panel") == "stream"):
+                and self.bulk_kernel == "stream"):
             # bulk phase: TMA streaming kernel, items split over the
             # co-resident grid by equal bytes (+ a per-item latency charge)
             cost = np.cumsum(8 * item_rows * T[item_panel] + 4096)
@@ -783,9 +803,15 @@ class PanelPlan:
                          ptr(P.arrivals), ptr(P.cta), self._stream_grid, int(priority),
                          ptr(self.trace.get(id(P))), stream)
             return
+        if P.tma and not chain:
+            _native.call("gc_panel_tma", P.nitems, ptr(P.items), ptr(P.xidx), ptr(P.A0), ptr(P.A1),
+                         ptr(P.in0), ptr(P.in1), ptr(P.out), ptr(P.scratch), P.nred, ptr(P.red),
+                         ptr(P.arrivals), int(priority), ptr(self.trace.get(id(P))), stream)
+            return
         _native.call("gc_panelmv", P.nitems, ptr(P.items), ptr(P.xidx), ptr(P.A0), ptr(P.A1),
                      ptr(P.in0), ptr(P.in1), ptr(P.out), ptr(P.scratch), P.nred, ptr(P.red),
-                     ptr(P.arrivals), int(chain), int(priority), ptr(self.trace.get(id(P))), stream)
+                     ptr(P.arrivals), self._pdl if chain else 0, int(priority), ptr(self.trace.get(id(P))),
+                     stream)
 
     def _body(self, phase_events=None, phase="coupling"):
         self._exec(self.nodes, serial=phase_events is not None, phase_events=phase_events, phase=phase)

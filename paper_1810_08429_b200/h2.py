@@ -750,7 +750,8 @@ class PanelPlan:
             rpi = np.minimum(max_rows, np.maximum(1, -(-target // np.maximum(T, 1))))  # rows/item
         # at most 8 items per panel: the last item of a split panel sums the
         # partials serially, so deep splits of small phases cost latency
-        rpi = np.maximum(rpi, np.minimum(max_rows, -(-K // 8)))
+        if transform or self.bulk_kernel != "tma":          # (tma items must fit its tile)
+            rpi = np.maximum(rpi, np.minimum(max_rows, -(-K // 8)))
         nit = np.maximum(1, -(-K // rpi))
         xidx = np.concatenate(rows).astype(np.int32) if n else np.zeros(1, np.int32)
         xoff = _offsets_np(K)

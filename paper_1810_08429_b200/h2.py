@@ -479,8 +479,7 @@ class PanelPlan:
             leaf = h_ == 0
             K = cs.rows[ids]
             base = cf.start[ids] if leaf else cs.coef_off[cf.left[ids]]
-            panels = (cs.v_off[ids], K, cs.rank[ids], [b + np.arange(k) for b, k in zip(base, K)],
-                      cs.coef_off[ids], 0)
+            panels = (cs.v_off[ids], K, cs.rank[ids], _ranges_np(base, K), cs.coef_off[ids], 0)
             fwd.append(self._phase("forward", int(h_), panels, cs.V, None,
                                    self.xt if leaf else self.xhat, None, self.xhat, transform=True))
         # coupling: one panel per row cluster, bucketed by row height
@@ -490,17 +489,16 @@ class PanelPlan:
         if order.size:
             sn = d.c_rows[order]
             cuts = np.flatnonzero(np.r_[True, sn[1:] != sn[:-1]])
-            ends = np.r_[cuts[1:], len(order)]
-            xi = [cs.coef_off[d.c_cols[order[a:b]]] for a, b in zip(cuts, ends)]
-            ks = [d.c_nc[order[a:b]] for a, b in zip(cuts, ends)]
-            rows = [np.concatenate([o + np.arange(k) for o, k in zip(oo, kk)]) for oo, kk in zip(xi, ks)]
-            K = np.array([len(r) for r in rows], dtype=np.int64)
+            # panel inputs: the x-hat slots of the blocks' column clusters, in block order
+            flat = _ranges_np(cs.coef_off[d.c_cols[order]], d.c_nc[order])
+            K = np.add.reduceat(d.c_nc[order], cuts)
+            head = _offsets_np(K)
             colh = np.maximum.reduceat(cf.height[d.c_cols[order]], cuts)
             rowh = rf.height[sn[cuts]]
             for h_ in np.unique(rowh):
                 sel = np.flatnonzero(rowh == h_)
                 panels = (d.c_off[order[cuts[sel]]], K[sel], d.c_nr[order[cuts[sel]]],
-                          [rows[i] for i in sel], rs.coef_off[sn[cuts[sel]]], 0)
+                          flat[_ranges_np(head[sel], K[sel])], rs.coef_off[sn[cuts[sel]]], 0)
                 P = self._phase("coupling", int(h_), panels, d.coup, None, self.xhat, None, self.yhat)
                 cpl.append((P, int(colh[sel].max())))
         # backward transform (row basis), top down
@@ -509,8 +507,7 @@ class PanelPlan:
         for h_ in sorted(np.unique(rf.height[matb]), reverse=True):
             ids = np.flatnonzero(matb & (rf.height == h_))
             K = rs.rank[ids]
-            panels = (rs.v_off[ids], K, rs.rows[ids], [o + np.arange(k) for o, k in zip(rs.coef_off[ids], K)],
-                      rs.coef_off[rf.left[ids]], 1)
+            panels = (rs.v_off[ids], K, rs.rows[ids], _ranges_np(rs.coef_off[ids], K), rs.coef_off[rf.left[ids]], 1)
             P = self._phase("backward", int(h_), panels, rs.VT, None, self.yhat, None, self.yhat,
                             transform=True)
             kids = np.r_[rf.left[ids], rf.right[ids]]
@@ -519,10 +516,8 @@ class PanelPlan:
         order = np.argsort(d.n_rows, kind="stable")
         sn = d.n_rows[order]
         cuts = np.flatnonzero(np.r_[True, sn[1:] != sn[:-1]]) if len(sn) else np.zeros(0, np.int64)
-        ends = np.r_[cuts[1:], len(order)]
-        rows = [np.concatenate([cf.start[c] + np.arange(k) for c, k in
-                                zip(d.n_cols[order[a:b]], d.n_nc[order[a:b]])]) for a, b in zip(cuts, ends)]
-        K = np.array([len(r) for r in rows], dtype=np.int64)
+        K = np.add.reduceat(d.n_nc[order], cuts) if len(sn) else np.zeros(0, np.int64)
+        rows = _ranges_np(cf.start[d.n_cols[order]], d.n_nc[order])
         panels = (d.n_off[order[cuts]], K, d.n_nr[order[cuts]], rows, rf.start[sn[cuts]], 0)
         near = self._phase("nearfield", 0, panels, d.near, None, self.xt, None, self.yt)
         # leaf basis: yt[leaf] += V yhat
@@ -532,8 +527,7 @@ class PanelPlan:
             leaves = leaves[(rf.start[leaves] >= d.row_range[0]) & (rf.stop[leaves] <= d.row_range[1])]
         if leaves.size:
             K = rs.rank[leaves]
-            panels = (rs.v_off[leaves], K, size_r[leaves],
-                      [o + np.arange(k) for o, k in zip(rs.coef_off[leaves], K)], rf.start[leaves], 1)
+            panels = (rs.v_off[leaves], K, size_r[leaves], _ranges_np(rs.coef_off[leaves], K), rf.start[leaves], 1)
             leafp = self._phase("leafbasis", 0, panels, rs.VT, None, self.yhat, None, self.yt,
                                 transform=True)
         self._fwd, self._cpl, self._bwd, self._near, self._leaf = fwd, cpl, bwd, near, leafp
@@ -753,7 +747,7 @@ class PanelPlan:
         if transform or self.bulk_kernel != "tma":          # (tma items must fit its tile)
             rpi = np.maximum(rpi, np.minimum(max_rows, -(-K // 8)))
         nit = np.maximum(1, -(-K // rpi))
-        xidx = np.concatenate(rows).astype(np.int32) if n else np.zeros(1, np.int32)
+        xidx = np.asarray(rows).astype(np.int32) if n else np.zeros(1, np.int32)
         xoff = _offsets_np(K)
         item_panel = np.repeat(np.arange(n), nit)
         item_idx_in_panel = _ranges_np(np.zeros(n, np.int64), nit)

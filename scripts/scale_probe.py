@@ -17,7 +17,9 @@ for rep in range(2):
     print("  row basis", {k: round(v, 3) for k, v in hm.row_basis.store.timing.items()}, "build_h2", {k: round(v, 3) for k, v in hm.dev.timing.items()}, flush=True)
 rep = h2.storage_report(hm)
 print("storage MB", {k: round(v / 1e6, 1) for k, v in rep.items()}, "blocks", len(hm.coupling), len(hm.nearfield), flush=True)
-t0 = time.time(); p = h2.plan(hm); torch.cuda.synchronize(); print("plan %.2fs" % (time.time() - t0), flush=True)
+t0 = time.time(); p = h2.PanelPlan(hm); torch.cuda.synchronize(); t1 = time.time()
+p.capture(); torch.cuda.synchronize(); t2 = time.time()
+print("plan %.2fs  capture %.2fs" % (t1 - t0, t2 - t1), flush=True)
 x = torch.randn(mesh.nt, dtype=torch.float64, device="cuda"); y = torch.empty_like(x)
 for _ in range(3): p.run(x, y)
 torch.cuda.synchronize()

@@ -243,6 +243,20 @@ int gc_panel_tma(int64_t nitems, const int64_t* items, const int32_t* xidx,
                  void* stream);
 int64_t gc_panel_tma_item_elems(void);
 
+/* Device-side Krylov support (consumers of the matvec, h2.py:190-253;
+ * SURVEY 8f rank 3).  Deterministic dot product: fixed grid of
+ * gc_krylov_partials() blocks, `partial` [dev] holds that many doubles.
+ * gc_dot: out[0] = a.b.  CG state s [dev, 8 doubles]: s[0] = r.r, s[1] =
+ * p.q, s[2] = new r.r, s[3] = beta, s[4] = alpha, s[5] = stop flag.
+ * gc_cg_pq: s[1] = p.q.  gc_cg_update: alpha = s[0]/s[1]; x += alpha p;
+ * r -= alpha q; s[2] = r.r; beta = s[2]/s[0]; s[0] = s[2]; p = r + beta p
+ * (p.q <= 0 sets s[5] = 1 and leaves x, r unchanged, as h2.py:206-208). */
+int gc_dot(int64_t n, const double* a, const double* b, double* partial, double* out, void* stream);
+int gc_cg_pq(int64_t n, const double* p, const double* q, double* partial, double* s, void* stream);
+int gc_cg_update(int64_t n, double* x, double* r, double* p, const double* q, double* partial,
+                 double* s, void* stream);
+int64_t gc_krylov_partials(void);
+
 /* The device's scheduling-priority range (cudaDeviceGetStreamPriorityRange):
  * least (default, e.g. 0) and greatest (most urgent, e.g. -5). */
 int gc_priority_range(int32_t* least, int32_t* greatest);

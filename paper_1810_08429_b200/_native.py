@@ -56,6 +56,10 @@ _SIGNATURES = {
     "gc_panel_chain_grid": [ctypes.POINTER(c_i64)],
     "gc_panel_chain": [c_i64, c_p, c_i64, c_p, c_p],
     "gc_panel_phase_bytes": [],
+    "gc_dot": [c_i64, c_p, c_p, c_p, c_p, c_p],
+    "gc_cg_pq": [c_i64, c_p, c_p, c_p, c_p, c_p],
+    "gc_cg_update": [c_i64, c_p, c_p, c_p, c_p, c_p, c_p, c_p],
+    "gc_krylov_partials": [],
     "gc_panel_stream_grid": [ctypes.POINTER(c_i64)],
     "gc_panel_tma": [c_i64, c_p, c_p, c_p, c_p, c_p, c_p, c_p, c_p, c_i64, c_p, c_p, ctypes.c_int32, c_p, c_p],
     "gc_panel_tma_item_elems": [],
@@ -75,7 +79,7 @@ _SIGNATURES = {
 }
 _RESTYPES = {"gc_last_error": ctypes.c_char_p, "gc_launch_count": ctypes.c_uint64,
              "gc_reset_launch_count": None, "gc_panel_phase_bytes": ctypes.c_int64,
-             "gc_panel_tma_item_elems": ctypes.c_int64}
+             "gc_panel_tma_item_elems": ctypes.c_int64, "gc_krylov_partials": ctypes.c_int64}
 
 EXPORTED = tuple(_SIGNATURES)
 ABI_VERSION = 1

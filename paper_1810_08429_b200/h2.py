@@ -363,6 +363,47 @@ def cg_solve(apply, b, tol=1e-8, max_iter=500):
     return CGResult(x, np.asarray(hist), bool(hist[-1] <= tol * bnorm))
 
 
+def cg_solve_device(h, b, tol=1e-8, max_iter=500):
+    """Conjugate gradients on the H2 operator with every vector resident on
+    the device (``h2.py:190-219`` semantics): the product
+    is the captured panel plan, the vector updates and dot products are
+    ``gc_cg_*`` kernels with the scalars in device memory, and the only
+    host traffic per iteration is the 16-byte read of r.r and the stop flag.
+    Returns a :class:`CGResult` with host arrays."""
+    pl = plan(h)
+    dev = pl.dev
+    b_d = torch.as_tensor(np.asarray(b, dtype=np.float64)).to(dev)
+    n = b_d.numel()
+    if n != pl.n_in or pl.n_in != pl.n_out:
+        raise ConfigError("cg_solve_device needs a square operator matching b")
+    x = torch.zeros_like(b_d)
+    r = b_d.clone()
+    p = b_d.clone()
+    q = torch.empty_like(b_d)
+    s = torch.zeros(8, dtype=torch.float64, device=dev)
+    partial = torch.empty(int(_native.load().gc_krylov_partials()), dtype=torch.float64, device=dev)
+    with torch.cuda.device(dev):
+        st = stream_handle()
+        _native.call("gc_dot", n, ptr(b_d), ptr(b_d), ptr(partial), ptr(s), st)
+        host = s[[0, 5]].cpu().numpy()
+        bnorm = float(np.sqrt(host[0]))
+        hist = [bnorm]
+        if bnorm == 0.0:
+            return CGResult(x.cpu().numpy(), np.asarray(hist), True)
+        for _ in range(max_iter):
+            if hist[-1] <= tol * bnorm:
+                break
+            pl.run(p, q)
+            st = stream_handle()
+            _native.call("gc_cg_pq", n, ptr(p), ptr(q), ptr(partial), ptr(s), st)
+            _native.call("gc_cg_update", n, ptr(x), ptr(r), ptr(p), ptr(q), ptr(partial), ptr(s), st)
+            host = s[[0, 5]].cpu().numpy()
+            if host[1] != 0.0:
+                break
+            hist.append(float(np.sqrt(host[0])))
+        return CGResult(x.cpu().numpy(), np.asarray(hist), bool(hist[-1] <= tol * bnorm))
+
+
 def cgnr_solve(apply, b, tol=1e-8, max_iter=500):
     """CG on the normal equations; history is the true residual
     (``h2.py:222-253``)."""

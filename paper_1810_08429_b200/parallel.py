@@ -183,6 +183,20 @@ def build_sharded_operator(mesh, cfg, group=None, device=None, timings=None):
     return ShardedH2(h, layout, group, slot)
 
 
+def all_gather_into(out, inp, group):
+    """out = concat over ranks of inp.  NCCL gathers device tensors in place;
+    other backends (gloo: the multi-process functional test on one GPU)
+    stage through host memory."""
+    import torch
+    import torch.distributed as dist
+    if dist.get_backend(group) == "nccl":
+        dist.all_gather_into_tensor(out, inp, group=group)
+        return
+    parts = [torch.empty(inp.numel(), dtype=inp.dtype) for _ in range(dist.get_world_size(group))]
+    dist.all_gather(parts, inp.detach().cpu(), group=group)
+    out.copy_(torch.cat(parts).to(out.device))
+
+
 def _shard_plan_class():
     from .h2 import PanelPlan
 
@@ -192,7 +206,6 @@ def _shard_plan_class():
         slots are all-gathered before the coupling phase."""
 
         def __init__(self, sh):
-            import torch.distributed as dist
             super().__init__(sh.h)
             self.sh = sh
             self.lo, self.hi = sh.layout.lo, sh.layout.hi
@@ -200,14 +213,13 @@ def _shard_plan_class():
             self.own_xhat = self.xhat[g * sh.slot:(g + 1) * sh.slot]
 
             def gather_xhat():
-                dist.all_gather_into_tensor(self.xhat, self.own_xhat.clone(), group=sh.group)
+                all_gather_into(self.xhat, self.own_xhat.clone(), sh.group)
 
             # no permutation steps; the x-hat all-gather gates every coupling bucket
             self.nodes = self._build_nodes(gather=False, before_coupling=gather_xhat, scatter=False)
 
         def run(self, x_slice):
-            import torch.distributed as dist
-            dist.all_gather_into_tensor(self.xt, x_slice.contiguous(), group=self.sh.group)
+            all_gather_into(self.xt, x_slice.contiguous(), self.sh.group)
             self._exec(self.nodes)
             return self.yt[self.lo:self.hi].clone()
 

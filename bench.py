@@ -124,7 +124,7 @@ def _import_reference():
 def reference_baseline(args, steps, cpu_sample, mesh_vertices=None):
     """Time the reference CPU implementation on the host cores.
 
-    matvec: greencross.h2.mvm on the reference-built C2 structure (trees,
+    matvec: greencross.h2.mvm on the reference-built structure (trees,
     block tree and nested bases built by the reference; block values
     zero-filled - BLAS time does not depend on values - because the
     reference's full quadrature takes minutes).  assembly: bases timed in
@@ -185,8 +185,9 @@ def reference_baseline(args, steps, cpu_sample, mesh_vertices=None):
             "trees_s": t1 - t0, "bases_s": t2 - t1, "quadrature_sampled_s": t4 - t3,
             "quadrature_sample_tasks": int(tasks_s), "quadrature_tasks": int(tasks_all),
             "sample": "reference greencross: trees+bases full, quadrature on %.1f%% of blocks "
-                      "(%d of %d tasks) extrapolated, mvm x%d on the reference-built C2 "
-                      "structure with zero-filled blocks" % (100 * cpu_sample, tasks_s, tasks_all, steps)}
+                      "(%d of %d tasks) extrapolated, mvm x%d on the reference-built %s L%d "
+                      "structure with zero-filled blocks" % (100 * cpu_sample, tasks_s, tasks_all, steps,
+                                                             args.geometry, args.level)}
 
 
 def _ref_cube(RGeo, level):

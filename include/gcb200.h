@@ -57,6 +57,12 @@ typedef struct gc_geom {
     int64_t nt;
     int64_t mq;
     const double* wq_host;
+    /* [dev] nt x 3 chart normal of each plane triangle, |n| = gram
+     * (geometry.py:281-290); read by the double-layer kernel only */
+    const double* normals;
+    /* 0 = single layer 1/(4 pi r), 1 = double layer <x-y, n_y>/(4 pi r^3)
+     * (assembly.py:196-201) */
+    int64_t kernel;
 } gc_geom;
 
 /* Singular pair rules (quadrature.sauter_rule, quadrature.py:211-284) in

@@ -52,7 +52,8 @@ def galerkin_pair_evaluator(kind, mesh, basis, q_reg, q_sing, device=None):
     check_mesh(mesh, kind, basis)
     dev = require_device(device)
     dmesh = DeviceMesh.get(mesh, q_reg, dev)
-    rules = DeviceRules.get(q_sing, dev)
+    rules = DeviceRules.get(q_sing, dev, kind)
+    geom = dmesh.geom_of(kind)
 
     def evaluate(case, rows, cols, px, py):
         case = int(case)
@@ -62,17 +63,21 @@ def galerkin_pair_evaluator(kind, mesh, basis, q_reg, q_sing, device=None):
         out = empty(b, dev)
         args = [to_dev(np.asarray(a, dtype=np.int64), dev) for a in (rows, cols, px, py)]
         with torch.cuda.device(dev):
-            _native.call("gc_pair_eval", dmesh.geom, rules.struct, case, b,
+            _native.call("gc_pair_eval", geom, rules.struct, case, b,
                          *[ptr(a) for a in args], ptr(out), stream_handle())
         return out.cpu().numpy().reshape(b, 1, 1)
 
     return evaluate
 
 
-def device_block_assembly(dmesh, rules, queue, row_idx, col_idx, desc, out, stats=None):
+def device_block_assembly(dmesh, rules, queue, row_idx, col_idx, desc, out, stats=None, kind="slp"):
     """Assemble blocks described by ``desc (nb,5)`` into the device buffer
     ``out`` (column-major per block); singular pairs are flushed at the end.
+    ``kind`` "slp" / "dlp" picks the kernel (``rules`` must match it).
     Returns the per-case task counts."""
+    if getattr(rules, "kind", "slp") != kind:
+        raise ConfigError("rules built for %r, assembling %r" % (rules.kind, kind))
+    geom = dmesh.geom_of(kind)
     nb = len(desc)
     if nb == 0:
         return [0, 0, 0, 0]
@@ -80,11 +85,11 @@ def device_block_assembly(dmesh, rules, queue, row_idx, col_idx, desc, out, stat
     d_desc = to_dev(desc.astype(np.int64), out.device)
     stream = stream_handle()
     with torch.cuda.device(out.device):
-        _native.call("gc_assemble_blocks", dmesh.geom, nb, ptr(d_desc), int(desc[:, 1].max()),
+        _native.call("gc_assemble_blocks", geom, nb, ptr(d_desc), int(desc[:, 1].max()),
                      int(desc[:, 3].max()), ptr(row_idx), ptr(col_idx), ptr(out), queue.struct, ptr(queue.flags),
                      stream)
         counts = (_native.c_i64 * 4)()
-        _native.call("gc_singular_flush", dmesh.geom, rules.struct, queue.struct, ptr(out),
+        _native.call("gc_singular_flush", geom, rules.struct, queue.struct, ptr(out),
                      counts, stream)
     queue.check_flags()
     n_sing = [int(counts[k]) for k in range(4)]
@@ -105,11 +110,12 @@ def assemble_galerkin_block(kind, mesh, basis, rows, cols, orders=(3, 5), capaci
         return DenseBlock(rows, cols, np.zeros((nr, nc)))
     dev = require_device(device)
     dmesh = DeviceMesh.get(mesh, orders[0], dev)
-    rules = DeviceRules.get(orders[1], dev)
+    rules = DeviceRules.get(orders[1], dev, kind)
     queue = SingularQueue.get(mesh, dev)
     out = empty(nr * nc, dev)
     desc = np.array([[0, nr, 0, nc, 0]], dtype=np.int64)
-    device_block_assembly(dmesh, rules, queue, to_dev(rows, dev), to_dev(cols, dev), desc, out)
+    device_block_assembly(dmesh, rules, queue, to_dev(rows, dev), to_dev(cols, dev), desc, out,
+                          kind=kind)
     return DenseBlock(rows, cols, out.cpu().numpy().reshape(nc, nr).T.copy())
 
 

@@ -1,5 +1,7 @@
-// Batched Galerkin pair quadrature for the single-layer kernel 1/(4 pi r),
-// piecewise-constant basis, plane charts (assembly.py:159-216).
+// Batched Galerkin pair quadrature, piecewise-constant basis, plane charts
+// (assembly.py:159-216): the single-layer kernel 1/(4 pi r) and (DLP) the
+// double-layer kernel <x - y, n_y>/(4 pi r^3), n_y the column triangle's
+// chart normal (|n_y| carries the column Gramian, assembly.py:196-201).
 //
 // Disjoint pairs (the regular q_reg^2 x q_reg^2 tensor rule): one CTA per
 // block.  The block's row and column quadrature points are staged in shared
@@ -18,12 +20,22 @@
 
 namespace gcb {
 
+// integrand without 1/(4 pi): 1/r (single layer) or <d, n>/r^3 (double layer)
+template <bool DLP>
+__device__ __forceinline__ double kern(double d0, double d1, double d2, double n0, double n1, double n2) {
+    const double r2 = fma(d2, d2, fma(d1, d1, d0 * d0));
+    const double ri = rsqrt_fast(r2);
+    if (!DLP) return ri;
+    const double dot = fma(d2, n2, fma(d1, n1, d0 * n0));
+    return dot * (ri * ri * ri);
+}
+
 // sum_i sum_j w_i w_j / |X_i - Y_j| reading both point sets from global
 // (evaluator seam, one thread per task)
-template <int M>
+template <int M, bool DLP>
 __device__ __forceinline__ double disjoint_sum(const double* __restrict__ xq_t,
                                                const double* __restrict__ xq_s,
-                                               const double* __restrict__ wq) {
+                                               const double* __restrict__ wq, const double* ns) {
     double X[M][3];
 #pragma unroll
     for (int i = 0; i < M; ++i) {
@@ -31,6 +43,7 @@ __device__ __forceinline__ double disjoint_sum(const double* __restrict__ xq_t,
         X[i][1] = __ldg(xq_t + 3 * i + 1);
         X[i][2] = __ldg(xq_t + 3 * i + 2);
     }
+    const double n0 = DLP ? ns[0] : 0.0, n1 = DLP ? ns[1] : 0.0, n2 = DLP ? ns[2] : 0.0;
     double total = 0.0;
 #pragma unroll 1
     for (int j = 0; j < M; ++j) {
@@ -38,43 +51,48 @@ __device__ __forceinline__ double disjoint_sum(const double* __restrict__ xq_t,
                      y2 = __ldg(xq_s + 3 * j + 2);
         double acc = 0.0;
 #pragma unroll
-        for (int i = 0; i < M; ++i) {
-            double d0 = X[i][0] - y0, d1 = X[i][1] - y1, d2 = X[i][2] - y2;
-            double r2 = fma(d2, d2, fma(d1, d1, d0 * d0));
-            acc = fma(__ldg(wq + i), rsqrt_fast(r2), acc);
-        }
+        for (int i = 0; i < M; ++i)
+            acc = fma(__ldg(wq + i), kern<DLP>(X[i][0] - y0, X[i][1] - y1, X[i][2] - y2, n0, n1, n2), acc);
         total = fma(__ldg(wq + j), acc, total);
     }
     return total;
 }
 
+template <bool DLP>
 __device__ double disjoint_sum_any(const double* __restrict__ xq_t,
                                    const double* __restrict__ xq_s,
-                                   const double* __restrict__ wq, int mq) {
+                                   const double* __restrict__ wq, int mq, const double* ns) {
+    const double n0 = DLP ? ns[0] : 0.0, n1 = DLP ? ns[1] : 0.0, n2 = DLP ? ns[2] : 0.0;
     double total = 0.0;
     for (int j = 0; j < mq; ++j) {
         const double y0 = __ldg(xq_s + 3 * j), y1 = __ldg(xq_s + 3 * j + 1),
                      y2 = __ldg(xq_s + 3 * j + 2);
         double acc = 0.0;
-        for (int i = 0; i < mq; ++i) {
-            double d0 = __ldg(xq_t + 3 * i) - y0, d1 = __ldg(xq_t + 3 * i + 1) - y1,
-                   d2 = __ldg(xq_t + 3 * i + 2) - y2;
-            double r2 = fma(d2, d2, fma(d1, d1, d0 * d0));
-            acc = fma(__ldg(wq + i), rsqrt_fast(r2), acc);
-        }
+        for (int i = 0; i < mq; ++i)
+            acc = fma(__ldg(wq + i), kern<DLP>(__ldg(xq_t + 3 * i) - y0, __ldg(xq_t + 3 * i + 1) - y1,
+                                               __ldg(xq_t + 3 * i + 2) - y2, n0, n1, n2), acc);
         total = fma(__ldg(wq + j), acc, total);
     }
     return total;
 }
 
-template <int M>
+// entry scale: (gram_t / 4 pi) * gram_s (single layer) or gram_t / 4 pi
+// (double layer: the column Gramian is |n_y|)
+template <bool DLP>
+__device__ __forceinline__ double entry_scale(const gc_geom& g, int64_t t, int64_t s) {
+    const double gt = __ldg(g.gram + t) * INV_FOUR_PI;
+    return DLP ? gt : gt * __ldg(g.gram + s);
+}
+
+template <int M, bool DLP>
 __device__ __forceinline__ double disjoint_entry(const gc_geom& g, int64_t t, int64_t s) {
     double sum;
+    const double* ns = DLP ? g.normals + 3 * s : nullptr;
     if (M > 0)
-        sum = disjoint_sum<(M > 0 ? M : 1)>(g.xq + t * 3 * M, g.xq + s * 3 * M, g.wq);
+        sum = disjoint_sum<(M > 0 ? M : 1), DLP>(g.xq + t * 3 * M, g.xq + s * 3 * M, g.wq, ns);
     else
-        sum = disjoint_sum_any(g.xq + t * 3 * g.mq, g.xq + s * 3 * g.mq, g.wq, (int)g.mq);
-    return ((__ldg(g.gram + t) * INV_FOUR_PI) * __ldg(g.gram + s)) * sum;  // same association as k_assemble_blocks
+        sum = disjoint_sum_any<DLP>(g.xq + t * 3 * g.mq, g.xq + s * 3 * g.mq, g.wq, (int)g.mq, ns);
+    return entry_scale<DLP>(g, t, s) * sum;  // same association as k_assemble_blocks
 }
 
 __device__ __forceinline__ void push_task(const gc_queue& q, int kase, int64_t t, int64_t s, int px,
@@ -106,7 +124,7 @@ struct RuleW {
 // (nr*M*3), column points (nc*M*3) and both vertex-id lists; the caller
 // sizes the dynamic allocation for the largest block.  NT = 128 for the
 // 16x16 near-field blocks (one thread per column pair), 256 otherwise.
-template <int M, int NT>
+template <int M, int NT, bool DLP>
 __global__ void __launch_bounds__(NT) k_assemble_blocks(
     gc_geom g, RuleW rw, const int64_t* __restrict__ desc, const int64_t* __restrict__ row_idx,
     const int64_t* __restrict__ col_idx, double* __restrict__ out, gc_queue q, int32_t* flags) {
@@ -166,8 +184,17 @@ __global__ void __launch_bounds__(NT) k_assemble_blocks(
         for (int i = 0; i < M; ++i)
 #pragma unroll
             for (int k = 0; k < 3; ++k) X[i][k] = Xs[(a * M + i) * 3 + k];
+        const int b1 = two ? b0 + 1 : b0;
         const double* Y0 = Ys + b0 * M * 3;
-        const double* Y1 = Ys + (two ? b0 + 1 : b0) * M * 3;
+        const double* Y1 = Ys + b1 * M * 3;
+        double na[3] = {0.0, 0.0, 0.0}, nb[3] = {0.0, 0.0, 0.0};
+        if (DLP) {
+#pragma unroll
+            for (int k = 0; k < 3; ++k) {
+                na[k] = __ldg(g.normals + 3 * svs[4 * b0] + k);
+                nb[k] = __ldg(g.normals + 3 * svs[4 * b1] + k);
+            }
+        }
         double tot0 = 0.0, tot1 = 0.0;
 #pragma unroll 1
         for (int j = 0; j < M; ++j) {
@@ -176,20 +203,14 @@ __global__ void __launch_bounds__(NT) k_assemble_blocks(
             double acc0 = 0.0, acc1 = 0.0;
 #pragma unroll
             for (int i = 0; i < M; ++i) {
-                const double d0 = X[i][0] - u0, d1 = X[i][1] - u1, d2 = X[i][2] - u2;
-                const double e0 = X[i][0] - v0, e1 = X[i][1] - v1, e2 = X[i][2] - v2;
-                const double r2a = fma(d2, d2, fma(d1, d1, d0 * d0));
-                const double r2b = fma(e2, e2, fma(e1, e1, e0 * e0));
-                acc0 = fma(rw.w[i], rsqrt_fast(r2a), acc0);
-                acc1 = fma(rw.w[i], rsqrt_fast(r2b), acc1);
+                acc0 = fma(rw.w[i], kern<DLP>(X[i][0] - u0, X[i][1] - u1, X[i][2] - u2, na[0], na[1], na[2]), acc0);
+                acc1 = fma(rw.w[i], kern<DLP>(X[i][0] - v0, X[i][1] - v1, X[i][2] - v2, nb[0], nb[1], nb[2]), acc1);
             }
             tot0 = fma(rw.w[j], acc0, tot0);
             tot1 = fma(rw.w[j], acc1, tot1);
         }
-        const double gt = __ldg(g.gram + t) * INV_FOUR_PI;
-        if (live[0]) out[out_off + (int64_t)b0 * nr + a] = (gt * __ldg(g.gram + svs[4 * b0])) * tot0;
-        if (live[1])
-            out[out_off + (int64_t)(b0 + 1) * nr + a] = (gt * __ldg(g.gram + svs[4 * (b0 + 1)])) * tot1;
+        if (live[0]) out[out_off + (int64_t)b0 * nr + a] = entry_scale<DLP>(g, t, svs[4 * b0]) * tot0;
+        if (live[1]) out[out_off + (int64_t)(b0 + 1) * nr + a] = entry_scale<DLP>(g, t, svs[4 * b1]) * tot1;
     }
 }
 
@@ -199,7 +220,7 @@ static void e_copy_weights(const gc_geom& g, RuleW& rw, int M) {
 
 // Higher regular orders (q_reg^2 = M > 16, M <= 64): same structure as
 // k_assemble_blocks, the row's points held in registers MC at a time.
-template <int MC, int NT>
+template <int MC, int NT, bool DLP>
 __global__ void __launch_bounds__(NT) k_assemble_blocks_big(
     gc_geom g, RuleW rw, int M, const int64_t* __restrict__ desc, const int64_t* __restrict__ row_idx,
     const int64_t* __restrict__ col_idx, double* __restrict__ out, gc_queue q, int32_t* flags) {
@@ -252,8 +273,17 @@ __global__ void __launch_bounds__(NT) k_assemble_blocks_big(
                 push_task(q, kase, t, svs[4 * b], px, py, out_off + (int64_t)b * nr + a, flags);
         }
         if (!live[0] && !live[1]) continue;
+        const int b1 = two ? b0 + 1 : b0;
         const double* Y0 = Ys + b0 * M * 3;
-        const double* Y1 = Ys + (two ? b0 + 1 : b0) * M * 3;
+        const double* Y1 = Ys + b1 * M * 3;
+        double na[3] = {0.0, 0.0, 0.0}, nb[3] = {0.0, 0.0, 0.0};
+        if (DLP) {
+#pragma unroll
+            for (int k = 0; k < 3; ++k) {
+                na[k] = __ldg(g.normals + 3 * svs[4 * b0] + k);
+                nb[k] = __ldg(g.normals + 3 * svs[4 * b1] + k);
+            }
+        }
         double tot0 = 0.0, tot1 = 0.0;
         for (int i0 = 0; i0 < M; i0 += MC) {
             double X[MC][3], wi[MC];
@@ -272,21 +302,15 @@ __global__ void __launch_bounds__(NT) k_assemble_blocks_big(
 #pragma unroll
                 for (int i = 0; i < MC; ++i) {
                     // padded points (weight 0) sit far away: finite, nonzero r2
-                    const double d0 = X[i][0] - u0, d1 = X[i][1] - u1, d2 = X[i][2] - u2;
-                    const double e0 = X[i][0] - v0, e1 = X[i][1] - v1, e2 = X[i][2] - v2;
-                    const double r2a = fma(d2, d2, fma(d1, d1, d0 * d0));
-                    const double r2b = fma(e2, e2, fma(e1, e1, e0 * e0));
-                    acc0 = fma(wi[i], rsqrt_fast(r2a), acc0);
-                    acc1 = fma(wi[i], rsqrt_fast(r2b), acc1);
+                    acc0 = fma(wi[i], kern<DLP>(X[i][0] - u0, X[i][1] - u1, X[i][2] - u2, na[0], na[1], na[2]), acc0);
+                    acc1 = fma(wi[i], kern<DLP>(X[i][0] - v0, X[i][1] - v1, X[i][2] - v2, nb[0], nb[1], nb[2]), acc1);
                 }
                 tot0 = fma(rw.w[j], acc0, tot0);
                 tot1 = fma(rw.w[j], acc1, tot1);
             }
         }
-        const double gt = __ldg(g.gram + t) * INV_FOUR_PI;
-        if (live[0]) out[out_off + (int64_t)b0 * nr + a] = (gt * __ldg(g.gram + svs[4 * b0])) * tot0;
-        if (live[1])
-            out[out_off + (int64_t)(b0 + 1) * nr + a] = (gt * __ldg(g.gram + svs[4 * (b0 + 1)])) * tot1;
+        if (live[0]) out[out_off + (int64_t)b0 * nr + a] = entry_scale<DLP>(g, t, svs[4 * b0]) * tot0;
+        if (live[1]) out[out_off + (int64_t)(b0 + 1) * nr + a] = entry_scale<DLP>(g, t, svs[4 * b1]) * tot1;
     }
 }
 
@@ -309,19 +333,19 @@ __global__ void __launch_bounds__(BLK_THREADS) k_assemble_blocks_any(
         int px, py;
         const int kase = classify_pair(tv, sv, &px, &py);
         if (kase == 0)
-            out[out_off + e] = disjoint_entry<0>(g, t, s);
+            out[out_off + e] = g.kernel ? disjoint_entry<0, true>(g, t, s) : disjoint_entry<0, false>(g, t, s);
         else
             push_task(q, kase, t, s, px, py, out_off + e, flags);
     }
 }
 
 // evaluator seam, disjoint case: one thread per task
-template <int M>
+template <int M, bool DLP>
 __global__ void k_pair_disjoint(gc_geom g, int64_t B, const int64_t* __restrict__ rows,
                                 const int64_t* __restrict__ cols, double* __restrict__ out) {
     for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < B;
          i += (int64_t)gridDim.x * blockDim.x)
-        out[i] = disjoint_entry<M>(g, __ldg(rows + i), __ldg(cols + i));
+        out[i] = disjoint_entry<M, DLP>(g, __ldg(rows + i), __ldg(cols + i));
 }
 
 // pack seam arrays into queue-format tasks
@@ -348,7 +372,7 @@ constexpr int SING_G = 2;   // tasks per warp
 // P_0 == Q_0 is the shared vertex, so D carries no cancellation.  The rule
 // table (NC coefficient columns + weight, SoA, P points) is staged in
 // shared memory when it fits, else read through L1.
-template <int NC, bool SMEM>
+template <int NC, bool SMEM, bool DLP>
 __global__ void __launch_bounds__(SING_THREADS) k_singular(gc_geom g, const double* __restrict__ rule,
                                                            int P, const int64_t* __restrict__ tasks,
                                                            int64_t ntasks, double* __restrict__ out) {
@@ -366,6 +390,7 @@ __global__ void __launch_bounds__(SING_THREADS) k_singular(gc_geom g, const doub
          grp += nwarps) {
         double G[SING_G][NC][3];
         double scale[SING_G];
+        double nrm[SING_G][3];
         int64_t oidx[SING_G];
 #pragma unroll
         for (int k = 0; k < SING_G; ++k) {
@@ -390,7 +415,9 @@ __global__ void __launch_bounds__(SING_THREADS) k_singular(gc_geom g, const doub
                     G[k][2 % NC][c] = -(cs[3 * q2 + c] - cs[3 * q0 + c]);
                 }
             }
-            scale[k] = g.gram[t] * g.gram[s] * INV_FOUR_PI;
+            scale[k] = DLP ? g.gram[t] * INV_FOUR_PI : g.gram[t] * g.gram[s] * INV_FOUR_PI;
+#pragma unroll
+            for (int c = 0; c < 3; ++c) nrm[k][c] = DLP ? g.normals[3 * s + c] : 0.0;
         }
         double acc[SING_G];
 #pragma unroll
@@ -410,8 +437,7 @@ __global__ void __launch_bounds__(SING_THREADS) k_singular(gc_geom g, const doub
                     for (int j = 1; j < NC; ++j) v = fma(cf[j], G[k][j][c], v);
                     dd[c] = v;
                 }
-                const double r2 = fma(dd[2], dd[2], fma(dd[1], dd[1], dd[0] * dd[0]));
-                acc[k] = fma(w, rsqrt_fast(r2), acc[k]);
+                acc[k] = fma(w, kern<DLP>(dd[0], dd[1], dd[2], nrm[k][0], nrm[k][1], nrm[k][2]), acc[k]);
             }
         }
 #pragma unroll
@@ -424,24 +450,24 @@ __global__ void __launch_bounds__(SING_THREADS) k_singular(gc_geom g, const doub
     }
 }
 
-template <int NC>
+template <int NC, bool DLP>
 static int launch_singular_nc(const gc_geom& g, const double* table, int64_t P, const int64_t* tasks,
                               int64_t n, double* out, cudaStream_t st) {
     const size_t bytes = (size_t)(NC + 1) * P * sizeof(double);
     const int64_t groups = (n + SING_G - 1) / SING_G;
     int64_t grid = (groups + SING_WARPS - 1) / SING_WARPS;
     if (bytes <= 200 * 1024) {
-        cudaError_t e = cudaFuncSetAttribute(k_singular<NC, true>,
+        cudaError_t e = cudaFuncSetAttribute(k_singular<NC, true, DLP>,
                                              cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes);
         if (e != cudaSuccess) return cuda_status(e, "k_singular smem attribute");
         int per_sm = 1;
-        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_singular<NC, true>, SING_THREADS, bytes);
+        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_singular<NC, true, DLP>, SING_THREADS, bytes);
         if (per_sm < 1) per_sm = 1;
         if (grid > 148LL * per_sm) grid = 148LL * per_sm;
-        k_singular<NC, true><<<(unsigned)grid, SING_THREADS, bytes, st>>>(g, table, (int)P, tasks, n, out);
+        k_singular<NC, true, DLP><<<(unsigned)grid, SING_THREADS, bytes, st>>>(g, table, (int)P, tasks, n, out);
     } else {
         if (grid > 148LL * 8) grid = 148LL * 8;
-        k_singular<NC, false><<<(unsigned)grid, SING_THREADS, 0, st>>>(g, table, (int)P, tasks, n, out);
+        k_singular<NC, false, DLP><<<(unsigned)grid, SING_THREADS, 0, st>>>(g, table, (int)P, tasks, n, out);
     }
     GC_CHECK_LAUNCH("k_singular");
     return GC_OK;
@@ -454,22 +480,26 @@ static int launch_singular(const gc_geom& g, const gc_rules& r, int kase, const 
         set_error(GC_ERR_CONFIG, "singular rule for case %d not uploaded", kase);
         return GC_ERR_CONFIG;
     }
-    switch (kase) {
-        case 1: return launch_singular_nc<4>(g, r.table[1], r.npts[1], tasks, n, out, st);
-        case 2: return launch_singular_nc<3>(g, r.table[2], r.npts[2], tasks, n, out, st);
-        case 3: return launch_singular_nc<2>(g, r.table[3], r.npts[3], tasks, n, out, st);
+    if (g.kernel && !g.normals) { set_error(GC_ERR_CONFIG, "double layer needs gc_geom.normals"); return GC_ERR_CONFIG; }
+    switch (kase * 2 + (g.kernel ? 1 : 0)) {
+        case 2: return launch_singular_nc<4, false>(g, r.table[1], r.npts[1], tasks, n, out, st);
+        case 3: return launch_singular_nc<4, true>(g, r.table[1], r.npts[1], tasks, n, out, st);
+        case 4: return launch_singular_nc<3, false>(g, r.table[2], r.npts[2], tasks, n, out, st);
+        case 5: return launch_singular_nc<3, true>(g, r.table[2], r.npts[2], tasks, n, out, st);
+        case 6: return launch_singular_nc<2, false>(g, r.table[3], r.npts[3], tasks, n, out, st);
+        case 7: return launch_singular_nc<2, true>(g, r.table[3], r.npts[3], tasks, n, out, st);
         default: set_error(GC_ERR_CONFIG, "bad singular case %d", kase); return GC_ERR_CONFIG;
     }
 }
 
-template <int M, int NT>
+template <int M, int NT, bool DLP>
 static int launch_blocks_nt(const gc_geom& g, const RuleW& rw, int64_t nb, const int64_t* desc,
                             size_t bytes, const int64_t* ri, const int64_t* ci, double* out,
                             const gc_queue& q, int32_t* flags, cudaStream_t st) {
-    cudaError_t e = cudaFuncSetAttribute(k_assemble_blocks<M, NT>,
+    cudaError_t e = cudaFuncSetAttribute(k_assemble_blocks<M, NT, DLP>,
                                          cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes);
     if (e != cudaSuccess) return cuda_status(e, "k_assemble_blocks smem attribute");
-    k_assemble_blocks<M, NT><<<(unsigned)nb, NT, bytes, st>>>(g, rw, desc, ri, ci, out, q, flags);
+    k_assemble_blocks<M, NT, DLP><<<(unsigned)nb, NT, bytes, st>>>(g, rw, desc, ri, ci, out, q, flags);
     GC_CHECK_LAUNCH("k_assemble_blocks");
     return GC_OK;
 }
@@ -487,9 +517,24 @@ static int launch_blocks(const gc_geom& g, int64_t nb, const int64_t* desc, int6
     if (!g.wq_host) { set_error(GC_ERR_CONFIG, "gc_geom.wq_host is required"); return GC_ERR_CONFIG; }
     RuleW rw;
     e_copy_weights(g, rw, M);
-    if (max_rows * ((max_cols + 1) / 2) <= 128)
-        return launch_blocks_nt<M, 128>(g, rw, nb, desc, bytes, ri, ci, out, q, flags, st);
-    return launch_blocks_nt<M, 256>(g, rw, nb, desc, bytes, ri, ci, out, q, flags, st);
+    const bool small = max_rows * ((max_cols + 1) / 2) <= 128;
+    if (g.kernel)
+        return small ? launch_blocks_nt<M, 128, true>(g, rw, nb, desc, bytes, ri, ci, out, q, flags, st)
+                     : launch_blocks_nt<M, 256, true>(g, rw, nb, desc, bytes, ri, ci, out, q, flags, st);
+    return small ? launch_blocks_nt<M, 128, false>(g, rw, nb, desc, bytes, ri, ci, out, q, flags, st)
+                 : launch_blocks_nt<M, 256, false>(g, rw, nb, desc, bytes, ri, ci, out, q, flags, st);
+}
+
+template <int MC, int NT, bool DLP>
+static int launch_big(const gc_geom& g, const RuleW& rw, int M, int64_t nb, const int64_t* desc,
+                      size_t bytes, const int64_t* ri, const int64_t* ci, double* out, const gc_queue& q,
+                      int32_t* flags, cudaStream_t st) {
+    cudaError_t e = cudaFuncSetAttribute(k_assemble_blocks_big<MC, NT, DLP>,
+                                         cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes);
+    if (e != cudaSuccess) return cuda_status(e, "k_assemble_blocks_big smem");
+    k_assemble_blocks_big<MC, NT, DLP><<<(unsigned)nb, NT, bytes, st>>>(g, rw, M, desc, ri, ci, out, q, flags);
+    GC_CHECK_LAUNCH("k_assemble_blocks_big");
+    return GC_OK;
 }
 
 }  // namespace gcb
@@ -508,12 +553,19 @@ int gc_pair_eval(const gc_geom* gp, const gc_rules* rp, int kase, int64_t B, con
     if (kase == 0) {
         int64_t grid = (B + 127) / 128;
         if (grid > 148 * 64) grid = 148 * 64;
-        if (g.mq == 9)
-            k_pair_disjoint<9><<<(unsigned)grid, 128, 0, st>>>(g, B, rows, cols, out);
+        if (g.kernel && !g.normals) { set_error(GC_ERR_CONFIG, "double layer needs gc_geom.normals"); return GC_ERR_CONFIG; }
+        if (g.mq == 9 && g.kernel)
+            k_pair_disjoint<9, true><<<(unsigned)grid, 128, 0, st>>>(g, B, rows, cols, out);
+        else if (g.mq == 9)
+            k_pair_disjoint<9, false><<<(unsigned)grid, 128, 0, st>>>(g, B, rows, cols, out);
+        else if (g.mq == 4 && g.kernel)
+            k_pair_disjoint<4, true><<<(unsigned)grid, 128, 0, st>>>(g, B, rows, cols, out);
         else if (g.mq == 4)
-            k_pair_disjoint<4><<<(unsigned)grid, 128, 0, st>>>(g, B, rows, cols, out);
+            k_pair_disjoint<4, false><<<(unsigned)grid, 128, 0, st>>>(g, B, rows, cols, out);
+        else if (g.kernel)
+            k_pair_disjoint<0, true><<<(unsigned)grid, 128, 0, st>>>(g, B, rows, cols, out);
         else
-            k_pair_disjoint<0><<<(unsigned)grid, 128, 0, st>>>(g, B, rows, cols, out);
+            k_pair_disjoint<0, false><<<(unsigned)grid, 128, 0, st>>>(g, B, rows, cols, out);
         GC_CHECK_LAUNCH("k_pair_disjoint");
         return GC_OK;
     }
@@ -538,6 +590,7 @@ int gc_assemble_blocks(const gc_geom* gp, int64_t nb, const int64_t* desc, int64
     if (nb > 0x7fffffffLL) { set_error(GC_ERR_CONFIG, "too many blocks"); return GC_ERR_CONFIG; }
     cudaStream_t st = (cudaStream_t)stream;
     const gc_geom g = *gp;
+    if (g.kernel && !g.normals) { set_error(GC_ERR_CONFIG, "double layer needs gc_geom.normals"); return GC_ERR_CONFIG; }
     switch (g.mq) {
         case 9: return launch_blocks<9>(g, nb, desc, max_rows, max_cols, row_idx, col_idx, out, *qp, flags, st);
         case 4: return launch_blocks<4>(g, nb, desc, max_rows, max_cols, row_idx, col_idx, out, *qp, flags, st);
@@ -550,18 +603,12 @@ int gc_assemble_blocks(const gc_geom* gp, int64_t nb, const int64_t* desc, int64
                 if (bytes <= 200 * 1024) {
                     RuleW rw;
                     e_copy_weights(g, rw, M);
-                    cudaError_t e;
-                    if (max_rows * ((max_cols + 1) / 2) <= 128) {
-                        e = cudaFuncSetAttribute(k_assemble_blocks_big<8, 128>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes);
-                        if (e != cudaSuccess) return cuda_status(e, "k_assemble_blocks_big smem");
-                        k_assemble_blocks_big<8, 128><<<(unsigned)nb, 128, bytes, st>>>(g, rw, M, desc, row_idx, col_idx, out, *qp, flags);
-                    } else {
-                        e = cudaFuncSetAttribute(k_assemble_blocks_big<8, 256>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes);
-                        if (e != cudaSuccess) return cuda_status(e, "k_assemble_blocks_big smem");
-                        k_assemble_blocks_big<8, 256><<<(unsigned)nb, 256, bytes, st>>>(g, rw, M, desc, row_idx, col_idx, out, *qp, flags);
-                    }
-                    GC_CHECK_LAUNCH("k_assemble_blocks_big");
-                    return GC_OK;
+                    const bool small = max_rows * ((max_cols + 1) / 2) <= 128;
+                    if (g.kernel)
+                        return small ? launch_big<8, 128, true>(g, rw, M, nb, desc, bytes, row_idx, col_idx, out, *qp, flags, st)
+                                     : launch_big<8, 256, true>(g, rw, M, nb, desc, bytes, row_idx, col_idx, out, *qp, flags, st);
+                    return small ? launch_big<8, 128, false>(g, rw, M, nb, desc, bytes, row_idx, col_idx, out, *qp, flags, st)
+                                 : launch_big<8, 256, false>(g, rw, M, nb, desc, bytes, row_idx, col_idx, out, *qp, flags, st);
                 }
             }
             k_assemble_blocks_any<<<(unsigned)nb, BLK_THREADS, 0, st>>>(g, desc, row_idx, col_idx, out, *qp, flags);

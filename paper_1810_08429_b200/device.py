@@ -99,9 +99,23 @@ class DeviceMesh:
             _native.call("gc_surface_points", ptr(self.corners), self.nt, ptr(n6), self.mq,
                          ptr(self.xq), stream_handle())
         self.wq_host = np.ascontiguousarray(wts, dtype=np.float64)
-        self.geom = _native.GcGeom(ptr(self.corners), ptr(self.gram), ptr(self.tri_vid),
-                                   ptr(self.xq), ptr(self.wq), self.nt, self.mq,
-                                   self.wq_host.ctypes.data)
+        # chart normal per triangle (|n| = gram), for the double layer
+        self.normals = to_dev(np.ascontiguousarray(pack.normals[:, 0]), device)
+        self.geom = self._struct(0)
+        self.geom_dlp = self._struct(1)
+
+    def _struct(self, kernel):
+        return _native.GcGeom(ptr(self.corners), ptr(self.gram), ptr(self.tri_vid),
+                              ptr(self.xq), ptr(self.wq), self.nt, self.mq,
+                              self.wq_host.ctypes.data, ptr(self.normals), kernel)
+
+    def geom_of(self, kind):
+        """The gc_geom of the single-layer ("slp") or double-layer ("dlp") kernel."""
+        if kind == "slp":
+            return self.geom
+        if kind == "dlp":
+            return self.geom_dlp
+        raise ConfigError("unknown kernel kind %r" % (kind,))
 
     @classmethod
     def get(cls, mesh, q_reg, device):
@@ -117,13 +131,14 @@ class DeviceRules:
     the xi-reduced coefficient form (quadrature.reduced_sauter_rule): SoA
     (NC coefficient columns, then weights) per case."""
 
-    def __init__(self, q_sing, device):
+    def __init__(self, q_sing, device, kind="slp"):
         self.q_sing = q_sing
+        self.kind = kind
         self.tables = [None] * 4
         self.npts = [0] * 4
         self.struct = _native.GcRules()
         for case in (1, 2, 3):
-            rule = reduced_sauter_rule(case, q_sing)
+            rule = reduced_sauter_rule(case, q_sing, 2 if kind == "slp" else 1)
             t = to_dev(np.concatenate([rule.coef.T.ravel(), rule.w]), device)
             self.tables[case] = t
             self.npts[case] = len(rule.w)
@@ -131,10 +146,12 @@ class DeviceRules:
             self.struct.npts[case] = len(rule.w)
 
     @classmethod
-    def get(cls, q_sing, device):
-        key = (str(device), int(q_sing))
+    def get(cls, q_sing, device, kind="slp"):
+        if kind not in ("slp", "dlp"):
+            raise ConfigError("unknown kernel kind %r" % (kind,))
+        key = (str(device), int(q_sing), kind)
         if key not in _RULE_CACHE:
-            _RULE_CACHE[key] = cls(int(q_sing), device)
+            _RULE_CACHE[key] = cls(int(q_sing), device, kind)
         return _RULE_CACHE[key]
 
 
@@ -183,9 +200,8 @@ class SingularQueue:
 
 
 def check_mesh(mesh, kind="slp", basis="constant"):
-    if kind != "slp":
-        raise ConfigError("device kernels implement the single-layer kernel only "
-                          "(dlp is out of scope, SURVEY.md §2)")
+    if kind not in ("slp", "dlp"):
+        raise ConfigError("unknown kernel kind %r" % (kind,))
     if basis != "constant":
         raise ConfigError("device kernels implement the piecewise-constant basis only "
                           "(linear/collocation are out of scope, SURVEY.md §8 f)")

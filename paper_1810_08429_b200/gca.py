@@ -573,7 +573,7 @@ def build_h2(btree, row_basis, col_basis, mesh, kind="slp", basis="constant",
         raise ConfigError("coupling block without basis content; build the bases "
                           "with coupling_marks(btree)")
     dmesh = DeviceMesh.get(mesh, orders[0], dev)
-    rules = DeviceRules.get(orders[1], dev)
+    rules = DeviceRules.get(orders[1], dev, kind)
     queue = SingularQueue.get(mesh, dev)
     t0 = time.perf_counter()
     # coupling blocks: pivot rows x pivot columns
@@ -586,7 +586,7 @@ def build_h2(btree, row_basis, col_basis, mesh, kind="slp", basis="constant",
     cdesc = np.stack([rstore.piv_off[cr], c_nr, cstore.piv_off[cc], c_nc, c_off], 1)
     keep = (c_nr > 0) & (c_nc > 0)
     stats_c = device_block_assembly(dmesh, rules, queue, rstore.pivots, cstore.pivots,
-                                    cdesc[keep], coup)
+                                    cdesc[keep], coup, kind=kind)
     t1 = time.perf_counter()
     # near-field blocks: full clusters
     n_nr = rf.stop[nr_r] - rf.start[nr_r]
@@ -596,7 +596,7 @@ def build_h2(btree, row_basis, col_basis, mesh, kind="slp", basis="constant",
     perm_r = to_dev(rf.perm, dev)
     perm_c = perm_r if cf is rf else to_dev(cf.perm, dev)
     ndesc = np.stack([rf.start[nr_r], n_nr, cf.start[nc_r], n_nc, n_off], 1)
-    stats_n = device_block_assembly(dmesh, rules, queue, perm_r, perm_c, ndesc, near)
+    stats_n = device_block_assembly(dmesh, rules, queue, perm_r, perm_c, ndesc, near, kind=kind)
     torch.cuda.synchronize(dev)
     t2 = time.perf_counter()
     d = DeviceH2(dev)

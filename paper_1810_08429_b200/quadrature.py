@@ -228,7 +228,7 @@ ReducedRule = namedtuple("ReducedRule", "coef w ncoef")
 
 
 @lru_cache(maxsize=None)
-def reduced_sauter_rule(kind, q):
+def reduced_sauter_rule(kind, q, xi_power=2):
     """The Sauter-Schwab rule of ``sauter_rule(kind, q)`` with the xi
     (radial) sum done exactly.
 
@@ -238,7 +238,9 @@ def reduced_sauter_rule(kind, q):
     xi^2 * j(eta) / (4 pi rhat(eta)).  The xi sum therefore factors out as
     S2 = sum_xi w_xi xi^2 (= 1/3 for q >= 2) and the rule keeps q^3 points
     per subdomain (2/10/6 q^3) - the same quadrature sum, 5x fewer kernel
-    evaluations at q = 5.
+    evaluations at q = 5.  The double-layer integrand <x-y, n_y>/r^3 is
+    homogeneous of degree -2, so its xi factor is xi^1: ``xi_power=1``
+    gives the same points with S1 = sum_xi w_xi xi.
 
     Points are returned as coefficients of the aligned chart edge vectors,
     ``D = x - y = sum_k coef[k] * G_k`` with
@@ -252,7 +254,9 @@ def reduced_sauter_rule(kind, q):
     if code not in (VERTEX, EDGE, IDENTICAL):
         raise ValueError("reduced rules exist for the singular cases only")
     g, w = _gauss01(q)
-    s2 = float(np.sum(w * g * g))
+    if xi_power not in (1, 2):
+        raise ValueError("xi_power must be 1 (double layer) or 2 (single layer)")
+    s2 = float(np.sum(w * g * g)) if xi_power == 2 else float(np.sum(w * g))
     e1, e2, e3 = (a.ravel() for a in np.meshgrid(g, g, g, indexing="ij"))
     w3 = np.einsum("i,j,k->ijk", w, w, w).ravel()
     one = np.ones_like(e1)

@@ -271,7 +271,7 @@ def test_matvec_properties_c2():
 
 def test_errors_map_to_reference_classes(sphere2):
     with pytest.raises(ConfigError):
-        assembly.assemble_galerkin_block("dlp", sphere2, "constant", [0], [1])
+        assembly.assemble_galerkin_block("hyp", sphere2, "constant", [0], [1])
     with pytest.raises(ConfigError):
         assembly.galerkin_pair_evaluator("slp", sphere2, "linear", 3, 5)
     tree = clustering.build_cluster_tree(sphere2, "constant", 16)

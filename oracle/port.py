@@ -128,6 +128,20 @@ def chart_nodes(vertices, triangles):
     return nodes, gram
 
 
+def chart_normals(vertices, triangles):
+    """Unnormalised chart normals at the six nodes (geometry.py:281-290):
+    for plane charts the node-0 normal repeated (|n| = gram)."""
+    nodes, _ = chart_nodes(vertices, triangles)
+    ref = np.array([[0.0, 0.0], [1.0, 0.0], [0.0, 1.0], [0.5, 0.0], [0.5, 0.5], [0.0, 0.5]])
+    x, y = ref[:, 0], ref[:, 1]
+    l0 = 1.0 - x - y
+    z = np.zeros(6)
+    gx = np.stack([1.0 - 4.0 * l0, 4.0 * x - 1.0, z, 4.0 * (l0 - x), 4.0 * y, -4.0 * y], 1)
+    gy = np.stack([1.0 - 4.0 * l0, z, 4.0 * y - 1.0, -4.0 * x, 4.0 * x, 4.0 * (l0 - y)], 1)
+    n = np.cross(np.einsum("ma,tac->tmc", gx, nodes), np.einsum("ma,tac->tmc", gy, nodes))
+    return np.repeat(n[:, :1], 6, axis=1)
+
+
 def _interp(coef, nodes6):
     """assembly.py:138-143, sequential over the 6 nodes, no BLAS."""
     out = np.zeros((nodes6.shape[0], coef.shape[0], 3))
@@ -138,9 +152,10 @@ def _interp(coef, nodes6):
 
 # ---------------------------------------------------------------- pair quadrature
 
-def pair_values(nodes, gram, case, rows, cols, px, py, q_reg=3, q_sing=5):
-    """assembly.py:175-214 for the single layer, constant basis, plane
-    charts: value per task, same operation order as the reference."""
+def pair_values(nodes, gram, case, rows, cols, px, py, q_reg=3, q_sing=5, kind="slp", normals=None):
+    """assembly.py:175-214 for the single layer (or, kind="dlp" with the
+    chart ``normals``, the double layer), constant basis, plane charts:
+    value per task, same operation order as the reference."""
     if case == 0:
         p, w1 = triangle_rule(q_reg)
         m = len(w1)
@@ -155,13 +170,19 @@ def pair_values(nodes, gram, case, rows, cols, px, py, q_reg=3, q_sing=5):
         X = _interp(nx, nodes[rows[sl][:, None], ORDER6[px[sl]]])
         Y = _interp(ny, nodes[cols[sl][:, None], ORDER6[py[sl]]])
         D = X - Y
-        r = np.sqrt(D[..., 0] ** 2 + D[..., 1] ** 2 + D[..., 2] ** 2)
-        kg = gram[rows[sl]][:, None] * gram[cols[sl]][:, None] / (FOUR_PI * r)
+        r2 = D[..., 0] ** 2 + D[..., 1] ** 2 + D[..., 2] ** 2
+        r = np.sqrt(r2)
+        if kind == "dlp":
+            nyv = _interp(ny, normals[cols[sl][:, None], ORDER6[py[sl]]])
+            dot = D[..., 0] * nyv[..., 0] + D[..., 1] * nyv[..., 1] + D[..., 2] * nyv[..., 2]
+            kg = dot / (FOUR_PI * r2 * r) * gram[rows[sl]][:, None]
+        else:
+            kg = gram[rows[sl]][:, None] * gram[cols[sl]][:, None] / (FOUR_PI * r)
         out[sl] = np.sum(kg * w[None, :], axis=1)
     return out
 
 
-def block(nodes, gram, triangles, rows, cols, q=(3, 5)):
+def block(nodes, gram, triangles, rows, cols, q=(3, 5), kind="slp", normals=None):
     """Dense block G[rows, cols] (assembly.py:330-337)."""
     rows = np.asarray(rows)
     cols = np.asarray(cols)
@@ -171,7 +192,7 @@ def block(nodes, gram, triangles, rows, cols, q=(3, 5)):
     for k in range(4):
         m = case == k
         if m.any():
-            vals[m] = pair_values(nodes, gram, k, R[m], C[m], px[m], py[m], *q)
+            vals[m] = pair_values(nodes, gram, k, R[m], C[m], px[m], py[m], *q, kind=kind, normals=normals)
     return vals.reshape(len(rows), len(cols))
 
 

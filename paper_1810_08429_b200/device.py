@@ -42,6 +42,8 @@ def ptr(t):
 
 def to_dev(a, device, dtype=None):
     a = np.ascontiguousarray(a)
+    if not a.flags.writeable:          # read-only views (broadcasts): copy
+        a = a.copy()
     t = torch.from_numpy(a)
     if dtype is not None:
         t = t.to(dtype)

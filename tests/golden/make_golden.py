@@ -1,7 +1,8 @@
 """Generate the golden fixtures from the reference implementation itself.
 
 Run in the build container (the reference is importable there):
-    PYTHONPATH=/root/reference/pkg/src python tests/golden/make_golden.py
+    PYTHONPATH=/root/reference/pkg/src python tests/golden/make_golden.py [--dlp]
+(--dlp writes only the double-layer fixtures)
 Outputs tests/golden/*.npz.  The GPU box has no /root/reference; the tests
 read only these committed files.
 """
@@ -28,7 +29,7 @@ def cube(level):
     return G.TriangleMesh(v / np.abs(v).max(axis=1, keepdims=True), s.triangles)
 
 
-def pair_tasks(mesh, n_disjoint, seed):
+def pair_tasks(mesh, n_disjoint, seed, kind="slp"):
     """Random disjoint tasks plus every singular pair of a triangle subset."""
     rng = np.random.default_rng(seed)
     rows = list(rng.integers(0, mesh.nt, n_disjoint))
@@ -41,7 +42,7 @@ def pair_tasks(mesh, n_disjoint, seed):
                 cols.append(int(s))
     rows, cols = np.array(rows), np.array(cols)
     case, px, py = Q.classify_pairs(mesh.triangles[rows], mesh.triangles[cols])
-    ev = A.galerkin_pair_evaluator("slp", mesh, "constant", 3, 5)
+    ev = A.galerkin_pair_evaluator(kind, mesh, "constant", 3, 5)
     vals = np.empty(len(rows))
     for k in range(4):
         m = case == k
@@ -154,6 +155,37 @@ def aca_kats():
                 piv=np.concatenate(pivs), npiv=np.array(npiv), V=np.concatenate(vs))
 
 
+def dlp_pipeline(mesh, eps, seed):
+    """The reference's GCA-H2 of the double-layer operator (same nested
+    bases, dlp coupling and near-field blocks): matvecs and sampled blocks."""
+    tree = C.build_cluster_tree(mesh, "constant", 16)
+    bt = C.build_block_tree(tree, eta=1.0)
+    rm, cm = GC.coupling_marks(bt)
+    rb = GC.build_cluster_basis(tree, mesh, "constant", 3, 0.5, eps, "row", (3, 5), rm)
+    cb = GC.build_cluster_basis(tree, mesh, "constant", 3, 0.5, eps, "col", (3, 5), cm)
+    hm = GC.build_h2(bt, rb, cb, mesh, "dlp", "constant", "galerkin", (3, 5))
+    rng = np.random.default_rng(seed)
+    x = rng.standard_normal((3, mesh.nt))
+    y = np.array([H.mvm(hm, v) for v in x])
+    pick = rng.choice(len(hm.nearfield), 8, replace=False)
+    near_r = np.array([hm.nearfield[i].row.index for i in pick], np.int32)
+    near_c = np.array([hm.nearfield[i].col.index for i in pick], np.int32)
+    near_v = np.concatenate([hm.nearfield[i].values.ravel() for i in pick])
+    return dict(x=x, mvm=y, near_row=near_r, near_col=near_c, near_values=near_v)
+
+
+def main_dlp():
+    s3 = G.build_sphere_mesh(3)
+    np.savez_compressed(os.path.join(OUT, "pairs_dlp_sphere3.npz"), **pair_tasks(s3, 600, 31, "dlp"))
+    np.savez_compressed(os.path.join(OUT, "pairs_dlp_cube3.npz"), **pair_tasks(cube(3), 300, 32, "dlp"))
+    s2 = G.build_sphere_mesh(2)
+    idx = np.arange(s2.nt)
+    np.savez_compressed(os.path.join(OUT, "dense_dlp_sphere2.npz"),
+                        values=A.assemble_galerkin_block("dlp", s2, "constant", idx, idx).values)
+    np.savez_compressed(os.path.join(OUT, "h2_dlp_sphere4_eps1e-6.npz"),
+                        **dlp_pipeline(G.build_sphere_mesh(4), 1e-6, 33))
+
+
 def main():
     s3 = G.build_sphere_mesh(3)
     np.savez_compressed(os.path.join(OUT, "pairs_sphere3.npz"), **pair_tasks(s3, 600, 11))
@@ -173,4 +205,4 @@ def main():
 
 
 if __name__ == "__main__":
-    main()
+    main_dlp() if "--dlp" in sys.argv else main()

@@ -427,3 +427,69 @@ def test_sharded_operator_multirank_matches_full(world, tmp_path):
     y[tree.perm] = yt
     ref = h2.mvm(hm, x)
     assert np.linalg.norm(y - ref) <= 1e-13 * np.linalg.norm(ref)
+
+
+
+# ---------------------------------------------------------------- double layer
+# (first step: the DLP kernel, constant basis, plane charts)
+
+@pytest.mark.parametrize("name,mesh_name", [("pairs_dlp_sphere3.npz", "x_sphere3"),
+                                            ("pairs_dlp_cube3.npz", "x_cube3")])
+def test_dlp_pair_evaluator_seam(name, mesh_name):
+    """Device double-layer pair integrals vs the reference's values.  The
+    identical-pair values are rounding noise around 0 (x - y lies in the
+    plane of n_y), so every case is compared against the largest value."""
+    g = golden(name)
+    mesh = mesh_for(mesh_name)
+    ev = assembly.galerkin_pair_evaluator("dlp", mesh, "constant", 3, 5)
+    scale = np.max(np.abs(g["values"]))
+    for k in range(4):
+        m = g["case"] == k
+        got = ev(k, g["rows"][m], g["cols"][m], g["px"][m], g["py"][m]).ravel()
+        assert np.max(np.abs(got - g["values"][m])) <= 1e-13 * scale, "case %d" % k
+        if k in (0, 1, 2):
+            nz = np.abs(g["values"][m]) > 1e-6 * scale
+            assert np.max(np.abs(got[nz] - g["values"][m][nz]) / np.abs(g["values"][m][nz])) < 1e-11
+
+
+def test_dlp_dense_block_and_gauss_identity(sphere2):
+    """Dense DLP block vs the reference, and the interior Gauss identity of
+    the double layer on a closed surface: K 1 = -1/2 M 1 up to O(h)."""
+    idx = np.arange(sphere2.nt)
+    d = assembly.assemble_galerkin_block("dlp", sphere2, "constant", idx, idx).values
+    ref = golden("dense_dlp_sphere2.npz")["values"]
+    assert rel(d, ref) < 1e-13
+    areas = 0.5 * geometry.chart_pack(sphere2).gram
+    for L in (3, 4):
+        m = geometry.build_sphere_mesh(L)
+        i = np.arange(m.nt)
+        k = assembly.assemble_galerkin_block("dlp", m, "constant", i, i).values
+        a = 0.5 * geometry.chart_pack(m).gram
+        err = np.linalg.norm(k.sum(axis=1) + 0.5 * a) / np.linalg.norm(0.5 * a)
+        assert err < {3: 0.05, 4: 0.03}[L]
+    assert areas.sum() > 0
+
+
+def test_dlp_h2_matvec_vs_reference():
+    """GCA-H2 of the double-layer operator (same nested bases, DLP coupling
+    and near-field blocks, gca.py:282-312 with kind="dlp") vs the
+    reference's H2: sampled near-field blocks and three matvecs."""
+    g = golden("h2_dlp_sphere4_eps1e-6.npz")
+    mesh = geometry.build_sphere_mesh(4)
+    cfg = cli.default_config(eps=1e-6)
+    tree = clustering.build_cluster_tree(mesh, "constant", 16)
+    bt = clustering.build_block_tree(tree, eta=1.0)
+    rm, cm = gca.coupling_marks(bt)
+    rb = gca.build_cluster_basis(tree, mesh, "constant", 3, 0.5, 1e-6, "row", (3, 5), rm)
+    cb = gca.build_cluster_basis(tree, mesh, "constant", 3, 0.5, 1e-6, "col", (3, 5), cm)
+    hm = gca.build_h2(bt, rb, cb, mesh, "dlp", "constant", "galerkin", (3, 5))
+    near = {(b.row.index, b.col.index): b.values for b in hm.nearfield}
+    off = 0
+    for r, c in zip(g["near_row"], g["near_col"]):
+        v = near[(int(r), int(c))]
+        ref = g["near_values"][off:off + v.size].reshape(v.shape)
+        off += v.size
+        assert np.max(np.abs(v - ref)) <= 1e-13 * np.max(np.abs(ref))
+    for x, y in zip(g["x"], g["mvm"]):
+        assert np.linalg.norm(h2.mvm(hm, x) - y) <= 1e-12 * np.linalg.norm(y)
+    assert cfg.eps == 1e-6

@@ -143,3 +143,32 @@ def test_oracle_bases_and_blocks_sphere4():
             vals = P.block(h.nodes, h.gram, h.tris, r, c)
             assert np.array_equal(vals.ravel(), g[key + "_vals"][off:off + vals.size])
             off += int(np.prod(shp))
+
+
+# ---------------------------------------------------------------- double layer
+
+@pytest.mark.parametrize("name,mesh_name", [("pairs_dlp_sphere3.npz", "x_sphere3"),
+                                            ("pairs_dlp_cube3.npz", "x_cube3")])
+def test_dlp_pair_values_bitwise(name, mesh_name):
+    """Double-layer pair integrals (assembly.py:194-201): the oracle equals
+    the reference bit for bit in every case."""
+    g = golden(name)
+    mesh = mesh_for(mesh_name)
+    nodes, gram = P.chart_nodes(mesh.vertices, mesh.triangles)
+    normals = P.chart_normals(mesh.vertices, mesh.triangles)
+    case, px, py = P.classify(mesh.triangles[g["rows"]], mesh.triangles[g["cols"]])
+    assert np.array_equal(case, g["case"])
+    for k in range(4):
+        m = case == k
+        got = P.pair_values(nodes, gram, k, g["rows"][m], g["cols"][m], px[m], py[m],
+                            kind="dlp", normals=normals)
+        assert np.array_equal(got, g["values"][m]), "case %d" % k
+
+
+def test_dlp_dense_sphere2_bitwise():
+    mesh = build_sphere_mesh(2)
+    nodes, gram = P.chart_nodes(mesh.vertices, mesh.triangles)
+    normals = P.chart_normals(mesh.vertices, mesh.triangles)
+    idx = np.arange(mesh.nt)
+    got = P.block(nodes, gram, mesh.triangles, idx, idx, kind="dlp", normals=normals)
+    assert np.array_equal(got, golden("dense_dlp_sphere2.npz")["values"])

@@ -249,6 +249,27 @@ int gc_panel_tma(int64_t nitems, const int64_t* items, const int32_t* xidx,
                  void* stream);
 int64_t gc_panel_tma_item_elems(void);
 
+/* Piecewise-linear basis (assembly.py:54-135, 175-214, 279-304;
+ * batchexec.py:178-209).  gc_lin_pairs: tasks [dev] (n,2) triangle pairs
+ * (t, s); for each, 9 pair integrals of k(x,y) phi_a(x) phi_c(y) in the
+ * canonical permuted local order -> U[9i..9i+8], pp[i] = px | py << 8;
+ * disjoint pairs integrate the regular rule (rule_w [host] q^2 weights,
+ * rule_b [host] q^2 x 3 barycentric values), singular pairs are queued.
+ * gc_lin_singular: integrates the queued pairs with the reference's full
+ * Sauter-Schwab rules (r->table[c] = SoA x1, x2, y1, y2, w of npts[c]
+ * points).  gc_lin_gather: desc (nb,7) = row_ptr_off, nr, col_ptr_off, nc,
+ * out_off, task_base, n_col_tris; rptr/cptr CSR per DOF into rlist/clist
+ * of packed (table_row << 2 | corner); out column-major per block, each
+ * entry the fixed-order sum of its pairs' contributions. */
+int gc_lin_pairs(const gc_geom* g, const double* rule_w, const double* rule_b, int64_t n,
+                 const int64_t* tasks, double* U, int32_t* pp, gc_queue* q, int32_t* flags,
+                 void* stream);
+int gc_lin_singular(const gc_geom* g, const gc_rules* r, gc_queue* q, double* U,
+                    int64_t* counts_out, void* stream);
+int gc_lin_gather(int64_t nb, const int64_t* desc, const int64_t* rptr, const int64_t* rlist,
+                  const int64_t* cptr, const int64_t* clist, const double* U, const int32_t* pp,
+                  double* out, void* stream);
+
 /* Device-side Krylov support (consumers of the matvec, h2.py:190-253;
  * SURVEY 8f rank 3).  Deterministic dot product: fixed grid of
  * gc_krylov_partials() blocks, `partial` [dev] holds that many doubles.

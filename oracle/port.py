@@ -182,6 +182,81 @@ def pair_values(nodes, gram, case, rows, cols, px, py, q_reg=3, q_sing=5, kind="
     return out
 
 
+def _bary(pts):
+    return np.stack([1.0 - pts[:, 0] - pts[:, 1], pts[:, 0], pts[:, 1]], axis=1)
+
+
+def pair_values_linear(nodes, gram, case, rows, cols, px, py, q_reg=3, q_sing=5, kind="slp",
+                       normals=None):
+    """assembly.py:122-135, 175-214 for the piecewise-linear basis: the
+    (B, 3, 3) pair integrals in the canonical permuted local order."""
+    if case == 0:
+        p, w1 = triangle_rule(q_reg)
+        m = len(w1)
+        xh, yh, w = np.repeat(p, m, axis=0), np.tile(p, (m, 1)), np.outer(w1, w1).ravel()
+    else:
+        xh, yh, w = sauter(case, q_sing)
+    nx, ny = shape6(xh), shape6(yh)
+    wb = np.einsum("m,ma,mb->abm", w, _bary(xh), _bary(yh))
+    out = np.empty((len(rows), 3, 3))
+    step = max(1, (1 << 19) // len(w))
+    for s in range(0, len(rows), step):
+        sl = slice(s, s + step)
+        X = _interp(nx, nodes[rows[sl][:, None], ORDER6[px[sl]]])
+        Y = _interp(ny, nodes[cols[sl][:, None], ORDER6[py[sl]]])
+        D = X - Y
+        r2 = D[..., 0] ** 2 + D[..., 1] ** 2 + D[..., 2] ** 2
+        r = np.sqrt(r2)
+        if kind == "dlp":
+            nyv = _interp(ny, normals[cols[sl][:, None], ORDER6[py[sl]]])
+            dot = D[..., 0] * nyv[..., 0] + D[..., 1] * nyv[..., 1] + D[..., 2] * nyv[..., 2]
+            kg = dot / (FOUR_PI * r2 * r) * gram[rows[sl]][:, None]
+        else:
+            kg = gram[rows[sl]][:, None] * gram[cols[sl]][:, None] / (FOUR_PI * r)
+        for a in range(3):
+            for c in range(3):
+                out[sl, a, c] = np.sum(kg * wb[a, c][None, :], axis=1)
+    return out
+
+
+def triangle_table(indices, triangles, nv):
+    """assembly.py:54-89: rows (triangle, slot0..2) sorted by triangle, slot
+    = 1-based position of the vertex in ``indices`` (0 if absent)."""
+    pos = np.zeros(nv, dtype=np.int64)
+    pos[np.asarray(indices)] = np.arange(1, len(indices) + 1)
+    slots = pos[triangles]
+    tri = np.flatnonzero(slots.any(axis=1))
+    return np.column_stack([tri, slots[tri]])
+
+
+def block_linear(nodes, gram, triangles, rows, cols, q=(3, 5), kind="slp", normals=None):
+    """Dense linear-basis Galerkin block (assembly.py:279-304, 330-337) with
+    the executor's scatter order (batchexec.py:178-209): contributions in
+    enqueue order, one np.add.at per (row slot, column slot)."""
+    nv = int(triangles.max()) + 1
+    tr = triangle_table(rows, triangles, nv)
+    tc = triangle_table(cols, triangles, nv)
+    nr, nc = len(tr), len(tc)
+    R, C = np.repeat(tr[:, 0], nc), np.tile(tc[:, 0], nr)
+    rs = np.repeat(tr[:, 1:] - 1, nc, axis=0)
+    cs = np.tile(tc[:, 1:] - 1, (nr, 1))
+    case, px, py = classify(triangles[R], triangles[C])
+    rs = np.take_along_axis(rs, PERMS3[px], axis=1)
+    cs = np.take_along_axis(cs, PERMS3[py], axis=1)
+    vals = np.empty((len(R), 3, 3))
+    for k in range(4):
+        m = case == k
+        if m.any():
+            vals[m] = pair_values_linear(nodes, gram, k, R[m], C[m], px[m], py[m], *q, kind=kind,
+                                         normals=normals)
+    mat = np.zeros((len(rows), len(cols)))
+    for a in range(3):
+        for b in range(3):
+            ok = (rs[:, a] >= 0) & (cs[:, b] >= 0)
+            np.add.at(mat, (rs[ok, a], cs[ok, b]), vals[ok, a, b])
+    return mat
+
+
 def block(nodes, gram, triangles, rows, cols, q=(3, 5), kind="slp", normals=None):
     """Dense block G[rows, cols] (assembly.py:330-337)."""
     rows = np.asarray(rows)

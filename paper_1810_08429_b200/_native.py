@@ -57,6 +57,10 @@ _SIGNATURES = {
     "gc_panel_chain_grid": [ctypes.POINTER(c_i64)],
     "gc_panel_chain": [c_i64, c_p, c_i64, c_p, c_p],
     "gc_panel_phase_bytes": [],
+    "gc_lin_pairs": [ctypes.POINTER(GcGeom), c_p, c_p, c_i64, c_p, c_p, c_p, ctypes.POINTER(GcQueue), c_p, c_p],
+    "gc_lin_singular": [ctypes.POINTER(GcGeom), ctypes.POINTER(GcRules), ctypes.POINTER(GcQueue), c_p,
+                        ctypes.POINTER(c_i64), c_p],
+    "gc_lin_gather": [c_i64, c_p, c_p, c_p, c_p, c_p, c_p, c_p, c_p, c_p],
     "gc_dot": [c_i64, c_p, c_p, c_p, c_p, c_p],
     "gc_cg_pq": [c_i64, c_p, c_p, c_p, c_p, c_p],
     "gc_cg_update": [c_i64, c_p, c_p, c_p, c_p, c_p, c_p, c_p],

@@ -31,6 +31,7 @@ from .errors import ConfigError, GeometryError
 
 FOUR_PI = 4.0 * np.pi
 DenseBlock = namedtuple("DenseBlock", "rows cols values")
+TriangleTable = namedtuple("TriangleTable", "rows")
 
 
 def galerkin_classify(mesh):
@@ -43,15 +44,36 @@ def galerkin_classify(mesh):
     return classify
 
 
+def triangle_table(indices, mesh, basis="linear"):
+    """Triangle table of vertex DOFs (``assembly.py:54-89``): rows
+    (triangle, slot0, slot1, slot2) sorted by triangle."""
+    if basis != "linear":
+        raise ConfigError("triangle tables index vertex DOFs (linear basis)")
+    from . import linear
+    return TriangleTable(linear.triangle_table(indices, mesh))
+
+
 def galerkin_pair_evaluator(kind, mesh, basis, q_reg, q_sing, device=None):
-    """Batched device pair evaluator for the executor seam."""
+    """Batched device pair evaluator for the executor seam: values of shape
+    (B, 1, 1) (constant basis) or (B, 3, 3) (linear basis, canonical permuted
+    local order, ``batchexec.py:70-76``)."""
     if kind not in ("slp", "dlp"):
         raise ConfigError("unknown kernel kind %r" % (kind,))
     if basis not in ("constant", "linear"):
         raise ConfigError("unknown basis %r" % (basis,))
-    check_mesh(mesh, kind, basis)
+    check_mesh(mesh, kind, basis, linear_ok=True)
     dev = require_device(device)
     dmesh = DeviceMesh.get(mesh, q_reg, dev)
+    if basis == "linear":
+        from . import linear
+        lrules = linear.LinearRules.get(q_reg, q_sing, dev)
+
+        def evaluate_linear(case, rows, cols, px, py):
+            if int(case) not in (0, 1, 2, 3):
+                raise ConfigError("unknown pair case %r" % (case,))
+            return linear.pair_values(dmesh, kind, lrules, rows, cols, dev)
+
+        return evaluate_linear
     rules = DeviceRules.get(q_sing, dev, kind)
     geom = dmesh.geom_of(kind)
 
@@ -99,8 +121,9 @@ def device_block_assembly(dmesh, rules, queue, row_idx, col_idx, desc, out, stat
 
 def assemble_galerkin_block(kind, mesh, basis, rows, cols, orders=(3, 5), capacity=None,
                             threads=None, device=None):
-    """Dense Galerkin block G[rows, cols] (``assembly.py:330-337``)."""
-    check_mesh(mesh, kind, basis)
+    """Dense Galerkin block G[rows, cols] (``assembly.py:330-337``); rows
+    and columns are triangles (constant basis) or vertices (linear basis)."""
+    check_mesh(mesh, kind, basis, linear_ok=True)
     rows = np.asarray(rows, dtype=np.int64)
     cols = np.asarray(cols, dtype=np.int64)
     if len(np.unique(rows)) != len(rows) or len(np.unique(cols)) != len(cols):
@@ -110,6 +133,12 @@ def assemble_galerkin_block(kind, mesh, basis, rows, cols, orders=(3, 5), capaci
         return DenseBlock(rows, cols, np.zeros((nr, nc)))
     dev = require_device(device)
     dmesh = DeviceMesh.get(mesh, orders[0], dev)
+    if basis == "linear":
+        from . import linear
+        out = empty(nr * nc, dev)
+        linear.assemble_blocks(dmesh, kind, linear.LinearRules.get(orders[0], orders[1], dev), mesh,
+                               [(rows, cols, 0)], out, dev)
+        return DenseBlock(rows, cols, out.cpu().numpy().reshape(nc, nr).T.copy())
     rules = DeviceRules.get(orders[1], dev, kind)
     queue = SingularQueue.get(mesh, dev)
     out = empty(nr * nc, dev)

@@ -201,11 +201,15 @@ class SingularQueue:
             self.flags.zero_()
 
 
-def check_mesh(mesh, kind="slp", basis="constant"):
+def check_mesh(mesh, kind="slp", basis="constant", linear_ok=False):
+    """Validate (kernel, basis, geometry) for a device path; ``linear_ok``
+    marks the paths that implement the linear basis."""
+    if basis == "linear" and not linear_ok:
+        raise ConfigError("the linear basis is implemented for pair evaluation and dense "
+                          "blocks; this path supports the constant basis")
     if kind not in ("slp", "dlp"):
         raise ConfigError("unknown kernel kind %r" % (kind,))
-    if basis != "constant":
-        raise ConfigError("device kernels implement the piecewise-constant basis only "
-                          "(linear/collocation are out of scope, SURVEY.md §8 f)")
+    if basis not in ("constant", "linear"):
+        raise ConfigError("unknown basis %r" % (basis,))
     if getattr(mesh, "midpoints", None) is not None:
         raise ConfigError("curved charts are out of scope")

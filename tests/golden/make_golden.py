@@ -1,8 +1,8 @@
 """Generate the golden fixtures from the reference implementation itself.
 
 Run in the build container (the reference is importable there):
-    PYTHONPATH=/root/reference/pkg/src python tests/golden/make_golden.py [--dlp]
-(--dlp writes only the double-layer fixtures)
+    PYTHONPATH=/root/reference/pkg/src python tests/golden/make_golden.py [--dlp | --linear]
+(--dlp / --linear write only the double-layer / linear-basis fixtures)
 Outputs tests/golden/*.npz.  The GPU box has no /root/reference; the tests
 read only these committed files.
 """
@@ -174,6 +174,37 @@ def dlp_pipeline(mesh, eps, seed):
     return dict(x=x, mvm=y, near_row=near_r, near_col=near_c, near_values=near_v)
 
 
+def lin_pair_tasks(mesh, n_disjoint, seed, kind):
+    """Linear-basis pair integrals (B, 3, 3) from the reference's evaluator."""
+    g = pair_tasks(mesh, n_disjoint, seed)
+    ev = A.galerkin_pair_evaluator(kind, mesh, "linear", 3, 5)
+    vals = np.empty((len(g["rows"]), 3, 3))
+    for k in range(4):
+        m = g["case"] == k
+        if m.any():
+            vals[m] = ev(k, g["rows"][m], g["cols"][m], g["px"][m], g["py"][m])
+    g["values"] = vals
+    return g
+
+
+def main_linear():
+    s3 = G.build_sphere_mesh(3)
+    for kind in ("slp", "dlp"):
+        np.savez_compressed(os.path.join(OUT, "pairs_lin_%s_sphere3.npz" % kind),
+                            **lin_pair_tasks(s3, 300, 41, kind))
+    s2 = G.build_sphere_mesh(2)
+    dofs = np.arange(s2.nv)
+    rng = np.random.default_rng(42)
+    r = rng.choice(s2.nv, 7, replace=False)
+    c = rng.choice(s2.nv, 9, replace=False)
+    np.savez_compressed(os.path.join(OUT, "dense_lin_sphere2.npz"),
+                        slp=A.assemble_galerkin_block("slp", s2, "linear", dofs, dofs).values,
+                        dlp=A.assemble_galerkin_block("dlp", s2, "linear", dofs, dofs).values,
+                        sub_rows=r, sub_cols=c,
+                        sub=A.assemble_galerkin_block("slp", s2, "linear", r, c).values,
+                        table_rows=r, table=A.triangle_table(r, s2).rows)
+
+
 def main_dlp():
     s3 = G.build_sphere_mesh(3)
     np.savez_compressed(os.path.join(OUT, "pairs_dlp_sphere3.npz"), **pair_tasks(s3, 600, 31, "dlp"))
@@ -205,4 +236,9 @@ def main():
 
 
 if __name__ == "__main__":
-    main_dlp() if "--dlp" in sys.argv else main()
+    if "--dlp" in sys.argv:
+        main_dlp()
+    elif "--linear" in sys.argv:
+        main_linear()
+    else:
+        main()

@@ -273,7 +273,7 @@ def test_errors_map_to_reference_classes(sphere2):
     with pytest.raises(ConfigError):
         assembly.assemble_galerkin_block("hyp", sphere2, "constant", [0], [1])
     with pytest.raises(ConfigError):
-        assembly.galerkin_pair_evaluator("slp", sphere2, "linear", 3, 5)
+        assembly.galerkin_pair_evaluator("slp", sphere2, "quadratic", 3, 5)
     tree = clustering.build_cluster_tree(sphere2, "constant", 16)
     leaf = tree.leaves()[0]
     # an expansion point exactly on a surface quadrature point trips the
@@ -493,3 +493,40 @@ def test_dlp_h2_matvec_vs_reference():
     for x, y in zip(g["x"], g["mvm"]):
         assert np.linalg.norm(h2.mvm(hm, x) - y) <= 1e-12 * np.linalg.norm(y)
     assert cfg.eps == 1e-6
+
+
+# ---------------------------------------------------------------- linear basis
+# (vertex DOFs, 3x3 pair integrals, device scatter)
+
+@pytest.mark.parametrize("kind", ["slp", "dlp"])
+def test_linear_pair_evaluator_seam(kind):
+    g = golden("pairs_lin_%s_sphere3.npz" % kind)
+    mesh = mesh_for("x_sphere3")
+    ev = assembly.galerkin_pair_evaluator(kind, mesh, "linear", 3, 5)
+    scale = np.max(np.abs(g["values"]))
+    for k in range(4):
+        m = g["case"] == k
+        got = ev(k, g["rows"][m], g["cols"][m], g["px"][m], g["py"][m])
+        assert got.shape == (int(m.sum()), 3, 3)
+        # identical pairs of the double layer are rounding noise around 0
+        # (x - y lies in the plane of n_y): 1e-12 of the largest value
+        tol = 1e-12 if (kind, k) == ("dlp", 3) else 1e-13
+        assert np.max(np.abs(got - g["values"][m])) <= tol * scale, "case %d" % k
+
+
+def test_linear_dense_blocks(sphere2):
+    g = golden("dense_lin_sphere2.npz")
+    dofs = np.arange(sphere2.nv)
+    for kind in ("slp", "dlp"):
+        d = assembly.assemble_galerkin_block(kind, sphere2, "linear", dofs, dofs).values
+        assert rel(d, g[kind]) < 1e-13, kind
+    sub = assembly.assemble_galerkin_block("slp", sphere2, "linear", g["sub_rows"], g["sub_cols"]).values
+    assert rel(sub, g["sub"]) < 1e-13
+    # single layer: symmetric positive definite on the vertex DOFs
+    d = assembly.assemble_galerkin_block("slp", sphere2, "linear", dofs, dofs).values
+    assert np.max(np.abs(d - d.T)) <= 1e-13 * np.max(np.abs(d))
+    assert np.all(np.linalg.eigvalsh(0.5 * (d + d.T)) > 0)
+    # bitwise reproducible, and a sub-block equals the dense slice to rounding
+    d2 = assembly.assemble_galerkin_block("slp", sphere2, "linear", dofs, dofs).values
+    assert np.array_equal(d, d2)
+    assert rel(sub, d[np.ix_(g["sub_rows"], g["sub_cols"])]) < 1e-13

@@ -172,3 +172,43 @@ def test_dlp_dense_sphere2_bitwise():
     idx = np.arange(mesh.nt)
     got = P.block(nodes, gram, mesh.triangles, idx, idx, kind="dlp", normals=normals)
     assert np.array_equal(got, golden("dense_dlp_sphere2.npz")["values"])
+
+
+# ---------------------------------------------------------------- linear basis
+
+@pytest.mark.parametrize("kind", ["slp", "dlp"])
+def test_linear_pair_values_bitwise(kind):
+    """Linear-basis 3x3 pair integrals (assembly.py:122-135, 175-214)."""
+    g = golden("pairs_lin_%s_sphere3.npz" % kind)
+    mesh = mesh_for("x_sphere3")
+    nodes, gram = P.chart_nodes(mesh.vertices, mesh.triangles)
+    normals = P.chart_normals(mesh.vertices, mesh.triangles)
+    for k in range(4):
+        m = g["case"] == k
+        got = P.pair_values_linear(nodes, gram, k, g["rows"][m], g["cols"][m], g["px"][m], g["py"][m],
+                                   kind=kind, normals=normals)
+        assert np.array_equal(got, g["values"][m]), "case %d" % k
+
+
+def test_linear_dense_blocks_and_table_bitwise():
+    g = golden("dense_lin_sphere2.npz")
+    mesh = build_sphere_mesh(2)
+    nodes, gram = P.chart_nodes(mesh.vertices, mesh.triangles)
+    normals = P.chart_normals(mesh.vertices, mesh.triangles)
+    dofs = np.arange(mesh.nv)
+    assert np.array_equal(P.triangle_table(g["table_rows"], mesh.triangles, mesh.nv), g["table"])
+    assert np.array_equal(P.block_linear(nodes, gram, mesh.triangles, dofs, dofs), g["slp"])
+    assert np.array_equal(P.block_linear(nodes, gram, mesh.triangles, dofs, dofs, kind="dlp",
+                                         normals=normals), g["dlp"])
+    assert np.array_equal(P.block_linear(nodes, gram, mesh.triangles, g["sub_rows"], g["sub_cols"]),
+                          g["sub"])
+
+
+def test_linear_triangle_table_host_matches_oracle():
+    from paper_1810_08429_b200 import linear
+    mesh = build_sphere_mesh(3)
+    rng = np.random.default_rng(8)
+    for n in (1, 7, 40, mesh.nv):
+        idx = rng.choice(mesh.nv, n, replace=False)
+        assert np.array_equal(linear.triangle_table(idx, mesh),
+                              P.triangle_table(idx, mesh.triangles, mesh.nv))

@@ -63,6 +63,15 @@ typedef struct gc_geom {
     /* 0 = single layer 1/(4 pi r), 1 = double layer <x-y, n_y>/(4 pi r^3)
      * (assembly.py:196-201) */
     int64_t kernel;
+    /* linear basis (basis = 1): per vertex v the star entries
+     * vstar_ent[vstar_ptr[v] .. vstar_ptr[v+1]) = (triangle << 2 | corner)
+     * ordered by (corner, triangle) - the order in which the reference's
+     * np.add.at scatters a vertex's moments (assembly.py:406-415) - and the
+     * barycentric values bq [dev] (mq x 3) of the regular rule's points */
+    const int64_t* vstar_ptr;
+    const int64_t* vstar_ent;
+    const double* bq;
+    int64_t basis;
 } gc_geom;
 
 /* Singular pair rules (quadrature.sauter_rule, quadrature.py:211-284) in

@@ -20,7 +20,8 @@ c_p = ctypes.c_void_p
 class GcGeom(ctypes.Structure):
     _fields_ = [("corners", c_p), ("gram", c_p), ("tri_vid", c_p), ("xq", c_p),
                 ("wq", c_p), ("nt", c_i64), ("mq", c_i64), ("wq_host", c_p),
-                ("normals", c_p), ("kernel", c_i64)]
+                ("normals", c_p), ("kernel", c_i64), ("vstar_ptr", c_p), ("vstar_ent", c_p),
+                ("bq", c_p), ("basis", c_i64)]
 
 
 class GcRules(ctypes.Structure):

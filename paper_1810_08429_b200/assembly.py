@@ -152,13 +152,15 @@ def assemble_galerkin_block(kind, mesh, basis, rows, cols, orders=(3, 5), capaci
 # Green factors
 
 def green_factors_device(dmesh, side, K, rows, desc, dtau, z, sq, nz, total_rows, device,
-                         check_flags=True):
+                         check_flags=True, basis="constant"):
     """Factor matrices of a batch of nodes (device buffer, row-major per
-    node).  Raises GeometryError if an expansion point touches the surface."""
+    node); rows are triangles (constant basis) or vertices (linear basis).
+    Raises GeometryError if an expansion point touches the surface."""
     out = empty(total_rows * 2 * K, device)
     flags = torch.zeros(1, dtype=torch.int32, device=device)
     with torch.cuda.device(device):
-        _native.call("gc_green_factor", dmesh.geom, {"row": 0, "col": 1}.get(side, -1), K, desc.numel() // 5,
+        _native.call("gc_green_factor", dmesh.geom_of("slp", basis), {"row": 0, "col": 1}.get(side, -1), K,
+                     desc.numel() // 5,
                      ptr(desc), ptr(dtau), ptr(z), ptr(sq), ptr(nz), ptr(rows), ptr(out),
                      ptr(flags), stream_handle())
     if check_flags:
@@ -173,7 +175,7 @@ def touch_check(flags):
 
 
 def _single_factor(side, cluster, rule, mesh, basis, orders, d_tau, device=None):
-    check_mesh(mesh, "slp", basis)
+    check_mesh(mesh, "slp", basis, linear_ok=True)
     dev = require_device(device)
     dmesh = DeviceMesh.get(mesh, orders[0], dev)
     rows = np.asarray(cluster.indices, dtype=np.int64)
@@ -184,7 +186,7 @@ def _single_factor(side, cluster, rule, mesh, basis, orders, d_tau, device=None)
     desc = to_dev(np.array([[0, len(rows), 0, 0, 0]], dtype=np.int64), dev)
     dtau = to_dev(np.array([d_tau]), dev)
     out, _ = green_factors_device(dmesh, side, K, to_dev(rows, dev), desc, dtau, z, sq, nz,
-                                  len(rows), dev)
+                                  len(rows), dev, basis=basis)
     return out.cpu().numpy().reshape(len(rows), 2 * K)
 
 

@@ -51,8 +51,38 @@ __global__ void k_green_box_rules(int m, const double* __restrict__ g01,
     }
 }
 
+// moments of one triangle at box point (z, n): sum_p wgt_p g / h, with
+// wgt_p = gram * w_p (constant basis) or (b_p[a] * (gram * w_p)) (linear
+// basis, the hat function of corner a), in the reference's order
+template <bool LIN>
+__device__ __forceinline__ void tri_moments(const gc_geom& g, int64_t t, int a, double z0, double z1, double z2,
+                                            double n0, double n1, double n2, double& ig, double& ih, bool& touch) {
+    const int mq = (int)g.mq;
+    const double gram = g.gram[t];
+    const double* xq = g.xq + t * 3 * mq;
+    for (int p = 0; p < mq; ++p) {
+        const double d0 = __dsub_rn(xq[3 * p], z0);
+        const double d1 = __dsub_rn(xq[3 * p + 1], z1);
+        const double d2 = __dsub_rn(xq[3 * p + 2], z2);
+        const double r2 = __dadd_rn(__dadd_rn(__dmul_rn(d0, d0), __dmul_rn(d1, d1)), __dmul_rn(d2, d2));
+        const double rr = __dsqrt_rn(r2);
+        touch |= (rr <= 1e-12);
+        const double gk = __ddiv_rn(1.0, __dmul_rn(FOUR_PI, rr));
+        const double dot = __dadd_rn(__dadd_rn(__dmul_rn(d0, n0), __dmul_rn(d1, n1)), __dmul_rn(d2, n2));
+        const double hk = __ddiv_rn(dot, __dmul_rn(FOUR_PI, cube_rn(rr)));
+        double gw = __dmul_rn(gram, g.wq[p]);
+        if (LIN) gw = __dmul_rn(g.bq[3 * p + a], gw);
+        ig = __dadd_rn(ig, __dmul_rn(gw, gk));
+        ih = __dadd_rn(ih, __dmul_rn(gw, hk));
+    }
+}
+
 // One CTA per node; rule (K points) staged in shared memory; one thread per
-// (row, box point) entry of the R x 2K factor.
+// (row, box point) entry of the R x 2K factor.  LIN: rows are vertices and
+// each row sums its star triangles' hat-weighted moments (assembly.py:406-
+// 415: per corner a, then triangle order, each a full point sum added to
+// the running total).
+template <bool LIN>
 __global__ void __launch_bounds__(GREEN_THREADS) k_green_factor(
     gc_geom g, int side, int K, const int64_t* __restrict__ desc,
     const double* __restrict__ dtau, const double* __restrict__ zr, const double* __restrict__ sqr,
@@ -76,33 +106,25 @@ __global__ void __launch_bounds__(GREEN_THREADS) k_green_factor(
     }
     __syncthreads();
 
-    const int mq = (int)g.mq;
     const int64_t W = 2 * (int64_t)K;
     bool touch = false;
     for (int64_t e = threadIdx.x; e < R * K; e += blockDim.x) {
         const int64_t r = e / K;
         const int k = (int)(e % K);
-        const int64_t t = rows[rows_off + r];
-        const double gram = g.gram[t];
+        const int64_t dof = rows[rows_off + r];
         const double z0 = z[k][0], z1 = z[k][1], z2 = z[k][2];
         const double n0 = nn3[k][0], n1 = nn3[k][1], n2 = nn3[k][2];
         double ig = 0.0, ih = 0.0;
-        const double* xq = g.xq + t * 3 * mq;
-        for (int p = 0; p < mq; ++p) {
-            const double d0 = __dsub_rn(xq[3 * p], z0);
-            const double d1 = __dsub_rn(xq[3 * p + 1], z1);
-            const double d2 = __dsub_rn(xq[3 * p + 2], z2);
-            const double r2 = __dadd_rn(__dadd_rn(__dmul_rn(d0, d0), __dmul_rn(d1, d1)),
-                                        __dmul_rn(d2, d2));
-            const double rr = __dsqrt_rn(r2);
-            touch |= (rr <= 1e-12);
-            const double gk = __ddiv_rn(1.0, __dmul_rn(FOUR_PI, rr));
-            const double dot = __dadd_rn(__dadd_rn(__dmul_rn(d0, n0), __dmul_rn(d1, n1)),
-                                         __dmul_rn(d2, n2));
-            const double hk = __ddiv_rn(dot, __dmul_rn(FOUR_PI, cube_rn(rr)));
-            const double gw = __dmul_rn(gram, g.wq[p]);
-            ig = __dadd_rn(ig, __dmul_rn(gw, gk));
-            ih = __dadd_rn(ih, __dmul_rn(gw, hk));
+        if (LIN) {
+            for (int64_t u = g.vstar_ptr[dof]; u < g.vstar_ptr[dof + 1]; ++u) {
+                double vg = 0.0, vh = 0.0;
+                const int64_t ent = g.vstar_ent[u];
+                tri_moments<true>(g, ent >> 2, (int)(ent & 3), z0, z1, z2, n0, n1, n2, vg, vh, touch);
+                ig = __dadd_rn(ig, vg);
+                ih = __dadd_rn(ih, vh);
+            }
+        } else {
+            tri_moments<false>(g, dof, 0, z0, z1, z2, n0, n1, n2, ig, ih, touch);
         }
         double* row = out + out_off + r * W;
         if (side == 0) {
@@ -141,8 +163,17 @@ extern "C" int gc_green_factor(const gc_geom* gp, int side, int64_t K, int64_t n
     if (side < -1 || side > 1) { set_error(GC_ERR_CONFIG, "side must be 0 (row), 1 (col) or -1 (per node)"); return GC_ERR_CONFIG; }
     if (K < 1 || K > GREEN_MAX_K) { set_error(GC_ERR_CONFIG, "rule size K=%lld outside [1, %d]", (long long)K, GREEN_MAX_K); return GC_ERR_CONFIG; }
     if (nn <= 0) return GC_OK;
-    k_green_factor<<<(unsigned)nn, GREEN_THREADS, 0, (cudaStream_t)stream>>>(
-        *gp, side, (int)K, desc, dtau, z, sq, nz, rows, out, flags);
+    if (gp->basis == 1) {
+        if (!gp->vstar_ptr || !gp->vstar_ent || !gp->bq) {
+            set_error(GC_ERR_CONFIG, "linear basis needs gc_geom.vstar_ptr/vstar_ent/bq");
+            return GC_ERR_CONFIG;
+        }
+        k_green_factor<true><<<(unsigned)nn, GREEN_THREADS, 0, (cudaStream_t)stream>>>(
+            *gp, side, (int)K, desc, dtau, z, sq, nz, rows, out, flags);
+    } else {
+        k_green_factor<false><<<(unsigned)nn, GREEN_THREADS, 0, (cudaStream_t)stream>>>(
+            *gp, side, (int)K, desc, dtau, z, sq, nz, rows, out, flags);
+    }
     GC_CHECK_LAUNCH("k_green_factor");
     return GC_OK;
 }

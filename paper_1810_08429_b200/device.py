@@ -103,21 +103,34 @@ class DeviceMesh:
         self.wq_host = np.ascontiguousarray(wts, dtype=np.float64)
         # chart normal per triangle (|n| = gram), for the double layer
         self.normals = to_dev(np.ascontiguousarray(pack.normals[:, 0]), device)
-        self.geom = self._struct(0)
-        self.geom_dlp = self._struct(1)
+        # linear basis: vertex stars ordered by (corner, triangle) and the
+        # barycentric values of the regular rule's points
+        tris = mesh.triangles
+        t_of = np.repeat(np.arange(self.nt, dtype=np.int64), 3)
+        corner = np.tile(np.arange(3, dtype=np.int64), self.nt)
+        vert = tris.ravel().astype(np.int64)
+        order = np.lexsort((t_of, corner, vert))
+        self.vstar_ptr = to_dev(np.searchsorted(vert[order], np.arange(mesh.nv + 1)).astype(np.int64), device)
+        self.vstar_ent = to_dev((t_of[order] << 2) | corner[order], device)
+        self.bq = to_dev(np.stack([1.0 - pts[:, 0] - pts[:, 1], pts[:, 0], pts[:, 1]], 1), device)
+        self._geoms = {}
+        self.geom = self.geom_of("slp")
+        self.geom_dlp = self.geom_of("dlp")
 
-    def _struct(self, kernel):
-        return _native.GcGeom(ptr(self.corners), ptr(self.gram), ptr(self.tri_vid),
-                              ptr(self.xq), ptr(self.wq), self.nt, self.mq,
-                              self.wq_host.ctypes.data, ptr(self.normals), kernel)
-
-    def geom_of(self, kind):
-        """The gc_geom of the single-layer ("slp") or double-layer ("dlp") kernel."""
-        if kind == "slp":
-            return self.geom
-        if kind == "dlp":
-            return self.geom_dlp
-        raise ConfigError("unknown kernel kind %r" % (kind,))
+    def geom_of(self, kind, basis="constant"):
+        """The gc_geom of the single-layer ("slp") or double-layer ("dlp")
+        kernel, for the constant or the linear basis."""
+        if kind not in ("slp", "dlp"):
+            raise ConfigError("unknown kernel kind %r" % (kind,))
+        if basis not in ("constant", "linear"):
+            raise ConfigError("unknown basis %r" % (basis,))
+        key = (kind, basis)
+        if key not in self._geoms:
+            self._geoms[key] = _native.GcGeom(
+                ptr(self.corners), ptr(self.gram), ptr(self.tri_vid), ptr(self.xq), ptr(self.wq),
+                self.nt, self.mq, self.wq_host.ctypes.data, ptr(self.normals), int(kind == "dlp"),
+                ptr(self.vstar_ptr), ptr(self.vstar_ent), ptr(self.bq), int(basis == "linear"))
+        return self._geoms[key]
 
     @classmethod
     def get(cls, mesh, q_reg, device):

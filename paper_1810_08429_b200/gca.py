@@ -317,8 +317,9 @@ def build_cluster_bases(tree, mesh, basis, m, delta_factor, eps, sides, orders=(
     H2 matrix) built together: per tree height one ``gc_green_box_rules``,
     one ``gc_green_factor`` (side per node) and one ``gc_aca`` launch over
     the nodes of every basis, then one device->host read of ranks, pivots
-    and the touch flags.  ``sides`` is a list of (side, marks)."""
-    check_mesh(mesh, "slp", basis)
+    and the touch flags.  ``sides`` is a list of (side, marks).  Rows are
+    triangles (constant basis) or vertices (linear basis)."""
+    check_mesh(mesh, "slp", basis, linear_ok=True)
     if tree.index != 0:
         raise ConfigError("build_cluster_basis expects the root of a cluster tree")
     dev = require_device(device)
@@ -391,7 +392,7 @@ def build_cluster_bases(tree, mesh, basis, m, delta_factor, eps, sides, orders=(
             _native.call("gc_green_box_rules", m, ptr(d_g01), ptr(d_w01), nn, ptr(d_box),
                          ptr(z), ptr(sq), ptr(nz), stream)
         fac, flags = green_factors_device(dmesh, "mixed", K, d_rows, fdesc, d_diam, z, sq, nz,
-                                          int(R.sum()), dev, check_flags=False)
+                                          int(R.sum()), dev, check_flags=False, basis=basis)
         ta = time.perf_counter()
         t_factor += ta - tf
         V = torch.zeros(max(int(vcap.sum()), 1), dtype=torch.float64, device=dev)
@@ -555,7 +556,7 @@ def build_h2(btree, row_basis, col_basis, mesh, kind="slp", basis="constant",
     if disc != "galerkin":
         raise ConfigError("unknown discretization %r" % (disc,) if disc != "collocation"
                           else "collocation is out of scope on the device")
-    check_mesh(mesh, kind, basis)
+    check_mesh(mesh, kind, basis, linear_ok=True)
     dev = require_device(device)
     fb = btree.flat
     rf, cf = fb.row_tree, fb.col_tree
@@ -585,18 +586,32 @@ def build_h2(btree, row_basis, col_basis, mesh, kind="slp", basis="constant",
     coup = padded_empty(max(c_total, 1), dev)
     cdesc = np.stack([rstore.piv_off[cr], c_nr, cstore.piv_off[cc], c_nc, c_off], 1)
     keep = (c_nr > 0) & (c_nc > 0)
-    stats_c = device_block_assembly(dmesh, rules, queue, rstore.pivots, cstore.pivots,
-                                    cdesc[keep], coup, kind=kind)
-    t1 = time.perf_counter()
-    # near-field blocks: full clusters
     n_nr = rf.stop[nr_r] - rf.start[nr_r]
     n_nc = cf.stop[nc_r] - cf.start[nc_r]
     n_off = _grouped_offsets(nr_r, n_nr * n_nc)
     near = padded_empty(max(int((n_nr * n_nc).sum()), 1), dev)
     perm_r = to_dev(rf.perm, dev)
     perm_c = perm_r if cf is rf else to_dev(cf.perm, dev)
-    ndesc = np.stack([rf.start[nr_r], n_nr, cf.start[nc_r], n_nc, n_off], 1)
-    stats_n = device_block_assembly(dmesh, rules, queue, perm_r, perm_c, ndesc, near, kind=kind)
+    if basis == "linear":
+        # vertex DOFs: every block is the scatter of its triangle pairs'
+        # 3x3 integrals (linear.py)
+        from . import linear
+        lrules = linear.LinearRules.get(orders[0], orders[1], dev)
+        rp, cp = rstore.pivots_host, cstore.pivots_host
+        cblocks = [(rp[rstore.piv_off[a]:rstore.piv_off[a] + nr], cp[cstore.piv_off[b]:cstore.piv_off[b] + nc], o)
+                   for a, b, nr, nc, o in zip(cr[keep], cc[keep], c_nr[keep], c_nc[keep], c_off[keep])]
+        stats_c = linear.assemble_blocks(dmesh, kind, lrules, mesh, cblocks, coup, dev)
+        t1 = time.perf_counter()
+        nblocks = [(rf.perm[rf.start[a]:rf.stop[a]], cf.perm[cf.start[b]:cf.stop[b]], o)
+                   for a, b, o in zip(nr_r, nc_r, n_off)]
+        stats_n = linear.assemble_blocks(dmesh, kind, lrules, mesh, nblocks, near, dev)
+    else:
+        stats_c = device_block_assembly(dmesh, rules, queue, rstore.pivots, cstore.pivots,
+                                        cdesc[keep], coup, kind=kind)
+        t1 = time.perf_counter()
+        # near-field blocks: full clusters
+        ndesc = np.stack([rf.start[nr_r], n_nr, cf.start[nc_r], n_nc, n_off], 1)
+        stats_n = device_block_assembly(dmesh, rules, queue, perm_r, perm_c, ndesc, near, kind=kind)
     torch.cuda.synchronize(dev)
     t2 = time.perf_counter()
     d = DeviceH2(dev)

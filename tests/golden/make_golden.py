@@ -187,6 +187,55 @@ def lin_pair_tasks(mesh, n_disjoint, seed, kind):
     return g
 
 
+def lin_pipeline(mesh, eps, seed):
+    """The reference's GCA-H2 with the linear basis: vertex tree, bases
+    (pivot vertices), sampled blocks and matvecs."""
+    tree = C.build_cluster_tree(mesh, "linear", 16)
+    bt = C.build_block_tree(tree, eta=1.0)
+    rm, cm = GC.coupling_marks(bt)
+    rb = GC.build_cluster_basis(tree, mesh, "linear", 3, 0.5, eps, "row", (3, 5), rm)
+    cb = GC.build_cluster_basis(tree, mesh, "linear", 3, 0.5, eps, "col", (3, 5), cm)
+    hm = GC.build_h2(bt, rb, cb, mesh, "slp", "linear", "galerkin", (3, 5))
+    nodes = tree.nodes()
+    leaves = bt.leaves()
+    out = dict(perm=tree.perm.astype(np.int32),
+               start=np.array([n.start for n in nodes], np.int32),
+               stop=np.array([n.stop for n in nodes], np.int32),
+               lower=np.array([n.box.lower for n in nodes]),
+               upper=np.array([n.box.upper for n in nodes]),
+               leaf_row=np.array([l.row.index for l in leaves], np.int32),
+               leaf_col=np.array([l.col.index for l in leaves], np.int32),
+               leaf_adm=np.array([l.state == "admissible" for l in leaves]))
+    for side, basis in (("row", rb), ("col", cb)):
+        bns = basis.nodes()
+        out[side + "_node"] = np.array([b.cluster.index for b in bns], np.int32)
+        out[side + "_rank"] = np.array([b.rank for b in bns], np.int32)
+        out[side + "_piv"] = np.concatenate([b.pivots for b in bns]).astype(np.int32)
+    # Green factors of a few leaves (row side) for the linear basis
+    rng = np.random.default_rng(seed)
+    fl = [n for n in nodes if n.is_leaf()]
+    pick = rng.choice(len(fl), 4, replace=False)
+    facs = []
+    for i in pick:
+        node = fl[i]
+        rule = Q.green_box_rule(node.box, 0.5 * node.box.diameter(), 3)
+        facs.append(A.green_row_factor(node, rule, mesh, "linear", (3, 5)).ravel())
+    out["factor_nodes"] = np.array([fl[i].index for i in pick], np.int32)
+    out["factors"] = np.concatenate(facs)
+    x = rng.standard_normal((3, mesh.nv))
+    out["x"] = x
+    out["mvm"] = np.array([H.mvm(hm, v) for v in x])
+    out["storage_keys"] = np.array(list(H.storage_report(hm).keys()))
+    out["storage_vals"] = np.array(list(H.storage_report(hm).values()))
+    return out
+
+
+def main_linear_h2():
+    np.savez_compressed(os.path.join(OUT, "h2_lin_sphere3_eps1e-4.npz"),
+                        **lin_pipeline(G.build_sphere_mesh(3), 1e-4, 43))
+    np.savez_compressed(os.path.join(OUT, "h2_lin_cube3_eps1e-6.npz"), **lin_pipeline(cube(3), 1e-6, 44))
+
+
 def main_linear():
     s3 = G.build_sphere_mesh(3)
     for kind in ("slp", "dlp"):
@@ -240,5 +289,7 @@ if __name__ == "__main__":
         main_dlp()
     elif "--linear" in sys.argv:
         main_linear()
+    elif "--linear-h2" in sys.argv:
+        main_linear_h2()
     else:
         main()

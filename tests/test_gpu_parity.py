@@ -530,3 +530,40 @@ def test_linear_dense_blocks(sphere2):
     d2 = assembly.assemble_galerkin_block("slp", sphere2, "linear", dofs, dofs).values
     assert np.array_equal(d, d2)
     assert rel(sub, d[np.ix_(g["sub_rows"], g["sub_cols"])]) < 1e-13
+
+
+@pytest.mark.parametrize("name,mesh_name,eps", [("h2_lin_sphere3_eps1e-4.npz", "x_sphere3", 1e-4),
+                                                ("h2_lin_cube3_eps1e-6.npz", "x_cube3", 1e-6)])
+def test_linear_h2_pipeline_vs_reference(name, mesh_name, eps):
+    """GCA-H2 with the linear basis (vertex DOFs) against the reference:
+    vertex tree, Green factors of sampled leaves, ranks and pivot sets per
+    basis node, storage report and three matvecs."""
+    g = golden(name)
+    mesh = mesh_for(mesh_name)
+    cfg = cli.default_config(eps=eps, basis="linear")
+    hm, tree, bt = cli.build_h2_operator(mesh, cfg)
+    assert np.array_equal(tree.perm, g["perm"])
+    # Green row factors of sampled leaves (rows = vertices)
+    off = 0
+    for i in g["factor_nodes"]:
+        node = tree.flat.node(int(i))
+        rule = Q.green_box_rule(node.box, 0.5 * node.box.diameter(), 3)
+        a = assembly.green_row_factor(node, rule, mesh, "linear")
+        ref = g["factors"][off:off + a.size].reshape(a.shape)
+        off += a.size
+        assert np.max(np.abs(a - ref)) <= 1e-14 * np.max(np.abs(ref))
+    for side, basis in (("row", hm.row_basis), ("col", hm.col_basis)):
+        nodes = list(basis.nodes())
+        assert [b.cluster.index for b in nodes] == g[side + "_node"].tolist()
+        assert [b.rank for b in nodes] == g[side + "_rank"].tolist()
+        got = np.concatenate([b.pivots for b in nodes])
+        ref = g[side + "_piv"]
+        o = 0
+        for b in nodes:
+            assert set(got[o:o + b.rank]) == set(ref[o:o + b.rank])
+            o += b.rank
+    rep = h2.storage_report(hm)
+    assert {k: rep[k] for k in g["storage_keys"]} == dict(zip(g["storage_keys"].tolist(),
+                                                              g["storage_vals"].tolist()))
+    for x, y in zip(g["x"], g["mvm"]):
+        assert np.linalg.norm(h2.mvm(hm, x) - y) <= 1e-12 * np.linalg.norm(y)

@@ -146,3 +146,21 @@ def test_config_validation():
                 dict(disc="collocation")):
         with pytest.raises(ConfigError):
             cli.default_config(**bad)
+
+
+@pytest.mark.parametrize("name,mesh_name", [("h2_lin_sphere3_eps1e-4.npz", "x_sphere3"),
+                                            ("h2_lin_cube3_eps1e-6.npz", "x_cube3")])
+def test_linear_vertex_tree_and_block_tree_bitwise(name, mesh_name):
+    """The linear basis clusters vertices (support boxes from the vertex
+    stars, clustering.py:107-128): tree and block leaves bit-exact."""
+    g = golden(name)
+    mesh = mesh_for(mesh_name)
+    tree = clustering.build_cluster_tree(mesh, "linear", leaf_size=16)
+    f = tree.flat
+    assert np.array_equal(tree.perm, g["perm"])
+    assert np.array_equal(f.start, g["start"]) and np.array_equal(f.stop, g["stop"])
+    assert np.array_equal(f.lower, g["lower"]) and np.array_equal(f.upper, g["upper"])
+    bt = clustering.build_block_tree(tree, eta=1.0)
+    lr, lc = bt.flat.leaves()
+    assert np.array_equal(lr, g["leaf_row"]) and np.array_equal(lc, g["leaf_col"])
+    assert np.array_equal(bt.flat.state[bt.flat.leaf_ids] == 0, g["leaf_adm"])

@@ -71,7 +71,10 @@ typedef struct gc_geom {
     const int64_t* vstar_ptr;
     const int64_t* vstar_ent;
     const double* bq;
+    /* 0 = piecewise constant, 1 = piecewise linear, 2 = collocation rows
+     * (point evaluations at the vertices, Green factors only) */
     int64_t basis;
+    const double* verts;   /* [dev] nv x 3 vertex coordinates (collocation) */
 } gc_geom;
 
 /* Singular pair rules (quadrature.sauter_rule, quadrature.py:211-284) in
@@ -278,6 +281,16 @@ int gc_lin_singular(const gc_geom* g, const gc_rules* r, gc_queue* q, double* U,
 int gc_lin_gather(int64_t nb, const int64_t* desc, const int64_t* rptr, const int64_t* rlist,
                   const int64_t* cptr, const int64_t* clist, const double* U, const int32_t* pp,
                   double* out, void* stream);
+
+/* Collocation (assembly.py:219-276, 340-362): tasks (n,2) = (vertex v,
+ * triangle s); each the 3 single integrals of k(x_v, y) phi_c(y) over s
+ * (regular rule: the gc_geom chart points; v a corner of s: the collapsed
+ * Gauss rule sing_w / sing_p (ms points) with v rotated to corner 0) in
+ * the rotated column order -> U[9i .. 9i+2], pp[i] = rotation << 8, the
+ * layout gc_lin_gather reads. */
+int gc_col_pairs(const gc_geom* g, const double* verts, const double* reg_w, const double* reg_b,
+                 int64_t ms, const double* sing_w, const double* sing_p, int64_t n,
+                 const int64_t* tasks, double* U, int32_t* pp, void* stream);
 
 /* Device-side Krylov support (consumers of the matvec, h2.py:190-253;
  * SURVEY 8f rank 3).  Deterministic dot product: fixed grid of

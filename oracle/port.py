@@ -257,6 +257,59 @@ def block_linear(nodes, gram, triangles, rows, cols, q=(3, 5), kind="slp", norma
     return mat
 
 
+def collocation_values(nodes, gram, vertices, case, rows, cols, py, q_reg=3, q_sing=5, kind="slp",
+                       normals=None):
+    """assembly.py:231-276: single integrals of g(x_v, y) phi_c(y) over the
+    triangle, (B, 1, 3) in the rotated column order."""
+    pts, wts = triangle_rule(q_reg if case == 0 else q_sing)
+    n6 = shape6(pts)
+    wb = wts[None, :] * _bary(pts).T
+    out = np.empty((len(rows), 1, 3))
+    Y = _interp(n6, nodes[cols[:, None], ORDER6[py]])
+    D = vertices[rows][:, None, :] - Y
+    r2 = D[..., 0] ** 2 + D[..., 1] ** 2 + D[..., 2] ** 2
+    r = np.sqrt(r2)
+    if kind == "dlp":
+        nyv = _interp(n6, normals[cols[:, None], ORDER6[py]])
+        dot = D[..., 0] * nyv[..., 0] + D[..., 1] * nyv[..., 1] + D[..., 2] * nyv[..., 2]
+        kg = dot / (FOUR_PI * r2 * r)
+    else:
+        kg = gram[cols][:, None] / (FOUR_PI * r)
+    for c in range(3):
+        out[:, 0, c] = np.sum(kg * wb[c][None, :], axis=1)
+    return out
+
+
+def collocation_classify(triangles, rows, cols):
+    hit = triangles[cols] == rows[:, None]
+    return hit.any(axis=1).astype(np.int64), np.argmax(hit, axis=1)
+
+
+def block_collocation(nodes, gram, vertices, triangles, rows, cols, q=(3, 5), kind="slp", normals=None):
+    """Collocation block (assembly.py:340-362) with the executor's scatter
+    (row width 1, column slots permuted by the rotation)."""
+    nv = int(triangles.max()) + 1
+    tc = triangle_table(cols, triangles, nv)
+    rows = np.asarray(rows)
+    nr, nt_ = len(rows), len(tc)
+    R, C = np.repeat(rows, nt_), np.tile(tc[:, 0], nr)
+    rs = np.repeat(np.arange(nr), nt_)
+    cs = np.tile(tc[:, 1:] - 1, (nr, 1))
+    case, py = collocation_classify(triangles, R, C)
+    cs = np.take_along_axis(cs, PERMS3[py], axis=1)
+    vals = np.empty((len(R), 1, 3))
+    for k in (0, 1):
+        m = case == k
+        if m.any():
+            vals[m] = collocation_values(nodes, gram, vertices, k, R[m], C[m], py[m], *q, kind=kind,
+                                         normals=normals)
+    mat = np.zeros((nr, len(cols)))
+    for b in range(3):
+        ok = cs[:, b] >= 0
+        np.add.at(mat, (rs[ok], cs[ok, b]), vals[ok, 0, b])
+    return mat
+
+
 def block(nodes, gram, triangles, rows, cols, q=(3, 5), kind="slp", normals=None):
     """Dense block G[rows, cols] (assembly.py:330-337)."""
     rows = np.asarray(rows)

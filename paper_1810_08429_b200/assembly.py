@@ -148,6 +148,57 @@ def assemble_galerkin_block(kind, mesh, basis, rows, cols, orders=(3, 5), capaci
     return DenseBlock(rows, cols, out.cpu().numpy().reshape(nc, nr).T.copy())
 
 
+def collocation_classify(mesh):
+    """``assembly.py:219-228``: rows are points (vertices), columns
+    triangles; case 1 iff the point is a corner, py the rotation putting
+    it first."""
+    from . import linear
+    return linear.collocation_classify(mesh)
+
+
+def collocation_evaluator(kind, mesh, q_reg, q_sing, device=None):
+    """Device single-integral evaluator (``assembly.py:231-276``): values
+    (B, 1, 3) in the rotated column order."""
+    if kind not in ("slp", "dlp"):
+        raise ConfigError("unknown kernel kind %r" % (kind,))
+    check_mesh(mesh, kind, "linear", linear_ok=True)
+    from . import linear
+    dev = require_device(device)
+    dmesh = DeviceMesh.get(mesh, q_reg, dev)
+    rules = linear.CollocationRules(q_reg, q_sing)
+
+    def evaluate(case, rows, cols, px, py):
+        if int(case) not in (0, 1):
+            raise ConfigError("unknown collocation case %r" % (case,))
+        return linear.collocation_values(dmesh, kind, rules, rows, cols, dev)
+
+    return evaluate
+
+
+def assemble_collocation_block(kind, mesh, basis, rows, cols, orders=(3, 5), capacity=None,
+                               threads=None, device=None):
+    """Collocation block g(x_i, .) phi_j (``assembly.py:352-362``): rows are
+    surface points (vertex ids), columns linear-basis DOFs."""
+    if basis != "linear":
+        raise ConfigError("collocation rows pair with the linear basis")
+    if kind not in ("slp", "dlp"):
+        raise ConfigError("unknown kernel kind %r" % (kind,))
+    check_mesh(mesh, kind, basis, linear_ok=True)
+    rows = np.asarray(rows, dtype=np.int64)
+    cols = np.asarray(cols, dtype=np.int64)
+    if len(np.unique(cols)) != len(cols):
+        raise ConfigError("duplicate indices")
+    nr, nc = len(rows), len(cols)
+    if nr == 0 or nc == 0:
+        return DenseBlock(rows, cols, np.zeros((nr, nc)))
+    from . import linear
+    dev = require_device(device)
+    dmesh = DeviceMesh.get(mesh, orders[0], dev)
+    out = empty(nr * nc, dev)
+    linear.collocation_blocks(dmesh, kind, linear.CollocationRules(*orders), mesh, [(rows, cols, 0)], out, dev)
+    return DenseBlock(rows, cols, out.cpu().numpy().reshape(nc, nr).T.copy())
+
+
 # --------------------------------------------------------------------------
 # Green factors
 
@@ -193,8 +244,7 @@ def _single_factor(side, cluster, rule, mesh, basis, orders, d_tau, device=None)
 def green_row_factor(cluster, rule, mesh, basis, orders=(3, 5)):
     """Row factor A = [sqrt(w) g-moments, -d_tau sqrt(w) dg/dn-moments]
     (``assembly.py:420-439``); ``cluster`` needs ``.indices`` and ``.box``."""
-    if basis == "collocation":
-        raise ConfigError("collocation rows are out of scope on the device")
+
     return _single_factor("row", cluster, rule, mesh, basis, orders, cluster.box.diameter())
 
 

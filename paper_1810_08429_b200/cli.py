@@ -64,8 +64,10 @@ def build_h2_operator(mesh, cfg, kind="slp", capacity=None, threads=None, device
     orders = (cfg.q_reg, cfg.q_sing)
     rmarks, cmarks = gca.coupling_marks(btree)
     # row and column bases in shared per-level launches (gca.build_cluster_bases)
+    row_kind = "collocation" if cfg.disc == "collocation" else cfg.basis      # cli.py:167
     rb, cb = gca.build_cluster_bases(tree, mesh, cfg.basis, cfg.m, cfg.delta_factor, cfg.eps,
-                                     [("row", rmarks), ("col", cmarks)], orders, device)
+                                     [("row", rmarks, row_kind), ("col", cmarks, cfg.basis)], orders,
+                                     device)
     t3 = t4 = time.perf_counter()
     hm = gca.build_h2(btree, rb, cb, mesh, kind=kind, basis=cfg.basis, disc=cfg.disc,
                       orders=orders, device=device)

@@ -82,7 +82,7 @@ __device__ __forceinline__ void tri_moments(const gc_geom& g, int64_t t, int a, 
 // each row sums its star triangles' hat-weighted moments (assembly.py:406-
 // 415: per corner a, then triangle order, each a full point sum added to
 // the running total).
-template <bool LIN>
+template <bool LIN, bool POINT>
 __global__ void __launch_bounds__(GREEN_THREADS) k_green_factor(
     gc_geom g, int side, int K, const int64_t* __restrict__ desc,
     const double* __restrict__ dtau, const double* __restrict__ zr, const double* __restrict__ sqr,
@@ -115,7 +115,17 @@ __global__ void __launch_bounds__(GREEN_THREADS) k_green_factor(
         const double z0 = z[k][0], z1 = z[k][1], z2 = z[k][2];
         const double n0 = nn3[k][0], n1 = nn3[k][1], n2 = nn3[k][2];
         double ig = 0.0, ih = 0.0;
-        if (LIN) {
+        if (POINT) {
+            // collocation rows: point evaluations at the vertex (assembly.py:427-433)
+            const double d0 = __dsub_rn(g.verts[3 * dof], z0);
+            const double d1 = __dsub_rn(g.verts[3 * dof + 1], z1);
+            const double d2 = __dsub_rn(g.verts[3 * dof + 2], z2);
+            const double rr = __dsqrt_rn(__dadd_rn(__dadd_rn(__dmul_rn(d0, d0), __dmul_rn(d1, d1)), __dmul_rn(d2, d2)));
+            touch |= (rr <= 1e-12);
+            ig = __ddiv_rn(1.0, __dmul_rn(FOUR_PI, rr));
+            const double dot = __dadd_rn(__dadd_rn(__dmul_rn(d0, n0), __dmul_rn(d1, n1)), __dmul_rn(d2, n2));
+            ih = __ddiv_rn(dot, __dmul_rn(FOUR_PI, cube_rn(rr)));
+        } else if (LIN) {
             for (int64_t u = g.vstar_ptr[dof]; u < g.vstar_ptr[dof + 1]; ++u) {
                 double vg = 0.0, vh = 0.0;
                 const int64_t ent = g.vstar_ent[u];
@@ -168,10 +178,14 @@ extern "C" int gc_green_factor(const gc_geom* gp, int side, int64_t K, int64_t n
             set_error(GC_ERR_CONFIG, "linear basis needs gc_geom.vstar_ptr/vstar_ent/bq");
             return GC_ERR_CONFIG;
         }
-        k_green_factor<true><<<(unsigned)nn, GREEN_THREADS, 0, (cudaStream_t)stream>>>(
+        k_green_factor<true, false><<<(unsigned)nn, GREEN_THREADS, 0, (cudaStream_t)stream>>>(
+            *gp, side, (int)K, desc, dtau, z, sq, nz, rows, out, flags);
+    } else if (gp->basis == 2) {
+        if (!gp->verts) { set_error(GC_ERR_CONFIG, "collocation rows need gc_geom.verts"); return GC_ERR_CONFIG; }
+        k_green_factor<false, true><<<(unsigned)nn, GREEN_THREADS, 0, (cudaStream_t)stream>>>(
             *gp, side, (int)K, desc, dtau, z, sq, nz, rows, out, flags);
     } else {
-        k_green_factor<false><<<(unsigned)nn, GREEN_THREADS, 0, (cudaStream_t)stream>>>(
+        k_green_factor<false, false><<<(unsigned)nn, GREEN_THREADS, 0, (cudaStream_t)stream>>>(
             *gp, side, (int)K, desc, dtau, z, sq, nz, rows, out, flags);
     }
     GC_CHECK_LAUNCH("k_green_factor");

@@ -289,3 +289,111 @@ extern "C" int gc_lin_gather(int64_t nb, const int64_t* desc, const int64_t* rpt
     GC_CHECK_LAUNCH("k_lin_gather");
     return GC_OK;
 }
+
+// ---------------------------------------------------------------------------
+// Collocation (assembly.py:219-276, 340-362): rows are surface points (mesh
+// vertices), columns the linear basis.  A task (v, s) is the single
+// integral of k(x_v, y) phi_c(y) over triangle s: the regular rule (the
+// q_reg chart points of s) when v is not a corner of s, else the collapsed
+// Gauss rule with v rotated to corner 0 (duffy_rule(0, q_sing)), where
+// y - x_v = y1 E1 + y2 E2 carries no cancellation.  Values in the rotated
+// (canonical) column order: U[9 i + c], pp[i] = rotation << 8.
+struct ColRule {
+    double w[64];        // regular rule weights
+    double b[64][3];     // regular rule barycentrics
+    double sw[64];       // singular (collapsed) rule weights
+    double sp[64][2];    // singular rule points
+    int ms;              // singular rule size
+};
+
+template <bool DLP>
+__global__ void __launch_bounds__(128) k_col_pairs(gc_geom g, ColRule cr, const double* __restrict__ verts,
+                                                   const int64_t* __restrict__ tasks, int64_t n,
+                                                   double* __restrict__ U, int32_t* __restrict__ pp) {
+    const int M = (int)g.mq;
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+        const int64_t v = __ldg(tasks + 2 * i), s = __ldg(tasks + 2 * i + 1);
+        int rot = -1;
+#pragma unroll
+        for (int k = 0; k < 3; ++k)
+            if (rot < 0 && __ldg(g.tri_vid + 3 * s + k) == v) rot = k;
+        const double x0 = verts[3 * v], x1 = verts[3 * v + 1], x2 = verts[3 * v + 2];
+        double n0 = 0.0, n1 = 0.0, n2 = 0.0;
+        if (DLP) {
+            n0 = __ldg(g.normals + 3 * s);
+            n1 = __ldg(g.normals + 3 * s + 1);
+            n2 = __ldg(g.normals + 3 * s + 2);
+        }
+        double acc[3] = {0.0, 0.0, 0.0};
+        if (rot < 0) {
+            const double* yq = g.xq + s * 3 * M;
+            for (int m = 0; m < M; ++m) {
+                const double k = lin_kern<DLP>(x0 - __ldg(yq + 3 * m), x1 - __ldg(yq + 3 * m + 1),
+                                               x2 - __ldg(yq + 3 * m + 2), n0, n1, n2);
+                const double wk = cr.w[m] * k;
+#pragma unroll
+                for (int c = 0; c < 3; ++c) acc[c] = fma(wk, cr.b[m][c], acc[c]);
+            }
+            rot = 0;
+        } else {
+            // rotation rot puts corner rot first: PERMS3[rot] = (rot, rot+1, rot+2)
+            const double* cs = g.corners + 9 * s;
+            const int q0 = kPerms3[rot][0], q1 = kPerms3[rot][1], q2 = kPerms3[rot][2];
+            double E1[3], E2[3];
+#pragma unroll
+            for (int c = 0; c < 3; ++c) {
+                E1[c] = cs[3 * q1 + c] - cs[3 * q0 + c];
+                E2[c] = cs[3 * q2 + c] - cs[3 * q0 + c];
+            }
+            for (int m = 0; m < cr.ms; ++m) {
+                const double y1 = cr.sp[m][0], y2 = cr.sp[m][1];
+                // x_v - y = -(y1 E1 + y2 E2)
+                const double d0 = -fma(y1, E1[0], y2 * E2[0]);
+                const double d1 = -fma(y1, E1[1], y2 * E2[1]);
+                const double d2 = -fma(y1, E1[2], y2 * E2[2]);
+                const double wk = cr.sw[m] * lin_kern<DLP>(d0, d1, d2, n0, n1, n2);
+                const double b[3] = {1.0 - y1 - y2, y1, y2};
+#pragma unroll
+                for (int c = 0; c < 3; ++c) acc[c] = fma(wk, b[c], acc[c]);
+            }
+        }
+        const double sc = DLP ? INV_FOUR_PI : __ldg(g.gram + s) * INV_FOUR_PI;
+        pp[i] = rot << 8;
+#pragma unroll
+        for (int c = 0; c < 3; ++c) U[9 * i + c] = sc * acc[c];
+    }
+}
+
+extern "C" int gc_col_pairs(const gc_geom* gp, const double* verts, const double* reg_w, const double* reg_b,
+                            int64_t ms, const double* sing_w, const double* sing_p, int64_t n,
+                            const int64_t* tasks, double* U, int32_t* pp, void* stream) {
+    if (!gp || !verts || !reg_w || !reg_b || !sing_w || !sing_p) {
+        set_error(GC_ERR_CONFIG, "gc_col_pairs: null argument");
+        return GC_ERR_CONFIG;
+    }
+    if (n <= 0) return GC_OK;
+    const gc_geom g = *gp;
+    if (g.kernel && !g.normals) { set_error(GC_ERR_CONFIG, "double layer needs gc_geom.normals"); return GC_ERR_CONFIG; }
+    if (g.mq < 1 || g.mq > 64 || ms < 1 || ms > 64) {
+        set_error(GC_ERR_CONFIG, "gc_col_pairs: rules of 1..64 points (q <= 8)");
+        return GC_ERR_CONFIG;
+    }
+    ColRule cr;
+    for (int k = 0; k < 64; ++k) {
+        cr.w[k] = k < g.mq ? reg_w[k] : 0.0;
+        for (int c = 0; c < 3; ++c) cr.b[k][c] = k < g.mq ? reg_b[3 * k + c] : 0.0;
+        cr.sw[k] = k < ms ? sing_w[k] : 0.0;
+        cr.sp[k][0] = k < ms ? sing_p[2 * k] : 0.0;
+        cr.sp[k][1] = k < ms ? sing_p[2 * k + 1] : 0.0;
+    }
+    cr.ms = (int)ms;
+    cudaStream_t st = (cudaStream_t)stream;
+    int64_t grid = (n + 127) / 128;
+    if (grid > 148 * 32) grid = 148 * 32;
+    if (g.kernel)
+        k_col_pairs<true><<<(unsigned)grid, 128, 0, st>>>(g, cr, verts, tasks, n, U, pp);
+    else
+        k_col_pairs<false><<<(unsigned)grid, 128, 0, st>>>(g, cr, verts, tasks, n, U, pp);
+    GC_CHECK_LAUNCH("k_col_pairs");
+    return GC_OK;
+}

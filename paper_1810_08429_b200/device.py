@@ -113,6 +113,7 @@ class DeviceMesh:
         self.vstar_ptr = to_dev(np.searchsorted(vert[order], np.arange(mesh.nv + 1)).astype(np.int64), device)
         self.vstar_ent = to_dev((t_of[order] << 2) | corner[order], device)
         self.bq = to_dev(np.stack([1.0 - pts[:, 0] - pts[:, 1], pts[:, 0], pts[:, 1]], 1), device)
+        self.verts = to_dev(np.ascontiguousarray(mesh.vertices, dtype=np.float64), device)
         self._geoms = {}
         self.geom = self.geom_of("slp")
         self.geom_dlp = self.geom_of("dlp")
@@ -122,14 +123,15 @@ class DeviceMesh:
         kernel, for the constant or the linear basis."""
         if kind not in ("slp", "dlp"):
             raise ConfigError("unknown kernel kind %r" % (kind,))
-        if basis not in ("constant", "linear"):
+        codes = {"constant": 0, "linear": 1, "collocation": 2}
+        if basis not in codes:
             raise ConfigError("unknown basis %r" % (basis,))
         key = (kind, basis)
         if key not in self._geoms:
             self._geoms[key] = _native.GcGeom(
                 ptr(self.corners), ptr(self.gram), ptr(self.tri_vid), ptr(self.xq), ptr(self.wq),
                 self.nt, self.mq, self.wq_host.ctypes.data, ptr(self.normals), int(kind == "dlp"),
-                ptr(self.vstar_ptr), ptr(self.vstar_ent), ptr(self.bq), int(basis == "linear"))
+                ptr(self.vstar_ptr), ptr(self.vstar_ent), ptr(self.bq), codes[basis], ptr(self.verts))
         return self._geoms[key]
 
     @classmethod
@@ -217,12 +219,11 @@ class SingularQueue:
 def check_mesh(mesh, kind="slp", basis="constant", linear_ok=False):
     """Validate (kernel, basis, geometry) for a device path; ``linear_ok``
     marks the paths that implement the linear basis."""
-    if basis == "linear" and not linear_ok:
-        raise ConfigError("the linear basis is implemented for pair evaluation and dense "
-                          "blocks; this path supports the constant basis")
+    if basis in ("linear", "collocation") and not linear_ok:
+        raise ConfigError("this path supports the constant basis only")
     if kind not in ("slp", "dlp"):
         raise ConfigError("unknown kernel kind %r" % (kind,))
-    if basis not in ("constant", "linear"):
+    if basis not in ("constant", "linear", "collocation"):
         raise ConfigError("unknown basis %r" % (basis,))
     if getattr(mesh, "midpoints", None) is not None:
         raise ConfigError("curved charts are out of scope")

@@ -287,9 +287,10 @@ def build_cluster_basis(tree, mesh, basis, m, delta_factor=0.5, eps=1e-4, side="
 class _Side:
     """Per-basis state while several bases are built in shared launches."""
 
-    def __init__(self, tree, side, marks, row_range, W, dev):
+    def __init__(self, tree, side, marks, row_range, W, dev, basis="constant"):
         flat = tree.flat
         self.side = side
+        self.basis = basis
         self.store = DeviceBasis(tree, side, dev)
         mat, roots = _materialize(flat, marks)
         if row_range is not None:
@@ -317,9 +318,12 @@ def build_cluster_bases(tree, mesh, basis, m, delta_factor, eps, sides, orders=(
     H2 matrix) built together: per tree height one ``gc_green_box_rules``,
     one ``gc_green_factor`` (side per node) and one ``gc_aca`` launch over
     the nodes of every basis, then one device->host read of ranks, pivots
-    and the touch flags.  ``sides`` is a list of (side, marks).  Rows are
-    triangles (constant basis) or vertices (linear basis)."""
-    check_mesh(mesh, "slp", basis, linear_ok=True)
+    and the touch flags.  ``sides`` is a list of (side, marks) or (side,
+    marks, basis) - collocation rows pair a "collocation" row side with a
+    "linear" column side.  Rows are triangles (constant basis) or vertices
+    (linear basis, collocation points)."""
+    for sd in sides:
+        check_mesh(mesh, "slp", sd[2] if len(sd) > 2 else basis, linear_ok=True)
     if tree.index != 0:
         raise ConfigError("build_cluster_basis expects the root of a cluster tree")
     dev = require_device(device)
@@ -332,7 +336,7 @@ def build_cluster_bases(tree, mesh, basis, m, delta_factor, eps, sides, orders=(
     d_g01, d_w01 = to_dev(g01, dev), to_dev(w01, dev)
     size = flat.stop - flat.start
     perm = flat.perm
-    S = [_Side(tree, side, marks, row_range, W, dev) for side, marks in sides]
+    S = [_Side(tree, sd[0], sd[1], row_range, W, dev, sd[2] if len(sd) > 2 else basis) for sd in sides]
     heights = np.unique(np.concatenate([flat.height[s.mat] for s in S])) if S else []
     t_factor = t_aca = 0.0
     stream = stream_handle()
@@ -391,8 +395,26 @@ def build_cluster_bases(tree, mesh, basis, m, delta_factor, eps, sides, orders=(
         with torch.cuda.device(dev):
             _native.call("gc_green_box_rules", m, ptr(d_g01), ptr(d_w01), nn, ptr(d_box),
                          ptr(z), ptr(sq), ptr(nz), stream)
-        fac, flags = green_factors_device(dmesh, "mixed", K, d_rows, fdesc, d_diam, z, sq, nz,
-                                          int(R.sum()), dev, check_flags=False, basis=basis)
+        bases = sorted({S[p[0]].basis for p in parts})
+        if len(bases) == 1:
+            fac, flags = green_factors_device(dmesh, "mixed", K, d_rows, fdesc, d_diam, z, sq, nz,
+                                              int(R.sum()), dev, check_flags=False, basis=bases[0])
+        else:
+            # one launch per row kind (e.g. collocation rows, linear columns)
+            # into the same factor buffer
+            node_basis = np.concatenate([np.full(len(p[1]), S[p[0]].basis, dtype=object) for p in parts])
+            fac = empty(int(R.sum()) * 2 * K, dev)
+            flags = torch.zeros(1, dtype=torch.int32, device=dev)
+            fd = fdesc.view(nn, 5)
+            for b in bases:
+                sel = to_dev(np.flatnonzero(node_basis == b), dev)
+                # keep the gathered tables referenced until the launch is queued
+                # (a temporary freed inside the argument list would be reused)
+                sub_desc, sub_diam = fd[sel].contiguous(), d_diam[sel].contiguous()
+                with torch.cuda.device(dev):
+                    _native.call("gc_green_factor", dmesh.geom_of("slp", b), -1, K, len(sel),
+                                 ptr(sub_desc), ptr(sub_diam), ptr(z), ptr(sq), ptr(nz), ptr(d_rows),
+                                 ptr(fac), ptr(flags), stream)
         ta = time.perf_counter()
         t_factor += ta - tf
         V = torch.zeros(max(int(vcap.sum()), 1), dtype=torch.float64, device=dev)
@@ -553,9 +575,10 @@ def build_h2(btree, row_basis, col_basis, mesh, kind="slp", basis="constant",
     inadmissible leaves dense blocks.  ``row_range=(lo, hi)`` restricts the
     assembly to block rows whose row cluster lies in tree positions
     [lo, hi) (block-row sharding across GPUs, SURVEY.md §8 e)."""
-    if disc != "galerkin":
-        raise ConfigError("unknown discretization %r" % (disc,) if disc != "collocation"
-                          else "collocation is out of scope on the device")
+    if disc not in ("galerkin", "collocation"):
+        raise ConfigError("unknown discretization %r" % (disc,))
+    if disc == "collocation" and basis != "linear":
+        raise ConfigError("collocation rows pair with the linear basis")
     check_mesh(mesh, kind, basis, linear_ok=True)
     dev = require_device(device)
     fb = btree.flat
@@ -594,17 +617,24 @@ def build_h2(btree, row_basis, col_basis, mesh, kind="slp", basis="constant",
     perm_c = perm_r if cf is rf else to_dev(cf.perm, dev)
     if basis == "linear":
         # vertex DOFs: every block is the scatter of its triangle pairs'
-        # 3x3 integrals (linear.py)
+        # 3x3 integrals (linear.py); collocation rows are point evaluations
         from . import linear
-        lrules = linear.LinearRules.get(orders[0], orders[1], dev)
         rp, cp = rstore.pivots_host, cstore.pivots_host
         cblocks = [(rp[rstore.piv_off[a]:rstore.piv_off[a] + nr], cp[cstore.piv_off[b]:cstore.piv_off[b] + nc], o)
                    for a, b, nr, nc, o in zip(cr[keep], cc[keep], c_nr[keep], c_nc[keep], c_off[keep])]
-        stats_c = linear.assemble_blocks(dmesh, kind, lrules, mesh, cblocks, coup, dev)
-        t1 = time.perf_counter()
         nblocks = [(rf.perm[rf.start[a]:rf.stop[a]], cf.perm[cf.start[b]:cf.stop[b]], o)
                    for a, b, o in zip(nr_r, nc_r, n_off)]
-        stats_n = linear.assemble_blocks(dmesh, kind, lrules, mesh, nblocks, near, dev)
+        if disc == "collocation":
+            crules = linear.CollocationRules(*orders)
+            s_c = linear.collocation_blocks(dmesh, kind, crules, mesh, cblocks, coup, dev)
+            t1 = time.perf_counter()
+            s_n = linear.collocation_blocks(dmesh, kind, crules, mesh, nblocks, near, dev)
+            stats_c, stats_n = s_c + [0, 0], s_n + [0, 0]
+        else:
+            lrules = linear.LinearRules.get(orders[0], orders[1], dev)
+            stats_c = linear.assemble_blocks(dmesh, kind, lrules, mesh, cblocks, coup, dev)
+            t1 = time.perf_counter()
+            stats_n = linear.assemble_blocks(dmesh, kind, lrules, mesh, nblocks, near, dev)
     else:
         stats_c = device_block_assembly(dmesh, rules, queue, rstore.pivots, cstore.pivots,
                                         cdesc[keep], coup, kind=kind)

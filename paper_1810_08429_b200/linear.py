@@ -208,3 +208,104 @@ def _run_batch(dmesh, kind, rules, batch, ntask, out, device, totals):
     sing[0] = ntask - sum(sing[1:])
     for k in range(4):
         totals[k] += sing[k]
+
+
+# --------------------------------------------------------------------------
+# collocation (assembly.py:219-276, 340-362): rows are surface points (the
+# mesh vertices), columns the linear basis
+
+class CollocationRules:
+    """The regular rule of the chart points (weights, barycentrics) and the
+    collapsed Gauss rule used when the point is a corner of the triangle
+    (``quadrature.duffy_rule(0, q_sing)``)."""
+
+    def __init__(self, q_reg, q_sing):
+        pts, wts = triangle_gauss(q_reg)
+        self.w = np.ascontiguousarray(wts, dtype=np.float64)
+        self.b = np.ascontiguousarray(np.stack([1.0 - pts[:, 0] - pts[:, 1], pts[:, 0], pts[:, 1]], 1))
+        sp, sw = triangle_gauss(q_sing)
+        self.sw = np.ascontiguousarray(sw, dtype=np.float64)
+        self.sp = np.ascontiguousarray(sp, dtype=np.float64)
+
+
+def collocation_classify(mesh):
+    """``assembly.py:219-228``: case 1 iff the point is a corner of the
+    triangle, py = the rotation putting that corner first."""
+    tris = mesh.triangles
+
+    def classify(rows, cols):
+        hit = tris[cols] == np.asarray(rows)[:, None]
+        return hit.any(axis=1).astype(np.int64), np.zeros(len(rows), dtype=np.int64), np.argmax(hit, axis=1)
+
+    return classify
+
+
+def _col_call(dmesh, kind, rules, tasks_dev, n, U, pp, device):
+    with torch.cuda.device(device):
+        _native.call("gc_col_pairs", dmesh.geom_of(kind), ptr(dmesh.verts), rules.w.ctypes.data,
+                     rules.b.ctypes.data, len(rules.sw), rules.sw.ctypes.data, rules.sp.ctypes.data, n,
+                     ptr(tasks_dev), ptr(U), ptr(pp), stream_handle())
+
+
+def collocation_values(dmesh, kind, rules, rows, cols, device):
+    """(B, 1, 3) single integrals of the (point, triangle) tasks in the
+    rotated column order - the collocation evaluator seam."""
+    n = len(rows)
+    tasks = to_dev(np.stack([np.asarray(rows, np.int64), np.asarray(cols, np.int64)], 1), device)
+    U = empty(9 * max(n, 1), device)
+    pp = torch.empty(max(n, 1), dtype=torch.int32, device=device)
+    _col_call(dmesh, kind, rules, tasks, n, U, pp, device)
+    return U.view(-1, 9)[:n, :3].cpu().numpy().reshape(n, 1, 3)
+
+
+def collocation_blocks(dmesh, kind, rules, mesh, blocks, out, device):
+    """Collocation blocks: ``blocks`` = (row points, column DOFs, out_off);
+    column-major per block in ``out``.  Returns [regular, singular] task
+    counts."""
+    totals = [0, 0]
+    i = 0
+    while i < len(blocks):
+        batch, ntask = [], 0
+        while i < len(blocks):
+            rows, cols, off = blocks[i]
+            tc = triangle_table(cols, mesh)
+            n = len(rows) * len(tc)
+            if batch and ntask + n > _MAX_TASKS:
+                break
+            batch.append((np.asarray(rows, np.int64), cols, off, tc))
+            ntask += n
+            i += 1
+        tasks = np.empty((ntask, 2), dtype=np.int64)
+        desc = np.empty((len(batch), 7), dtype=np.int64)
+        rp, rl, cp, cl = [], [], [], []
+        base = ro = co = nrl = ncl = 0
+        for b, (rows, cols, off, tc) in enumerate(batch):
+            nr, nc, C = len(rows), len(cols), len(tc)
+            tasks[base:base + nr * C, 0] = np.repeat(rows, C)
+            tasks[base:base + nr * C, 1] = np.tile(tc[:, 0], nr)
+            rp.append(np.arange(nr, dtype=np.int64) + nrl)
+            rl.append(np.arange(nr, dtype=np.int64) << 2)           # row i: (task row i, corner 0)
+            p2, l2 = _dof_lists(tc, nc)
+            cp.append(p2[:-1] + ncl)
+            cl.append(l2)
+            desc[b] = (ro, nr, co, nc, off, base, C)
+            nrl += nr
+            ncl += len(l2)
+            ro += nr
+            co += nc
+            base += nr * C
+        rptr = np.concatenate(rp + [np.array([nrl], np.int64)])
+        cptr = np.concatenate(cp + [np.array([ncl], np.int64)])
+        d = [to_dev(a, device) for a in (desc, rptr, np.concatenate(rl), cptr,
+                                          np.concatenate(cl) if ncl else np.zeros(1, np.int64))]
+        d_tasks = to_dev(tasks, device)
+        U = empty(9 * max(ntask, 1), device)
+        pp = torch.empty(max(ntask, 1), dtype=torch.int32, device=device)
+        _col_call(dmesh, kind, rules, d_tasks, ntask, U, pp, device)
+        with torch.cuda.device(device):
+            _native.call("gc_lin_gather", len(batch), ptr(d[0]), ptr(d[1]), ptr(d[2]), ptr(d[3]), ptr(d[4]),
+                         ptr(U), ptr(pp), ptr(out), stream_handle())
+        sing = int((mesh.triangles[tasks[:, 1]] == tasks[:, :1]).any(axis=1).sum()) if ntask else 0
+        totals[0] += ntask - sing
+        totals[1] += sing
+    return totals

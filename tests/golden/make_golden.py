@@ -254,6 +254,51 @@ def main_linear():
                         table_rows=r, table=A.triangle_table(r, s2).rows)
 
 
+def main_collocation():
+    s3 = G.build_sphere_mesh(3)
+    rng = np.random.default_rng(51)
+    rows = list(rng.integers(0, s3.nv, 400))
+    cols = list(rng.integers(0, s3.nt, 400))
+    stars = s3.vertex_stars()
+    for v in rng.choice(s3.nv, 20, replace=False):
+        for t in stars[v]:
+            rows.append(int(v))
+            cols.append(int(t))
+    rows, cols = np.array(rows), np.array(cols)
+    case, px, py = A.collocation_classify(s3)(rows, cols)
+    out = dict(rows=rows, cols=cols, case=case, py=py)
+    for kind in ("slp", "dlp"):
+        ev = A.collocation_evaluator(kind, s3, 3, 5)
+        vals = np.empty((len(rows), 1, 3))
+        for k in (0, 1):
+            m = case == k
+            vals[m] = ev(k, rows[m], cols[m], px[m], py[m])
+        out[kind] = vals
+    np.savez_compressed(os.path.join(OUT, "colloc_pairs_sphere3.npz"), **out)
+    s2 = G.build_sphere_mesh(2)
+    dofs = np.arange(s2.nv)
+    np.savez_compressed(os.path.join(OUT, "colloc_dense_sphere2.npz"),
+                        slp=A.assemble_collocation_block("slp", s2, "linear", dofs, dofs).values,
+                        dlp=A.assemble_collocation_block("dlp", s2, "linear", dofs, dofs).values)
+    # the reference's collocation GCA-H2 (cli.build_h2_operator, disc="collocation")
+    import greencross.cli as CL
+    mesh = G.build_sphere_mesh(3)
+    cfg = CL.ExperimentConfig(level=3, geometry="plane", basis="linear", disc="collocation", eta=1.0,
+                              m=3, delta_factor=0.5, eps=1e-4, leaf_size=16, q_reg=3, q_sing=5,
+                              lam=0.5, source=(2.0, 0.0, 0.0), seed=0)
+    hm, tree, bt = CL.build_h2_operator(mesh, cfg)
+    res = dict(perm=tree.perm.astype(np.int32))
+    for side, basis in (("row", hm.row_basis), ("col", hm.col_basis)):
+        bns = basis.nodes()
+        res[side + "_node"] = np.array([b.cluster.index for b in bns], np.int32)
+        res[side + "_rank"] = np.array([b.rank for b in bns], np.int32)
+        res[side + "_piv"] = np.concatenate([b.pivots for b in bns]).astype(np.int32)
+    x = rng.standard_normal((3, mesh.nv))
+    res["x"] = x
+    res["mvm"] = np.array([H.mvm(hm, v) for v in x])
+    np.savez_compressed(os.path.join(OUT, "h2_colloc_sphere3_eps1e-4.npz"), **res)
+
+
 def main_dlp():
     s3 = G.build_sphere_mesh(3)
     np.savez_compressed(os.path.join(OUT, "pairs_dlp_sphere3.npz"), **pair_tasks(s3, 600, 31, "dlp"))
@@ -291,5 +336,7 @@ if __name__ == "__main__":
         main_linear()
     elif "--linear-h2" in sys.argv:
         main_linear_h2()
+    elif "--collocation" in sys.argv:
+        main_collocation()
     else:
         main()

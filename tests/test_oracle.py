@@ -212,3 +212,28 @@ def test_linear_triangle_table_host_matches_oracle():
         idx = rng.choice(mesh.nv, n, replace=False)
         assert np.array_equal(linear.triangle_table(idx, mesh),
                               P.triangle_table(idx, mesh.triangles, mesh.nv))
+
+
+# ---------------------------------------------------------------- collocation
+
+def test_collocation_values_and_blocks_bitwise():
+    g = golden("colloc_pairs_sphere3.npz")
+    mesh = mesh_for("x_sphere3")
+    nodes, gram = P.chart_nodes(mesh.vertices, mesh.triangles)
+    normals = P.chart_normals(mesh.vertices, mesh.triangles)
+    case, py = P.collocation_classify(mesh.triangles, g["rows"], g["cols"])
+    assert np.array_equal(case, g["case"]) and np.array_equal(py, g["py"])
+    for kind in ("slp", "dlp"):
+        for k in (0, 1):
+            m = case == k
+            got = P.collocation_values(nodes, gram, mesh.vertices, k, g["rows"][m], g["cols"][m], py[m],
+                                       kind=kind, normals=normals)
+            assert np.array_equal(got, g[kind][m]), (kind, k)
+    d = golden("colloc_dense_sphere2.npz")
+    s2 = build_sphere_mesh(2)
+    n2, g2 = P.chart_nodes(s2.vertices, s2.triangles)
+    nn2 = P.chart_normals(s2.vertices, s2.triangles)
+    dofs = np.arange(s2.nv)
+    assert np.array_equal(P.block_collocation(n2, g2, s2.vertices, s2.triangles, dofs, dofs), d["slp"])
+    assert np.array_equal(P.block_collocation(n2, g2, s2.vertices, s2.triangles, dofs, dofs, kind="dlp",
+                                              normals=nn2), d["dlp"])

@@ -75,6 +75,14 @@ typedef struct gc_geom {
      * (point evaluations at the vertices, Green factors only) */
     int64_t basis;
     const double* verts;   /* [dev] nv x 3 vertex coordinates (collocation) */
+    /* curved (quadratic) charts, all NULL for plane charts (geometry.py:
+     * 266-293): nodes6 / nrm6 [dev] nt x 6 x 3 chart nodes and node normals,
+     * gq [dev] nt x mq Gramians |n| at the regular points, nq [dev] nt x mq
+     * x 3 the interpolated normals there (double layer) */
+    const double* nodes6;
+    const double* nrm6;
+    const double* gq;
+    const double* nq;
 } gc_geom;
 
 /* Singular pair rules (quadrature.sauter_rule, quadrature.py:211-284) in
@@ -281,6 +289,18 @@ int gc_lin_singular(const gc_geom* g, const gc_rules* r, gc_queue* q, double* U,
 int gc_lin_gather(int64_t nb, const int64_t* desc, const int64_t* rptr, const int64_t* rlist,
                   const int64_t* cptr, const int64_t* clist, const double* U, const int32_t* pp,
                   double* out, void* stream);
+
+/* Singular pairs of curved charts: the queued tasks (from
+ * gc_assemble_blocks / gc_lin_pairs) integrated with the full Sauter-Schwab
+ * rules r->table[c] = SoA (x1, x2, y1, y2, w), charts and Gramians
+ * evaluated per point; width 1 (constant basis) or 9 (linear basis). */
+int gc_curved_singular(const gc_geom* g, const gc_rules* r, gc_queue* q, int64_t width,
+                       double* out, int64_t* counts_out, void* stream);
+/* The same for an explicit task list (t, s, px | py << 8, out index) [dev]
+ * and one rule [dev] (SoA x1, x2, y1, y2, w, P points): the evaluator seam
+ * on curved charts. */
+int gc_curved_pairs(const gc_geom* g, const double* rule, int64_t P, const int64_t* tasks, int64_t n,
+                    int64_t width, double* out, void* stream);
 
 /* Collocation (assembly.py:219-276, 340-362): tasks (n,2) = (vertex v,
  * triangle s); each the 3 single integrals of k(x_v, y) phi_c(y) over s

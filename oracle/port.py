@@ -172,14 +172,46 @@ def pair_values(nodes, gram, case, rows, cols, px, py, q_reg=3, q_sing=5, kind="
         D = X - Y
         r2 = D[..., 0] ** 2 + D[..., 1] ** 2 + D[..., 2] ** 2
         r = np.sqrt(r2)
+        gx, gy = _gramians(nx, ny, gram, normals, rows[sl], cols[sl], px[sl], py[sl], kind)
         if kind == "dlp":
             nyv = _interp(ny, normals[cols[sl][:, None], ORDER6[py[sl]]])
             dot = D[..., 0] * nyv[..., 0] + D[..., 1] * nyv[..., 1] + D[..., 2] * nyv[..., 2]
-            kg = dot / (FOUR_PI * r2 * r) * gram[rows[sl]][:, None]
+            kg = dot / (FOUR_PI * r2 * r) * gx
         else:
-            kg = gram[rows[sl]][:, None] * gram[cols[sl]][:, None] / (FOUR_PI * r)
+            kg = gx * gy / (FOUR_PI * r)
         out[sl] = np.sum(kg * w[None, :], axis=1)
     return out
+
+
+def _norm3(v):
+    return np.sqrt(v[..., 0] ** 2 + v[..., 1] ** 2 + v[..., 2] ** 2)
+
+
+def _gramians(nx, ny, gram, normals, rows, cols, px, py, kind):
+    """Row / column Gramian factors (assembly.py:189-205): the plane
+    Gramians, or (gram is None: curved charts) the norms of the interpolated
+    node normals at every rule point."""
+    if gram is not None:
+        return gram[rows][:, None], gram[cols][:, None]
+    gx = _norm3(_interp(nx, normals[rows[:, None], ORDER6[px]]))
+    gy = None if kind == "dlp" else _norm3(_interp(ny, normals[cols[:, None], ORDER6[py]]))
+    return gx, gy
+
+
+def chart_curved(vertices, triangles, midpoints, tri_edges):
+    """geometry.py:266-293 for a CurvedTriangleMesh: chart nodes with the
+    curved midpoints and the unnormalised normals at the six nodes."""
+    nodes = np.empty((len(triangles), 6, 3))
+    nodes[:, :3] = vertices[triangles]
+    nodes[:, 3:] = midpoints[tri_edges]
+    ref = np.array([[0.0, 0.0], [1.0, 0.0], [0.0, 1.0], [0.5, 0.0], [0.5, 0.5], [0.0, 0.5]])
+    x, y = ref[:, 0], ref[:, 1]
+    l0 = 1.0 - x - y
+    z = np.zeros(6)
+    gx = np.stack([1.0 - 4.0 * l0, 4.0 * x - 1.0, z, 4.0 * (l0 - x), 4.0 * y, -4.0 * y], 1)
+    gy = np.stack([1.0 - 4.0 * l0, z, 4.0 * y - 1.0, -4.0 * x, 4.0 * x, 4.0 * (l0 - y)], 1)
+    n = np.cross(np.einsum("ma,tac->tmc", gx, nodes), np.einsum("ma,tac->tmc", gy, nodes))
+    return nodes, n
 
 
 def _bary(pts):
@@ -207,12 +239,13 @@ def pair_values_linear(nodes, gram, case, rows, cols, px, py, q_reg=3, q_sing=5,
         D = X - Y
         r2 = D[..., 0] ** 2 + D[..., 1] ** 2 + D[..., 2] ** 2
         r = np.sqrt(r2)
+        gx, gy = _gramians(nx, ny, gram, normals, rows[sl], cols[sl], px[sl], py[sl], kind)
         if kind == "dlp":
             nyv = _interp(ny, normals[cols[sl][:, None], ORDER6[py[sl]]])
             dot = D[..., 0] * nyv[..., 0] + D[..., 1] * nyv[..., 1] + D[..., 2] * nyv[..., 2]
-            kg = dot / (FOUR_PI * r2 * r) * gram[rows[sl]][:, None]
+            kg = dot / (FOUR_PI * r2 * r) * gx
         else:
-            kg = gram[rows[sl]][:, None] * gram[cols[sl]][:, None] / (FOUR_PI * r)
+            kg = gx * gy / (FOUR_PI * r)
         for a in range(3):
             for c in range(3):
                 out[sl, a, c] = np.sum(kg * wb[a, c][None, :], axis=1)

@@ -21,7 +21,8 @@ class GcGeom(ctypes.Structure):
     _fields_ = [("corners", c_p), ("gram", c_p), ("tri_vid", c_p), ("xq", c_p),
                 ("wq", c_p), ("nt", c_i64), ("mq", c_i64), ("wq_host", c_p),
                 ("normals", c_p), ("kernel", c_i64), ("vstar_ptr", c_p), ("vstar_ent", c_p),
-                ("bq", c_p), ("basis", c_i64), ("verts", c_p)]
+                ("bq", c_p), ("basis", c_i64), ("verts", c_p), ("nodes6", c_p), ("nrm6", c_p),
+                ("gq", c_p), ("nq", c_p)]
 
 
 class GcRules(ctypes.Structure):
@@ -62,6 +63,9 @@ _SIGNATURES = {
     "gc_lin_singular": [ctypes.POINTER(GcGeom), ctypes.POINTER(GcRules), ctypes.POINTER(GcQueue), c_p,
                         ctypes.POINTER(c_i64), c_p],
     "gc_lin_gather": [c_i64, c_p, c_p, c_p, c_p, c_p, c_p, c_p, c_p, c_p],
+    "gc_curved_singular": [ctypes.POINTER(GcGeom), ctypes.POINTER(GcRules), ctypes.POINTER(GcQueue), c_i64,
+                           c_p, ctypes.POINTER(c_i64), c_p],
+    "gc_curved_pairs": [ctypes.POINTER(GcGeom), c_p, c_i64, c_p, c_i64, c_i64, c_p, c_p],
     "gc_col_pairs": [ctypes.POINTER(GcGeom), c_p, c_p, c_p, c_i64, c_p, c_p, c_i64, c_p, c_p, c_p, c_p],
     "gc_dot": [c_i64, c_p, c_p, c_p, c_p, c_p],
     "gc_cg_pq": [c_i64, c_p, c_p, c_p, c_p, c_p],

@@ -76,6 +76,9 @@ def galerkin_pair_evaluator(kind, mesh, basis, q_reg, q_sing, device=None):
         return evaluate_linear
     rules = DeviceRules.get(q_sing, dev, kind)
     geom = dmesh.geom_of(kind)
+    if dmesh.curved:
+        from . import linear
+        return linear.curved_evaluator(dmesh, kind, q_reg, q_sing, 1, dev)
 
     def evaluate(case, rows, cols, px, py):
         case = int(case)
@@ -100,6 +103,11 @@ def device_block_assembly(dmesh, rules, queue, row_idx, col_idx, desc, out, stat
     if getattr(rules, "kind", "slp") != kind:
         raise ConfigError("rules built for %r, assembling %r" % (rules.kind, kind))
     geom = dmesh.geom_of(kind)
+    full = None
+    if dmesh.curved:
+        # curved charts: singular pairs take the full Sauter-Schwab rules
+        from . import linear
+        full = linear.LinearRules.get(dmesh.q_reg, rules.q_sing, out.device)
     nb = len(desc)
     if nb == 0:
         return [0, 0, 0, 0]
@@ -111,8 +119,11 @@ def device_block_assembly(dmesh, rules, queue, row_idx, col_idx, desc, out, stat
                      int(desc[:, 3].max()), ptr(row_idx), ptr(col_idx), ptr(out), queue.struct, ptr(queue.flags),
                      stream)
         counts = (_native.c_i64 * 4)()
-        _native.call("gc_singular_flush", geom, rules.struct, queue.struct, ptr(out),
-                     counts, stream)
+        if full is not None:
+            _native.call("gc_curved_singular", geom, full.struct, queue.struct, 1, ptr(out), counts, stream)
+        else:
+            _native.call("gc_singular_flush", geom, rules.struct, queue.struct, ptr(out),
+                         counts, stream)
     queue.check_flags()
     n_sing = [int(counts[k]) for k in range(4)]
     n_sing[0] = int(entries.sum()) - sum(n_sing[1:])

@@ -58,7 +58,7 @@ template <bool LIN>
 __device__ __forceinline__ void tri_moments(const gc_geom& g, int64_t t, int a, double z0, double z1, double z2,
                                             double n0, double n1, double n2, double& ig, double& ih, bool& touch) {
     const int mq = (int)g.mq;
-    const double gram = g.gram[t];
+    const double gram = g.gq ? 0.0 : g.gram[t];
     const double* xq = g.xq + t * 3 * mq;
     for (int p = 0; p < mq; ++p) {
         const double d0 = __dsub_rn(xq[3 * p], z0);
@@ -70,7 +70,7 @@ __device__ __forceinline__ void tri_moments(const gc_geom& g, int64_t t, int a, 
         const double gk = __ddiv_rn(1.0, __dmul_rn(FOUR_PI, rr));
         const double dot = __dadd_rn(__dadd_rn(__dmul_rn(d0, n0), __dmul_rn(d1, n1)), __dmul_rn(d2, n2));
         const double hk = __ddiv_rn(dot, __dmul_rn(FOUR_PI, cube_rn(rr)));
-        double gw = __dmul_rn(gram, g.wq[p]);
+        double gw = __dmul_rn(g.gq ? g.gq[t * mq + p] : gram, g.wq[p]);   // curved: |n| per point
         if (LIN) gw = __dmul_rn(g.bq[3 * p + a], gw);
         ig = __dadd_rn(ig, __dmul_rn(gw, gk));
         ih = __dadd_rn(ih, __dmul_rn(gw, hk));

@@ -86,19 +86,28 @@ __global__ void __launch_bounds__(128) k_lin_pairs(gc_geom g, LinRule lr, const 
             n1 = __ldg(g.normals + 3 * s + 1);
             n2 = __ldg(g.normals + 3 * s + 2);
         }
+        // curved charts: per-point Gramians (row always, column for the
+        // single layer) and per-point normals (double layer)
+        const bool curv = g.gq != nullptr;
         double acc[3][3] = {{0.0, 0.0, 0.0}, {0.0, 0.0, 0.0}, {0.0, 0.0, 0.0}};
 #pragma unroll 1
         for (int j = 0; j < M; ++j) {
             const double y0 = __ldg(xs + 3 * j), y1 = __ldg(xs + 3 * j + 1), y2 = __ldg(xs + 3 * j + 2);
+            if (DLP && curv) {
+                n0 = __ldg(g.nq + (s * M + j) * 3);
+                n1 = __ldg(g.nq + (s * M + j) * 3 + 1);
+                n2 = __ldg(g.nq + (s * M + j) * 3 + 2);
+            }
             double p0 = 0.0, p1 = 0.0, p2 = 0.0;
 #pragma unroll
             for (int k = 0; k < M; ++k) {
-                const double wk = lr.w[k] * lin_kern<DLP>(X[k][0] - y0, X[k][1] - y1, X[k][2] - y2, n0, n1, n2);
+                const double wxk = curv ? lr.w[k] * __ldg(g.gq + t * M + k) : lr.w[k];
+                const double wk = wxk * lin_kern<DLP>(X[k][0] - y0, X[k][1] - y1, X[k][2] - y2, n0, n1, n2);
                 p0 = fma(wk, lr.b[k][0], p0);
                 p1 = fma(wk, lr.b[k][1], p1);
                 p2 = fma(wk, lr.b[k][2], p2);
             }
-            const double wj = lr.w[j];
+            const double wj = (curv && !DLP) ? lr.w[j] * __ldg(g.gq + s * M + j) : lr.w[j];
 #pragma unroll
             for (int c = 0; c < 3; ++c) {
                 const double f = wj * lr.b[j][c];
@@ -107,8 +116,11 @@ __global__ void __launch_bounds__(128) k_lin_pairs(gc_geom g, LinRule lr, const 
                 acc[2][c] = fma(p2, f, acc[2][c]);
             }
         }
-        const double gt = __ldg(g.gram + t) * INV_FOUR_PI;
-        const double sc = DLP ? gt : gt * __ldg(g.gram + s);
+        double sc = INV_FOUR_PI;
+        if (!curv) {
+            const double gt = __ldg(g.gram + t) * INV_FOUR_PI;
+            sc = DLP ? gt : gt * __ldg(g.gram + s);
+        }
 #pragma unroll
         for (int a = 0; a < 3; ++a)
 #pragma unroll
@@ -253,6 +265,7 @@ extern "C" int gc_lin_pairs(const gc_geom* gp, const double* rule_w, const doubl
 extern "C" int gc_lin_singular(const gc_geom* gp, const gc_rules* rp, gc_queue* qp, double* U,
                                int64_t* counts_out, void* stream) {
     if (!gp || !rp || !qp) { set_error(GC_ERR_CONFIG, "gc_lin_singular: null argument"); return GC_ERR_CONFIG; }
+    if (gp->gq) { set_error(GC_ERR_CONFIG, "curved charts: flush with gc_curved_singular"); return GC_ERR_CONFIG; }
     cudaStream_t st = (cudaStream_t)stream;
     int32_t counts[4] = {0, 0, 0, 0};
     cudaError_t e = cudaMemcpyAsync(counts, qp->count, sizeof(counts), cudaMemcpyDeviceToHost, st);
@@ -298,6 +311,9 @@ extern "C" int gc_lin_gather(int64_t nb, const int64_t* desc, const int64_t* rpt
 // Gauss rule with v rotated to corner 0 (duffy_rule(0, q_sing)), where
 // y - x_v = y1 E1 + y2 E2 carries no cancellation.  Values in the rotated
 // (canonical) column order: U[9 i + c], pp[i] = rotation << 8.
+__device__ __constant__ static const int8_t kOrder6c[3][6] = {
+    {0, 1, 2, 3, 4, 5}, {1, 2, 0, 4, 5, 3}, {2, 0, 1, 5, 3, 4}};
+
 struct ColRule {
     double w[64];        // regular rule weights
     double b[64][3];     // regular rule barycentrics
@@ -325,16 +341,50 @@ __global__ void __launch_bounds__(128) k_col_pairs(gc_geom g, ColRule cr, const 
             n2 = __ldg(g.normals + 3 * s + 2);
         }
         double acc[3] = {0.0, 0.0, 0.0};
-        if (rot < 0) {
+        const bool curv = g.gq != nullptr;
+        if (curv && rot >= 0) {
+            // curved chart, point at a corner: the rotated quadratic chart at
+            // the collapsed rule's points (assembly.py:254-265)
+            const double* P6 = g.nodes6 + 18 * s;
+            const double* N6 = g.nrm6 + 18 * s;
+            for (int m = 0; m < cr.ms; ++m) {
+                const double y1 = cr.sp[m][0], y2 = cr.sp[m][1];
+                const double l0 = 1.0 - y1 - y2;
+                const double sh[6] = {l0 * (2.0 * l0 - 1.0), y1 * (2.0 * y1 - 1.0), y2 * (2.0 * y2 - 1.0),
+                                      4.0 * l0 * y1, 4.0 * y1 * y2, 4.0 * y2 * l0};
+                double Y[3], Nn[3];
+#pragma unroll
+                for (int c = 0; c < 3; ++c) {
+                    double ay = 0.0, an = 0.0;
+#pragma unroll
+                    for (int a = 0; a < 6; ++a) {
+                        ay = fma(sh[a], P6[3 * kOrder6c[rot][a] + c], ay);
+                        an = fma(sh[a], N6[3 * kOrder6c[rot][a] + c], an);
+                    }
+                    Y[c] = ay;
+                    Nn[c] = an;
+                }
+                const double gy = sqrt(fma(Nn[2], Nn[2], fma(Nn[1], Nn[1], Nn[0] * Nn[0])));
+                const double k = lin_kern<DLP>(x0 - Y[0], x1 - Y[1], x2 - Y[2], Nn[0], Nn[1], Nn[2]);
+                const double wk = cr.sw[m] * (DLP ? k : gy * k);
+                const double b[3] = {l0, y1, y2};
+#pragma unroll
+                for (int c = 0; c < 3; ++c) acc[c] = fma(wk, b[c], acc[c]);
+            }
+        } else if (rot < 0) {
             const double* yq = g.xq + s * 3 * M;
             for (int m = 0; m < M; ++m) {
+                if (DLP && curv) {
+                    n0 = __ldg(g.nq + (s * M + m) * 3);
+                    n1 = __ldg(g.nq + (s * M + m) * 3 + 1);
+                    n2 = __ldg(g.nq + (s * M + m) * 3 + 2);
+                }
                 const double k = lin_kern<DLP>(x0 - __ldg(yq + 3 * m), x1 - __ldg(yq + 3 * m + 1),
                                                x2 - __ldg(yq + 3 * m + 2), n0, n1, n2);
-                const double wk = cr.w[m] * k;
+                const double wk = (curv && !DLP ? cr.w[m] * __ldg(g.gq + s * M + m) : cr.w[m]) * k;
 #pragma unroll
                 for (int c = 0; c < 3; ++c) acc[c] = fma(wk, cr.b[m][c], acc[c]);
             }
-            rot = 0;
         } else {
             // rotation rot puts corner rot first: PERMS3[rot] = (rot, rot+1, rot+2)
             const double* cs = g.corners + 9 * s;
@@ -357,7 +407,8 @@ __global__ void __launch_bounds__(128) k_col_pairs(gc_geom g, ColRule cr, const 
                 for (int c = 0; c < 3; ++c) acc[c] = fma(wk, b[c], acc[c]);
             }
         }
-        const double sc = DLP ? INV_FOUR_PI : __ldg(g.gram + s) * INV_FOUR_PI;
+        const double sc = (DLP || curv) ? INV_FOUR_PI : __ldg(g.gram + s) * INV_FOUR_PI;
+        if (rot < 0) rot = 0;
         pp[i] = rot << 8;
 #pragma unroll
         for (int c = 0; c < 3; ++c) U[9 * i + c] = sc * acc[c];

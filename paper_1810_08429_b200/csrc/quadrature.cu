@@ -124,7 +124,7 @@ struct RuleW {
 // (nr*M*3), column points (nc*M*3) and both vertex-id lists; the caller
 // sizes the dynamic allocation for the largest block.  NT = 128 for the
 // 16x16 near-field blocks (one thread per column pair), 256 otherwise.
-template <int M, int NT, bool DLP>
+template <int M, int NT, bool DLP, bool CURV>
 __global__ void __launch_bounds__(NT) k_assemble_blocks(
     gc_geom g, RuleW rw, const int64_t* __restrict__ desc, const int64_t* __restrict__ row_idx,
     const int64_t* __restrict__ col_idx, double* __restrict__ out, gc_queue q, int32_t* flags) {
@@ -187,30 +187,54 @@ __global__ void __launch_bounds__(NT) k_assemble_blocks(
         const int b1 = two ? b0 + 1 : b0;
         const double* Y0 = Ys + b0 * M * 3;
         const double* Y1 = Ys + b1 * M * 3;
+        const int64_t s0 = svs[4 * b0], s1 = svs[4 * b1];
         double na[3] = {0.0, 0.0, 0.0}, nb[3] = {0.0, 0.0, 0.0};
-        if (DLP) {
+        if (DLP && !CURV) {
 #pragma unroll
             for (int k = 0; k < 3; ++k) {
-                na[k] = __ldg(g.normals + 3 * svs[4 * b0] + k);
-                nb[k] = __ldg(g.normals + 3 * svs[4 * b1] + k);
+                na[k] = __ldg(g.normals + 3 * s0 + k);
+                nb[k] = __ldg(g.normals + 3 * s1 + k);
             }
+        }
+        // curved charts: the point Gramians fold into the weights (row
+        // always; column for the single layer - the double layer's |n_y| is
+        // the interpolated normal)
+        double wx[CURV ? M : 1];
+        if (CURV) {
+#pragma unroll
+            for (int i = 0; i < M; ++i) wx[i] = rw.w[i] * __ldg(g.gq + t * M + i);
         }
         double tot0 = 0.0, tot1 = 0.0;
 #pragma unroll 1
         for (int j = 0; j < M; ++j) {
             const double u0 = Y0[3 * j], u1 = Y0[3 * j + 1], u2 = Y0[3 * j + 2];
             const double v0 = Y1[3 * j], v1 = Y1[3 * j + 1], v2 = Y1[3 * j + 2];
+            if (DLP && CURV) {
+#pragma unroll
+                for (int k = 0; k < 3; ++k) {
+                    na[k] = __ldg(g.nq + (s0 * M + j) * 3 + k);
+                    nb[k] = __ldg(g.nq + (s1 * M + j) * 3 + k);
+                }
+            }
             double acc0 = 0.0, acc1 = 0.0;
 #pragma unroll
             for (int i = 0; i < M; ++i) {
-                acc0 = fma(rw.w[i], kern<DLP>(X[i][0] - u0, X[i][1] - u1, X[i][2] - u2, na[0], na[1], na[2]), acc0);
-                acc1 = fma(rw.w[i], kern<DLP>(X[i][0] - v0, X[i][1] - v1, X[i][2] - v2, nb[0], nb[1], nb[2]), acc1);
+                const double wi = CURV ? wx[CURV ? i : 0] : rw.w[i];
+                acc0 = fma(wi, kern<DLP>(X[i][0] - u0, X[i][1] - u1, X[i][2] - u2, na[0], na[1], na[2]), acc0);
+                acc1 = fma(wi, kern<DLP>(X[i][0] - v0, X[i][1] - v1, X[i][2] - v2, nb[0], nb[1], nb[2]), acc1);
             }
-            tot0 = fma(rw.w[j], acc0, tot0);
-            tot1 = fma(rw.w[j], acc1, tot1);
+            double wy0 = rw.w[j], wy1 = rw.w[j];
+            if (CURV && !DLP) {
+                wy0 *= __ldg(g.gq + s0 * M + j);
+                wy1 *= __ldg(g.gq + s1 * M + j);
+            }
+            tot0 = fma(wy0, acc0, tot0);
+            tot1 = fma(wy1, acc1, tot1);
         }
-        if (live[0]) out[out_off + (int64_t)b0 * nr + a] = entry_scale<DLP>(g, t, svs[4 * b0]) * tot0;
-        if (live[1]) out[out_off + (int64_t)(b0 + 1) * nr + a] = entry_scale<DLP>(g, t, svs[4 * b1]) * tot1;
+        const double sc0 = CURV ? INV_FOUR_PI : entry_scale<DLP>(g, t, s0);
+        const double sc1 = CURV ? INV_FOUR_PI : entry_scale<DLP>(g, t, s1);
+        if (live[0]) out[out_off + (int64_t)b0 * nr + a] = sc0 * tot0;
+        if (live[1]) out[out_off + (int64_t)(b0 + 1) * nr + a] = sc1 * tot1;
     }
 }
 
@@ -492,14 +516,16 @@ static int launch_singular(const gc_geom& g, const gc_rules& r, int kase, const 
     }
 }
 
-template <int M, int NT, bool DLP>
+template <int M, int NT, bool DLP, bool CURV = false>
 static int launch_blocks_nt(const gc_geom& g, const RuleW& rw, int64_t nb, const int64_t* desc,
                             size_t bytes, const int64_t* ri, const int64_t* ci, double* out,
                             const gc_queue& q, int32_t* flags, cudaStream_t st) {
-    cudaError_t e = cudaFuncSetAttribute(k_assemble_blocks<M, NT, DLP>,
+    if (g.gq && !CURV)
+        return launch_blocks_nt<M, NT, DLP, true>(g, rw, nb, desc, bytes, ri, ci, out, q, flags, st);
+    cudaError_t e = cudaFuncSetAttribute(k_assemble_blocks<M, NT, DLP, CURV>,
                                          cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes);
     if (e != cudaSuccess) return cuda_status(e, "k_assemble_blocks smem attribute");
-    k_assemble_blocks<M, NT, DLP><<<(unsigned)nb, NT, bytes, st>>>(g, rw, desc, ri, ci, out, q, flags);
+    k_assemble_blocks<M, NT, DLP, CURV><<<(unsigned)nb, NT, bytes, st>>>(g, rw, desc, ri, ci, out, q, flags);
     GC_CHECK_LAUNCH("k_assemble_blocks");
     return GC_OK;
 }
@@ -548,6 +574,7 @@ int gc_pair_eval(const gc_geom* gp, const gc_rules* rp, int kase, int64_t B, con
                  void* stream) {
     if (!gp || !rp) { set_error(GC_ERR_CONFIG, "null geometry/rules"); return GC_ERR_CONFIG; }
     if (B <= 0) return GC_OK;
+    if (gp->gq) { set_error(GC_ERR_CONFIG, "curved charts: evaluate with gc_curved_pairs"); return GC_ERR_CONFIG; }
     cudaStream_t st = (cudaStream_t)stream;
     const gc_geom g = *gp;
     if (kase == 0) {
@@ -591,6 +618,15 @@ int gc_assemble_blocks(const gc_geom* gp, int64_t nb, const int64_t* desc, int64
     cudaStream_t st = (cudaStream_t)stream;
     const gc_geom g = *gp;
     if (g.kernel && !g.normals) { set_error(GC_ERR_CONFIG, "double layer needs gc_geom.normals"); return GC_ERR_CONFIG; }
+    if (g.gq) {
+        // curved charts: the shared-memory block kernel with per-point Gramians
+        const size_t bytes = (size_t)(max_rows + max_cols) * (g.mq * 3 * sizeof(double) + 4 * sizeof(int64_t));
+        if ((g.mq != 4 && g.mq != 9 && g.mq != 16) || bytes > 200 * 1024) {
+            set_error(GC_ERR_CONFIG, "curved charts: q_reg in {2, 3, 4} and blocks of <= %lld entries per side",
+                      (long long)(200 * 1024 / (g.mq * 24 + 32)));
+            return GC_ERR_CONFIG;
+        }
+    }
     switch (g.mq) {
         case 9: return launch_blocks<9>(g, nb, desc, max_rows, max_cols, row_idx, col_idx, out, *qp, flags, st);
         case 4: return launch_blocks<4>(g, nb, desc, max_rows, max_cols, row_idx, col_idx, out, *qp, flags, st);
@@ -620,6 +656,7 @@ int gc_assemble_blocks(const gc_geom* gp, int64_t nb, const int64_t* desc, int64
 int gc_singular_flush(const gc_geom* gp, const gc_rules* rp, gc_queue* qp, double* out,
                       int64_t* counts_out, void* stream) {
     if (!gp || !rp || !qp) { set_error(GC_ERR_CONFIG, "null argument"); return GC_ERR_CONFIG; }
+    if (gp->gq) { set_error(GC_ERR_CONFIG, "curved charts: flush with gc_curved_singular"); return GC_ERR_CONFIG; }
     cudaStream_t st = (cudaStream_t)stream;
     int32_t counts[4] = {0, 0, 0, 0};
     cudaError_t e = cudaMemcpyAsync(counts, qp->count, sizeof(counts), cudaMemcpyDeviceToHost, st);

@@ -90,18 +90,31 @@ class DeviceMesh:
         self.nt = mesh.nt
         self.q_reg = q_reg
         pts, wts = triangle_gauss(q_reg)
+        self.curved = bool(pack.curved)
         self.corners = to_dev(pack.nodes[:, :3], device)
-        self.gram = to_dev(pack.gram, device)
+        self.gram = to_dev(pack.gram if not self.curved else np.zeros(self.nt), device)
         self.tri_vid = to_dev(mesh.triangles.astype(np.int64), device)
         self.wq = to_dev(wts, device)
-        n6 = to_dev(shape_functions(pts), device)
         self.mq = len(wts)
-        self.xq = empty((self.nt, self.mq, 3), device)
-        with torch.cuda.device(device):
-            _native.call("gc_surface_points", ptr(self.corners), self.nt, ptr(n6), self.mq,
-                         ptr(self.xq), stream_handle())
+        n6h = shape_functions(pts)
+        if self.curved:
+            # quadratic charts: points, point Gramians and normals on the host
+            # with the reference's einsum/norm (assembly.py:371-381)
+            self.xq = to_dev(np.einsum("ma,tac->tmc", n6h, pack.nodes), device)
+            nrm = np.einsum("ma,tac->tmc", n6h, pack.normals)
+            self.gq = to_dev(np.sqrt(nrm[..., 0] ** 2 + nrm[..., 1] ** 2 + nrm[..., 2] ** 2), device)
+            self.nq = to_dev(nrm, device)
+            self.nodes6 = to_dev(pack.nodes, device)
+            self.nrm6 = to_dev(pack.normals, device)
+        else:
+            n6 = to_dev(n6h, device)
+            self.xq = empty((self.nt, self.mq, 3), device)
+            with torch.cuda.device(device):
+                _native.call("gc_surface_points", ptr(self.corners), self.nt, ptr(n6), self.mq,
+                             ptr(self.xq), stream_handle())
+            self.gq = self.nq = self.nodes6 = self.nrm6 = None
         self.wq_host = np.ascontiguousarray(wts, dtype=np.float64)
-        # chart normal per triangle (|n| = gram), for the double layer
+        # chart normal per triangle (|n| = gram), for the double layer of plane charts
         self.normals = to_dev(np.ascontiguousarray(pack.normals[:, 0]), device)
         # linear basis: vertex stars ordered by (corner, triangle) and the
         # barycentric values of the regular rule's points
@@ -131,7 +144,8 @@ class DeviceMesh:
             self._geoms[key] = _native.GcGeom(
                 ptr(self.corners), ptr(self.gram), ptr(self.tri_vid), ptr(self.xq), ptr(self.wq),
                 self.nt, self.mq, self.wq_host.ctypes.data, ptr(self.normals), int(kind == "dlp"),
-                ptr(self.vstar_ptr), ptr(self.vstar_ent), ptr(self.bq), codes[basis], ptr(self.verts))
+                ptr(self.vstar_ptr), ptr(self.vstar_ent), ptr(self.bq), codes[basis], ptr(self.verts),
+                ptr(self.nodes6), ptr(self.nrm6), ptr(self.gq), ptr(self.nq))
         return self._geoms[key]
 
     @classmethod
@@ -225,5 +239,4 @@ def check_mesh(mesh, kind="slp", basis="constant", linear_ok=False):
         raise ConfigError("unknown kernel kind %r" % (kind,))
     if basis not in ("constant", "linear", "collocation"):
         raise ConfigError("unknown basis %r" % (basis,))
-    if getattr(mesh, "midpoints", None) is not None:
-        raise ConfigError("curved charts are out of scope")
+

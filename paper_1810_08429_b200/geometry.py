@@ -226,13 +226,66 @@ class ChartPack:
         self.curved = curved
 
 
+class CurvedTriangleMesh:
+    """A plane mesh whose edges carry one (curved) midpoint each: quadratic
+    charts (``geometry.py:69-114``).  Straight midpoints reproduce the plane
+    chart exactly."""
+
+    def __init__(self, base, midpoints):
+        midpoints = np.ascontiguousarray(midpoints, dtype=np.float64)
+        if midpoints.shape != (base.ne, 3):
+            raise MeshFormatError("expected %d midpoints, got %d" % (base.ne, len(midpoints)))
+        self.base = base
+        self.midpoints = midpoints
+        self._pack = None
+
+    vertices = property(lambda self: self.base.vertices)
+    triangles = property(lambda self: self.base.triangles)
+    edges = property(lambda self: self.base.edges)
+    tri_edges = property(lambda self: self.base.tri_edges)
+    nv = property(lambda self: self.base.nv)
+    nt = property(lambda self: self.base.nt)
+    ne = property(lambda self: self.base.ne)
+
+    def vertex_stars(self):
+        return self.base.vertex_stars()
+
+    def centroids(self):
+        return self.base.centroids()
+
+    def __repr__(self):
+        return "CurvedTriangleMesh(nv=%d, nt=%d)" % (self.nv, self.nt)
+
+
+def to_curved(mesh, project_to_unit_sphere=False):
+    """One midpoint per edge (``geometry.py:204-210``): the straight edge
+    midpoint, optionally projected onto the unit sphere."""
+    v, e = mesh.vertices, mesh.edges
+    mid = 0.5 * (v[e[:, 0]] + v[e[:, 1]])
+    if project_to_unit_sphere:
+        mid = mid / np.linalg.norm(mid, axis=1, keepdims=True)
+    return CurvedTriangleMesh(mesh, mid)
+
+
 def chart_pack(mesh):
-    """Build and cache the plane :class:`ChartPack` of ``mesh``
-    (``geometry.py:266-293``)."""
+    """Build and cache the :class:`ChartPack` of ``mesh``
+    (``geometry.py:266-293``): plane charts (constant normal and Gramian)
+    or quadratic charts of a :class:`CurvedTriangleMesh` (normals at the six
+    nodes, no constant Gramian)."""
     if getattr(mesh, "_pack", None) is not None:
         return mesh._pack
+    if isinstance(mesh, CurvedTriangleMesh):
+        nodes = np.empty((mesh.nt, 6, 3))
+        nodes[:, :3] = mesh.vertices[mesh.triangles]
+        nodes[:, 3:] = mesh.midpoints[mesh.tri_edges]
+        grads = _shape_gradients_at_nodes()                 # (6 nodes, 6 shapes, 2)
+        du = np.einsum("ma,tac->tmc", grads[:, :, 0], nodes)
+        dv = np.einsum("ma,tac->tmc", grads[:, :, 1], nodes)
+        mesh._pack = ChartPack(np.ascontiguousarray(nodes), np.ascontiguousarray(np.cross(du, dv)),
+                               None, True)
+        return mesh._pack
     if not isinstance(mesh, TriangleMesh):
-        raise ConfigError("only plane TriangleMesh geometry is supported")
+        raise ConfigError("unsupported mesh type %r" % (type(mesh).__name__,))
     corners = mesh.vertices[mesh.triangles]
     nodes = np.empty((mesh.nt, 6, 3))
     nodes[:, :3] = corners
@@ -275,9 +328,25 @@ def chart_eval(mesh, triangle, xhat):
 
 
 def surface_area(mesh, quad_order=4):
+    """Integral of the Gramian over all charts (``geometry.py:341-352``)."""
     from .quadrature import triangle_gauss
-    _, w = triangle_gauss(quad_order)
-    return float(w.sum() * chart_pack(mesh).gram.sum())
+    pts, w = triangle_gauss(quad_order)
+    pack = chart_pack(mesh)
+    if not pack.curved:
+        return float(w.sum() * pack.gram.sum())
+    normals = np.einsum("ma,tac->tmc", shape_functions(pts), pack.normals)
+    return float((np.linalg.norm(normals, axis=2) @ w).sum())
+
+
+def point_gramians(mesh, pts):
+    """Per-triangle Gramians at reference points ``pts`` (nt, M): |n| of the
+    interpolated chart normal (``assembly.py:371-381`` for curved charts);
+    the plane Gramian repeated for plane charts."""
+    pack = chart_pack(mesh)
+    if not pack.curved:
+        return np.repeat(pack.gram[:, None], len(pts), axis=1)
+    normals = np.einsum("ma,tac->tmc", shape_functions(pts), pack.normals)
+    return np.sqrt(normals[..., 0] ** 2 + normals[..., 1] ** 2 + normals[..., 2] ** 2)
 
 
 # --------------------------------------------------------------------------

@@ -140,9 +140,46 @@ def pair_values(dmesh, kind, rules, rows, cols, device):
         _native.call("gc_lin_pairs", dmesh.geom_of(kind), rules.w.ctypes.data, rules.b.ctypes.data, n,
                      ptr(tasks), ptr(U), ptr(pp), q.struct, ptr(q.flags), st)
         counts = (_native.c_i64 * 4)()
-        _native.call("gc_lin_singular", dmesh.geom_of(kind), rules.struct, q.struct, ptr(U), counts, st)
+        _flush(dmesh, kind, rules, q, U, counts, st)
     q.check()
     return U.cpu().numpy().reshape(n, 3, 3)
+
+
+def _flush(dmesh, kind, rules, q, U, counts, st):
+    """Singular pairs of a batch: affine charts with the full rules
+    (gc_lin_singular), curved charts evaluated point by point
+    (gc_curved_singular)."""
+    if dmesh.curved:
+        _native.call("gc_curved_singular", dmesh.geom_of(kind), rules.struct, q.struct, 9, ptr(U), counts, st)
+    else:
+        _native.call("gc_lin_singular", dmesh.geom_of(kind), rules.struct, q.struct, ptr(U), counts, st)
+
+
+def curved_evaluator(dmesh, kind, q_reg, q_sing, width, device):
+    """Evaluator seam on curved charts: every case (the disjoint tensor rule
+    included) through gc_curved_pairs; values (B,1,1) or (B,3,3)."""
+    lr = LinearRules.get(q_reg, q_sing, device)
+    pts, wts = triangle_gauss(q_reg)
+    m = len(wts)
+    x, y = np.repeat(pts, m, axis=0), np.tile(pts, (m, 1))
+    reg = to_dev(np.concatenate([x[:, 0], x[:, 1], y[:, 0], y[:, 1], np.outer(wts, wts).ravel()]), device)
+
+    def evaluate(case, rows, cols, px, py):
+        case = int(case)
+        if case not in (0, 1, 2, 3):
+            raise ConfigError("unknown pair case %r" % (case,))
+        n = len(rows)
+        pk = np.asarray(px, np.int64) | (np.asarray(py, np.int64) << 8)
+        tasks = to_dev(np.stack([np.asarray(rows, np.int64), np.asarray(cols, np.int64), pk,
+                                 np.arange(n, dtype=np.int64)], 1), device)
+        table, P = (reg, m * m) if case == 0 else (lr.tables[case], int(lr.struct.npts[case]))
+        out = empty(width * max(n, 1), device)
+        with torch.cuda.device(device):
+            _native.call("gc_curved_pairs", dmesh.geom_of(kind), ptr(table), P, ptr(tasks), n, width, ptr(out),
+                         stream_handle())
+        return out[:width * n].cpu().numpy().reshape(n, 1 if width == 1 else 3, 1 if width == 1 else 3)
+
+    return evaluate
 
 
 def assemble_blocks(dmesh, kind, rules, mesh, blocks, out, device):
@@ -200,7 +237,7 @@ def _run_batch(dmesh, kind, rules, batch, ntask, out, device, totals):
         _native.call("gc_lin_pairs", dmesh.geom_of(kind), rules.w.ctypes.data, rules.b.ctypes.data, ntask,
                      ptr(d_tasks), ptr(U), ptr(pp), q.struct, ptr(q.flags), st)
         counts = (_native.c_i64 * 4)()
-        _native.call("gc_lin_singular", dmesh.geom_of(kind), rules.struct, q.struct, ptr(U), counts, st)
+        _flush(dmesh, kind, rules, q, U, counts, st)
         _native.call("gc_lin_gather", len(batch), ptr(d[0]), ptr(d[1]), ptr(d[2]), ptr(d[3]), ptr(d[4]),
                      ptr(U), ptr(pp), ptr(out), st)
     q.check()

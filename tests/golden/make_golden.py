@@ -299,6 +299,66 @@ def main_collocation():
     np.savez_compressed(os.path.join(OUT, "h2_colloc_sphere3_eps1e-4.npz"), **res)
 
 
+def curved_pipeline(mesh, basis, eps, seed):
+    tree = C.build_cluster_tree(mesh, basis, 16)
+    bt = C.build_block_tree(tree, eta=1.0)
+    rm, cm = GC.coupling_marks(bt)
+    rb = GC.build_cluster_basis(tree, mesh, basis, 3, 0.5, eps, "row", (3, 5), rm)
+    cb = GC.build_cluster_basis(tree, mesh, basis, 3, 0.5, eps, "col", (3, 5), cm)
+    hm = GC.build_h2(bt, rb, cb, mesh, "slp", basis, "galerkin", (3, 5))
+    nodes = tree.nodes()
+    out = dict(perm=tree.perm.astype(np.int32),
+               lower=np.array([n.box.lower for n in nodes]), upper=np.array([n.box.upper for n in nodes]))
+    for side, b in (("row", rb), ("col", cb)):
+        bns = b.nodes()
+        out[side + "_node"] = np.array([x.cluster.index for x in bns], np.int32)
+        out[side + "_rank"] = np.array([x.rank for x in bns], np.int32)
+        out[side + "_piv"] = np.concatenate([x.pivots for x in bns]).astype(np.int32)
+    rng = np.random.default_rng(seed)
+    fl = [n for n in nodes if n.is_leaf()]
+    pick = rng.choice(len(fl), 3, replace=False)
+    facs = []
+    for i in pick:
+        node = fl[i]
+        rule = Q.green_box_rule(node.box, 0.5 * node.box.diameter(), 3)
+        facs.append(A.green_row_factor(node, rule, mesh, basis, (3, 5)).ravel())
+    out["factor_nodes"] = np.array([fl[i].index for i in pick], np.int32)
+    out["factors"] = np.concatenate(facs)
+    n = mesh.nt if basis == "constant" else mesh.nv
+    x = rng.standard_normal((2, n))
+    out["x"] = x
+    out["mvm"] = np.array([H.mvm(hm, v) for v in x])
+    return out
+
+
+def main_curved():
+    c3 = G.to_curved(G.build_sphere_mesh(3), project_to_unit_sphere=True)
+    c2 = G.to_curved(G.build_sphere_mesh(2), project_to_unit_sphere=True)
+    out = {}
+    g = pair_tasks(c3, 300, 61)
+    out.update({"rows": g["rows"], "cols": g["cols"], "case": g["case"], "px": g["px"], "py": g["py"]})
+    for kind in ("slp", "dlp"):
+        for basis, w in (("constant", 1), ("linear", 3)):
+            ev = A.galerkin_pair_evaluator(kind, c3, basis, 3, 5)
+            vals = np.empty((len(g["rows"]), w, w))
+            for k in range(4):
+                m = g["case"] == k
+                vals[m] = ev(k, g["rows"][m], g["cols"][m], g["px"][m], g["py"][m])
+            out["%s_%s" % (kind, basis)] = vals
+    np.savez_compressed(os.path.join(OUT, "curved_pairs_sphere3.npz"), **out)
+    idx, dofs = np.arange(c2.nt), np.arange(c2.nv)
+    np.savez_compressed(os.path.join(OUT, "curved_dense_sphere2.npz"),
+                        slp_constant=A.assemble_galerkin_block("slp", c2, "constant", idx, idx).values,
+                        dlp_linear=A.assemble_galerkin_block("dlp", c2, "linear", dofs, dofs).values,
+                        colloc_dlp=A.assemble_collocation_block("dlp", c2, "linear", dofs, dofs).values,
+                        mass_linear=A.mass_block(c2, "linear", dofs, dofs).values)
+    np.savez_compressed(os.path.join(OUT, "curved_h2_constant_sphere3.npz"),
+                        **curved_pipeline(c3, "constant", 1e-4, 62))
+    c4 = G.to_curved(G.build_sphere_mesh(4), project_to_unit_sphere=True)
+    np.savez_compressed(os.path.join(OUT, "curved_h2_linear_sphere4.npz"),
+                        **curved_pipeline(c4, "linear", 1e-4, 63))
+
+
 def main_dlp():
     s3 = G.build_sphere_mesh(3)
     np.savez_compressed(os.path.join(OUT, "pairs_dlp_sphere3.npz"), **pair_tasks(s3, 600, 31, "dlp"))
@@ -338,5 +398,7 @@ if __name__ == "__main__":
         main_linear_h2()
     elif "--collocation" in sys.argv:
         main_collocation()
+    elif "--curved" in sys.argv:
+        main_curved()
     else:
         main()

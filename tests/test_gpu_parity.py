@@ -621,3 +621,73 @@ def test_collocation_h2_vs_reference():
             o += b.rank
     for x, y in zip(g["x"], g["mvm"]):
         assert np.linalg.norm(h2.mvm(hm, x) - y) <= 1e-12 * np.linalg.norm(y)
+
+
+# ---------------------------------------------------------------- curved charts
+
+def _curved(level):
+    return geometry.to_curved(geometry.build_sphere_mesh(level), project_to_unit_sphere=True)
+
+
+def test_curved_pair_evaluator_seam():
+    g = golden("curved_pairs_sphere3.npz")
+    mesh = _curved(3)
+    for kind in ("slp", "dlp"):
+        for basis in ("constant", "linear"):
+            ref = g["%s_%s" % (kind, basis)]
+            ev = assembly.galerkin_pair_evaluator(kind, mesh, basis, 3, 5)
+            scale = np.max(np.abs(ref))
+            for k in range(4):
+                m = g["case"] == k
+                got = ev(k, g["rows"][m], g["cols"][m], g["px"][m], g["py"][m])
+                assert got.shape == ref[m].shape
+                assert np.max(np.abs(got - ref[m])) <= 1e-12 * scale, (kind, basis, k)
+
+
+def test_curved_dense_blocks():
+    g = golden("curved_dense_sphere2.npz")
+    mesh = _curved(2)
+    idx, dofs = np.arange(mesh.nt), np.arange(mesh.nv)
+    d = assembly.assemble_galerkin_block("slp", mesh, "constant", idx, idx).values
+    assert rel(d, g["slp_constant"]) < 1e-12
+    d = assembly.assemble_galerkin_block("dlp", mesh, "linear", dofs, dofs).values
+    assert rel(d, g["dlp_linear"]) < 1e-12
+    d = assembly.assemble_collocation_block("dlp", mesh, "linear", dofs, dofs).values
+    assert rel(d, g["colloc_dlp"]) < 1e-10
+    # interior Gauss identity on the curved sphere (test_assembly.py:93-104):
+    # (M/2 + K) 1 = 0 to O(h^2)
+    k = assembly.assemble_galerkin_block("dlp", _curved(3), "linear", np.arange(258), np.arange(258)).values
+    assert np.abs(k.sum(axis=1)).max() > 0
+    m2 = g["mass_linear"]
+    k2 = assembly.assemble_galerkin_block("dlp", mesh, "linear", dofs, dofs).values
+    r = (0.5 * m2 + k2) @ np.ones(mesh.nv)
+    assert np.linalg.norm(r) / np.linalg.norm(m2 @ np.ones(mesh.nv)) < 2e-5
+
+
+@pytest.mark.parametrize("basis,level,name", [("constant", 3, "curved_h2_constant_sphere3.npz"),
+                                              ("linear", 4, "curved_h2_linear_sphere4.npz")])
+def test_curved_h2_vs_reference(basis, level, name):
+    g = golden(name)
+    mesh = _curved(level)
+    cfg = cli.default_config(eps=1e-4, basis=basis)
+    hm, tree, bt = cli.build_h2_operator(mesh, cfg)
+    assert np.array_equal(tree.perm, g["perm"])
+    off = 0
+    for i in g["factor_nodes"]:
+        node = tree.flat.node(int(i))
+        rule = Q.green_box_rule(node.box, 0.5 * node.box.diameter(), 3)
+        a = assembly.green_row_factor(node, rule, mesh, basis)
+        ref = g["factors"][off:off + a.size].reshape(a.shape)
+        off += a.size
+        assert np.max(np.abs(a - ref)) <= 1e-13 * np.max(np.abs(ref))
+    for side, b in (("row", hm.row_basis), ("col", hm.col_basis)):
+        nodes = list(b.nodes())
+        assert [x.rank for x in nodes] == g[side + "_rank"].tolist()
+        got = np.concatenate([x.pivots for x in nodes])
+        ref = g[side + "_piv"]
+        o = 0
+        for x in nodes:
+            assert set(got[o:o + x.rank]) == set(ref[o:o + x.rank])
+            o += x.rank
+    for x, y in zip(g["x"], g["mvm"]):
+        assert np.linalg.norm(h2.mvm(hm, x) - y) <= 1e-12 * np.linalg.norm(y)

@@ -237,3 +237,46 @@ def test_collocation_values_and_blocks_bitwise():
     assert np.array_equal(P.block_collocation(n2, g2, s2.vertices, s2.triangles, dofs, dofs), d["slp"])
     assert np.array_equal(P.block_collocation(n2, g2, s2.vertices, s2.triangles, dofs, dofs, kind="dlp",
                                               normals=nn2), d["dlp"])
+
+
+# ---------------------------------------------------------------- curved charts
+
+def _curved3():
+    from paper_1810_08429_b200.geometry import to_curved
+    return to_curved(build_sphere_mesh(3), project_to_unit_sphere=True)
+
+
+def test_curved_pair_values_bitwise():
+    """Curved (quadratic) charts: pair integrals with point Gramians from the
+    interpolated node normals (assembly.py:189-205), all four cases, both
+    kernels and bases."""
+    g = golden("curved_pairs_sphere3.npz")
+    m = _curved3()
+    nodes, normals = P.chart_curved(m.vertices, m.triangles, m.midpoints, m.tri_edges)
+    for kind in ("slp", "dlp"):
+        for k in range(4):
+            sel = g["case"] == k
+            args = (nodes, None, k, g["rows"][sel], g["cols"][sel], g["px"][sel], g["py"][sel])
+            got = P.pair_values(*args, kind=kind, normals=normals)
+            assert np.array_equal(got, g["%s_constant" % kind][sel][:, 0, 0]), (kind, k)
+            got = P.pair_values_linear(*args, kind=kind, normals=normals)
+            assert np.array_equal(got, g["%s_linear" % kind][sel]), (kind, k)
+
+
+def test_curved_chart_pack_and_trees_bitwise():
+    """Host curved geometry (to_curved, chart_pack, control points) and the
+    cluster trees built on it, constant and linear, vs the reference."""
+    from paper_1810_08429_b200 import clustering, geometry
+    m = _curved3()
+    pack = geometry.chart_pack(m)
+    nodes, normals = P.chart_curved(m.vertices, m.triangles, m.midpoints, m.tri_edges)
+    assert np.array_equal(pack.nodes, nodes) and np.array_equal(pack.normals, normals)
+    g = golden("curved_h2_constant_sphere3.npz")
+    t = clustering.build_cluster_tree(m, "constant", 16)
+    assert np.array_equal(t.perm, g["perm"])
+    assert np.array_equal(t.flat.lower, g["lower"]) and np.array_equal(t.flat.upper, g["upper"])
+    m4 = geometry.to_curved(build_sphere_mesh(4), project_to_unit_sphere=True)
+    g = golden("curved_h2_linear_sphere4.npz")
+    t = clustering.build_cluster_tree(m4, "linear", 16)
+    assert np.array_equal(t.perm, g["perm"])
+    assert np.array_equal(t.flat.lower, g["lower"]) and np.array_equal(t.flat.upper, g["upper"])

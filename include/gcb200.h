@@ -220,7 +220,8 @@ int gc_segmv(int64_t nseg, const int64_t* seg, const int64_t* blk,
  * serialization (PDL): the kernel prefetches its matrix chunk while the
  * previous kernel on the stream drains and waits for it before reading in
  * (for the latency-bound transform levels); chain = 1 releases the next
- * launch at each CTA's start, chain = 2 after each CTA's item.  priority != 0 sets the
+ * launch at each CTA's start, chain = 2 after each CTA's item; chain | 4
+ * runs one warp per item (whole panels of <= 256 rows, 8 per CTA).  priority != 0 sets the
  * launch's scheduling priority (CUDA stream-priority scale, lower = more
  * urgent; 0 = the stream's own).  trace (optional, NULL = off)
  * = [dev] 2 x uint64 receiving min(start) / max(end) %globaltimer (ns) of

@@ -53,6 +53,7 @@ _SIGNATURES = {
     "gc_aca": [c_i64, c_p, c_i64, ctypes.c_double, c_i64, c_p, c_p, c_p, c_p, c_p, c_i64, c_p],
     "gc_gather": [c_p, c_p, c_i64, c_p, c_p],
     "gc_scatter": [c_p, c_p, c_i64, c_p, c_p],
+    "gc_scatter2": [c_p, c_p, c_p, c_i64, c_p, c_p],
     "gc_segmv": [c_i64, c_p, c_p, c_p, c_p, c_p, c_p, c_p, ctypes.c_int, c_i64, c_p],
     "gc_panelmv": [c_i64, c_p, c_p, c_p, c_p, c_p, c_p, c_p, c_p, c_i64, c_p, c_p, ctypes.c_int32,
                    ctypes.c_int32, c_p, c_p],

@@ -657,6 +657,25 @@ __device__ void warp_item(const PanelPhase& P, int64_t item, double* xs, int lan
     if (lane == 0) P.arrivals[slot] = 0;
 }
 
+// One warp per item (a whole small panel: the many tiny panels of the
+// lower transform levels - leaf bases of 16 rows, sibling transfers): 8
+// items per CTA instead of one, so a level of 2048 panels is 256 CTAs.
+// CHAIN: programmatic dependent launch as in k_panelmv.
+template <bool CHAIN>
+__global__ void __launch_bounds__(PAN_THREADS) k_panel_warp(PanelPhase P) {
+    __shared__ double xs[PAN_THREADS / 32][WARP_MAX_ROWS];
+    if (CHAIN) asm volatile("griddepcontrol.launch_dependents;");
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    const int64_t item = (int64_t)blockIdx.x * (PAN_THREADS / 32) + warp;
+    if (P.trace != nullptr && threadIdx.x == 0) atomicMin(P.trace, globaltimer());
+    if (CHAIN) asm volatile("griddepcontrol.wait;" ::: "memory");
+    if (item < P.nitems) warp_item(P, item, xs[warp], lane);
+    if (P.trace != nullptr) {
+        __syncthreads();
+        if (threadIdx.x == 0) atomicMax(P.trace + 1, globaltimer());
+    }
+}
+
 // A run of consecutive chain phases (transform levels) in ONE co-resident
 // launch: warps stride over each phase's items, prefetch their items of
 // the next phase into L2, and the grid meets at a barrier between phases.
@@ -719,7 +738,7 @@ extern "C" int gc_panelmv(int64_t nitems, const int64_t* items, const int32_t* x
     cfg.stream = (cudaStream_t)stream;
     cudaLaunchAttribute attr[2];
     int na = 0;
-    if (chain) {
+    if (chain & 3) {
         attr[na].id = cudaLaunchAttributeProgrammaticStreamSerialization;
         attr[na].val.programmaticStreamSerializationAllowed = 1;
         ++na;
@@ -731,9 +750,17 @@ extern "C" int gc_panelmv(int64_t nitems, const int64_t* items, const int32_t* x
     }
     cfg.attrs = attr;
     cfg.numAttrs = na;
-    cudaError_t e = chain == 1   ? cudaLaunchKernelEx(&cfg, k_panelmv<true, 1>, P)
-                    : chain == 2 ? cudaLaunchKernelEx(&cfg, k_panelmv<true, 2>, P)
-                                 : cudaLaunchKernelEx(&cfg, k_panelmv<false, 0>, P);
+    cudaError_t e;
+    if (chain & 4) {
+        // warp-granular items (whole panels of <= WARP_MAX_ROWS rows)
+        cfg.gridDim = dim3((unsigned)((nitems + PAN_THREADS / 32 - 1) / (PAN_THREADS / 32)));
+        e = (chain & 3) ? cudaLaunchKernelEx(&cfg, k_panel_warp<true>, P)
+                        : cudaLaunchKernelEx(&cfg, k_panel_warp<false>, P);
+    } else {
+        e = chain == 1   ? cudaLaunchKernelEx(&cfg, k_panelmv<true, 1>, P)
+          : chain == 2 ? cudaLaunchKernelEx(&cfg, k_panelmv<true, 2>, P)
+                       : cudaLaunchKernelEx(&cfg, k_panelmv<false, 0>, P);
+    }
     if (e != cudaSuccess) return cuda_status(e, "k_panelmv");
     count_launch();
     return GC_OK;

@@ -43,6 +43,14 @@ __global__ void k_scatter(const double* __restrict__ yt, const int64_t* __restri
         y[__ldg(perm + i)] = yt[i];
 }
 
+// y[perm[i]] = yt[i] + yt2[i]
+__global__ void k_scatter2(const double* __restrict__ yt, const double* __restrict__ yt2,
+                           const int64_t* __restrict__ perm, int64_t n, double* __restrict__ y) {
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
+         i += (int64_t)gridDim.x * blockDim.x)
+        y[__ldg(perm + i)] = yt[i] + yt2[i];
+}
+
 // xq[t,m,c] = sum_a n6[m,a] * node[t,a,c], sequential, no contraction; nodes
 // 3..5 are the straight midpoints 0.5*(p_i + p_j) (geometry.py:278-280).
 __global__ void k_surface_points(const double* __restrict__ corners, int64_t nt,
@@ -123,6 +131,14 @@ int gc_scatter(const double* yt, const int64_t* perm, int64_t n, double* y, void
     if (n <= 0) return GC_OK;
     k_scatter<<<grid_for(n, 256), 256, 0, (cudaStream_t)stream>>>(yt, perm, n, y);
     GC_CHECK_LAUNCH("gc_scatter");
+    return GC_OK;
+}
+
+int gc_scatter2(const double* yt, const double* yt2, const int64_t* perm, int64_t n, double* y,
+                void* stream) {
+    if (n <= 0) return GC_OK;
+    k_scatter2<<<grid_for(n, 256), 256, 0, (cudaStream_t)stream>>>(yt, yt2, perm, n, y);
+    GC_CHECK_LAUNCH("gc_scatter2");
     return GC_OK;
 }
 

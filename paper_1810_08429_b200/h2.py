@@ -446,7 +446,7 @@ _STREAM_MAX_T = 1024        # ST_MAX_T in csrc/h2mv.cu
 
 class _Phase:
     __slots__ = ("name", "height", "items", "xidx", "red", "arrivals", "nitems", "nred", "A0", "A1",
-                 "in0", "in1", "out", "scratch", "bytes", "cta", "in_elems", "out_elems", "tma")
+                 "in0", "in1", "out", "scratch", "bytes", "cta", "in_elems", "out_elems", "tma", "warp")
 
 
 class _Node:
@@ -492,6 +492,7 @@ class PanelPlan:
         self.y = torch.zeros(self.n_out, **f64)
         self.xt = torch.zeros(self.n_in, **f64)
         self.yt = torch.zeros(self.n_out, **f64)
+        self.yt2 = torch.zeros(self.n_out, **f64)     # leaf-basis part, summed in the scatter
         self.xhat = torch.zeros(max(cs.coef_size, 1), **f64)
         self.yhat = torch.zeros(max(rs.coef_size, 1), **f64)
         # "pdl": one launch per transform level; "persistent": runs of levels
@@ -506,6 +507,9 @@ class PanelPlan:
         # chain launches: 0 = plain, 1 = PDL released at CTA start, 2 = PDL
         # released after each CTA's item
         self._pdl = int(os.environ.get("GC_CHAIN_PDL", "1"))
+        # transform levels with at least this many panels run one warp per panel
+        # (168 us vs 144 us for the full C2 product: kept as an option)
+        self._warp_min_panels = int(os.environ.get("GC_WARP_MIN_PANELS", str(1 << 40)))   # off: measured slower
         grid = _native.ctypes.c_int64(0)
         _native.call("gc_panel_chain_grid", _native.ctypes.byref(grid))
         self._chain_grid = grid.value
@@ -569,7 +573,9 @@ class PanelPlan:
         if leaves.size:
             K = rs.rank[leaves]
             panels = (rs.v_off[leaves], K, size_r[leaves], _ranges_np(rs.coef_off[leaves], K), rf.start[leaves], 1)
-            leafp = self._phase("leafbasis", 0, panels, rs.VT, None, self.yhat, None, self.yt,
+            # into yt2 (overwritten): the leaf basis need not wait for the near field
+            panels = panels[:5] + (0,)
+            leafp = self._phase("leafbasis", 0, panels, rs.VT, None, self.yhat, None, self.yt2,
                                 transform=True)
         self._fwd, self._cpl, self._bwd, self._near, self._leaf = fwd, cpl, bwd, near, leafp
         self.phases = [P for P in [near] + fwd + [c for c, _ in cpl] + [b for b, _ in bwd] + [leafp]
@@ -695,13 +701,15 @@ class PanelPlan:
             k = add_steps("backward", [P for P, _ in grp], [prev] + [bucket[x] for x in need if x in bucket])
             if k is not None:
                 prev = k
-        tail = [prev] + list(bucket.values()) + ([near] if near is not None else [])
+        tail = [prev] + list(bucket.values())
         if self._leaf is not None and self._leaf.nitems:
             prev = add(_Node("leafbasis", "chain", tail, phase=self._leaf, priority=greatest))
             tail = [prev]
+        if near is not None:
+            tail = tail + [near]
         if scatter:
             k = add(_Node("scatter", "chain", tail, fn=lambda: _native.call(
-                "gc_scatter", ptr(self.yt), ptr(self.perm_out), self.n_out, ptr(self.y), st())))
+                "gc_scatter2", ptr(self.yt), ptr(self.yt2), ptr(self.perm_out), self.n_out, ptr(self.y), st())))
             nodes[k].launches = 1
         else:
             add(_Node("join", "chain", tail, fn=lambda: None))
@@ -820,6 +828,9 @@ class PanelPlan:
                                 dtype=torch.float64, device=self.dev)
         P.bytes = 8 * elems
         P.in_elems, P.out_elems = int(K.sum()), int(T.sum())
+        # many small whole panels (lower transform levels): one warp each
+        P.warp = bool(transform and n >= self._warp_min_panels and len(items) == n
+                      and int(K.max()) <= _WARP_MAX_ROWS)
         P.cta = None
         P.tma = bool(not transform and self.bulk_kernel == "tma" and n and int(T.max()) <= self._tma_elems)
         if (not transform and n and int(T.max()) <= _STREAM_MAX_T and self._stream_grid > 0
@@ -844,10 +855,10 @@ class PanelPlan:
                          ptr(P.in0), ptr(P.in1), ptr(P.out), ptr(P.scratch), P.nred, ptr(P.red),
                          ptr(P.arrivals), int(priority), ptr(self.trace.get(id(P))), stream)
             return
+        mode = (self._pdl if chain else 0) | (4 if P.warp else 0)
         _native.call("gc_panelmv", P.nitems, ptr(P.items), ptr(P.xidx), ptr(P.A0), ptr(P.A1),
                      ptr(P.in0), ptr(P.in1), ptr(P.out), ptr(P.scratch), P.nred, ptr(P.red),
-                     ptr(P.arrivals), self._pdl if chain else 0, int(priority), ptr(self.trace.get(id(P))),
-                     stream)
+                     ptr(P.arrivals), mode, int(priority), ptr(self.trace.get(id(P))), stream)
 
     def _body(self, phase_events=None, phase="coupling"):
         self._exec(self.nodes, serial=phase_events is not None, phase_events=phase_events, phase=phase)

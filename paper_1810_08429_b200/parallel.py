@@ -221,7 +221,7 @@ def _shard_plan_class():
         def run(self, x_slice):
             all_gather_into(self.xt, x_slice.contiguous(), self.sh.group)
             self._exec(self.nodes)
-            return self.yt[self.lo:self.hi].clone()
+            return self.yt[self.lo:self.hi] + self.yt2[self.lo:self.hi]
 
     return ShardPlan
 

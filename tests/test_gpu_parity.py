@@ -341,7 +341,8 @@ def test_other_quadrature_orders_vs_oracle(q):
 
 @pytest.mark.parametrize("env", [
     {"GC_BULK_KERNEL": "tma"}, {"GC_BULK_KERNEL": "stream"}, {"GC_CHAIN_PDL": "0"},
-    {"GC_CHAIN_PDL": "2"}, {"GC_CHAIN_MODE": "persistent"}, {"GC_ITEM_ELEMS": "1024"}])
+    {"GC_CHAIN_PDL": "2"}, {"GC_CHAIN_MODE": "persistent"}, {"GC_ITEM_ELEMS": "1024"},
+    {"GC_WARP_MIN_PANELS": "1"}])
 def test_matvec_schedule_variants_agree(env, monkeypatch):
     """Every product schedule / bulk kernel variant (h2.PanelPlan) gives the
     default plan's result: bitwise where only the schedule changes, <= 1e-14

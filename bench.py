@@ -261,12 +261,22 @@ def run_native(args):
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
-    torch.cuda.set_device(local)
+    # one rank per GPU; GC_DIST_BACKEND=gloo runs the N > 1 path functionally
+    # with several ranks sharing fewer GPUs (host-staged collectives)
+    backend = os.environ.get("GC_DIST_BACKEND", "nccl")
+    dev_index = local % max(torch.cuda.device_count(), 1) if backend != "nccl" else local
+    torch.cuda.set_device(dev_index)
     if world > 1:
         import torch.distributed as dist
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        if backend == "nccl":
+            dist.init_process_group("nccl", device_id=torch.device("cuda", dev_index))
+        else:
+            dist.init_process_group(backend)
         from paper_1810_08429_b200 import parallel
-        return parallel.bench_distributed(args, rank, world, local, METRIC, workload(args))
+        peaks = json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json"))) \
+            if os.path.exists(os.path.join(ROOT, "MEASURED_PEAKS.json")) else {}
+        return parallel.bench_distributed(args, rank, world, dev_index, METRIC, workload(args),
+                                          clock_sampler=ClockSampler, peaks=peaks)
     mesh = (geometry.build_sphere_mesh(args.level) if args.geometry == "sphere"
             else geometry.build_cube_mesh(args.level))
     cfg = cli.default_config(level=args.level, eps=args.eps)

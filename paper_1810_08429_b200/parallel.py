@@ -125,6 +125,25 @@ class ShardedH2:
         with torch.cuda.device(self.plan.dev):
             return self.plan.run(x_slice)
 
+    def mvm(self, x_slice):
+        """Host-facing product: this rank's slice of x (numpy, tree order) in,
+        its slice of y out, through pinned staging buffers."""
+        import numpy as np
+        import torch
+        x_slice = np.ascontiguousarray(x_slice, dtype=np.float64)
+        if x_slice.shape != (self.layout.hi - self.layout.lo,):
+            raise ConfigError("slice of length %d, shard owns %d rows"
+                              % (x_slice.size, self.layout.hi - self.layout.lo))
+        if getattr(self, "_pin", None) is None:
+            self._pin = (torch.empty(x_slice.size, dtype=torch.float64).pin_memory(),
+                         torch.empty(x_slice.size, dtype=torch.float64).pin_memory())
+        xin, yout = self._pin
+        xin.numpy()[:] = x_slice
+        y = self.mvm_local(xin.to("cuda", non_blocking=True))
+        yout.copy_(y, non_blocking=True)
+        torch.cuda.current_stream().synchronize()
+        return yout.numpy().copy()
+
 
 def build_sharded_operator(mesh, cfg, group=None, device=None, timings=None):
     """Trees, block tree, own bases, allgathered column pivots and the own
@@ -230,16 +249,21 @@ def ShardPlan(sh):
     return _shard_plan_class()(sh)
 
 
-def bench_distributed(args, rank, world, local, metric, workload):
+def bench_distributed(args, rank, world, local, metric, workload, clock_sampler=None, peaks=None):
     """bench.py at N > 1: the same workload sharded by block rows, strong
-    scaling; time = max over ranks of CUDA-event time per product."""
+    scaling; time = max over ranks of CUDA-event time per product.  Also
+    reports the end-to-end product through ``ShardedH2.mvm`` (host slice in,
+    host slice out), the own-kernel launch count, clocks sampled during the
+    timed region (rank 0's GPU) and rank 0's dominant launch roofline."""
     import json
     import time
 
+    import numpy as np
     import torch
     import torch.distributed as dist
 
-    from . import cli, geometry, h2
+    from . import _native, cli, geometry, h2
+    from .device import stream_handle
     mesh = (geometry.build_sphere_mesh(args.level) if args.geometry == "sphere"
             else geometry.build_cube_mesh(args.level))
     cfg = cli.default_config(level=args.level, eps=args.eps)
@@ -257,21 +281,79 @@ def bench_distributed(args, rank, world, local, metric, workload):
                         dtype=torch.float64, device="cuda")
     dist.all_reduce(mine)
     n = mesh.nt
-    nbytes = float(mine.item()) / 1.0 + 16 * n
-    x = torch.randn(sh.layout.hi - sh.layout.lo, dtype=torch.float64, device="cuda")
+    nbytes = float(mine.item()) + 16 * n
+    m_own = sh.layout.hi - sh.layout.lo
+    x = torch.randn(m_own, dtype=torch.float64, device="cuda")
     for _ in range(args.warmup):
         sh.mvm_local(x)
     torch.cuda.synchronize()
     dist.barrier()
+    sampler = clock_sampler(local) if (clock_sampler is not None and rank == 0) else None
+    if sampler is not None:
+        sampler.__enter__()
+    # ~1 s of products under the clock sampler, then the timed steps
+    flag = torch.ones(1, dtype=torch.float64, device="cuda")
+    w0 = time.perf_counter()
+    while True:
+        for _ in range(20):
+            sh.mvm_local(x)
+        torch.cuda.synchronize()
+        flag.fill_(1.0 if time.perf_counter() - w0 < 1.0 else 0.0)
+        dist.all_reduce(flag, op=dist.ReduceOp.MIN)       # every rank stops together
+        if flag.item() == 0.0:
+            break
+    dist.barrier()
+    l0 = _native.launch_count()
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     e0.record()
     for _ in range(args.steps):
         sh.mvm_local(x)
     e1.record()
     torch.cuda.synchronize()
+    launches = torch.tensor([_native.launch_count() - l0], dtype=torch.float64, device="cuda")
     t = torch.tensor([e0.elapsed_time(e1) * 1e-3 / args.steps], dtype=torch.float64, device="cuda")
     dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    dist.all_reduce(launches)
     dist.barrier()
+    if sampler is not None:
+        sampler.__exit__(None, None, None)
+    # end to end through the public sharded API: host slice -> product -> host slice
+    xh = np.random.default_rng(rank).standard_normal(m_own)
+    for _ in range(3):
+        sh.mvm(xh)
+    torch.cuda.synchronize()
+    dist.barrier()
+    k_e2e = max(10, args.steps // 2)
+    w0 = time.perf_counter()
+    for _ in range(k_e2e):
+        sh.mvm(xh)
+    te = torch.tensor([(time.perf_counter() - w0) / k_e2e], dtype=torch.float64, device="cuda")
+    dist.all_reduce(te, op=dist.ReduceOp.MAX)
+    # rank 0: its largest coupling bucket launched alone, L2 flushed
+    roof = None
+    if rank == 0 and sh.plan is not None:
+        p = sh.plan
+        buckets = [P for P in p.phases if P.name == "coupling"]
+        if buckets:
+            big = max(buckets, key=lambda P: P.bytes)
+            flush = torch.empty(32 << 20, dtype=torch.float64, device="cuda")
+            ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(5)]
+            for a_, b_ in ev:
+                flush.zero_()
+                a_.record()
+                p._launch(big, stream_handle())
+                b_.record()
+            torch.cuda.synchronize()
+            del flush
+            sec = float(np.mean([a_.elapsed_time(b_) for a_, b_ in ev])) * 1e-3
+            byts = big.bytes + 8 * big.in_elems + 8 * big.out_elems
+            hbm = (peaks or {}).get("hbm_gbs", 6650.0)
+            roof = {"bound": "hbm", "kernel": "k_panelmv, rank 0's largest coupling bucket",
+                    "achieved": round(byts / sec / 1e9, 1), "peak": hbm, "unit": "GB/s",
+                    "frac": round(byts / sec / 1e9 / hbm, 4), "traffic": None,
+                    "algorithmic_bytes_per_launch": int(byts), "avg_launch_s": sec,
+                    "step": {"achieved": round(nbytes / float(t.item()) / 1e9, 1),
+                             "frac": round(nbytes / float(t.item()) / 1e9 / hbm, 4)}}
     if rank == 0:
         s = float(t.item())
         print(json.dumps({
@@ -279,6 +361,14 @@ def bench_distributed(args, rank, world, local, metric, workload):
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(s * 1e3, 4),
             "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f64",
             "data": "synthetic", "config": dict(workload, parallelism="block-row x%d" % world),
-            "assembly": {"value": round(float(asm.item()), 4), "unit": "s"},
-            "e2e": None, "gpu_launches": None}))
+            "assembly": {"value": round(float(asm.item()), 4), "unit": "s",
+                         "phases_s": {k: round(v, 4) for k, v in timings.items()}},
+            "roofline": roof,
+            "e2e": {"value": round(nbytes / float(te.item()) / 1e9, 2), "unit": "GB/s",
+                    "h2d_bytes_per_step": 8 * n, "d2h_bytes_per_step": 8 * n,
+                    "ms_per_step": round(float(te.item()) * 1e3, 4),
+                    "api": "paper_1810_08429_b200.parallel.ShardedH2.mvm(numpy slice) on every rank"},
+            "gpu_launches": int(launches.item()),
+            "gpu_launches_note": "own kernels over all ranks in the timed region",
+            "clocks": sampler.summary() if sampler is not None else None}))
     dist.destroy_process_group()

@@ -103,15 +103,26 @@ class BasisNode:
     rank); ``pivots`` are global dof indices.  ``v`` and ``transfer`` are
     host views of the device store, copied on first access."""
 
-    __slots__ = ("cluster", "pivots", "children", "_store", "_slot", "_v", "_transfer")
+    __slots__ = ("cluster", "pivots", "_children", "_kids", "_store", "_slot", "_v", "_transfer")
 
-    def __init__(self, cluster, pivots, children, store, slot):
+    def __init__(self, cluster, pivots, children, store, slot, kids=None):
         self.cluster = cluster
         self.pivots = pivots
-        self.children = children
+        self._children = children
+        self._kids = kids              # lazy: slot -> children tuple
         self._store, self._slot = store, slot
         self._v = None
         self._transfer = None
+
+    @property
+    def children(self):
+        if self._children is None:
+            self._children = self._kids(self._slot)
+        return self._children
+
+    @children.setter
+    def children(self, value):
+        self._children = value
 
     @property
     def rank(self):
@@ -148,12 +159,49 @@ class BasisNode:
 
 
 class ClusterBasis:
-    """Nested basis over a (possibly partial) cluster tree (``gca.py:124-146``)."""
+    """Nested basis over a (possibly partial) cluster tree (``gca.py:124-146``).
+
+    Built from a device store, the per-node Python objects are created on
+    first access (a C2 basis has ~4,000 nodes; the product never needs
+    them)."""
 
     def __init__(self, roots, by_index, store=None):
-        self.roots = roots
+        self._roots = roots
+        self._root_ids = None
         self._by_index = by_index
         self.store = store
+
+    @classmethod
+    def lazy(cls, store, flat, root_ids):
+        b = cls(None, {}, store)
+        b._root_ids = [int(r) for r in root_ids]
+        b._flat = flat
+        return b
+
+    def _get(self, i):
+        bn = self._by_index.get(i)
+        if bn is None:
+            st, flat = self.store, self._flat
+            o_, r_ = st.piv_off[i], st.rank[i]
+            bn = BasisNode(flat.node(i), st.pivots_host[o_:o_ + r_], None, st, i, self._kids_of)
+            self._by_index[i] = bn
+        return bn
+
+    def _kids_of(self, i):
+        flat = self._flat
+        if flat.is_leaf[i]:
+            return ()
+        return (self._get(int(flat.left[i])), self._get(int(flat.right[i])))
+
+    @property
+    def roots(self):
+        if self._roots is None:
+            self._roots = [self._get(r) for r in self._root_ids]
+        return self._roots
+
+    @roots.setter
+    def roots(self, value):
+        self._roots = value
 
     @property
     def root(self):
@@ -162,7 +210,12 @@ class ClusterBasis:
         return self.roots[0]
 
     def node(self, cluster):
-        return self._by_index[cluster.index]
+        i = cluster.index if hasattr(cluster, "index") else int(cluster)
+        if self._root_ids is not None:
+            if not self.store.available[i] or not self.store.materialized[i]:
+                raise KeyError(i)
+            return self._get(i)
+        return self._by_index[i]
 
     def nodes(self):
         return [bn for r in self.roots for bn in r.nodes()]
@@ -469,16 +522,7 @@ def build_cluster_bases(tree, mesh, basis, m, delta_factor, eps, sides, orders=(
         st.coef_off, st.coef_size = coef_layout(flat, s.roots, st.rank)
         st.timing = {"factor_s": t_factor, "aca_s": t_aca, "total_s": time.perf_counter() - t0,
                      "shared_with": len(S)}
-        by_index = {}
-
-        def make(i, st=st, by_index=by_index):
-            kids = () if flat.is_leaf[i] else (make(int(flat.left[i])), make(int(flat.right[i])))
-            o_, r_ = st.piv_off[i], st.rank[i]
-            bn = BasisNode(flat.node(i), st.pivots_host[o_:o_ + r_], kids, st, i)
-            by_index[i] = bn
-            return bn
-
-        out.append(ClusterBasis([make(int(r)) for r in s.roots], by_index, st))
+        out.append(ClusterBasis.lazy(st, flat, s.roots))
     return out
 
 

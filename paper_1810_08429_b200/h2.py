@@ -871,9 +871,17 @@ class PanelPlan:
             self._body()                   # warm-up outside capture
         torch.cuda.current_stream().wait_stream(s)
         torch.cuda.synchronize(self.dev)
+        # capture_begin/end on a side stream directly: torch.cuda.graph()
+        # would empty the caching allocator first (and the assembly's next
+        # allocations would pay cudaMalloc again)
         g = torch.cuda.CUDAGraph()
-        with torch.cuda.graph(g):
-            self._body()
+        with torch.cuda.stream(s):
+            g.capture_begin()
+            try:
+                self._body()
+            finally:
+                g.capture_end()
+        torch.cuda.current_stream().wait_stream(s)
         torch.cuda.synchronize(self.dev)
         self.graph = g
         return g

@@ -95,11 +95,13 @@ def galerkin_pair_evaluator(kind, mesh, basis, q_reg, q_sing, device=None):
     return evaluate
 
 
-def device_block_assembly(dmesh, rules, queue, row_idx, col_idx, desc, out, stats=None, kind="slp"):
+def device_block_assembly(dmesh, rules, queue, row_idx, col_idx, desc, out, stats=None, kind="slp",
+                          d_desc=None):
     """Assemble blocks described by ``desc (nb,5)`` into the device buffer
     ``out`` (column-major per block); singular pairs are flushed at the end.
-    ``kind`` "slp" / "dlp" picks the kernel (``rules`` must match it).
-    Returns the per-case task counts."""
+    ``kind`` "slp" / "dlp" picks the kernel (``rules`` must match it);
+    ``d_desc`` is an already uploaded copy of ``desc``.  Returns the per-case
+    task counts."""
     if getattr(rules, "kind", "slp") != kind:
         raise ConfigError("rules built for %r, assembling %r" % (rules.kind, kind))
     geom = dmesh.geom_of(kind)
@@ -112,7 +114,8 @@ def device_block_assembly(dmesh, rules, queue, row_idx, col_idx, desc, out, stat
     if nb == 0:
         return [0, 0, 0, 0]
     entries = desc[:, 1] * desc[:, 3]
-    d_desc = to_dev(desc.astype(np.int64), out.device)
+    if d_desc is None:
+        d_desc = to_dev(desc.astype(np.int64), out.device)
     stream = stream_handle()
     with torch.cuda.device(out.device):
         _native.call("gc_assemble_blocks", geom, nb, ptr(d_desc), int(desc[:, 1].max()),

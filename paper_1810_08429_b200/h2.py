@@ -442,6 +442,7 @@ _ITEM_ELEMS = int(os.environ.get("GC_ITEM_ELEMS", 16384))  # ~128 KB of matrix d
 _ITEM_MAX_ROWS = 1024       # PAN_MAX_ROWS in csrc/h2mv.cu
 _WARP_MAX_ROWS = 256        # WARP_MAX_ROWS in csrc/h2mv.cu
 _STREAM_MAX_T = 1024        # ST_MAX_T in csrc/h2mv.cu
+_RESIDENT = 148 * 8         # resident k_panelmv CTAs (32 registers, 256 threads)
 
 
 class _Phase:
@@ -510,6 +511,7 @@ class PanelPlan:
         # transform levels with at least this many panels run one warp per panel
         # (168 us vs 144 us for the full C2 product: kept as an option)
         self._warp_min_panels = int(os.environ.get("GC_WARP_MIN_PANELS", str(1 << 40)))   # off: measured slower
+        self._balance_waves = os.environ.get("GC_BALANCE_WAVES", "0") == "1"
         grid = _native.ctypes.c_int64(0)
         _native.call("gc_panel_chain_grid", _native.ctypes.byref(grid))
         self._chain_grid = grid.value
@@ -786,6 +788,10 @@ class PanelPlan:
         else:
             # chunk rows so every phase has >= ~4 items per SM when it can
             target = max(256, min(_ITEM_ELEMS, elems // (148 * 4) + 1))
+            if self._balance_waves and elems > _ITEM_ELEMS * _RESIDENT:
+                # whole waves: ~k x (resident CTAs) items of <= _ITEM_ELEMS
+                waves = -(-elems // (_ITEM_ELEMS * _RESIDENT))
+                target = -(-elems // (waves * _RESIDENT))
             max_rows = _ITEM_MAX_ROWS
         if not transform and self.bulk_kernel == "tma":
             rpi = np.minimum(max_rows, np.maximum(1, target // np.maximum(T, 1)))  # fits the smem tile

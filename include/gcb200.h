@@ -313,6 +313,23 @@ int gc_col_pairs(const gc_geom* g, const double* verts, const double* reg_w, con
                  int64_t ms, const double* sing_w, const double* sing_p, int64_t n,
                  const int64_t* tasks, double* U, int32_t* pp, void* stream);
 
+/* Cluster-tree construction per depth (clustering.py:131-162): segmented
+ * support boxes box[6s..6s+5] = (min lo, max hi) over rows [start, stop)
+ * of pack [dev] (n x 9 = lo | hi | point); and one split step - the split
+ * coordinate of each dof of each splitting segment (start, len, head,
+ * axis [dev] each nseg int64; offsets [dev] nseg+1 int32 = head and end),
+ * a stable segmented sort (CUB), and pack_new[pos] = pack_old[src],
+ * perm_new[pos] = perm_old[src] (the *_new buffers start as copies);
+ * scratch keys (2 nitems doubles), vals (2 nitems int32) and temp
+ * (gc_tree_sort_bytes) are caller-owned device memory. */
+int gc_tree_boxes(int64_t nseg, const int64_t* start, const int64_t* stop, const double* pack,
+                  double* box, void* stream);
+int gc_tree_sort_bytes(int64_t nitems, int64_t nseg, int64_t* bytes);
+int gc_tree_split(int64_t nseg, const int64_t* seg_start, const int64_t* seg_len, const int64_t* seg_head,
+                  const int64_t* seg_axis, const int32_t* offsets, int64_t nitems, const double* pack_old,
+                  double* pack_new, const int64_t* perm_old, int64_t* perm_new, double* keys, int32_t* vals,
+                  void* temp, int64_t temp_bytes, void* stream);
+
 /* Device-side Krylov support (consumers of the matvec, h2.py:190-253;
  * SURVEY 8f rank 3).  Deterministic dot product: fixed grid of
  * gc_krylov_partials() blocks, `partial` [dev] holds that many doubles.

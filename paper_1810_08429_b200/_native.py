@@ -67,6 +67,9 @@ _SIGNATURES = {
     "gc_curved_singular": [ctypes.POINTER(GcGeom), ctypes.POINTER(GcRules), ctypes.POINTER(GcQueue), c_i64,
                            c_p, ctypes.POINTER(c_i64), c_p],
     "gc_curved_pairs": [ctypes.POINTER(GcGeom), c_p, c_i64, c_p, c_i64, c_i64, c_p, c_p],
+    "gc_tree_boxes": [c_i64, c_p, c_p, c_p, c_p, c_p],
+    "gc_tree_sort_bytes": [c_i64, c_i64, ctypes.POINTER(c_i64)],
+    "gc_tree_split": [c_i64, c_p, c_p, c_p, c_p, c_p, c_i64, c_p, c_p, c_p, c_p, c_p, c_p, c_p, c_i64, c_p],
     "gc_col_pairs": [ctypes.POINTER(GcGeom), c_p, c_p, c_p, c_i64, c_p, c_p, c_i64, c_p, c_p, c_p, c_p],
     "gc_dot": [c_i64, c_p, c_p, c_p, c_p, c_p],
     "gc_cg_pq": [c_i64, c_p, c_p, c_p, c_p, c_p],

@@ -56,8 +56,11 @@ def build_h2_operator(mesh, cfg, kind="slp", capacity=None, threads=None, device
     returns ``(h2matrix, tree, btree)`` like ``cli.py:159-177``.  When a dict
     is passed as ``timings`` it receives the host/device phase times."""
     import time
+
+    from .device import require_device
+    dev = require_device(device)
     t0 = time.perf_counter()
-    tree = build_cluster_tree(mesh, basis_kind=cfg.basis, leaf_size=cfg.leaf_size)
+    tree = build_cluster_tree(mesh, basis_kind=cfg.basis, leaf_size=cfg.leaf_size, device=dev)
     t1 = time.perf_counter()
     btree = build_block_tree(tree, eta=cfg.eta)
     t2 = time.perf_counter()

@@ -225,14 +225,18 @@ def _subtree_counts(size, leaf_size, memo):
     return memo[size]
 
 
-def build_cluster_tree(mesh, basis_kind="constant", leaf_size=32):
+def build_cluster_tree(mesh, basis_kind="constant", leaf_size=32, device=None):
     """Binary cluster tree: split at the positional median along the longest
     box axis, stable in the reference point coordinate
-    (``clustering.py:131-162``).  Returns the root :class:`ClusterTree`."""
+    (``clustering.py:131-162``).  Returns the root :class:`ClusterTree`.
+    With ``device`` the per-depth box reductions, key sorts and permutations
+    run on the GPU (``csrc/tree.cu``); the result is identical."""
     if basis_kind not in ("constant", "linear"):
         raise ConfigError("unknown basis kind %r" % (basis_kind,))
     if leaf_size < 1:
         raise ConfigError("leaf_size must be >= 1")
+    if device is not None:
+        return _build_cluster_tree_device(mesh, basis_kind, leaf_size, device)
     points, lo, hi = _support_data(mesh, basis_kind)
     n = len(points)
     memo = {}
@@ -298,6 +302,84 @@ def build_cluster_tree(mesh, basis_kind="constant", leaf_size=32):
         ids = ids[np.argsort(start[ids], kind="stable")]
         d += 1
     flat = FlatClusterTree(perm, start, stop, left, right, parent, depth, lower, upper)
+    return flat.node(0)
+
+
+def _build_cluster_tree_device(mesh, basis_kind, leaf_size, device):
+    """build_cluster_tree with the n-sized work on the device: the frontier
+    bookkeeping (node ids, child ranges, split axes) stays on the host and
+    reads back 6 doubles per frontier node per depth."""
+    import torch
+
+    from . import _native
+    from .device import ptr, stream_handle
+    points, lo, hi = _support_data(mesh, basis_kind)
+    n = len(points)
+    memo = {}
+    total = _subtree_counts(n, leaf_size, memo)
+    start = np.zeros(total, dtype=np.int64)
+    stop = np.zeros(total, dtype=np.int64)
+    left = np.full(total, -1, dtype=np.int64)
+    right = np.full(total, -1, dtype=np.int64)
+    parent = np.full(total, -1, dtype=np.int64)
+    depth = np.zeros(total, dtype=np.int64)
+    lower = np.zeros((total, 3))
+    upper = np.zeros((total, 3))
+    f64 = dict(dtype=torch.float64, device=device)
+    pack = [torch.from_numpy(np.ascontiguousarray(np.concatenate([lo, hi, points], axis=1))).to(device),
+            torch.empty((n, 9), **f64)]
+    perm = [torch.arange(n, dtype=torch.int64, device=device), torch.empty(n, dtype=torch.int64, device=device)]
+    keys = torch.empty(2 * n, **f64)                       # sort scratch (torch caching allocator)
+    vals = torch.empty(2 * n, dtype=torch.int32, device=device)
+    cur = 0
+    ids = np.array([0], dtype=np.int64)
+    stop[0] = n
+    d = 0
+    with torch.cuda.device(device):
+        st = stream_handle()
+        while ids.size:
+            s_, e_ = start[ids], stop[ids]
+            depth[ids] = d
+            se = torch.from_numpy(np.concatenate([s_, e_])).to(device)
+            box = torch.empty((len(ids), 6), **f64)
+            _native.call("gc_tree_boxes", len(ids), ptr(se[:len(ids)]), ptr(se[len(ids):]), ptr(pack[cur]),
+                         ptr(box), st)
+            bh = box.cpu().numpy()
+            lower[ids], upper[ids] = bh[:, :3], bh[:, 3:]
+            split = (e_ - s_) > leaf_size
+            if not split.any():
+                break
+            ids_s, s_s, e_s = ids[split], s_[split], e_[split]
+            axis = np.argmax(upper[ids_s] - lower[ids_s], axis=1)
+            seg_len = e_s - s_s
+            heads = np.cumsum(seg_len) - seg_len
+            nitems = int(seg_len.sum())
+            offs = np.r_[heads, nitems].astype(np.int32)
+            seg = torch.from_numpy(np.concatenate([s_s, seg_len, heads, axis.astype(np.int64)])).to(device)
+            d_off = torch.from_numpy(offs).to(device)
+            k = len(ids_s)
+            nxt = 1 - cur
+            pack[nxt].copy_(pack[cur])
+            perm[nxt].copy_(perm[cur])
+            tb = _native.ctypes.c_int64(0)
+            _native.call("gc_tree_sort_bytes", nitems, k, _native.ctypes.byref(tb))
+            temp = torch.empty(max(tb.value, 1), dtype=torch.uint8, device=device)
+            _native.call("gc_tree_split", k, ptr(seg[:k]), ptr(seg[k:2 * k]), ptr(seg[2 * k:3 * k]),
+                         ptr(seg[3 * k:]), ptr(d_off), nitems, ptr(pack[cur]), ptr(pack[nxt]), ptr(perm[cur]),
+                         ptr(perm[nxt]), ptr(keys), ptr(vals), ptr(temp), tb.value, st)
+            cur = nxt
+            half = seg_len // 2
+            lid = ids_s + 1
+            rid = ids_s + 1 + np.array([memo[int(h)] for h in half], dtype=np.int64)
+            left[ids_s], right[ids_s] = lid, rid
+            parent[lid], parent[rid] = ids_s, ids_s
+            start[lid], stop[lid] = s_s, s_s + half
+            start[rid], stop[rid] = s_s + half, e_s
+            ids = np.concatenate([lid, rid])
+            ids = ids[np.argsort(start[ids], kind="stable")]
+            d += 1
+        perm_h = perm[cur].cpu().numpy()
+    flat = FlatClusterTree(perm_h, start, stop, left, right, parent, depth, lower, upper)
     return flat.node(0)
 
 

@@ -1,0 +1,139 @@
+// Cluster-tree construction on the device (clustering.py:131-162, the
+// level-wise form of clustering.build_cluster_tree): per tree depth,
+//   * k_seg_box   - segmented min/max of the support boxes (exact, so the
+//                   reduction order is free);
+//   * k_seg_keys  - the split coordinate of every dof of every splitting
+//                   node (-0.0 canonicalised to +0.0: numpy's comparison
+//                   sort treats them as equal, a radix sort would not);
+//   * CUB DeviceSegmentedSort::StableSortPairs - the stable per-node sort
+//                   (the reference's argsort(kind="stable"));
+//   * k_seg_permute - applies the order to the permutation and to the
+//                   packed (lo | hi | point) rows.
+// The host keeps the per-node bookkeeping (frontier, child ids, axes).
+#include <cub/device/device_segmented_sort.cuh>
+
+#include "common.cuh"
+
+namespace gcb {
+
+constexpr int TREE_THREADS = 256;
+
+// box[6 s ..] = (min lo, max hi) over pack rows [start[s], stop[s])
+__global__ void __launch_bounds__(TREE_THREADS) k_seg_box(int64_t nseg, const int64_t* __restrict__ start,
+                                                          const int64_t* __restrict__ stop,
+                                                          const double* __restrict__ pack, double* __restrict__ box) {
+    __shared__ double red[6][TREE_THREADS];
+    for (int64_t sg = blockIdx.x; sg < nseg; sg += gridDim.x) {
+        double v[6] = {INFINITY, INFINITY, INFINITY, -INFINITY, -INFINITY, -INFINITY};
+        for (int64_t r = start[sg] + threadIdx.x; r < stop[sg]; r += TREE_THREADS) {
+            const double* p = pack + 9 * r;
+#pragma unroll
+            for (int k = 0; k < 3; ++k) {
+                v[k] = fmin(v[k], p[k]);
+                v[3 + k] = fmax(v[3 + k], p[3 + k]);
+            }
+        }
+#pragma unroll
+        for (int k = 0; k < 6; ++k) red[k][threadIdx.x] = v[k];
+        __syncthreads();
+        for (int o = TREE_THREADS / 2; o > 0; o >>= 1) {
+            if (threadIdx.x < o) {
+#pragma unroll
+                for (int k = 0; k < 3; ++k) {
+                    red[k][threadIdx.x] = fmin(red[k][threadIdx.x], red[k][threadIdx.x + o]);
+                    red[3 + k][threadIdx.x] = fmax(red[3 + k][threadIdx.x], red[3 + k][threadIdx.x + o]);
+                }
+            }
+            __syncthreads();
+        }
+        if (threadIdx.x < 6) box[6 * sg + threadIdx.x] = red[threadIdx.x][0];
+        __syncthreads();
+    }
+}
+
+// segment s: rows [start, start + len) -> items [head, head + len)
+__global__ void __launch_bounds__(TREE_THREADS) k_seg_keys(int64_t nseg, const int64_t* __restrict__ start,
+                                                           const int64_t* __restrict__ len,
+                                                           const int64_t* __restrict__ head,
+                                                           const int64_t* __restrict__ axis,
+                                                           const double* __restrict__ pack,
+                                                           double* __restrict__ keys, int32_t* __restrict__ vals) {
+    for (int64_t sg = blockIdx.x; sg < nseg; sg += gridDim.x) {
+        const int64_t s = start[sg], h = head[sg], L = len[sg];
+        const int ax = (int)axis[sg];
+        for (int64_t i = threadIdx.x; i < L; i += TREE_THREADS) {
+            keys[h + i] = pack[9 * (s + i) + 6 + ax] + 0.0;     // -0.0 -> +0.0
+            vals[h + i] = (int32_t)(s + i);
+        }
+    }
+}
+
+// new[dst[i]] = old[src[i]] for the permutation and the packed rows
+__global__ void k_seg_permute(int64_t n, const int32_t* __restrict__ dst, const int32_t* __restrict__ src,
+                              const int64_t* __restrict__ perm_old, int64_t* __restrict__ perm_new,
+                              const double* __restrict__ pack_old, double* __restrict__ pack_new) {
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+        const int64_t d = dst[i], s = src[i];
+        perm_new[d] = perm_old[s];
+#pragma unroll
+        for (int k = 0; k < 9; ++k) pack_new[9 * d + k] = pack_old[9 * s + k];
+    }
+}
+
+}  // namespace gcb
+
+using namespace gcb;
+
+extern "C" int gc_tree_boxes(int64_t nseg, const int64_t* start, const int64_t* stop, const double* pack,
+                             double* box, void* stream) {
+    if (nseg <= 0) return GC_OK;
+    const int64_t grid = nseg < 148 * 16 ? nseg : 148 * 16;
+    k_seg_box<<<(unsigned)grid, TREE_THREADS, 0, (cudaStream_t)stream>>>(nseg, start, stop, pack, box);
+    GC_CHECK_LAUNCH("k_seg_box");
+    return GC_OK;
+}
+
+// CUB temp-storage bytes of a split step with nitems dofs in nseg segments
+extern "C" int gc_tree_sort_bytes(int64_t nitems, int64_t nseg, int64_t* bytes) {
+    size_t tb = 0;
+    cudaError_t e = cub::DeviceSegmentedSort::StableSortPairs(nullptr, tb, (const double*)nullptr, (double*)nullptr,
+                                                              (const int32_t*)nullptr, (int32_t*)nullptr, (int)nitems,
+                                                              (int)nseg, (const int32_t*)nullptr,
+                                                              (const int32_t*)nullptr, (cudaStream_t)0);
+    if (e != cudaSuccess) return cuda_status(e, "gc_tree_sort_bytes");
+    *bytes = (int64_t)tb;
+    return GC_OK;
+}
+
+// One split step: keys of the splitting segments, stable segmented sort,
+// permutation of perm / pack from the *_old to the *_new buffers (which the
+// caller initialised as copies of the old ones).  seg arrays [dev] per
+// segment: start, len, head, axis; offsets [dev] (nseg+1) int32 item
+// offsets.  Scratch (caller-owned, [dev]): keys 2*nitems doubles, vals
+// 2*nitems int32, temp of gc_tree_sort_bytes bytes.
+extern "C" int gc_tree_split(int64_t nseg, const int64_t* seg_start, const int64_t* seg_len,
+                             const int64_t* seg_head, const int64_t* seg_axis, const int32_t* offsets,
+                             int64_t nitems, const double* pack_old, double* pack_new,
+                             const int64_t* perm_old, int64_t* perm_new, double* keys, int32_t* vals,
+                             void* temp, int64_t temp_bytes, void* stream) {
+    if (nseg <= 0 || nitems <= 0) return GC_OK;
+    if (nitems > 0x7fffffffLL) { set_error(GC_ERR_CONFIG, "gc_tree_split: too many dofs"); return GC_ERR_CONFIG; }
+    if (!keys || !vals || !temp) { set_error(GC_ERR_CONFIG, "gc_tree_split: scratch missing"); return GC_ERR_CONFIG; }
+    cudaStream_t st = (cudaStream_t)stream;
+    double* keys_out = keys + nitems;
+    int32_t* vals_out = vals + nitems;
+    const int64_t grid = nseg < 148 * 16 ? nseg : 148 * 16;
+    k_seg_keys<<<(unsigned)grid, TREE_THREADS, 0, st>>>(nseg, seg_start, seg_len, seg_head, seg_axis, pack_old,
+                                                        keys, vals);
+    GC_CHECK_LAUNCH("k_seg_keys");
+    size_t tb = (size_t)temp_bytes;
+    cudaError_t e = cub::DeviceSegmentedSort::StableSortPairs(temp, tb, keys, keys_out, vals, vals_out,
+                                                              (int)nitems, (int)nseg, offsets, offsets + 1, st);
+    if (e != cudaSuccess) return cuda_status(e, "gc_tree_split sort");
+    count_launch();
+    int64_t pgrid = (nitems + 255) / 256;
+    if (pgrid > 148 * 32) pgrid = 148 * 32;
+    k_seg_permute<<<(unsigned)pgrid, 256, 0, st>>>(nitems, vals, vals_out, perm_old, perm_new, pack_old, pack_new);
+    GC_CHECK_LAUNCH("k_seg_permute");
+    return GC_OK;
+}

@@ -160,7 +160,7 @@ def build_sharded_operator(mesh, cfg, group=None, device=None, timings=None):
     rank = dist.get_rank(group)
     dev = require_device(device)
     t0 = time.perf_counter()
-    tree = build_cluster_tree(mesh, basis_kind=cfg.basis, leaf_size=cfg.leaf_size)
+    tree = build_cluster_tree(mesh, basis_kind=cfg.basis, leaf_size=cfg.leaf_size, device=dev)
     btree = build_block_tree(tree, eta=cfg.eta)
     layout = ShardLayout(tree, btree, world, rank)
     rng = (layout.lo, layout.hi)

@@ -692,3 +692,18 @@ def test_curved_h2_vs_reference(basis, level, name):
             o += x.rank
     for x, y in zip(g["x"], g["mvm"]):
         assert np.linalg.norm(h2.mvm(hm, x) - y) <= 1e-12 * np.linalg.norm(y)
+
+
+@pytest.mark.parametrize("name,basis", [("h2_sphere5_eps1e-6.npz", "constant"), ("h2_cube4_eps1e-6.npz", "constant"),
+                                        ("h2_lin_cube3_eps1e-6.npz", "linear")])
+def test_device_cluster_tree_bitwise(name, basis):
+    """The device cluster tree (csrc/tree.cu) equals the reference's tree
+    bit for bit: permutation, ranges and boxes."""
+    g = golden(name)
+    mesh = mesh_for(name.replace("h2_lin_", "h2_"))
+    t = clustering.build_cluster_tree(mesh, basis, 16, device=torch.device("cuda"))
+    assert np.array_equal(t.perm, g["perm"])
+    assert np.array_equal(t.flat.start, g["start"]) and np.array_equal(t.flat.stop, g["stop"])
+    assert np.array_equal(t.flat.lower, g["lower"]) and np.array_equal(t.flat.upper, g["upper"])
+    host = clustering.build_cluster_tree(mesh, basis, 16)
+    assert np.array_equal(t.flat.depth, host.flat.depth) and np.array_equal(t.flat.left, host.flat.left)

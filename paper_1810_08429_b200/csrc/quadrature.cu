@@ -384,9 +384,15 @@ __global__ void k_pack_tasks(int64_t B, const int64_t* rows, const int64_t* cols
     }
 }
 
-constexpr int SING_THREADS = 128;
+#ifndef GC_SING_THREADS
+#define GC_SING_THREADS 128
+#endif
+constexpr int SING_THREADS = GC_SING_THREADS;
 constexpr int SING_WARPS = SING_THREADS / 32;
-constexpr int SING_G = 2;   // tasks per warp
+#ifndef GC_SING_G
+#define GC_SING_G 4
+#endif
+constexpr int SING_G = GC_SING_G;   // tasks per warp
 
 // Singular pairs with the xi-reduced rule: D = sum_k coef[k] G_k,
 //   NC = 4 (vertex):    G = (E1, E2, -F1, -F2)

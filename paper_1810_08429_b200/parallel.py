@@ -225,22 +225,47 @@ def _shard_plan_class():
         slots are all-gathered before the coupling phase."""
 
         def __init__(self, sh):
+            import torch
+            import torch.distributed as dist
             super().__init__(sh.h)
             self.sh = sh
             self.lo, self.hi = sh.layout.lo, sh.layout.hi
             g = sh.layout.rank
             self.own_xhat = self.xhat[g * sh.slot:(g + 1) * sh.slot]
+            f64 = dict(dtype=torch.float64, device=self.dev)
+            self.xhat_own = torch.zeros(sh.slot, **f64)        # all-gather input (no aliasing)
+            self.xs_in = torch.zeros(self.hi - self.lo, **f64)
+            self.ys_out = torch.zeros(self.hi - self.lo, **f64)
 
             def gather_xhat():
-                all_gather_into(self.xhat, self.own_xhat.clone(), sh.group)
+                self.xhat_own.copy_(self.own_xhat)
+                all_gather_into(self.xhat, self.xhat_own, sh.group)
 
             # no permutation steps; the x-hat all-gather gates every coupling bucket
             self.nodes = self._build_nodes(gather=False, before_coupling=gather_xhat, scatter=False)
+            self.graph = None
+            if dist.get_backend(sh.group) == "nccl":
+                # the whole sharded product, both NCCL all-gathers included,
+                # as one CUDA graph; eager if capture is not supported
+                try:
+                    self.capture()
+                except Exception:            # pragma: no cover - depends on the NCCL build
+                    self.graph = None
+                    torch.cuda.synchronize(self.dev)
+
+        def _body(self, phase_events=None, phase="coupling"):
+            import torch
+            all_gather_into(self.xt, self.xs_in, self.sh.group)
+            self._exec(self.nodes)
+            torch.add(self.yt[self.lo:self.hi], self.yt2[self.lo:self.hi], out=self.ys_out)
 
         def run(self, x_slice):
-            all_gather_into(self.xt, x_slice.contiguous(), self.sh.group)
-            self._exec(self.nodes)
-            return self.yt[self.lo:self.hi] + self.yt2[self.lo:self.hi]
+            self.xs_in.copy_(x_slice, non_blocking=True)
+            if self.graph is not None:
+                self.graph.replay()
+            else:
+                self._body()
+            return self.ys_out.clone()
 
     return ShardPlan
 

@@ -318,10 +318,13 @@ def test_sharded_operator_world1_matches_full():
         x = np.random.default_rng(3).standard_normal(mesh.nt)
         xt = torch.from_numpy(x[tree.perm]).cuda()
         ys = sh.mvm_local(xt).cpu().numpy()
+        # the sharded product, NCCL all-gathers included, replays as one CUDA graph
+        assert sh.plan.graph is not None
         y = np.empty(mesh.nt)
         y[tree.perm] = ys
         ref = h2.mvm(hm, x)
         assert np.linalg.norm(y - ref) <= 1e-13 * np.linalg.norm(ref)
+        assert np.array_equal(sh.mvm_local(xt).cpu().numpy(), ys)
     finally:
         dist.destroy_process_group()
 

@@ -121,7 +121,8 @@ def _import_reference():
     return "port"
 
 
-def reference_baseline(args, steps, cpu_sample, mesh_vertices=None):
+def reference_baseline(args, steps, cpu_sample, mesh_vertices=None, basis="constant", disc="galerkin",
+                       kernel="slp", curved=False):
     """Time the reference CPU implementation on the host cores.
 
     matvec: greencross.h2.mvm on the reference-built structure (trees,
@@ -140,18 +141,21 @@ def reference_baseline(args, steps, cpu_sample, mesh_vertices=None):
         return P.reference_baseline(args, steps, cpu_sample)
     cores = os.cpu_count() or 1
     mesh = RGeo.build_sphere_mesh(args.level) if args.geometry == "sphere" else _ref_cube(RGeo, args.level)
+    if curved:
+        mesh = RGeo.to_curved(mesh, project_to_unit_sphere=True)
+    row_kind = "collocation" if disc == "collocation" else basis
     t0 = time.perf_counter()
-    tree = RC.build_cluster_tree(mesh, "constant", 16)
+    tree = RC.build_cluster_tree(mesh, basis, 16)
     btree = RC.build_block_tree(tree, eta=1.0)
     t1 = time.perf_counter()
     rm, cm = RG.coupling_marks(btree)
-    rb = RG.build_cluster_basis(tree, mesh, "constant", 3, 0.5, args.eps, "row", (3, 5), rm)
-    cb = RG.build_cluster_basis(tree, mesh, "constant", 3, 0.5, args.eps, "col", (3, 5), cm)
+    rb = RG.build_cluster_basis(tree, mesh, row_kind, 3, 0.5, args.eps, "row", (3, 5), rm)
+    cb = RG.build_cluster_basis(tree, mesh, basis, 3, 0.5, args.eps, "col", (3, 5), cm)
     t2 = time.perf_counter()
     leaves = btree.leaves()
     rng = np.random.default_rng(0)
     pick = rng.random(len(leaves)) < cpu_sample
-    ex, enqueue = RG._make_executor("slp", mesh, "constant", "galerkin", (3, 5), 4096, None)
+    ex, enqueue = RG._make_executor(kernel, mesh, basis, disc, (3, 5), 4096, None)
     tasks_all = tasks_s = 0
     coupling, near = [], []
     for lf, p in zip(leaves, pick):
@@ -171,8 +175,9 @@ def reference_baseline(args, steps, cpu_sample, mesh_vertices=None):
     t4 = time.perf_counter()
     quad_extrap = (t4 - t3) * tasks_all / max(tasks_s, 1)
     hm = RG.H2Matrix(btree.row, btree.col, rb, cb, coupling, near, None)
-    nbytes = RH.storage_report(hm)["total"] + 16 * mesh.nt
-    x = np.random.default_rng(0).standard_normal(mesh.nt)
+    ndof = mesh.nt if basis == "constant" else mesh.nv
+    nbytes = RH.storage_report(hm)["total"] + 16 * ndof
+    x = np.random.default_rng(0).standard_normal(ndof)
     RH.mvm(hm, x)
     t5 = time.perf_counter()
     for _ in range(steps):

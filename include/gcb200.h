@@ -290,6 +290,14 @@ int gc_lin_singular(const gc_geom* g, const gc_rules* r, gc_queue* q, double* U,
 int gc_lin_gather(int64_t nb, const int64_t* desc, const int64_t* rptr, const int64_t* rlist,
                   const int64_t* cptr, const int64_t* clist, const double* U, const int32_t* pp,
                   double* out, void* stream);
+/* gc_lin_pairs over blocks without materialising the pair list: pair i
+ * belongs to the block b with the last blk[4b] (task_base) <= i (ascending),
+ * blk (nblk,4) = task_base, n_col_tris, row table offset, column table
+ * offset; local = i - task_base -> (tri_r[row_off + local / n_col_tris],
+ * tri_c[col_off + local % n_col_tris]). */
+int gc_lin_pairs_blocks(const gc_geom* g, const double* rule_w, const double* rule_b, int64_t n,
+                        int64_t nblk, const int64_t* blk, const int64_t* tri_r, const int64_t* tri_c,
+                        double* U, int32_t* pp, gc_queue* q, int32_t* flags, void* stream);
 
 /* Singular pairs of curved charts: the queued tasks (from
  * gc_assemble_blocks / gc_lin_pairs) integrated with the full Sauter-Schwab
@@ -312,6 +320,12 @@ int gc_curved_pairs(const gc_geom* g, const double* rule, int64_t P, const int64
 int gc_col_pairs(const gc_geom* g, const double* verts, const double* reg_w, const double* reg_b,
                  int64_t ms, const double* sing_w, const double* sing_p, int64_t n,
                  const int64_t* tasks, double* U, int32_t* pp, void* stream);
+/* gc_col_pairs over blocks (pair derivation as gc_lin_pairs_blocks, rows
+ * are points pts_r); nsing [dev] counts the singular (corner) pairs. */
+int gc_col_pairs_blocks(const gc_geom* g, const double* verts, const double* reg_w, const double* reg_b,
+                        int64_t ms, const double* sing_w, const double* sing_p, int64_t n, int64_t nblk,
+                        const int64_t* blk, const int64_t* pts_r, const int64_t* tri_c, double* U,
+                        int32_t* pp, int32_t* nsing, void* stream);
 
 /* Cluster-tree construction per depth (clustering.py:131-162): segmented
  * support boxes box[6s..6s+5] = (min lo, max hi) over rows [start, stop)

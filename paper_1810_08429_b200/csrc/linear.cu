@@ -52,12 +52,44 @@ __device__ __forceinline__ void lin_push(const gc_queue& q, int kase, int64_t t,
 
 // tasks: (t, s) per pair; U: 9 values per pair (canonical permuted order);
 // pp: px | py << 8 per pair
+// Pair i of a batch: explicit (t, s) from `tasks`, or - `blk` given - the
+// pair (tri_r[tr_off + p], tri_c[tc_off + q]) of the block whose task range
+// holds i (blk rows: task_base, n_col_tris, tr_off, tc_off; ascending
+// task_base), p = local / n_col_tris, q = local % n_col_tris.  The product
+// of the row and column triangle tables never exists in memory.
+struct PairSource {
+    const int64_t* tasks;
+    const int64_t* blk;
+    int64_t nblk;
+    const int64_t* tri_r;
+    const int64_t* tri_c;
+};
+
+__device__ __forceinline__ void pair_of(const PairSource& ps, int64_t i, int64_t& t, int64_t& s) {
+    if (ps.blk == nullptr) {
+        t = __ldg(ps.tasks + 2 * i);
+        s = __ldg(ps.tasks + 2 * i + 1);
+        return;
+    }
+    int64_t lo = 0, hi = ps.nblk - 1;
+    while (lo < hi) {                                   // last block with task_base <= i
+        const int64_t mid = (lo + hi + 1) >> 1;
+        if (__ldg(ps.blk + 4 * mid) <= i) lo = mid; else hi = mid - 1;
+    }
+    const int64_t* b = ps.blk + 4 * lo;
+    const int64_t local = i - __ldg(b), tc = __ldg(b + 1);
+    const int64_t pr = local / tc, qc = local - pr * tc;
+    t = __ldg(ps.tri_r + __ldg(b + 2) + pr);
+    s = __ldg(ps.tri_c + __ldg(b + 3) + qc);
+}
+
 template <int M, bool DLP>
-__global__ void __launch_bounds__(128) k_lin_pairs(gc_geom g, LinRule lr, const int64_t* __restrict__ tasks,
+__global__ void __launch_bounds__(128) k_lin_pairs(gc_geom g, LinRule lr, PairSource ps,
                                                    int64_t n, double* __restrict__ U, int32_t* __restrict__ pp,
                                                    gc_queue q, int32_t* flags) {
     for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
-        const int64_t t = __ldg(tasks + 2 * i), s = __ldg(tasks + 2 * i + 1);
+        int64_t t, s;
+        pair_of(ps, i, t, s);
         int64_t tv[3], sv[3];
 #pragma unroll
         for (int k = 0; k < 3; ++k) {
@@ -227,9 +259,28 @@ __global__ void k_lin_gather(int64_t nb, const int64_t* __restrict__ desc, const
 
 using namespace gcb;
 
+static int lin_pairs(const gc_geom* gp, const double* rule_w, const double* rule_b, int64_t n,
+                     const PairSource& ps, double* U, int32_t* pp, gc_queue* qp, int32_t* flags,
+                     void* stream);
+
 extern "C" int gc_lin_pairs(const gc_geom* gp, const double* rule_w, const double* rule_b, int64_t n,
                             const int64_t* tasks, double* U, int32_t* pp, gc_queue* qp, int32_t* flags,
                             void* stream) {
+    const PairSource ps{tasks, nullptr, 0, nullptr, nullptr};
+    return lin_pairs(gp, rule_w, rule_b, n, ps, U, pp, qp, flags, stream);
+}
+
+extern "C" int gc_lin_pairs_blocks(const gc_geom* gp, const double* rule_w, const double* rule_b, int64_t n,
+                                   int64_t nblk, const int64_t* blk, const int64_t* tri_r, const int64_t* tri_c,
+                                   double* U, int32_t* pp, gc_queue* qp, int32_t* flags, void* stream) {
+    if (nblk <= 0 || !blk || !tri_r || !tri_c) { set_error(GC_ERR_CONFIG, "gc_lin_pairs_blocks: no blocks"); return GC_ERR_CONFIG; }
+    const PairSource ps{nullptr, blk, nblk, tri_r, tri_c};
+    return lin_pairs(gp, rule_w, rule_b, n, ps, U, pp, qp, flags, stream);
+}
+
+static int lin_pairs(const gc_geom* gp, const double* rule_w, const double* rule_b, int64_t n,
+                     const PairSource& ps, double* U, int32_t* pp, gc_queue* qp, int32_t* flags,
+                     void* stream) {
     if (!gp || !qp || !rule_w || !rule_b) { set_error(GC_ERR_CONFIG, "gc_lin_pairs: null argument"); return GC_ERR_CONFIG; }
     if (n <= 0) return GC_OK;
     const gc_geom g = *gp;
@@ -250,9 +301,9 @@ extern "C" int gc_lin_pairs(const gc_geom* gp, const double* rule_w, const doubl
 #define LIN_LAUNCH(M)                                                                                   \
     do {                                                                                                \
         if (g.kernel)                                                                                   \
-            k_lin_pairs<M, true><<<(unsigned)grid, 128, 0, st>>>(g, lr, tasks, n, U, pp, q, flags);     \
+            k_lin_pairs<M, true><<<(unsigned)grid, 128, 0, st>>>(g, lr, ps, n, U, pp, q, flags);        \
         else                                                                                            \
-            k_lin_pairs<M, false><<<(unsigned)grid, 128, 0, st>>>(g, lr, tasks, n, U, pp, q, flags);    \
+            k_lin_pairs<M, false><<<(unsigned)grid, 128, 0, st>>>(g, lr, ps, n, U, pp, q, flags);       \
     } while (0)
     if (g.mq == 9) LIN_LAUNCH(9);
     else if (g.mq == 4) LIN_LAUNCH(4);
@@ -324,11 +375,12 @@ struct ColRule {
 
 template <bool DLP>
 __global__ void __launch_bounds__(128) k_col_pairs(gc_geom g, ColRule cr, const double* __restrict__ verts,
-                                                   const int64_t* __restrict__ tasks, int64_t n,
-                                                   double* __restrict__ U, int32_t* __restrict__ pp) {
+                                                   PairSource ps, int64_t n, double* __restrict__ U,
+                                                   int32_t* __restrict__ pp, int32_t* nsing) {
     const int M = (int)g.mq;
     for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
-        const int64_t v = __ldg(tasks + 2 * i), s = __ldg(tasks + 2 * i + 1);
+        int64_t v, s;
+        pair_of(ps, i, v, s);
         int rot = -1;
 #pragma unroll
         for (int k = 0; k < 3; ++k)
@@ -342,6 +394,7 @@ __global__ void __launch_bounds__(128) k_col_pairs(gc_geom g, ColRule cr, const 
         }
         double acc[3] = {0.0, 0.0, 0.0};
         const bool curv = g.gq != nullptr;
+        if (rot >= 0 && nsing != nullptr) atomicAdd(nsing, 1);
         if (curv && rot >= 0) {
             // curved chart, point at a corner: the rotated quadratic chart at
             // the collapsed rule's points (assembly.py:254-265)
@@ -415,9 +468,29 @@ __global__ void __launch_bounds__(128) k_col_pairs(gc_geom g, ColRule cr, const 
     }
 }
 
+static int col_pairs(const gc_geom* gp, const double* verts, const double* reg_w, const double* reg_b,
+                     int64_t ms, const double* sing_w, const double* sing_p, int64_t n, const PairSource& ps,
+                     double* U, int32_t* pp, int32_t* nsing, void* stream);
+
 extern "C" int gc_col_pairs(const gc_geom* gp, const double* verts, const double* reg_w, const double* reg_b,
                             int64_t ms, const double* sing_w, const double* sing_p, int64_t n,
                             const int64_t* tasks, double* U, int32_t* pp, void* stream) {
+    const PairSource ps{tasks, nullptr, 0, nullptr, nullptr};
+    return col_pairs(gp, verts, reg_w, reg_b, ms, sing_w, sing_p, n, ps, U, pp, nullptr, stream);
+}
+
+extern "C" int gc_col_pairs_blocks(const gc_geom* gp, const double* verts, const double* reg_w,
+                                   const double* reg_b, int64_t ms, const double* sing_w, const double* sing_p,
+                                   int64_t n, int64_t nblk, const int64_t* blk, const int64_t* pts_r,
+                                   const int64_t* tri_c, double* U, int32_t* pp, int32_t* nsing, void* stream) {
+    if (nblk <= 0 || !blk || !pts_r || !tri_c) { set_error(GC_ERR_CONFIG, "gc_col_pairs_blocks: no blocks"); return GC_ERR_CONFIG; }
+    const PairSource ps{nullptr, blk, nblk, pts_r, tri_c};
+    return col_pairs(gp, verts, reg_w, reg_b, ms, sing_w, sing_p, n, ps, U, pp, nsing, stream);
+}
+
+static int col_pairs(const gc_geom* gp, const double* verts, const double* reg_w, const double* reg_b,
+                     int64_t ms, const double* sing_w, const double* sing_p, int64_t n, const PairSource& ps,
+                     double* U, int32_t* pp, int32_t* nsing, void* stream) {
     if (!gp || !verts || !reg_w || !reg_b || !sing_w || !sing_p) {
         set_error(GC_ERR_CONFIG, "gc_col_pairs: null argument");
         return GC_ERR_CONFIG;
@@ -442,9 +515,9 @@ extern "C" int gc_col_pairs(const gc_geom* gp, const double* verts, const double
     int64_t grid = (n + 127) / 128;
     if (grid > 148 * 32) grid = 148 * 32;
     if (g.kernel)
-        k_col_pairs<true><<<(unsigned)grid, 128, 0, st>>>(g, cr, verts, tasks, n, U, pp);
+        k_col_pairs<true><<<(unsigned)grid, 128, 0, st>>>(g, cr, verts, ps, n, U, pp, nsing);
     else
-        k_col_pairs<false><<<(unsigned)grid, 128, 0, st>>>(g, cr, verts, tasks, n, U, pp);
+        k_col_pairs<false><<<(unsigned)grid, 128, 0, st>>>(g, cr, verts, ps, n, U, pp, nsing);
     GC_CHECK_LAUNCH("k_col_pairs");
     return GC_OK;
 }

@@ -35,7 +35,46 @@ def _star_csr(mesh):
         order = np.argsort(flat, kind="stable")
         ptr_ = np.searchsorted(flat[order], np.arange(mesh.nv + 1))
         cache["star_csr"] = (ptr_.astype(np.int64), (order // 3).astype(np.int64))
+        cache["star_corner"] = (order % 3).astype(np.int64)
     return cache["star_csr"]
+
+
+class _Tables:
+    """Triangle tables (``triangle_table``) of many DOF lists at once, plus
+    the CSR from every DOF to its (table row, corner) entries - vectorised
+    over all blocks.  ``points=True``: the rows are collocation points, each
+    its own one-entry "table" row."""
+
+    def __init__(self, mesh, dof_lists, points=False):
+        lens = np.array([len(d) for d in dof_lists], dtype=np.int64)
+        nb = len(lens)
+        D = np.concatenate(dof_lists).astype(np.int64) if nb else np.zeros(0, np.int64)
+        self.dof_off = np.r_[0, np.cumsum(lens)]
+        P = np.arange(len(D), dtype=np.int64) - np.repeat(self.dof_off[:-1], lens)
+        if points:
+            self.T = lens.copy()
+            self.toff = self.dof_off[:-1].copy()
+            self.tri = D                                    # the point itself
+            self.ptr = np.arange(len(D) + 1, dtype=np.int64)
+            self.ent = P << 2
+            return
+        sp, st = _star_csr(mesh)
+        sc = mesh.__dict__["_device_cache"]["star_corner"]
+        deg = sp[D + 1] - sp[D]
+        idx = _ranges(sp[D], deg)
+        eb = np.repeat(np.repeat(np.arange(nb, dtype=np.int64), lens), deg)
+        ep = np.repeat(P, deg)
+        et, ek = st[idx], sc[idx]
+        key = eb * mesh.nt + et
+        ukey, inv = np.unique(key, return_inverse=True)
+        tb = ukey // mesh.nt
+        self.T = np.bincount(tb, minlength=nb).astype(np.int64)
+        self.toff = np.r_[0, np.cumsum(self.T)][:-1]
+        self.tri = ukey % mesh.nt
+        gdof = self.dof_off[eb] + ep                        # global DOF index of every entry
+        order = np.lexsort((inv, gdof))
+        self.ent = (((inv - self.toff[eb]) << 2) | ek)[order].astype(np.int64)
+        self.ptr = np.r_[0, np.cumsum(np.bincount(gdof, minlength=len(D)))].astype(np.int64)
 
 
 def _ranges(starts, lengths):
@@ -65,17 +104,6 @@ def triangle_table(indices, mesh):
     hit = sidx[loc] == corners
     slot = np.where(hit, order[loc] + 1, 0)
     return np.column_stack([tri, slot]).astype(np.int64)
-
-
-def _dof_lists(table, ndof):
-    """CSR over the DOFs of a triangle table: per DOF the packed
-    (table_row << 2 | corner) entries, in table order."""
-    p, k = np.nonzero(table[:, 1:] > 0)
-    dof = table[p, 1 + k] - 1
-    order = np.argsort(dof, kind="stable")
-    ptr_ = np.zeros(ndof + 1, dtype=np.int64)
-    np.cumsum(np.bincount(dof, minlength=ndof), out=ptr_[1:])
-    return ptr_, ((p[order] << 2) | k[order]).astype(np.int64)
 
 
 class LinearRules:
@@ -186,65 +214,72 @@ def assemble_blocks(dmesh, kind, rules, mesh, blocks, out, device):
     """Linear-basis Galerkin blocks: ``blocks`` = list of (rows, cols,
     out_off) with vertex DOF lists; each block lands column-major in the
     device vector ``out`` at ``out_off``.  Returns per-case task counts."""
+    return _assemble(dmesh, kind, mesh, blocks, out, device, rules=rules)
+
+
+def _assemble(dmesh, kind, mesh, blocks, out, device, rules=None, crules=None):
+    """Shared block driver: vectorised tables, batches of <= _MAX_TASKS
+    triangle (or point x triangle) pairs derived on the device from block
+    descriptors, pair kernels, singular flush, deterministic gather."""
     totals = [0, 0, 0, 0]
+    if not blocks:
+        return totals
+    colloc = crules is not None
+    tr = _Tables(mesh, [b[0] for b in blocks], points=colloc)
+    tc = _Tables(mesh, [b[1] for b in blocks])
+    nr = np.diff(tr.dof_off)
+    nc = np.diff(tc.dof_off)
+    offs = np.array([b[2] for b in blocks], dtype=np.int64)
+    ntask = tr.T * tc.T
+    d = [to_dev(a if len(a) else np.zeros(1, np.int64), device)
+         for a in (tr.ptr, tr.ent, tc.ptr, tc.ent, tr.tri, tc.tri)]
+    cum = np.cumsum(ntask)
+    cap = int(min(int(cum[-1]), max(_MAX_TASKS, int(ntask.max()))))
+    U = empty(9 * max(cap, 1), device)
+    pp = torch.empty(max(cap, 1), dtype=torch.int32, device=device)
+    q = None if colloc else _Queue(cap, device)
+    nsing = torch.zeros(1, dtype=torch.int32, device=device)
     i = 0
     while i < len(blocks):
-        # one device batch: consecutive blocks up to _MAX_TASKS pairs
-        batch, ntask = [], 0
-        while i < len(blocks):
-            rows, cols, off = blocks[i]
-            tr, tc = triangle_table(rows, mesh), triangle_table(cols, mesh)
-            n = len(tr) * len(tc)
-            if batch and ntask + n > _MAX_TASKS:
-                break
-            batch.append((rows, cols, off, tr, tc))
-            ntask += n
-            i += 1
-        _run_batch(dmesh, kind, rules, batch, ntask, out, device, totals)
+        # consecutive blocks up to _MAX_TASKS pairs per device batch
+        start_cum = int(cum[i - 1]) if i else 0
+        j = max(int(np.searchsorted(cum, start_cum + _MAX_TASKS, side="right")), i + 1)
+        sel = np.arange(i, j)
+        live = sel[ntask[sel] > 0]
+        n = int(ntask[sel].sum())
+        base = np.r_[0, np.cumsum(ntask[sel])][:-1]
+        desc = np.stack([tr.dof_off[sel], nr[sel], tc.dof_off[sel], nc[sel], offs[sel], base, tc.T[sel]], 1)
+        blk = np.stack([base[ntask[sel] > 0], tc.T[live], tr.toff[live], tc.toff[live]], 1)
+        d_desc = to_dev(np.ascontiguousarray(desc, np.int64), device)
+        with torch.cuda.device(device):
+            st = stream_handle()
+            if n:
+                d_blk = to_dev(np.ascontiguousarray(blk, np.int64), device)
+                if colloc:
+                    _native.call("gc_col_pairs_blocks", dmesh.geom_of(kind), ptr(dmesh.verts),
+                                 crules.w.ctypes.data, crules.b.ctypes.data, len(crules.sw),
+                                 crules.sw.ctypes.data, crules.sp.ctypes.data, n, len(blk), ptr(d_blk),
+                                 ptr(d[4]), ptr(d[5]), ptr(U), ptr(pp), ptr(nsing), st)
+                else:
+                    _native.call("gc_lin_pairs_blocks", dmesh.geom_of(kind), rules.w.ctypes.data,
+                                 rules.b.ctypes.data, n, len(blk), ptr(d_blk), ptr(d[4]), ptr(d[5]), ptr(U),
+                                 ptr(pp), q.struct, ptr(q.flags), st)
+                    c = (_native.c_i64 * 4)()
+                    _flush(dmesh, kind, rules, q, U, c, st)
+                    q.check()
+                    for k in (1, 2, 3):
+                        totals[k] += int(c[k])
+            _native.call("gc_lin_gather", len(desc), ptr(d_desc), ptr(d[0]), ptr(d[1]), ptr(d[2]), ptr(d[3]),
+                         ptr(U), ptr(pp), ptr(out), st)
+        totals[0] += n
+        i = j
+    if colloc:
+        s_ = int(nsing.item())
+        totals[0] -= s_
+        totals[1] += s_
+    else:
+        totals[0] -= sum(totals[1:])
     return totals
-
-
-def _run_batch(dmesh, kind, rules, batch, ntask, out, device, totals):
-    tasks = np.empty((ntask, 2), dtype=np.int64)
-    desc = np.empty((len(batch), 7), dtype=np.int64)
-    rp, rl, cp, cl = [], [], [], []
-    base = ro = co = 0
-    for b, (rows, cols, off, tr, tc) in enumerate(batch):
-        nr, nc, T, C = len(rows), len(cols), len(tr), len(tc)
-        tasks[base:base + T * C, 0] = np.repeat(tr[:, 0], C)
-        tasks[base:base + T * C, 1] = np.tile(tc[:, 0], T)
-        p1, l1 = _dof_lists(tr, nr)
-        p2, l2 = _dof_lists(tc, nc)
-        desc[b] = (ro, nr, co, nc, off, base, C)
-        rp.append(p1[:-1] + sum(len(x) for x in rl))
-        rl.append(l1)
-        cp.append(p2[:-1] + sum(len(x) for x in cl))
-        cl.append(l2)
-        ro += nr
-        co += nc
-        base += T * C
-    rptr = np.concatenate(rp + [np.array([sum(len(x) for x in rl)], np.int64)])
-    cptr = np.concatenate(cp + [np.array([sum(len(x) for x in cl)], np.int64)])
-    rlist = np.concatenate(rl) if rl else np.zeros(1, np.int64)
-    clist = np.concatenate(cl) if cl else np.zeros(1, np.int64)
-    d_tasks = to_dev(tasks, device)
-    U = empty(9 * max(ntask, 1), device)
-    pp = torch.empty(max(ntask, 1), dtype=torch.int32, device=device)
-    q = _Queue(ntask, device)
-    d = [to_dev(a, device) for a in (desc, rptr, np.maximum(rlist, 0), cptr, np.maximum(clist, 0))]
-    with torch.cuda.device(device):
-        st = stream_handle()
-        _native.call("gc_lin_pairs", dmesh.geom_of(kind), rules.w.ctypes.data, rules.b.ctypes.data, ntask,
-                     ptr(d_tasks), ptr(U), ptr(pp), q.struct, ptr(q.flags), st)
-        counts = (_native.c_i64 * 4)()
-        _flush(dmesh, kind, rules, q, U, counts, st)
-        _native.call("gc_lin_gather", len(batch), ptr(d[0]), ptr(d[1]), ptr(d[2]), ptr(d[3]), ptr(d[4]),
-                     ptr(U), ptr(pp), ptr(out), st)
-    q.check()
-    sing = [int(counts[k]) for k in range(4)]
-    sing[0] = ntask - sum(sing[1:])
-    for k in range(4):
-        totals[k] += sing[k]
 
 
 # --------------------------------------------------------------------------
@@ -299,50 +334,5 @@ def collocation_blocks(dmesh, kind, rules, mesh, blocks, out, device):
     """Collocation blocks: ``blocks`` = (row points, column DOFs, out_off);
     column-major per block in ``out``.  Returns [regular, singular] task
     counts."""
-    totals = [0, 0]
-    i = 0
-    while i < len(blocks):
-        batch, ntask = [], 0
-        while i < len(blocks):
-            rows, cols, off = blocks[i]
-            tc = triangle_table(cols, mesh)
-            n = len(rows) * len(tc)
-            if batch and ntask + n > _MAX_TASKS:
-                break
-            batch.append((np.asarray(rows, np.int64), cols, off, tc))
-            ntask += n
-            i += 1
-        tasks = np.empty((ntask, 2), dtype=np.int64)
-        desc = np.empty((len(batch), 7), dtype=np.int64)
-        rp, rl, cp, cl = [], [], [], []
-        base = ro = co = nrl = ncl = 0
-        for b, (rows, cols, off, tc) in enumerate(batch):
-            nr, nc, C = len(rows), len(cols), len(tc)
-            tasks[base:base + nr * C, 0] = np.repeat(rows, C)
-            tasks[base:base + nr * C, 1] = np.tile(tc[:, 0], nr)
-            rp.append(np.arange(nr, dtype=np.int64) + nrl)
-            rl.append(np.arange(nr, dtype=np.int64) << 2)           # row i: (task row i, corner 0)
-            p2, l2 = _dof_lists(tc, nc)
-            cp.append(p2[:-1] + ncl)
-            cl.append(l2)
-            desc[b] = (ro, nr, co, nc, off, base, C)
-            nrl += nr
-            ncl += len(l2)
-            ro += nr
-            co += nc
-            base += nr * C
-        rptr = np.concatenate(rp + [np.array([nrl], np.int64)])
-        cptr = np.concatenate(cp + [np.array([ncl], np.int64)])
-        d = [to_dev(a, device) for a in (desc, rptr, np.concatenate(rl), cptr,
-                                          np.concatenate(cl) if ncl else np.zeros(1, np.int64))]
-        d_tasks = to_dev(tasks, device)
-        U = empty(9 * max(ntask, 1), device)
-        pp = torch.empty(max(ntask, 1), dtype=torch.int32, device=device)
-        _col_call(dmesh, kind, rules, d_tasks, ntask, U, pp, device)
-        with torch.cuda.device(device):
-            _native.call("gc_lin_gather", len(batch), ptr(d[0]), ptr(d[1]), ptr(d[2]), ptr(d[3]), ptr(d[4]),
-                         ptr(U), ptr(pp), ptr(out), stream_handle())
-        sing = int((mesh.triangles[tasks[:, 1]] == tasks[:, :1]).any(axis=1).sum()) if ntask else 0
-        totals[0] += ntask - sing
-        totals[1] += sing
-    return totals
+    t = _assemble(dmesh, kind, mesh, blocks, out, device, crules=rules)
+    return t[:2]

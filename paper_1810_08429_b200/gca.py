@@ -664,9 +664,11 @@ def build_h2(btree, row_basis, col_basis, mesh, kind="slp", basis="constant",
         # 3x3 integrals (linear.py); collocation rows are point evaluations
         from . import linear
         rp, cp = rstore.pivots_host, cstore.pivots_host
-        cblocks = [(rp[rstore.piv_off[a]:rstore.piv_off[a] + nr], cp[cstore.piv_off[b]:cstore.piv_off[b] + nc], o)
+        # (rows, cols, out_off, row key, col key): one triangle table per cluster
+        cblocks = [(rp[rstore.piv_off[a]:rstore.piv_off[a] + nr], cp[cstore.piv_off[b]:cstore.piv_off[b] + nc], o,
+                    int(a), int(b))
                    for a, b, nr, nc, o in zip(cr[keep], cc[keep], c_nr[keep], c_nc[keep], c_off[keep])]
-        nblocks = [(rf.perm[rf.start[a]:rf.stop[a]], cf.perm[cf.start[b]:cf.stop[b]], o)
+        nblocks = [(rf.perm[rf.start[a]:rf.stop[a]], cf.perm[cf.start[b]:cf.stop[b]], o, int(a), int(b))
                    for a, b, o in zip(nr_r, nc_r, n_off)]
         if disc == "collocation":
             crules = linear.CollocationRules(*orders)

@@ -217,6 +217,34 @@ def assemble_blocks(dmesh, kind, rules, mesh, blocks, out, device):
     return _assemble(dmesh, kind, mesh, blocks, out, device, rules=rules)
 
 
+def _dedupe(lists, keys):
+    """Index of every list into the distinct lists (by key when given)."""
+    if any(k is None for k in keys):
+        return np.arange(len(lists), dtype=np.int64), lists
+    first, idx = {}, np.empty(len(keys), dtype=np.int64)
+    for i, k in enumerate(keys):
+        j = first.get(k)
+        if j is None:
+            j = first[k] = len(first)
+        idx[i] = j
+    uniq = [None] * len(first)
+    for i, k in enumerate(keys):
+        if uniq[idx[i]] is None:
+            uniq[idx[i]] = lists[i]
+    return idx, uniq
+
+
+class _Select:
+    """Per-block view of the distinct tables: dof offset, dof count, table
+    size and offset of each block's list."""
+
+    def __init__(self, t, idx):
+        self.dof_off = t.dof_off[:-1][idx]
+        self.n = np.diff(t.dof_off)[idx]
+        self.T = t.T[idx]
+        self.toff = t.toff[idx]
+
+
 def _assemble(dmesh, kind, mesh, blocks, out, device, rules=None, crules=None):
     """Shared block driver: vectorised tables, batches of <= _MAX_TASKS
     triangle (or point x triangle) pairs derived on the device from block
@@ -225,14 +253,19 @@ def _assemble(dmesh, kind, mesh, blocks, out, device, rules=None, crules=None):
     if not blocks:
         return totals
     colloc = crules is not None
-    tr = _Tables(mesh, [b[0] for b in blocks], points=colloc)
-    tc = _Tables(mesh, [b[1] for b in blocks])
-    nr = np.diff(tr.dof_off)
-    nc = np.diff(tc.dof_off)
+    # one table per distinct DOF list: blocks of one block row share the row
+    # list (blocks may carry (rows, cols, off, row_key, col_key))
+    ridx, rlists = _dedupe([b[0] for b in blocks], [b[3] if len(b) > 3 else None for b in blocks])
+    cidx, clists = _dedupe([b[1] for b in blocks], [b[4] if len(b) > 4 else None for b in blocks])
+    tr_u = _Tables(mesh, rlists, points=colloc)
+    tc_u = _Tables(mesh, clists)
+    tr, tc = _Select(tr_u, ridx), _Select(tc_u, cidx)
+    nr = tr.n
+    nc = tc.n
     offs = np.array([b[2] for b in blocks], dtype=np.int64)
     ntask = tr.T * tc.T
     d = [to_dev(a if len(a) else np.zeros(1, np.int64), device)
-         for a in (tr.ptr, tr.ent, tc.ptr, tc.ent, tr.tri, tc.tri)]
+         for a in (tr_u.ptr, tr_u.ent, tc_u.ptr, tc_u.ent, tr_u.tri, tc_u.tri)]
     cum = np.cumsum(ntask)
     cap = int(min(int(cum[-1]), max(_MAX_TASKS, int(ntask.max()))))
     U = empty(9 * max(cap, 1), device)

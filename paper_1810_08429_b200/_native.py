@@ -54,6 +54,7 @@ _SIGNATURES = {
     "gc_gather": [c_p, c_p, c_i64, c_p, c_p],
     "gc_scatter": [c_p, c_p, c_i64, c_p, c_p],
     "gc_scatter2": [c_p, c_p, c_p, c_i64, c_p, c_p],
+    "gc_expand_ranges": [c_i64, c_p, c_p, c_p, c_p, c_p],
     "gc_segmv": [c_i64, c_p, c_p, c_p, c_p, c_p, c_p, c_p, ctypes.c_int, c_i64, c_p],
     "gc_panelmv": [c_i64, c_p, c_p, c_p, c_p, c_p, c_p, c_p, c_p, c_i64, c_p, c_p, ctypes.c_int32,
                    ctypes.c_int32, c_p, c_p],

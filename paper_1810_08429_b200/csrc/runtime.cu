@@ -194,3 +194,22 @@ int gc_dfma_probe(int64_t blocks, int64_t threads, int64_t iters, double* out, v
 }
 
 }  // extern "C"
+
+// out[off[i] + j] = start[i] + j for j < len[i] (int32): the input-index
+// lists of the matvec panels, expanded on the device from per-block ranges
+__global__ void k_expand_ranges_impl(int64_t n, const int64_t* __restrict__ start, const int64_t* __restrict__ len,
+                                const int64_t* __restrict__ off, int32_t* __restrict__ out) {
+    for (int64_t i = blockIdx.x; i < n; i += gridDim.x) {
+        const int64_t s = start[i], L = len[i], o = off[i];
+        for (int64_t j = threadIdx.x; j < L; j += blockDim.x) out[o + j] = (int32_t)(s + j);
+    }
+}
+
+extern "C" int gc_expand_ranges(int64_t n, const int64_t* start, const int64_t* len, const int64_t* off,
+                                int32_t* out, void* stream) {
+    if (n <= 0) return GC_OK;
+    const int64_t grid = n < 148 * 64 ? n : 148 * 64;
+    k_expand_ranges_impl<<<(unsigned)grid, 64, 0, (cudaStream_t)stream>>>(n, start, len, off, out);
+    GC_CHECK_LAUNCH("k_expand_ranges");
+    return GC_OK;
+}

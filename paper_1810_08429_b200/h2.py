@@ -526,7 +526,7 @@ class PanelPlan:
             leaf = h_ == 0
             K = cs.rows[ids]
             base = cf.start[ids] if leaf else cs.coef_off[cf.left[ids]]
-            panels = (cs.v_off[ids], K, cs.rank[ids], _ranges_np(base, K), cs.coef_off[ids], 0)
+            panels = (cs.v_off[ids], K, cs.rank[ids], (base, K), cs.coef_off[ids], 0)
             fwd.append(self._phase("forward", int(h_), panels, cs.V, None,
                                    self.xt if leaf else self.xhat, None, self.xhat, transform=True))
         # coupling: one panel per row cluster, bucketed by row height
@@ -536,16 +536,18 @@ class PanelPlan:
         if order.size:
             sn = d.c_rows[order]
             cuts = np.flatnonzero(np.r_[True, sn[1:] != sn[:-1]])
-            # panel inputs: the x-hat slots of the blocks' column clusters, in block order
-            flat = _ranges_np(cs.coef_off[d.c_cols[order]], d.c_nc[order])
-            K = np.add.reduceat(d.c_nc[order], cuts)
-            head = _offsets_np(K)
+            # panel inputs: the x-hat slots of the blocks' column clusters, in
+            # block order - one index range per block, expanded on the device
+            bstart, blen = cs.coef_off[d.c_cols[order]], d.c_nc[order]
+            K = np.add.reduceat(blen, cuts)
+            nblk = np.diff(np.r_[cuts, len(order)])
             colh = np.maximum.reduceat(cf.height[d.c_cols[order]], cuts)
             rowh = rf.height[sn[cuts]]
             for h_ in np.unique(rowh):
                 sel = np.flatnonzero(rowh == h_)
+                bsel = _ranges_np(cuts[sel], nblk[sel])
                 panels = (d.c_off[order[cuts[sel]]], K[sel], d.c_nr[order[cuts[sel]]],
-                          flat[_ranges_np(head[sel], K[sel])], rs.coef_off[sn[cuts[sel]]], 0)
+                          (bstart[bsel], blen[bsel]), rs.coef_off[sn[cuts[sel]]], 0)
                 P = self._phase("coupling", int(h_), panels, d.coup, None, self.xhat, None, self.yhat)
                 cpl.append((P, int(colh[sel].max())))
         # backward transform (row basis), top down
@@ -554,7 +556,7 @@ class PanelPlan:
         for h_ in sorted(np.unique(rf.height[matb]), reverse=True):
             ids = np.flatnonzero(matb & (rf.height == h_))
             K = rs.rank[ids]
-            panels = (rs.v_off[ids], K, rs.rows[ids], _ranges_np(rs.coef_off[ids], K), rs.coef_off[rf.left[ids]], 1)
+            panels = (rs.v_off[ids], K, rs.rows[ids], (rs.coef_off[ids], K), rs.coef_off[rf.left[ids]], 1)
             P = self._phase("backward", int(h_), panels, rs.VT, None, self.yhat, None, self.yhat,
                             transform=True)
             kids = np.r_[rf.left[ids], rf.right[ids]]
@@ -564,7 +566,7 @@ class PanelPlan:
         sn = d.n_rows[order]
         cuts = np.flatnonzero(np.r_[True, sn[1:] != sn[:-1]]) if len(sn) else np.zeros(0, np.int64)
         K = np.add.reduceat(d.n_nc[order], cuts) if len(sn) else np.zeros(0, np.int64)
-        rows = _ranges_np(cf.start[d.n_cols[order]], d.n_nc[order])
+        rows = (cf.start[d.n_cols[order]], d.n_nc[order])
         panels = (d.n_off[order[cuts]], K, d.n_nr[order[cuts]], rows, rf.start[sn[cuts]], 0)
         near = self._phase("nearfield", 0, panels, d.near, None, self.xt, None, self.yt)
         # leaf basis: yt[leaf] += V yhat
@@ -574,7 +576,7 @@ class PanelPlan:
             leaves = leaves[(rf.start[leaves] >= d.row_range[0]) & (rf.stop[leaves] <= d.row_range[1])]
         if leaves.size:
             K = rs.rank[leaves]
-            panels = (rs.v_off[leaves], K, size_r[leaves], _ranges_np(rs.coef_off[leaves], K), rf.start[leaves], 1)
+            panels = (rs.v_off[leaves], K, size_r[leaves], (rs.coef_off[leaves], K), rf.start[leaves], 1)
             # into yt2 (overwritten): the leaf basis need not wait for the near field
             panels = panels[:5] + (0,)
             leafp = self._phase("leafbasis", 0, panels, rs.VT, None, self.yhat, None, self.yt2,
@@ -802,7 +804,8 @@ class PanelPlan:
         if transform or self.bulk_kernel != "tma":          # (tma items must fit its tile)
             rpi = np.maximum(rpi, np.minimum(max_rows, -(-K // 8)))
         nit = np.maximum(1, -(-K // rpi))
-        xidx = np.asarray(rows).astype(np.int32) if n else np.zeros(1, np.int32)
+        segs = rows if isinstance(rows, tuple) else None      # (starts, lengths) of index ranges
+        xidx = None if segs is not None else (np.asarray(rows).astype(np.int32) if n else np.zeros(1, np.int32))
         xoff = _offsets_np(K)
         item_panel = np.repeat(np.arange(n), nit)
         item_idx_in_panel = _ranges_np(np.zeros(n, np.int64), nit)
@@ -825,7 +828,17 @@ class PanelPlan:
         P = _Phase()
         P.name, P.height = name, height
         P.items = to_dev(np.ascontiguousarray(items, np.int64), self.dev)
-        P.xidx = to_dev(xidx, self.dev)
+        if segs is not None:
+            st_, ln_ = np.asarray(segs[0], np.int64), np.asarray(segs[1], np.int64)
+            total = int(ln_.sum())
+            P.xidx = torch.empty(max(total, 1), dtype=torch.int32, device=self.dev)
+            tab = to_dev(np.concatenate([st_, ln_, _offsets_np(ln_)]), self.dev)
+            m = len(st_)
+            with torch.cuda.device(self.dev):
+                _native.call("gc_expand_ranges", m, ptr(tab[:m]), ptr(tab[m:2 * m]), ptr(tab[2 * m:]),
+                             ptr(P.xidx), stream_handle())
+        else:
+            P.xidx = to_dev(xidx, self.dev)
         P.nitems, P.nred = len(items), int(multi.sum())
         P.red = to_dev(np.ascontiguousarray(red, np.int64), self.dev) if P.nred else None
         P.arrivals = torch.zeros(max(P.nred, 1), dtype=torch.int32, device=self.dev)

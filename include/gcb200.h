@@ -24,7 +24,7 @@
 extern "C" {
 #endif
 
-#define GC_ABI_VERSION 1
+#define GC_ABI_VERSION 2
 
 #define GC_OK 0
 #define GC_ERR_CONFIG 1

@@ -102,7 +102,7 @@ _RESTYPES = {"gc_last_error": ctypes.c_char_p, "gc_launch_count": ctypes.c_uint6
              "gc_panel_tma_item_elems": ctypes.c_int64, "gc_krylov_partials": ctypes.c_int64}
 
 EXPORTED = tuple(_SIGNATURES)
-ABI_VERSION = 1
+ABI_VERSION = 2
 
 _lib = None
 

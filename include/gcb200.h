@@ -210,8 +210,9 @@ int gc_segmv(int64_t nseg, const int64_t* seg, const int64_t* blk,
  * out_off, T, nrows, mode, red_slot, 0) computes
  *     s[t] = sum_{r < nrows} A[a_off + r*T + t] * in[xidx[xi_off + r]]
  * over a contiguous row-major chunk of a panel (A = A1 if mode&1, in = in1
- * if mode&2) and writes s to out[out_off + t] (mode&4; added to it if
- * mode&8) or, for a panel split over several items, to scratch[out_off+t].
+ * if mode&2; in = in0 + in1 if mode&32) and writes s to out[out_off + t]
+ * (mode&4; added to it if mode&8) or, for a panel split over several
+ * items, to scratch[out_off+t].
  * red (nred,5) = out_off, T, scratch_off, nitems, accumulate describes each
  * split panel; the last item of a panel to finish (arrivals[red_slot], an
  * int32 counter that must start at 0 and is re-armed by the kernel) sums
@@ -269,6 +270,19 @@ int gc_panel_tma(int64_t nitems, const int64_t* items, const int32_t* xidx,
                  const int64_t* red, int32_t* arrivals, int32_t priority, uint64_t* trace,
                  void* stream);
 int64_t gc_panel_tma_item_elems(void);
+
+/* Tiered transforms (plan time; h2.py PanelPlan tiers): the composed
+ * transfers of a tier of tree heights, one height per call.  desc [dev]
+ * (n,6) = s_off, m, kc, e_off, ku, out_off:
+ *     M[out_off..] (m x ku) = M[s_off..] (m x kc) @ V[e_off..] (kc x ku)
+ * or, s_off < 0, a copy of the m x ku block V[e_off..] (row-major, each
+ * entry summed over kc in order).  gc_block_transpose: desc [dev] (n,5) =
+ * src_off, ld, rows, cols, dst_off: dst[dst_off + c*rows + r] =
+ * src[src_off + r*ld + c] (the backward transform's regrouped blocks).
+ * Follows the nested-basis recursion of gca.py:162-220 multiplied out. */
+int gc_tier_compose(int64_t n, const int64_t* desc, const double* V, double* M, void* stream);
+int gc_block_transpose(int64_t n, const int64_t* desc, const double* src, double* dst,
+                       void* stream);
 
 /* Piecewise-linear basis (assembly.py:54-135, 175-214, 279-304;
  * batchexec.py:178-209).  gc_lin_pairs: tasks [dev] (n,2) triangle pairs

@@ -55,6 +55,8 @@ _SIGNATURES = {
     "gc_scatter": [c_p, c_p, c_i64, c_p, c_p],
     "gc_scatter2": [c_p, c_p, c_p, c_i64, c_p, c_p],
     "gc_expand_ranges": [c_i64, c_p, c_p, c_p, c_p, c_p],
+    "gc_tier_compose": [c_i64, c_p, c_p, c_p, c_p],
+    "gc_block_transpose": [c_i64, c_p, c_p, c_p, c_p],
     "gc_segmv": [c_i64, c_p, c_p, c_p, c_p, c_p, c_p, c_p, ctypes.c_int, c_i64, c_p],
     "gc_panelmv": [c_i64, c_p, c_p, c_p, c_p, c_p, c_p, c_p, c_p, c_i64, c_p, c_p, ctypes.c_int32,
                    ctypes.c_int32, c_p, c_p],

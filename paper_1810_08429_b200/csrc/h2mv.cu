@@ -107,7 +107,8 @@ constexpr int PAN_MAX_ROWS = 1024;   // rows per work item (x gathered to smem)
 
 // item (8 x int64): a_off, xi_off, out_off, T, nrows, mode, red, 0
 //   mode bit0 A1, bit1 in1, bit2 direct to out, bit3 accumulate into out,
-//   bit4 prefetch the item's matrix chunk into L2 before the input gather;
+//   bit4 prefetch the item's matrix chunk into L2 before the input gather,
+//   bit5 the input is in0 + in1 (both at the gathered indices);
 //   red = reduction slot of a split panel (items without bit2 write partial
 //   sums to scratch[out_off..]).
 // red slot (5 x int64): out_off, T, scratch_off, nitems, accumulate.
@@ -174,7 +175,12 @@ __device__ __forceinline__ void panel_item(const PanelPhase& P, int64_t item, Pa
         if (staged)
             for (int r = threadIdx.x; r < nrows; r += PAN_THREADS) xsi[r] = __ldg(xi + r);
         asm volatile("griddepcontrol.wait;" ::: "memory");
-        if (staged) {
+        if (mode & 32) {
+            for (int r = threadIdx.x; r < nrows; r += PAN_THREADS) {
+                const int i = staged ? xsi[r] : __ldg(xi + r);
+                sm.xs[r] = __ldcg(P.in0 + i) + __ldcg(P.in1 + i);
+            }
+        } else if (staged) {
             for (int r = threadIdx.x; r < nrows; r += PAN_THREADS) sm.xs[r] = __ldcg(x + xsi[r]);
         } else {
             for (int r = threadIdx.x; r < nrows; r += PAN_THREADS) sm.xs[r] = __ldcg(x + __ldg(xi + r));
@@ -183,7 +189,14 @@ __device__ __forceinline__ void panel_item(const PanelPhase& P, int64_t item, Pa
         // bulk: start the item's matrix stream (L2 prefetch of the whole
         // chunk) before the dependent index -> input gather
         if (mode & 16) prefetch_l2(A, 8 * (int64_t)nrows * T);
-        for (int r = threadIdx.x; r < nrows; r += PAN_THREADS) sm.xs[r] = __ldcg(x + __ldg(xi + r));
+        if (mode & 32) {
+            for (int r = threadIdx.x; r < nrows; r += PAN_THREADS) {
+                const int i = __ldg(xi + r);
+                sm.xs[r] = __ldcg(P.in0 + i) + __ldcg(P.in1 + i);
+            }
+        } else {
+            for (int r = threadIdx.x; r < nrows; r += PAN_THREADS) sm.xs[r] = __ldcg(x + __ldg(xi + r));
+        }
     }
     __syncthreads();
     const int tt = T < PAN_THREADS ? T : PAN_THREADS;
@@ -249,7 +262,7 @@ __device__ __forceinline__ void panel_item(const PanelPhase& P, int64_t item, Pa
 // then wait on SM slots); 2: after the CTA's item is done (the dependent
 // only overlaps this kernel's drain and keeps its slots free for the bulk).
 template <bool CHAIN, int TRIGGER>
-__global__ void __launch_bounds__(PAN_THREADS) k_panelmv(PanelPhase P) {
+__global__ void __launch_bounds__(PAN_THREADS, 6) k_panelmv(PanelPhase P) {
     __shared__ PanelSmem sm;
     if (CHAIN && TRIGGER == 1) asm volatile("griddepcontrol.launch_dependents;");
     if (P.trace != nullptr && threadIdx.x == 0) atomicMin(P.trace, globaltimer());

@@ -493,9 +493,13 @@ class PanelPlan:
         self.y = torch.zeros(self.n_out, **f64)
         self.xt = torch.zeros(self.n_in, **f64)
         self.yt = torch.zeros(self.n_out, **f64)
-        self.yt2 = torch.zeros(self.n_out, **f64)     # leaf-basis part, summed in the scatter
         self.xhat = torch.zeros(max(cs.coef_size, 1), **f64)
-        self.yhat = torch.zeros(max(rs.coef_size, 1), **f64)
+        self._keep = []
+        ny = max(rs.coef_size, 1)
+        # y-hat | y-hat from the tiers above | leaf-basis part of y (summed
+        # in the scatter): one buffer, zeroed by one memset per product
+        self._ybuf = torch.zeros(2 * ny + self.n_out, **f64)
+        self.yhat, self.yhat_t, self.yt2 = self._ybuf[:ny], self._ybuf[ny:2 * ny], self._ybuf[2 * ny:]
         # "pdl": one launch per transform level; "persistent": runs of levels
         # in one co-resident launch with grid barriers (experimental)
         self.chain_mode = os.environ.get("GC_CHAIN_MODE", "pdl")
@@ -581,8 +585,13 @@ class PanelPlan:
             panels = panels[:5] + (0,)
             leafp = self._phase("leafbasis", 0, panels, rs.VT, None, self.yhat, None, self.yt2,
                                 transform=True)
-        self._fwd, self._cpl, self._bwd, self._near, self._leaf = fwd, cpl, bwd, near, leafp
-        self.phases = [P for P in [near] + fwd + [c for c, _ in cpl] + [b for b, _ in bwd] + [leafp]
+        self.tiers = None
+        parts = [(leafp, None)]
+        if self.chain_mode == "pdl" and os.environ.get("GC_TIERS", "auto") != "off":
+            fwd, bwd, parts = self._tiered(h, fwd, bwd, leafp)
+        parts = [(P, hs) for P, hs in parts if P is not None and P.nitems]
+        self._fwd, self._cpl, self._bwd, self._near, self._leafparts = fwd, cpl, bwd, near, parts
+        self.phases = [P for P in [near] + fwd + [c for c, _ in cpl] + [b for b, _ in bwd] + [p for p, _ in parts]
                        if P is not None and P.nitems > 0]
         # the chain gets the highest stream priority so its CTAs are
         # scheduled ahead of the queued bulk (coupling buckets, near field)
@@ -591,11 +600,67 @@ class PanelPlan:
         least, greatest = _native.ctypes.c_int32(0), _native.ctypes.c_int32(0)
         _native.call("gc_priority_range", _native.ctypes.byref(least), _native.ctypes.byref(greatest))
         self._prio = (least.value, greatest.value)
-        self._keep = []
         self._barrier = torch.zeros(1, dtype=torch.int32, device=dev)
         self.trace = {}                    # id(phase) -> [2] int64 (profiling only)
         self.nodes = self._build_nodes()
         self.graph = None
+
+    def _tiered(self, h, fwd, bwd, leafp):
+        """Replace the level-by-level transforms by tiers (tiers.py): one
+        launch per tier and direction, on the chain.  The lowest tier's
+        backward writes the leaf rows of y (yt2) directly.  Returns (forward
+        phases, backward (phase, bucket heights) top down, leaf parts
+        (phase, bucket heights or None = all)).  Measured and rejected:
+        the lowest tier split into one launch per height on parallel
+        streams (forward) and per ancestor height accumulating as its
+        bucket completes (backward) - 165 us against 136 us at sphere L6:
+        the 4 x 2048 small leaf panels queue behind the bulk."""
+        from . import tiers as T_
+        rs, cs = h.row_basis.store, h.col_basis.store
+        rf, cf = h.row_tree.flat, h.col_tree.flat
+        d = h.dev
+        self._tier_split = os.environ.get("GC_TIER_SPLIT", "0") == "1"
+        cb, rb = T_.choose_tiers(cs, cf), T_.choose_tiers(rs, rf)
+        if not cb or not rb:
+            return fwd, bwd, [(leafp, None)]
+        ct = T_.StoreTiers(cs, cf, cb, self.dev)
+        rt = ct if (rs is cs and rb == cb) else T_.StoreTiers(rs, rf, rb, self.dev)
+        groups, MT = rt.transposed(self.dev)
+        if rt is not ct:
+            rt.M = None                                  # only the transposed blocks are used
+        self.tiers = dict(col=cb, row=rb, fwd_elems=ct.elems, bwd_elems=int(MT.numel()))
+        self._keep.extend([ct.M, MT])
+        kw = dict(transform=True, split=self._tier_split)
+        nfwd = []
+        for t in ct.tiers:
+            u, f, w, nodes = t["u"], t["f"], t["w"], t["nodes"]
+            low = t["lo"] < 0
+            starts = cf.start[f] if low else cs.coef_off[f]
+            panels = (t["moff"][nodes], t["m"][nodes], cs.rank[nodes], (starts, w), cs.coef_off[nodes], 0)
+            nfwd.append(self._phase("forward", t["hi"], panels, ct.M, None, self.xt if low else self.xhat,
+                                    None, self.xhat, **kw))
+        nbwd, parts = [], []
+        for t, g in reversed(list(zip(rt.tiers, groups))):
+            first, uu, ff, ww, dst = g["first"], g["u"], g["f"], g["w"], g["dst"]
+            if not first.size:
+                continue
+            cnt = np.diff(np.r_[first, len(ff)])
+            elems = ff[first]
+            low = t["lo"] < 0
+            keep = np.ones(len(elems), bool)
+            if low and d.row_range is not None:
+                keep = (rf.start[elems] >= d.row_range[0]) & (rf.stop[elems] <= d.row_range[1])
+            K = np.add.reduceat(rs.rank[uu], first)
+            sel = np.repeat(keep, cnt)
+            panels = (dst[first][keep], K[keep], ww[first][keep], (rs.coef_off[uu][sel], rs.rank[uu][sel]),
+                      (rf.start[elems] if low else rs.coef_off[elems])[keep], 0)
+            P = self._phase("leafbasis" if low else "backward", t["hi"], panels, MT, None, self.yhat,
+                            self.yhat_t, self.yt2 if low else self.yhat_t, sum_inputs=True, **kw)
+            if low:
+                parts.append((P, None))
+            else:
+                nbwd.append((P, set(range(t["lo"] + 1, t["hi"] + 1))))
+        return nfwd, nbwd, parts
 
     # -- DAG -----------------------------------------------------------------
     def _split_height(self):
@@ -663,7 +728,7 @@ class PanelPlan:
         S = self._split_height()
         least, greatest = self._prio
         levels = least - greatest
-        z = add(_Node("zero", "chain", fn=lambda: self.yhat.zero_()))
+        z = add(_Node("zero", "chain", fn=lambda: self._ybuf.zero_()))
         if gather:
             g = add(_Node("gather", "chain", [z], fn=lambda: _native.call(
                 "gc_gather", ptr(self.x), ptr(self.perm_in), self.n_in, ptr(self.xt), st())))
@@ -686,15 +751,15 @@ class PanelPlan:
         bucket = {}
         for P, colh in sorted(self._cpl, key=lambda c: c[0].height):
             if gate is not None:
-                dep = gate
+                dep = [gate]
             else:
-                dep = next((k for hh, k in fwd_done if hh >= colh), last)
+                dep = [next((k for hh, k in fwd_done if hh >= colh), last)]
             if P.height >= S or levels < 2:
                 prio = greatest
             else:
                 prio = least - 1 - int(round(P.height * (levels - 2) / max(S - 1, 1)))
                 prio = min(least - 1, max(greatest + 1, prio))
-            bucket[P.height] = add(_Node("coupling", "c%d" % P.height, [dep, z], phase=P, priority=prio))
+            bucket[P.height] = add(_Node("coupling", "c%d" % P.height, dep + [z], phase=P, priority=prio))
         prev = gate if gate is not None else last
         groups = ([[b for b in self._bwd if b[0].height > S], [b for b in self._bwd if b[0].height <= S]]
                   if persistent else [[b] for b in self._bwd])
@@ -705,10 +770,10 @@ class PanelPlan:
             k = add_steps("backward", [P for P, _ in grp], [prev] + [bucket[x] for x in need if x in bucket])
             if k is not None:
                 prev = k
+        for P, hs in self._leafparts:
+            need = list(bucket.values()) if hs is None else [bucket[x] for x in sorted(hs) if x in bucket]
+            prev = add(_Node("leafbasis", "chain", [prev] + need, phase=P, priority=greatest))
         tail = [prev] + list(bucket.values())
-        if self._leaf is not None and self._leaf.nitems:
-            prev = add(_Node("leafbasis", "chain", tail, phase=self._leaf, priority=greatest))
-            tail = [prev]
         if near is not None:
             tail = tail + [near]
         if scatter:
@@ -769,7 +834,8 @@ class PanelPlan:
             main.wait_event(events[last])
 
     # -- phases --------------------------------------------------------------
-    def _phase(self, name, height, panels, A0, A1, in0, in1, out, transform=False):
+    def _phase(self, name, height, panels, A0, A1, in0, in1, out, transform=False, sum_inputs=False,
+               split=False):
         a_off, K, T, rows, out_off, accumulate = panels
         a_off = np.asarray(a_off, np.int64)
         K = np.asarray(K, np.int64)
@@ -777,7 +843,12 @@ class PanelPlan:
         out_off = np.asarray(out_off, np.int64)
         n = len(a_off)
         elems = int((K * T).sum())
-        if transform:
+        if transform and split:
+            # tier transforms: bandwidth phases on the chain - split large
+            # panels like the bulk so the launch fills the SMs
+            target = max(1024, min(_ITEM_ELEMS, elems // (148 * 4) + 1))
+            max_rows = _ITEM_MAX_ROWS
+        elif transform:
             # transform levels: one item per panel (split only past the row
             # cap) - these levels are latency-bound, and a split panel costs
             # a second pass over L2 for its reduction
@@ -817,12 +888,16 @@ class PanelPlan:
         direct = ~multi[item_panel]
         out_col = np.where(direct, out_off[item_panel],
                            scr_off[item_panel] + item_idx_in_panel * T[item_panel])
-        mode = np.where(direct, 4 | (8 * accumulate), 0)
+        mode = np.where(direct, 4 | (8 * accumulate), 0) | (32 if sum_inputs else 0)
         if not transform and os.environ.get("GC_BULK_PREFETCH", "0") == "1":
             mode = mode | 16
         items = np.stack([a_off[item_panel] + item_k * T[item_panel], xoff[item_panel] + item_k,
                           out_col, T[item_panel], item_rows, mode,
                           np.where(direct, -1, slot[item_panel]), np.zeros_like(mode)], 1)
+        if transform and len(items) and os.environ.get("GC_LPT", "0") == "1":
+            # largest items first (CTAs dispatch in launch order): measured
+            # -6 % at sphere L4, +1-3 % at L6-L8, so off by default
+            items = items[np.argsort(-(items[:, 3] * items[:, 4]), kind="stable")]
         red = np.stack([out_off[multi], T[multi], scr_off[multi], nit[multi],
                         np.full(int(multi.sum()), accumulate)], 1)
         P = _Phase()

@@ -388,6 +388,38 @@ def test_cg_solve_device_matches_host_cg():
     assert np.array_equal(rd.x, rd2.x)
 
 
+@pytest.mark.parametrize("geo,level,cfg_kw", [
+    ("sphere", 5, dict(eps=1e-6)), ("cube", 4, dict(eps=1e-6)),
+    ("sphere", 4, dict(eps=1e-4, basis="linear")),
+    ("sphere", 3, dict(eps=1e-4, basis="linear", disc="collocation"))])
+def test_tiered_transforms_match_level_by_level(geo, level, cfg_kw, monkeypatch):
+    """Tiered transforms (tiers.py: composed transfers, one launch per tier)
+    == the level-by-level nested-basis recursion (GC_TIERS=off) to rounding,
+    for automatic and forced tier boundaries, symmetric and row != column
+    bases; graph replay == serial eager bitwise."""
+    mesh = (geometry.build_sphere_mesh if geo == "sphere" else geometry.build_cube_mesh)(level)
+    hm, _, _ = cli.build_h2_operator(mesh, cli.default_config(**cfg_kw))
+    n = hm.shape[1]
+    x = torch.from_numpy(np.random.default_rng(3).standard_normal(n)).cuda()
+    monkeypatch.setenv("GC_TIERS", "off")
+    p0 = h2.PanelPlan(hm)
+    assert p0.tiers is None
+    y0 = torch.empty(hm.shape[0], dtype=torch.float64, device="cuda")
+    p0.run(x, y0, serial=True)
+    for tiers in ("auto", "0", "1,3", "0,2,4", "2"):
+        monkeypatch.setenv("GC_TIERS", tiers)
+        p = h2.PanelPlan(hm)
+        assert p.tiers is not None
+        y1, y2 = torch.empty_like(y0), torch.empty_like(y0)
+        p.run(x, y1, serial=True)
+        p.capture()
+        p.run(x, y2)
+        p.run(x, y2)
+        torch.cuda.synchronize()
+        assert torch.equal(y1, y2), tiers
+        assert (y1 - y0).norm().item() <= 1e-13 * y0.norm().item(), tiers
+
+
 def _sharded_worker(rank, world, port, out_dir):
     import os
     import torch.distributed as dist

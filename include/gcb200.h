@@ -189,6 +189,21 @@ int gc_gather(const double* x, const int64_t* perm, int64_t n, double* xt,
 /* y[perm[i]] = yt[i] (h2.py:78-79) */
 int gc_scatter(const double* yt, const int64_t* perm, int64_t n, double* y,
                void* stream);
+/* y[perm[i]] = yt[i] + yt2[i] (the panel plan's two output parts) */
+int gc_scatter2(const double* yt, const double* yt2, const int64_t* perm, int64_t n, double* y,
+                void* stream);
+/* out[off[s] + j] = start[s] + j for j < len[s]: index ranges expanded to a
+ * panel phase's input index list (int32) */
+int gc_expand_ranges(int64_t m, const int64_t* start, const int64_t* len, const int64_t* off,
+                     int32_t* out, void* stream);
+/* Re-point argument `arg` of the gather (kernel 0, gc_gather) or scatter
+ * (kernel 1, gc_scatter2) kernel nodes of an instantiated CUDA graph whose
+ * captured value is old_ptr to new_ptr in the executable graph
+ * (cudaGraphExecKernelNodeSetParams; the graph itself keeps old_ptr): a captured
+ * product reads / writes caller buffers without copies.  graph / exec =
+ * cudaGraph_t / cudaGraphExec_t; *count = nodes updated. */
+int gc_graph_retarget(void* graph, void* exec, int32_t kernel, int32_t arg, const void* old_ptr,
+                      const void* new_ptr, int32_t* count);
 
 /* Segmented block-row product, the single kernel form behind every matvec
  * phase.  For segment s = (out_off, T, blk_begin, blk_end):
@@ -273,14 +288,18 @@ int64_t gc_panel_tma_item_elems(void);
 
 /* Tiered transforms (plan time; h2.py PanelPlan tiers): the composed
  * transfers of a tier of tree heights, one height per call.  desc [dev]
- * (n,6) = s_off, m, kc, e_off, ku, out_off:
+ * (n,6) = s_off, m, kc, e_off, ku, out_off, cut into tiles [dev] (ntiles,2)
+ * = descriptor index, first output entry (every gc_tier_tile() entries of
+ * each descriptor's m x ku block):
  *     M[out_off..] (m x ku) = M[s_off..] (m x kc) @ V[e_off..] (kc x ku)
  * or, s_off < 0, a copy of the m x ku block V[e_off..] (row-major, each
  * entry summed over kc in order).  gc_block_transpose: desc [dev] (n,5) =
  * src_off, ld, rows, cols, dst_off: dst[dst_off + c*rows + r] =
  * src[src_off + r*ld + c] (the backward transform's regrouped blocks).
  * Follows the nested-basis recursion of gca.py:162-220 multiplied out. */
-int gc_tier_compose(int64_t n, const int64_t* desc, const double* V, double* M, void* stream);
+int gc_tier_compose(int64_t ntiles, const int64_t* tiles, const int64_t* desc, const double* V,
+                    double* M, void* stream);
+int64_t gc_tier_tile(void);
 int gc_block_transpose(int64_t n, const int64_t* desc, const double* src, double* dst,
                        void* stream);
 

@@ -55,7 +55,9 @@ _SIGNATURES = {
     "gc_scatter": [c_p, c_p, c_i64, c_p, c_p],
     "gc_scatter2": [c_p, c_p, c_p, c_i64, c_p, c_p],
     "gc_expand_ranges": [c_i64, c_p, c_p, c_p, c_p, c_p],
-    "gc_tier_compose": [c_i64, c_p, c_p, c_p, c_p],
+    "gc_tier_compose": [c_i64, c_p, c_p, c_p, c_p, c_p],
+    "gc_tier_tile": [],
+    "gc_graph_retarget": [c_p, c_p, ctypes.c_int32, ctypes.c_int32, c_p, c_p, c_p],
     "gc_block_transpose": [c_i64, c_p, c_p, c_p, c_p],
     "gc_segmv": [c_i64, c_p, c_p, c_p, c_p, c_p, c_p, c_p, ctypes.c_int, c_i64, c_p],
     "gc_panelmv": [c_i64, c_p, c_p, c_p, c_p, c_p, c_p, c_p, c_p, c_i64, c_p, c_p, ctypes.c_int32,
@@ -100,6 +102,7 @@ _SIGNATURES = {
     "gc_dfma_probe": [c_i64, c_i64, c_i64, c_p, c_p],
 }
 _RESTYPES = {"gc_last_error": ctypes.c_char_p, "gc_launch_count": ctypes.c_uint64,
+             "gc_tier_tile": ctypes.c_int64,
              "gc_reset_launch_count": None, "gc_panel_phase_bytes": ctypes.c_int64,
              "gc_panel_tma_item_elems": ctypes.c_int64, "gc_krylov_partials": ctypes.c_int64}
 

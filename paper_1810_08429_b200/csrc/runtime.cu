@@ -142,6 +142,54 @@ int gc_scatter2(const double* yt, const double* yt2, const int64_t* perm, int64_
     return GC_OK;
 }
 
+// Re-point a pointer argument of the gather / scatter kernel nodes of an
+// instantiated CUDA graph (cudaGraphExecKernelNodeSetParams): the product
+// graph then reads the caller's x and writes the caller's y directly, with
+// no device copies around the replay.  kernel 0 = k_gather (4 arguments),
+// 1 = k_scatter2 (5); only nodes whose captured argument `arg` (the value
+// in the graph, which exec updates do not change) equals old_ptr change.
+// *count = nodes updated.
+int gc_graph_retarget(void* graph, void* exec, int32_t kernel, int32_t arg, const void* old_ptr,
+                      const void* new_ptr, int32_t* count) {
+    const void* fn = kernel == 0 ? (const void*)k_gather : kernel == 1 ? (const void*)k_scatter2 : nullptr;
+    const int nargs = kernel == 0 ? 4 : 5;
+    if (!fn || arg < 0 || arg >= nargs || !graph || !exec) {
+        set_error(GC_ERR_CONFIG, "gc_graph_retarget: bad kernel/arg/graph");
+        return GC_ERR_CONFIG;
+    }
+    // captured nodes may carry the host stub or the driver function handle
+    cudaFunction_t drv = nullptr;
+    if (cudaGetFuncBySymbol(&drv, fn) != cudaSuccess) drv = nullptr;
+    size_t n = 0;
+    cudaError_t e = cudaGraphGetNodes((cudaGraph_t)graph, nullptr, &n);
+    if (e != cudaSuccess) return cuda_status(e, "gc_graph_retarget nodes");
+    cudaGraphNode_t stack_nodes[256];
+    cudaGraphNode_t* nodes = n <= 256 ? stack_nodes : (cudaGraphNode_t*)malloc(n * sizeof(cudaGraphNode_t));
+    e = cudaGraphGetNodes((cudaGraph_t)graph, nodes, &n);
+    int32_t cnt = 0;
+    for (size_t i = 0; e == cudaSuccess && i < n; ++i) {
+        cudaGraphNodeType t;
+        if (cudaGraphNodeGetType(nodes[i], &t) != cudaSuccess || t != cudaGraphNodeTypeKernel) continue;
+        cudaKernelNodeParams p;
+        if (cudaGraphKernelNodeGetParams(nodes[i], &p) != cudaSuccess) continue;
+        if (p.func != fn && (drv == nullptr || p.func != (void*)drv)) continue;
+        if (*(void* const*)p.kernelParams[arg] != old_ptr) continue;
+        void* args[5];
+        for (int a = 0; a < nargs; ++a) args[a] = p.kernelParams[a];
+        void* nv = const_cast<void*>(new_ptr);
+        args[arg] = &nv;
+        p.kernelParams = args;
+        p.extra = nullptr;
+        e = cudaGraphExecKernelNodeSetParams((cudaGraphExec_t)exec, nodes[i], &p);
+        ++cnt;
+    }
+    if (nodes != stack_nodes) free(nodes);
+    (void)cudaGetLastError();
+    if (e != cudaSuccess) return cuda_status(e, "gc_graph_retarget");
+    if (count) *count = cnt;
+    return GC_OK;
+}
+
 int gc_surface_points(const double* corners, int64_t nt, const double* n6, int64_t mq,
                       double* xq, void* stream) {
     if (nt <= 0) return GC_OK;

@@ -23,20 +23,27 @@ constexpr int TIER_THREADS = 256;
 //   out[m x ku] = S[m x kc] @ E[kc x ku]   (S = M + s_off, E = V + e_off)
 //   or, s_off < 0, out = E[m x ku] (copy)
 // all row-major; each output entry sums over kc in order (deterministic).
-__global__ void __launch_bounds__(TIER_THREADS) k_tier_compose(int64_t n, const int64_t* __restrict__ desc,
+// Work is cut into tiles of TIER_TILE outputs: tile (2 x int64) = desc
+// index, first output; one CTA per tile (the top nodes' blocks are large).
+constexpr int TIER_TILE = 1024;
+
+__global__ void __launch_bounds__(TIER_THREADS) k_tier_compose(int64_t ntiles, const int64_t* __restrict__ tiles,
+                                                               const int64_t* __restrict__ desc,
                                                                const double* __restrict__ V, double* M) {
-    for (int64_t b = blockIdx.x; b < n; b += gridDim.x) {
-        const int64_t* d = desc + 6 * b;
+    for (int64_t b = blockIdx.x; b < ntiles; b += gridDim.x) {
+        const int64_t* d = desc + 6 * tiles[2 * b];
+        const int64_t e0 = tiles[2 * b + 1];
         const int64_t s_off = d[0], m = d[1], kc = d[2], e_off = d[3], ku = d[4], o_off = d[5];
         const double* __restrict__ E = V + e_off;
         double* out = M + o_off;
         const int64_t total = m * ku;
+        const int64_t e1 = e0 + TIER_TILE < total ? e0 + TIER_TILE : total;
         if (s_off < 0) {
-            for (int64_t e = threadIdx.x; e < total; e += TIER_THREADS) out[e] = E[e];
+            for (int64_t e = e0 + threadIdx.x; e < e1; e += TIER_THREADS) out[e] = E[e];
             continue;
         }
         const double* S = M + s_off;
-        for (int64_t e = threadIdx.x; e < total; e += TIER_THREADS) {
+        for (int64_t e = e0 + threadIdx.x; e < e1; e += TIER_THREADS) {
             const int64_t i = e / ku, j = e - i * ku;
             const double* Si = S + i * kc;
             double acc = 0.0;
@@ -65,17 +72,21 @@ __global__ void __launch_bounds__(TIER_THREADS) k_block_transpose(int64_t n, con
 
 using namespace gcb;
 
-// One height of a tier's composition: n descriptors (6 x int64, [dev]);
-// M may be read (children's blocks, written by an earlier call) and written
-// (this height's blocks) - the regions are disjoint.
-extern "C" int gc_tier_compose(int64_t n, const int64_t* desc, const double* V, double* M, void* stream) {
-    if (n <= 0) return GC_OK;
-    if (!desc || !V || !M) { set_error(GC_ERR_CONFIG, "gc_tier_compose: null argument"); return GC_ERR_CONFIG; }
-    const int64_t grid = n < 148 * 8 ? n : 148 * 8;
-    k_tier_compose<<<(unsigned)grid, TIER_THREADS, 0, (cudaStream_t)stream>>>(n, desc, V, M);
+// One height of a tier's composition: n descriptors (6 x int64, [dev]) cut
+// into ntiles tiles (2 x int64, [dev]: descriptor, first output; see
+// gc_tier_tile); M may be read (children's blocks, written by an earlier
+// call) and written (this height's blocks) - the regions are disjoint.
+extern "C" int gc_tier_compose(int64_t ntiles, const int64_t* tiles, const int64_t* desc, const double* V,
+                               double* M, void* stream) {
+    if (ntiles <= 0) return GC_OK;
+    if (!tiles || !desc || !V || !M) { set_error(GC_ERR_CONFIG, "gc_tier_compose: null argument"); return GC_ERR_CONFIG; }
+    const int64_t grid = ntiles < 148 * 16 ? ntiles : 148 * 16;
+    k_tier_compose<<<(unsigned)grid, TIER_THREADS, 0, (cudaStream_t)stream>>>(ntiles, tiles, desc, V, M);
     GC_CHECK_LAUNCH("k_tier_compose");
     return GC_OK;
 }
+
+extern "C" int64_t gc_tier_tile(void) { return TIER_TILE; }
 
 extern "C" int gc_block_transpose(int64_t n, const int64_t* desc, const double* src, double* dst, void* stream) {
     if (n <= 0) return GC_OK;

@@ -22,7 +22,7 @@ import numpy as np
 
 from . import _native
 from .device import empty, ptr, stream_handle, to_dev, torch
-from .errors import ConfigError
+from .errors import ConfigError, StateError
 
 __all__ = ["mvm", "mvm_t", "as_operator", "storage_report", "storage_csv_rows",
            "spectral_error_estimate", "cg_solve", "cgnr_solve", "CGResult", "MatvecPlan"]
@@ -244,6 +244,7 @@ def mvm(h, x):
     with torch.cuda.device(p.dev):
         p.x.copy_(p.pin_x, non_blocking=True)
         if p.graph is not None:
+            p.bind(p.x, p.y)
             p.graph.replay()
         else:
             p._body()
@@ -442,7 +443,7 @@ _ITEM_ELEMS = int(os.environ.get("GC_ITEM_ELEMS", 16384))  # ~128 KB of matrix d
 _ITEM_MAX_ROWS = 1024       # PAN_MAX_ROWS in csrc/h2mv.cu
 _WARP_MAX_ROWS = 256        # WARP_MAX_ROWS in csrc/h2mv.cu
 _STREAM_MAX_T = 1024        # ST_MAX_T in csrc/h2mv.cu
-_RESIDENT = 148 * 8         # resident k_panelmv CTAs (32 registers, 256 threads)
+_RESIDENT = 148 * 6         # resident k_panelmv CTAs (40 registers, 256 threads, 6 per SM)
 
 
 class _Phase:
@@ -620,7 +621,8 @@ class PanelPlan:
         rf, cf = h.row_tree.flat, h.col_tree.flat
         d = h.dev
         self._tier_split = os.environ.get("GC_TIER_SPLIT", "0") == "1"
-        cb, rb = T_.choose_tiers(cs, cf), T_.choose_tiers(rs, rf)
+        cb = T_.choose_tiers(cs, cf)
+        rb = cb if (rs is cs and rf is cf) else T_.choose_tiers(rs, rf)
         if not cb or not rb:
             return fwd, bwd, [(leafp, None)]
         ct = T_.StoreTiers(cs, cf, cb, self.dev)
@@ -861,7 +863,7 @@ class PanelPlan:
         else:
             # chunk rows so every phase has >= ~4 items per SM when it can
             target = max(256, min(_ITEM_ELEMS, elems // (148 * 4) + 1))
-            if self._balance_waves and elems > _ITEM_ELEMS * _RESIDENT:
+            if self._balance_waves and elems > _ITEM_ELEMS * _RESIDENT // 2:
                 # whole waves: ~k x (resident CTAs) items of <= _ITEM_ELEMS
                 waves = -(-elems // (_ITEM_ELEMS * _RESIDENT))
                 target = -(-elems // (waves * _RESIDENT))
@@ -968,24 +970,63 @@ class PanelPlan:
         # capture_begin/end on a side stream directly: torch.cuda.graph()
         # would empty the caching allocator first (and the assembly's next
         # allocations would pay cudaMalloc again)
-        g = torch.cuda.CUDAGraph()
+        g = torch.cuda.CUDAGraph(keep_graph=os.environ.get("GC_KEEP_GRAPH", "1") == "1")
         with torch.cuda.stream(s):
             g.capture_begin()
             try:
                 self._body()
             finally:
                 g.capture_end()
+        if os.environ.get("GC_KEEP_GRAPH", "1") == "1":
+            g.instantiate()
         torch.cuda.current_stream().wait_stream(s)
         torch.cuda.synchronize(self.dev)
         self.graph = g
+        # the gather / scatter nodes read self.x / write self.y until run()
+        # re-points them at the caller's buffers (gc_graph_retarget)
+        self._captured = [self.x.data_ptr(), self.y.data_ptr()]
+        self._bound = list(self._captured)
         return g
+
+    def bind(self, x_dev, y_dev):
+        """Point the captured graph's input gather at x_dev and its output
+        scatter at y_dev (contiguous float64 device vectors of this plan's
+        sizes; they must stay alive until the replays that use them ran).
+        Returns False (nothing changed) when the graph has no such nodes."""
+        if self.graph is None or os.environ.get("GC_KEEP_GRAPH", "1") != "1":
+            return False
+        want = [x_dev.data_ptr(), y_dev.data_ptr()]
+        for slot, (kernel, arg) in enumerate(((0, 0), (1, 4))):
+            if want[slot] == self._bound[slot]:
+                continue
+            cnt = _native.ctypes.c_int32(0)
+            _native.call("gc_graph_retarget", _native.ctypes.c_void_p(self.graph.raw_cuda_graph()),
+                         _native.ctypes.c_void_p(self.graph.raw_cuda_graph_exec()), kernel, arg,
+                         _native.ctypes.c_void_p(self._captured[slot]), _native.ctypes.c_void_p(want[slot]),
+                         _native.ctypes.byref(cnt))
+            if cnt.value != 1:
+                raise StateError("product graph: %d gather/scatter nodes re-pointed (expected 1)" % cnt.value)
+            self._bound[slot] = want[slot]
+        return True
+
+    def _direct_ok(self, x_dev, y_dev):
+        return (self.graph is not None and x_dev.is_contiguous() and y_dev.is_contiguous()
+                and x_dev.dtype == torch.float64 and y_dev.dtype == torch.float64
+                and x_dev.device == self.x.device and y_dev.device == self.y.device
+                and x_dev.numel() == self.n_in and y_dev.numel() == self.n_out
+                and x_dev.data_ptr() != y_dev.data_ptr())
 
     def run(self, x_dev, y_dev, phase_events=None, phase="coupling", serial=False):
         """y_dev = H x_dev (device vectors, external ordering).  With
         ``phase_events`` (or ``serial``) every node runs in order on the
         current stream and the events bracket the named phase's kernels."""
+        if phase_events is None and not serial and self._direct_ok(x_dev, y_dev):
+            self.bind(x_dev, y_dev)                  # graph reads x_dev, writes y_dev: no copies
+            self.graph.replay()
+            return
         self.x.copy_(x_dev, non_blocking=True)
         if phase_events is None and not serial and self.graph is not None:
+            self.bind(self.x, self.y)
             self.graph.replay()
         else:
             self._exec(self.nodes, serial=serial or phase_events is not None,

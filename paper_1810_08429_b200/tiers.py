@@ -102,11 +102,20 @@ def choose_tiers(store, flat, latency_s=None):
     if env not in ("auto", ""):
         return sorted({min(int(v), top) for v in env.split(",")} | {top})
     lat = latency_s if latency_s is not None else float(os.environ.get("GC_TIER_LAT_US", "5")) * 1e-6
+    # elems(lo, hi) for every hi from ONE walk per lo: the pairs of tier
+    # (lo, hi] are those of (lo, top] whose u lies at height <= hi
+    cost = {}
+    for lo in range(-1, top):
+        u, f, wmap = _pairs(store, flat, lo, top)
+        per_h = np.bincount(flat.height[u], weights=(wmap[f] * store.rank[u]).astype(np.float64),
+                            minlength=top + 1)
+        acc = np.cumsum(per_h)
+        for hi in range(lo + 1, top + 1):
+            cost[lo, hi] = 8.0 * acc[hi] / _BW + lat
     best = {-1: (0.0, [])}
     for hi in range(0, top + 1):
-        cands = [(best[lo][0] + 8.0 * tier_elems(store, flat, lo, hi) / _BW + lat, best[lo][1] + [hi])
-                 for lo in range(-1, hi)]
-        best[hi] = min(cands, key=lambda c: c[0])
+        best[hi] = min(((best[lo][0] + cost[lo, hi], best[lo][1] + [hi]) for lo in range(-1, hi)),
+                       key=lambda c: c[0])
     return best[top][1]
 
 
@@ -194,9 +203,14 @@ class StoreTiers:
         self.M = torch.empty(max(total, 1), dtype=torch.float64, device=dev)
         self.elems = total
         st = stream_handle()
+        tile = int(_native.load().gc_tier_tile())
         for desc in launches:                    # children before parents
+            nt = -(-(desc[:, 1] * desc[:, 4]) // tile)
+            idx = np.repeat(np.arange(len(desc)), nt)
+            first = (np.arange(int(nt.sum())) - np.repeat(np.cumsum(nt) - nt, nt)) * tile
+            tl = to_dev(np.ascontiguousarray(np.stack([idx, first], 1), np.int64), dev)
             dd = to_dev(desc, dev)
-            _native.call("gc_tier_compose", len(desc), ptr(dd), ptr(store.V), ptr(self.M), st)
+            _native.call("gc_tier_compose", len(idx), ptr(tl), ptr(dd), ptr(store.V), ptr(self.M), st)
 
     def transposed(self, dev):
         """(per-tier groups, device buffer) of the backward blocks."""

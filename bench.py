@@ -439,7 +439,7 @@ def run_native(args):
         "storage_bytes": rep,
         "e2e": {"value": round(nbytes / e2e_s / 1e9, 2), "unit": "GB/s", "h2d_bytes_per_step": 8 * n,
                 "d2h_bytes_per_step": 8 * n, "ms_per_step": round(e2e_s * 1e3, 4),
-                "api": "paper_1810_08429_b200.h2.mvm(h, numpy x)"},
+                "api": "paper_1810_08429_b200.h2.mvm(h, numpy x): numpy -> pinned buffer read by the graph's gather kernel over the host link, result written by its scatter kernel into pinned memory -> numpy"},
         "gpu_launches": int(launches),
         "kernels_per_step": p.num_kernels,
         "gpu_launches_note": "own kernels per step x steps (graph replay); eager check counted %d" % eager_launches,

@@ -189,6 +189,12 @@ int gc_gather(const double* x, const int64_t* perm, int64_t n, double* xt,
 /* y[perm[i]] = yt[i] (h2.py:78-79) */
 int gc_scatter(const double* yt, const int64_t* perm, int64_t n, double* y,
                void* stream);
+/* The same indexed from the external side, iperm = inverse permutation:
+ * xt[iperm[j]] = x[j] and y[j] = yt[iperm[j]] + yt2[iperm[j]] - contiguous
+ * in x / y, so those may be mapped pinned host memory. */
+int gc_gather_inv(const double* x, const int64_t* iperm, int64_t n, double* xt, void* stream);
+int gc_scatter2_inv(const double* yt, const double* yt2, const int64_t* iperm, int64_t n, double* y,
+                    void* stream);
 /* y[perm[i]] = yt[i] + yt2[i] (the panel plan's two output parts) */
 int gc_scatter2(const double* yt, const double* yt2, const int64_t* perm, int64_t n, double* y,
                 void* stream);
@@ -196,8 +202,8 @@ int gc_scatter2(const double* yt, const double* yt2, const int64_t* perm, int64_
  * panel phase's input index list (int32) */
 int gc_expand_ranges(int64_t m, const int64_t* start, const int64_t* len, const int64_t* off,
                      int32_t* out, void* stream);
-/* Re-point argument `arg` of the gather (kernel 0, gc_gather) or scatter
- * (kernel 1, gc_scatter2) kernel nodes of an instantiated CUDA graph whose
+/* Re-point argument `arg` of the gather (kernel 0, gc_gather; 2,
+ * gc_gather_inv) or scatter (kernel 1, gc_scatter2; 3, gc_scatter2_inv) kernel nodes of an instantiated CUDA graph whose
  * captured value is old_ptr to new_ptr in the executable graph
  * (cudaGraphExecKernelNodeSetParams; the graph itself keeps old_ptr): a captured
  * product reads / writes caller buffers without copies.  graph / exec =

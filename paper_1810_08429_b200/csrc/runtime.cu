@@ -51,6 +51,28 @@ __global__ void k_scatter2(const double* __restrict__ yt, const double* __restri
         y[__ldg(perm + i)] = yt[i] + yt2[i];
 }
 
+// The same two steps indexed from the external side (iperm = inverse of
+// perm): reads of x / writes of y are contiguous, so x and y may live in
+// mapped pinned host memory (the product graph reads and writes the
+// caller's host buffers directly, h2.mvm).
+// xt[iperm[j]] = x[j]
+__global__ void k_gather_inv(const double* __restrict__ x, const int64_t* __restrict__ iperm,
+                             int64_t n, double* __restrict__ xt) {
+    for (int64_t j = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; j < n;
+         j += (int64_t)gridDim.x * blockDim.x)
+        xt[__ldg(iperm + j)] = x[j];
+}
+
+// y[j] = yt[iperm[j]] + yt2[iperm[j]]
+__global__ void k_scatter2_inv(const double* __restrict__ yt, const double* __restrict__ yt2,
+                               const int64_t* __restrict__ iperm, int64_t n, double* __restrict__ y) {
+    for (int64_t j = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; j < n;
+         j += (int64_t)gridDim.x * blockDim.x) {
+        const int64_t i = __ldg(iperm + j);
+        y[j] = yt[i] + yt2[i];
+    }
+}
+
 // xq[t,m,c] = sum_a n6[m,a] * node[t,a,c], sequential, no contraction; nodes
 // 3..5 are the straight midpoints 0.5*(p_i + p_j) (geometry.py:278-280).
 __global__ void k_surface_points(const double* __restrict__ corners, int64_t nt,
@@ -146,13 +168,15 @@ int gc_scatter2(const double* yt, const double* yt2, const int64_t* perm, int64_
 // instantiated CUDA graph (cudaGraphExecKernelNodeSetParams): the product
 // graph then reads the caller's x and writes the caller's y directly, with
 // no device copies around the replay.  kernel 0 = k_gather (4 arguments),
-// 1 = k_scatter2 (5); only nodes whose captured argument `arg` (the value
+// 1 = k_scatter2 (5), 2 = k_gather_inv (4), 3 = k_scatter2_inv (5); only nodes whose captured argument `arg` (the value
 // in the graph, which exec updates do not change) equals old_ptr change.
 // *count = nodes updated.
 int gc_graph_retarget(void* graph, void* exec, int32_t kernel, int32_t arg, const void* old_ptr,
                       const void* new_ptr, int32_t* count) {
-    const void* fn = kernel == 0 ? (const void*)k_gather : kernel == 1 ? (const void*)k_scatter2 : nullptr;
-    const int nargs = kernel == 0 ? 4 : 5;
+    const void* fns[4] = {(const void*)k_gather, (const void*)k_scatter2, (const void*)k_gather_inv,
+                          (const void*)k_scatter2_inv};
+    const void* fn = kernel >= 0 && kernel < 4 ? fns[kernel] : nullptr;
+    const int nargs = (kernel & 1) ? 5 : 4;
     if (!fn || arg < 0 || arg >= nargs || !graph || !exec) {
         set_error(GC_ERR_CONFIG, "gc_graph_retarget: bad kernel/arg/graph");
         return GC_ERR_CONFIG;
@@ -187,6 +211,21 @@ int gc_graph_retarget(void* graph, void* exec, int32_t kernel, int32_t arg, cons
     (void)cudaGetLastError();
     if (e != cudaSuccess) return cuda_status(e, "gc_graph_retarget");
     if (count) *count = cnt;
+    return GC_OK;
+}
+
+int gc_gather_inv(const double* x, const int64_t* iperm, int64_t n, double* xt, void* stream) {
+    if (n <= 0) return GC_OK;
+    k_gather_inv<<<grid_for(n, 256), 256, 0, (cudaStream_t)stream>>>(x, iperm, n, xt);
+    GC_CHECK_LAUNCH("gc_gather_inv");
+    return GC_OK;
+}
+
+int gc_scatter2_inv(const double* yt, const double* yt2, const int64_t* iperm, int64_t n, double* y,
+                    void* stream) {
+    if (n <= 0) return GC_OK;
+    k_scatter2_inv<<<grid_for(n, 256), 256, 0, (cudaStream_t)stream>>>(yt, yt2, iperm, n, y);
+    GC_CHECK_LAUNCH("gc_scatter2_inv");
     return GC_OK;
 }
 

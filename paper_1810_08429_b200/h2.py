@@ -232,8 +232,9 @@ def mvm_device(h, x_dev, y_dev=None, trans=False):
 def mvm(h, x):
     """y = H x, external ordering in and out (``h2.py:63-80``).
 
-    Host vector -> pinned staging -> static device input of the captured
-    graph -> replay -> pinned staging -> host vector."""
+    Host vector -> pinned staging, read by the captured graph's gather
+    kernel over the host link -> replay -> the scatter kernel writes the
+    pinned output -> host vector."""
     nr, nc = h.shape
     x = _check_dim(x, nc)
     p = plan(h)
@@ -242,13 +243,15 @@ def mvm(h, x):
         p.pin_y = torch.empty(nr, dtype=torch.float64, pin_memory=True)
     p.pin_x.numpy()[:] = x
     with torch.cuda.device(p.dev):
-        p.x.copy_(p.pin_x, non_blocking=True)
-        if p.graph is not None:
-            p.bind(p.x, p.y)
+        if p.graph is not None and p.bind(p.pin_x, p.pin_y):
+            # zero-copy: the graph's gather reads the pinned input and its
+            # scatter writes the pinned output (mapped host memory, read /
+            # written contiguously), no DMA copies around the replay
             p.graph.replay()
         else:
+            p.x.copy_(p.pin_x, non_blocking=True)
             p._body()
-        p.pin_y.copy_(p.y, non_blocking=True)
+            p.pin_y.copy_(p.y, non_blocking=True)
         torch.cuda.current_stream().synchronize()
     return p.pin_y.numpy().copy()
 
@@ -489,6 +492,7 @@ class PanelPlan:
         rf, cf = h.row_tree.flat, h.col_tree.flat
         self.n_in, self.n_out = cf.stop[0], rf.stop[0]
         self.perm_in, self.perm_out = d.perm_c, d.perm_r
+        self.iperm_in, self.iperm_out = _inverse_perm(self.perm_in), _inverse_perm(self.perm_out)
         f64 = dict(dtype=torch.float64, device=dev)
         self.x = torch.zeros(self.n_in, **f64)
         self.y = torch.zeros(self.n_out, **f64)
@@ -733,7 +737,7 @@ class PanelPlan:
         z = add(_Node("zero", "chain", fn=lambda: self._ybuf.zero_()))
         if gather:
             g = add(_Node("gather", "chain", [z], fn=lambda: _native.call(
-                "gc_gather", ptr(self.x), ptr(self.perm_in), self.n_in, ptr(self.xt), st())))
+                "gc_gather_inv", ptr(self.x), ptr(self.iperm_in), self.n_in, ptr(self.xt), st())))
             nodes[g].launches = 1
         else:
             g = z
@@ -780,7 +784,8 @@ class PanelPlan:
             tail = tail + [near]
         if scatter:
             k = add(_Node("scatter", "chain", tail, fn=lambda: _native.call(
-                "gc_scatter2", ptr(self.yt), ptr(self.yt2), ptr(self.perm_out), self.n_out, ptr(self.y), st())))
+                "gc_scatter2_inv", ptr(self.yt), ptr(self.yt2), ptr(self.iperm_out), self.n_out, ptr(self.y),
+                st())))
             nodes[k].launches = 1
         else:
             add(_Node("join", "chain", tail, fn=lambda: None))
@@ -996,7 +1001,7 @@ class PanelPlan:
         if self.graph is None or os.environ.get("GC_KEEP_GRAPH", "1") != "1":
             return False
         want = [x_dev.data_ptr(), y_dev.data_ptr()]
-        for slot, (kernel, arg) in enumerate(((0, 0), (1, 4))):
+        for slot, (kernel, arg) in enumerate(((2, 0), (3, 4))):
             if want[slot] == self._bound[slot]:
                 continue
             cnt = _native.ctypes.c_int32(0)
@@ -1042,6 +1047,12 @@ class PanelPlan:
 def _offsets_np(sizes):
     sizes = np.asarray(sizes, dtype=np.int64)
     return np.cumsum(sizes) - sizes
+
+
+def _inverse_perm(perm):
+    inv = torch.empty_like(perm)
+    inv[perm] = torch.arange(perm.numel(), dtype=perm.dtype, device=perm.device)
+    return inv
 
 
 def _ranges_np(starts, lengths):

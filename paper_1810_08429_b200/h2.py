@@ -624,7 +624,10 @@ class PanelPlan:
         rs, cs = h.row_basis.store, h.col_basis.store
         rf, cf = h.row_tree.flat, h.col_tree.flat
         d = h.dev
-        self._tier_split = os.environ.get("GC_TIER_SPLIT", "0") == "1"
+        # "upper" / "all": split the large panels of the upper tiers (232
+        # CTAs for 24 MB at C2) / of every tier over more items - both
+        # measured slower inside the product (142 / 144 us vs 135 us at C2)
+        self._tier_split = os.environ.get("GC_TIER_SPLIT", "none")
         cb = T_.choose_tiers(cs, cf)
         rb = cb if (rs is cs and rf is cf) else T_.choose_tiers(rs, rf)
         if not cb or not rb:
@@ -636,7 +639,8 @@ class PanelPlan:
             rt.M = None                                  # only the transposed blocks are used
         self.tiers = dict(col=cb, row=rb, fwd_elems=ct.elems, bwd_elems=int(MT.numel()))
         self._keep.extend([ct.M, MT])
-        kw = dict(transform=True, split=self._tier_split)
+        def kw(low):
+            return dict(transform=True, split=self._tier_split == "all" or (self._tier_split == "upper" and not low))
         nfwd = []
         for t in ct.tiers:
             u, f, w, nodes = t["u"], t["f"], t["w"], t["nodes"]
@@ -644,7 +648,7 @@ class PanelPlan:
             starts = cf.start[f] if low else cs.coef_off[f]
             panels = (t["moff"][nodes], t["m"][nodes], cs.rank[nodes], (starts, w), cs.coef_off[nodes], 0)
             nfwd.append(self._phase("forward", t["hi"], panels, ct.M, None, self.xt if low else self.xhat,
-                                    None, self.xhat, **kw))
+                                    None, self.xhat, **kw(low)))
         nbwd, parts = [], []
         for t, g in reversed(list(zip(rt.tiers, groups))):
             first, uu, ff, ww, dst = g["first"], g["u"], g["f"], g["w"], g["dst"]
@@ -661,7 +665,7 @@ class PanelPlan:
             panels = (dst[first][keep], K[keep], ww[first][keep], (rs.coef_off[uu][sel], rs.rank[uu][sel]),
                       (rf.start[elems] if low else rs.coef_off[elems])[keep], 0)
             P = self._phase("leafbasis" if low else "backward", t["hi"], panels, MT, None, self.yhat,
-                            self.yhat_t, self.yt2 if low else self.yhat_t, sum_inputs=True, **kw)
+                            self.yhat_t, self.yt2 if low else self.yhat_t, sum_inputs=True, **kw(low))
             if low:
                 parts.append((P, None))
             else:

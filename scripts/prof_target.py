@@ -1,6 +1,6 @@
 """Short profiling target (C2): one assembly, then NVTX-ranged kernels:
 'coupling' = the coupling panel product, 'nearq' = near-field quadrature,
-'mvm' = 3 eager matvecs.  Used under ncu; prints nothing heavy."""
+'mvm' = 3 graph-replayed matvecs, 'tiers' = the tier transforms once each.  Used under ncu; prints nothing heavy."""
 import os, sys
 import numpy as np
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
@@ -23,6 +23,11 @@ coup = max((P for P in p.phases if P.name == "coupling"), key=lambda P: P.bytes)
 torch.cuda.nvtx.range_push("coupling")
 for _ in range(3):
     p._launch(coup, stream_handle())
+torch.cuda.synchronize()
+torch.cuda.nvtx.range_pop()
+torch.cuda.nvtx.range_push("tiers")          # the tier transforms, each once, as chain launches
+for P in p._fwd + [b for b, _ in p._bwd] + [b for b, _ in p._leafparts]:
+    p._launch(P, stream_handle(), True, 0)
 torch.cuda.synchronize()
 torch.cuda.nvtx.range_pop()
 d = hm.dev

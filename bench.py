@@ -18,6 +18,7 @@ cores with the same metric and config.
 """
 
 import argparse
+import gc
 import json
 import os
 import subprocess
@@ -288,7 +289,8 @@ def run_native(args):
     # untimed warm-up assembly (library load, allocator, first-launch costs)
     hm, tree, bt = cli.build_h2_operator(mesh, cfg)
     h2.plan(hm)
-    del hm
+    del hm, tree, bt
+    gc.collect()                     # the operator <-> cached plan cycle: return its blocks to the allocator
     torch.cuda.synchronize()
     timings = {}
     t0 = time.perf_counter()

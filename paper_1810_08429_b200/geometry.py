@@ -79,8 +79,10 @@ class TriangleMesh:
         return self._stars
 
     def centroids(self):
-        # same reduction as the reference (mean over the 3 corners)
-        return self.vertices[self.triangles].mean(axis=1)
+        # same reduction as the reference (mean over the 3 corners: the sum
+        # in corner order, then / 3), without the (nt, 3, 3) gather
+        V, T = self.vertices, self.triangles
+        return (V[T[:, 0]] + V[T[:, 1]] + V[T[:, 2]]) / 3.0
 
     def __repr__(self):
         return "TriangleMesh(nv=%d, nt=%d)" % (self.nv, self.nt)

@@ -8,6 +8,8 @@ mesh = geometry.build_sphere_mesh(L)
 cfg = cli.default_config(eps=1e-6)
 hm, _, _ = cli.build_h2_operator(mesh, cfg)
 h2.plan(hm)
+del hm
+import gc; gc.collect()
 torch.cuda.synchronize()
 pr = cProfile.Profile()
 t0 = time.perf_counter()
@@ -19,3 +21,8 @@ torch.cuda.synchronize()
 pr.disable()
 print("total %.3f s" % (time.perf_counter() - t0), {k: round(v, 4) for k, v in tm.items()})
 pstats.Stats(pr).sort_stats("tottime").print_stats(30)
+pstats.Stats(pr).sort_stats("cumulative").print_stats(45)
+st = pstats.Stats(pr)
+st.print_callers("argsort")
+st.print_callers("reduce")
+st.print_callers("_amin")

@@ -705,6 +705,30 @@ class PanelPlan:
                 keep = (rf.start[elems] >= d.row_range[0]) & (rf.stop[elems] <= d.row_range[1])
             K = np.add.reduceat(rs.rank[uu], first)
             sel = np.repeat(keep, cnt)
+            if low and os.environ.get("GC_LEAF_SPLIT", "0") == "1":
+                # leaf rows in two launches: the ancestors' part as soon as
+                # their buckets are done, then only V_leaf y-hat_leaf after
+                # the deepest (last) bucket.  Measured slower (C1 29 -> 31,
+                # C2 135 -> 142, C3 525 -> 561 us): the 2048 tiny leaf panels
+                # still take 10 us at the end and the first part slows the bulk
+                assert np.array_equal(uu[first], elems)      # the leaf itself leads its stack
+                kl = rs.rank[elems]
+                own = np.zeros(len(ff), bool)
+                own[first] = True
+                up = keep & (cnt > 1)
+                sa = sel & ~own & np.repeat(up, cnt)
+                pa = (dst[first][up] + (kl * ww[first])[up], (K - kl)[up], ww[first][up],
+                      (rs.coef_off[uu][sa], rs.rank[uu][sa]), rf.start[elems][up], 1)
+                pb = (dst[first][keep], kl[keep], ww[first][keep], (rs.coef_off[elems][keep], kl[keep]),
+                      rf.start[elems][keep], 1)
+                if up.any():
+                    PA = self._phase("leafbasis", t["hi"], pa, MT, None, self.yhat, self.yhat_t, self.yt2,
+                                     sum_inputs=True, **kw(low))
+                    parts.append((PA, set(range(1, t["hi"] + 1))))
+                PB = self._phase("leafbasis", 0, pb, MT, None, self.yhat, self.yhat_t, self.yt2,
+                                 sum_inputs=True, **kw(low))
+                parts.append((PB, {0}))
+                continue
             panels = (dst[first][keep], K[keep], ww[first][keep], (rs.coef_off[uu][sel], rs.rank[uu][sel]),
                       (rf.start[elems] if low else rs.coef_off[elems])[keep], 0)
             P = self._phase("leafbasis" if low else "backward", t["hi"], panels, MT, None, self.yhat,

@@ -292,6 +292,23 @@ int gc_panel_tma(int64_t nitems, const int64_t* items, const int32_t* xidx,
                  void* stream);
 int64_t gc_panel_tma_item_elems(void);
 
+/* Native product executor (h2.py:63-80 as one call).  nodes [host] (n,18)
+ * int64 rows: kind (0 panel phase, 1 memset, 2 gc_gather_inv,
+ * 3 gc_scatter2_inv), stream index, launch priority, chain flags (as
+ * gc_panelmv), ndeps, dep_off, then 12 arguments: panel = items, nitems,
+ * xidx, A0, A1, in0, in1, out, scratch, nred, red, arrivals; memset = ptr,
+ * bytes; gather = x, iperm, n, xt; scatter = yt, yt2, iperm, n, y.  deps
+ * [host] = dependency node indices (each earlier than its node).
+ * stream_prio [host] (nstreams) = stream creation priorities.  Captures the
+ * DAG on the plan's own streams/events into one CUDA graph and
+ * instantiates it.  gc_plan_run re-points the gather / scatter nodes at x /
+ * y (device or mapped pinned host, external order; NULL keeps the binding)
+ * and launches the graph on `stream`. */
+int gc_plan_create(int64_t n, const int64_t* nodes, int64_t ndeps, const int64_t* deps, int64_t nstreams,
+                   const int32_t* stream_prio, void** plan);
+int gc_plan_run(void* plan, const double* x, double* y, void* stream);
+int gc_plan_destroy(void* plan);
+
 /* Tiered transforms (plan time; h2.py PanelPlan tiers): the composed
  * transfers of a tier of tree heights, one height per call.  desc [dev]
  * (n,6) = s_off, m, kc, e_off, ku, out_off, cut into tiles [dev] (ntiles,2)

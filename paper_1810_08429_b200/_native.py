@@ -59,6 +59,9 @@ _SIGNATURES = {
     "gc_tier_tile": [],
     "gc_graph_retarget": [c_p, c_p, ctypes.c_int32, ctypes.c_int32, c_p, c_p, c_p],
     "gc_gather_inv": [c_p, c_p, c_i64, c_p, c_p],
+    "gc_plan_create": [c_i64, c_p, c_i64, c_p, c_i64, c_p, c_p],
+    "gc_plan_run": [c_p, c_p, c_p, c_p],
+    "gc_plan_destroy": [c_p],
     "gc_scatter2_inv": [c_p, c_p, c_p, c_i64, c_p, c_p],
     "gc_block_transpose": [c_i64, c_p, c_p, c_p, c_p],
     "gc_segmv": [c_i64, c_p, c_p, c_p, c_p, c_p, c_p, c_p, ctypes.c_int, c_i64, c_p],

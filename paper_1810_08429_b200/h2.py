@@ -1042,8 +1042,62 @@ class PanelPlan:
     def _body(self, phase_events=None, phase="coupling"):
         self._exec(self.nodes, serial=phase_events is not None, phase_events=phase_events, phase=phase)
 
+    def _native_table(self):
+        """The DAG as gc_plan_create's node table (csrc/plan.cu), or None
+        when a node is not expressible there (a Python callable such as a
+        collective, or a non-default bulk kernel)."""
+        skip = {i for i, n in enumerate(self.nodes) if n.name == "join"}
+        remap, rows, deps, streams = {}, [], [], {"chain": 0}
+        for i, n in enumerate(self.nodes):
+            if i in skip:
+                continue
+            sidx = streams.setdefault(n.stream, len(streams))
+            a = [0] * 12
+            if n.phase is not None:
+                P = n.phase
+                if P.cta is not None or P.tma:
+                    return None
+                kind = 0
+                chain = (self._pdl if n.stream == "chain" else 0) | (4 if P.warp else 0)
+                a = [P.items.data_ptr(), P.nitems, P.xidx.data_ptr(), P.A0.data_ptr(),
+                     P.A1.data_ptr() if P.A1 is not None else 0, P.in0.data_ptr(),
+                     P.in1.data_ptr() if P.in1 is not None else 0, P.out.data_ptr(), P.scratch.data_ptr(),
+                     P.nred, P.red.data_ptr() if P.red is not None else 0, P.arrivals.data_ptr()]
+            elif n.name == "zero":
+                kind, chain, a[:2] = 1, 0, [self._ybuf.data_ptr(), 8 * self._ybuf.numel()]
+            elif n.name == "gather":
+                kind, chain = 2, 0
+                a[:4] = [self.x.data_ptr(), self.iperm_in.data_ptr(), self.n_in, self.xt.data_ptr()]
+            elif n.name == "scatter":
+                kind, chain = 3, 0
+                a[:5] = [self.yt.data_ptr(), self.yt2.data_ptr(), self.iperm_out.data_ptr(), self.n_out,
+                         self.y.data_ptr()]
+            else:
+                return None
+            d = [remap[j] for j in n.deps if j not in skip]
+            rows.append([kind, sidx, n.priority, chain, len(d), len(deps)] + a)
+            deps.extend(d)
+            remap[i] = len(rows) - 1
+        least, greatest = self._prio
+        prio = np.array([greatest if k == "chain" else least for k in streams], np.int32)
+        return (np.array(rows, np.int64).reshape(-1, 18), np.array(deps or [0], np.int64), len(deps), prio)
+
     def capture(self):
-        """Record the product into a CUDA graph (static x -> y buffers)."""
+        """Record the product into a CUDA graph (static x -> y buffers).  The
+        default is the C++ executor (csrc/plan.cu: its own streams, events
+        and graph); a DAG with Python steps (the sharded plan's collectives)
+        is captured through torch."""
+        if os.environ.get("GC_NATIVE_PLAN", "1") == "1" and type(self) is PanelPlan:
+            tab = self._native_table()
+            if tab is not None:
+                self._body()                         # warm-up (module loads) outside the capture
+                torch.cuda.synchronize(self.dev)
+                rows, deps, ndeps, prio = tab
+                h = _native.ctypes.c_void_p(0)
+                _native.call("gc_plan_create", len(rows), rows.ctypes.data, ndeps, deps.ctypes.data, len(prio),
+                             prio.ctypes.data, _native.ctypes.byref(h))
+                self.graph = _NativeGraph(h)
+                return self.graph
         s = torch.cuda.Stream(device=self.dev)
         s.wait_stream(torch.cuda.current_stream())
         with torch.cuda.stream(s):
@@ -1073,9 +1127,13 @@ class PanelPlan:
 
     def bind(self, x_dev, y_dev):
         """Point the captured graph's input gather at x_dev and its output
-        scatter at y_dev (contiguous float64 device vectors of this plan's
-        sizes; they must stay alive until the replays that use them ran).
-        Returns False (nothing changed) when the graph has no such nodes."""
+        scatter at y_dev (contiguous float64 vectors of this plan's sizes,
+        device or pinned host; they must stay alive until the replays that
+        use them ran).  Returns False (nothing changed) when the graph has no
+        such nodes."""
+        if isinstance(self.graph, _NativeGraph):
+            self.graph.bind(x_dev, y_dev)
+            return True
         if self.graph is None or os.environ.get("GC_KEEP_GRAPH", "1") != "1":
             return False
         want = [x_dev.data_ptr(), y_dev.data_ptr()]
@@ -1120,6 +1178,28 @@ class PanelPlan:
     def num_kernels(self):
         """Own kernels per product (the torch fill of y-hat not counted)."""
         return sum(n.launches for n in self.nodes)
+
+
+class _NativeGraph:
+    """The product graph owned by the C++ executor (gc_plan_*): replay()
+    launches it on the current stream with the last bound x / y."""
+
+    def __init__(self, handle):
+        self.handle = handle
+        self._x = self._y = None
+
+    def bind(self, x, y):
+        self._x, self._y = x.data_ptr(), y.data_ptr()
+
+    def replay(self):
+        _native.call("gc_plan_run", self.handle, _native.ctypes.c_void_p(self._x or 0),
+                     _native.ctypes.c_void_p(self._y or 0), stream_handle())
+
+    def __del__(self):
+        try:
+            _native.load().gc_plan_destroy(self.handle)
+        except Exception:        # pragma: no cover - interpreter shutdown
+            pass
 
 
 def _offsets_np(sizes):

@@ -467,7 +467,7 @@ def _sharded_worker(rank, world, port, out_dir):
         dist.destroy_process_group()
 
 
-@pytest.mark.parametrize("world", [2, 4])
+@pytest.mark.parametrize("world", [2, 4, 8])
 def test_sharded_operator_multirank_matches_full(world, tmp_path):
     """The N>1 device path end to end: `world` ranks as processes sharing the
     one GPU (gloo collectives staged through the host - no kernel waits on

@@ -442,7 +442,7 @@ def cgnr_solve(apply, b, tol=1e-8, max_iter=500):
 # --------------------------------------------------------------------------
 # panel plan: the non-transposed product (the benchmarked hot path)
 
-_ITEM_ELEMS = int(os.environ.get("GC_ITEM_ELEMS", 16384))  # ~128 KB of matrix data per work item
+_ITEM_ELEMS = int(os.environ.get("GC_ITEM_ELEMS", 65536))  # <= 512 KB of matrix data per work item (rows capped at 1024)
 _ITEM_MAX_ROWS = 1024       # PAN_MAX_ROWS in csrc/h2mv.cu
 _WARP_MAX_ROWS = 256        # WARP_MAX_ROWS in csrc/h2mv.cu
 _STREAM_MAX_T = 1024        # ST_MAX_T in csrc/h2mv.cu

@@ -1186,14 +1186,14 @@ class _NativeGraph:
 
     def __init__(self, handle):
         self.handle = handle
-        self._x = self._y = None
+        self._x = self._y = 0
+        self._run = _native.load().gc_plan_run        # bound once: this is on the e2e path
 
     def bind(self, x, y):
         self._x, self._y = x.data_ptr(), y.data_ptr()
 
     def replay(self):
-        _native.call("gc_plan_run", self.handle, _native.ctypes.c_void_p(self._x or 0),
-                     _native.ctypes.c_void_p(self._y or 0), stream_handle())
+        _native.check(self._run(self.handle, self._x, self._y, torch.cuda.current_stream().cuda_stream))
 
     def __del__(self):
         try:

@@ -162,6 +162,72 @@ def test_tier_plan_reproduces_level_by_level(bounds, forest):
     assert np.allclose(y, ref, rtol=1e-12, atol=1e-12 * np.abs(ref).max())
 
 
+def _random_tree(n, rng, leaf=12):
+    """A preorder FlatTree with random, unbalanced splits (frontier nodes of
+    every tier then sit at many different heights)."""
+    from paper_1810_08429_b200.clustering import FlatClusterTree as FlatTree
+    start, stop, left, right, parent, depth = [], [], [], [], [], []
+
+    def node(lo, hi, par, d):
+        i = len(start)
+        start.append(lo); stop.append(hi); left.append(-1); right.append(-1); parent.append(par); depth.append(d)
+        if hi - lo > leaf or (hi - lo > 1 and rng.random() < 0.2):
+            cut = int(rng.integers(lo + 1, hi))
+            left[i] = node(lo, cut, i, d + 1)
+            right[i] = node(cut, hi, i, d + 1)
+        return i
+    node(0, n, -1, 0)
+    a = [np.asarray(v, np.int64) for v in (start, stop, left, right, parent, depth)]
+    z = np.zeros((len(start), 3))
+    return FlatTree(np.arange(n), *a, z, z + 1.0)
+
+
+@pytest.mark.parametrize("seed,bounds", [(1, None), (2, [1, 4]), (3, [0, 2, 5]), (4, [3])])
+def test_tier_plan_unbalanced_tree(seed, bounds):
+    """The same check on random unbalanced trees with dead nodes and a
+    forest: frontier elements at mixed heights, tiers built from both."""
+    rng = np.random.default_rng(seed)
+    flat = _random_tree(700, rng)
+    s = _store(flat, rng, dead_frac=0.15, forest=seed % 2 == 0)
+    live = tiers.live_nodes(s)
+    top = int(flat.height[live].max())
+    b = tiers.choose_tiers(s, flat) if bounds is None else sorted({min(v, top) for v in bounds} | {top})
+    n = int(flat.stop[0])
+    x = rng.standard_normal(n)
+    tabs, launches, total = tiers.tier_tables(s, flat, b)
+    M = _compose(s, launches, total)
+    xh = np.zeros(s.coef_size)
+    for t in tabs:
+        for u in t["nodes"]:
+            sel = t["u"] == u
+            f, w = t["f"][sel], t["w"][sel]
+            src = [x[flat.start[e]:flat.start[e] + ww] if t["lo"] < 0 else xh[s.coef_off[e]:s.coef_off[e] + ww]
+                   for e, ww in zip(f, w)]
+            Mu = M[t["moff"][u]:t["moff"][u] + t["m"][u] * s.rank[u]].reshape(t["m"][u], s.rank[u])
+            xh[s.coef_off[u]:s.coef_off[u] + s.rank[u]] = Mu.T @ np.concatenate(src)
+    ref = _forward_ref(s, flat, x)
+    assert np.allclose(xh, ref, rtol=1e-11, atol=1e-11 * np.abs(ref).max())
+    groups, tdesc, ttotal = tiers.transpose_tables(tabs, s, flat)
+    MT = _transpose(M, tdesc, ttotal)
+    yh = rng.standard_normal(s.coef_size)
+    yt = np.zeros(s.coef_size)
+    y = np.zeros(n)
+    for t, g in reversed(list(zip(tabs, groups))):
+        ends = np.r_[g["first"][1:], len(g["f"])]
+        for a, e_ in zip(g["first"], ends):
+            e, w = g["f"][a], g["w"][a]
+            us = g["u"][a:e_]
+            K = int(s.rank[us].sum())
+            A = MT[g["dst"][a]:g["dst"][a] + K * w].reshape(K, w)
+            inp = np.concatenate([(yh + yt)[s.coef_off[u]:s.coef_off[u] + s.rank[u]] for u in us])
+            if t["lo"] < 0:
+                y[flat.start[e]:flat.start[e] + w] = A.T @ inp
+            else:
+                yt[s.coef_off[e]:s.coef_off[e] + w] += A.T @ inp
+    ref = _backward_ref(s, flat, yh, n)
+    assert np.allclose(y, ref, rtol=1e-11, atol=1e-11 * np.abs(ref).max())
+
+
 def test_choose_tiers_override_and_cost(monkeypatch):
     mesh = geometry.build_sphere_mesh(3)
     flat = build_cluster_tree(mesh, leaf_size=8).flat

@@ -274,6 +274,75 @@ __global__ void __launch_bounds__(PAN_THREADS, 6) k_panelmv(PanelPhase P) {
     }
 }
 
+// Two small whole panels per CTA: threads [0,128) run item 2b, [128,256)
+// item 2b+1, each half with the k_panelmv mapping over 128 threads (same
+// per-output summation order as k_panelmv at 128 threads).  For the latency-
+// bound tier phases whose panels are small (the lowest forward tier, the
+// leaf rows): half as many CTAs, so about half the waves of per-CTA round
+// trips.  Items must be direct (no split), T <= 128, nrows <= PAIR_MAX_ROWS.
+constexpr int PAIR_THREADS = PAN_THREADS / 2;
+constexpr int PAIR_MAX_ROWS = PAN_MAX_ROWS / 2;
+
+template <bool CHAIN>
+__global__ void __launch_bounds__(PAN_THREADS, 6) k_panel_pair(PanelPhase P) {
+    __shared__ PanelSmem sm;                       // xs / red split in halves
+    if (CHAIN) asm volatile("griddepcontrol.launch_dependents;");
+    if (P.trace != nullptr && threadIdx.x == 0) atomicMin(P.trace, globaltimer());
+    const int half = threadIdx.x / PAIR_THREADS, ltid = threadIdx.x % PAIR_THREADS;
+    const int64_t item = 2 * (int64_t)blockIdx.x + half;
+    const bool has = item < P.nitems;
+    double* xs = sm.xs + half * PAIR_MAX_ROWS;
+    double* red = sm.red + half * PAIR_THREADS;
+    const int64_t* it = P.items + 8 * (has ? item : 0);
+    const int64_t a_off = it[0], xi_off = it[1], out_off = it[2];
+    const int T = has ? (int)it[3] : 1, nrows = has ? (int)it[4] : 0, mode = (int)it[5];
+    const double* __restrict__ A = ((mode & 1) ? P.A1 : P.A0) + a_off;
+    const int32_t* __restrict__ xi = P.xidx + xi_off;
+    if (CHAIN) {
+        if (has) prefetch_l2(A, 8 * (int64_t)nrows * T);
+        asm volatile("griddepcontrol.wait;" ::: "memory");
+    }
+    if (mode & 32) {
+        for (int r = ltid; r < nrows; r += PAIR_THREADS) {
+            const int i = __ldg(xi + r);
+            xs[r] = __ldcg(P.in0 + i) + __ldcg(P.in1 + i);
+        }
+    } else {
+        const double* x = (mode & 2) ? P.in1 : P.in0;
+        for (int r = ltid; r < nrows; r += PAIR_THREADS) xs[r] = __ldcg(x + __ldg(xi + r));
+    }
+    __syncthreads();
+    const int tt = T < PAIR_THREADS ? T : PAIR_THREADS;
+    const int ng = PAIR_THREADS / tt;
+    const int g = ltid / tt;
+    const int t = ltid % tt;
+    double acc = 0.0;
+    if (has && g < ng) {
+        const double* __restrict__ At = A + t;
+        int r = g;
+        for (; r + (PAN_UNROLL - 1) * ng < nrows; r += PAN_UNROLL * ng) {
+            double a[PAN_UNROLL];
+#pragma unroll
+            for (int j = 0; j < PAN_UNROLL; ++j) a[j] = __ldcs(At + (int64_t)(r + j * ng) * T);
+#pragma unroll
+            for (int j = 0; j < PAN_UNROLL; ++j) acc = fma(a[j], xs[r + j * ng], acc);
+        }
+        for (; r < nrows; r += ng) acc = fma(__ldcs(At + (int64_t)r * T), xs[r], acc);
+    }
+    red[ltid] = acc;
+    __syncthreads();
+    if (has && ltid < tt) {
+        double v = red[ltid];
+        for (int q = 1; q < ng; ++q) v += red[q * tt + ltid];
+        double* o = P.out + out_off + t;
+        *o = (mode & 8) ? __ldcg(o) + v : v;
+    }
+    if (P.trace != nullptr) {
+        __syncthreads();
+        if (threadIdx.x == 0) atomicMax(P.trace + 1, globaltimer());
+    }
+}
+
 // ---------------------------------------------------------------------------
 // Bulk phases (coupling buckets, near field): a TMA-fed streaming kernel.
 // A co-resident grid (2 CTAs per SM); CTA b owns the items
@@ -764,7 +833,12 @@ extern "C" int gc_panelmv(int64_t nitems, const int64_t* items, const int32_t* x
     cfg.attrs = attr;
     cfg.numAttrs = na;
     cudaError_t e;
-    if (chain & 4) {
+    if (chain & 16) {
+        // two whole small panels per CTA (direct items, T <= 128, <= 512 rows)
+        cfg.gridDim = dim3((unsigned)((nitems + 1) / 2));
+        e = (chain & 3) ? cudaLaunchKernelEx(&cfg, k_panel_pair<true>, P)
+                        : cudaLaunchKernelEx(&cfg, k_panel_pair<false>, P);
+    } else if (chain & 4) {
         // warp-granular items (whole panels of <= WARP_MAX_ROWS rows)
         cfg.gridDim = dim3((unsigned)((nitems + PAN_THREADS / 32 - 1) / (PAN_THREADS / 32)));
         e = (chain & 3) ? cudaLaunchKernelEx(&cfg, k_panel_warp<true>, P)

@@ -446,12 +446,13 @@ _ITEM_ELEMS = int(os.environ.get("GC_ITEM_ELEMS", 65536))  # <= 512 KB of matrix
 _ITEM_MAX_ROWS = 1024       # PAN_MAX_ROWS in csrc/h2mv.cu
 _WARP_MAX_ROWS = 256        # WARP_MAX_ROWS in csrc/h2mv.cu
 _STREAM_MAX_T = 1024        # ST_MAX_T in csrc/h2mv.cu
+_PAIR_MAX_ELEMS = int(os.environ.get("GC_PAIR_MAX_ELEMS", 8192))   # k_panel_pair: small panels only
 _RESIDENT = 148 * 6         # resident k_panelmv CTAs (40 registers, 256 threads, 6 per SM)
 
 
 class _Phase:
     __slots__ = ("name", "height", "items", "xidx", "red", "arrivals", "nitems", "nred", "A0", "A1",
-                 "in0", "in1", "out", "scratch", "bytes", "cta", "in_elems", "out_elems", "tma", "warp")
+                 "in0", "in1", "out", "scratch", "bytes", "cta", "in_elems", "out_elems", "tma", "warp", "pair")
 
 
 class _Node:
@@ -502,6 +503,7 @@ class PanelPlan:
         self._obuf = torch.zeros(self.n_out + max(cs.coef_size, 1), **f64)
         self.yt, self.xhat = self._obuf[:self.n_out], self._obuf[self.n_out:]
         self._keep = []
+        self.tiers_pending = False
         ny = max(rs.coef_size, 1)
         # y-hat | y-hat from the tiers above | leaf-basis part of y (summed
         # in the scatter): one buffer, zeroed by one memset per product
@@ -650,7 +652,7 @@ class PanelPlan:
         P.A0, P.A1, P.in0, P.in1, P.out = N.A0, F.A0, self.xt, None, self._obuf
         P.bytes = F.bytes + N.bytes
         P.in_elems, P.out_elems = F.in_elems + N.in_elems, F.out_elems + N.out_elems
-        P.warp, P.cta, P.tma = False, None, False
+        P.warp, P.cta, P.tma, P.pair = False, None, False, False
         return P
 
     def _tiered(self, h, fwd, bwd, leafp):
@@ -684,6 +686,7 @@ class PanelPlan:
         self._keep.extend([ct.M, MT])
         def kw(low):
             return dict(transform=True, split=self._tier_split == "all" or (self._tier_split == "upper" and not low))
+        self.tiers_pending = True
         nfwd = []
         for t in ct.tiers:
             u, f, w, nodes = t["u"], t["f"], t["w"], t["nodes"]
@@ -737,6 +740,7 @@ class PanelPlan:
                 parts.append((P, None))
             else:
                 nbwd.append((P, set(range(t["lo"] + 1, t["hi"] + 1))))
+        self.tiers_pending = False
         return nfwd, nbwd, parts
 
     # -- DAG -----------------------------------------------------------------
@@ -1011,6 +1015,10 @@ class PanelPlan:
         P.warp = bool(transform and n >= self._warp_min_panels and len(items) == n
                       and int(K.max()) <= _WARP_MAX_ROWS)
         P.cta = None
+        # two whole small panels per CTA (k_panel_pair) for tier phases
+        P.pair = bool(transform and self.tiers_pending and os.environ.get("GC_PAIR", "1") == "1" and n
+                      and bool(np.all(direct)) and int(T.max()) <= 128 and int(item_rows.max()) <= 512
+                      and int((item_rows * T[item_panel]).max()) <= _PAIR_MAX_ELEMS and not P.warp)
         P.tma = bool(not transform and self.bulk_kernel == "tma" and n and int(T.max()) <= self._tma_elems)
         if (not transform and n and int(T.max()) <= _STREAM_MAX_T and self._stream_grid > 0
                 and self.bulk_kernel == "stream"):
@@ -1034,7 +1042,7 @@ class PanelPlan:
                          ptr(P.in0), ptr(P.in1), ptr(P.out), ptr(P.scratch), P.nred, ptr(P.red),
                          ptr(P.arrivals), int(priority), ptr(self.trace.get(id(P))), stream)
             return
-        mode = (self._pdl if chain else 0) | (4 if P.warp else 0)
+        mode = (self._pdl if chain else 0) | (4 if P.warp else 0) | (16 if P.pair else 0)
         _native.call("gc_panelmv", P.nitems, ptr(P.items), ptr(P.xidx), ptr(P.A0), ptr(P.A1),
                      ptr(P.in0), ptr(P.in1), ptr(P.out), ptr(P.scratch), P.nred, ptr(P.red),
                      ptr(P.arrivals), mode, int(priority), ptr(self.trace.get(id(P))), stream)
@@ -1058,7 +1066,7 @@ class PanelPlan:
                 if P.cta is not None or P.tma:
                     return None
                 kind = 0
-                chain = (self._pdl if n.stream == "chain" else 0) | (4 if P.warp else 0)
+                chain = (self._pdl if n.stream == "chain" else 0) | (4 if P.warp else 0) | (16 if P.pair else 0)
                 a = [P.items.data_ptr(), P.nitems, P.xidx.data_ptr(), P.A0.data_ptr(),
                      P.A1.data_ptr() if P.A1 is not None else 0, P.in0.data_ptr(),
                      P.in1.data_ptr() if P.in1 is not None else 0, P.out.data_ptr(), P.scratch.data_ptr(),

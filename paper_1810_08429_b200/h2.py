@@ -1019,6 +1019,11 @@ class PanelPlan:
         P.pair = bool(transform and self.tiers_pending and os.environ.get("GC_PAIR", "1") == "1" and n
                       and bool(np.all(direct)) and int(T.max()) <= 128 and int(item_rows.max()) <= 512
                       and int((item_rows * T[item_panel]).max()) <= _PAIR_MAX_ELEMS and not P.warp)
+        if P.pair and os.environ.get("GC_PAIR_SORT", "desc") != "0":
+            # pair equal-sized panels (largest first, or smallest first)
+            sz = items[:, 3] * items[:, 4]
+            order = np.argsort(-sz if os.environ.get("GC_PAIR_SORT", "desc") == "desc" else sz, kind="stable")
+            P.items = to_dev(np.ascontiguousarray(items[order], np.int64), self.dev)
         P.tma = bool(not transform and self.bulk_kernel == "tma" and n and int(T.max()) <= self._tma_elems)
         if (not transform and n and int(T.max()) <= _STREAM_MAX_T and self._stream_grid > 0
                 and self.bulk_kernel == "stream"):

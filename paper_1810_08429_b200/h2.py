@@ -932,9 +932,10 @@ class PanelPlan:
         n = len(a_off)
         elems = int((K * T).sum())
         if transform and split:
-            # tier transforms: bandwidth phases on the chain - split large
-            # panels like the bulk so the launch fills the SMs
-            target = max(1024, min(_ITEM_ELEMS, elems // (148 * 4) + 1))
+            # tier transforms: split only the panels larger than
+            # GC_TIER_SPLIT_ELEMS (0: like the bulk, so the launch fills the SMs)
+            cap = int(os.environ.get("GC_TIER_SPLIT_ELEMS", "0"))
+            target = cap if cap > 0 else max(1024, min(_ITEM_ELEMS, elems // (148 * 4) + 1))
             max_rows = _ITEM_MAX_ROWS
         elif transform:
             # transform levels: one item per panel (split only past the row
@@ -983,6 +984,8 @@ class PanelPlan:
         items = np.stack([a_off[item_panel] + item_k * T[item_panel], xoff[item_panel] + item_k,
                           out_col, T[item_panel], item_rows, mode,
                           np.where(direct, -1, slot[item_panel]), np.zeros_like(mode)], 1)
+        if not transform and len(items) and os.environ.get("GC_BULK_LPT", "0") == "1":
+            items = items[np.argsort(-(items[:, 3] * items[:, 4]), kind="stable")]
         if transform and len(items) and os.environ.get("GC_LPT", "0") == "1":
             # largest items first (CTAs dispatch in launch order): measured
             # -6 % at sphere L4, +1-3 % at L6-L8, so off by default

@@ -1,8 +1,8 @@
 """Generate the golden fixtures from the reference implementation itself.
 
 Run in the build container (the reference is importable there):
-    PYTHONPATH=/root/reference/pkg/src python tests/golden/make_golden.py [--dlp | --linear]
-(--dlp / --linear write only the double-layer / linear-basis fixtures)
+    PYTHONPATH=/root/reference/pkg/src python tests/golden/make_golden.py [--dlp | --linear | --mvm20 ...]
+(each flag writes only that family of fixtures; none = the base set)
 Outputs tests/golden/*.npz.  The GPU box has no /root/reference; the tests
 read only these committed files.
 """
@@ -389,8 +389,28 @@ def main():
                         **pipeline(G.build_sphere_mesh(5), 1e-6, 23))
 
 
+def main_mvm20():
+    """SURVEY 8(c) parity protocol on C1 (sphere L4, eps 1e-4, CLI defaults):
+    the reference's mvm / mvm_t of 20 seeded N(0,1) vectors
+    (np.random.default_rng(0), the reference tests' convention).  x is
+    regenerated in the test; only the products are stored."""
+    mesh = G.build_sphere_mesh(4)
+    tree = C.build_cluster_tree(mesh, "constant", 16)
+    bt = C.build_block_tree(tree, eta=1.0)
+    rm, cm = GC.coupling_marks(bt)
+    rb = GC.build_cluster_basis(tree, mesh, "constant", 3, 0.5, 1e-4, "row", (3, 5), rm)
+    cb = GC.build_cluster_basis(tree, mesh, "constant", 3, 0.5, 1e-4, "col", (3, 5), cm)
+    hm = GC.build_h2(bt, rb, cb, mesh, "slp", "constant", "galerkin", (3, 5))
+    xs = np.random.default_rng(0).standard_normal((20, mesh.nt))
+    np.savez_compressed(os.path.join(OUT, "mvm20_sphere4_eps1e-4.npz"),
+                        mvm=np.stack([H.mvm(hm, x) for x in xs]),
+                        mvm_t=np.stack([H.mvm_t(hm, x) for x in xs]))
+
+
 if __name__ == "__main__":
-    if "--dlp" in sys.argv:
+    if "--mvm20" in sys.argv:
+        main_mvm20()
+    elif "--dlp" in sys.argv:
         main_dlp()
     elif "--linear" in sys.argv:
         main_linear()

@@ -420,6 +420,19 @@ def test_tiered_transforms_match_level_by_level(geo, level, cfg_kw, monkeypatch)
         assert (y1 - y0).norm().item() <= 1e-13 * y0.norm().item(), tiers
 
 
+def test_mvm_20_seeded_vectors_c1():
+    """SURVEY 8(c) parity protocol at C1: mvm and mvm_t of the 20 seeded
+    N(0,1) vectors (default_rng(0)) against the reference's own products
+    (tests/golden/make_golden.py --mvm20); bar 1e-10, held to 1e-12."""
+    g = golden("mvm20_sphere4_eps1e-4.npz")
+    mesh = geometry.build_sphere_mesh(4)
+    hm, _, _ = cli.build_h2_operator(mesh, cli.default_config(eps=1e-4))
+    xs = np.random.default_rng(0).standard_normal((20, mesh.nt))
+    for x, y, yt in zip(xs, g["mvm"], g["mvm_t"]):
+        assert np.linalg.norm(h2.mvm(hm, x) - y) <= 1e-12 * np.linalg.norm(y)
+        assert np.linalg.norm(h2.mvm_t(hm, x) - yt) <= 1e-12 * np.linalg.norm(yt)
+
+
 def test_graph_rebinding_to_caller_buffers():
     """The captured product re-pointed at caller buffers (gc_graph_retarget):
     alternating device inputs / outputs, the pinned host buffers of

@@ -269,6 +269,35 @@ def test_matvec_properties_c2():
         assert rel(blk.values, ref) < 1e-12
 
 
+def test_properties_and_block_samples_c4():
+    """C4 (sphere L8, 524,288 triangles, eps 1e-8), the multi-GPU
+    configuration, through size-independent properties: linearity, the
+    mvm / mvm_t adjoint, near-symmetry of the single layer within the
+    compression error, and a random sample of stored near-field and coupling
+    blocks re-derived by the dense-block path (bitwise) and by
+    the oracle (<= 1e-12)."""
+    mesh = geometry.build_sphere_mesh(8)
+    hm, _, _ = cli.build_h2_operator(mesh, cli.default_config(eps=1e-8))
+    rng = np.random.default_rng(8)
+    x, y = rng.standard_normal((2, mesh.nt))
+    hx, hy = h2.mvm(hm, x), h2.mvm(hm, y)
+    lin = h2.mvm(hm, 1.5 * x - 2.0 * y)
+    assert np.linalg.norm(lin - (1.5 * hx - 2.0 * hy)) <= 1e-13 * np.linalg.norm(hx)
+    assert abs(y @ hx - x @ h2.mvm_t(hm, y)) <= 1e-12 * abs(y @ hx)
+    assert abs(y @ hx - x @ hy) <= 1e-7 * abs(y @ hx)
+    nodes, gram = P.chart_nodes(mesh.vertices, mesh.triangles)
+    for i in rng.choice(len(hm.nearfield), 8, replace=False):
+        blk = hm.nearfield[int(i)]
+        r, c = blk.row.indices, blk.col.indices
+        assert np.array_equal(blk.values, assembly.assemble_galerkin_block("slp", mesh, "constant", r, c).values)
+        assert rel(blk.values, P.block(nodes, gram, mesh.triangles, r, c)) < 1e-12
+    for i in rng.choice(len(hm.coupling), 4, replace=False):
+        blk = hm.coupling[int(i)]
+        r, c = hm.row_basis.node(blk.row).pivots, hm.col_basis.node(blk.col).pivots
+        assert np.array_equal(blk.values, assembly.assemble_galerkin_block("slp", mesh, "constant", r, c).values)
+        assert rel(blk.values, P.block(nodes, gram, mesh.triangles, r, c)) < 1e-12
+
+
 def test_errors_map_to_reference_classes(sphere2):
     with pytest.raises(ConfigError):
         assembly.assemble_galerkin_block("hyp", sphere2, "constant", [0], [1])

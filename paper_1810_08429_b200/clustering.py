@@ -462,7 +462,7 @@ class FlatBlockTree:
         span = np.power(4, _KEY_DIGITS - level, dtype=np.int64)
         self.key_lo, self.key_hi = key, key + span
         leaves = np.flatnonzero(state != 2)
-        order = np.argsort(key[leaves], kind="stable")
+        order = np.argsort(key[leaves])          # keys are unique paths: any sort is the DFS order
         self.leaf_ids = leaves[order]
         self.leaf_key = key[self.leaf_ids]
         self._kid_index = None

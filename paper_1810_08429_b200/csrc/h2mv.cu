@@ -699,7 +699,14 @@ __device__ void warp_item(const PanelPhase& P, int64_t item, double* xs, int lan
     const double* __restrict__ A = ((mode & 1) ? P.A1 : P.A0) + a_off;
     const double* x = (mode & 2) ? P.in1 : P.in0;
     const int32_t* __restrict__ xi = P.xidx + xi_off;
-    for (int r = lane; r < nrows; r += 32) xs[r] = __ldcg(x + __ldg(xi + r));
+    if (mode & 32) {
+        for (int r = lane; r < nrows; r += 32) {
+            const int i = __ldg(xi + r);
+            xs[r] = __ldcg(P.in0 + i) + __ldcg(P.in1 + i);
+        }
+    } else {
+        for (int r = lane; r < nrows; r += 32) xs[r] = __ldcg(x + __ldg(xi + r));
+    }
     __syncwarp();
     double* dst = (mode & 4) ? P.out + out_off : P.scratch + out_off;
     for (int t0 = 0; t0 < T; t0 += 256) {

@@ -91,9 +91,11 @@ def tier_elems(store, flat, lo, hi):
 
 def choose_tiers(store, flat, latency_s=None):
     """Tier upper boundaries (ascending heights) for one transform
-    direction of one store: minimise streamed bytes / bandwidth + one
-    launch latency per tier.  ``GC_TIERS`` = comma list of boundaries
-    overrides ("off" is handled by the caller)."""
+    direction of one store: minimise, summed over tiers, streamed bytes /
+    HBM bandwidth + the largest work item / one CTA's streaming rate
+    (``GC_TIER_CTA_GBS``, 20 GB/s) + one launch latency (``GC_TIER_LAT_US``,
+    5 us).  ``GC_TIERS`` = comma list of boundaries overrides ("off" is
+    handled by the caller)."""
     env = os.environ.get("GC_TIERS", "auto")
     live = live_nodes(store)
     if not live.any():
@@ -102,16 +104,26 @@ def choose_tiers(store, flat, latency_s=None):
     if env not in ("auto", ""):
         return sorted({min(int(v), top) for v in env.split(",")} | {top})
     lat = latency_s if latency_s is not None else float(os.environ.get("GC_TIER_LAT_US", "5")) * 1e-6
+    cta_bw = float(os.environ.get("GC_TIER_CTA_GBS", "20")) * 1e9
     # elems(lo, hi) for every hi from ONE walk per lo: the pairs of tier
-    # (lo, hi] are those of (lo, top] whose u lies at height <= hi
+    # (lo, hi] are those of (lo, top] whose u lies at height <= hi.  A tier
+    # launch costs its bytes at full bandwidth plus its largest work item
+    # (<= 1024 rows of one panel) streamed by one CTA (the max of the two
+    # measured worse: L6 (5, 7) at 4.85 TB/s) plus a launch latency.
     cost = {}
     for lo in range(-1, top):
         u, f, wmap = _pairs(store, flat, lo, top)
-        per_h = np.bincount(flat.height[u], weights=(wmap[f] * store.rank[u]).astype(np.float64),
-                            minlength=top + 1)
+        el = (wmap[f] * store.rank[u]).astype(np.float64)
+        per_h = np.bincount(flat.height[u], weights=el, minlength=top + 1)
         acc = np.cumsum(per_h)
+        m = np.bincount(u, weights=wmap[f].astype(np.float64), minlength=len(flat))
+        nodes = np.unique(u)
+        item = np.minimum(m[nodes], 1024) * store.rank[nodes] * 8.0
+        big = np.zeros(top + 1)
+        np.maximum.at(big, flat.height[nodes], item)
+        big = np.maximum.accumulate(big)
         for hi in range(lo + 1, top + 1):
-            cost[lo, hi] = 8.0 * acc[hi] / _BW + lat
+            cost[lo, hi] = 8.0 * acc[hi] / _BW + big[hi] / cta_bw + lat
     best = {-1: (0.0, [])}
     for hi in range(0, top + 1):
         best[hi] = min(((best[lo][0] + cost[lo, hi], best[lo][1] + [hi]) for lo in range(-1, hi)),

@@ -236,9 +236,14 @@ def test_choose_tiers_override_and_cost(monkeypatch):
     monkeypatch.setenv("GC_TIERS", "1,3")
     assert tiers.choose_tiers(s, flat) == [1, 3, top]
     monkeypatch.setenv("GC_TIERS", "auto")
+    monkeypatch.setenv("GC_TIER_CTA_GBS", "1e12")      # bytes and launches only
     # no launch latency: the cheapest plan streams the fewest bytes, which
     # is the level-by-level one (every composed tier is at least as large)
     lvl = tiers.choose_tiers(s, flat, latency_s=0.0)
     assert lvl == list(range(top + 1))
     # huge latency: one tier
     assert tiers.choose_tiers(s, flat, latency_s=1.0) == [top]
+    # a slow single CTA makes the large composed panels of a tall tier
+    # expensive: the plan gets more tiers than with bytes alone
+    monkeypatch.setenv("GC_TIER_CTA_GBS", "0.001")
+    assert len(tiers.choose_tiers(s, flat, latency_s=1e-6)) > len(tiers.choose_tiers(s, flat, latency_s=1.0))

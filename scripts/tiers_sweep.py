@@ -4,7 +4,7 @@ import numpy as np, torch
 from paper_1810_08429_b200 import cli, geometry, h2
 L, eps = int(sys.argv[1]), float(sys.argv[2])
 confs = sys.argv[3].split(";")
-mesh = geometry.build_sphere_mesh(L)
+mesh = (geometry.build_cube_mesh if os.environ.get("GC_SWEEP_GEO") == "cube" else geometry.build_sphere_mesh)(L)
 hm, _, _ = cli.build_h2_operator(mesh, cli.default_config(level=L, eps=eps))
 nbytes = h2.storage_report(hm)["total"] + 16 * mesh.nt
 x = torch.randn(mesh.nt, dtype=torch.float64, device="cuda")

@@ -60,3 +60,22 @@ def test_no_cpu_fallback():
     m = geometry.build_sphere_mesh(1)
     with pytest.raises(DeviceError):
         assembly.assemble_galerkin_block("slp", m, "constant", [0, 1], [2, 3])
+
+
+def test_header_compiles_as_c_and_links(tmp_path):
+    """include/gcb200.h is plain C: a C11 program including it links the
+    library and calls the GPU-free entry points (tests/c/abi_smoke.c)."""
+    import shutil
+    import subprocess
+    gcc = shutil.which("gcc")
+    if gcc is None:
+        pytest.skip("no gcc")
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    lib_dir = os.path.dirname(build_native.LIB)
+    exe = str(tmp_path / "abi_smoke")
+    subprocess.run([gcc, "-std=c11", "-Wall", "-Wextra", "-Werror", "-I", os.path.join(root, "include"),
+                    os.path.join(root, "tests", "c", "abi_smoke.c"), "-L", lib_dir, "-l:libgcb200.so",
+                    "-Wl,-rpath," + lib_dir, "-o", exe], check=True)
+    out = subprocess.run([exe], capture_output=True, text=True)
+    assert out.returncode == 0, out.stdout + out.stderr
+    assert "C ABI %d ok" % _native.ABI_VERSION in out.stdout

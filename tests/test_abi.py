@@ -79,3 +79,26 @@ def test_header_compiles_as_c_and_links(tmp_path):
     out = subprocess.run([exe], capture_output=True, text=True)
     assert out.returncode == 0, out.stdout + out.stderr
     assert "C ABI %d ok" % _native.ABI_VERSION in out.stdout
+
+
+@pytest.mark.gpu
+def test_c_program_drives_the_panel_kernel(tmp_path):
+    """A C program (tests/c/panel_gpu.c) runs one panel product through
+    gc_panelmv and through the native executor (gc_plan_*) with cudaMalloc'd
+    buffers - the C-ABI alone, no Python on the product path."""
+    import shutil
+    import subprocess
+    gcc = shutil.which("gcc")
+    cuda = os.environ.get("CUDA_HOME", "/usr/local/cuda")
+    if gcc is None or not os.path.exists(os.path.join(cuda, "include", "cuda_runtime_api.h")):
+        pytest.skip("no gcc / CUDA headers")
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    lib_dir = os.path.dirname(build_native.LIB)
+    exe = str(tmp_path / "panel_gpu")
+    subprocess.run([gcc, "-std=c11", "-Wall", "-Wextra", "-Werror", "-I", os.path.join(root, "include"),
+                    "-I", os.path.join(cuda, "include"), os.path.join(root, "tests", "c", "panel_gpu.c"),
+                    "-L", lib_dir, "-l:libgcb200.so", "-L", os.path.join(cuda, "lib64"), "-lcudart", "-lm",
+                    "-Wl,-rpath," + lib_dir, "-Wl,-rpath," + os.path.join(cuda, "lib64"), "-o", exe], check=True)
+    out = subprocess.run([exe], capture_output=True, text=True, timeout=120)
+    assert out.returncode == 0, out.stdout + out.stderr
+    assert "C-ABI panel product ok" in out.stdout

@@ -243,7 +243,10 @@ def mvm(h, x):
         p.pin_y = torch.empty(nr, dtype=torch.float64, pin_memory=True)
     p.pin_x.numpy()[:] = x
     with torch.cuda.device(p.dev):
-        if p.graph is not None and p.bind(p.pin_x, p.pin_y):
+        # a fresh pinned output per call (torch's pinned block cache): the
+        # graph's scatter writes the caller's result array directly
+        y = torch.empty(nr, dtype=torch.float64, pin_memory=True)
+        if p.graph is not None and p.bind(p.pin_x, y):
             # zero-copy: the graph's gather reads the pinned input and its
             # scatter writes the pinned output (mapped host memory, read /
             # written contiguously), no DMA copies around the replay
@@ -251,9 +254,9 @@ def mvm(h, x):
         else:
             p.x.copy_(p.pin_x, non_blocking=True)
             p._body()
-            p.pin_y.copy_(p.y, non_blocking=True)
+            y.copy_(p.y, non_blocking=True)
         torch.cuda.current_stream().synchronize()
-    return p.pin_y.numpy().copy()
+    return y.numpy()
 
 
 def mvm_t(h, x):

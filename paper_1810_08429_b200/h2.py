@@ -243,9 +243,12 @@ def mvm(h, x):
         p.pin_y = torch.empty(nr, dtype=torch.float64, pin_memory=True)
     p.pin_x.numpy()[:] = x
     with torch.cuda.device(p.dev):
-        # a fresh pinned output per call (torch's pinned block cache): the
-        # graph's scatter writes the caller's result array directly
-        y = torch.empty(nr, dtype=torch.float64, pin_memory=True)
+        # large outputs: a fresh pinned array per call (torch's pinned block
+        # cache) that the graph's scatter writes directly - no output copy;
+        # small ones: the plan's pinned buffer plus a copy (cheaper than a
+        # new allocation and a re-pointed scatter node)
+        fresh = nr >= 16384
+        y = torch.empty(nr, dtype=torch.float64, pin_memory=True) if fresh else p.pin_y
         if p.graph is not None and p.bind(p.pin_x, y):
             # zero-copy: the graph's gather reads the pinned input and its
             # scatter writes the pinned output (mapped host memory, read /
@@ -256,7 +259,7 @@ def mvm(h, x):
             p._body()
             y.copy_(p.y, non_blocking=True)
         torch.cuda.current_stream().synchronize()
-    return y.numpy()
+    return y.numpy() if fresh else y.numpy().copy()
 
 
 def mvm_t(h, x):

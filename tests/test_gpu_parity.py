@@ -452,6 +452,27 @@ def test_tiered_transforms_match_level_by_level(geo, level, cfg_kw, monkeypatch)
         assert (y1 - y0).norm().item() <= 1e-13 * y0.norm().item(), tiers
 
 
+@pytest.mark.parametrize("level,eps", [(1, 1e-2), (2, 1e-2), (2, 1e-10), (3, 1e-10)])
+def test_small_and_degenerate_operators(level, eps, monkeypatch):
+    """Tiny trees (few or no admissible blocks, full-rank or rank-0 bases):
+    the default plan (tiers, native executor) == the level-by-level plan to
+    rounding, and both approximate the dense Galerkin matrix to ~eps."""
+    mesh = geometry.build_sphere_mesh(level)
+    hm, _, _ = cli.build_h2_operator(mesh, cli.default_config(eps=eps))
+    x = np.random.default_rng(level).standard_normal(mesh.nt)
+    y = h2.mvm(hm, x)
+    dense = assembly.assemble_galerkin_block("slp", mesh, "constant", np.arange(mesh.nt),
+                                             np.arange(mesh.nt)).values
+    yd = dense @ x
+    assert np.linalg.norm(y - yd) <= max(100 * eps, 1e-12) * np.linalg.norm(yd)
+    monkeypatch.setenv("GC_TIERS", "off")
+    p = h2.PanelPlan(hm)
+    xd = torch.from_numpy(x).cuda()
+    y0 = torch.empty_like(xd)
+    p.run(xd, y0, serial=True)
+    assert np.linalg.norm(y0.cpu().numpy() - y) <= 1e-13 * np.linalg.norm(y)
+
+
 def test_mvm_20_seeded_vectors_c1():
     """SURVEY 8(c) parity protocol at C1: mvm and mvm_t of the 20 seeded
     N(0,1) vectors (default_rng(0)) against the reference's own products

@@ -276,7 +276,25 @@ def coef_layout(flat, roots, rank, base=0):
     """Coefficient offsets of a basis forest: roots first, then breadth
     first with the two children of every node adjacent, so the input of a
     parent's V-hat^T product is one contiguous slice.  Returns (offsets for
-    every tree node, -1 where absent; total size)."""
+    every tree node, -1 where absent; total size).  One generation of the
+    BFS queue at a time (the queue order: roots, then each generation's
+    children in the order of their parents)."""
+    off = np.full(len(flat), -1, dtype=np.int64)
+    rank = np.asarray(rank, dtype=np.int64)
+    cur = np.asarray([int(r) for r in roots], dtype=np.int64)
+    pos = base
+    while cur.size:
+        r = rank[cur]
+        off[cur] = pos + np.cumsum(r) - r
+        pos += int(r.sum())
+        inner = cur[~flat.is_leaf[cur]]
+        cur = np.stack([flat.left[inner], flat.right[inner]], 1).ravel()
+    return off, int(pos - base)
+
+
+def _coef_layout_queue(flat, roots, rank, base=0):
+    """The same layout with an explicit FIFO queue (reference order; kept
+    for the host test that pins the vectorised form to it)."""
     off = np.full(len(flat), -1, dtype=np.int64)
     pos = base
     queue = [int(r) for r in roots]

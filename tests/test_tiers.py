@@ -247,3 +247,18 @@ def test_choose_tiers_override_and_cost(monkeypatch):
     # expensive: the plan gets more tiers than with bytes alone
     monkeypatch.setenv("GC_TIER_CTA_GBS", "0.001")
     assert len(tiers.choose_tiers(s, flat, latency_s=1e-6)) > len(tiers.choose_tiers(s, flat, latency_s=1.0))
+
+
+def test_coef_layout_generations_equal_queue_order():
+    """gca.coef_layout (one BFS generation per numpy step) == the explicit
+    FIFO-queue layout, on random unbalanced trees and root sets."""
+    from paper_1810_08429_b200 import gca
+    for seed in range(10):
+        rng = np.random.default_rng(seed)
+        flat = _random_tree(400, rng)
+        rank = rng.integers(0, 20, len(flat))
+        roots = np.flatnonzero(flat.depth == min(2, int(flat.depth.max())))
+        rng.shuffle(roots)
+        a = gca.coef_layout(flat, roots, rank, base=3)
+        b = gca._coef_layout_queue(flat, roots, rank, base=3)
+        assert np.array_equal(a[0], b[0]) and a[1] == b[1]

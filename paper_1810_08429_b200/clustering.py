@@ -494,12 +494,20 @@ def _admissible_many(rt, ct, r, c, eta):
     1e-12 relative of flipping it is redone with the reference's 1-D BLAS
     norm, so the decision is bit-for-bit the reference's."""
     d = np.maximum(rt.diam[r], ct.diam[c])
-    gap = np.maximum(0.0, np.maximum(rt.lower[r] - ct.upper[c], ct.lower[c] - rt.upper[r]))
-    rhs = 2.0 * eta * _gap_norm_vector(gap)
+    # per coordinate (1-D gathers of the box columns; same values as the
+    # (N, 3) form, about 3x faster)
+    lo_r, up_r, lo_c, up_c = rt.lower.T, rt.upper.T, ct.lower.T, ct.upper.T
+    g = []
+    for k in range(3):
+        a = lo_r[k][r] - up_c[k][c]
+        np.maximum(a, lo_c[k][c] - up_r[k][r], out=a)
+        np.maximum(a, 0.0, out=a)
+        g.append(a)
+    rhs = 2.0 * eta * np.sqrt((g[0] * g[0] + g[1] * g[1]) + g[2] * g[2])
     adm = d <= rhs
     close = np.flatnonzero(np.abs(d - rhs) <= 1e-12 * np.maximum(d, rhs))
     for i in close:
-        adm[i] = d[i] <= 2.0 * eta * _blas_norm(gap[i])
+        adm[i] = d[i] <= 2.0 * eta * _blas_norm(np.array([g[0][i], g[1][i], g[2][i]]))
     return adm
 
 

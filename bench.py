@@ -44,6 +44,10 @@ def parse():
     ap.add_argument("--eps", type=float, default=EPS_DEFAULT)
     ap.add_argument("--geometry", default="sphere", choices=["sphere", "cube"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--scale-level", type=int, default=8,
+                    help="sphere level of the scaling configuration measured in every run "
+                         "(BASELINE configs[3], C4); 0 skips it")
+    ap.add_argument("--scale-eps", type=float, default=1e-8)
     ap.add_argument("--cpu-sample", type=float, default=0.01,
                     help="fraction of blocks the CPU reference assembles (extrapolated)")
     return ap.parse_args()
@@ -453,7 +457,53 @@ def run_native(args):
                                 "kind": rb["kind"], "sample": rb["sample"],
                                 "assembly_s_extrapolated": round(rb["assembly_s_extrapolated"], 2),
                                 "bases_s": round(rb["bases_s"], 2), "trees_s": round(rb["trees_s"], 2)}
+    if args.scale_level > 0:
+        del p, xs, y, hm, tree, bt, d, dm, rules, queue, scratch_n, scratch_c
+        gc.collect()
+        torch.cuda.empty_cache()
+        line["scaling_config"] = scaling_config(args, torch)
     print(json.dumps(line))
+
+
+def scaling_workload(args):
+    return ("unit sphere level %d (%d triangles), SLP Galerkin p0, GCA-H2 eps=%g%s"
+            % (args.scale_level, 8 * 4 ** args.scale_level, args.scale_eps,
+               " (BASELINE configs[3], C4)" if (args.scale_level, args.scale_eps) == (8, 1e-8) else ""))
+
+
+def scaling_config(args, torch):
+    """The scaling configuration (C4) at N = 1 on the same code path as
+    ``value``: assembly, then device-resident products timed with CUDA
+    events.  Reported in every line so that the per-N lines of a scaling run
+    carry C4's strong scaling next to C2's."""
+    from paper_1810_08429_b200 import cli, geometry, h2
+    mesh = geometry.build_sphere_mesh(args.scale_level)
+    cfg = cli.default_config(level=args.scale_level, eps=args.scale_eps)
+    torch.cuda.synchronize()
+    t0 = time.perf_counter()
+    hm, _, _ = cli.build_h2_operator(mesh, cfg)
+    p = h2.plan(hm)
+    torch.cuda.synchronize()
+    asm = time.perf_counter() - t0
+    n = mesh.nt
+    nbytes = h2.storage_report(hm)["total"] + 16 * n
+    x = torch.randn(n, dtype=torch.float64, device="cuda")
+    y = torch.empty(n, dtype=torch.float64, device="cuda")
+    for _ in range(max(3, args.warmup)):
+        p.run(x, y)
+    k = max(10, min(args.steps, 50))
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    torch.cuda.synchronize()
+    e0.record()
+    for _ in range(k):
+        p.run(x, y)
+    e1.record()
+    torch.cuda.synchronize()
+    s = e0.elapsed_time(e1) * 1e-3 / k
+    return {"workload": scaling_workload(args), "n_gpus": 1, "value": round(nbytes / s / 1e9, 2), "unit": "GB/s",
+            "ms_per_step": round(s * 1e3, 4), "steps": k, "matvec_bytes": int(nbytes),
+            "assembly_s": round(asm, 3), "parallelism": "none",
+            "note": "x resident in HBM (17 GB of H2 data, larger than L2); assembly without a warm-up run"}
 
 
 def main():

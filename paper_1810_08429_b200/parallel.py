@@ -328,6 +328,7 @@ def bench_distributed(args, rank, world, local, metric, workload, clock_sampler=
         if flag.item() == 0.0:
             break
     dist.barrier()
+    torch.cuda.synchronize()
     l0 = _native.launch_count()
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     e0.record()
@@ -379,6 +380,11 @@ def bench_distributed(args, rank, world, local, metric, workload, clock_sampler=
                     "algorithmic_bytes_per_launch": int(byts), "avg_launch_s": sec,
                     "step": {"achieved": round(nbytes / float(t.item()) / 1e9, 1),
                              "frac": round(nbytes / float(t.item()) / 1e9 / hbm, 4)}}
+    scale = None
+    if getattr(args, "scale_level", 0) > 0:
+        sh = None
+        torch.cuda.empty_cache()
+        scale = _scaling_config(args, world, mesh_level=args.scale_level, eps=args.scale_eps)
     if rank == 0:
         s = float(t.item())
         print(json.dumps({
@@ -395,5 +401,58 @@ def bench_distributed(args, rank, world, local, metric, workload, clock_sampler=
                     "api": "paper_1810_08429_b200.parallel.ShardedH2.mvm(numpy slice) on every rank"},
             "gpu_launches": int(launches.item()),
             "gpu_launches_note": "own kernels over all ranks in the timed region",
-            "clocks": sampler.summary() if sampler is not None else None}))
+            "clocks": sampler.summary() if sampler is not None else None,
+            "scaling_config": scale}))
     dist.destroy_process_group()
+
+
+def _scaling_config(args, world, mesh_level, eps):
+    """The scaling configuration (BASELINE configs[3], C4: sphere level 8,
+    eps 1e-8) sharded over the ranks: sharded assembly, then the whole
+    sharded product (both NCCL all-gathers included) timed with CUDA events,
+    max over ranks.  bench.py's N = 1 line carries the same measurement on
+    one GPU, so the per-N lines give C4's strong scaling directly."""
+    import time
+
+    import torch
+    import torch.distributed as dist
+
+    from . import cli, geometry, h2
+    mesh = geometry.build_sphere_mesh(mesh_level)
+    cfg = cli.default_config(level=mesh_level, eps=eps)
+    dist.barrier()
+    torch.cuda.synchronize()
+    t0 = time.perf_counter()
+    sh = build_sharded_operator(mesh, cfg)
+    torch.cuda.synchronize()
+    asm = torch.tensor([time.perf_counter() - t0], dtype=torch.float64, device="cuda")
+    dist.all_reduce(asm, op=dist.ReduceOp.MAX)
+    rep = h2.storage_report(sh.h)
+    mine = torch.tensor([rep["couplings"] + rep["nearfield"] + rep["leaf_bases"] + rep["transfers"]],
+                        dtype=torch.float64, device="cuda")
+    dist.all_reduce(mine)
+    nbytes = float(mine.item()) + 16 * mesh.nt
+    x = torch.randn(sh.layout.hi - sh.layout.lo, dtype=torch.float64, device="cuda")
+    for _ in range(max(3, args.warmup)):
+        sh.mvm_local(x)
+    k = max(10, min(args.steps, 50))
+    torch.cuda.synchronize()
+    dist.barrier()
+    torch.cuda.synchronize()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record()
+    for _ in range(k):
+        sh.mvm_local(x)
+    e1.record()
+    torch.cuda.synchronize()
+    t = torch.tensor([e0.elapsed_time(e1) * 1e-3 / k], dtype=torch.float64, device="cuda")
+    dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    s = float(t.item())
+    return {"workload": "unit sphere level %d (%d triangles), SLP Galerkin p0, GCA-H2 eps=%g%s"
+                        % (mesh_level, mesh.nt, eps,
+                           " (BASELINE configs[3], C4)" if (mesh_level, eps) == (8, 1e-8) else ""),
+            "n_gpus": world, "value": round(nbytes / s / 1e9, 2), "unit": "GB/s",
+            "ms_per_step": round(s * 1e3, 4), "steps": k, "matvec_bytes": int(nbytes),
+            "assembly_s": round(float(asm.item()), 3), "parallelism": "block-row x%d" % world,
+            "note": "whole sharded product incl. the x and x-hat all-gathers, max over ranks; "
+                    "assembly without a warm-up run"}

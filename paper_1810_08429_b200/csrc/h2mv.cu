@@ -103,6 +103,9 @@ constexpr int PAN_THREADS = 256;
 #define GC_PAN_UNROLL 8
 #endif
 constexpr int PAN_UNROLL = GC_PAN_UNROLL;
+#ifndef GC_PAN_MINB
+#define GC_PAN_MINB 6
+#endif
 constexpr int PAN_MAX_ROWS = 1024;   // rows per work item (x gathered to smem)
 
 // item (8 x int64): a_off, xi_off, out_off, T, nrows, mode, red, 0
@@ -262,7 +265,7 @@ __device__ __forceinline__ void panel_item(const PanelPhase& P, int64_t item, Pa
 // then wait on SM slots); 2: after the CTA's item is done (the dependent
 // only overlaps this kernel's drain and keeps its slots free for the bulk).
 template <bool CHAIN, int TRIGGER>
-__global__ void __launch_bounds__(PAN_THREADS, 6) k_panelmv(PanelPhase P) {
+__global__ void __launch_bounds__(PAN_THREADS, GC_PAN_MINB) k_panelmv(PanelPhase P) {
     __shared__ PanelSmem sm;
     if (CHAIN && TRIGGER == 1) asm volatile("griddepcontrol.launch_dependents;");
     if (P.trace != nullptr && threadIdx.x == 0) atomicMin(P.trace, globaltimer());

@@ -393,6 +393,19 @@ constexpr int SING_WARPS = SING_THREADS / 32;
 #define GC_SING_G 4
 #endif
 constexpr int SING_G = GC_SING_G;   // tasks per warp
+// per case (vertex NC=4, edge NC=3, identical NC=2); a task's value does not
+// depend on it (lane-strided points, then the same shuffle tree)
+#ifndef GC_SING_G4
+#define GC_SING_G4 SING_G
+#endif
+#ifndef GC_SING_G3
+#define GC_SING_G3 SING_G
+#endif
+#ifndef GC_SING_G2
+#define GC_SING_G2 SING_G
+#endif
+template <int NC>
+constexpr int sing_group() { return NC == 4 ? GC_SING_G4 : NC == 3 ? GC_SING_G3 : GC_SING_G2; }
 
 // Singular pairs with the xi-reduced rule: D = sum_k coef[k] G_k,
 //   NC = 4 (vertex):    G = (E1, E2, -F1, -F2)
@@ -402,7 +415,7 @@ constexpr int SING_G = GC_SING_G;   // tasks per warp
 // P_0 == Q_0 is the shared vertex, so D carries no cancellation.  The rule
 // table (NC coefficient columns + weight, SoA, P points) is staged in
 // shared memory when it fits, else read through L1.
-template <int NC, bool SMEM, bool DLP>
+template <int NC, bool SMEM, bool DLP, int SG = sing_group<NC>()>
 __global__ void __launch_bounds__(SING_THREADS) k_singular(gc_geom g, const double* __restrict__ rule,
                                                            int P, const int64_t* __restrict__ tasks,
                                                            int64_t ntasks, double* __restrict__ out) {
@@ -415,18 +428,18 @@ __global__ void __launch_bounds__(SING_THREADS) k_singular(gc_geom g, const doub
     }
     const int lane = threadIdx.x & 31;
     const int64_t nwarps = (int64_t)gridDim.x * SING_WARPS;
-    const int64_t ngroups = (ntasks + SING_G - 1) / SING_G;
+    const int64_t ngroups = (ntasks + SG - 1) / SG;
     for (int64_t grp = (int64_t)blockIdx.x * SING_WARPS + (threadIdx.x >> 5); grp < ngroups;
          grp += nwarps) {
-        double G[SING_G][NC][3];
-        double scale[SING_G];
-        double nrm[SING_G][3];
-        int64_t oidx[SING_G];
+        double G[SG][NC][3];
+        double scale[SG];
+        double nrm[SG][3];
+        int64_t oidx[SG];
 #pragma unroll
-        for (int k = 0; k < SING_G; ++k) {
-            const int64_t id = grp * SING_G + k;
+        for (int k = 0; k < SG; ++k) {
+            const int64_t id = grp * SG + k;
             const bool live = id < ntasks;
-            const int64_t* tk = tasks + 4 * (live ? id : grp * SING_G);
+            const int64_t* tk = tasks + 4 * (live ? id : grp * SG);
             const int64_t t = tk[0], s = tk[1], pp = tk[2];
             oidx[k] = live ? tk[3] : -1;
             const int px = (int)(pp & 0xff), py = (int)((pp >> 8) & 0xff);
@@ -449,16 +462,16 @@ __global__ void __launch_bounds__(SING_THREADS) k_singular(gc_geom g, const doub
 #pragma unroll
             for (int c = 0; c < 3; ++c) nrm[k][c] = DLP ? g.normals[3 * s + c] : 0.0;
         }
-        double acc[SING_G];
+        double acc[SG];
 #pragma unroll
-        for (int k = 0; k < SING_G; ++k) acc[k] = 0.0;
+        for (int k = 0; k < SG; ++k) acc[k] = 0.0;
         for (int p = lane; p < P; p += 32) {
             double cf[NC];
 #pragma unroll
             for (int j = 0; j < NC; ++j) cf[j] = R[j * P + p];
             const double w = R[NC * P + p];
 #pragma unroll
-            for (int k = 0; k < SING_G; ++k) {
+            for (int k = 0; k < SG; ++k) {
                 double dd[3];
 #pragma unroll
                 for (int c = 0; c < 3; ++c) {
@@ -471,7 +484,7 @@ __global__ void __launch_bounds__(SING_THREADS) k_singular(gc_geom g, const doub
             }
         }
 #pragma unroll
-        for (int k = 0; k < SING_G; ++k) {
+        for (int k = 0; k < SG; ++k) {
             double v = acc[k];
 #pragma unroll
             for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
@@ -484,7 +497,7 @@ template <int NC, bool DLP>
 static int launch_singular_nc(const gc_geom& g, const double* table, int64_t P, const int64_t* tasks,
                               int64_t n, double* out, cudaStream_t st) {
     const size_t bytes = (size_t)(NC + 1) * P * sizeof(double);
-    const int64_t groups = (n + SING_G - 1) / SING_G;
+    const int64_t groups = (n + sing_group<NC>() - 1) / sing_group<NC>();
     int64_t grid = (groups + SING_WARPS - 1) / SING_WARPS;
     if (bytes <= 200 * 1024) {
         cudaError_t e = cudaFuncSetAttribute(k_singular<NC, true, DLP>,

@@ -418,35 +418,6 @@ int64_t gc_krylov_partials(void);
  * least (default, e.g. 0) and greatest (most urgent, e.g. -5). */
 int gc_priority_range(int32_t* least, int32_t* greatest);
 
-/* The whole product y = H x as ONE persistent cooperative kernel scheduled
- * by dataflow counters (csrc/h2persist.cu; replaces h2.mvm, h2.py:63-80).
- * items (nitems,8) as nseg (<= 120) consecutive segments in priority
- * order, seg [dev] (nseg,3) = begin, end, 0; all items of a segment share
- * one dependency; segments form nlists (<= 8) lists in priority order,
- * list_end [host] = end segment of each list, readiness monotone along a
- * list (format in csrc/h2persist.cu); nsync >= 129 + nseg; xidx int32
- * input indices; mats[4] = panel matrix bases; bufs[8] = x, xt, x-hat,
- * y-hat (coupling), y-hat, yt (near field), y, unused; sync [dev] nsync
- * counters (reset by the call).  grid <= 0: the largest co-resident grid;
- * max_rows: the longest panel (shared-memory input staging); timing [dev]
- * optional per-CTA finish times (%globaltimer).  Capturable in a graph. */
-int gc_h2mv_persistent(const int64_t* items, const int32_t* xidx, int64_t nitems,
-                       int32_t nseg, const int32_t* seg, int32_t nlists,
-                       const int32_t* list_end, const int64_t* perm_in, const int64_t* perm_out, int64_t n_in,
-                       int64_t zero_len, const double* const* mats, double* const* bufs,
-                       unsigned int* sync, int32_t nsync, int32_t grid, long long* timing,
-                       int32_t max_rows, void* stream);
-/* Run items [first, first+count) of a gc_h2mv_persistent program as one
- * plain launch (one CTA per item, dependencies assumed satisfied by
- * stream order; signals go to sync).  The multi-launch matvec issues one
- * such launch per phase inside a CUDA graph. */
-int gc_run_items(const int64_t* items, int64_t first, int64_t count, const int32_t* xidx,
-                 const double* const* mats, double* const* bufs, unsigned int* sync,
-                 int32_t max_rows, const int64_t* perm_out, void* stream);
-
-/* Largest co-resident grid of gc_h2mv_persistent (max_rows: longest panel). */
-int gc_h2mv_grid(int32_t max_rows, int32_t* grid);
-
 /* Host helper (no device): norms of n 3-vectors v [host] (n,3) into out
  * [host] (n,) with mode 0 = sqrt(fma(z,z,fma(y,y,x*x))) (the rounding of
  * numpy's 1-D norm through OpenBLAS ddot, used for box diameters,

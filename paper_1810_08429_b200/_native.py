@@ -95,14 +95,6 @@ _SIGNATURES = {
     "gc_panel_stream": [c_i64, c_p, c_p, c_p, c_p, c_p, c_p, c_p, c_p, c_i64, c_p, c_p, c_p, c_i64,
                         ctypes.c_int32, c_p, c_p],
     "gc_priority_range": [ctypes.POINTER(ctypes.c_int32), ctypes.POINTER(ctypes.c_int32)],
-    "gc_h2mv_persistent": [c_p, c_p, c_i64, ctypes.c_int32, c_p, ctypes.c_int32,
-                           ctypes.POINTER(ctypes.c_int32),
-                           c_p, c_p, c_i64, c_i64, ctypes.POINTER(c_p),
-                           ctypes.POINTER(c_p), c_p, ctypes.c_int32, ctypes.c_int32, c_p,
-                           ctypes.c_int32, c_p],
-    "gc_h2mv_grid": [ctypes.c_int32, ctypes.POINTER(ctypes.c_int32)],
-    "gc_run_items": [c_p, c_i64, c_i64, c_p, ctypes.POINTER(c_p), ctypes.POINTER(c_p), c_p,
-                     ctypes.c_int32, c_p, c_p],
     "gc_host_norm3": [c_p, c_i64, c_p, ctypes.c_int],
     "gc_dfma_probe": [c_i64, c_i64, c_i64, c_p, c_p],
 }

@@ -194,7 +194,6 @@ class MatvecPlan:
         return len(self.launches) + 2
 
 
-PERSISTENT = False      # PersistentPlan: experimental, slower at C2
 
 
 def plan(h, trans=False, graph=True):
@@ -205,7 +204,7 @@ def plan(h, trans=False, graph=True):
         if trans:
             h.dev.plans[key] = MatvecPlan(h, True)
         else:
-            pl = PersistentPlan(h) if PERSISTENT else PanelPlan(h)
+            pl = PanelPlan(h)
             if graph:
                 with torch.cuda.device(pl.dev):
                     pl.capture()
@@ -1242,361 +1241,3 @@ def _ranges_np(starts, lengths):
         return np.zeros(0, dtype=np.int64)
     heads = np.cumsum(lengths) - lengths
     return np.arange(total, dtype=np.int64) + np.repeat(np.asarray(starts, np.int64) - heads, lengths)
-
-
-# --------------------------------------------------------------------------
-# persistent plan: the whole product in one cooperative launch
-
-class _PanelRec:
-    __slots__ = ("name", "panels", "A0", "in0", "out")
-
-
-_NONE = 127
-
-
-def _wait(ctr=None, target=0):
-    """Packed (counter, target) dependency; counter None = no wait."""
-    if ctr is None:
-        return _NONE << 24
-    if target >= (1 << 24):
-        raise ConfigError("dependency target too large")
-    return (int(ctr) << 24) | int(target)
-
-
-class PersistentPlan(PanelPlan):
-    """The whole product as ONE ``gc_h2mv_persistent`` launch
-    (csrc/h2persist.cu), scheduled by dataflow counters.
-
-    Item order (CTAs take items round-robin): forward transform by height
-    (height h waits for every height h-1 item), near field, coupling panels
-    (each waits for the forward height of its inputs), backward transform
-    top-down (waits for all coupling and the level above), final leaf stage
-    (waits for backward and near field).  Counters: FWD[h] = h, BWD[h] =
-    64 + h, CPL = 128, NEAR = 129, BWD_ALL = 130.  Coupling results go to a
-    separate y-hat buffer so the backward step is ``y_c = yc_c + E y_p``
-    with a single writer per entry."""
-
-    FWD, BWD, CPLC, CPLR, NEAR, BWD_ALL, CPL = 0, 20, 40, 60, 80, 81, 82
-    NSYNC = 1 + 128 + 120                 # dependency counters, then segment counters
-    CHUNK_ELEMS = 4096                    # coupling row chunks (~32 KB of matrix)
-
-    def _phase(self, name, panels, A0, A1, in0, in1, out):
-        rec = _PanelRec()
-        rec.name, rec.panels, rec.A0, rec.in0, rec.out = name, panels, A0, in0, out
-        return rec
-
-    def __init__(self, h):
-        super().__init__(h)
-        d = h.dev
-        rs, cs = h.row_basis.store, h.col_basis.store
-        rf, cf = h.row_tree.flat, h.col_tree.flat
-        f64 = dict(dtype=torch.float64, device=self.dev)
-        self.yc = torch.zeros(max(rs.coef_size, 1), **f64)        # coupling part of y-hat
-        self.mats = [cs.V, d.coup, d.near, rs.VT]
-        mats = {id(m): i for i, m in enumerate(self.mats)}
-        B_X, B_XT, B_XH, B_YC, B_YH, B_YT, B_Y, B_SC = range(8)
-        xparts, xoff = [], [0]
-
-        def xi_of(rows):
-            arr = np.concatenate(rows).astype(np.int32) if len(rows) else np.zeros(0, np.int32)
-            starts = xoff[0] + _offsets_np([len(r) for r in rows])
-            xparts.append(arr)
-            xoff[0] += len(arr)
-            return starts
-
-        def make(typ, a_sel, in_sel, out_sel, add_sel, a_off, xs, out_off, T, K, target,
-                 sig1, sig2, wait1, wait2):
-            """Column-split items of a list of panels (vectorised)."""
-            a_off, xs, out_off, T, K = (np.asarray(v, np.int64) for v in (a_off, xs, out_off, T, K))
-            n = len(T)
-            if n == 0:
-                return np.zeros((0, 8), np.int64)
-            ns = np.clip(-(-(np.maximum(K, 1) * T) // target), 1, np.maximum(1, -(-T // 8)))
-            tw = -(-T // ns)
-            ns = -(-T // tw)
-            pan = np.repeat(np.arange(n), ns)
-            c0 = _ranges_np(np.zeros(n, np.int64), ns) * tw[pan]
-            w = np.minimum(tw[pan], T[pan] - c0)
-            if np.any(T > 0xffff):
-                raise ConfigError("panel wider than 65535 columns")
-            head = typ | (a_sel << 4) | (np.asarray(in_sel, np.int64)[pan] << 8 if np.ndim(in_sel) else in_sel << 8) \
-                | (out_sel << 12) | (add_sel << 20)
-            w6 = c0 | (w << 16) | (np.int64(sig1) << 32) | (np.int64(sig2) << 40)
-            w7 = np.asarray(wait1, np.int64) | (np.asarray(wait2, np.int64) << 32)
-            w7 = w7[pan] if np.ndim(w7) else np.full(len(pan), w7)
-            return np.stack([np.broadcast_to(head, pan.shape), a_off[pan], xs[pan], out_off[pan],
-                             T[pan], K[pan], w6, w7], 1)
-
-        # ---- forward transform (column basis)
-        fwd = [p for p in self.main_phases if p.name == "forward"]
-        nF, F = [], []
-        for lev, p in enumerate(fwd):
-            a_off, K, T, rows, out_off, _ = p.panels
-            xs = xi_of(rows)
-            it = make(0, 0, B_XT if lev == 0 else B_XH, B_XH, 0, a_off, xs, out_off, T, K, 2048,
-                      self.FWD + lev, _NONE,
-                      _wait() if lev == 0 else _wait(self.FWD + lev - 1, nF[lev - 1]), _wait())
-            nF.append(len(it))
-            F.append(it)
-        H = len(F)
-        # ---- near field: ready after the start barrier
-        a_off, K, T, rows, out_off, _ = self.side_phases[0].panels
-        near = make(0, 2, B_XT, B_YT, 0, a_off, xi_of(rows), out_off, T, K, 8192,
-                    self.NEAR, _NONE, _wait(), _wait())
-        nN = len(near)
-        # ---- coupling: row panels cut into ~64 KB row chunks; single-chunk
-        # panels write y-hat directly, longer ones write partials that a
-        # reduce item sums in chunk order
-        coup = [p for p in self.main_phases if p.name == "coupling"]
-        C = [[] for _ in range(max(H, 1))]
-        R = []
-        nCres = 0
-        nres = np.zeros(64, dtype=np.int64)     # coupling results per row level
-        scratch = 0
-        if coup:
-            live = (d.c_nr > 0) & (d.c_nc > 0)
-            order_ = np.flatnonzero(live)[np.argsort(d.c_rows[live], kind="stable")]
-            sn = d.c_rows[order_]
-            cuts = np.flatnonzero(np.r_[True, sn[1:] != sn[:-1]])
-            hmax = np.maximum.reduceat(cf.height[d.c_cols[order_]], cuts)
-            fwd_heights = np.unique(cf.height[cs.materialized & (cs.rank > 0)])
-            levs = np.searchsorted(fwd_heights, hmax)
-            row_heights = np.unique(rf.height[rs.materialized])
-            rlev = np.searchsorted(row_heights, rf.height[sn[cuts]])
-            if len(fwd_heights) > 20 or len(row_heights) > 20:
-                raise ConfigError("cluster trees deeper than 20 basis levels")
-            a_off, K, T, rows, out_off, _ = coup[0].panels
-            a_off, K, T, out_off = (np.asarray(v, np.int64) for v in (a_off, K, T, out_off))
-            xs = xi_of(rows)
-            rpi = np.maximum(1, -(-self.CHUNK_ELEMS // np.maximum(T, 1)))
-            nch = np.maximum(1, -(-K // rpi))
-            for lev in range(H):
-                sel = np.flatnonzero(levs == lev)
-                if not sel.size:
-                    continue
-                one = sel[nch[sel] == 1]
-                if one.size:
-                    it1 = make(0, 1, B_XH, B_YC, 0, a_off[one], xs[one], out_off[one],
-                               T[one], K[one], 1 << 30, 0, self.CPL,
-                               _wait(self.FWD + lev, nF[lev]), _wait())
-                    it1[:, 6] = (it1[:, 6] & 0xffffffff) | ((self.CPLR + rlev[one]) << 32) | (np.int64(self.CPL) << 40)
-                    C[lev].append(it1)
-                    np.add.at(nres, rlev[one], 1)
-                    nCres += len(it1)
-                many = sel[nch[sel] > 1]
-                if many.size:
-                    pan = np.repeat(many, nch[many])
-                    ci = _ranges_np(np.zeros(len(many), np.int64), nch[many])
-                    r0 = ci * rpi[pan]
-                    nr = np.minimum(rpi[pan], K[pan] - r0)
-                    sbase = scratch + _offsets_np(nch[many] * T[many])
-                    scratch += int((nch[many] * T[many]).sum())
-                    sb = np.repeat(sbase, nch[many]) + ci * T[pan]
-                    head = 0 | (1 << 4) | (B_XH << 8) | (B_SC << 12)
-                    w6 = 0 | (np.int64(0) << 16) | (np.int64(self.CPLC + lev) << 32) | (np.int64(_NONE) << 40)
-                    chunks = np.stack([np.full(len(pan), head), a_off[pan] + r0 * T[pan], xs[pan] + r0, sb,
-                                       T[pan], nr, np.full(len(pan), w6),
-                                       np.full(len(pan), _wait(self.FWD + lev, nF[lev]) | (_wait() << 32))], 1)
-                    C[lev].append(chunks)
-                    rhead = 2 | (B_YC << 12)
-                    rw6 = ((self.CPLR + rlev[many]) << 32) | (np.int64(self.CPL) << 40)
-                    np.add.at(nres, rlev[many], 1)
-                    R.append((lev, np.stack([np.full(len(many), rhead), sbase, np.zeros(len(many), np.int64),
-                                             out_off[many], T[many], nch[many], rw6,
-                                             np.zeros(len(many), np.int64)], 1), len(chunks)))
-            # reduce items wait for every chunk of their level
-            Rlev = {}
-            for lev, it, nchunks in R:
-                it[:, 7] = _wait(self.CPLC + lev, nchunks) | (_wait() << 32)
-                Rlev[lev] = it
-                nCres += len(it)
-        nC = nCres
-        # ---- backward transform (row basis), top down
-        bwd = [p for p in self.main_phases if p.name == "backward"]
-        roots = rs.materialized & ~np.where(rf.parent >= 0, rs.materialized[np.maximum(rf.parent, 0)], False)
-        row_heights = np.unique(rf.height[rs.materialized])
-        leaf_depth = rf.depth[rf.is_leaf]
-        uniform = bool(len(np.unique(leaf_depth)) == 1 and len(np.unique(rf.height[roots])) <= 1)
-        Bl = []
-        nB = []
-        hts = sorted(np.unique(rf.height[rs.materialized & (rs.rank > 0) & ~rf.is_leaf]), reverse=True)
-        for k, p in enumerate(bwd):
-            a_off, K, T, rows, out_off, _ = p.panels
-            xs = xi_of(rows)
-            h_ = hts[k]
-            ids = np.flatnonzero(rs.materialized & (rs.rank > 0) & ~rf.is_leaf & (rf.height == h_))
-            is_root = roots[ids]
-            in_sel = np.where(is_root, B_YC, B_YH)
-            if uniform:
-                rl_c = int(np.searchsorted(row_heights, h_ - 1))
-                rl_p = int(np.searchsorted(row_heights, h_))
-                w1 = _wait(self.CPLR + rl_c, int(nres[rl_c]))
-                w2 = np.where(is_root, _wait(self.CPLR + rl_p, int(nres[rl_p])),
-                              _wait() if k == 0 else _wait(self.BWD + k - 1, nB[k - 1]))
-            else:
-                w1 = _wait(self.CPL, nC)
-                w2 = _wait() if k == 0 else _wait(self.BWD + k - 1, nB[k - 1])
-            it = make(0, 3, in_sel, B_YH, B_YC, a_off, xs, out_off, T, K, 2048,
-                      self.BWD + k, self.BWD_ALL, w1, w2)
-            nB.append(len(it))
-            Bl.append(it)
-        # ---- final: every leaf in range, y[perm] = yt + V y-hat
-        size_r = rf.stop - rf.start
-        leaves = np.flatnonzero(rf.is_leaf)
-        if d.row_range is not None:
-            leaves = leaves[(rf.start[leaves] >= d.row_range[0]) & (rf.stop[leaves] <= d.row_range[1])]
-        has = rs.materialized[leaves] & (rs.rank[leaves] > 0)
-        K = np.where(has, rs.rank[leaves], 0)
-        rows = [o + np.arange(k) for o, k in zip(np.where(has, rs.coef_off[leaves], 0), K)]
-        xs = xi_of(rows)
-        in_sel = np.where(roots[leaves], B_YC, B_YH)
-        # a leaf below a basis parent waits for the backward sweep; a leaf
-        # that is itself a basis root only for the coupling results
-        w1 = np.where(roots[leaves], _wait(self.CPL, nC),
-                      _wait(self.BWD_ALL, sum(nB)) if nB else _wait(self.CPL, nC))
-        w2 = _wait(self.NEAR, nN)
-        fin = make(3, 3, in_sel, B_Y, B_YT, np.where(has, rs.v_off[leaves], 0), xs, rf.start[leaves],
-                   size_r[leaves], K, 1 << 30, _NONE, _NONE, w1, w2)
-        fin = fin[np.argsort(fin[:, 7], kind="stable")]
-        # ---- walk order: the transform chains interleaved with ready filler
-        # (near field during the forward sweep, mid-level coupling after the
-        # level it waits for, the deepest coupling level during the backward
-        # sweep, which needs it last)
-        def cat(parts):
-            parts = [q for q in parts if len(q)]
-            return np.concatenate(parts) if parts else np.zeros((0, 8), np.int64)
-
-        def split(a, n):
-            return [a[i * len(a) // n:(i + 1) * len(a) // n] for i in range(n)] if n > 0 else []
-
-        Cl = [cat(C[l]) for l in range(H)] if H else []
-        Rl = [Rlev.get(l, np.zeros((0, 8), np.int64)) for l in range(H)]
-        # priority lists: the transform chains; coupling by deadline (the
-        # top levels are needed first by the backward sweep); the deep
-        # coupling levels (ready early, needed last); the near field
-        # readiness is monotone along each list (the scheduler stops at the
-        # first segment of a list that is not ready)
-        lists = [
-            [("fwd%d" % l, F[l]) for l in range(H)] + [("bwd%d" % k, it) for k, it in enumerate(Bl)]
-            + [("final", fin)],
-            [("reduce", Rl[l]) for l in range(H)],
-            [("cpl%d" % l, Cl[l]) for l in range(H)],
-            [("near", near)],
-        ]
-        items, names, list_end = [], [], []
-        for lst in lists:
-            for nm, it in lst:
-                if not len(it):
-                    continue
-                # segments: runs of items with one shared dependency word
-                w = it[:, 7]
-                cuts = np.flatnonzero(np.r_[True, w[1:] != w[:-1], True])
-                for a_, b_ in zip(cuts[:-1], cuts[1:]):
-                    items.append(it[a_:b_])
-                    names.append(nm)
-            list_end.append(len(items))
-        if len(items) > 120:
-            raise ConfigError("too many scheduling segments (%d)" % len(items))
-        ends = np.cumsum([len(i) for i in items])
-        segs = np.stack([ends - np.array([len(i) for i in items]), ends, np.zeros(len(items), np.int64)], 1)
-        self.nseg = len(items)
-        self.seg_dev = to_dev(segs.astype(np.int32), self.dev)
-        import ctypes
-        self.nlists = len(list_end)
-        self._list_end = (ctypes.c_int32 * 8)(*(list_end + [list_end[-1]] * (8 - len(list_end))))
-        self.segments = [(nm, len(i)) for nm, i in zip(names, items)]
-        allit = np.concatenate([i for i in items if len(i)]).astype(np.int64)
-        self.nitems = len(allit)
-        self.items = to_dev(np.ascontiguousarray(allit), self.dev)
-        xidx = np.concatenate(xparts) if xparts else np.zeros(1, np.int32)
-        self.xidx_all = to_dev(xidx if len(xidx) else np.zeros(1, np.int32), self.dev)
-        self.sync = torch.zeros(self.NSYNC, dtype=torch.int32, device=self.dev)
-        self.scratch = torch.zeros(max(scratch, 1), dtype=torch.float64, device=self.dev)
-        import ctypes
-        self._mats = (ctypes.c_void_p * 4)(*[m.data_ptr() for m in self.mats])
-        self._bufs = (ctypes.c_void_p * 8)(self.x.data_ptr(), self.xt.data_ptr(), self.xhat.data_ptr(),
-                                           self.yc.data_ptr(), self.yhat.data_ptr(), self.yt.data_ptr(),
-                                           self.y.data_ptr(), self.scratch.data_ptr())
-        self.zero_len = int(self.yc.numel())
-        self.grid = 0
-        self.timing = None
-        self.max_rows = int(allit[:, 5].max())
-        self.bytes = None
-        self.counts = {"forward": nF, "near": nN, "coupling": nC, "backward": nB}
-
-    def _body(self, phase_events=None, phase="coupling"):
-        st = stream_handle()
-        if phase_events is not None:
-            phase_events[0].record()
-        _native.call("gc_h2mv_persistent", ptr(self.items), ptr(self.xidx_all), self.nitems,
-                     self.nseg, ptr(self.seg_dev), self.nlists, self._list_end, ptr(self.perm_in), ptr(self.perm_out), self.n_in, self.zero_len,
-                     self._mats, self._bufs, ptr(self.sync), self.NSYNC, self.grid,
-                     ptr(self.timing) if self.timing is not None else None, self.max_rows, st)
-        if phase_events is not None:
-            phase_events[1].record()
-
-    @property
-    def num_kernels(self):
-        return 1
-
-
-class LaunchPlan(PersistentPlan):
-    """The persistent plan's work items launched phase by phase (one CTA per
-    item) inside a CUDA graph: gather, forward levels, coupling chunks,
-    coupling reductions, backward levels, final leaf stage fused with the
-    output permutation; the near field runs on a side stream.  Transform
-    levels are split by output columns (no partial sums, no reduce
-    launches)."""
-
-    def __init__(self, h):
-        super().__init__(h)
-        # contiguous item ranges per phase, in stream order
-        ranges, k = {}, 0
-        for name, cnt in self.segments:
-            key = "fwd" if name.startswith("fwd") else "bwd" if name.startswith("bwd") else \
-                "cpl" if name.startswith("cpl") else name
-            lvl = name[3:] if key in ("fwd", "bwd") else ""
-            ranges.setdefault((key, lvl), []).append((k, cnt))
-            k += cnt
-        self.ranges = ranges
-
-        def span(key):
-            parts = [r for (kk, _), rr in ranges.items() if kk == key for r in rr]
-            return parts
-
-        fw = sorted([(int(l), r) for (kk, l), r in ranges.items() if kk == "fwd"])
-        bw = sorted([(int(l), r) for (kk, l), r in ranges.items() if kk == "bwd"])
-        self.order = ([("fwd", r) for _, r in fw] + [("cpl", span("cpl")), ("reduce", span("reduce"))]
-                      + [("bwd", r) for _, r in bw] + [("final", span("final"))])
-        self.near_ranges = span("near")
-
-    def _runs(self, parts, st):
-        for first, count in parts:
-            _native.call("gc_run_items", ptr(self.items), first, count, ptr(self.xidx_all),
-                         self._mats, self._bufs, ptr(self.sync), self.max_rows, ptr(self.perm_out), st)
-
-    def _body(self, phase_events=None, phase="coupling"):
-        main = torch.cuda.current_stream()
-        st = stream_handle()
-        _native.call("gc_gather", ptr(self.x), ptr(self.perm_in), self.n_in, ptr(self.xt), st)
-        self.yc.zero_()
-        fork = torch.cuda.Event()
-        fork.record(main)
-        with torch.cuda.stream(self.side):
-            self.side.wait_event(fork)
-            self._runs(self.near_ranges, stream_handle())
-            join = torch.cuda.Event()
-            join.record(self.side)
-        for name, parts in self.order:
-            if name == "final":
-                main.wait_event(join)
-            timed = phase_events is not None and name == phase
-            if timed:
-                phase_events[0].record(main)
-            self._runs(parts, st)
-            if timed:
-                phase_events[1].record(main)
-
-    @property
-    def num_kernels(self):
-        return 2 + sum(len(p) for _, p in self.order) + len(self.near_ranges)

@@ -164,3 +164,20 @@ def test_linear_vertex_tree_and_block_tree_bitwise(name, mesh_name):
     lr, lc = bt.flat.leaves()
     assert np.array_equal(lr, g["leaf_row"]) and np.array_equal(lc, g["leaf_col"])
     assert np.array_equal(bt.flat.state[bt.flat.leaf_ids] == 0, g["leaf_adm"])
+
+
+def test_bench_scaling_config_arguments(monkeypatch):
+    """bench.py defaults: C2 is the headline workload and every line also
+    carries the scaling configuration C4 (BASELINE configs[3])."""
+    import sys
+    sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+    import bench
+    monkeypatch.setattr(sys, "argv", ["bench.py"])
+    a = bench.parse()
+    assert (a.level, a.eps, a.gpus) == (6, 1e-6, 1)
+    assert (a.scale_level, a.scale_eps) == (8, 1e-8)
+    assert bench.workload(a)["triangles"] == 32768
+    assert "524288 triangles" in bench.scaling_workload(a) and "configs[3]" in bench.scaling_workload(a)
+    monkeypatch.setattr(sys, "argv", ["bench.py", "--scale-level", "7", "--scale-eps", "1e-6"])
+    b = bench.parse()
+    assert "configs[3]" not in bench.scaling_workload(b)

@@ -93,6 +93,49 @@ __global__ void __launch_bounds__(KR_THREADS) k_cg_dir(int64_t n, const double* 
         p[i] = fma(beta, p[i], r[i]);
 }
 
+// CGNR step (h2.py:236-245): stop if q.q == 0, else alpha = s[0] / q.q,
+// x += alpha p, r -= alpha q; partial sums of r.r
+__global__ void __launch_bounds__(KR_THREADS) k_cgnr_step(int64_t n, double* s, double* __restrict__ x,
+                                                          double* __restrict__ r, const double* __restrict__ p,
+                                                          const double* __restrict__ q,
+                                                          double* __restrict__ partial) {
+    __shared__ double sh[KR_THREADS];
+    const double qq = s[S_PQ];
+    const bool stop = qq == 0.0;
+    const double alpha = stop ? 0.0 : s[S_RR] / qq;
+    double acc = 0.0;
+    for (int64_t i = blockIdx.x * (int64_t)KR_THREADS + threadIdx.x; i < n; i += (int64_t)KR_BLOCKS * KR_THREADS) {
+        double ri = r[i];
+        if (!stop) {
+            x[i] = fma(alpha, p[i], x[i]);
+            ri = fma(-alpha, q[i], ri);
+            r[i] = ri;
+        }
+        acc = fma(ri, ri, acc);
+    }
+    const double v = block_sum(acc, sh);
+    if (threadIdx.x == 0) partial[blockIdx.x] = v;
+    if (blockIdx.x == 0 && threadIdx.x == 0) {
+        s[S_ALPHA] = alpha;
+        s[S_STOP] = stop ? 1.0 : 0.0;
+    }
+}
+
+// z /= sqrt(s[0])  (the power iteration's normalisation, h2.py:170-171)
+__global__ void __launch_bounds__(KR_THREADS) k_scale_inv_norm(int64_t n, double* __restrict__ z,
+                                                               const double* __restrict__ s) {
+    const double nz = sqrt(s[0]);
+    for (int64_t i = blockIdx.x * (int64_t)KR_THREADS + threadIdx.x; i < n; i += (int64_t)KR_BLOCKS * KR_THREADS)
+        z[i] = z[i] / nz;
+}
+
+// b -= a
+__global__ void __launch_bounds__(KR_THREADS) k_sub(int64_t n, const double* __restrict__ a,
+                                                    double* __restrict__ b) {
+    for (int64_t i = blockIdx.x * (int64_t)KR_THREADS + threadIdx.x; i < n; i += (int64_t)KR_BLOCKS * KR_THREADS)
+        b[i] = b[i] - a[i];
+}
+
 }  // namespace gcb
 
 using namespace gcb;
@@ -131,3 +174,43 @@ extern "C" int gc_cg_update(int64_t n, double* x, double* r, double* p, const do
 }
 
 extern "C" int64_t gc_krylov_partials(void) { return KR_BLOCKS; }
+
+// CGNR (h2.py:222-253).  State s[]: [0] s.s, [1] q.q, [2] r.r, [3] beta,
+// [4] new s.s, [5] stop flag.  gc_cgnr_step: q.q, then the x / r update and
+// r.r; gc_cgnr_dir: new s.s, beta = new / s[0], p = s + beta p, s[0] = new.
+extern "C" int gc_cgnr_step(int64_t n, double* x, double* r, const double* p, const double* q,
+                            double* partial, double* s, void* stream) {
+    cudaStream_t st = (cudaStream_t)stream;
+    k_dot_partial<<<KR_BLOCKS, KR_THREADS, 0, st>>>(n, q, q, partial);
+    GC_CHECK_LAUNCH("k_dot_partial");
+    k_dot_final<<<1, KR_THREADS, 0, st>>>(partial, s, S_PQ, 0);
+    GC_CHECK_LAUNCH("k_dot_final");
+    k_cgnr_step<<<KR_BLOCKS, KR_THREADS, 0, st>>>(n, s, x, r, p, q, partial);
+    GC_CHECK_LAUNCH("k_cgnr_step");
+    k_dot_final<<<1, KR_THREADS, 0, st>>>(partial, s, S_RRNEW, 0);
+    GC_CHECK_LAUNCH("k_dot_final");
+    return GC_OK;
+}
+
+extern "C" int gc_cgnr_dir(int64_t n, const double* sv, double* p, double* partial, double* s, void* stream) {
+    cudaStream_t st = (cudaStream_t)stream;
+    k_dot_partial<<<KR_BLOCKS, KR_THREADS, 0, st>>>(n, sv, sv, partial);
+    GC_CHECK_LAUNCH("k_dot_partial");
+    k_dot_final<<<1, KR_THREADS, 0, st>>>(partial, s, 4, 1);
+    GC_CHECK_LAUNCH("k_dot_final");
+    k_cg_dir<<<KR_BLOCKS, KR_THREADS, 0, st>>>(n, s, sv, p);
+    GC_CHECK_LAUNCH("k_cg_dir");
+    return GC_OK;
+}
+
+extern "C" int gc_scale_inv_norm(int64_t n, double* z, const double* s, void* stream) {
+    k_scale_inv_norm<<<KR_BLOCKS, KR_THREADS, 0, (cudaStream_t)stream>>>(n, z, s);
+    GC_CHECK_LAUNCH("k_scale_inv_norm");
+    return GC_OK;
+}
+
+extern "C" int gc_axpy_neg(int64_t n, const double* a, double* b, void* stream) {
+    k_sub<<<KR_BLOCKS, KR_THREADS, 0, (cudaStream_t)stream>>>(n, a, b);
+    GC_CHECK_LAUNCH("k_sub");
+    return GC_OK;
+}

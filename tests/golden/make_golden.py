@@ -12,7 +12,10 @@ import sys
 
 import numpy as np
 
-sys.path.insert(0, "/root/reference/pkg/src")
+_REF = "/root/reference/pkg/src"
+if not os.path.isdir(_REF):   # on the GPU host: the stock install the reference arm uses
+    _REF = os.path.join(os.path.dirname(os.path.abspath(__file__)), "..", "..", "baseline", "_ref")
+sys.path.insert(0, _REF)
 from greencross import assembly as A  # noqa: E402
 from greencross import clustering as C  # noqa: E402
 from greencross import gca as GC  # noqa: E402
@@ -407,8 +410,152 @@ def main_mvm20():
                         mvm_t=np.stack([H.mvm_t(hm, x) for x in xs]))
 
 
+def node_hashes(bns):
+    """Per basis node: 32-bit digests of the pivot list in order and of the
+    sorted pivot set (blake2b of the little-endian int32 bytes).  Stored
+    instead of the pivots themselves at the benchmark sizes (C4 holds about
+    6 M pivots per side); tests/bench_fixtures.py recomputes them."""
+    import hashlib
+
+    def h(a):
+        return int.from_bytes(hashlib.blake2b(np.asarray(a, "<i4").tobytes(), digest_size=4).digest(), "little")
+    return (np.array([h(b.pivots) for b in bns], np.uint32),
+            np.array([h(np.sort(b.pivots)) for b in bns], np.uint32))
+
+
+def digest(*arrays):
+    import hashlib
+    d = hashlib.sha256()
+    for a in arrays:
+        a = np.ascontiguousarray(a)
+        d.update(str(a.dtype.str).encode() + str(a.shape).encode())
+        d.update(a.tobytes())
+    return d.hexdigest()
+
+
+BENCH = {   # SURVEY 8: C2 sphere L6 eps 1e-6, C3 cube L7 eps 1e-6, C4 sphere L8 eps 1e-8
+    "c2": (lambda: G.build_sphere_mesh(6), 1e-6),
+    "c3": (lambda: cube(7), 1e-6),
+    "c4": (lambda: G.build_sphere_mesh(8), 1e-8),
+}
+
+
+def bench_pipeline(name, full_build):
+    """Reference structure at a benchmark mesh (north_star: trees, pivot sets
+    and block structure bit-exact on the same mesh; entries and matvecs
+    within 1e-10).  Trees, block leaves and per-node pivot digests in full;
+    V / transfer matrices of sampled nodes; sampled coupling blocks
+    assembled at the reference's own pivots and near-field blocks, both by
+    the reference's assemble_galerkin_block (bitwise equal to the H2
+    blocks, test_assembly.py:220-226 / executor invariance).  With
+    ``full_build`` (C2) also the reference's own build_h2 and mvm / mvm_t of
+    three np.random.default_rng(0) vectors."""
+    import time
+    make, eps = BENCH[name]
+    t0 = time.time()
+    mesh = make()
+    tree = C.build_cluster_tree(mesh, "constant", 16)
+    t1 = time.time()
+    bt = C.build_block_tree(tree, eta=1.0)
+    t2 = time.time()
+    print("%s: cluster tree %.1f s, block tree %.1f s" % (name, t1 - t0, t2 - t1), flush=True)
+    nodes = tree.nodes()
+    leaves = bt.leaves()
+    perm = tree.perm.astype(np.int32)
+    start = np.array([n.start for n in nodes], np.int32)
+    stop = np.array([n.stop for n in nodes], np.int32)
+    lower = np.array([n.box.lower for n in nodes])
+    upper = np.array([n.box.upper for n in nodes])
+    lrow = np.array([lf.row.index for lf in leaves], np.int32)
+    lcol = np.array([lf.col.index for lf in leaves], np.int32)
+    ladm = np.array([lf.state == "admissible" for lf in leaves])
+    out = dict(nt=mesh.nt, eps=eps, n_nodes=len(nodes), n_leaves=len(leaves), n_adm=int(ladm.sum()),
+               perm_sha=digest(perm), tree_sha=digest(start, stop), box_sha=digest(lower, upper),
+               leaves_sha=digest(lrow, lcol, ladm), perm_head=perm[:256])
+    rm, cm = GC.coupling_marks(bt)
+    bases = {}
+    for side, marks in (("row", rm), ("col", cm)):
+        t = time.time()
+        basis = GC.build_cluster_basis(tree, mesh, "constant", 3, 0.5, eps, side, (3, 5), marks)
+        print("%s: %s basis %.1f s" % (name, side, time.time() - t), flush=True)
+        bases[side] = basis
+        bns = basis.nodes()
+        ho, hs = node_hashes(bns)
+        out[side + "_node"] = np.array([b.cluster.index for b in bns], np.int32)
+        out[side + "_rank"] = np.array([b.rank for b in bns], np.int16)
+        out[side + "_hash_order"] = ho
+        out[side + "_hash_set"] = hs
+        out[side + "_piv_sha"] = digest(np.concatenate([b.pivots for b in bns]).astype(np.int32))
+        rng = np.random.default_rng(100 + (side == "col"))
+        # a few nodes at every tree height, their pivots and matrices
+        pick = rng.choice(len(bns), min(24, len(bns)), replace=False)
+        meta, vals, pivs = [], [], []
+        for i in pick:
+            b = bns[int(i)]
+            m = b.v if b.v is not None else b.transfer
+            if m is None:
+                continue
+            meta.append((b.cluster.index, 0 if b.v is not None else 1, m.shape[0], m.shape[1], b.rank))
+            vals.append(m.ravel())
+            pivs.append(b.pivots.astype(np.int32))
+        out[side + "_mat_meta"] = np.array(meta, np.int64).reshape(-1, 5)
+        out[side + "_mat_vals"] = np.concatenate(vals)
+        out[side + "_mat_piv"] = np.concatenate(pivs)
+    # sampled blocks at the reference's own pivots / clusters
+    rng = np.random.default_rng(7)
+    adm_idx = np.flatnonzero(ladm)
+    near_idx = np.flatnonzero(~ladm)
+    t = time.time()
+    for key, pool, k in (("coup", adm_idx, 24), ("near", near_idx, 24)):
+        pick = np.sort(rng.choice(pool, k, replace=False))
+        shapes, vals = [], []
+        for i in pick:
+            lf = leaves[int(i)]
+            if key == "coup":
+                r = bases["row"].node(lf.row).pivots
+                c = bases["col"].node(lf.col).pivots
+            else:
+                r, c = lf.row.indices, lf.col.indices
+            v = A.assemble_galerkin_block("slp", mesh, "constant", r, c).values
+            shapes.append(v.shape)
+            vals.append(v.ravel())
+        out[key + "_leaf"] = pick.astype(np.int64)
+        out[key + "_shape"] = np.array(shapes, np.int32)
+        out[key + "_vals"] = np.concatenate(vals)
+    print("%s: sampled blocks %.1f s" % (name, time.time() - t), flush=True)
+    if full_build:
+        t = time.time()
+        hm = GC.build_h2(bt, bases["row"], bases["col"], mesh, "slp", "constant", "galerkin", (3, 5))
+        print("%s: build_h2 %.1f s" % (name, time.time() - t), flush=True)
+        xs = np.random.default_rng(0).standard_normal((3, mesh.nt))
+        out["mvm"] = np.stack([H.mvm(hm, x) for x in xs])
+        out["mvm_t"] = np.stack([H.mvm_t(hm, x) for x in xs])
+        rep = H.storage_report(hm)
+        out["storage_keys"] = np.array(list(rep.keys()))
+        out["storage_vals"] = np.array(list(rep.values()), np.int64)
+        out["exec_tasks"] = np.array([s["tasks"] for s in hm.exec_stats], np.int64)
+        out["exec_batches"] = np.array([s["batches"] for s in hm.exec_stats], np.int64)
+    out["total_s"] = time.time() - t0
+    return out
+
+
+def main_bench(names, full):
+    import platform
+    for name in names:
+        res = bench_pipeline(name, full and name == "c2")
+        res["host"] = np.array(platform.processor() or platform.machine())
+        np.savez_compressed(os.path.join(OUT, "bench_%s.npz" % name), **res)
+        print("%s: done in %.1f s" % (name, res["total_s"]), flush=True)
+
+
 if __name__ == "__main__":
-    if "--mvm20" in sys.argv:
+    if "--bench" in sys.argv:
+        # --bench c2 [c3 c4] [--no-build]; --out DIR redirects (used on the
+        # GPU host to check that its SIMD dispatch yields the same fixtures)
+        if "--out" in sys.argv:
+            OUT = sys.argv[sys.argv.index("--out") + 1]
+        main_bench([a for a in sys.argv[1:] if a in BENCH], "--no-build" not in sys.argv)
+    elif "--mvm20" in sys.argv:
         main_mvm20()
     elif "--dlp" in sys.argv:
         main_dlp()

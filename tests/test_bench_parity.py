@@ -1,0 +1,242 @@
+"""Parity with the reference at the BENCHMARK meshes (north_star: "cluster
+trees, pivot sets and block structure bit-exact ... matrix entries and
+matvec results within 1e-10 relative"; SURVEY 8c parity protocol).
+
+Fixtures: tests/golden/bench_{c2,c3,c4}.npz, made by greencross itself
+(``tests/golden/make_golden.py --bench c2 c3 c4``): C2 sphere L6 eps 1e-6,
+C3 cube L7 eps 1e-6, C4 sphere L8 eps 1e-8 with the CLI defaults.  Trees
+and block leaves are stored as sha256 digests, the bases as per-node
+32-bit digests of the pivot list (in order) and of the sorted pivot set,
+plus ranks; V / transfer matrices and coupling / near-field blocks of
+sampled nodes and leaves (the blocks assembled by the reference's
+``assemble_galerkin_block`` at the reference's own pivots / clusters);
+at C2 also the reference's own ``build_h2`` products ``mvm`` / ``mvm_t``
+of three ``default_rng(0)`` vectors, storage report and task counts.
+
+CPU tests pin the host-built trees and block trees; ``-m gpu`` tests pin
+the device pipeline (device cluster tree, bases, blocks, matvec)."""
+
+import hashlib
+
+import numpy as np
+import pytest
+
+from conftest import golden
+
+CONFIGS = {"c2": ("sphere", 6, 1e-6), "c3": ("cube", 7, 1e-6), "c4": ("sphere", 8, 1e-8)}
+
+
+def digest(*arrays):
+    d = hashlib.sha256()
+    for a in arrays:
+        a = np.ascontiguousarray(a)
+        d.update(str(a.dtype.str).encode() + str(a.shape).encode())
+        d.update(a.tobytes())
+    return d.hexdigest()
+
+
+def h32(a):
+    return int.from_bytes(hashlib.blake2b(np.asarray(a, "<i4").tobytes(), digest_size=4).digest(), "little")
+
+
+def mesh_of(cfg):
+    from paper_1810_08429_b200 import geometry
+    kind, level, _ = CONFIGS[cfg]
+    return geometry.build_sphere_mesh(level) if kind == "sphere" else geometry.build_cube_mesh(level)
+
+
+def tree_digests(tree):
+    f = tree.flat
+    return dict(perm_sha=digest(np.asarray(f.perm, np.int32)),
+                tree_sha=digest(np.asarray(f.start, np.int32), np.asarray(f.stop, np.int32)),
+                box_sha=digest(np.asarray(f.lower, np.float64), np.asarray(f.upper, np.float64)))
+
+
+def leaf_digest(bt):
+    fb = bt.flat
+    ids = fb.leaf_ids
+    return digest(np.asarray(fb.row[ids], np.int32), np.asarray(fb.col[ids], np.int32),
+                  np.asarray(fb.state[ids] == 0))
+
+
+@pytest.mark.parametrize("cfg", ["c2", "c3", "c4"])
+def test_host_trees_match_reference(cfg):
+    """Host-built cluster tree (perm, preorder start/stop, boxes) and block
+    tree (leaves in DFS order with their states) == the reference's, bit
+    for bit, at the benchmark meshes."""
+    from paper_1810_08429_b200 import clustering
+    g = golden("bench_%s.npz" % cfg)
+    mesh = mesh_of(cfg)
+    assert mesh.nt == int(g["nt"])
+    tree = clustering.build_cluster_tree(mesh, "constant", 16)
+    bt = clustering.build_block_tree(tree, eta=1.0)
+    d = tree_digests(tree)
+    assert np.array_equal(np.asarray(tree.flat.perm[:256], np.int32), g["perm_head"])
+    for k in ("perm_sha", "tree_sha", "box_sha"):
+        assert d[k] == str(g[k]), k
+    assert len(tree.flat) == int(g["n_nodes"])
+    assert len(bt.flat.leaf_ids) == int(g["n_leaves"])
+    assert int((bt.flat.state[bt.flat.leaf_ids] == 0).sum()) == int(g["n_adm"])
+    assert leaf_digest(bt) == str(g["leaves_sha"])
+
+
+def test_fixtures_are_self_consistent():
+    """The stored per-node digests agree with the stored sampled pivots."""
+    for cfg in CONFIGS:
+        g = golden("bench_%s.npz" % cfg)
+        for side in ("row", "col"):
+            nodes = list(g[side + "_node"])
+            off = 0
+            for idx, kind, r, c, rank in g[side + "_mat_meta"]:
+                piv = g[side + "_mat_piv"][off:off + rank]
+                off += rank
+                j = nodes.index(idx)
+                assert h32(piv) == int(g[side + "_hash_order"][j])
+                assert h32(np.sort(piv)) == int(g[side + "_hash_set"][j])
+                assert int(g[side + "_rank"][j]) == rank
+
+
+# --------------------------------------------------------------------------
+# device pipeline (GPU)
+
+_BUILT = {}
+
+
+def built(cfg):
+    """The device GCA-H2 operator of a benchmark configuration (cached per
+    module run: C4 takes ~2 s to assemble)."""
+    if cfg not in _BUILT:
+        from paper_1810_08429_b200 import cli
+        _BUILT.clear()
+        mesh = mesh_of(cfg)
+        hm, tree, bt = cli.build_h2_operator(mesh, cli.default_config(eps=CONFIGS[cfg][2]))
+        _BUILT[cfg] = (mesh, hm, tree, bt)
+    return _BUILT[cfg]
+
+
+def _order_map(mine, ref):
+    """Index array k such that mine[k] == ref (same sets)."""
+    pos = {int(p): i for i, p in enumerate(mine)}
+    return np.array([pos[int(p)] for p in ref], np.int64)
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("cfg", ["c2", "c3", "c4"])
+def test_structure_matches_reference(cfg):
+    """Device pipeline at a benchmark mesh: cluster tree (built on the
+    device), block tree, basis node lists and ranks bit-exact; pivot SETS
+    bit-exact at every node; pivot ORDER bit-exact except at ulp-level
+    ties of |R| (numpy's SIMD r**3), counted and
+    bounded at 0.5 % of the nodes; sampled V / transfer matrices within
+    1e-10 relative (columns matched by pivot)."""
+    g = golden("bench_%s.npz" % cfg)
+    mesh, hm, tree, bt = built(cfg)
+    d = tree_digests(tree)
+    for k in ("perm_sha", "tree_sha", "box_sha"):
+        assert d[k] == str(g[k]), k
+    assert leaf_digest(bt) == str(g["leaves_sha"])
+    report = {}
+    for side, basis in (("row", hm.row_basis), ("col", hm.col_basis)):
+        nodes = basis.nodes()
+        assert np.array_equal(np.array([b.cluster.index for b in nodes], np.int32), g[side + "_node"])
+        assert np.array_equal(np.array([b.rank for b in nodes], np.int16), g[side + "_rank"])
+        hs = np.array([h32(np.sort(b.pivots)) for b in nodes], np.uint32)
+        ho = np.array([h32(b.pivots) for b in nodes], np.uint32)
+        bad_set = np.flatnonzero(hs != g[side + "_hash_set"])
+        assert bad_set.size == 0, "pivot sets differ at %d nodes (first %s)" % (
+            bad_set.size, [nodes[i].cluster.index for i in bad_set[:5]])
+        n_order = int((ho != g[side + "_hash_order"]).sum())
+        report[side] = n_order
+        assert n_order <= max(1, len(nodes) // 200), (side, n_order, len(nodes))
+        # sampled V (leaf) / transfer matrices, columns (and transfer rows)
+        # matched by pivot identity
+        by = {b.cluster.index: b for b in nodes}
+        off = voff = 0
+        for idx, kind, r, c, rank in g[side + "_mat_meta"]:
+            ref_piv = g[side + "_mat_piv"][off:off + rank]
+            ref = g[side + "_mat_vals"][voff:voff + r * c].reshape(r, c)
+            off, voff = off + rank, voff + r * c
+            b = by[int(idx)]
+            m = b.v if kind == 0 else b.transfer
+            assert m.shape == ref.shape
+            if kind == 0:                       # leaf V: rows = cluster dofs, cols = own pivots
+                m = m[:, _order_map(b.pivots, ref_piv)]
+            else:                               # transfer: rows = own pivots, cols = parent pivots
+                m = m[_order_map(b.pivots, ref_piv)]
+                if not np.array_equal(by[int(b.cluster.flat.parent[b.cluster.index])].pivots,
+                                      _parent_ref_pivots(g, side, b)):
+                    continue                    # parent took a tied pivot in the other order
+            assert np.linalg.norm(m - ref) <= 1e-10 * max(np.linalg.norm(ref), 1.0), (side, idx)
+    print("%s: pivot order differs at %d row / %d col nodes (sets identical)" % (cfg, report["row"], report["col"]))
+
+
+def _parent_ref_pivots(g, side, b):
+    """The reference pivot list of b's parent if the fixture sampled it,
+    else b's parent's own pivots (order assumed equal: the digest check
+    above bounds the exceptions)."""
+    p = int(b.cluster.flat.parent[b.cluster.index])
+    off = 0
+    for idx, kind, r, c, rank in g[side + "_mat_meta"]:
+        if int(idx) == p:
+            return g[side + "_mat_piv"][off:off + rank]
+        off += rank
+    return None if p < 0 else _own_pivots(b, p)
+
+
+def _own_pivots(b, p):
+    return b._store.pivots_host[b._store.piv_off[p]:b._store.piv_off[p] + b._store.rank[p]]
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("cfg", ["c2", "c3", "c4"])
+def test_block_samples_match_reference(cfg):
+    """Sampled coupling blocks (entries at the reference's pivot rows x
+    pivot columns, rows / columns matched by pivot identity) and near-field
+    blocks within 1e-12 relative of the reference's own assembly."""
+    g = golden("bench_%s.npz" % cfg)
+    mesh, hm, tree, bt = built(cfg)
+    fb = bt.flat
+    leaf_ids = fb.leaf_ids
+    adm = fb.state[leaf_ids] == 0
+    # position of each leaf inside hm.coupling / hm.nearfield (DFS order)
+    pos_c = np.cumsum(adm) - 1
+    pos_n = np.cumsum(~adm) - 1
+    # nodes whose pivot ORDER equals the reference's (all but ulp ties)
+    same = {}
+    for side, basis in (("row", hm.row_basis), ("col", hm.col_basis)):
+        ref_h = dict(zip(g[side + "_node"].tolist(), g[side + "_hash_order"].tolist()))
+        same[side] = {b.cluster.index: h32(b.pivots) == ref_h[b.cluster.index] for b in basis.nodes()}
+    skipped = 0
+    for key, blocks, pos in (("coup", hm.coupling, pos_c), ("near", hm.nearfield, pos_n)):
+        off = 0
+        for leaf, shp in zip(g[key + "_leaf"], g[key + "_shape"]):
+            n = int(np.prod(shp))
+            ref = g[key + "_vals"][off:off + n].reshape(shp)
+            off += n
+            blk = blocks[int(pos[int(leaf)])]
+            v = blk.values
+            assert v.shape == tuple(shp)
+            if key == "coup" and not (same["row"][blk.row.index] and same["col"][blk.col.index]):
+                skipped += 1                     # tied pivots taken in the other order
+                continue
+            assert np.max(np.abs(v - ref)) <= 1e-12 * np.max(np.abs(ref)), (cfg, key, leaf)
+    assert skipped <= 2
+
+
+@pytest.mark.gpu
+def test_matvec_matches_reference_c2():
+    """C2: the device product (h2.mvm / h2.mvm_t, external ordering) of the
+    reference's three default_rng(0) vectors against the reference's own
+    build_h2 + mvm; north_star bar 1e-10, held to 1e-12.  Storage report and
+    per-case task counts equal the reference's."""
+    from paper_1810_08429_b200 import h2
+    g = golden("bench_c2.npz")
+    mesh, hm, tree, bt = built("c2")
+    xs = np.random.default_rng(0).standard_normal((3, mesh.nt))
+    for x, y, yt in zip(xs, g["mvm"], g["mvm_t"]):
+        assert np.linalg.norm(h2.mvm(hm, x) - y) <= 1e-12 * np.linalg.norm(y)
+        assert np.linalg.norm(h2.mvm_t(hm, x) - yt) <= 1e-12 * np.linalg.norm(yt)
+    rep = h2.storage_report(hm)
+    assert {k: rep[k] for k in g["storage_keys"]} == dict(zip(g["storage_keys"].tolist(),
+                                                              g["storage_vals"].tolist()))
+    assert [s["tasks"] for s in hm.exec_stats] == g["exec_tasks"].tolist()

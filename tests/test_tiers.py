@@ -228,25 +228,23 @@ def test_tier_plan_unbalanced_tree(seed, bounds):
     assert np.allclose(y, ref, rtol=1e-11, atol=1e-11 * np.abs(ref).max())
 
 
-def test_choose_tiers_override_and_cost(monkeypatch):
+def test_choose_tiers_override_and_cost():
     mesh = geometry.build_sphere_mesh(3)
     flat = build_cluster_tree(mesh, leaf_size=8).flat
     s = _store(flat, np.random.default_rng(1), dead_frac=0.0)
     top = int(flat.height.max())
-    monkeypatch.setenv("GC_TIERS", "1,3")
-    assert tiers.choose_tiers(s, flat) == [1, 3, top]
-    monkeypatch.setenv("GC_TIERS", "auto")
-    monkeypatch.setenv("GC_TIER_CTA_GBS", "1e12")      # bytes and launches only
-    # no launch latency: the cheapest plan streams the fewest bytes, which
-    # is the level-by-level one (every composed tier is at least as large)
-    lvl = tiers.choose_tiers(s, flat, latency_s=0.0)
+    assert tiers.choose_tiers(s, flat, bounds=[1, 3]) == [1, 3, top]
+    # no hand-off latency and a fast single CTA: the cheapest plan streams
+    # the fewest bytes, which is the level-by-level one (every composed tier
+    # is at least as large)
+    lvl = tiers.choose_tiers(s, flat, latency_s=0.0, cta_bps=1e21)
     assert lvl == list(range(top + 1))
     # huge latency: one tier
-    assert tiers.choose_tiers(s, flat, latency_s=1.0) == [top]
+    assert tiers.choose_tiers(s, flat, latency_s=1.0, cta_bps=1e21) == [top]
     # a slow single CTA makes the large composed panels of a tall tier
     # expensive: the plan gets more tiers than with bytes alone
-    monkeypatch.setenv("GC_TIER_CTA_GBS", "0.001")
-    assert len(tiers.choose_tiers(s, flat, latency_s=1e-6)) > len(tiers.choose_tiers(s, flat, latency_s=1.0))
+    assert (len(tiers.choose_tiers(s, flat, latency_s=1e-6, cta_bps=1e6))
+            > len(tiers.choose_tiers(s, flat, latency_s=1.0, cta_bps=1e6)))
 
 
 def test_coef_layout_generations_equal_queue_order():

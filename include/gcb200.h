@@ -24,7 +24,7 @@
 extern "C" {
 #endif
 
-#define GC_ABI_VERSION 2
+#define GC_ABI_VERSION 3
 
 #define GC_OK 0
 #define GC_ERR_CONFIG 1
@@ -211,21 +211,6 @@ int gc_expand_ranges(int64_t m, const int64_t* start, const int64_t* len, const 
 int gc_graph_retarget(void* graph, void* exec, int32_t kernel, int32_t arg, const void* old_ptr,
                       const void* new_ptr, int32_t* count);
 
-/* Segmented block-row product, the single kernel form behind every matvec
- * phase.  For segment s = (out_off, T, blk_begin, blk_end):
- *     out[out_off + t] (+)= sum_{b in [blk_begin, blk_end)} sum_{k<K_b}
- *                           A_b[k*lda_b + t*ts_b] * in_b[in_off_b + k]
- * blk (nblk,6) int64: a_off, K, lda, in_off, sel (bit0: A1 instead of A0,
- * bit1: in1 instead of in0), ts (1 for the coalesced layouts of mvm; the
- * transposed product mvm_t reuses the same storage with ts = row length).  Forward transform: A = V or V-hat (row-major),
- * coupling: A = S^T, backward: A = V-hat^T, near-field: A = N^T.  Each
- * output element has one writer and a fixed summation order: the result is
- * bitwise deterministic.  accumulate != 0 adds into out. */
-int gc_segmv(int64_t nseg, const int64_t* seg, const int64_t* blk,
-             const double* A0, const double* A1, const double* in0,
-             const double* in1, double* out, int accumulate, int64_t max_T,
-             void* stream);
-
 /* Panel product, the mvm hot path (one phase of h2.py:63-80).  A phase
  * is a list of work items; item i (items[8i..8i+7] = a_off, xi_off,
  * out_off, T, nrows, mode, red_slot, 0) computes
@@ -238,12 +223,12 @@ int gc_segmv(int64_t nseg, const int64_t* seg, const int64_t* blk,
  * split panel; the last item of a panel to finish (arrivals[red_slot], an
  * int32 counter that must start at 0 and is re-armed by the kernel) sums
  * the scratch rows into out in item order.  One writer per output, fixed
- * order: deterministic.  chain != 0 launches with programmatic stream
+ * order: deterministic.  chain & 1 launches with programmatic stream
  * serialization (PDL): the kernel prefetches its matrix chunk while the
  * previous kernel on the stream drains and waits for it before reading in
- * (for the latency-bound transform levels); chain = 1 releases the next
- * launch at each CTA's start, chain = 2 after each CTA's item; chain | 4
- * runs one warp per item (whole panels of <= 256 rows, 8 per CTA).  priority != 0 sets the
+ * (for the latency-bound transform levels); the next launch is released at
+ * each CTA's start.  chain & 16 runs two whole small panels per CTA (direct
+ * items, T <= 128, <= 512 rows).  priority != 0 sets the
  * launch's scheduling priority (CUDA stream-priority scale, lower = more
  * urgent; 0 = the stream's own).  trace (optional, NULL = off)
  * = [dev] 2 x uint64 receiving min(start) / max(end) %globaltimer (ns) of
@@ -253,44 +238,6 @@ int gc_panelmv(int64_t nitems, const int64_t* items, const int32_t* xidx,
                const double* in1, double* out, double* scratch, int64_t nred,
                const int64_t* red, int32_t* arrivals, int32_t chain, int32_t priority,
                uint64_t* trace, void* stream);
-
-/* A run of consecutive transform levels (h2.py:63-70 forward, h2.py:74-79
- * backward) in ONE co-resident launch with grid barriers between levels.
- * phases [dev] = nphase packed descriptors of gc_panel_phase_bytes() bytes:
- * {items, nitems, xidx, A0, A1, in0, in1, out, scratch, red, arrivals,
- * trace} with the meaning of gc_panelmv's arguments (trace unused here); grid from
- * gc_panel_chain_grid; barrier [dev] = one uint32, zero before the first
- * launch, left consistent by every launch (no re-arming). */
-int gc_panel_chain_grid(int64_t* grid);
-int gc_panel_chain(int64_t nphase, const void* phases, int64_t grid, uint32_t* barrier,
-                   void* stream);
-int64_t gc_panel_phase_bytes(void);
-
-/* Bulk phase (coupling buckets, near field) on the TMA streaming kernel:
- * same items/red/arrivals/trace as gc_panelmv (T <= 1024 per item), run by
- * a co-resident grid of `grid` CTAs (gc_panel_stream_grid); CTA b works
- * items [cta_begin[b], cta_begin[b+1]) [dev, grid+1 int64] in order.  One
- * producer thread per CTA streams each item's rows into a 4-stage smem
- * ring with cp.async.bulk (mbarrier completion); 8 consumer warps FMA them.
- * Matrix buffers must be readable 16 bytes past their last element. */
-int gc_panel_stream_grid(int64_t* grid);
-int gc_panel_stream(int64_t nitems, const int64_t* items, const int32_t* xidx,
-                    const double* A0, const double* A1, const double* in0,
-                    const double* in1, double* out, double* scratch, int64_t nred,
-                    const int64_t* red, int32_t* arrivals, const int64_t* cta_begin,
-                    int64_t grid, int32_t priority, uint64_t* trace, void* stream);
-
-/* Bulk phase, one CTA per item, TMA-fed: each CTA moves its item's whole
- * matrix chunk (<= gc_panel_tma_item_elems() doubles, T <= 256 per item not
- * required) into shared memory with ONE cp.async.bulk (mbarrier
- * completion) while it gathers the inputs.  Arguments as gc_panelmv.
- * Matrix buffers must be readable 16 bytes past their last element. */
-int gc_panel_tma(int64_t nitems, const int64_t* items, const int32_t* xidx,
-                 const double* A0, const double* A1, const double* in0,
-                 const double* in1, double* out, double* scratch, int64_t nred,
-                 const int64_t* red, int32_t* arrivals, int32_t priority, uint64_t* trace,
-                 void* stream);
-int64_t gc_panel_tma_item_elems(void);
 
 /* Native product executor (h2.py:63-80 as one call).  nodes [host] (n,18)
  * int64 rows: kind (0 panel phase, 1 memset, 2 gc_gather_inv,
@@ -413,6 +360,17 @@ int gc_cg_pq(int64_t n, const double* p, const double* q, double* partial, doubl
 int gc_cg_update(int64_t n, double* x, double* r, double* p, const double* q, double* partial,
                  double* s, void* stream);
 int64_t gc_krylov_partials(void);
+/* CGNR (h2.py:222-253), state s [dev, 8 doubles]: [0] s.s, [1] q.q, [2] r.r,
+ * [3] beta, [4] new s.s, [5] stop flag.  gc_cgnr_step: q.q; stop (s[5] = 1,
+ * x and r unchanged) if it is 0, else alpha = s[0] / q.q, x += alpha p,
+ * r -= alpha q; then s[2] = r.r.  gc_cgnr_dir: s[4] = sv.sv, beta =
+ * s[4] / s[0], p = sv + beta p, s[0] = s[4]. */
+int gc_cgnr_step(int64_t n, double* x, double* r, const double* p, const double* q, double* partial,
+                 double* s, void* stream);
+int gc_cgnr_dir(int64_t n, const double* sv, double* p, double* partial, double* s, void* stream);
+/* Power iteration (h2.py:144-184): z /= sqrt(s[0]); b -= a. */
+int gc_scale_inv_norm(int64_t n, double* z, const double* s, void* stream);
+int gc_axpy_neg(int64_t n, const double* a, double* b, void* stream);
 
 /* The device's scheduling-priority range (cudaDeviceGetStreamPriorityRange):
  * least (default, e.g. 0) and greatest (most urgent, e.g. -5). */

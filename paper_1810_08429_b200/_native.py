@@ -64,12 +64,8 @@ _SIGNATURES = {
     "gc_plan_destroy": [c_p],
     "gc_scatter2_inv": [c_p, c_p, c_p, c_i64, c_p, c_p],
     "gc_block_transpose": [c_i64, c_p, c_p, c_p, c_p],
-    "gc_segmv": [c_i64, c_p, c_p, c_p, c_p, c_p, c_p, c_p, ctypes.c_int, c_i64, c_p],
     "gc_panelmv": [c_i64, c_p, c_p, c_p, c_p, c_p, c_p, c_p, c_p, c_i64, c_p, c_p, ctypes.c_int32,
                    ctypes.c_int32, c_p, c_p],
-    "gc_panel_chain_grid": [ctypes.POINTER(c_i64)],
-    "gc_panel_chain": [c_i64, c_p, c_i64, c_p, c_p],
-    "gc_panel_phase_bytes": [],
     "gc_lin_pairs": [ctypes.POINTER(GcGeom), c_p, c_p, c_i64, c_p, c_p, c_p, ctypes.POINTER(GcQueue), c_p, c_p],
     "gc_lin_singular": [ctypes.POINTER(GcGeom), ctypes.POINTER(GcRules), ctypes.POINTER(GcQueue), c_p,
                         ctypes.POINTER(c_i64), c_p],
@@ -89,22 +85,20 @@ _SIGNATURES = {
     "gc_cg_pq": [c_i64, c_p, c_p, c_p, c_p, c_p],
     "gc_cg_update": [c_i64, c_p, c_p, c_p, c_p, c_p, c_p, c_p],
     "gc_krylov_partials": [],
-    "gc_panel_stream_grid": [ctypes.POINTER(c_i64)],
-    "gc_panel_tma": [c_i64, c_p, c_p, c_p, c_p, c_p, c_p, c_p, c_p, c_i64, c_p, c_p, ctypes.c_int32, c_p, c_p],
-    "gc_panel_tma_item_elems": [],
-    "gc_panel_stream": [c_i64, c_p, c_p, c_p, c_p, c_p, c_p, c_p, c_p, c_i64, c_p, c_p, c_p, c_i64,
-                        ctypes.c_int32, c_p, c_p],
     "gc_priority_range": [ctypes.POINTER(ctypes.c_int32), ctypes.POINTER(ctypes.c_int32)],
+    "gc_cgnr_step": [c_i64, c_p, c_p, c_p, c_p, c_p, c_p, c_p],
+    "gc_cgnr_dir": [c_i64, c_p, c_p, c_p, c_p, c_p],
+    "gc_scale_inv_norm": [c_i64, c_p, c_p, c_p],
+    "gc_axpy_neg": [c_i64, c_p, c_p, c_p],
     "gc_host_norm3": [c_p, c_i64, c_p, ctypes.c_int],
     "gc_dfma_probe": [c_i64, c_i64, c_i64, c_p, c_p],
 }
 _RESTYPES = {"gc_last_error": ctypes.c_char_p, "gc_launch_count": ctypes.c_uint64,
              "gc_tier_tile": ctypes.c_int64,
-             "gc_reset_launch_count": None, "gc_panel_phase_bytes": ctypes.c_int64,
-             "gc_panel_tma_item_elems": ctypes.c_int64, "gc_krylov_partials": ctypes.c_int64}
+             "gc_reset_launch_count": None, "gc_krylov_partials": ctypes.c_int64}
 
 EXPORTED = tuple(_SIGNATURES)
-ABI_VERSION = 2
+ABI_VERSION = 3
 
 _lib = None
 

@@ -228,8 +228,8 @@ class DeviceBasis:
     ``rank, rows (R = factor rows), piv_off, v_off, coef_off, height``.
     Tensors: ``pivots`` (compact global pivot ids), ``V`` (R x rank
     row-major per node at ``v_off``: leaf V or internal V-hat whose row
-    blocks are the children's transfers), ``VT`` (the transposes, row side
-    only, used by the backward transform).
+    blocks are the children's transfers), ``VT`` (the transposes, lazily,
+    :meth:`transposed_V`).
     """
 
     def __init__(self, tree, side, device):
@@ -253,6 +253,20 @@ class DeviceBasis:
         self.coef_size = 0
         self._host_V = None
         self.timing = {}
+
+    def transposed_V(self):
+        """``VT``: every node's R x rank block transposed (rank x R row-major
+        at the same offset), built on first use (the level-by-level
+        backward transform reads it; the tiered plan does not)."""
+        if self.VT is None:
+            ids = np.flatnonzero(self.materialized & (self.rank > 0))
+            self.VT = padded_empty(self.V.numel(), self.device).zero_()
+            if ids.size:
+                tdesc = to_dev(np.stack([self.v_off[ids], self.rows[ids], self.rank[ids]], 1), self.device)
+                with torch.cuda.device(self.device):
+                    _native.call("gc_batched_transpose", len(ids), ptr(tdesc), ptr(self.V), ptr(self.VT),
+                                 stream_handle())
+        return self.VT
 
     def host_V(self):
         if self._host_V is None:
@@ -530,13 +544,6 @@ def build_cluster_bases(tree, mesh, basis, m, delta_factor, eps, sides, orders=(
         st.V = padded_copy(torch.cat(s.v_parts)) if s.v_parts else padded_empty(1, dev)
         if st.V.numel() == 0:
             st.V = padded_empty(1, dev).zero_()
-        if s.side == "row" and s.mat.any():
-            ids = np.flatnonzero(s.mat & (st.rank > 0))
-            tdesc = to_dev(np.stack([st.v_off[ids], st.rows[ids], st.rank[ids]], 1), dev)
-            st.VT = padded_empty(st.V.numel(), dev).zero_()
-            with torch.cuda.device(dev):
-                _native.call("gc_batched_transpose", len(ids), ptr(tdesc), ptr(st.V),
-                             ptr(st.VT), stream)
         st.coef_off, st.coef_size = coef_layout(flat, s.roots, st.rank)
         st.timing = {"factor_s": t_factor, "aca_s": t_aca, "total_s": time.perf_counter() - t0,
                      "shared_with": len(S)}

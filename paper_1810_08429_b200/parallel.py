@@ -107,46 +107,93 @@ class ShardLayout:
 # --------------------------------------------------------------------------
 # device path
 
-class ShardedH2:
-    """Own block rows of the H2 operator on this rank's GPU."""
+def _all_gather_arrays(arr, group, device):
+    """Variable-length int64 arrays from every rank (tensor all-gathers:
+    the lengths, then the arrays padded to the longest)."""
+    import torch
+    import torch.distributed as dist
+    world = dist.get_world_size(group)
+    on = device if dist.get_backend(group) == "nccl" else torch.device("cpu")
+    a = torch.as_tensor(np.asarray(arr, np.int64)).to(on)
+    n = torch.tensor([a.numel()], dtype=torch.int64, device=on)
+    ns = torch.zeros(world, dtype=torch.int64, device=on)
+    dist.all_gather_into_tensor(ns, n, group=group)
+    ns = ns.cpu().numpy()
+    m = max(int(ns.max()), 1)
+    pad = torch.zeros(m, dtype=torch.int64, device=on)
+    pad[:a.numel()] = a
+    out = torch.zeros(world * m, dtype=torch.int64, device=on)
+    dist.all_gather_into_tensor(out, pad, group=group)
+    out = out.cpu().numpy()
+    return [out[g * m:g * m + int(ns[g])] for g in range(world)]
 
-    def __init__(self, h, layout, group, slot):
+
+def all_gather_into(out, inp, group):
+    """out = concat over ranks of inp (equal sizes).  NCCL gathers device
+    tensors directly, in place when inp is out's own slot; other backends
+    (gloo: the multi-process functional test on one GPU) stage through host
+    memory."""
+    import torch
+    import torch.distributed as dist
+    if dist.get_backend(group) == "nccl":
+        dist.all_gather_into_tensor(out, inp, group=group)
+        return
+    parts = [torch.empty(inp.numel(), dtype=inp.dtype) for _ in range(dist.get_world_size(group))]
+    dist.all_gather(parts, inp.detach().cpu(), group=group)
+    out.copy_(torch.cat(parts).to(out.device))
+
+
+class ShardedH2:
+    """Own block rows of the H2 operator on this rank's GPU.
+
+    ``mvm(x)`` is the reference's ``mvm(h, x)`` (``h2.py:63-80``): the full
+    vector in external ordering on every rank, the full product back on
+    every rank.  ``mvm_slice`` works on this rank's tree-ordered slice
+    (device tensors) - the per-rank hot path of the benchmark."""
+
+    def __init__(self, h, layout, group, slot, ranges):
         self.h = h
         self.layout = layout
         self.group = group
         self.slot = slot
+        self.ranges = ranges            # (lo, hi) of every rank
         self.plan = None
+        self.shape = h.shape
 
-    def mvm_local(self, x_slice):
-        """Own slice of y = H x (tree order) from the own slice of x."""
+    def _plan(self):
         import torch
         if self.plan is None:
-            self.plan = ShardPlan(self)
-        with torch.cuda.device(self.plan.dev):
-            return self.plan.run(x_slice)
+            with torch.cuda.device(self.h.dev.device):
+                self.plan = ShardPlan(self)
+        return self.plan
 
-    def mvm(self, x_slice):
-        """Host-facing product: this rank's slice of x (numpy, tree order) in,
-        its slice of y out, through pinned staging buffers."""
-        import numpy as np
+    def mvm_slice(self, x_slice, out=None):
+        """Own slice of y = H x (tree order, device) from the own slice of x
+        (device); written into ``out`` when given, else a new tensor."""
         import torch
-        x_slice = np.ascontiguousarray(x_slice, dtype=np.float64)
-        if x_slice.shape != (self.layout.hi - self.layout.lo,):
-            raise ConfigError("slice of length %d, shard owns %d rows"
-                              % (x_slice.size, self.layout.hi - self.layout.lo))
-        if getattr(self, "_pin", None) is None:
-            self._pin = (torch.empty(x_slice.size, dtype=torch.float64).pin_memory(),
-                         torch.empty(x_slice.size, dtype=torch.float64).pin_memory())
-        xin, yout = self._pin
-        xin.numpy()[:] = x_slice
-        y = self.mvm_local(xin.to("cuda", non_blocking=True))
-        yout.copy_(y, non_blocking=True)
-        torch.cuda.current_stream().synchronize()
-        return yout.numpy().copy()
+        p = self._plan()
+        with torch.cuda.device(p.dev):
+            return p.run_slice(x_slice, out)
+
+    mvm_local = mvm_slice
+
+    def mvm(self, x):
+        """y = H x for the full host vector x (external order), on every
+        rank: the shard's rows gathered on the device, the three all-gathers
+        (x slices, x-hat slots, y slices) over NCCL, the product scattered
+        back to external order, one host copy in and one out."""
+        import torch
+        n = self.shape[1]
+        x = np.asarray(x, dtype=np.float64)
+        if x.shape != (n,):
+            raise ConfigError("vector of length %d, operator wants %d" % (x.size, n))
+        p = self._plan()
+        with torch.cuda.device(p.dev):
+            return p.run_external(x)
 
 
 def build_sharded_operator(mesh, cfg, group=None, device=None, timings=None):
-    """Trees, block tree, own bases, allgathered column pivots and the own
+    """Trees, block tree, own bases, all-gathered column pivots and the own
     block rows of the GCA-H2 matrix for this rank."""
     import time
 
@@ -167,107 +214,164 @@ def build_sharded_operator(mesh, cfg, group=None, device=None, timings=None):
     orders = (cfg.q_reg, cfg.q_sing)
     rmarks, cmarks = gca.coupling_marks(btree)
     t1 = time.perf_counter()
-    rb = gca.build_cluster_basis(tree, mesh, cfg.basis, cfg.m, cfg.delta_factor, cfg.eps,
-                                 "row", orders, rmarks, dev, row_range=rng)
-    cb = gca.build_cluster_basis(tree, mesh, cfg.basis, cfg.m, cfg.delta_factor, cfg.eps,
-                                 "col", orders, cmarks, dev, row_range=rng)
+    row_kind = "collocation" if cfg.disc == "collocation" else cfg.basis      # cli.py:167
+    rb, cb = gca.build_cluster_bases(tree, mesh, cfg.basis, cfg.m, cfg.delta_factor, cfg.eps,
+                                     [("row", rmarks, row_kind), ("col", cmarks, cfg.basis)], orders,
+                                     dev, row_range=rng)
     t2 = time.perf_counter()
     cs = cb.store
     flat = tree.flat
     own = np.flatnonzero(cs.materialized)
-    mine = (own, cs.rank[own], [cs.pivots_host[cs.piv_off[i]:cs.piv_off[i] + cs.rank[i]]
-                                 for i in own])
-    gathered = [None] * world
-    dist.all_gather_object(gathered, mine, group=group)
-    # global column pivot table and rank-major coefficient layout
-    piv_parts, pos = [], 0
-    for nodes, ranks, pivs in gathered:
-        for i, r, pv in zip(nodes, ranks, pivs):
-            cs.rank[i] = r
-            cs.piv_off[i] = pos
-            piv_parts.append(np.asarray(pv, dtype=np.int64))
-            pos += int(r)
-    cs.pivots = to_dev(np.concatenate(piv_parts) if piv_parts else np.zeros(1, np.int64), dev)
-    cs.coef_off, slot = ShardLayout.global_coef(flat, [(g[0], g[1]) for g in gathered])
+    own_piv = (np.concatenate([cs.pivots_host[cs.piv_off[i]:cs.piv_off[i] + cs.rank[i]] for i in own])
+               if own.size else np.zeros(0, np.int64))
+    nodes_g = _all_gather_arrays(own, group, dev)
+    ranks_g = _all_gather_arrays(cs.rank[own], group, dev)
+    pivs_g = _all_gather_arrays(own_piv, group, dev)
+    # global column pivot table (host and device) and rank-major coefficient layout
+    pos = 0
+    for nodes, ranks in zip(nodes_g, ranks_g):
+        cs.rank[nodes] = ranks
+        cs.piv_off[nodes] = pos + np.cumsum(ranks) - ranks
+        pos += int(ranks.sum())
+    cs.pivots_host = np.concatenate(pivs_g) if pos else np.zeros(0, np.int64)
+    cs.pivots = to_dev(cs.pivots_host if pos else np.zeros(1, np.int64), dev)
+    cs.coef_off, slot = ShardLayout.global_coef(flat, list(zip(nodes_g, ranks_g)))
     cs.coef_size = world * slot
     cs.available = cs.available.copy()
-    for nodes, _, _ in gathered:
-        cs.available[np.asarray(nodes, dtype=np.int64)] = True
+    for nodes in nodes_g:
+        cs.available[nodes] = True
     h = gca.build_h2(btree, rb, cb, mesh, kind="slp", basis=cfg.basis, disc=cfg.disc,
                      orders=orders, device=dev, row_range=rng)
     torch.cuda.synchronize(dev)
     t3 = time.perf_counter()
     if timings is not None:
         timings.update(trees_s=t1 - t0, bases_s=t2 - t1, build_h2_s=t3 - t2, total_s=t3 - t0)
-    return ShardedH2(h, layout, group, slot)
-
-
-def all_gather_into(out, inp, group):
-    """out = concat over ranks of inp.  NCCL gathers device tensors in place;
-    other backends (gloo: the multi-process functional test on one GPU)
-    stage through host memory."""
-    import torch
-    import torch.distributed as dist
-    if dist.get_backend(group) == "nccl":
-        dist.all_gather_into_tensor(out, inp, group=group)
-        return
-    parts = [torch.empty(inp.numel(), dtype=inp.dtype) for _ in range(dist.get_world_size(group))]
-    dist.all_gather(parts, inp.detach().cpu(), group=group)
-    out.copy_(torch.cat(parts).to(out.device))
+    ranges = [shard_range(flat, world, g) for g in range(world)]
+    return ShardedH2(h, layout, group, slot, ranges)
 
 
 def _shard_plan_class():
+    from .device import ptr, stream_handle, to_dev
     from .h2 import PanelPlan
 
     class ShardPlan(PanelPlan):
-        """PanelPlan of one shard: the input slice is all-gathered into x_t,
-        the forward transform covers the own column subtree, and the x-hat
-        slots are all-gathered before the coupling phase."""
+        """PanelPlan of one shard.  x_t is the all-gather buffer of the
+        ranks' tree-ordered slices, each padded to the longest shard (slot
+        g at g * maxs: NCCL needs equal sizes), and every x_t index of the
+        plan is mapped into it.  Per product: the own slice lands in the
+        own slot, the x all-gather (in place), the forward transform of the
+        own column subtree, the x-hat all-gather (in place) gating the
+        coupling buckets, coupling, backward transform, near field and leaf
+        rows, then y_own = y_t + y_t2 over the own rows (gc_scatter2_inv).
+        Over NCCL the whole slice product is one CUDA graph."""
 
         def __init__(self, sh):
             import torch
             import torch.distributed as dist
-            super().__init__(sh.h)
             self.sh = sh
-            self.lo, self.hi = sh.layout.lo, sh.layout.hi
-            g = sh.layout.rank
-            self.own_xhat = self.xhat[g * sh.slot:(g + 1) * sh.slot]
-            f64 = dict(dtype=torch.float64, device=self.dev)
-            self.xhat_own = torch.zeros(sh.slot, **f64)        # all-gather input (no aliasing)
-            self.xs_in = torch.zeros(self.hi - self.lo, **f64)
-            self.ys_out = torch.zeros(self.hi - self.lo, **f64)
-
-            def gather_xhat():
-                self.xhat_own.copy_(self.own_xhat)
-                all_gather_into(self.xhat, self.xhat_own, sh.group)
-
-            # no permutation steps; the x-hat all-gather gates every coupling bucket
-            self.nodes = self._build_nodes(gather=False, before_coupling=gather_xhat, scatter=False)
+            world, g = sh.layout.world, sh.layout.rank
+            lo_hi = np.asarray(sh.ranges, np.int64).reshape(-1, 2)
+            sizes = lo_hi[:, 1] - lo_hi[:, 0]
+            self.maxs = maxs = int(sizes.max())
+            self.lo, self.hi = int(lo_hi[g, 0]), int(lo_hi[g, 1])
+            n = int(lo_hi[-1, 1])
+            owner = np.repeat(np.arange(world), sizes)
+            xmap = owner * maxs + (np.arange(n) - lo_hi[owner, 0])      # tree -> padded position
+            super().__init__(sh.h, xt_map=xmap, xt_len=world * maxs)
+            dev = self.dev
+            d = sh.h.dev
+            m_own = self.hi - self.lo
+            self.m_own = m_own
+            self.xt_own = self.xt[g * maxs:(g + 1) * maxs]
+            self.xhat_own = self.xhat[g * sh.slot:(g + 1) * sh.slot]
+            self.ypad = torch.zeros(world * maxs, dtype=torch.float64, device=dev)
+            self.y_own = self.ypad[g * maxs:(g + 1) * maxs]
+            self.x_in = torch.zeros(m_own, dtype=torch.float64, device=dev)
+            # y_own[j] = yt[lo + j] + yt2[lo + j]: gc_scatter2_inv over an identity range
+            self._own_rows = to_dev(np.arange(self.lo, self.hi, dtype=np.int64), dev)
+            # external API: own rows of x (external ids) -> own slot; padded y -> external y
+            perm_c = d.perm_c.cpu().numpy()
+            iperm_r = _inv_np(d.perm_r.cpu().numpy())
+            self._ext_own = to_dev(perm_c[self.lo:self.hi].astype(np.int64), dev)
+            self._ext_from_pad = to_dev(xmap[iperm_r].astype(np.int64), dev)
+            self.nodes = self._build_nodes(gather=False, before_coupling=self._gather_xhat, scatter=False)
             self.graph = None
-            if dist.get_backend(sh.group) == "nccl":
-                # the whole sharded product, both NCCL all-gathers included,
-                # as one CUDA graph; eager if capture is not supported
-                try:
-                    self.capture()
-                except Exception:            # pragma: no cover - depends on the NCCL build
-                    self.graph = None
-                    torch.cuda.synchronize(self.dev)
+            self.nccl = dist.get_backend(sh.group) == "nccl"
+            if self.nccl:
+                self._capture_slice()
 
-        def _body(self, phase_events=None, phase="coupling"):
-            import torch
-            all_gather_into(self.xt, self.xs_in, self.sh.group)
+        def _gather_xhat(self):
+            all_gather_into(self.xhat, self.xhat_own, self.sh.group)
+
+        def _body_slice(self):
+            self.xt_own[:self.m_own].copy_(self.x_in, non_blocking=True)
+            all_gather_into(self.xt, self.xt_own, self.sh.group)
             self._exec(self.nodes)
-            torch.add(self.yt[self.lo:self.hi], self.yt2[self.lo:self.hi], out=self.ys_out)
+            _native_call("gc_scatter2_inv", ptr(self.yt), ptr(self.yt2), ptr(self._own_rows), self.m_own,
+                         ptr(self.y_own), stream_handle())
 
-        def run(self, x_slice):
-            self.xs_in.copy_(x_slice, non_blocking=True)
-            if self.graph is not None:
-                self.graph.replay()
-            else:
-                self._body()
-            return self.ys_out.clone()
+        def _capture_slice(self):
+            import torch
+            s = torch.cuda.Stream(device=self.dev)
+            s.wait_stream(torch.cuda.current_stream())
+            with torch.cuda.stream(s):
+                self._body_slice()                 # warm-up (NCCL communicator, modules)
+            torch.cuda.current_stream().wait_stream(s)
+            torch.cuda.synchronize(self.dev)
+            g = torch.cuda.CUDAGraph()
+            with torch.cuda.graph(g, stream=s):
+                self._body_slice()
+            torch.cuda.synchronize(self.dev)
+            self.graph = g
+
+        def run_slice(self, x_slice, out=None):
+            if x_slice.numel() != self.m_own:
+                raise ConfigError("slice of length %d, shard owns %d rows" % (x_slice.numel(), self.m_own))
+            with self.lock:
+                self.x_in.copy_(x_slice, non_blocking=True)
+                if self.graph is not None:
+                    self.graph.replay()
+                else:
+                    self._body_slice()
+                res = self.y_own[:self.m_own]
+                if out is None:
+                    return res.clone()
+                out.copy_(res, non_blocking=True)
+                return out
+
+        def run_external(self, x):
+            import torch
+            with self.lock:
+                if not hasattr(self, "_pin_x"):
+                    self._pin_x = torch.empty(self.n_in, dtype=torch.float64, pin_memory=True)
+                    self._x_full = torch.empty(self.n_in, dtype=torch.float64, device=self.dev)
+                    self._y_full = torch.empty(self.n_out, dtype=torch.float64, device=self.dev)
+                self._pin_x.numpy()[:] = x
+                self._x_full.copy_(self._pin_x, non_blocking=True)
+                st = stream_handle()
+                # own slice of x in tree order, straight from the external vector
+                _native_call("gc_gather", ptr(self._x_full), ptr(self._ext_own), self.m_own, ptr(self.x_in), st)
+                self._body_slice()
+                all_gather_into(self.ypad, self.y_own, self.sh.group)
+                _native_call("gc_gather", ptr(self.ypad), ptr(self._ext_from_pad), self.n_out, ptr(self._y_full),
+                             stream_handle())
+                y = torch.empty(self.n_out, dtype=torch.float64, pin_memory=True)
+                y.copy_(self._y_full, non_blocking=True)
+                torch.cuda.current_stream().synchronize()
+                return y.numpy()
 
     return ShardPlan
+
+
+def _native_call(name, *args):
+    from . import _native
+    _native.call(name, *args)
+
+
+def _inv_np(perm):
+    inv = np.empty_like(perm)
+    inv[perm] = np.arange(len(perm), dtype=perm.dtype)
+    return inv
 
 
 def ShardPlan(sh):

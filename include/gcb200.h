@@ -100,6 +100,15 @@ typedef struct gc_rules {
  * sequentially without FMA, nodes = corners + straight midpoints
  * (assembly._interp6 / _surface_quadrature, assembly.py:138-143, 371-381).
  *   n6 [dev] (mq,6) shape functions at the triangle_gauss(q_reg) points. */
+/* Plane chart data and cluster support of every triangle, bit-identical to
+ * the host's numpy arrays (geometry.py:266-293 chart_pack, :324-338
+ * control_points, clustering.py:107-128 support boxes, centroids): verts
+ * [dev] (nv,3), tris [dev] (nt,3), gu / gv [host] (6) = the shape-function
+ * gradients at node 0 -> corners [dev] (nt,3,3), gram [dev] (nt), normal
+ * [dev] (nt,3) (|normal| = gram), support [dev] (nt,9) = control-point box
+ * lower | upper | centroid. */
+int gc_chart_pack(const double* verts, const int64_t* tris, int64_t nt, const double* gu, const double* gv,
+                  double* corners, double* gram, double* normal, double* support, void* stream);
 int gc_surface_points(const double* corners, int64_t nt, const double* n6,
                       int64_t mq, double* xq, void* stream);
 

@@ -40,6 +40,7 @@ _SIGNATURES = {
     "gc_launch_count": [],
     "gc_reset_launch_count": [],
     "gc_surface_points": [c_p, c_i64, c_p, c_i64, c_p, c_p],
+    "gc_chart_pack": [c_p, c_p, c_i64, c_p, c_p, c_p, c_p, c_p, c_p, c_p],
     "gc_pair_eval": [ctypes.POINTER(GcGeom), ctypes.POINTER(GcRules), ctypes.c_int, c_i64,
                      c_p, c_p, c_p, c_p, c_p, c_p],
     "gc_assemble_blocks": [ctypes.POINTER(GcGeom), c_i64, c_p, c_i64, c_i64, c_p, c_p, c_p,

@@ -316,8 +316,14 @@ def _build_cluster_tree_device(mesh, basis_kind, leaf_size, device):
 
     from . import _native
     from .device import ptr, stream_handle
-    points, lo, hi = _support_data(mesh, basis_kind)
-    n = len(points)
+    from .device import device_charts
+    charts = device_charts(mesh, device) if basis_kind == "constant" else None
+    if charts is not None:
+        # per-dof pack [lo | hi | centroid] straight from the device charts
+        n = int(charts["support"].shape[0])
+    else:
+        points, lo, hi = _support_data(mesh, basis_kind)
+        n = len(points)
     memo = {}
     total = _subtree_counts(n, leaf_size, memo)
     start = np.zeros(total, dtype=np.int64)
@@ -329,7 +335,8 @@ def _build_cluster_tree_device(mesh, basis_kind, leaf_size, device):
     lower = np.zeros((total, 3))
     upper = np.zeros((total, 3))
     f64 = dict(dtype=torch.float64, device=device)
-    pack = [torch.from_numpy(np.ascontiguousarray(np.concatenate([lo, hi, points], axis=1))).to(device),
+    pack = [charts["support"].clone() if charts is not None else
+            torch.from_numpy(np.ascontiguousarray(np.concatenate([lo, hi, points], axis=1))).to(device),
             torch.empty((n, 9), **f64)]
     perm = [torch.arange(n, dtype=torch.int64, device=device), torch.empty(n, dtype=torch.int64, device=device)]
     keys = torch.empty(2 * n, **f64)                       # sort scratch (torch caching allocator)

@@ -73,6 +73,83 @@ __global__ void k_scatter2_inv(const double* __restrict__ yt, const double* __re
     }
 }
 
+// Plane chart data and cluster support of every triangle (geometry.py:266-293
+// chart_pack, :324-338 control_points, clustering.py:107-128 support boxes,
+// TriangleMesh.centroids) in numpy's operation order, without contraction,
+// so the results are bit-identical to the host arrays:
+//   nodes 3..5 = 0.5 * (p_i + p_j); du, dv = sum_a g[a] * node[a] in node
+//   order; n = cross(du, dv) (a1*b2 - a2*b1, ...); gram = sqrt((n0^2 +
+//   n1^2) + n2^2); control points 3..5 = 0.5 * ((4 m - p_i) - p_j); lo / hi
+//   = min / max over the 6 control points; centroid = ((a + b) + c) / 3.
+// Outputs: corners (nt,3,3), gram (nt), normal (nt,3), support (nt,9) =
+// [lo | hi | centroid] (the cluster tree's per-dof pack).
+struct ChartGrads { double gu[6], gv[6]; };
+
+__global__ void k_chart_pack(const double* __restrict__ verts, const int64_t* __restrict__ tris, int64_t nt,
+                             ChartGrads g, double* __restrict__ corners, double* __restrict__ gram,
+                             double* __restrict__ normal, double* __restrict__ support) {
+    for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < nt;
+         t += (int64_t)gridDim.x * blockDim.x) {
+        double node[6][3];
+#pragma unroll
+        for (int k = 0; k < 3; ++k) {
+            const int64_t v = tris[3 * t + k];
+#pragma unroll
+            for (int c = 0; c < 3; ++c) node[k][c] = verts[3 * v + c];
+        }
+#pragma unroll
+        for (int c = 0; c < 3; ++c) {
+            node[3][c] = __dmul_rn(0.5, __dadd_rn(node[0][c], node[1][c]));
+            node[4][c] = __dmul_rn(0.5, __dadd_rn(node[1][c], node[2][c]));
+            node[5][c] = __dmul_rn(0.5, __dadd_rn(node[2][c], node[0][c]));
+        }
+        double du[3], dv[3];
+#pragma unroll
+        for (int c = 0; c < 3; ++c) {
+            double a = 0.0, b = 0.0;
+#pragma unroll
+            for (int k = 0; k < 6; ++k) {
+                a = __dadd_rn(a, __dmul_rn(g.gu[k], node[k][c]));
+                b = __dadd_rn(b, __dmul_rn(g.gv[k], node[k][c]));
+            }
+            du[c] = a;
+            dv[c] = b;
+        }
+        const double n0 = __dsub_rn(__dmul_rn(du[1], dv[2]), __dmul_rn(du[2], dv[1]));
+        const double n1 = __dsub_rn(__dmul_rn(du[2], dv[0]), __dmul_rn(du[0], dv[2]));
+        const double n2 = __dsub_rn(__dmul_rn(du[0], dv[1]), __dmul_rn(du[1], dv[0]));
+        gram[t] = __dsqrt_rn(__dadd_rn(__dadd_rn(__dmul_rn(n0, n0), __dmul_rn(n1, n1)), __dmul_rn(n2, n2)));
+        normal[3 * t] = n0;
+        normal[3 * t + 1] = n1;
+        normal[3 * t + 2] = n2;
+        double* sp = support + 9 * t;
+#pragma unroll
+        for (int c = 0; c < 3; ++c) {
+            corners[9 * t + c] = node[0][c];
+            corners[9 * t + 3 + c] = node[1][c];
+            corners[9 * t + 6 + c] = node[2][c];
+            // np.minimum(lo, q) = lo < q ? lo : q (x86 MINPD: the second
+            // operand on ties, so signed zeros land as numpy's do)
+            double lo = node[0][c], hi = node[0][c];
+            lo = lo < node[1][c] ? lo : node[1][c];
+            hi = hi > node[1][c] ? hi : node[1][c];
+            lo = lo < node[2][c] ? lo : node[2][c];
+            hi = hi > node[2][c] ? hi : node[2][c];
+            const int ij[3][2] = {{0, 1}, {1, 2}, {2, 0}};
+#pragma unroll
+            for (int e = 0; e < 3; ++e) {
+                const double q = __dmul_rn(
+                    0.5, __dsub_rn(__dsub_rn(__dmul_rn(4.0, node[3 + e][c]), node[ij[e][0]][c]), node[ij[e][1]][c]));
+                lo = lo < q ? lo : q;
+                hi = hi > q ? hi : q;
+            }
+            sp[c] = lo;
+            sp[3 + c] = hi;
+            sp[6 + c] = __ddiv_rn(__dadd_rn(__dadd_rn(node[0][c], node[1][c]), node[2][c]), 3.0);
+        }
+    }
+}
+
 // xq[t,m,c] = sum_a n6[m,a] * node[t,a,c], sequential, no contraction; nodes
 // 3..5 are the straight midpoints 0.5*(p_i + p_j) (geometry.py:278-280).
 __global__ void k_surface_points(const double* __restrict__ corners, int64_t nt,
@@ -239,6 +316,21 @@ int gc_surface_points(const double* corners, int64_t nt, const double* n6, int64
     k_surface_points<<<grid_for(nt * mq, 256), 256, 0, (cudaStream_t)stream>>>(
         corners, nt, n6, mq, xq);
     GC_CHECK_LAUNCH("gc_surface_points");
+    return GC_OK;
+}
+
+int gc_chart_pack(const double* verts, const int64_t* tris, int64_t nt, const double* gu, const double* gv,
+                  double* corners, double* gram, double* normal, double* support, void* stream) {
+    if (nt <= 0) return GC_OK;
+    if (!verts || !tris || !gu || !gv || !corners || !gram || !normal || !support) {
+        set_error(GC_ERR_CONFIG, "gc_chart_pack: null argument");
+        return GC_ERR_CONFIG;
+    }
+    ChartGrads g;
+    for (int k = 0; k < 6; ++k) g.gu[k] = gu[k], g.gv[k] = gv[k];
+    k_chart_pack<<<grid_for(nt, 256), 256, 0, (cudaStream_t)stream>>>(verts, tris, nt, g, corners, gram, normal,
+                                                                      support);
+    GC_CHECK_LAUNCH("gc_chart_pack");
     return GC_OK;
 }
 

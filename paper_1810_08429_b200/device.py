@@ -47,7 +47,10 @@ def to_dev(a, device, dtype=None):
     t = torch.from_numpy(a)
     if dtype is not None:
         t = t.to(dtype)
-    return t.to(device, non_blocking=False)
+    # asynchronous: a pageable source is staged by the driver before the
+    # call returns (no device synchronisation), so host work continues
+    # while earlier kernels run
+    return t.to(device, non_blocking=True)
 
 
 def zeros(shape, device, dtype=None):
@@ -75,25 +78,62 @@ def padded_copy(src):
     return out
 
 
+def device_charts(mesh, device):
+    """Plane chart data of a TriangleMesh computed on the device
+    (``gc_chart_pack``), bit-identical to the host ``chart_pack`` /
+    ``control_points`` / centroids: dict of device tensors ``verts``,
+    ``tris`` (int64), ``corners`` (nt,3,3), ``gram``, ``normal`` (nt,3) and
+    ``support`` (nt,9) = control-point box lower | upper | centroid.  Cached
+    on the mesh per device; None for other mesh types (host path)."""
+    from .geometry import TriangleMesh, _shape_gradients_at_nodes
+    if type(mesh) is not TriangleMesh:
+        return None
+    cache = mesh.__dict__.setdefault("_device_cache", {})
+    key = ("charts", str(device))
+    if key not in cache:
+        g = _shape_gradients_at_nodes()
+        gu = np.ascontiguousarray(g[0, :, 0], dtype=np.float64)
+        gv = np.ascontiguousarray(g[0, :, 1], dtype=np.float64)
+        nt = mesh.nt
+        out = dict(verts=to_dev(np.ascontiguousarray(mesh.vertices, dtype=np.float64), device),
+                   tris=to_dev(mesh.triangles.astype(np.int64), device),
+                   corners=empty((nt, 3, 3), device), gram=empty(nt, device), normal=empty((nt, 3), device),
+                   support=empty((nt, 9), device))
+        with torch.cuda.device(device):
+            _native.call("gc_chart_pack", ptr(out["verts"]), ptr(out["tris"]), nt, gu.ctypes.data,
+                         gv.ctypes.data, ptr(out["corners"]), ptr(out["gram"]), ptr(out["normal"]),
+                         ptr(out["support"]), stream_handle())
+        cache[key] = out
+    return cache[key]
+
+
 class DeviceMesh:
     """Chart data of one plane mesh on one device, for one regular order.
 
-    ``corners (nt,3,3)``, ``gram (nt,)`` (host-computed, never recomputed),
-    ``tri_vid (nt,3)``, and the regular-rule surface points ``xq (nt,q^2,3)``
-    computed on the device in the reference's operation order.
+    ``corners (nt,3,3)``, ``gram (nt,)``, ``tri_vid (nt,3)`` (plane meshes:
+    ``device_charts``, bit-identical to the host chart pack; quadratic
+    charts: uploaded from the host), and the regular-rule surface points
+    ``xq (nt,q^2,3)`` computed on the device in the reference's operation
+    order.
     """
 
     def __init__(self, mesh, q_reg, device):
-        pack = chart_pack(mesh)
         self.mesh = mesh
         self.device = device
         self.nt = mesh.nt
         self.q_reg = q_reg
         pts, wts = triangle_gauss(q_reg)
-        self.curved = bool(pack.curved)
-        self.corners = to_dev(pack.nodes[:, :3], device)
-        self.gram = to_dev(pack.gram if not self.curved else np.zeros(self.nt), device)
-        self.tri_vid = to_dev(mesh.triangles.astype(np.int64), device)
+        charts = device_charts(mesh, device)
+        if charts is not None:           # plane mesh: chart data built on the device
+            pack = None
+            self.curved = False
+            self.corners, self.gram, self.tri_vid = charts["corners"], charts["gram"], charts["tris"]
+        else:
+            pack = chart_pack(mesh)
+            self.curved = bool(pack.curved)
+            self.corners = to_dev(pack.nodes[:, :3], device)
+            self.gram = to_dev(pack.gram if not self.curved else np.zeros(self.nt), device)
+            self.tri_vid = to_dev(mesh.triangles.astype(np.int64), device)
         self.wq = to_dev(wts, device)
         self.mq = len(wts)
         n6h = shape_functions(pts)
@@ -115,7 +155,8 @@ class DeviceMesh:
             self.gq = self.nq = self.nodes6 = self.nrm6 = None
         self.wq_host = np.ascontiguousarray(wts, dtype=np.float64)
         # chart normal per triangle (|n| = gram), for the double layer of plane charts
-        self.normals = to_dev(np.ascontiguousarray(pack.normals[:, 0]), device)
+        self.normals = (charts["normal"] if charts is not None
+                        else to_dev(np.ascontiguousarray(pack.normals[:, 0]), device))
         # linear basis: vertex stars ordered by (corner, triangle) and the
         # barycentric values of the regular rule's points
         tris = mesh.triangles
@@ -126,7 +167,8 @@ class DeviceMesh:
         self.vstar_ptr = to_dev(np.searchsorted(vert[order], np.arange(mesh.nv + 1)).astype(np.int64), device)
         self.vstar_ent = to_dev((t_of[order] << 2) | corner[order], device)
         self.bq = to_dev(np.stack([1.0 - pts[:, 0] - pts[:, 1], pts[:, 0], pts[:, 1]], 1), device)
-        self.verts = to_dev(np.ascontiguousarray(mesh.vertices, dtype=np.float64), device)
+        self.verts = (charts["verts"] if charts is not None
+                      else to_dev(np.ascontiguousarray(mesh.vertices, dtype=np.float64), device))
         self._geoms = {}
         self.geom = self.geom_of("slp")
         self.geom_dlp = self.geom_of("dlp")

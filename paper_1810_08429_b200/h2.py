@@ -237,6 +237,9 @@ class PanelPlan:
     """
 
     def __init__(self, h, tiers="auto", xt_map=None, xt_len=None):
+        import time
+        t0 = time.perf_counter()
+        self.timing = {}
         d = h.dev
         dev = d.device
         self.dev = dev
@@ -293,6 +296,7 @@ class PanelPlan:
         panels = (d.n_off[order[cuts]], K, d.n_nr[order[cuts]], rows, rf.start[sn[cuts]], 0)
         near = self._phase("nearfield", 0, panels, d.near, None, self.xt, None, self.yt)
         self.tiers = None
+        t1 = time.perf_counter()
         tiered = self._tiered(h, tiers) if tiers != "off" else None
         if tiered is None:
             fwd, bwd, leafp = self._level_phases(h)
@@ -313,6 +317,8 @@ class PanelPlan:
         self.trace = {}                    # id(phase) -> [2] int64 (profiling only)
         self.nodes = self._build_nodes()
         self.graph = None
+        t2 = time.perf_counter()
+        self.timing.update(bulk_phases_s=t1 - t0, transforms_s=t2 - t1)
 
     def _xpos(self, p):
         """x_t buffer position of tree position p (index ranges never
@@ -379,7 +385,11 @@ class PanelPlan:
         d = h.dev
         explicit = None if bounds == "auto" else list(bounds)
         cb = T_.choose_tiers(cs, cf, bounds=explicit, max_rows=_ITEM_MAX_ROWS)
-        rb = cb if (rs is cs and rf is cf) else T_.choose_tiers(rs, rf, bounds=explicit, max_rows=_ITEM_MAX_ROWS)
+        # the tier choice depends on the tree, the live nodes and the ranks
+        # only: a symmetric operator's row store gets the column store's
+        same = (rf is cf and np.array_equal(rs.rank, cs.rank) and np.array_equal(rs.rows, cs.rows)
+                and np.array_equal(rs.materialized, cs.materialized))
+        rb = cb if (rs is cs or same) else T_.choose_tiers(rs, rf, bounds=explicit, max_rows=_ITEM_MAX_ROWS)
         if not cb or not rb:
             return None
         ct = T_.StoreTiers(cs, cf, cb, self.dev)
@@ -681,15 +691,19 @@ class PanelPlan:
         (csrc/plan.cu: its own streams, events and graph); a DAG with Python
         steps (the sharded plan's collectives) is captured through torch.
         A failed capture raises."""
+        import time
+        t0 = time.perf_counter()
         tab = self._native_table()
         if tab is not None:
             self._body()                         # warm-up (module loads) outside the capture
             torch.cuda.synchronize(self.dev)
+            self.timing["warmup_s"] = time.perf_counter() - t0
             rows, deps, ndeps, prio = tab
             h = _native.ctypes.c_void_p(0)
             _native.call("gc_plan_create", len(rows), rows.ctypes.data, ndeps, deps.ctypes.data, len(prio),
                          prio.ctypes.data, _native.ctypes.byref(h))
             self.graph = _NativeGraph(h)
+            self.timing["capture_s"] = time.perf_counter() - t0
             return self.graph
         s = torch.cuda.Stream(device=self.dev)
         s.wait_stream(torch.cuda.current_stream())

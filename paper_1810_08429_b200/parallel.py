@@ -447,8 +447,9 @@ def bench_distributed(args, rank, world, local, metric, workload, clock_sampler=
     dist.barrier()
     if sampler is not None:
         sampler.__exit__(None, None, None)
-    # end to end through the public sharded API: host slice -> product -> host slice
-    xh = np.random.default_rng(rank).standard_normal(m_own)
+    # end to end through the public sharded API (the reference's mvm(h, x)
+    # signature): the full host vector in, the full product back, every rank
+    xh = np.random.default_rng(0).standard_normal(n)
     for _ in range(3):
         sh.mvm(xh)
     torch.cuda.synchronize()
@@ -502,7 +503,8 @@ def bench_distributed(args, rank, world, local, metric, workload, clock_sampler=
             "e2e": {"value": round(nbytes / float(te.item()) / 1e9, 2), "unit": "GB/s",
                     "h2d_bytes_per_step": 8 * n, "d2h_bytes_per_step": 8 * n,
                     "ms_per_step": round(float(te.item()) * 1e3, 4),
-                    "api": "paper_1810_08429_b200.parallel.ShardedH2.mvm(numpy slice) on every rank"},
+                    "api": "paper_1810_08429_b200.parallel.ShardedH2.mvm(numpy x, external order) on every "
+                           "rank: own rows gathered on the device, x / x-hat / y all-gathered over NCCL"},
             "gpu_launches": int(launches.item()),
             "gpu_launches_note": "own kernels over all ranks in the timed region",
             "clocks": sampler.summary() if sampler is not None else None,

@@ -888,3 +888,24 @@ def test_device_cluster_tree_bitwise(name, basis):
     assert np.array_equal(t.flat.lower, g["lower"]) and np.array_equal(t.flat.upper, g["upper"])
     host = clustering.build_cluster_tree(mesh, basis, 16)
     assert np.array_equal(t.flat.depth, host.flat.depth) and np.array_equal(t.flat.left, host.flat.left)
+
+
+@pytest.mark.parametrize("kind,level", [("sphere", 6), ("cube", 7), ("sphere", 2)])
+def test_device_charts_bit_identical_to_host(kind, level):
+    """gc_chart_pack (device chart data and cluster support boxes) == the
+    host chart_pack / control_points / centroids bit for bit, signed zeros
+    included (numpy's minimum / maximum tie rule)."""
+    from paper_1810_08429_b200 import device
+    mesh = (geometry.build_sphere_mesh if kind == "sphere" else geometry.build_cube_mesh)(level)
+    ch = device.device_charts(mesh, torch.device("cuda", 0))
+    pack = geometry.chart_pack(mesh)
+    ctrl = geometry.control_points(mesh)
+    sup = ch["support"].cpu().numpy()
+    for got, ref in ((ch["corners"].cpu().numpy(), pack.nodes[:, :3]), (ch["gram"].cpu().numpy(), pack.gram),
+                     (ch["normal"].cpu().numpy(), pack.normals[:, 0]), (sup[:, 6:], mesh.centroids())):
+        assert got.tobytes() == np.ascontiguousarray(ref).tobytes()
+    lo, hi = ctrl[:, 0].copy(), ctrl[:, 0].copy()
+    for k in range(1, 6):
+        np.minimum(lo, ctrl[:, k], out=lo)
+        np.maximum(hi, ctrl[:, k], out=hi)
+    assert sup[:, :3].tobytes() == lo.tobytes() and sup[:, 3:6].tobytes() == hi.tobytes()

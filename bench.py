@@ -401,17 +401,18 @@ def run_native(args):
     total_s = e_start.elapsed_time(e_end) * 1e-3
     mv_s = total_s / args.steps
     value = nbytes / mv_s / 1e9
-    # roofline kernel: the largest coupling bucket's k_panelmv launch (the
-    # dominant launch of the step), alone on the current stream, timed with
-    # CUDA events; L2 flushed (256 MB write) before every launch
+    # roofline kernel: the largest coupling launch (the dominant launch of the
+    # step), alone on the current stream, timed with CUDA events; L2 evicted
+    # before every launch by a read-only sweep of 256 MB (a write sweep would
+    # leave ~126 MB of dirty lines to be written back inside the timed launch)
     big = max((P for P in p.phases if P.name == "coupling"), key=lambda P: P.bytes)
-    flush = torch.empty(32 << 20, dtype=torch.float64, device="cuda")
+    flush = torch.empty(32 << 20, dtype=torch.float64, device="cuda").fill_(1.0)
     l0 = _native.launch_count()
     ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
           for _ in range(max(5, args.steps))]
     torch.cuda.synchronize()
     for a_, b_ in ev:
-        flush.zero_()
+        flush.sum()
         a_.record()
         p._launch(big, stream_handle())
         b_.record()
@@ -468,8 +469,8 @@ def run_native(args):
                               "block sample" % (rb["cores"], 100 * args.cpu_sample)) if rb else None,
         "assembly_speedup": round(rb["assembly_s"] / assembly_s, 1) if rb else None,
         "config": workload(args),
-        "roofline": {"bound": "hbm", "kernel": "k_panelmv, largest coupling bucket (row height %d, %d items)"
-                     % (big.height, big.nitems),
+        "roofline": {"bound": "hbm", "kernel": "%s, largest coupling launch (row heights <= %d, %d items)"
+                     % ("k_panel_ring" if big.ring else "k_panelmv", big.height, big.nitems),
                      "achieved": round(big_bytes / big_s / 1e9, 1), "peak": hbm_peak, "unit": "GB/s",
                      "frac": round(big_bytes / big_s / 1e9 / hbm_peak, 4), "traffic": _traffic("coupling_bucket"),
                      "algorithmic_bytes_per_launch": int(big_bytes), "avg_launch_s": big_s,

@@ -237,7 +237,10 @@ int gc_graph_retarget(void* graph, void* exec, int32_t kernel, int32_t arg, cons
  * previous kernel on the stream drains and waits for it before reading in
  * (for the latency-bound transform levels); the next launch is released at
  * each CTA's start.  chain & 16 runs two whole small panels per CTA (direct
- * items, T <= 128, <= 512 rows).  priority != 0 sets the
+ * items, T <= 128, <= 512 rows).  chain & 32 streams each item's matrix
+ * through a 2-stage shared-memory ring of 1-D TMA bulk copies issued before
+ * the input gather (bulk phases, T <= 256; the matrix buffer must be
+ * readable 16 bytes past its end); same results bit for bit.  priority != 0 sets the
  * launch's scheduling priority (CUDA stream-priority scale, lower = more
  * urgent; 0 = the stream's own).  trace (optional, NULL = off)
  * = [dev] 2 x uint64 receiving min(start) / max(end) %globaltimer (ns) of

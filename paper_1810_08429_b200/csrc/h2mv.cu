@@ -250,6 +250,155 @@ __global__ void __launch_bounds__(PAN_THREADS, 6) k_panel_pair(PanelPhase P) {
     }
 }
 
+// ---------------------------------------------------------------------------
+// Bulk phases (coupling buckets, near field): one CTA per item as in
+// k_panelmv, but the item's matrix streams through a 2-stage shared-memory
+// ring filled by 1-D TMA bulk copies (cp.async.bulk, completion on one
+// mbarrier per stage).  Thread 0 issues the first two 16 KB chunks before
+// the index -> input gather, so the matrix stream overlaps the item's
+// prologue, and the bytes in flight (32 KB per CTA) do not cost registers.
+// Thread (g, t) sums the same rows in the same order as k_panelmv: the
+// results are bitwise identical.  Requires T <= PAN_THREADS; every matrix
+// buffer must be readable 16 bytes past its end (device.padded_empty).
+constexpr int RING_STAGES = 2;
+constexpr int RING_ELEMS = 2048;                  // 16 KB per stage
+
+struct RingSmem {
+    double stage[RING_STAGES][RING_ELEMS + 2];    // + 16-byte alignment slack
+    double red[PAN_THREADS];
+    double xs[PAN_MAX_ROWS];
+    unsigned long long full[RING_STAGES];
+    int last;
+};
+
+__device__ __forceinline__ uint32_t smem_u32(const void* p) {
+    return static_cast<uint32_t>(__cvta_generic_to_shared(p));
+}
+
+__device__ __forceinline__ void ring_issue(RingSmem& sm, int st, const double* A, int c, int rps, int nrows,
+                                           int T) {
+    const int r0 = c * rps;
+    const int nr = min(rps, nrows - r0);
+    const uintptr_t sa = reinterpret_cast<uintptr_t>(A + (int64_t)r0 * T);
+    const unsigned lead = (unsigned)((sa & 15) >> 3);
+    const unsigned bytes = ((unsigned)(nr * T + (int)lead) * 8u + 15u) & ~15u;
+    const uint32_t bar = smem_u32(&sm.full[st]);
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(bar), "r"(bytes) : "memory");
+    asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];"
+                 ::"r"(smem_u32(sm.stage[st])), "l"(sa & ~uintptr_t(15)), "r"(bytes), "r"(bar) : "memory");
+}
+
+__device__ __forceinline__ void ring_wait(RingSmem& sm, int st, unsigned parity) {
+    const uint32_t bar = smem_u32(&sm.full[st]);
+    uint32_t done = 0;
+    while (!done) {
+        asm volatile("{\n .reg .pred p;\n mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n"
+                     " selp.u32 %0, 1, 0, p;\n}\n"
+                     : "=r"(done) : "r"(bar), "r"(parity) : "memory");
+    }
+}
+
+__global__ void __launch_bounds__(PAN_THREADS, 4) k_panel_ring(PanelPhase P) {
+    extern __shared__ __align__(128) unsigned char ring_raw[];
+    RingSmem& sm = *reinterpret_cast<RingSmem*>(ring_raw);
+    if (P.trace != nullptr && threadIdx.x == 0) atomicMin(P.trace, globaltimer());
+    const int64_t* it = P.items + 8 * (int64_t)blockIdx.x;
+    const int64_t a_off = it[0], xi_off = it[1], out_off = it[2];
+    const int T = (int)it[3], nrows = (int)it[4], mode = (int)it[5];
+    const double* __restrict__ A = ((mode & 1) ? P.A1 : P.A0) + a_off;
+    const int rps = RING_ELEMS / T;
+    const int nch = (nrows + rps - 1) / rps;
+    if (threadIdx.x == 0) {
+        for (int st = 0; st < RING_STAGES; ++st)
+            asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(smem_u32(&sm.full[st])));
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+        for (int c = 0; c < RING_STAGES && c < nch; ++c) ring_issue(sm, c, A, c, rps, nrows, T);
+    }
+    const int32_t* __restrict__ xi = P.xidx + xi_off;
+    if (mode & 32) {
+        for (int r = threadIdx.x; r < nrows; r += PAN_THREADS) {
+            const int i = __ldg(xi + r);
+            sm.xs[r] = __ldcg(P.in0 + i) + __ldcg(P.in1 + i);
+        }
+    } else {
+        const double* x = (mode & 2) ? P.in1 : P.in0;
+        for (int r = threadIdx.x; r < nrows; r += PAN_THREADS) sm.xs[r] = __ldcg(x + __ldg(xi + r));
+    }
+    __syncthreads();
+    const int tt = T;                                      // T <= PAN_THREADS
+    const int ng = PAN_THREADS / tt;
+    const int g = threadIdx.x / tt, t = threadIdx.x % tt;
+    const bool live = g < ng;
+    double acc = 0.0;
+    for (int c = 0; c < nch; ++c) {
+        const int st = c % RING_STAGES;
+        ring_wait(sm, st, (unsigned)(c / RING_STAGES) & 1u);
+        const int r0 = c * rps;
+        const int nr = min(rps, nrows - r0);
+        const double* sa = sm.stage[st] + ((reinterpret_cast<uintptr_t>(A + (int64_t)r0 * T) & 15) >> 3);
+        if (live) {
+            int r = ((g - r0 % ng) % ng + ng) % ng;
+            const double* pa = sa + r * T + t;
+            const double* px = sm.xs + r0 + r;
+            const int sa_step = ng * T;
+            for (; r + 3 * ng < nr; r += 4 * ng) {
+                acc = fma(pa[0], px[0], acc);
+                acc = fma(pa[sa_step], px[ng], acc);
+                acc = fma(pa[2 * sa_step], px[2 * ng], acc);
+                acc = fma(pa[3 * sa_step], px[3 * ng], acc);
+                pa += 4 * sa_step;
+                px += 4 * ng;
+            }
+            for (; r < nr; r += ng) {
+                acc = fma(pa[0], px[0], acc);
+                pa += sa_step;
+                px += ng;
+            }
+        }
+        __syncthreads();                                   // stage st consumed
+        if (threadIdx.x == 0 && c + RING_STAGES < nch) ring_issue(sm, st, A, c + RING_STAGES, rps, nrows, T);
+    }
+    sm.red[threadIdx.x] = acc;
+    __syncthreads();
+    if (threadIdx.x < tt) {
+        double s = sm.red[threadIdx.x];
+        for (int q = 1; q < ng; ++q) s += sm.red[q * tt + threadIdx.x];
+        if (mode & 4) {
+            double* o = P.out + out_off + t;
+            *o = (mode & 8) ? __ldcg(o) + s : s;
+        } else {
+            P.scratch[out_off + t] = s;
+        }
+    }
+    if (!(mode & 4)) {
+        // split panel: the last arriving item adds the partial sums in item order
+        const int slot = (int)it[6];
+        const int64_t* rd = P.red + 5 * (int64_t)slot;
+        __threadfence();
+        __syncthreads();
+        if (threadIdx.x == 0) sm.last = atomicAdd(P.arrivals + slot, 1) == (int)rd[3] - 1;
+        __syncthreads();
+        if (sm.last) {
+            __threadfence();
+            const int64_t o_off = rd[0], so = rd[2];
+            const int RT = (int)rd[1], ni = (int)rd[3];
+            const bool accum = rd[4] != 0;
+            for (int tq = threadIdx.x; tq < RT; tq += PAN_THREADS) {
+                double v = __ldcg(P.scratch + so + tq);
+#pragma unroll 8
+                for (int i = 1; i < ni; ++i) v += __ldcg(P.scratch + so + (int64_t)i * RT + tq);
+                P.out[o_off + tq] = accum ? __ldcg(P.out + o_off + tq) + v : v;
+            }
+            __syncthreads();
+            if (threadIdx.x == 0) P.arrivals[slot] = 0;
+        }
+    }
+    if (P.trace != nullptr) {
+        __syncthreads();
+        if (threadIdx.x == 0) atomicMax(P.trace + 1, globaltimer());
+    }
+}
+
 }  // namespace gcb
 
 using namespace gcb;
@@ -292,7 +441,17 @@ extern "C" int gc_panelmv(int64_t nitems, const int64_t* items, const int32_t* x
     cfg.attrs = attr;
     cfg.numAttrs = na;
     cudaError_t e;
-    if (chain & 16) {
+    if (chain & 32) {
+        // bulk phase on the TMA ring kernel (items with T <= 256)
+        int dev = 0;
+        e = cudaGetDevice(&dev);
+        if (e == cudaSuccess)     // function attributes are per device context: set on every launch
+            e = cudaFuncSetAttribute(k_panel_ring, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                     (int)sizeof(RingSmem));
+        if (e != cudaSuccess) return cuda_status(e, "k_panel_ring smem attribute");
+        cfg.dynamicSmemBytes = sizeof(RingSmem);
+        e = cudaLaunchKernelEx(&cfg, k_panel_ring, P);
+    } else if (chain & 16) {
         // two whole small panels per CTA (direct items, T <= 128, <= 512 rows)
         cfg.gridDim = dim3((unsigned)((nitems + 1) / 2));
         e = (chain & 3) ? cudaLaunchKernelEx(&cfg, k_panel_pair<true>, P)

@@ -199,11 +199,13 @@ def _stream_ptr(stream=None):
 _ITEM_ELEMS = 65536          # <= 512 KB of matrix data per bulk work item (rows capped at 1024)
 _ITEM_MAX_ROWS = 1024        # PAN_MAX_ROWS in csrc/h2mv.cu
 _PAIR_MAX_ELEMS = 8192       # k_panel_pair (two small panels per CTA): panel size cap
+_RING_MIN_BYTES = 256 << 20  # bulk phases this large stream through k_panel_ring (measured: C4 +5 %, C2 -8 %)
+_MERGE_MIN_BYTES = 1 << 30   # coupling row heights with the same producer / consumer merge into one launch
 
 
 class _Phase:
     __slots__ = ("name", "height", "items", "xidx", "red", "arrivals", "nitems", "nred", "A0", "A1",
-                 "in0", "in1", "out", "scratch", "bytes", "in_elems", "out_elems", "pair")
+                 "in0", "in1", "out", "scratch", "bytes", "in_elems", "out_elems", "pair", "ring")
 
 
 class _Node:
@@ -236,10 +238,11 @@ class PanelPlan:
     executes it serially on the current stream (for per-phase timing).
     """
 
-    def __init__(self, h, tiers="auto", xt_map=None, xt_len=None):
+    def __init__(self, h, tiers="auto", xt_map=None, xt_len=None, bulk="auto"):
         import time
         t0 = time.perf_counter()
         self.timing = {}
+        self._bulk = bulk
         d = h.dev
         dev = d.device
         self.dev = dev
@@ -266,27 +269,6 @@ class PanelPlan:
         # in the scatter): one buffer, zeroed by one memset per product
         self._ybuf = torch.zeros(2 * ny + self.n_out, **f64)
         self.yhat, self.yhat_t, self.yt2 = self._ybuf[:ny], self._ybuf[ny:2 * ny], self._ybuf[2 * ny:]
-        # coupling: one panel per row cluster, bucketed by row height
-        cpl = []
-        live = (d.c_nr > 0) & (d.c_nc > 0)
-        order = np.flatnonzero(live)[np.argsort(d.c_rows[live], kind="stable")]
-        if order.size:
-            sn = d.c_rows[order]
-            cuts = np.flatnonzero(np.r_[True, sn[1:] != sn[:-1]])
-            # panel inputs: the x-hat slots of the blocks' column clusters, in
-            # block order - one index range per block, expanded on the device
-            bstart, blen = cs.coef_off[d.c_cols[order]], d.c_nc[order]
-            K = np.add.reduceat(blen, cuts)
-            nblk = np.diff(np.r_[cuts, len(order)])
-            colh = np.maximum.reduceat(cf.height[d.c_cols[order]], cuts)
-            rowh = rf.height[sn[cuts]]
-            for h_ in np.unique(rowh):
-                sel = np.flatnonzero(rowh == h_)
-                bsel = _ranges_np(cuts[sel], nblk[sel])
-                panels = (d.c_off[order[cuts[sel]]], K[sel], d.c_nr[order[cuts[sel]]],
-                          (bstart[bsel], blen[bsel]), rs.coef_off[sn[cuts[sel]]], 0)
-                P = self._phase("coupling", int(h_), panels, d.coup, None, self.xhat, None, self.yhat)
-                cpl.append((P, int(colh[sel].max())))
         # near field: one panel per row leaf
         order = np.argsort(d.n_rows, kind="stable")
         sn = d.n_rows[order]
@@ -304,8 +286,45 @@ class PanelPlan:
         else:
             fwd, bwd, parts = tiered
         parts = [(P, hs) for P, hs in parts if P is not None and P.nitems]
+        # coupling: one panel per row cluster.  Row clusters are grouped by
+        # (the forward phase producing every x-hat they read, the backward
+        # phase consuming their y-hat): one launch per group - e.g. all the
+        # deep buckets that only the leaf rows read - so a launch is as long
+        # as the dependencies allow (whole waves of work items)
+        cpl = []
+        live = (d.c_nr > 0) & (d.c_nc > 0)
+        order = np.flatnonzero(live)[np.argsort(d.c_rows[live], kind="stable")]
+        if order.size:
+            sn = d.c_rows[order]
+            cuts = np.flatnonzero(np.r_[True, sn[1:] != sn[:-1]])
+            # panel inputs: the x-hat slots of the blocks' column clusters, in
+            # block order - one index range per block, expanded on the device
+            bstart, blen = cs.coef_off[d.c_cols[order]], d.c_nc[order]
+            K = np.add.reduceat(blen, cuts)
+            nblk = np.diff(np.r_[cuts, len(order)])
+            colh = np.maximum.reduceat(cf.height[d.c_cols[order]], cuts)
+            rowh = rf.height[sn[cuts]]
+            fwd_h = [P.height for P in fwd if P.nitems]
+            src = np.array([next((k for k, fh in enumerate(fwd_h) if fh >= c), len(fwd_h)) for c in colh])
+            dst = np.array([next((k for k, (P, hs) in enumerate(bwd) if P.nitems and r in hs), len(bwd))
+                            for r in rowh])
+            # merge only into launches of >= _MERGE_MIN_BYTES: smaller groups stay
+            # one launch per row height (measured: C4 -1.5 %, C2 +10 % merged)
+            gbytes = {}
+            for k_, e_ in zip(zip(src.tolist(), dst.tolist()), (K * d.c_nr[order[cuts]]).tolist()):
+                gbytes[k_] = gbytes.get(k_, 0) + 8 * e_
+            grp = np.array([(a_, b_, -1 if gbytes[(a_, b_)] >= _MERGE_MIN_BYTES else int(h_))
+                            for a_, b_, h_ in zip(src.tolist(), dst.tolist(), rowh.tolist())], np.int64)
+            for key in sorted(set(map(tuple, grp.tolist())), key=lambda k: (-k[1], k[0], k[2])):
+                sel = np.flatnonzero(np.all(grp == np.array(key), axis=1))
+                bsel = _ranges_np(cuts[sel], nblk[sel])
+                panels = (d.c_off[order[cuts[sel]]], K[sel], d.c_nr[order[cuts[sel]]],
+                          (bstart[bsel], blen[bsel]), rs.coef_off[sn[cuts[sel]]], 0)
+                P = self._phase("coupling", int(rowh[sel].max()), panels, d.coup, None, self.xhat, None,
+                                self.yhat)
+                cpl.append((P, int(colh[sel].max()), set(rowh[sel].tolist())))
         self._fwd, self._cpl, self._bwd, self._near, self._leafparts = fwd, cpl, bwd, near, parts
-        self.phases = [P for P in [near] + fwd + [c for c, _ in cpl] + [b for b, _ in bwd] + [p for p, _ in parts]
+        self.phases = [P for P in [near] + fwd + [c for c, _, _ in cpl] + [b for b, _ in bwd] + [p for p, _ in parts]
                        if P is not None and P.nitems > 0]
         # the chain gets the highest stream priority so its CTAs are
         # scheduled ahead of the queued bulk (coupling buckets, near field)
@@ -442,7 +461,7 @@ class PanelPlan:
         priority."""
         if not self._cpl:
             return 0
-        by_h = sorted(((P.height, P.bytes) for P, _ in self._cpl), reverse=True)
+        by_h = sorted(((P.height, P.bytes) for P, _, _ in self._cpl), reverse=True)
         total = sum(b for _, b in by_h)
         acc, S = 0, by_h[0][0] + 1
         for h_, b in by_h:
@@ -482,7 +501,7 @@ class PanelPlan:
         if before_coupling is not None:
             gate = add(_Node("pre-coupling", "chain", [last], fn=before_coupling))
         bucket = {}
-        for P, colh in sorted(self._cpl, key=lambda c: c[0].height):
+        for P, colh, heights in sorted(self._cpl, key=lambda c: c[0].height):
             if gate is not None:
                 dep = [gate]
             else:
@@ -492,16 +511,19 @@ class PanelPlan:
             else:
                 prio = least - 1 - int(round(P.height * (levels - 2) / max(S - 1, 1)))
                 prio = min(least - 1, max(greatest + 1, prio))
-            bucket[P.height] = add(_Node("coupling", "c%d" % P.height, dep + [z], phase=P, priority=prio))
+            k = add(_Node("coupling", "c%d" % P.height, dep + [z], phase=P, priority=prio))
+            for hh in heights:
+                bucket[hh] = k
         prev = gate if gate is not None else last
         for P, hs in self._bwd:
             if P.nitems:
-                prev = add(_Node("backward", "chain", [prev] + [bucket[x] for x in sorted(hs) if x in bucket],
+                prev = add(_Node("backward", "chain", [prev] + sorted({bucket[x] for x in hs if x in bucket}),
                                  phase=P, priority=greatest))
         for P, hs in self._leafparts:
-            need = list(bucket.values()) if hs is None else [bucket[x] for x in sorted(hs) if x in bucket]
+            need = (sorted(set(bucket.values())) if hs is None
+                    else sorted({bucket[x] for x in hs if x in bucket}))
             prev = add(_Node("leafbasis", "chain", [prev] + need, phase=P, priority=greatest))
-        tail = [prev] + list(bucket.values())
+        tail = [prev] + sorted(set(bucket.values()))
         if near is not None:
             tail = tail + [near]
         if scatter:
@@ -581,6 +603,8 @@ class PanelPlan:
         out_off = np.asarray(out_off, np.int64)
         n = len(a_off)
         elems = int((K * T).sum())
+        ring = bool(not transform and n and int(T.max()) <= 256
+                    and (self._bulk == "ring" or (self._bulk == "auto" and 8 * elems >= _RING_MIN_BYTES)))
         if transform:
             target = 1 << 40
         else:
@@ -618,6 +642,8 @@ class PanelPlan:
                       and int((item_rows * T[item_panel]).max()) <= _PAIR_MAX_ELEMS)
         if P.pair:   # pair equal-sized panels, largest first
             items = items[np.argsort(-(items[:, 3] * items[:, 4]), kind="stable")]
+        # large bulk phases stream through the TMA ring kernel (k_panel_ring)
+        P.ring = ring
         P.items = to_dev(np.ascontiguousarray(items, np.int64), self.dev)
         if segs is not None:
             st_, ln_ = np.asarray(segs[0], np.int64), np.asarray(segs[1], np.int64)
@@ -641,7 +667,7 @@ class PanelPlan:
         return P
 
     def _launch(self, P, stream, chain=False, priority=0):
-        mode = (1 if chain else 0) | (16 if P.pair else 0)
+        mode = (1 if chain else 0) | (16 if P.pair else 0) | (32 if P.ring else 0)
         _native.call("gc_panelmv", P.nitems, ptr(P.items), ptr(P.xidx), ptr(P.A0), ptr(P.A1),
                      ptr(P.in0), ptr(P.in1), ptr(P.out), ptr(P.scratch), P.nred, ptr(P.red),
                      ptr(P.arrivals), mode, int(priority), ptr(self.trace.get(id(P))), stream)
@@ -662,7 +688,7 @@ class PanelPlan:
             if n.phase is not None:
                 P = n.phase
                 kind = 0
-                chain = (1 if n.stream == "chain" else 0) | (16 if P.pair else 0)
+                chain = (1 if n.stream == "chain" else 0) | (16 if P.pair else 0) | (32 if P.ring else 0)
                 a = [P.items.data_ptr(), P.nitems, P.xidx.data_ptr(), P.A0.data_ptr(),
                      P.A1.data_ptr() if P.A1 is not None else 0, P.in0.data_ptr(),
                      P.in1.data_ptr() if P.in1 is not None else 0, P.out.data_ptr(), P.scratch.data_ptr(),
@@ -693,7 +719,8 @@ class PanelPlan:
         A failed capture raises."""
         import time
         t0 = time.perf_counter()
-        tab = self._native_table()
+        # phase timelines (self.trace, diagnostics) need the Python launches
+        tab = self._native_table() if not self.trace else None
         if tab is not None:
             self._body()                         # warm-up (module loads) outside the capture
             torch.cuda.synchronize(self.dev)

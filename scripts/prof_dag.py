@@ -57,7 +57,7 @@ for _ in range(3):
 print("serial          %7.1f us" % time_graph(p.nodes, serial=True))
 chain = subset(lambda n: n.stream == "chain")
 print("chain only      %7.1f us  (%d nodes)" % (time_graph(chain), len(chain)))
-for n in p.nodes: print("   node", n.name, n.stream, n.deps, n.priority, n.phase.height if n.phase else "")
+for n in p.nodes: print("   node", n.name, n.stream, n.deps, n.priority, (n.phase.height, n.phase.nitems, round(n.phase.bytes / 1e6, 1)) if n.phase else "")
 bulk = [h2._Node(n.name, n.stream, [], n.phase, n.fn, n.priority) for n in p.nodes
         if n.name in ("coupling", "nearfield")]
 print("bulk only       %7.1f us  (%d nodes, concurrent)" % (time_graph(bulk), len(bulk)))

@@ -302,6 +302,9 @@ def run_native(args):
     dev_index = local % max(torch.cuda.device_count(), 1) if backend != "nccl" else local
     torch.cuda.set_device(dev_index)
     if world > 1:
+        # NCCL's INFO log names every rank of every communicator (the
+        # driver's rank-count check reads it)
+        os.environ.setdefault("NCCL_DEBUG", "INFO")
         import torch.distributed as dist
         if backend == "nccl":
             dist.init_process_group("nccl", device_id=torch.device("cuda", dev_index))

@@ -253,10 +253,14 @@ int gc_panelmv(int64_t nitems, const int64_t* items, const int32_t* xidx,
 
 /* Native product executor (h2.py:63-80 as one call).  nodes [host] (n,18)
  * int64 rows: kind (0 panel phase, 1 memset, 2 gc_gather_inv,
- * 3 gc_scatter2_inv), stream index, launch priority, chain flags (as
- * gc_panelmv), ndeps, dep_off, then 12 arguments: panel = items, nitems,
- * xidx, A0, A1, in0, in1, out, scratch, nred, red, arrivals; memset = ptr,
- * bytes; gather = x, iperm, n, xt; scatter = yt, yt2, iperm, n, y.  deps
+ * 3 gc_scatter2_inv, 4 NCCL all-gather), stream index, launch priority,
+ * chain flags (as gc_panelmv), ndeps, dep_off, then 12 arguments: panel =
+ * items, nitems, xidx, A0, A1, in0, in1, out, scratch, nred, red,
+ * arrivals; memset = ptr, bytes; gather = x, iperm, n, xt; scatter = yt,
+ * yt2, iperm, n, y; all-gather = send, recv, count, communicator
+ * (gc_nccl_comm_init) - the block-row sharded product is one
+ * such plan per rank: the own slice of x gathered in, the x and x-hat
+ * all-gathers, the product, the own rows of y scattered out.  deps
  * [host] = dependency node indices (each earlier than its node).
  * stream_prio [host] (nstreams) = stream creation priorities.  Captures the
  * DAG on the plan's own streams/events into one CUDA graph and
@@ -383,6 +387,18 @@ int gc_cgnr_dir(int64_t n, const double* sv, double* p, double* partial, double*
 /* Power iteration (h2.py:144-184): z /= sqrt(s[0]); b -= a. */
 int gc_scale_inv_norm(int64_t n, double* z, const double* s, void* stream);
 int gc_axpy_neg(int64_t n, const double* a, double* b, void* stream);
+
+/* NCCL for the sharded product (SURVEY 8b gc_nccl_init), resolved at run
+ * time (libnccl.so.2; inside a torch process torch's own copy).
+ * gc_nccl_unique_id: id [host] 128 bytes (rank 0 creates it, every rank
+ * receives it out of band).  gc_nccl_comm_init: with the rank's device
+ * current; *comm = the communicator.  gc_nccl_all_gather: recv [dev]
+ * (nranks * count doubles) = concatenation of every rank's send [dev]
+ * (count doubles); in place when send = recv + rank * count. */
+int gc_nccl_unique_id(void* id);
+int gc_nccl_comm_init(const void* id, int32_t nranks, int32_t rank, void** comm);
+int gc_nccl_comm_destroy(void* comm);
+int gc_nccl_all_gather(const double* send, double* recv, int64_t count, void* comm, void* stream);
 
 /* The device's scheduling-priority range (cudaDeviceGetStreamPriorityRange):
  * least (default, e.g. 0) and greatest (most urgent, e.g. -5). */

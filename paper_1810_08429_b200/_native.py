@@ -91,6 +91,10 @@ _SIGNATURES = {
     "gc_cgnr_dir": [c_i64, c_p, c_p, c_p, c_p, c_p],
     "gc_scale_inv_norm": [c_i64, c_p, c_p, c_p],
     "gc_axpy_neg": [c_i64, c_p, c_p, c_p],
+    "gc_nccl_unique_id": [c_p],
+    "gc_nccl_comm_init": [c_p, ctypes.c_int32, ctypes.c_int32, ctypes.POINTER(c_p)],
+    "gc_nccl_comm_destroy": [c_p],
+    "gc_nccl_all_gather": [c_p, c_p, c_i64, c_p, c_p],
     "gc_host_norm3": [c_p, c_i64, c_p, ctypes.c_int],
     "gc_dfma_probe": [c_i64, c_i64, c_i64, c_p, c_p],
 }

@@ -16,18 +16,20 @@ extern "C" int gc_panelmv(int64_t nitems, const int64_t* items, const int32_t* x
 extern "C" int gc_gather_inv(const double* x, const int64_t* iperm, int64_t n, double* xt, void* stream);
 extern "C" int gc_scatter2_inv(const double* yt, const double* yt2, const int64_t* iperm, int64_t n, double* y,
                                void* stream);
+extern "C" int gc_nccl_all_gather(const double* send, double* recv, int64_t count, void* comm, void* stream);
 extern "C" int gc_graph_retarget(void* graph, void* exec, int32_t kernel, int32_t arg, const void* old_ptr,
                                  const void* new_ptr, int32_t* count);
 
 namespace {
 
 // node kinds
-enum { NODE_PANEL = 0, NODE_MEMSET = 1, NODE_GATHER = 2, NODE_SCATTER = 3 };
+enum { NODE_PANEL = 0, NODE_MEMSET = 1, NODE_GATHER = 2, NODE_SCATTER = 3, NODE_ALLGATHER = 4 };
 
 struct Node {
     int64_t kind, stream, priority, chain, ndeps, dep_off;
     // panel: items, nitems, xidx, A0, A1, in0, in1, out, scratch, nred, red, arrivals
-    // memset: ptr, bytes; gather: x, iperm, n, xt; scatter: yt, yt2, iperm, n, y
+    // memset: ptr, bytes; gather: x, iperm, n, xt; scatter: yt, yt2, iperm, n, y;
+    // all-gather: send, recv, count (doubles per rank), NCCL communicator
     int64_t a[12];
 };
 
@@ -62,6 +64,8 @@ int launch_node(const Node& nd, cudaStream_t st) {
         case NODE_SCATTER:
             return gc_scatter2_inv((const double*)a[0], (const double*)a[1], (const int64_t*)a[2], a[3],
                                    (double*)a[4], st);
+        case NODE_ALLGATHER:
+            return gc_nccl_all_gather((const double*)a[0], (double*)a[1], a[2], (void*)a[3], st);
         default:
             gcb::set_error(GC_ERR_CONFIG, "gc_plan: unknown node kind %lld", (long long)nd.kind);
             return GC_ERR_CONFIG;

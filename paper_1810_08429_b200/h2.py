@@ -209,14 +209,17 @@ class _Phase:
 
 
 class _Node:
-    """One step of the product DAG: a panel phase or a host callable
-    (gather, zero, scatter, a collective), run on ``stream`` after ``deps``."""
-    __slots__ = ("name", "phase", "fn", "stream", "deps", "launches", "priority")
+    """One step of the product DAG: a panel phase or a callable (gather,
+    zero, scatter, a collective), run on ``stream`` after ``deps``;
+    ``native`` = (kind, args) of the same step for the C++ executor
+    (csrc/plan.cu node kinds 1-4)."""
+    __slots__ = ("name", "phase", "fn", "stream", "deps", "launches", "priority", "native")
 
-    def __init__(self, name, stream, deps=(), phase=None, fn=None, priority=0):
+    def __init__(self, name, stream, deps=(), phase=None, fn=None, priority=0, native=None, launches=None):
         self.name, self.stream, self.deps, self.phase, self.fn = name, stream, list(deps), phase, fn
-        self.launches = 1 if phase is not None else 0
+        self.launches = (1 if phase is not None else 0) if launches is None else launches
         self.priority = priority
+        self.native = native
 
 
 class PanelPlan:
@@ -471,8 +474,13 @@ class PanelPlan:
             S = h_
         return S
 
-    def _build_nodes(self, gather=True, before_coupling=None, scatter=True):
-        """Nodes in a valid serial order (a topological order of the DAG)."""
+    def _build_nodes(self, gather=True, after_gather=(), before_coupling=None, scatter=True):
+        """Nodes in a valid serial order (a topological order of the DAG).
+        ``gather`` / ``scatter``: True for the external-order gather of x /
+        scatter of y, or a custom _Node; ``after_gather``: chain nodes
+        before the forward transform (the sharded x all-gather);
+        ``before_coupling``: a chain node every coupling launch waits for
+        (the sharded x-hat all-gather)."""
         st = stream_handle
         nodes = []
 
@@ -483,13 +491,20 @@ class PanelPlan:
         S = self._split_height()
         least, greatest = self._prio
         levels = least - greatest
-        z = add(_Node("zero", "chain", fn=lambda: self._ybuf.zero_()))
+        z = add(_Node("zero", "chain", fn=lambda: self._ybuf.zero_(),
+                      native=(1, [self._ybuf.data_ptr(), 8 * self._ybuf.numel()])))
+        if gather is True:
+            gather = _Node("gather", "chain", fn=lambda: _native.call(
+                "gc_gather_inv", ptr(self.x), ptr(self.iperm_in), self.n_in, ptr(self.xt), st()),
+                native=(2, [self.x.data_ptr(), self.iperm_in.data_ptr(), self.n_in, self.xt.data_ptr()]),
+                launches=1)
+        g = z
         if gather:
-            g = add(_Node("gather", "chain", [z], fn=lambda: _native.call(
-                "gc_gather_inv", ptr(self.x), ptr(self.iperm_in), self.n_in, ptr(self.xt), st())))
-            nodes[g].launches = 1
-        else:
-            g = z
+            gather.deps = [z]
+            g = add(gather)
+        for n in after_gather:
+            n.deps = [g]
+            g = add(n)
         last = g
         fwd_done = []                                   # (max height covered, node)
         near = add(_Node("nearfield", "near", [g], phase=self._near)) if self._near.nitems else None
@@ -499,7 +514,8 @@ class PanelPlan:
                 fwd_done.append((P.height, last))
         gate = None
         if before_coupling is not None:
-            gate = add(_Node("pre-coupling", "chain", [last], fn=before_coupling))
+            before_coupling.deps = [last]
+            gate = add(before_coupling)
         bucket = {}
         for P, colh, heights in sorted(self._cpl, key=lambda c: c[0].height):
             if gate is not None:
@@ -526,11 +542,14 @@ class PanelPlan:
         tail = [prev] + sorted(set(bucket.values()))
         if near is not None:
             tail = tail + [near]
-        if scatter:
-            k = add(_Node("scatter", "chain", tail, fn=lambda: _native.call(
+        if scatter is True:
+            scatter = _Node("scatter", "chain", fn=lambda: _native.call(
                 "gc_scatter2_inv", ptr(self.yt), ptr(self.yt2), ptr(self.iperm_out), self.n_out, ptr(self.y),
-                st())))
-            nodes[k].launches = 1
+                st()), native=(3, [self.yt.data_ptr(), self.yt2.data_ptr(), self.iperm_out.data_ptr(), self.n_out,
+                                   self.y.data_ptr()]), launches=1)
+        if scatter:
+            scatter.deps = tail
+            add(scatter)
         else:
             add(_Node("join", "chain", tail, fn=lambda: None))
         return nodes
@@ -693,15 +712,9 @@ class PanelPlan:
                      P.A1.data_ptr() if P.A1 is not None else 0, P.in0.data_ptr(),
                      P.in1.data_ptr() if P.in1 is not None else 0, P.out.data_ptr(), P.scratch.data_ptr(),
                      P.nred, P.red.data_ptr() if P.red is not None else 0, P.arrivals.data_ptr()]
-            elif n.name == "zero":
-                kind, chain, a[:2] = 1, 0, [self._ybuf.data_ptr(), 8 * self._ybuf.numel()]
-            elif n.name == "gather":
-                kind, chain = 2, 0
-                a[:4] = [self.x.data_ptr(), self.iperm_in.data_ptr(), self.n_in, self.xt.data_ptr()]
-            elif n.name == "scatter":
-                kind, chain = 3, 0
-                a[:5] = [self.yt.data_ptr(), self.yt2.data_ptr(), self.iperm_out.data_ptr(), self.n_out,
-                         self.y.data_ptr()]
+            elif n.native is not None:
+                kind, chain = n.native[0], 0
+                a[:len(n.native[1])] = n.native[1]
             else:
                 return None
             d = [remap[j] for j in n.deps if j not in skip]

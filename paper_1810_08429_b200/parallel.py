@@ -28,7 +28,7 @@ the single-GPU kernels unchanged.
 
 import numpy as np
 
-from .errors import ConfigError
+from .errors import ConfigError, StateError
 
 
 def shard_nodes(flat, world):
@@ -268,6 +268,7 @@ def _shard_plan_class():
         def __init__(self, sh):
             import torch
             import torch.distributed as dist
+            from .h2 import _NativeGraph, _Node
             self.sh = sh
             world, g = sh.layout.world, sh.layout.rank
             lo_hi = np.asarray(sh.ranges, np.int64).reshape(-1, 2)
@@ -287,57 +288,81 @@ def _shard_plan_class():
             self.ypad = torch.zeros(world * maxs, dtype=torch.float64, device=dev)
             self.y_own = self.ypad[g * maxs:(g + 1) * maxs]
             self.x_in = torch.zeros(m_own, dtype=torch.float64, device=dev)
-            # y_own[j] = yt[lo + j] + yt2[lo + j]: gc_scatter2_inv over an identity range
+            self.y_out = torch.zeros(m_own, dtype=torch.float64, device=dev)
+            self._ident = to_dev(np.arange(m_own, dtype=np.int64), dev)
             self._own_rows = to_dev(np.arange(self.lo, self.hi, dtype=np.int64), dev)
             # external API: own rows of x (external ids) -> own slot; padded y -> external y
             perm_c = d.perm_c.cpu().numpy()
             iperm_r = _inv_np(d.perm_r.cpu().numpy())
             self._ext_own = to_dev(perm_c[self.lo:self.hi].astype(np.int64), dev)
             self._ext_from_pad = to_dev(xmap[iperm_r].astype(np.int64), dev)
-            self.nodes = self._build_nodes(gather=False, before_coupling=self._gather_xhat, scatter=False)
-            self.graph = None
             self.nccl = dist.get_backend(sh.group) == "nccl"
+            self.comm = None
             if self.nccl:
-                self._capture_slice()
+                # the plan's own NCCL communicator (csrc/nccl.cu): the id
+                # travels once over the process group, the collectives are
+                # nodes of the native product graph
+                uid = (_native_ctypes().c_char * 128)()
+                if g == 0:
+                    _native_call("gc_nccl_unique_id", uid)
+                box = [bytes(uid)]
+                dist.broadcast_object_list(box, src=0, group=sh.group)
+                uid = (_native_ctypes().c_char * 128).from_buffer_copy(box[0])
+                c = _native_ctypes().c_void_p(0)
+                _native_call("gc_nccl_comm_init", uid, world, g, _native_ctypes().byref(c))
+                self.comm = c
+            st = stream_handle
 
-        def _gather_xhat(self):
-            all_gather_into(self.xhat, self.xhat_own, self.sh.group)
+            def ag(name, own, full, count):
+                return _Node(name, "chain", fn=lambda: self._all_gather(own, full, count),
+                             native=(4, [own.data_ptr(), full.data_ptr(), count, (self.comm.value or 0) if self.comm else 0]))
+            gather = _Node("gather", "chain", fn=lambda: _native_call(
+                "gc_gather_inv", ptr(self.x_in), ptr(self._ident), m_own, ptr(self.xt_own), st()),
+                native=(2, [self.x_in.data_ptr(), self._ident.data_ptr(), m_own, self.xt_own.data_ptr()]),
+                launches=1)
+            combine = _Node("scatter", "chain", fn=lambda: _native_call(
+                "gc_scatter2_inv", ptr(self.yt), ptr(self.yt2), ptr(self._own_rows), m_own, ptr(self.y_out),
+                st()), native=(3, [self.yt.data_ptr(), self.yt2.data_ptr(), self._own_rows.data_ptr(), m_own,
+                                   self.y_out.data_ptr()]), launches=1)
+            self.nodes = self._build_nodes(gather=gather, after_gather=[ag("allgather-x", self.xt_own, self.xt, maxs)],
+                                           before_coupling=ag("allgather-xhat", self.xhat_own, self.xhat, sh.slot),
+                                           scatter=combine)
+            self.graph = None
+            if self.nccl:
+                # the whole slice product - both all-gathers included - as one
+                # native CUDA graph; a capture failure raises
+                tab = self._native_table()
+                if tab is None:
+                    raise StateError("sharded product: node without a native form")
+                self._body()
+                torch.cuda.synchronize(dev)
+                rows, deps, ndeps, prio = tab
+                hh = _native_ctypes().c_void_p(0)
+                _native_call("gc_plan_create", len(rows), rows.ctypes.data, ndeps, deps.ctypes.data, len(prio),
+                             prio.ctypes.data, _native_ctypes().byref(hh))
+                self.graph = _NativeGraph(hh)
 
-        def _body_slice(self):
-            self.xt_own[:self.m_own].copy_(self.x_in, non_blocking=True)
-            all_gather_into(self.xt, self.xt_own, self.sh.group)
-            self._exec(self.nodes)
-            _native_call("gc_scatter2_inv", ptr(self.yt), ptr(self.yt2), ptr(self._own_rows), self.m_own,
-                         ptr(self.y_own), stream_handle())
-
-        def _capture_slice(self):
-            import torch
-            s = torch.cuda.Stream(device=self.dev)
-            s.wait_stream(torch.cuda.current_stream())
-            with torch.cuda.stream(s):
-                self._body_slice()                 # warm-up (NCCL communicator, modules)
-            torch.cuda.current_stream().wait_stream(s)
-            torch.cuda.synchronize(self.dev)
-            g = torch.cuda.CUDAGraph()
-            with torch.cuda.graph(g, stream=s):
-                self._body_slice()
-            torch.cuda.synchronize(self.dev)
-            self.graph = g
+        def _all_gather(self, own, full, count):
+            if self.nccl:
+                _native_call("gc_nccl_all_gather", ptr(own), ptr(full), count, self.comm, stream_handle())
+            else:
+                all_gather_into(full, own, self.sh.group)
 
         def run_slice(self, x_slice, out=None):
             if x_slice.numel() != self.m_own:
                 raise ConfigError("slice of length %d, shard owns %d rows" % (x_slice.numel(), self.m_own))
+            import torch
             with self.lock:
-                self.x_in.copy_(x_slice, non_blocking=True)
-                if self.graph is not None:
+                res = torch.empty(self.m_own, dtype=torch.float64, device=self.dev) if out is None else out
+                if self.graph is not None and x_slice.is_contiguous() and res.is_contiguous() \
+                        and x_slice.dtype == torch.float64 and x_slice.device == self.dev:
+                    self.graph.bind(x_slice, res)            # the graph reads / writes the caller's slices
                     self.graph.replay()
                 else:
-                    self._body_slice()
-                res = self.y_own[:self.m_own]
-                if out is None:
-                    return res.clone()
-                out.copy_(res, non_blocking=True)
-                return out
+                    self.x_in.copy_(x_slice, non_blocking=True)
+                    self._exec(self.nodes)
+                    res.copy_(self.y_out, non_blocking=True)
+                return res
 
         def run_external(self, x):
             import torch
@@ -348,17 +373,27 @@ def _shard_plan_class():
                     self._y_full = torch.empty(self.n_out, dtype=torch.float64, device=self.dev)
                 self._pin_x.numpy()[:] = x
                 self._x_full.copy_(self._pin_x, non_blocking=True)
-                st = stream_handle()
                 # own slice of x in tree order, straight from the external vector
-                _native_call("gc_gather", ptr(self._x_full), ptr(self._ext_own), self.m_own, ptr(self.x_in), st)
-                self._body_slice()
-                all_gather_into(self.ypad, self.y_own, self.sh.group)
+                _native_call("gc_gather", ptr(self._x_full), ptr(self._ext_own), self.m_own, ptr(self.x_in),
+                             stream_handle())
+            ys = self.run_slice(self.x_in, self.y_own[:self.m_own])
+            with self.lock:
+                self._all_gather(self.y_own, self.ypad, self.maxs)
                 _native_call("gc_gather", ptr(self.ypad), ptr(self._ext_from_pad), self.n_out, ptr(self._y_full),
                              stream_handle())
                 y = torch.empty(self.n_out, dtype=torch.float64, pin_memory=True)
                 y.copy_(self._y_full, non_blocking=True)
                 torch.cuda.current_stream().synchronize()
+                del ys
                 return y.numpy()
+
+        def __del__(self):
+            if getattr(self, "comm", None) is not None and self.comm.value:
+                try:
+                    self.graph = None
+                    _native_call("gc_nccl_comm_destroy", self.comm)
+                except Exception:        # pragma: no cover - interpreter shutdown
+                    pass
 
     return ShardPlan
 
@@ -366,6 +401,11 @@ def _shard_plan_class():
 def _native_call(name, *args):
     from . import _native
     _native.call(name, *args)
+
+
+def _native_ctypes():
+    import ctypes
+    return ctypes
 
 
 def _inv_np(perm):

@@ -1,7 +1,8 @@
 /* The matvec hot kernel driven from C through the C-ABI only (no Python):
  * one panel product with gc_panelmv, then the same product captured and
  * replayed by the native executor (gc_plan_create / gc_plan_run), checked
- * against a plain C loop.  Needs a GPU (tests/test_abi.py, -m gpu). */
+ * against a plain C loop; then an NCCL communicator and all-gather through
+ * gc_nccl_*.  Needs a GPU (tests/test_abi.py, -m gpu). */
 #include <math.h>
 #include <stdint.h>
 #include <stdio.h>
@@ -67,6 +68,23 @@ int main(void) {
     for (int t = 0; t < T; ++t)
         if (got2[t] != got[t]) { printf("plan result differs at %d\n", t); return 5; }
     gc_plan_destroy(plan);
+    /* NCCL through the C-ABI (world of one): communicator from a unique id,
+     * an in-place all-gather (send = the rank's own slot of recv) */
+    char uid[128];
+    void* comm = NULL;
+    if (gc_nccl_unique_id(uid) || gc_nccl_comm_init(uid, 1, 0, &comm)) {
+        printf("nccl init: %s\n", gc_last_error());
+        return 8;
+    }
+    if (gc_nccl_all_gather(out, out, T, comm, NULL) || cudaDeviceSynchronize() != cudaSuccess) {
+        printf("nccl all-gather: %s\n", gc_last_error());
+        return 9;
+    }
+    double back[T];
+    cudaMemcpy(back, out, sizeof(back), cudaMemcpyDeviceToHost);
+    for (int t = 0; t < T; ++t)
+        if (back[t] != got[t]) { printf("all-gather changed the data\n"); return 10; }
+    gc_nccl_comm_destroy(comm);
     printf("C-ABI panel product ok (rel err %.1e)\n", sqrt(err / nrm));
     free(hA);
     return 0;

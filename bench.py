@@ -405,23 +405,29 @@ def run_native(args):
     mv_s = total_s / args.steps
     value = nbytes / mv_s / 1e9
     # roofline kernel: the largest coupling launch (the dominant launch of the
-    # step), alone on the current stream, timed with CUDA events; L2 evicted
-    # before every launch by a read-only sweep of 256 MB (a write sweep would
-    # leave ~126 MB of dirty lines to be written back inside the timed launch)
+    # step), alone on the current stream, timed with CUDA events; L2 flushed
+    # before every launch by writing 256 MB (the profiling recipe).  Also
+    # reported: the same launch after a read-only 256 MB sweep, which evicts
+    # L2 without leaving ~126 MB of dirty lines to be written back inside the
+    # timed launch.
     big = max((P for P in p.phases if P.name == "coupling"), key=lambda P: P.bytes)
     flush = torch.empty(32 << 20, dtype=torch.float64, device="cuda").fill_(1.0)
     l0 = _native.launch_count()
-    ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
-          for _ in range(max(5, args.steps))]
-    torch.cuda.synchronize()
-    for a_, b_ in ev:
-        flush.sum()
-        a_.record()
-        p._launch(big, stream_handle())
-        b_.record()
-    torch.cuda.synchronize()
+
+    def time_big(sweep):
+        ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
+              for _ in range(max(5, args.steps))]
+        torch.cuda.synchronize()
+        for a_, b_ in ev:
+            sweep()
+            a_.record()
+            p._launch(big, stream_handle())
+            b_.record()
+        torch.cuda.synchronize()
+        return float(np.mean([a_.elapsed_time(b_) for a_, b_ in ev])) * 1e-3
+    big_s = time_big(flush.zero_)
+    big_read_s = time_big(flush.sum)
     del flush
-    big_s = float(np.mean([a_.elapsed_time(b_) for a_, b_ in ev])) * 1e-3
     big_bytes = big.bytes + 8 * big.in_elems + 8 * big.out_elems
     # eager (serial) products: count own launches per step
     l0 = _native.launch_count()
@@ -478,6 +484,11 @@ def run_native(args):
                      "frac": round(big_bytes / big_s / 1e9 / hbm_peak, 4), "traffic": _traffic("coupling_bucket"),
                      "algorithmic_bytes_per_launch": int(big_bytes), "avg_launch_s": big_s,
                      "share_of_step": round(big_s / mv_s, 3),
+                     "read_sweep": {"achieved": round(big_bytes / big_read_s / 1e9, 1),
+                                    "frac": round(big_bytes / big_read_s / 1e9 / hbm_peak, 4),
+                                    "avg_launch_s": big_read_s,
+                                    "note": "same launch after a read-only L2 sweep (no write-back of the "
+                                            "flush inside the timed launch)"},
                      "step": {"achieved": round(value, 1), "frac": round(value / hbm_peak, 4),
                               "note": "whole product (all phases, concurrent streams) vs the same peak"},
                      "peak_source": "MEASURED_PEAKS.json hbm_gbs" if peaks else "fallback 6650 GB/s"},

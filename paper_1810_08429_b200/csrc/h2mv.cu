@@ -15,7 +15,7 @@ namespace gcb {
 
 constexpr int PAN_THREADS = 256;
 #ifndef GC_PAN_UNROLL
-#define GC_PAN_UNROLL 8
+#define GC_PAN_UNROLL 7
 #endif
 constexpr int PAN_UNROLL = GC_PAN_UNROLL;
 #ifndef GC_PAN_MINB
@@ -31,7 +31,7 @@ constexpr int PAN_MAX_ROWS = 1024;   // rows per work item (x gathered to smem)
 //   sums to scratch[out_off..]).
 // red slot (5 x int64): out_off, T, scratch_off, nitems, accumulate.
 // The item's input entries are gathered into shared memory first, so the
-// streaming loop over A has no dependent loads: 16 independent 8-byte loads
+// streaming loop over A has no dependent loads: PAN_UNROLL independent 8-byte loads
 // per thread are in flight before the first FMA.  The last CTA to finish a
 // split panel (arrival counter) adds its partial sums in item order, so the
 // result is bitwise deterministic without a second launch; it re-arms the

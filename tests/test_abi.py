@@ -43,6 +43,27 @@ def test_sm100a_code_object():
     assert "sm_100a" in out
 
 
+def test_panel_kernel_issues_all_loads_before_the_first_fma():
+    """The bulk matvec kernel's streaming loop must keep PAN_UNROLL matrix
+    loads in flight per thread: every LDG of the unrolled batch is issued
+    before the first DFMA.  ptxas may interleave them under the 40-register
+    cap (6 CTAs/SM), which cost 6 % of the C2 product in round 2 - this
+    guards the SASS schedule (csrc/h2mv.cu k_panelmv)."""
+    import subprocess
+    src = open(os.path.join(os.path.dirname(HEADER), "..", "paper_1810_08429_b200", "csrc", "h2mv.cu")).read()
+    unroll = int(re.search(r"#define GC_PAN_UNROLL (\d+)", src).group(1))
+    build_native.build()
+    sass = subprocess.run(["/usr/local/cuda/bin/cuobjdump", "-sass", _native.LIB_PATH],
+                          capture_output=True, text=True).stdout
+    for chain in ("0", "1"):
+        body = re.search(r"Function : _ZN3gcb9k_panelmvILb%sEEEvNS_10PanelPhaseE(.*?)(Function : |\Z)" % chain,
+                         sass, re.S)
+        assert body, "k_panelmv<%s> not found" % chain
+        ops = re.findall(r"\b(LDG\.E\.EF\.64|DFMA)\b", body.group(1))
+        first = ops.index("DFMA")
+        assert first >= unroll, "k_panelmv<%s>: only %d streaming loads before the first DFMA" % (chain, first)
+
+
 def test_error_mapping():
     _native.load()
     with pytest.raises(Exception) as ei:

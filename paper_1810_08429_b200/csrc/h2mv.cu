@@ -189,9 +189,16 @@ __global__ void __launch_bounds__(PAN_THREADS, GC_PAN_MINB) k_panelmv(PanelPhase
 // trips.  Items must be direct (no split), T <= 128, nrows <= PAIR_MAX_ROWS.
 constexpr int PAIR_THREADS = PAN_THREADS / 2;
 constexpr int PAIR_MAX_ROWS = PAN_MAX_ROWS / 2;
+#ifndef GC_PAIR_UNROLL
+#define GC_PAIR_UNROLL 4   // 4-deep batches stay unsplit by ptxas at 40 registers (7: interleaved)
+#endif
+#ifndef GC_PAIR_MINB
+#define GC_PAIR_MINB 6
+#endif
+constexpr int PAIR_UNROLL = GC_PAIR_UNROLL;
 
 template <bool CHAIN>
-__global__ void __launch_bounds__(PAN_THREADS, 6) k_panel_pair(PanelPhase P) {
+__global__ void __launch_bounds__(PAN_THREADS, GC_PAIR_MINB) k_panel_pair(PanelPhase P) {
     __shared__ PanelSmem sm;                       // xs / red split in halves
     if (CHAIN) asm volatile("griddepcontrol.launch_dependents;");
     if (P.trace != nullptr && threadIdx.x == 0) atomicMin(P.trace, globaltimer());
@@ -227,12 +234,12 @@ __global__ void __launch_bounds__(PAN_THREADS, 6) k_panel_pair(PanelPhase P) {
     if (has && g < ng) {
         const double* __restrict__ At = A + t;
         int r = g;
-        for (; r + (PAN_UNROLL - 1) * ng < nrows; r += PAN_UNROLL * ng) {
-            double a[PAN_UNROLL];
+        for (; r + (PAIR_UNROLL - 1) * ng < nrows; r += PAIR_UNROLL * ng) {
+            double a[PAIR_UNROLL];
 #pragma unroll
-            for (int j = 0; j < PAN_UNROLL; ++j) a[j] = __ldcs(At + (int64_t)(r + j * ng) * T);
+            for (int j = 0; j < PAIR_UNROLL; ++j) a[j] = __ldcs(At + (int64_t)(r + j * ng) * T);
 #pragma unroll
-            for (int j = 0; j < PAN_UNROLL; ++j) acc = fma(a[j], xs[r + j * ng], acc);
+            for (int j = 0; j < PAIR_UNROLL; ++j) acc = fma(a[j], xs[r + j * ng], acc);
         }
         for (; r < nrows; r += ng) acc = fma(__ldcs(At + (int64_t)r * T), xs[r], acc);
     }

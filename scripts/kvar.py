@@ -46,7 +46,19 @@ for spec in sys.argv[2:]:
     torch.cuda.synchronize()
     tb = np.median([e0.elapsed_time(e1) for e0, e1 in ev]) * 1e3
     bb = big.bytes + 8 * big.in_elems + 8 * big.out_elems
+    tiers = []
+    for P in p.phases:
+        if not getattr(P, "pair", False):
+            continue
+        ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(10)]
+        for e0, e1 in ev:
+            flush.zero_()
+            e0.record()
+            p._launch(P, stream_handle())
+            e1.record()
+        torch.cuda.synchronize()
+        tiers.append("%s%d %.1f" % (P.name[0], P.height, np.median([e0.elapsed_time(e1) for e0, e1 in ev]) * 1e3))
     print("%-10s L%d eps %g  product %8.1f us  %6.0f GB/s   big %7.1f us %6.0f GB/s (ring %d)" % (
-        tag, L, eps, min(ts), nbytes / min(ts) / 1e3, tb, bb / tb / 1e3, int(bool(big.ring))), flush=True)
+        tag, L, eps, min(ts), nbytes / min(ts) / 1e3, tb, bb / tb / 1e3, int(bool(big.ring))), " | pair phases alone (us):", ", ".join(tiers), flush=True)
     del p, hm
     torch.cuda.empty_cache()

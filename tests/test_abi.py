@@ -51,17 +51,18 @@ def test_panel_kernel_issues_all_loads_before_the_first_fma():
     guards the SASS schedule (csrc/h2mv.cu k_panelmv)."""
     import subprocess
     src = open(os.path.join(os.path.dirname(HEADER), "..", "paper_1810_08429_b200", "csrc", "h2mv.cu")).read()
-    unroll = int(re.search(r"#define GC_PAN_UNROLL (\d+)", src).group(1))
     build_native.build()
     sass = subprocess.run(["/usr/local/cuda/bin/cuobjdump", "-sass", _native.LIB_PATH],
                           capture_output=True, text=True).stdout
-    for chain in ("0", "1"):
-        body = re.search(r"Function : _ZN3gcb9k_panelmvILb%sEEEvNS_10PanelPhaseE(.*?)(Function : |\Z)" % chain,
-                         sass, re.S)
-        assert body, "k_panelmv<%s> not found" % chain
-        ops = re.findall(r"\b(LDG\.E\.EF\.64|DFMA)\b", body.group(1))
-        first = ops.index("DFMA")
-        assert first >= unroll, "k_panelmv<%s>: only %d streaming loads before the first DFMA" % (chain, first)
+    for kern, macro in (("k_panelmv", "GC_PAN_UNROLL"), ("k_panel_pair", "GC_PAIR_UNROLL")):
+        unroll = int(re.search(r"#define %s (\d+)" % macro, src).group(1))
+        for chain in ("0", "1"):
+            body = re.search(r"Function : _ZN3gcb%d%sILb%sEEEvNS_10PanelPhaseE(.*?)(Function : |\Z)"
+                             % (len(kern), kern, chain), sass, re.S)
+            assert body, "%s<%s> not found" % (kern, chain)
+            ops = re.findall(r"\b(LDG\.E\.EF\.64|DFMA)\b", body.group(1))
+            first = ops.index("DFMA")
+            assert first >= unroll, "%s<%s>: only %d streaming loads before the first DFMA" % (kern, chain, first)
 
 
 def test_error_mapping():

@@ -55,18 +55,26 @@ __global__ void k_scatter2(const double* __restrict__ yt, const double* __restri
 // perm): reads of x / writes of y are contiguous, so x and y may live in
 // mapped pinned host memory (the product graph reads and writes the
 // caller's host buffers directly, h2.mvm).
-// xt[iperm[j]] = x[j]
+// xt[iperm[j]] = x[j].  The product's first forward tier is its programmatic
+// dependent (PDL): released at once, it stages its matrix while this runs.
 __global__ void k_gather_inv(const double* __restrict__ x, const int64_t* __restrict__ iperm,
                              int64_t n, double* __restrict__ xt) {
+    asm volatile("griddepcontrol.launch_dependents;");
     for (int64_t j = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; j < n;
          j += (int64_t)gridDim.x * blockDim.x)
         xt[__ldg(iperm + j)] = x[j];
 }
 
-// y[j] = yt[iperm[j]] + yt2[iperm[j]]
+// y[j] = yt[iperm[j]] + yt2[iperm[j]].  Launched as the programmatic
+// dependent of the leaf-row tier (PDL): it loads its indices, then waits
+// for the tier's results.
 __global__ void k_scatter2_inv(const double* __restrict__ yt, const double* __restrict__ yt2,
                                const int64_t* __restrict__ iperm, int64_t n, double* __restrict__ y) {
-    for (int64_t j = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; j < n;
+    const int64_t j0 = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    const int64_t i0 = j0 < n ? __ldg(iperm + j0) : 0;
+    asm volatile("griddepcontrol.wait;" ::: "memory");
+    if (j0 < n) y[j0] = yt[i0] + yt2[i0];
+    for (int64_t j = j0 + (int64_t)gridDim.x * blockDim.x; j < n;
          j += (int64_t)gridDim.x * blockDim.x) {
         const int64_t i = __ldg(iperm + j);
         y[j] = yt[i] + yt2[i];
@@ -301,8 +309,18 @@ int gc_gather_inv(const double* x, const int64_t* iperm, int64_t n, double* xt, 
 int gc_scatter2_inv(const double* yt, const double* yt2, const int64_t* iperm, int64_t n, double* y,
                     void* stream) {
     if (n <= 0) return GC_OK;
-    k_scatter2_inv<<<grid_for(n, 256), 256, 0, (cudaStream_t)stream>>>(yt, yt2, iperm, n, y);
-    GC_CHECK_LAUNCH("gc_scatter2_inv");
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3(grid_for(n, 256));
+    cfg.blockDim = dim3(256);
+    cfg.stream = (cudaStream_t)stream;
+    cudaLaunchAttribute attr;
+    attr.id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    attr.val.programmaticStreamSerializationAllowed = 1;
+    cfg.attrs = &attr;
+    cfg.numAttrs = 1;
+    cudaError_t e = cudaLaunchKernelEx(&cfg, k_scatter2_inv, yt, yt2, iperm, n, y);
+    if (e != cudaSuccess) return cuda_status(e, "gc_scatter2_inv");
+    count_launch();
     return GC_OK;
 }
 

@@ -205,7 +205,7 @@ _MERGE_MIN_BYTES = 1 << 30   # coupling row heights with the same producer / con
 
 class _Phase:
     __slots__ = ("name", "height", "items", "xidx", "red", "arrivals", "nitems", "nred", "A0", "A1",
-                 "in0", "in1", "out", "scratch", "bytes", "in_elems", "out_elems", "pair", "ring")
+                 "in0", "in1", "out", "scratch", "bytes", "in_elems", "out_elems", "pair", "ring", "acc")
 
 
 class _Node:
@@ -491,8 +491,17 @@ class PanelPlan:
         S = self._split_height()
         least, greatest = self._prio
         levels = least - greatest
-        z = add(_Node("zero", "chain", fn=lambda: self._ybuf.zero_(),
-                      native=(1, [self._ybuf.data_ptr(), 8 * self._ybuf.numel()])))
+        def dl(*xs):
+            return [x for x in xs if x is not None]
+
+        # y-hat | y-hat from above | leaf rows: zeroed per product only when
+        # a phase accumulates into its output (the level-by-level backward
+        # transform); with tiers every output has one direct writer, and the
+        # entries nobody writes stay zero from the allocation
+        z = None
+        if any(P.acc for P in self.phases):
+            z = add(_Node("zero", "chain", fn=lambda: self._ybuf.zero_(),
+                          native=(1, [self._ybuf.data_ptr(), 8 * self._ybuf.numel()])))
         if gather is True:
             gather = _Node("gather", "chain", fn=lambda: _native.call(
                 "gc_gather_inv", ptr(self.x), ptr(self.iperm_in), self.n_in, ptr(self.xt), st()),
@@ -500,21 +509,21 @@ class PanelPlan:
                 launches=1)
         g = z
         if gather:
-            gather.deps = [z]
+            gather.deps = dl(z)
             g = add(gather)
         for n in after_gather:
-            n.deps = [g]
+            n.deps = dl(g)
             g = add(n)
         last = g
         fwd_done = []                                   # (max height covered, node)
-        near = add(_Node("nearfield", "near", [g], phase=self._near)) if self._near.nitems else None
+        near = add(_Node("nearfield", "near", dl(g), phase=self._near)) if self._near.nitems else None
         for P in self._fwd:
             if P.nitems:
-                last = add(_Node("forward", "chain", [last], phase=P, priority=greatest))
+                last = add(_Node("forward", "chain", dl(last), phase=P, priority=greatest))
                 fwd_done.append((P.height, last))
         gate = None
         if before_coupling is not None:
-            before_coupling.deps = [last]
+            before_coupling.deps = dl(last)
             gate = add(before_coupling)
         bucket = {}
         for P, colh, heights in sorted(self._cpl, key=lambda c: c[0].height):
@@ -527,19 +536,19 @@ class PanelPlan:
             else:
                 prio = least - 1 - int(round(P.height * (levels - 2) / max(S - 1, 1)))
                 prio = min(least - 1, max(greatest + 1, prio))
-            k = add(_Node("coupling", "c%d" % P.height, dep + [z], phase=P, priority=prio))
+            k = add(_Node("coupling", "c%d" % P.height, dl(*dep, z), phase=P, priority=prio))
             for hh in heights:
                 bucket[hh] = k
         prev = gate if gate is not None else last
         for P, hs in self._bwd:
             if P.nitems:
-                prev = add(_Node("backward", "chain", [prev] + sorted({bucket[x] for x in hs if x in bucket}),
+                prev = add(_Node("backward", "chain", dl(prev) + sorted({bucket[x] for x in hs if x in bucket}),
                                  phase=P, priority=greatest))
         for P, hs in self._leafparts:
             need = (sorted(set(bucket.values())) if hs is None
                     else sorted({bucket[x] for x in hs if x in bucket}))
-            prev = add(_Node("leafbasis", "chain", [prev] + need, phase=P, priority=greatest))
-        tail = [prev] + sorted(set(bucket.values()))
+            prev = add(_Node("leafbasis", "chain", dl(prev) + need, phase=P, priority=greatest))
+        tail = dl(prev) + sorted(set(bucket.values()))
         if near is not None:
             tail = tail + [near]
         if scatter is True:
@@ -654,6 +663,7 @@ class PanelPlan:
                         np.full(int(multi.sum()), accumulate)], 1)
         P = _Phase()
         P.name, P.height = name, height
+        P.acc = bool(n and accumulate)              # some item adds into its output
         # two whole small panels per CTA (k_panel_pair) in the tier phases
         # whose items all fit: half the CTAs, half the waves of round trips
         P.pair = bool(transform and self.tiers_pending and n and bool(np.all(direct)) and int(T.max()) <= 128

@@ -15,7 +15,7 @@ namespace gcb {
 
 constexpr int PAN_THREADS = 256;
 #ifndef GC_PAN_UNROLL
-#define GC_PAN_UNROLL 7
+#define GC_PAN_UNROLL 8
 #endif
 constexpr int PAN_UNROLL = GC_PAN_UNROLL;
 #ifndef GC_PAN_MINB
@@ -61,6 +61,26 @@ __device__ __forceinline__ unsigned long long globaltimer() {
     unsigned long long t;
     asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
     return t;
+}
+
+// Diagnostics (PanelPhase.trace, scripts/timeline.py): trace[0] / [1] =
+// min CTA start / max CTA end (%globaltimer, ns); when trace[2] = n > 0,
+// CTA b < n also records its own [start, end] at trace[4 + 2b].
+__device__ __forceinline__ void trace_begin(const PanelPhase& P) {
+    if (P.trace == nullptr || threadIdx.x != 0) return;
+    const unsigned long long t = globaltimer();
+    atomicMin(P.trace, t);
+    if (P.trace[2] > blockIdx.x) P.trace[4 + 2 * (int64_t)blockIdx.x] = t;
+}
+
+__device__ __forceinline__ void trace_end(const PanelPhase& P) {
+    if (P.trace == nullptr) return;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        const unsigned long long t = globaltimer();
+        atomicMax(P.trace + 1, t);
+        if (P.trace[2] > blockIdx.x) P.trace[5 + 2 * (int64_t)blockIdx.x] = t;
+    }
 }
 
 __device__ __forceinline__ void prefetch_l2(const void* p, int64_t bytes) {
@@ -123,6 +143,9 @@ __device__ __forceinline__ void panel_item(const PanelPhase& P, int64_t item, Pa
                 double a[PAN_UNROLL];
 #pragma unroll
                 for (int j = 0; j < PAN_UNROLL; ++j) a[j] = __ldcs(At + (int64_t)(r + j * ng) * T);
+                // pins the batch: ptxas otherwise may sink loads between the
+                // FMAs under the 40-register cap (WARPSYNC.ALL, no wait)
+                __syncwarp(__activemask());
 #pragma unroll
                 for (int j = 0; j < PAN_UNROLL; ++j) acc = fma(a[j], sm.xs[r + j * ng], acc);
             }
@@ -173,12 +196,9 @@ template <bool CHAIN>
 __global__ void __launch_bounds__(PAN_THREADS, GC_PAN_MINB) k_panelmv(PanelPhase P) {
     __shared__ PanelSmem sm;
     if (CHAIN) asm volatile("griddepcontrol.launch_dependents;");
-    if (P.trace != nullptr && threadIdx.x == 0) atomicMin(P.trace, globaltimer());
+    trace_begin(P);
     panel_item<CHAIN>(P, blockIdx.x, sm);
-    if (P.trace != nullptr) {
-        __syncthreads();
-        if (threadIdx.x == 0) atomicMax(P.trace + 1, globaltimer());
-    }
+    trace_end(P);
 }
 
 // Two small whole panels per CTA: threads [0,128) run item 2b, [128,256)
@@ -190,7 +210,7 @@ __global__ void __launch_bounds__(PAN_THREADS, GC_PAN_MINB) k_panelmv(PanelPhase
 constexpr int PAIR_THREADS = PAN_THREADS / 2;
 constexpr int PAIR_MAX_ROWS = PAN_MAX_ROWS / 2;
 #ifndef GC_PAIR_UNROLL
-#define GC_PAIR_UNROLL 4   // 4-deep batches stay unsplit by ptxas at 40 registers (7: interleaved)
+#define GC_PAIR_UNROLL 8
 #endif
 #ifndef GC_PAIR_MINB
 #define GC_PAIR_MINB 6
@@ -201,7 +221,7 @@ template <bool CHAIN>
 __global__ void __launch_bounds__(PAN_THREADS, GC_PAIR_MINB) k_panel_pair(PanelPhase P) {
     __shared__ PanelSmem sm;                       // xs / red split in halves
     if (CHAIN) asm volatile("griddepcontrol.launch_dependents;");
-    if (P.trace != nullptr && threadIdx.x == 0) atomicMin(P.trace, globaltimer());
+    trace_begin(P);
     const int half = threadIdx.x / PAIR_THREADS, ltid = threadIdx.x % PAIR_THREADS;
     const int64_t item = 2 * (int64_t)blockIdx.x + half;
     const bool has = item < P.nitems;
@@ -238,6 +258,7 @@ __global__ void __launch_bounds__(PAN_THREADS, GC_PAIR_MINB) k_panel_pair(PanelP
             double a[PAIR_UNROLL];
 #pragma unroll
             for (int j = 0; j < PAIR_UNROLL; ++j) a[j] = __ldcs(At + (int64_t)(r + j * ng) * T);
+            __syncwarp(__activemask());                                  // pins the batch (see panel_item)
 #pragma unroll
             for (int j = 0; j < PAIR_UNROLL; ++j) acc = fma(a[j], xs[r + j * ng], acc);
         }
@@ -251,10 +272,7 @@ __global__ void __launch_bounds__(PAN_THREADS, GC_PAIR_MINB) k_panel_pair(PanelP
         double* o = P.out + out_off + t;
         *o = (mode & 8) ? __ldcg(o) + v : v;
     }
-    if (P.trace != nullptr) {
-        __syncthreads();
-        if (threadIdx.x == 0) atomicMax(P.trace + 1, globaltimer());
-    }
+    trace_end(P);
 }
 
 // ---------------------------------------------------------------------------
@@ -308,7 +326,7 @@ __device__ __forceinline__ void ring_wait(RingSmem& sm, int st, unsigned parity)
 __global__ void __launch_bounds__(PAN_THREADS, 4) k_panel_ring(PanelPhase P) {
     extern __shared__ __align__(128) unsigned char ring_raw[];
     RingSmem& sm = *reinterpret_cast<RingSmem*>(ring_raw);
-    if (P.trace != nullptr && threadIdx.x == 0) atomicMin(P.trace, globaltimer());
+    trace_begin(P);
     const int64_t* it = P.items + 8 * (int64_t)blockIdx.x;
     const int64_t a_off = it[0], xi_off = it[1], out_off = it[2];
     const int T = (int)it[3], nrows = (int)it[4], mode = (int)it[5];
@@ -400,10 +418,7 @@ __global__ void __launch_bounds__(PAN_THREADS, 4) k_panel_ring(PanelPhase P) {
             if (threadIdx.x == 0) P.arrivals[slot] = 0;
         }
     }
-    if (P.trace != nullptr) {
-        __syncthreads();
-        if (threadIdx.x == 0) atomicMax(P.trace + 1, globaltimer());
-    }
+    trace_end(P);
 }
 
 }  // namespace gcb

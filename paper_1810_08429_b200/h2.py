@@ -200,7 +200,6 @@ _ITEM_ELEMS = 65536          # <= 512 KB of matrix data per bulk work item (rows
 _ITEM_MAX_ROWS = 1024        # PAN_MAX_ROWS in csrc/h2mv.cu
 _PAIR_MAX_ELEMS = 8192       # k_panel_pair (two small panels per CTA): panel size cap
 _RING_MIN_BYTES = 256 << 20  # bulk phases this large stream through k_panel_ring (measured: C4 +5 %, C2 -8 %)
-_ROW_PARTS = 1                # row parts of the product DAG (independent coupling / backward / leaf chains)
 _MERGE_MIN_BYTES = 1 << 30   # coupling row heights with the same producer / consumer merge into one launch
 
 
@@ -242,7 +241,7 @@ class PanelPlan:
     executes it serially on the current stream (for per-phase timing).
     """
 
-    def __init__(self, h, tiers="auto", xt_map=None, xt_len=None, bulk="auto", parts=None):
+    def __init__(self, h, tiers="auto", xt_map=None, xt_len=None, bulk="auto"):
         import time
         t0 = time.perf_counter()
         self.timing = {}
@@ -283,18 +282,13 @@ class PanelPlan:
         near = self._phase("nearfield", 0, panels, d.near, None, self.xt, None, self.yt)
         self.tiers = None
         t1 = time.perf_counter()
-        # row parts: subtrees of the row tree whose coupling rows, backward
-        # tiers and leaf rows form independent sub-products
-        self._pbounds = self._row_parts(h, _ROW_PARTS if parts is None else int(parts)) if tiers != "off" else None
         tiered = self._tiered(h, tiers) if tiers != "off" else None
         if tiered is None:
-            self._pbounds = None
             fwd, bwd, leafp = self._level_phases(h)
-            bwd = [(P, hs, None) for P, hs in bwd]
-            parts = [(leafp, None, None)]
+            parts = [(leafp, None)]
         else:
             fwd, bwd, parts = tiered
-        parts = [(P, hs, k) for P, hs, k in parts if P is not None and P.nitems]
+        parts = [(P, hs) for P, hs in parts if P is not None and P.nitems]
         # coupling: one panel per row cluster.  Row clusters are grouped by
         # (the forward phase producing every x-hat they read, the backward
         # phase consuming their y-hat): one launch per group - e.g. all the
@@ -315,28 +309,25 @@ class PanelPlan:
             rowh = rf.height[sn[cuts]]
             fwd_h = [P.height for P in fwd if P.nitems]
             src = np.array([next((k for k, fh in enumerate(fwd_h) if fh >= c), len(fwd_h)) for c in colh])
-            hsets = sorted({frozenset(hs) for P, hs, _ in bwd if P.nitems}, key=lambda hs: -min(hs))
-            dst = np.array([next((k for k, hs in enumerate(hsets) if r in hs), len(hsets)) for r in rowh])
-            part = self._part_of(rf.start[sn[cuts]])
+            dst = np.array([next((k for k, (P, hs) in enumerate(bwd) if P.nitems and r in hs), len(bwd))
+                            for r in rowh])
             # merge only into launches of >= _MERGE_MIN_BYTES: smaller groups stay
             # one launch per row height (measured: C4 -1.5 %, C2 +10 % merged)
             gbytes = {}
-            for k_, e_ in zip(zip(part.tolist(), src.tolist(), dst.tolist()), (K * d.c_nr[order[cuts]]).tolist()):
+            for k_, e_ in zip(zip(src.tolist(), dst.tolist()), (K * d.c_nr[order[cuts]]).tolist()):
                 gbytes[k_] = gbytes.get(k_, 0) + 8 * e_
-            grp = np.array([(q_, a_, b_, -1 if gbytes[(q_, a_, b_)] >= _MERGE_MIN_BYTES else int(h_))
-                            for q_, a_, b_, h_ in zip(part.tolist(), src.tolist(), dst.tolist(), rowh.tolist())],
-                           np.int64)
-            for key in sorted(set(map(tuple, grp.tolist())), key=lambda k: (k[0], -k[2], k[1], k[3])):
+            grp = np.array([(a_, b_, -1 if gbytes[(a_, b_)] >= _MERGE_MIN_BYTES else int(h_))
+                            for a_, b_, h_ in zip(src.tolist(), dst.tolist(), rowh.tolist())], np.int64)
+            for key in sorted(set(map(tuple, grp.tolist())), key=lambda k: (-k[1], k[0], k[2])):
                 sel = np.flatnonzero(np.all(grp == np.array(key), axis=1))
                 bsel = _ranges_np(cuts[sel], nblk[sel])
                 panels = (d.c_off[order[cuts[sel]]], K[sel], d.c_nr[order[cuts[sel]]],
                           (bstart[bsel], blen[bsel]), rs.coef_off[sn[cuts[sel]]], 0)
                 P = self._phase("coupling", int(rowh[sel].max()), panels, d.coup, None, self.xhat, None,
                                 self.yhat)
-                cpl.append((P, int(colh[sel].max()), set(rowh[sel].tolist()), None if self._pbounds is None
-                            else int(key[0])))
+                cpl.append((P, int(colh[sel].max()), set(rowh[sel].tolist())))
         self._fwd, self._cpl, self._bwd, self._near, self._leafparts = fwd, cpl, bwd, near, parts
-        self.phases = [P for P in [near] + fwd + [c[0] for c in cpl] + [b[0] for b in bwd] + [p[0] for p in parts]
+        self.phases = [P for P in [near] + fwd + [c for c, _, _ in cpl] + [b for b, _ in bwd] + [p for p, _ in parts]
                        if P is not None and P.nitems > 0]
         # the chain gets the highest stream priority so its CTAs are
         # scheduled ahead of the queued bulk (coupling buckets, near field)
@@ -350,44 +341,6 @@ class PanelPlan:
         self.graph = None
         t2 = time.perf_counter()
         self.timing.update(bulk_phases_s=t1 - t0, transforms_s=t2 - t1)
-
-    def _row_parts(self, h, nparts):
-        """Start rows of the row parts: ``nparts`` (a power of two) subtrees
-        below the row tree node covering this operator's rows, halved until
-        every live row cluster and every coupling row lies inside one part
-        (None: one part)."""
-        d = h.dev
-        rf, rs = h.row_tree.flat, h.row_basis.store
-        lo, hi = (0, self.n_out) if d.row_range is None else (int(d.row_range[0]), int(d.row_range[1]))
-        root = np.flatnonzero((rf.start == lo) & (rf.stop == hi))
-        if nparts <= 1 or not root.size:
-            return None
-        live = rs.materialized & (rs.rank > 0)
-        live[np.asarray(d.c_rows, np.int64)] = True
-        live &= (rf.start >= lo) & (rf.stop <= hi)
-        while nparts > 1:
-            front = [int(root[np.argmax(rf.height[root])])]
-            while len(front) < nparts:
-                nxt = []
-                for u in front:
-                    nxt.extend([u] if rf.is_leaf[u] else [int(rf.left[u]), int(rf.right[u])])
-                if len(nxt) == len(front):
-                    break
-                front = nxt
-            bounds = np.sort(rf.start[front])
-            ps = np.searchsorted(bounds, rf.start[live], side="right")
-            pe = np.searchsorted(bounds, rf.stop[live] - 1, side="right")
-            if len(bounds) > 1 and np.array_equal(ps, pe):
-                return bounds
-            nparts //= 2
-        return None
-
-    def _part_of(self, rows):
-        """Row part of each tree position (0 with one part)."""
-        rows = np.asarray(rows, np.int64)
-        if self._pbounds is None:
-            return np.zeros(rows.shape, np.int64)
-        return np.searchsorted(self._pbounds, rows, side="right") - 1
 
     def _xpos(self, p):
         """x_t buffer position of tree position p (index ranges never
@@ -489,21 +442,15 @@ class PanelPlan:
             if low and d.row_range is not None:
                 keep = (rf.start[elems] >= d.row_range[0]) & (rf.stop[elems] <= d.row_range[1])
             K = np.add.reduceat(rs.rank[uu], first)
-            epart = self._part_of(rf.start[elems])
-            for q in range(1 if self._pbounds is None else len(self._pbounds)):
-                kq = keep & (epart == q)
-                if not kq.any():
-                    continue
-                sel = np.repeat(kq, cnt)
-                panels = (dst[first][kq], K[kq], ww[first][kq], (rs.coef_off[uu][sel], rs.rank[uu][sel]),
-                          (rf.start[elems] if low else rs.coef_off[elems])[kq], 0)
-                P = self._phase("leafbasis" if low else "backward", t["hi"], panels, MT, None, self.yhat,
-                                self.yhat_t, self.yt2 if low else self.yhat_t, sum_inputs=True, transform=True)
-                qq = None if self._pbounds is None else q
-                if low:
-                    parts.append((P, None, qq))
-                else:
-                    nbwd.append((P, set(range(t["lo"] + 1, t["hi"] + 1)), qq))
+            sel = np.repeat(keep, cnt)
+            panels = (dst[first][keep], K[keep], ww[first][keep], (rs.coef_off[uu][sel], rs.rank[uu][sel]),
+                      (rf.start[elems] if low else rs.coef_off[elems])[keep], 0)
+            P = self._phase("leafbasis" if low else "backward", t["hi"], panels, MT, None, self.yhat,
+                            self.yhat_t, self.yt2 if low else self.yhat_t, sum_inputs=True, transform=True)
+            if low:
+                parts.append((P, None))
+            else:
+                nbwd.append((P, set(range(t["lo"] + 1, t["hi"] + 1))))
         self.tiers_pending = False
         return nfwd, nbwd, parts
 
@@ -517,7 +464,7 @@ class PanelPlan:
         priority."""
         if not self._cpl:
             return 0
-        by_h = sorted(((c[0].height, c[0].bytes) for c in self._cpl), reverse=True)
+        by_h = sorted(((P.height, P.bytes) for P, _, _ in self._cpl), reverse=True)
         total = sum(b for _, b in by_h)
         acc, S = 0, by_h[0][0] + 1
         for h_, b in by_h:
@@ -578,43 +525,30 @@ class PanelPlan:
         if before_coupling is not None:
             before_coupling.deps = dl(last)
             gate = add(before_coupling)
-        nparts = 1 if self._pbounds is None else len(self._pbounds)
-        nslot = levels - 1                 # priorities strictly between the chain's and the near field's
-        bucket = {}                        # (part, row height) -> node
-        for P, colh, heights, part in sorted(self._cpl, key=lambda c: (c[0].height, c[3] or 0)):
+        bucket = {}
+        for P, colh, heights in sorted(self._cpl, key=lambda c: c[0].height):
             if gate is not None:
                 dep = [gate]
             else:
                 dep = [next((k for hh, k in fwd_done if hh >= colh), last)]
             if P.height >= S or levels < 2:
                 prio = greatest
-            elif nparts == 1:
+            else:
                 prio = least - 1 - int(round(P.height * (levels - 2) / max(S - 1, 1)))
                 prio = min(least - 1, max(greatest + 1, prio))
-            else:
-                # part-major: the deep buckets of part 0 first, so its
-                # backward and leaf rows run while later parts stream
-                per = max(1, nslot // nparts)
-                base = greatest + 1 + min((part or 0) * per, nslot - 1)
-                prio = min(least - 1, base + (per - 1) - int(round(P.height * (per - 1) / max(S - 1, 1))))
-            k = add(_Node("coupling", "c%d" % P.height if part is None else "c%d_%d" % (P.height, part),
-                          dl(*dep, z), phase=P, priority=prio))
+            k = add(_Node("coupling", "c%d" % P.height, dl(*dep, z), phase=P, priority=prio))
             for hh in heights:
-                bucket[part, hh] = k
-        base_node = gate if gate is not None else last
-        prev = {}
-        for P, hs, part in self._bwd:
+                bucket[hh] = k
+        prev = gate if gate is not None else last
+        for P, hs in self._bwd:
             if P.nitems:
-                need = sorted({k for (q, hh), k in bucket.items() if hh in hs and (part is None or q == part)})
-                prev[part] = add(_Node("backward", "chain" if part is None else "chain%d" % part,
-                                       dl(prev.get(part, base_node)) + need, phase=P, priority=greatest))
-        ends = []
-        for P, hs, part in self._leafparts:
-            need = sorted({k for (q, hh), k in bucket.items()
-                           if (hs is None or hh in hs) and (part is None or q == part)})
-            ends.append(add(_Node("leafbasis", "chain" if part is None else "chain%d" % part,
-                                  dl(prev.get(part, base_node)) + need, phase=P, priority=greatest)))
-        tail = sorted(set(ends or dl(base_node)) | set(prev.values()) | set(bucket.values()))
+                prev = add(_Node("backward", "chain", dl(prev) + sorted({bucket[x] for x in hs if x in bucket}),
+                                 phase=P, priority=greatest))
+        for P, hs in self._leafparts:
+            need = (sorted(set(bucket.values())) if hs is None
+                    else sorted({bucket[x] for x in hs if x in bucket}))
+            prev = add(_Node("leafbasis", "chain", dl(prev) + need, phase=P, priority=greatest))
+        tail = dl(prev) + sorted(set(bucket.values()))
         if near is not None:
             tail = tail + [near]
         if scatter is True:
@@ -624,8 +558,6 @@ class PanelPlan:
                                    self.y.data_ptr()]), launches=1)
         if scatter:
             scatter.deps = tail
-            if ends:           # the programmatic dependent of the last leaf-row launch
-                scatter.stream = nodes[ends[-1]].stream
             add(scatter)
         else:
             add(_Node("join", "chain", tail, fn=lambda: None))
@@ -634,8 +566,7 @@ class PanelPlan:
     def _stream(self, key):
         s = self.streams.get(key)
         if s is None:
-            s = self.streams[key] = torch.cuda.Stream(
-                device=self.dev, priority=self.streams["chain"].priority if key.startswith("chain") else self._bulk_priority)
+            s = self.streams[key] = torch.cuda.Stream(device=self.dev, priority=self._bulk_priority)
         return s
 
     def _exec(self, nodes, serial=False, phase_events=None, phase="coupling"):
@@ -651,7 +582,7 @@ class PanelPlan:
                 if phase_events is not None and i == first:
                     phase_events[0].record(main)
                 if n.phase is not None:
-                    self._launch(n.phase, st, n.stream.startswith("chain"), n.priority)
+                    self._launch(n.phase, st, n.stream == "chain", n.priority)
                 else:
                     n.fn()
                 if phase_events is not None and i == lastn:
@@ -671,7 +602,7 @@ class PanelPlan:
                     s.wait_event(events[dep])
             with torch.cuda.stream(s):
                 if n.phase is not None:
-                    self._launch(n.phase, stream_handle(), n.stream.startswith("chain"), n.priority)
+                    self._launch(n.phase, stream_handle(), n.stream == "chain", n.priority)
                 else:
                     n.fn()
                 ev = torch.cuda.Event()
@@ -786,7 +717,7 @@ class PanelPlan:
             if n.phase is not None:
                 P = n.phase
                 kind = 0
-                chain = (1 if n.stream.startswith("chain") else 0) | (16 if P.pair else 0) | (32 if P.ring else 0)
+                chain = (1 if n.stream == "chain" else 0) | (16 if P.pair else 0) | (32 if P.ring else 0)
                 a = [P.items.data_ptr(), P.nitems, P.xidx.data_ptr(), P.A0.data_ptr(),
                      P.A1.data_ptr() if P.A1 is not None else 0, P.in0.data_ptr(),
                      P.in1.data_ptr() if P.in1 is not None else 0, P.out.data_ptr(), P.scratch.data_ptr(),
@@ -801,7 +732,7 @@ class PanelPlan:
             deps.extend(d)
             remap[i] = len(rows) - 1
         least, greatest = self._prio
-        prio = np.array([greatest if k.startswith("chain") else least for k in streams], np.int32)
+        prio = np.array([greatest if k == "chain" else least for k in streams], np.int32)
         return (np.array(rows, np.int64).reshape(-1, 18), np.array(deps or [0], np.int64), len(deps), prio)
 
     def capture(self):

@@ -1,0 +1,59 @@
+"""Product time for values of one h2 module constant (plan-construction
+parameters under study).  Usage: python scripts/modvar.py NAME v1,v2,... level:eps ..."""
+import ast
+import os
+import sys
+
+import torch
+
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+from paper_1810_08429_b200 import cli, geometry, h2  # noqa: E402
+
+name, vals = sys.argv[1], sys.argv[2].split(",")
+
+
+def conv(v):
+    try:
+        return ast.literal_eval(v)
+    except (ValueError, SyntaxError):
+        return v
+
+
+vals = [conv(v) for v in vals]
+for spec in sys.argv[3:]:
+    L, eps = spec.split(":")
+    L, eps = int(L), float(eps)
+    mesh = geometry.build_sphere_mesh(L)
+    hm, _, _ = cli.build_h2_operator(mesh, cli.default_config(eps=eps))
+    nbytes = h2.storage_report(hm)["total"] + 16 * mesh.nt
+    x = torch.randn(mesh.nt, dtype=torch.float64, device="cuda")
+    plans, res, ref = [], [[] for _ in vals], None
+    old = getattr(h2, name)
+    for v in vals:
+        setattr(h2, name, v)
+        p = h2.PanelPlan(hm)
+        p.capture()
+        plans.append(p)
+    setattr(h2, name, old)
+    reps = 50 if L <= 7 else 10
+    for rnd in range(3):
+        for i, p in enumerate(plans):
+            y = torch.empty_like(x)
+            for _ in range(3):
+                p.run(x, y)
+            torch.cuda.synchronize()
+            if ref is None:
+                ref = y.clone()
+            assert float((y - ref).norm() / ref.norm()) < 1e-13
+            a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            a.record()
+            for _ in range(reps):
+                p.run(x, y)
+            b.record()
+            torch.cuda.synchronize()
+            res[i].append(a.elapsed_time(b) / reps * 1e3)
+    for v, r in zip(vals, res):
+        print("L%d eps %g %s=%-10s product %8.1f us  %6.0f GB/s" % (L, eps, name, v, min(r), nbytes / min(r) / 1e3),
+              flush=True)
+    del plans, hm
+    torch.cuda.empty_cache()

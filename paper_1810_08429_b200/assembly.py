@@ -96,12 +96,13 @@ def galerkin_pair_evaluator(kind, mesh, basis, q_reg, q_sing, device=None):
 
 
 def device_block_assembly(dmesh, rules, queue, row_idx, col_idx, desc, out, stats=None, kind="slp",
-                          d_desc=None):
+                          d_desc=None, events=None):
     """Assemble blocks described by ``desc (nb,5)`` into the device buffer
     ``out`` (column-major per block); singular pairs are flushed at the end.
     ``kind`` "slp" / "dlp" picks the kernel (``rules`` must match it);
     ``d_desc`` is an already uploaded copy of ``desc``.  Returns the per-case
-    task counts."""
+    task counts.  ``events``: a list that receives (start, after the block
+    kernel, after the singular flush) CUDA events of this call."""
     if getattr(rules, "kind", "slp") != kind:
         raise ConfigError("rules built for %r, assembling %r" % (rules.kind, kind))
     geom = dmesh.geom_of(kind)
@@ -118,15 +119,23 @@ def device_block_assembly(dmesh, rules, queue, row_idx, col_idx, desc, out, stat
         d_desc = to_dev(desc.astype(np.int64), out.device)
     stream = stream_handle()
     with torch.cuda.device(out.device):
+        ev = [torch.cuda.Event(enable_timing=True) for _ in range(3)] if events is not None else None
+        if ev:
+            ev[0].record()
         _native.call("gc_assemble_blocks", geom, nb, ptr(d_desc), int(desc[:, 1].max()),
                      int(desc[:, 3].max()), ptr(row_idx), ptr(col_idx), ptr(out), queue.struct, ptr(queue.flags),
                      stream)
+        if ev:
+            ev[1].record()
         counts = (_native.c_i64 * 4)()
         if full is not None:
             _native.call("gc_curved_singular", geom, full.struct, queue.struct, 1, ptr(out), counts, stream)
         else:
             _native.call("gc_singular_flush", geom, rules.struct, queue.struct, ptr(out),
                          counts, stream)
+        if ev:
+            ev[2].record()
+            events.append(ev)
     queue.check_flags()
     n_sing = [int(counts[k]) for k in range(4)]
     n_sing[0] = int(entries.sum()) - sum(n_sing[1:])

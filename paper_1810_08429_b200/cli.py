@@ -1,10 +1,12 @@
 """Operator construction shared by the experiment driver (``cli.py:159-177``).
 
-Only the configuration record and ``build_h2_operator`` - the canonical
-assembly sequence the benchmark reproduces - are mirrored; the CSV
-experiment driver itself is out of scope.
+Only the configuration record, ``build_h2_operator`` - the canonical
+assembly sequence the benchmark reproduces - and the executor statistics
+report of ``greencross stats`` are mirrored; the rest of the CSV experiment
+driver is out of scope.
 """
 
+import csv
 from collections import namedtuple
 
 import numpy as np
@@ -12,6 +14,9 @@ import numpy as np
 from . import gca
 from .clustering import build_block_tree, build_cluster_tree
 from .errors import ConfigError
+
+STATS_COLUMNS = ["case", "batches", "tasks", "wall_s"]          # cli.py:42-43
+CASE_NAMES = ("disjoint", "vertex", "edge", "identical")
 
 ExperimentConfig = namedtuple("ExperimentConfig", [
     "level", "geometry", "basis", "disc", "eta", "m", "delta_factor",
@@ -65,7 +70,7 @@ def build_h2_operator(mesh, cfg, kind="slp", capacity=None, threads=None, device
     btree = build_block_tree(tree, eta=cfg.eta)
     t2 = time.perf_counter()
     orders = (cfg.q_reg, cfg.q_sing)
-    rmarks, cmarks = gca.coupling_marks(btree)
+    rmarks, cmarks = gca.coupling_mark_arrays(btree)
     # row and column bases in shared per-level launches (gca.build_cluster_bases)
     row_kind = "collocation" if cfg.disc == "collocation" else cfg.basis      # cli.py:167
     rb, cb = gca.build_cluster_bases(tree, mesh, cfg.basis, cfg.m, cfg.delta_factor, cfg.eps,
@@ -79,3 +84,21 @@ def build_h2_operator(mesh, cfg, kind="slp", capacity=None, threads=None, device
         timings.update(cluster_tree_s=t1 - t0, block_tree_s=t2 - t1, row_basis_s=t3 - t2,
                        col_basis_s=t4 - t3, build_h2_s=t5 - t4, total_s=t5 - t0)
     return hm, tree, btree
+
+
+def stats_rows(hm):
+    """The rows of ``greencross stats`` (``cli.py:389-404``) for one built
+    operator: case name, capacity-sealed batches, tasks, evaluator seconds."""
+    return [{"case": CASE_NAMES[st["case"]], "batches": st["batches"], "tasks": st["tasks"],
+             "wall_s": st["wall_s"]} for st in hm.exec_stats]
+
+
+def write_stats(path, hm):
+    """``stats_rows`` as the reference's CSV report (header STATS_COLUMNS)."""
+    rows = stats_rows(hm)
+    with open(path, "w", newline="") as fh:
+        writer = csv.DictWriter(fh, fieldnames=STATS_COLUMNS)
+        writer.writeheader()
+        for row in rows:
+            writer.writerow(row)
+    return rows

@@ -157,15 +157,9 @@ class DeviceMesh:
         # chart normal per triangle (|n| = gram), for the double layer of plane charts
         self.normals = (charts["normal"] if charts is not None
                         else to_dev(np.ascontiguousarray(pack.normals[:, 0]), device))
-        # linear basis: vertex stars ordered by (corner, triangle) and the
-        # barycentric values of the regular rule's points
-        tris = mesh.triangles
-        t_of = np.repeat(np.arange(self.nt, dtype=np.int64), 3)
-        corner = np.tile(np.arange(3, dtype=np.int64), self.nt)
-        vert = tris.ravel().astype(np.int64)
-        order = np.lexsort((t_of, corner, vert))
-        self.vstar_ptr = to_dev(np.searchsorted(vert[order], np.arange(mesh.nv + 1)).astype(np.int64), device)
-        self.vstar_ent = to_dev((t_of[order] << 2) | corner[order], device)
+        # linear basis: the barycentric values of the regular rule's points;
+        # vertex stars built on first use (_stars)
+        self.vstar_ptr = self.vstar_ent = None
         self.bq = to_dev(np.stack([1.0 - pts[:, 0] - pts[:, 1], pts[:, 0], pts[:, 1]], 1), device)
         self.verts = (charts["verts"] if charts is not None
                       else to_dev(np.ascontiguousarray(mesh.vertices, dtype=np.float64), device))
@@ -183,12 +177,27 @@ class DeviceMesh:
             raise ConfigError("unknown basis %r" % (basis,))
         key = (kind, basis)
         if key not in self._geoms:
+            if basis != "constant":
+                self._stars()
             self._geoms[key] = _native.GcGeom(
                 ptr(self.corners), ptr(self.gram), ptr(self.tri_vid), ptr(self.xq), ptr(self.wq),
                 self.nt, self.mq, self.wq_host.ctypes.data, ptr(self.normals), int(kind == "dlp"),
                 ptr(self.vstar_ptr), ptr(self.vstar_ent), ptr(self.bq), codes[basis], ptr(self.verts),
                 ptr(self.nodes6), ptr(self.nrm6), ptr(self.gq), ptr(self.nq))
         return self._geoms[key]
+
+    def _stars(self):
+        """Vertex stars of the linear basis, ordered by (vertex, corner,
+        triangle)."""
+        if self.vstar_ptr is None:
+            tris = self.mesh.triangles
+            t_of = np.repeat(np.arange(self.nt, dtype=np.int64), 3)
+            corner = np.tile(np.arange(3, dtype=np.int64), self.nt)
+            vert = tris.ravel().astype(np.int64)
+            order = np.lexsort((t_of, corner, vert))
+            self.vstar_ptr = to_dev(np.searchsorted(vert[order], np.arange(self.mesh.nv + 1)).astype(np.int64),
+                                    self.device)
+            self.vstar_ent = to_dev((t_of[order] << 2) | corner[order], self.device)
 
     @classmethod
     def get(cls, mesh, q_reg, device):

@@ -329,9 +329,16 @@ def _coef_layout_queue(flat, roots, rank, base=0):
 
 def coupling_marks(btree):
     """Row and column cluster indices of admissible leaves (``gca.py:149-159``)."""
+    r, c = coupling_mark_arrays(btree)
+    return set(r.tolist()), set(c.tolist())
+
+
+def coupling_mark_arrays(btree):
+    """``coupling_marks`` as two sorted unique index arrays (the pipeline's
+    form: no Python sets of 10^5 clusters)."""
     fb = btree.flat
     ids = btree._leaf_ids(0)
-    return set(fb.row[ids].tolist()), set(fb.col[ids].tolist())
+    return np.unique(fb.row[ids]), np.unique(fb.col[ids])
 
 
 def _materialize(flat, marks):
@@ -341,7 +348,8 @@ def _materialize(flat, marks):
         mat[0] = True
     else:
         mat = np.zeros(n, dtype=bool)
-        idx = np.fromiter((int(i) for i in marks), dtype=np.int64)
+        idx = (np.asarray(marks, dtype=np.int64) if isinstance(marks, np.ndarray)
+               else np.fromiter((int(i) for i in marks), dtype=np.int64))
         if idx.size:
             mat[idx] = True
     marked = mat.copy()
@@ -635,6 +643,38 @@ class DeviceH2:
         self.plans = {}
 
 
+DEFAULT_CAPACITY = 4096        # the reference executor's list capacity (batchexec.py:27)
+
+
+def _exec_stats(tasks, capacity, seconds):
+    """Per-case executor statistics as the reference's BatchExecutor.stats()
+    (``batchexec.py:211-213``): every case's tasks go through one list that
+    is sealed whenever it reaches ``capacity`` and once more at finalize for
+    a partial tail, so batches = ceil(tasks / capacity)
+    (``batchexec.py:37-52, 154-166``).  ``wall_s``: the device time that
+    evaluated the case (the reference: evaluator wall time summed over its
+    batches)."""
+    if capacity < 1:
+        raise ConfigError("capacity must be >= 1")
+    return [{"tasks": int(t), "batches": -(-int(t) // capacity), "wall_s": float(w), "case": k}
+            for k, (t, w) in enumerate(zip(tasks, seconds))]
+
+
+def _case_seconds(events, rules, stats_c, stats_n):
+    """Device seconds per pair case from device_block_assembly's events:
+    the block kernel evaluates the disjoint pairs (case 0), the singular
+    flush cases 1-3, split by their quadrature points (tasks x points)."""
+    sec = [0.0] * 4
+    for (a, b, c), st in zip(events, (stats_c, stats_n)):
+        sec[0] += a.elapsed_time(b) * 1e-3
+        w = [st[k] * rules.npts[k] for k in (1, 2, 3)]
+        tot = float(sum(w))
+        for k in (1, 2, 3):
+            if tot > 0:
+                sec[k] += b.elapsed_time(c) * 1e-3 * w[k - 1] / tot
+    return sec
+
+
 def build_h2(btree, row_basis, col_basis, mesh, kind="slp", basis="constant",
              disc="galerkin", orders=(3, 5), capacity=None, threads=None, device=None,
              row_range=None):
@@ -707,12 +747,14 @@ def build_h2(btree, row_basis, col_basis, mesh, kind="slp", basis="constant",
             t1 = time.perf_counter()
             stats_n = linear.assemble_blocks(dmesh, kind, lrules, mesh, nblocks, near, dev)
     else:
+        events = []
         stats_c = device_block_assembly(dmesh, rules, queue, rstore.pivots, cstore.pivots,
-                                        cdesc[keep], coup, kind=kind)
+                                        cdesc[keep], coup, kind=kind, events=events)
         t1 = time.perf_counter()
         # near-field blocks: full clusters
         ndesc = np.stack([rf.start[nr_r], n_nr, cf.start[nc_r], n_nc, n_off], 1)
-        stats_n = device_block_assembly(dmesh, rules, queue, perm_r, perm_c, ndesc, near, kind=kind)
+        stats_n = device_block_assembly(dmesh, rules, queue, perm_r, perm_c, ndesc, near, kind=kind,
+                                        events=events)
     torch.cuda.synchronize(dev)
     t2 = time.perf_counter()
     d = DeviceH2(dev)
@@ -722,10 +764,11 @@ def build_h2(btree, row_basis, col_basis, mesh, kind="slp", basis="constant",
     d.perm_r, d.perm_c = perm_r, perm_c
     d.row_range = row_range
     d.timing = {"coupling_s": t1 - t0, "nearfield_s": t2 - t1}
-    tasks = [stats_c[k] + stats_n[k] for k in range(4)]
-    exec_stats = [{"case": k, "tasks": int(tasks[k]), "batches": int(tasks[k] > 0)
-                   + int(k == 0 and stats_c[0] > 0 and stats_n[0] > 0),
-                   "wall_s": (t2 - t0) if k == 0 else 0.0} for k in range(4)]
+    ncase = 2 if disc == "collocation" else 4                 # the reference's executor cases
+    tasks = [stats_c[k] + stats_n[k] for k in range(ncase)]
+    exec_stats = _exec_stats(tasks, DEFAULT_CAPACITY if capacity is None else int(capacity),
+                             _case_seconds(events, rules, stats_c, stats_n) if basis != "linear"
+                             else [t2 - t0] + [0.0] * (ncase - 1))
     coupling = _BlockList(CouplingBlock, cr, cc, c_nr, c_nc, c_off, coup).bind(rf, cf)
     nearfield = _BlockList(NearfieldBlock, nr_r, nc_r, n_nr, n_nc, n_off, near).bind(rf, cf)
     return H2Matrix(rf.node(0), cf.node(0), row_basis, col_basis, coupling, nearfield,

@@ -307,18 +307,24 @@ class PanelPlan:
             nblk = np.diff(np.r_[cuts, len(order)])
             colh = np.maximum.reduceat(cf.height[d.c_cols[order]], cuts)
             rowh = rf.height[sn[cuts]]
-            fwd_h = [P.height for P in fwd if P.nitems]
-            src = np.array([next((k for k, fh in enumerate(fwd_h) if fh >= c), len(fwd_h)) for c in colh])
-            dst = np.array([next((k for k, (P, hs) in enumerate(bwd) if P.nitems and r in hs), len(bwd))
-                            for r in rowh])
+            # src: the first forward phase (ascending heights) covering the
+            # panel's highest column cluster; dst: the first backward phase
+            # (top down) whose heights include the row cluster's
+            fwd_h = np.array([P.height for P in fwd if P.nitems], np.int64)
+            src = np.searchsorted(fwd_h, colh, side="left")
+            tab = np.full(int(rowh.max()) + 1, len(bwd), np.int64)
+            for k in reversed(range(len(bwd))):
+                P, hs = bwd[k]
+                if P.nitems:
+                    hh = np.array([v for v in hs if 0 <= v < len(tab)], np.int64)
+                    tab[hh] = k
+            dst = tab[rowh]
             # merge only into launches of >= _MERGE_MIN_BYTES: smaller groups stay
             # one launch per row height (measured: C4 -1.5 %, C2 +10 % merged)
-            gbytes = {}
-            for k_, e_ in zip(zip(src.tolist(), dst.tolist()), (K * d.c_nr[order[cuts]]).tolist()):
-                gbytes[k_] = gbytes.get(k_, 0) + 8 * e_
-            grp = np.array([(a_, b_, -1 if gbytes[(a_, b_)] >= _MERGE_MIN_BYTES else int(h_))
-                            for a_, b_, h_ in zip(src.tolist(), dst.tolist(), rowh.tolist())], np.int64)
-            for key in sorted(set(map(tuple, grp.tolist())), key=lambda k: (-k[1], k[0], k[2])):
+            pair_key = src * (len(bwd) + 1) + dst
+            gbytes = np.bincount(pair_key, weights=8.0 * (K * d.c_nr[order[cuts]]))
+            grp = np.stack([src, dst, np.where(gbytes[pair_key] >= _MERGE_MIN_BYTES, -1, rowh)], 1).astype(np.int64)
+            for key in sorted(map(tuple, np.unique(grp, axis=0).tolist()), key=lambda k: (-k[1], k[0], k[2])):
                 sel = np.flatnonzero(np.all(grp == np.array(key), axis=1))
                 bsel = _ranges_np(cuts[sel], nblk[sel])
                 panels = (d.c_off[order[cuts[sel]]], K[sel], d.c_nr[order[cuts[sel]]],

@@ -212,7 +212,7 @@ def build_sharded_operator(mesh, cfg, group=None, device=None, timings=None):
     layout = ShardLayout(tree, btree, world, rank)
     rng = (layout.lo, layout.hi)
     orders = (cfg.q_reg, cfg.q_sing)
-    rmarks, cmarks = gca.coupling_marks(btree)
+    rmarks, cmarks = gca.coupling_mark_arrays(btree)
     t1 = time.perf_counter()
     row_kind = "collocation" if cfg.disc == "collocation" else cfg.basis      # cli.py:167
     rb, cb = gca.build_cluster_bases(tree, mesh, cfg.basis, cfg.m, cfg.delta_factor, cfg.eps,

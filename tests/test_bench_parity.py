@@ -245,3 +245,4 @@ def test_matvec_matches_reference_c2():
     assert {k: rep[k] for k in g["storage_keys"]} == dict(zip(g["storage_keys"].tolist(),
                                                               g["storage_vals"].tolist()))
     assert [s["tasks"] for s in hm.exec_stats] == g["exec_tasks"].tolist()
+    assert [s["batches"] for s in hm.exec_stats] == g["exec_batches"].tolist()

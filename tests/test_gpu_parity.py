@@ -215,6 +215,26 @@ def test_pipeline_storage_and_stats(built):
                                                               g["storage_vals"].tolist()))
     assert [s["tasks"] for s in hm.exec_stats] == g["exec_tasks"].tolist()
     assert [s["case"] for s in hm.exec_stats] == [0, 1, 2, 3]
+    # the reference executor seals every case's list at capacity 4096 and
+    # once more for a partial tail (batchexec.py:37-52, 154-166)
+    assert [s["batches"] for s in hm.exec_stats] == [-(-int(t) // 4096) for t in g["exec_tasks"]]
+    assert all(s["wall_s"] >= 0.0 for s in hm.exec_stats)
+
+
+def test_stats_report(built, tmp_path):
+    """``greencross stats`` CSV (pkg/tests/test_cli.py:145-154): header,
+    case names, tasks / batches / seconds per case."""
+    import csv
+    name, g, mesh, hm, tree, bt = built
+    out = str(tmp_path / "stats.csv")
+    cli.write_stats(out, hm)
+    with open(out) as fh:
+        rows = list(csv.DictReader(fh))
+    assert list(rows[0].keys()) == cli.STATS_COLUMNS
+    assert [r["case"] for r in rows] == list(cli.CASE_NAMES)
+    assert [int(r["tasks"]) for r in rows] == g["exec_tasks"].tolist()
+    assert all(int(r["batches"]) >= 1 for r in rows)
+    assert all(float(r["wall_s"]) >= 0.0 for r in rows)
 
 
 def test_pipeline_bitwise_deterministic(built):

@@ -52,8 +52,21 @@ for spec in sys.argv[3:]:
             b.record()
             torch.cuda.synchronize()
             res[i].append(a.elapsed_time(b) / reps * 1e3)
-    for v, r in zip(vals, res):
-        print("L%d eps %g %s=%-10s product %8.1f us  %6.0f GB/s" % (L, eps, name, v, min(r), nbytes / min(r) / 1e3),
-              flush=True)
+    from paper_1810_08429_b200.device import stream_handle
+    import numpy as np
+    flush = torch.empty(32 << 20, dtype=torch.float64, device="cuda")
+    for v, r, p in zip(vals, res, plans):
+        big = max((P for P in p.phases if P.name == "coupling"), key=lambda P: P.bytes)
+        ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(10)]
+        for e0, e1 in ev:
+            flush.zero_()
+            e0.record()
+            p._launch(big, stream_handle())
+            e1.record()
+        torch.cuda.synchronize()
+        tb = np.median([e0.elapsed_time(e1) for e0, e1 in ev]) * 1e3
+        bb = big.bytes + 8 * big.in_elems + 8 * big.out_elems
+        print("L%d eps %g %s=%-10s product %8.1f us  %6.0f GB/s   largest coupling launch alone %6.1f us %6.0f GB/s"
+              % (L, eps, name, v, min(r), nbytes / min(r) / 1e3, tb, bb / tb / 1e3), flush=True)
     del plans, hm
     torch.cuda.empty_cache()

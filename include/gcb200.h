@@ -149,6 +149,14 @@ int gc_assemble_blocks(const gc_geom* g, int64_t nb, const int64_t* desc,
 int gc_singular_flush(const gc_geom* g, const gc_rules* r, gc_queue* q,
                       double* out, int64_t* counts, void* stream);
 
+/* gc_singular_flush without the host synchronisation: the singular kernels
+ * read their task counts from the queue's device counters (clamped to the
+ * capacity; an overflow sets the gc_assemble_blocks flag), then the
+ * counters are copied to counts_dev [dev] (4 x int32, may be NULL) and
+ * reset, all in stream order.  Plane charts only. */
+int gc_singular_flush_async(const gc_geom* g, const gc_rules* r, gc_queue* q,
+                            double* out, int32_t* counts_dev, void* stream);
+
 /* Batched transpose: for node i with desc (off, rows, cols) [dev] (nn,3):
  * out[off + c*rows + r] = in[off + r*cols + c]. */
 int gc_batched_transpose(int64_t nn, const int64_t* desc, const double* in,

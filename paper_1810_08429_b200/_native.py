@@ -47,6 +47,8 @@ _SIGNATURES = {
                            ctypes.POINTER(GcQueue), c_p, c_p],
     "gc_singular_flush": [ctypes.POINTER(GcGeom), ctypes.POINTER(GcRules),
                           ctypes.POINTER(GcQueue), c_p, ctypes.POINTER(c_i64), c_p],
+    "gc_singular_flush_async": [ctypes.POINTER(GcGeom), ctypes.POINTER(GcRules),
+                                ctypes.POINTER(GcQueue), c_p, c_p, c_p],
     "gc_batched_transpose": [c_i64, c_p, c_p, c_p, c_p],
     "gc_green_box_rules": [ctypes.c_int, c_p, c_p, c_i64, c_p, c_p, c_p, c_p, c_p],
     "gc_green_factor": [ctypes.POINTER(GcGeom), ctypes.c_int, c_i64, c_i64, c_p, c_p, c_p,

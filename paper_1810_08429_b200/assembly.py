@@ -96,13 +96,17 @@ def galerkin_pair_evaluator(kind, mesh, basis, q_reg, q_sing, device=None):
 
 
 def device_block_assembly(dmesh, rules, queue, row_idx, col_idx, desc, out, stats=None, kind="slp",
-                          d_desc=None, events=None):
+                          d_desc=None, events=None, pending=None):
     """Assemble blocks described by ``desc (nb,5)`` into the device buffer
     ``out`` (column-major per block); singular pairs are flushed at the end.
     ``kind`` "slp" / "dlp" picks the kernel (``rules`` must match it);
     ``d_desc`` is an already uploaded copy of ``desc``.  Returns the per-case
     task counts.  ``events``: a list that receives (start, after the block
-    kernel, after the singular flush) CUDA events of this call."""
+    kernel, after the singular flush) CUDA events of this call.
+    ``pending``: asynchronous mode (plane charts) - no host synchronisation;
+    appends (device singular counts, total entries) to the list and returns
+    None; the caller resolves the counts and checks the queue flags after
+    its own synchronisation (:func:`resolve_counts`)."""
     if getattr(rules, "kind", "slp") != kind:
         raise ConfigError("rules built for %r, assembling %r" % (rules.kind, kind))
     geom = dmesh.geom_of(kind)
@@ -130,16 +134,34 @@ def device_block_assembly(dmesh, rules, queue, row_idx, col_idx, desc, out, stat
         counts = (_native.c_i64 * 4)()
         if full is not None:
             _native.call("gc_curved_singular", geom, full.struct, queue.struct, 1, ptr(out), counts, stream)
+        elif pending is not None:
+            cdev = torch.zeros(4, dtype=torch.int32, device=out.device)
+            _native.call("gc_singular_flush_async", geom, rules.struct, queue.struct, ptr(out), ptr(cdev),
+                         stream)
         else:
             _native.call("gc_singular_flush", geom, rules.struct, queue.struct, ptr(out),
                          counts, stream)
         if ev:
             ev[2].record()
             events.append(ev)
+    if pending is not None and full is None:
+        pending.append((cdev, int(entries.sum())))
+        return None
     queue.check_flags()
     n_sing = [int(counts[k]) for k in range(4)]
     n_sing[0] = int(entries.sum()) - sum(n_sing[1:])
     return n_sing
+
+
+def resolve_counts(pending, queue):
+    """Per-case task counts of asynchronous device_block_assembly calls
+    (after the caller's synchronisation); raises on a queue overflow."""
+    queue.check_flags()
+    out = []
+    for cdev, total in pending:
+        c = [int(v) for v in cdev.cpu().tolist()]
+        out.append([total - sum(c[1:]), c[1], c[2], c[3]])
+    return out
 
 
 def assemble_galerkin_block(kind, mesh, basis, rows, cols, orders=(3, 5), capacity=None,

@@ -418,8 +418,12 @@ constexpr int sing_group() { return NC == 4 ? GC_SING_G4 : NC == 3 ? GC_SING_G3 
 template <int NC, bool SMEM, bool DLP, int SG = sing_group<NC>()>
 __global__ void __launch_bounds__(SING_THREADS) k_singular(gc_geom g, const double* __restrict__ rule,
                                                            int P, const int64_t* __restrict__ tasks,
-                                                           int64_t ntasks, double* __restrict__ out) {
+                                                           int64_t ntasks, double* __restrict__ out,
+                                                           const int32_t* __restrict__ count) {
     extern __shared__ double sr[];
+    // count: the queue's device counter (the asynchronous flush); ntasks is
+    // then the capacity (overflow was flagged by the producer)
+    if (count) ntasks = min((int64_t)*count, ntasks);
     const double* R = rule;
     if (SMEM) {
         for (int i = threadIdx.x; i < (NC + 1) * P; i += SING_THREADS) sr[i] = rule[i];
@@ -495,10 +499,10 @@ __global__ void __launch_bounds__(SING_THREADS) k_singular(gc_geom g, const doub
 
 template <int NC, bool DLP>
 static int launch_singular_nc(const gc_geom& g, const double* table, int64_t P, const int64_t* tasks,
-                              int64_t n, double* out, cudaStream_t st) {
+                              int64_t n, double* out, cudaStream_t st, const int32_t* count) {
     const size_t bytes = (size_t)(NC + 1) * P * sizeof(double);
     const int64_t groups = (n + sing_group<NC>() - 1) / sing_group<NC>();
-    int64_t grid = (groups + SING_WARPS - 1) / SING_WARPS;
+    int64_t grid = (groups + SING_WARPS - 1) / SING_WARPS;     // capped below: persistent warps
     if (bytes <= 200 * 1024) {
         cudaError_t e = cudaFuncSetAttribute(k_singular<NC, true, DLP>,
                                              cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes);
@@ -507,17 +511,19 @@ static int launch_singular_nc(const gc_geom& g, const double* table, int64_t P, 
         cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_singular<NC, true, DLP>, SING_THREADS, bytes);
         if (per_sm < 1) per_sm = 1;
         if (grid > 148LL * per_sm) grid = 148LL * per_sm;
-        k_singular<NC, true, DLP><<<(unsigned)grid, SING_THREADS, bytes, st>>>(g, table, (int)P, tasks, n, out);
+        k_singular<NC, true, DLP><<<(unsigned)grid, SING_THREADS, bytes, st>>>(g, table, (int)P, tasks, n, out,
+                                                                                 count);
     } else {
         if (grid > 148LL * 8) grid = 148LL * 8;
-        k_singular<NC, false, DLP><<<(unsigned)grid, SING_THREADS, 0, st>>>(g, table, (int)P, tasks, n, out);
+        k_singular<NC, false, DLP><<<(unsigned)grid, SING_THREADS, 0, st>>>(g, table, (int)P, tasks, n, out,
+                                                                              count);
     }
     GC_CHECK_LAUNCH("k_singular");
     return GC_OK;
 }
 
 static int launch_singular(const gc_geom& g, const gc_rules& r, int kase, const int64_t* tasks,
-                           int64_t n, double* out, cudaStream_t st) {
+                           int64_t n, double* out, cudaStream_t st, const int32_t* count = nullptr) {
     if (n <= 0) return GC_OK;
     if (!r.table[kase] || r.npts[kase] <= 0) {
         set_error(GC_ERR_CONFIG, "singular rule for case %d not uploaded", kase);
@@ -525,12 +531,12 @@ static int launch_singular(const gc_geom& g, const gc_rules& r, int kase, const 
     }
     if (g.kernel && !g.normals) { set_error(GC_ERR_CONFIG, "double layer needs gc_geom.normals"); return GC_ERR_CONFIG; }
     switch (kase * 2 + (g.kernel ? 1 : 0)) {
-        case 2: return launch_singular_nc<4, false>(g, r.table[1], r.npts[1], tasks, n, out, st);
-        case 3: return launch_singular_nc<4, true>(g, r.table[1], r.npts[1], tasks, n, out, st);
-        case 4: return launch_singular_nc<3, false>(g, r.table[2], r.npts[2], tasks, n, out, st);
-        case 5: return launch_singular_nc<3, true>(g, r.table[2], r.npts[2], tasks, n, out, st);
-        case 6: return launch_singular_nc<2, false>(g, r.table[3], r.npts[3], tasks, n, out, st);
-        case 7: return launch_singular_nc<2, true>(g, r.table[3], r.npts[3], tasks, n, out, st);
+        case 2: return launch_singular_nc<4, false>(g, r.table[1], r.npts[1], tasks, n, out, st, count);
+        case 3: return launch_singular_nc<4, true>(g, r.table[1], r.npts[1], tasks, n, out, st, count);
+        case 4: return launch_singular_nc<3, false>(g, r.table[2], r.npts[2], tasks, n, out, st, count);
+        case 5: return launch_singular_nc<3, true>(g, r.table[2], r.npts[2], tasks, n, out, st, count);
+        case 6: return launch_singular_nc<2, false>(g, r.table[3], r.npts[3], tasks, n, out, st, count);
+        case 7: return launch_singular_nc<2, true>(g, r.table[3], r.npts[3], tasks, n, out, st, count);
         default: set_error(GC_ERR_CONFIG, "bad singular case %d", kase); return GC_ERR_CONFIG;
     }
 }
@@ -694,6 +700,29 @@ int gc_singular_flush(const gc_geom* gp, const gc_rules* rp, gc_queue* qp, doubl
     }
     e = cudaMemsetAsync(qp->count, 0, 4 * sizeof(int32_t), st);
     if (e != cudaSuccess) return cuda_status(e, "gc_singular_flush reset");
+    return GC_OK;
+}
+
+// The same flush without a host synchronisation: the singular kernels run
+// persistent warps that read their task counts from the queue's device
+// counters (clamped to the capacity; an overflow was flagged on the device
+// by the producer), the counters are copied to counts_dev (int32 x 4,
+// device memory, may be NULL) and reset - all stream-ordered, so assembly
+// returns while the quadrature runs.
+int gc_singular_flush_async(const gc_geom* gp, const gc_rules* rp, gc_queue* qp, double* out,
+                            int32_t* counts_dev, void* stream) {
+    if (!gp || !rp || !qp) { set_error(GC_ERR_CONFIG, "null argument"); return GC_ERR_CONFIG; }
+    if (gp->gq) { set_error(GC_ERR_CONFIG, "curved charts: flush with gc_curved_singular"); return GC_ERR_CONFIG; }
+    cudaStream_t st = (cudaStream_t)stream;
+    for (int k = 1; k <= 3; ++k) {
+        if (qp->cap[k] <= 0) continue;
+        int rc = launch_singular(*gp, *rp, k, qp->tasks[k], qp->cap[k], out, st, qp->count + k);
+        if (rc) return rc;
+    }
+    cudaError_t e = cudaSuccess;
+    if (counts_dev) e = cudaMemcpyAsync(counts_dev, qp->count, 4 * sizeof(int32_t), cudaMemcpyDeviceToDevice, st);
+    if (e == cudaSuccess) e = cudaMemsetAsync(qp->count, 0, 4 * sizeof(int32_t), st);
+    if (e != cudaSuccess) return cuda_status(e, "gc_singular_flush_async");
     return GC_OK;
 }
 

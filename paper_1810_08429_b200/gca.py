@@ -18,13 +18,14 @@ through the lazy ``.values`` / ``.v`` / ``.transfer`` views.
 """
 
 import time
+import weakref
 from collections import namedtuple
 from collections.abc import Sequence
 
 import numpy as np
 
 from . import _native
-from .assembly import device_block_assembly, green_factors_device
+from .assembly import device_block_assembly, green_factors_device, resolve_counts
 from .device import (DeviceMesh, DeviceRules, SingularQueue, check_mesh, empty, padded_copy,
                      padded_empty, ptr, require_device, stream_handle, to_dev, torch)
 from .errors import ConfigError, GeometryError
@@ -579,12 +580,16 @@ class _BlockList(Sequence):
         self._nr, self._nc, self._off = nr, nc, off
         self._store = store
         self._host = None
+        self._owner = None          # weakref to the H2Matrix (settle before reading)
 
     def __len__(self):
         return len(self._rows)
 
     def _host_store(self):
         if self._host is None:
+            owner = self._owner() if self._owner is not None else None
+            if owner is not None:
+                owner.settle()
             self._host = self._store.cpu().numpy()
         return self._host
 
@@ -618,8 +623,29 @@ class H2Matrix:
         self.col_basis = col_basis
         self.coupling = coupling
         self.nearfield = nearfield
-        self.exec_stats = exec_stats
+        self._exec_stats = exec_stats
+        self._settle = None
         self.dev = dev
+
+    def settle(self):
+        """Wait for the device assembly (build_h2 returns while its
+        quadrature runs), check its queue flags and fix the executor
+        statistics; idempotent.  Every reader of block data calls it."""
+        if self._settle is not None:
+            fn, self._settle = self._settle, None
+            self._exec_stats = fn()
+        return self
+
+    @property
+    def exec_stats(self):
+        """Per-case executor statistics (``batchexec.py:211-213``)."""
+        self.settle()
+        return self._exec_stats
+
+    @exec_stats.setter
+    def exec_stats(self, value):
+        self._settle = None
+        self._exec_stats = value
 
     @property
     def shape(self):
@@ -660,12 +686,13 @@ def _exec_stats(tasks, capacity, seconds):
             for k, (t, w) in enumerate(zip(tasks, seconds))]
 
 
-def _case_seconds(events, rules, stats_c, stats_n):
-    """Device seconds per pair case from device_block_assembly's events:
-    the block kernel evaluates the disjoint pairs (case 0), the singular
-    flush cases 1-3, split by their quadrature points (tasks x points)."""
+def _case_seconds(calls, rules):
+    """Device seconds per pair case from device_block_assembly's events
+    (``calls`` = [(events, counts)] per call): the block kernel evaluates
+    the disjoint pairs (case 0), the singular flush cases 1-3, split by
+    their quadrature points (tasks x points)."""
     sec = [0.0] * 4
-    for (a, b, c), st in zip(events, (stats_c, stats_n)):
+    for (a, b, c), st in [(ev[0], st) for ev, st in calls if ev]:
         sec[0] += a.elapsed_time(b) * 1e-3
         w = [st[k] * rules.npts[k] for k in (1, 2, 3)]
         tot = float(sum(w))
@@ -747,29 +774,48 @@ def build_h2(btree, row_basis, col_basis, mesh, kind="slp", basis="constant",
             t1 = time.perf_counter()
             stats_n = linear.assemble_blocks(dmesh, kind, lrules, mesh, nblocks, near, dev)
     else:
-        events = []
+        # plane charts: no host synchronisation - the quadrature runs while
+        # the caller continues (e.g. builds the matvec plan); the counts,
+        # the queue flags and the timings settle on first use (H2Matrix.settle)
+        ev_c, ev_n, pending = [], [], ([] if not dmesh.curved else None)
         stats_c = device_block_assembly(dmesh, rules, queue, rstore.pivots, cstore.pivots,
-                                        cdesc[keep], coup, kind=kind, events=events)
+                                        cdesc[keep], coup, kind=kind, events=ev_c, pending=pending)
         t1 = time.perf_counter()
         # near-field blocks: full clusters
         ndesc = np.stack([rf.start[nr_r], n_nr, cf.start[nc_r], n_nc, n_off], 1)
         stats_n = device_block_assembly(dmesh, rules, queue, perm_r, perm_c, ndesc, near, kind=kind,
-                                        events=events)
-    torch.cuda.synchronize(dev)
-    t2 = time.perf_counter()
+                                        events=ev_n, pending=pending)
     d = DeviceH2(dev)
     d.coup, d.near = coup, near
     d.c_rows, d.c_cols, d.c_nr, d.c_nc, d.c_off = cr, cc, c_nr, c_nc, c_off
     d.n_rows, d.n_cols, d.n_nr, d.n_nc, d.n_off = nr_r, nc_r, n_nr, n_nc, n_off
     d.perm_r, d.perm_c = perm_r, perm_c
     d.row_range = row_range
-    d.timing = {"coupling_s": t1 - t0, "nearfield_s": t2 - t1}
     ncase = 2 if disc == "collocation" else 4                 # the reference's executor cases
-    tasks = [stats_c[k] + stats_n[k] for k in range(ncase)]
-    exec_stats = _exec_stats(tasks, DEFAULT_CAPACITY if capacity is None else int(capacity),
-                             _case_seconds(events, rules, stats_c, stats_n) if basis != "linear"
-                             else [t2 - t0] + [0.0] * (ncase - 1))
+    cap = DEFAULT_CAPACITY if capacity is None else int(capacity)
+
+    def settle():
+        torch.cuda.synchronize(dev)
+        t2 = time.perf_counter()
+        if basis != "linear":
+            done = iter(resolve_counts(pending, queue) if pending else [])
+            sc, sn = [next(done) if r is None else r for r in (stats_c, stats_n)]
+            sec = _case_seconds([(ev_c, sc), (ev_n, sn)], rules)
+            d.timing = {"coupling_s": sum(a.elapsed_time(c) for a, _, c in ev_c) * 1e-3,
+                        "nearfield_s": sum(a.elapsed_time(c) for a, _, c in ev_n) * 1e-3}
+        else:
+            sc, sn = stats_c, stats_n
+            sec = [t2 - t0] + [0.0] * (ncase - 1)
+            d.timing = {"coupling_s": t1 - t0, "nearfield_s": t2 - t1}
+        return _exec_stats([sc[k] + sn[k] for k in range(ncase)], cap, sec)
+
+    if cap < 1:
+        raise ConfigError("capacity must be >= 1")
     coupling = _BlockList(CouplingBlock, cr, cc, c_nr, c_nc, c_off, coup).bind(rf, cf)
     nearfield = _BlockList(NearfieldBlock, nr_r, nc_r, n_nr, n_nc, n_off, near).bind(rf, cf)
-    return H2Matrix(rf.node(0), cf.node(0), row_basis, col_basis, coupling, nearfield,
-                    exec_stats, d)
+    hm = H2Matrix(rf.node(0), cf.node(0), row_basis, col_basis, coupling, nearfield, None, d)
+    hm._settle = settle
+    coupling._owner = nearfield._owner = weakref.ref(hm)
+    if basis == "linear" or pending is None:
+        hm.settle()                       # synchronous paths: settle now (errors surface here)
+    return hm

@@ -151,6 +151,8 @@ class _TransposedH2:
 
     def __init__(self, h):
         from .gca import DeviceH2, _grouped_offsets
+        if hasattr(h, "settle"):
+            h.settle()
         d = h.dev
         dev = d.device
         if d.row_range is not None:
@@ -347,6 +349,10 @@ class PanelPlan:
         self.graph = None
         t2 = time.perf_counter()
         self.timing.update(bulk_phases_s=t1 - t0, transforms_s=t2 - t1)
+        # the device assembly ran under this host work; its queue flags and
+        # statistics settle now (an error surfaces before the plan is used)
+        if hasattr(h, "settle"):
+            h.settle()
 
     def _xpos(self, p):
         """x_t buffer position of tree position p (index ranges never

@@ -252,6 +252,10 @@ class PanelPlan:
         dev = d.device
         self.dev = dev
         self.lock = threading.Lock()
+        self._dev_index = torch.device(dev).index
+        if self._dev_index is None:
+            self._dev_index = torch.cuda.current_device()
+        self._pin_x_np = None
         # x_t positions of the tree-ordered input (a shard: its padded
         # all-gather layout, parallel.ShardPlan)
         self._xmap = None if xt_map is None else np.asarray(xt_map, np.int64)
@@ -851,10 +855,24 @@ class PanelPlan:
         scatter kernel writes a fresh pinned array (torch's pinned block
         cache) that is returned without a copy."""
         with self.lock:
-            with torch.cuda.device(self.dev):
-                if not hasattr(self, "_pin_x"):
+            g = self.graph
+            if isinstance(g, _NativeGraph) and torch.cuda.current_device() == self._dev_index:
+                # the e2e hot path: one staging copy, one C call, one sync
+                if self._pin_x_np is None:
                     self._pin_x = torch.empty(self.n_in, dtype=torch.float64, pin_memory=True)
-                self._pin_x.numpy()[:] = x
+                    self._pin_x_np = self._pin_x.numpy()
+                np.copyto(self._pin_x_np, x)
+                y = torch.empty(self.n_out, dtype=torch.float64, pin_memory=True)
+                st = torch.cuda.current_stream()
+                _native.check(g._run(g.handle, self._pin_x.data_ptr(), y.data_ptr(), st.cuda_stream))
+                g._x, g._y = self._pin_x.data_ptr(), y.data_ptr()
+                st.synchronize()
+                return y.numpy()
+            with torch.cuda.device(self.dev):
+                if self._pin_x_np is None:
+                    self._pin_x = torch.empty(self.n_in, dtype=torch.float64, pin_memory=True)
+                    self._pin_x_np = self._pin_x.numpy()
+                np.copyto(self._pin_x_np, x)
                 y = torch.empty(self.n_out, dtype=torch.float64, pin_memory=True)
                 if self.graph is not None and self.bind(self._pin_x, y):
                     self.graph.replay()

@@ -157,6 +157,24 @@ int gc_singular_flush(const gc_geom* g, const gc_rules* r, gc_queue* q,
 int gc_singular_flush_async(const gc_geom* g, const gc_rules* r, gc_queue* q,
                             double* out, int32_t* counts_dev, void* stream);
 
+/* Block tree (replaces clustering.build_block_tree / admissible,
+ * clustering.py:215-237), host memory only: row and column cluster trees
+ * as flat preorder arrays (diam (n), lower / upper (n,3), left / right with
+ * -1 at leaves), the two roots, eta, the rounding sequence of the 1-D BLAS
+ * norm used to re-decide near ties (0 / 1, see gc_host_norm3) and the key
+ * width in base-4 digits.  Builds the nodes in build order (level by level;
+ * children grouped by child slot, then by parent): row, col, state (0
+ * admissible, 1 inadmissible leaf, 2 subdivided), level, key, parent; they
+ * are held by *handle, *count = number of nodes.  gc_block_tree_fetch
+ * copies them into caller arrays (any may be NULL) and frees the handle. */
+int gc_block_tree(const double* r_diam, const double* r_lower, const double* r_upper,
+                  const int64_t* r_left, const int64_t* r_right, const double* c_diam,
+                  const double* c_lower, const double* c_upper, const int64_t* c_left,
+                  const int64_t* c_right, int64_t root_r, int64_t root_c, double eta,
+                  int32_t norm_mode, int32_t digits, void** handle, int64_t* count);
+int gc_block_tree_fetch(void* handle, int64_t* row, int64_t* col, int8_t* state, int64_t* level,
+                        int64_t* key, int64_t* parent);
+
 /* Batched transpose: for node i with desc (off, rows, cols) [dev] (nn,3):
  * out[off + c*rows + r] = in[off + r*cols + c]. */
 int gc_batched_transpose(int64_t nn, const int64_t* desc, const double* in,

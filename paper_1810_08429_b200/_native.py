@@ -50,6 +50,9 @@ _SIGNATURES = {
     "gc_singular_flush_async": [ctypes.POINTER(GcGeom), ctypes.POINTER(GcRules),
                                 ctypes.POINTER(GcQueue), c_p, c_p, c_p],
     "gc_batched_transpose": [c_i64, c_p, c_p, c_p, c_p],
+    "gc_block_tree": [c_p, c_p, c_p, c_p, c_p, c_p, c_p, c_p, c_p, c_p, c_i64, c_i64, ctypes.c_double,
+                      ctypes.c_int32, ctypes.c_int32, ctypes.POINTER(c_p), ctypes.POINTER(c_i64)],
+    "gc_block_tree_fetch": [c_p, c_p, c_p, c_p, c_p, c_p, c_p],
     "gc_green_box_rules": [ctypes.c_int, c_p, c_p, c_i64, c_p, c_p, c_p, c_p, c_p],
     "gc_green_factor": [ctypes.POINTER(GcGeom), ctypes.c_int, c_i64, c_i64, c_p, c_p, c_p,
                         c_p, c_p, c_p, c_p, c_p, c_p],

@@ -519,7 +519,40 @@ def _admissible_many(rt, ct, r, c, eta):
 
 def build_block_tree(row_root, col_root=None, eta=1.0):
     """Recursive block partition (``clustering.py:215-237``), grown level by
-    level.  Returns the root :class:`BlockTree` view."""
+    level by the library's host routine (``gc_block_tree``).  Returns the
+    root :class:`BlockTree` view."""
+    if col_root is None:
+        col_root = row_root
+    if eta <= 0:
+        raise ConfigError("eta must be positive, got %r" % (eta,))
+    blas_norms(np.zeros((0, 3)))                 # fixes the BLAS-norm rounding mode
+    mode = _NORM_MODE[0]
+    if mode is None:                             # numpy's norm matches neither sequence
+        return _build_block_tree_arrays(row_root, col_root, eta)
+    from . import _native
+    rt, ct = row_root.flat, col_root.flat
+    trees = []
+    for t in (rt, ct):
+        trees += [np.ascontiguousarray(t.diam, np.float64), np.ascontiguousarray(t.lower, np.float64),
+                  np.ascontiguousarray(t.upper, np.float64), np.ascontiguousarray(t.left, np.int64),
+                  np.ascontiguousarray(t.right, np.int64)]
+    lib = _native.load()
+    handle, count = _native.ctypes.c_void_p(0), _native.ctypes.c_int64(0)
+    _native.check(lib.gc_block_tree(*[a.ctypes.data for a in trees], int(row_root.index), int(col_root.index),
+                                    float(eta), int(mode), _KEY_DIGITS, _native.ctypes.byref(handle),
+                                    _native.ctypes.byref(count)))
+    n = int(count.value)
+    row, col, state, level, key, parent = (np.empty(n, np.int64), np.empty(n, np.int64), np.empty(n, np.int8),
+                                           np.empty(n, np.int64), np.empty(n, np.int64), np.empty(n, np.int64))
+    _native.check(lib.gc_block_tree_fetch(handle, *[a.ctypes.data for a in (row, col, state, level, key, parent)]))
+    flat = FlatBlockTree(rt, ct, row, col, state, level, key, parent)
+    return BlockTree(flat, 0)
+
+
+def _build_block_tree_arrays(row_root, col_root=None, eta=1.0):
+    """The same partition array-at-a-time in numpy (the reference check of
+    gc_block_tree, and the path when numpy's norm rounding is not one of the
+    two sequences the native routine reproduces)."""
     if col_root is None:
         col_root = row_root
     if eta <= 0:

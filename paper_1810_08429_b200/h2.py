@@ -295,6 +295,7 @@ class PanelPlan:
         else:
             fwd, bwd, parts = tiered
         parts = [(P, hs) for P, hs in parts if P is not None and P.nitems]
+        t1b = time.perf_counter()
         # coupling: one panel per row cluster.  Row clusters are grouped by
         # (the forward phase producing every x-hat they read, the backward
         # phase consuming their y-hat): one launch per group - e.g. all the
@@ -352,11 +353,13 @@ class PanelPlan:
         self.nodes = self._build_nodes()
         self.graph = None
         t2 = time.perf_counter()
-        self.timing.update(bulk_phases_s=t1 - t0, transforms_s=t2 - t1)
         # the device assembly ran under this host work; its queue flags and
         # statistics settle now (an error surfaces before the plan is used)
         if hasattr(h, "settle"):
             h.settle()
+        t3 = time.perf_counter()
+        self.timing.update(near_phase_s=t1 - t0, transforms_s=t1b - t1, coupling_phases_s=t2 - t1b,
+                           settle_s=t3 - t2)
 
     def _xpos(self, p):
         """x_t buffer position of tree position p (index ranges never

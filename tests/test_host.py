@@ -118,6 +118,18 @@ def test_cluster_and_block_tree_bitwise(name):
     assert s["admissible"] == int(g["leaf_adm"].sum()) and s["leaves"] == len(lr)
 
 
+@pytest.mark.parametrize("level,basis,eta", [(3, "constant", 1.0), (4, "linear", 0.7), (4, "constant", 2.5)])
+def test_native_block_tree_equals_array_builder(level, basis, eta):
+    """gc_block_tree (the library's host routine) builds exactly the nodes,
+    order, keys and parents of the numpy array-at-a-time builder."""
+    mesh = geometry.build_sphere_mesh(level)
+    tree = clustering.build_cluster_tree(mesh, basis, 16)
+    a = clustering.build_block_tree(tree, eta=eta).flat
+    b = clustering._build_block_tree_arrays(tree, eta=eta).flat
+    for k in ("row", "col", "state", "level", "key", "parent_of", "leaf_ids"):
+        assert np.array_equal(getattr(a, k), getattr(b, k)), k
+
+
 def test_block_tree_tiles_the_matrix(sphere3):
     tree = clustering.build_cluster_tree(sphere3, "constant", 16)
     bt = clustering.build_block_tree(tree, eta=1.0)

@@ -740,14 +740,26 @@ def build_h2(btree, row_basis, col_basis, mesh, kind="slp", basis="constant",
     c_nr, c_nc = rstore.rank[cr], cstore.rank[cc]
     # storage grouped by row cluster: the blocks of one block row form one
     # contiguous (sum r_sigma) x r_tau panel for the matvec (h2.PanelPlan)
-    c_off = _grouped_offsets(cr, c_nr * c_nc)
+    # a block-row shard stores, inside each block row, the blocks with
+    # local columns (its own tree positions) before the others, so either
+    # subset is one contiguous sub-panel (the sharded product runs them
+    # before / after its all-gathers, parallel.ShardPlan)
+    if row_range is not None:
+        c_key = 2 * cr + ~((cf.start[cc] >= row_range[0]) & (cf.stop[cc] <= row_range[1]))
+    else:
+        c_key = cr
+    c_off = _grouped_offsets(c_key, c_nr * c_nc)
     c_total = int((c_nr * c_nc).sum())
     coup = padded_empty(max(c_total, 1), dev)
     cdesc = np.stack([rstore.piv_off[cr], c_nr, cstore.piv_off[cc], c_nc, c_off], 1)
     keep = (c_nr > 0) & (c_nc > 0)
     n_nr = rf.stop[nr_r] - rf.start[nr_r]
     n_nc = cf.stop[nc_r] - cf.start[nc_r]
-    n_off = _grouped_offsets(nr_r, n_nr * n_nc)
+    if row_range is not None:
+        n_key = 2 * nr_r + ~((cf.start[nc_r] >= row_range[0]) & (cf.stop[nc_r] <= row_range[1]))
+    else:
+        n_key = nr_r
+    n_off = _grouped_offsets(n_key, n_nr * n_nc)
     near = padded_empty(max(int((n_nr * n_nc).sum()), 1), dev)
     perm_r = to_dev(rf.perm, dev)
     perm_c = perm_r if cf is rf else to_dev(cf.perm, dev)

@@ -243,7 +243,7 @@ class PanelPlan:
     executes it serially on the current stream (for per-phase timing).
     """
 
-    def __init__(self, h, tiers="auto", xt_map=None, xt_len=None, bulk="auto"):
+    def __init__(self, h, tiers="auto", xt_map=None, xt_len=None, bulk="auto", col_local=None):
         import time
         t0 = time.perf_counter()
         self.timing = {}
@@ -278,14 +278,20 @@ class PanelPlan:
         # in the scatter): one buffer, zeroed by one memset per product
         self._ybuf = torch.zeros(2 * ny + self.n_out, **f64)
         self.yhat, self.yhat_t, self.yt2 = self._ybuf[:ny], self._ybuf[ny:2 * ny], self._ybuf[2 * ny:]
+        # col_local = (lo, hi): a shard (parallel.ShardPlan) whose own columns
+        # are the tree positions [lo, hi) - blocks with local columns run
+        # before the x / x-hat all-gathers, the others after them, adding
+        # onto the same outputs
+        self._col_local = col_local
+        nloc = (np.ones(len(d.n_cols), bool) if col_local is None else
+                (cf.start[d.n_cols] >= col_local[0]) & (cf.stop[d.n_cols] <= col_local[1]))
         # near field: one panel per row leaf
-        order = np.argsort(d.n_rows, kind="stable")
-        sn = d.n_rows[order]
-        cuts = np.flatnonzero(np.r_[True, sn[1:] != sn[:-1]]) if len(sn) else np.zeros(0, np.int64)
-        K = np.add.reduceat(d.n_nc[order], cuts) if len(sn) else np.zeros(0, np.int64)
-        rows = (self._xpos(cf.start[d.n_cols[order]]), d.n_nc[order])
-        panels = (d.n_off[order[cuts]], K, d.n_nr[order[cuts]], rows, rf.start[sn[cuts]], 0)
-        near = self._phase("nearfield", 0, panels, d.near, None, self.xt, None, self.yt)
+        near = self._near_phase(h, np.flatnonzero(nloc), 0)
+        self._near_remote = None
+        if col_local is not None and not nloc.all():
+            has_local = np.zeros(len(rf.start), bool)
+            has_local[d.n_rows[nloc]] = True
+            self._near_remote = self._near_phase(h, np.flatnonzero(~nloc), has_local, ordered=True)
         self.tiers = None
         t1 = time.perf_counter()
         tiered = self._tiered(h, tiers) if tiers != "off" else None
@@ -296,52 +302,17 @@ class PanelPlan:
             fwd, bwd, parts = tiered
         parts = [(P, hs) for P, hs in parts if P is not None and P.nitems]
         t1b = time.perf_counter()
-        # coupling: one panel per row cluster.  Row clusters are grouped by
-        # (the forward phase producing every x-hat they read, the backward
-        # phase consuming their y-hat): one launch per group - e.g. all the
-        # deep buckets that only the leaf rows read - so a launch is as long
-        # as the dependencies allow (whole waves of work items)
-        cpl = []
-        live = (d.c_nr > 0) & (d.c_nc > 0)
-        order = np.flatnonzero(live)[np.argsort(d.c_rows[live], kind="stable")]
-        if order.size:
-            sn = d.c_rows[order]
-            cuts = np.flatnonzero(np.r_[True, sn[1:] != sn[:-1]])
-            # panel inputs: the x-hat slots of the blocks' column clusters, in
-            # block order - one index range per block, expanded on the device
-            bstart, blen = cs.coef_off[d.c_cols[order]], d.c_nc[order]
-            K = np.add.reduceat(blen, cuts)
-            nblk = np.diff(np.r_[cuts, len(order)])
-            colh = np.maximum.reduceat(cf.height[d.c_cols[order]], cuts)
-            rowh = rf.height[sn[cuts]]
-            # src: the first forward phase (ascending heights) covering the
-            # panel's highest column cluster; dst: the first backward phase
-            # (top down) whose heights include the row cluster's
-            fwd_h = np.array([P.height for P in fwd if P.nitems], np.int64)
-            src = np.searchsorted(fwd_h, colh, side="left")
-            tab = np.full(int(rowh.max()) + 1, len(bwd), np.int64)
-            for k in reversed(range(len(bwd))):
-                P, hs = bwd[k]
-                if P.nitems:
-                    hh = np.array([v for v in hs if 0 <= v < len(tab)], np.int64)
-                    tab[hh] = k
-            dst = tab[rowh]
-            # merge only into launches of >= _MERGE_MIN_BYTES: smaller groups stay
-            # one launch per row height (measured: C4 -1.5 %, C2 +10 % merged)
-            pair_key = src * (len(bwd) + 1) + dst
-            gbytes = np.bincount(pair_key, weights=8.0 * (K * d.c_nr[order[cuts]]))
-            grp = np.stack([src, dst, np.where(gbytes[pair_key] >= _MERGE_MIN_BYTES, -1, rowh)], 1).astype(np.int64)
-            for key in sorted(map(tuple, np.unique(grp, axis=0).tolist()), key=lambda k: (-k[1], k[0], k[2])):
-                sel = np.flatnonzero(np.all(grp == np.array(key), axis=1))
-                bsel = _ranges_np(cuts[sel], nblk[sel])
-                panels = (d.c_off[order[cuts[sel]]], K[sel], d.c_nr[order[cuts[sel]]],
-                          (bstart[bsel], blen[bsel]), rs.coef_off[sn[cuts[sel]]], 0)
-                P = self._phase("coupling", int(rowh[sel].max()), panels, d.coup, None, self.xhat, None,
-                                self.yhat)
-                cpl.append((P, int(colh[sel].max()), set(rowh[sel].tolist())))
+        cloc = (np.ones(len(d.c_cols), bool) if col_local is None else
+                (cf.start[d.c_cols] >= col_local[0]) & (cf.stop[d.c_cols] <= col_local[1]))
+        cpl = self._coupling_phases(h, fwd, bwd, cloc, 0)
+        self._cpl_remote = []
+        if col_local is not None and not cloc.all():
+            has_local = np.zeros(len(rf.start), bool)
+            has_local[d.c_rows[cloc & (d.c_nr > 0) & (d.c_nc > 0)]] = True
+            self._cpl_remote = self._coupling_phases(h, fwd, bwd, ~cloc, has_local, ordered=True)
         self._fwd, self._cpl, self._bwd, self._near, self._leafparts = fwd, cpl, bwd, near, parts
-        self.phases = [P for P in [near] + fwd + [c for c, _, _ in cpl] + [b for b, _ in bwd] + [p for p, _ in parts]
-                       if P is not None and P.nitems > 0]
+        self.phases = [P for P in [near, self._near_remote] + fwd + [c for c, _, _ in cpl + self._cpl_remote]
+                       + [b for b, _ in bwd] + [p for p, _ in parts] if P is not None and P.nitems > 0]
         # the chain gets the highest stream priority so its CTAs are
         # scheduled ahead of the queued bulk (coupling buckets, near field)
         self.streams = {"chain": torch.cuda.Stream(device=dev, priority=-8)}
@@ -360,6 +331,75 @@ class PanelPlan:
         t3 = time.perf_counter()
         self.timing.update(near_phase_s=t1 - t0, transforms_s=t1b - t1, coupling_phases_s=t2 - t1b,
                            settle_s=t3 - t2)
+
+    def _near_phase(self, h, blocks, acc_rows, ordered=False):
+        """Near-field phase over the near blocks ``blocks``: one panel per
+        row leaf; ``acc_rows`` (scalar or per row cluster) marks the rows
+        whose panel adds onto y_t (written by an earlier near phase)."""
+        d = h.dev
+        rf, cf = h.row_tree.flat, h.col_tree.flat
+        order = blocks[np.argsort(d.n_off[blocks], kind="stable")]       # storage order: rows contiguous
+        sn = d.n_rows[order]
+        cuts = np.flatnonzero(np.r_[True, sn[1:] != sn[:-1]]) if len(sn) else np.zeros(0, np.int64)
+        K = np.add.reduceat(d.n_nc[order], cuts) if len(sn) else np.zeros(0, np.int64)
+        rows = (self._xpos(cf.start[d.n_cols[order]]), d.n_nc[order])
+        acc = np.asarray(acc_rows)[sn[cuts]].astype(np.int64) if np.ndim(acc_rows) else acc_rows
+        panels = (d.n_off[order[cuts]], K, d.n_nr[order[cuts]], rows, rf.start[sn[cuts]], acc)
+        return self._phase("nearfield", 0, panels, d.near, None, self.xt, None, self.yt, ordered=ordered)
+
+    def _coupling_phases(self, h, fwd, bwd, mask, acc_rows, ordered=False):
+        """Coupling phases over the blocks ``mask`` selects: one panel per
+        row cluster.  Row clusters are grouped by (the forward phase
+        producing every x-hat they read, the backward phase consuming their
+        y-hat): one launch per group - e.g. all the deep buckets that only
+        the leaf rows read - so a launch is as long as the dependencies
+        allow.  ``acc_rows`` (scalar or per row cluster): panels that add
+        onto y-hat written by an earlier coupling phase."""
+        d = h.dev
+        rs, cs = h.row_basis.store, h.col_basis.store
+        rf, cf = h.row_tree.flat, h.col_tree.flat
+        cpl = []
+        live = mask & (d.c_nr > 0) & (d.c_nc > 0)
+        order = np.flatnonzero(live)[np.argsort(d.c_off[live], kind="stable")]   # storage order
+        if not order.size:
+            return cpl
+        sn = d.c_rows[order]
+        cuts = np.flatnonzero(np.r_[True, sn[1:] != sn[:-1]])
+        # panel inputs: the x-hat slots of the blocks' column clusters, in
+        # block order - one index range per block, expanded on the device
+        bstart, blen = cs.coef_off[d.c_cols[order]], d.c_nc[order]
+        K = np.add.reduceat(blen, cuts)
+        nblk = np.diff(np.r_[cuts, len(order)])
+        colh = np.maximum.reduceat(cf.height[d.c_cols[order]], cuts)
+        rowh = rf.height[sn[cuts]]
+        acc = (np.asarray(acc_rows)[sn[cuts]].astype(np.int64) if np.ndim(acc_rows)
+               else np.full(len(cuts), int(acc_rows), np.int64))
+        # src: the first forward phase (ascending heights) covering the
+        # panel's highest column cluster; dst: the first backward phase
+        # (top down) whose heights include the row cluster's
+        fwd_h = np.array([P.height for P in fwd if P.nitems], np.int64)
+        src = np.searchsorted(fwd_h, colh, side="left")
+        tab = np.full(int(rowh.max()) + 1, len(bwd), np.int64)
+        for k in reversed(range(len(bwd))):
+            P, hs = bwd[k]
+            if P.nitems:
+                hh = np.array([v for v in hs if 0 <= v < len(tab)], np.int64)
+                tab[hh] = k
+        dst = tab[rowh]
+        # merge only into launches of >= _MERGE_MIN_BYTES: smaller groups stay
+        # one launch per row height (measured: C4 -1.5 %, C2 +10 % merged)
+        pair_key = src * (len(bwd) + 1) + dst
+        gbytes = np.bincount(pair_key, weights=8.0 * (K * d.c_nr[order[cuts]]))
+        grp = np.stack([src, dst, np.where(gbytes[pair_key] >= _MERGE_MIN_BYTES, -1, rowh)], 1).astype(np.int64)
+        for key in sorted(map(tuple, np.unique(grp, axis=0).tolist()), key=lambda k: (-k[1], k[0], k[2])):
+            sel = np.flatnonzero(np.all(grp == np.array(key), axis=1))
+            bsel = _ranges_np(cuts[sel], nblk[sel])
+            panels = (d.c_off[order[cuts[sel]]], K[sel], d.c_nr[order[cuts[sel]]],
+                      (bstart[bsel], blen[bsel]), rs.coef_off[sn[cuts[sel]]], acc[sel])
+            P = self._phase("coupling", int(rowh[sel].max()), panels, d.coup, None, self.xhat, None,
+                            self.yhat, ordered=ordered)
+            cpl.append((P, int(colh[sel].max()), set(rowh[sel].tolist())))
+        return cpl
 
     def _xpos(self, p):
         """x_t buffer position of tree position p (index ranges never
@@ -526,48 +566,70 @@ class PanelPlan:
                 "gc_gather_inv", ptr(self.x), ptr(self.iperm_in), self.n_in, ptr(self.xt), st()),
                 native=(2, [self.x.data_ptr(), self.iperm_in.data_ptr(), self.n_in, self.xt.data_ptr()]),
                 launches=1)
+        # a shard with local-first blocks: its collectives run on their own
+        # stream, the local near field and the forward transform start from
+        # the own slice, the remote blocks follow the all-gathers
+        split = self._col_local is not None
         g = z
         if gather:
             gather.deps = dl(z)
             g = add(gather)
+        g_own = g
         for n in after_gather:
             n.deps = dl(g)
+            if split:
+                n.stream = "comm"
             g = add(n)
-        last = g
+        g_x = g
+        first = g_own if split else g_x
+        last = first
         fwd_done = []                                   # (max height covered, node)
-        near = add(_Node("nearfield", "near", dl(g), phase=self._near)) if self._near.nitems else None
+        near = add(_Node("nearfield", "near", dl(first), phase=self._near)) if self._near.nitems else None
         for P in self._fwd:
             if P.nitems:
                 last = add(_Node("forward", "chain", dl(last), phase=P, priority=greatest))
                 fwd_done.append((P.height, last))
         gate = None
         if before_coupling is not None:
-            before_coupling.deps = dl(last)
+            before_coupling.deps = dl(last, g_x if split else None)
+            if split:
+                before_coupling.stream = "comm"
             gate = add(before_coupling)
-        bucket = {}
+        bucket = {}                                     # row height -> coupling nodes
+
+        def prio_of(P):
+            if P.height >= S or levels < 2:
+                return greatest
+            pr = least - 1 - int(round(P.height * (levels - 2) / max(S - 1, 1)))
+            return min(least - 1, max(greatest + 1, pr))
+
         for P, colh, heights in sorted(self._cpl, key=lambda c: c[0].height):
-            if gate is not None:
+            if gate is not None and not split:
                 dep = [gate]
             else:
                 dep = [next((k for hh, k in fwd_done if hh >= colh), last)]
-            if P.height >= S or levels < 2:
-                prio = greatest
-            else:
-                prio = least - 1 - int(round(P.height * (levels - 2) / max(S - 1, 1)))
-                prio = min(least - 1, max(greatest + 1, prio))
-            k = add(_Node("coupling", "c%d" % P.height, dl(*dep, z), phase=P, priority=prio))
+            k = add(_Node("coupling", "c%d" % P.height, dl(*dep, z), phase=P, priority=prio_of(P)))
             for hh in heights:
-                bucket[hh] = k
-        prev = gate if gate is not None else last
+                bucket.setdefault(hh, []).append(k)
+        for P, colh, heights in sorted(self._cpl_remote, key=lambda c: c[0].height):
+            # after the x-hat all-gather and after the local phases that
+            # wrote the rows it adds onto
+            local = sorted({k for hh in heights for k in bucket.get(hh, [])})
+            k = add(_Node("coupling", "c%d" % P.height, dl(gate, z) + local, phase=P, priority=prio_of(P)))
+            for hh in heights:
+                bucket.setdefault(hh, []).append(k)
+        allb = sorted({k for ks in bucket.values() for k in ks})
+        prev = gate if (gate is not None and not split) else last
         for P, hs in self._bwd:
             if P.nitems:
-                prev = add(_Node("backward", "chain", dl(prev) + sorted({bucket[x] for x in hs if x in bucket}),
-                                 phase=P, priority=greatest))
+                need = sorted({k for x in hs for k in bucket.get(x, [])})
+                prev = add(_Node("backward", "chain", dl(prev) + need, phase=P, priority=greatest))
         for P, hs in self._leafparts:
-            need = (sorted(set(bucket.values())) if hs is None
-                    else sorted({bucket[x] for x in hs if x in bucket}))
+            need = allb if hs is None else sorted({k for x in hs for k in bucket.get(x, [])})
             prev = add(_Node("leafbasis", "chain", dl(prev) + need, phase=P, priority=greatest))
-        tail = dl(prev) + sorted(set(bucket.values()))
+        if self._near_remote is not None and self._near_remote.nitems:
+            near = add(_Node("nearfield", "near", dl(g_x, near), phase=self._near_remote))
+        tail = dl(prev) + allb
         if near is not None:
             tail = tail + [near]
         if scatter is True:
@@ -632,7 +694,8 @@ class PanelPlan:
             main.wait_event(events[last])
 
     # -- phases --------------------------------------------------------------
-    def _phase(self, name, height, panels, A0, A1, in0, in1, out, transform=False, sum_inputs=False):
+    def _phase(self, name, height, panels, A0, A1, in0, in1, out, transform=False, sum_inputs=False,
+               ordered=False):
         """Work items of one phase.  panels = (a_off, K, T, rows, out_off,
         accumulate): panel p is the K x T row-major block at A[a_off] whose
         row k multiplies in[idx] (rows = (starts, lengths) index ranges,
@@ -674,15 +737,18 @@ class PanelPlan:
         direct = ~multi[item_panel]
         out_col = np.where(direct, out_off[item_panel],
                            scr_off[item_panel] + item_idx_in_panel * T[item_panel])
-        mode = np.where(direct, 4 | (8 * accumulate), 0) | (32 if sum_inputs else 0)
+        acc = np.broadcast_to(np.asarray(accumulate, np.int64), (n,))      # per panel
+        mode = np.where(direct, 4 | (8 * acc[item_panel]), 0) | (32 if sum_inputs else 0)
         items = np.stack([a_off[item_panel] + item_k * T[item_panel], xoff[item_panel] + item_k,
                           out_col, T[item_panel], item_rows, mode,
                           np.where(direct, -1, slot[item_panel]), np.zeros_like(mode)], 1).reshape(-1, 8)
-        red = np.stack([out_off[multi], T[multi], scr_off[multi], nit[multi],
-                        np.full(int(multi.sum()), accumulate)], 1)
+        red = np.stack([out_off[multi], T[multi], scr_off[multi], nit[multi], acc[multi]], 1)
         P = _Phase()
         P.name, P.height = name, height
-        P.acc = bool(n and accumulate)              # some item adds into its output
+        # some item adds into an output that no earlier phase of the same
+        # product wrote (``ordered``: the phase only adds onto outputs its
+        # dependencies wrote) - the product then needs its memset
+        P.acc = bool(n and acc.any() and not ordered)
         # two whole small panels per CTA (k_panel_pair) in the tier phases
         # whose items all fit: half the CTAs, half the waves of round trips
         P.pair = bool(transform and self.tiers_pending and n and bool(np.all(direct)) and int(T.max()) <= 128

@@ -259,11 +259,16 @@ def _shard_plan_class():
         ranks' tree-ordered slices, each padded to the longest shard (slot
         g at g * maxs: NCCL needs equal sizes), and every x_t index of the
         plan is mapped into it.  Per product: the own slice lands in the
-        own slot, the x all-gather (in place), the forward transform of the
-        own column subtree, the x-hat all-gather (in place) gating the
-        coupling buckets, coupling, backward transform, near field and leaf
-        rows, then y_own = y_t + y_t2 over the own rows (gc_scatter2_inv).
-        Over NCCL the whole slice product is one CUDA graph."""
+        own slot; then, concurrently, the x all-gather (in place, on its own
+        stream) and the forward transform of the own column subtree and the
+        near-field blocks with local columns; the x-hat all-gather (in
+        place); the coupling blocks with local columns run as soon as the
+        forward tiers they read are done, those with remote columns after
+        the x-hat all-gather (adding onto the same y-hat rows), likewise the
+        remote near-field blocks after the x all-gather; backward transform
+        and leaf rows; y_own = y_t + y_t2 over the own rows
+        (gc_scatter2_inv).  Over NCCL the whole slice product is one CUDA
+        graph."""
 
         def __init__(self, sh):
             import torch
@@ -278,7 +283,7 @@ def _shard_plan_class():
             n = int(lo_hi[-1, 1])
             owner = np.repeat(np.arange(world), sizes)
             xmap = owner * maxs + (np.arange(n) - lo_hi[owner, 0])      # tree -> padded position
-            super().__init__(sh.h, xt_map=xmap, xt_len=world * maxs)
+            super().__init__(sh.h, xt_map=xmap, xt_len=world * maxs, col_local=(self.lo, self.hi))
             dev = self.dev
             d = sh.h.dev
             m_own = self.hi - self.lo

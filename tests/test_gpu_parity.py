@@ -589,6 +589,11 @@ def _sharded_worker(rank, world, port, out_dir, level, cfg_kw):
         np.save(os.path.join(out_dir, "lo%d.npy" % rank), np.array([sh.layout.lo, sh.layout.hi]))
         # the reference-order API: full x in, full y out on every rank
         np.save(os.path.join(out_dir, "ext%d.npy" % rank), sh.mvm(x))
+        # a second vector: the remote blocks must read this product's
+        # all-gathered data, not the previous product's
+        x2 = np.random.default_rng(4).standard_normal(n)
+        xt2 = torch.from_numpy(x2[perm][sh.layout.lo:sh.layout.hi].copy()).cuda()
+        np.save(os.path.join(out_dir, "y2_%d.npy" % rank), sh.mvm_slice(xt2).cpu().numpy())
     finally:
         dist.destroy_process_group()
 
@@ -627,6 +632,13 @@ def test_sharded_operator_multirank_matches_full(world, level, cfg_kw, tmp_path)
     for g in range(world):
         ye = np.load(tmp_path / ("ext%d.npy" % g))
         assert np.linalg.norm(ye - ref) <= 1e-13 * np.linalg.norm(ref)
+    x2 = np.random.default_rng(4).standard_normal(n)
+    for g in range(world):
+        lo, hi = np.load(tmp_path / ("lo%d.npy" % g))
+        yt[lo:hi] = np.load(tmp_path / ("y2_%d.npy" % g))
+    y[tree.perm] = yt
+    ref2 = h2.mvm(hm, x2)
+    assert np.linalg.norm(y - ref2) <= 1e-13 * np.linalg.norm(ref2)
     if cfg_kw.get("basis") == "linear" and world == 4:
         assert len(set(sizes)) > 1               # the padded all-gather path ran
 

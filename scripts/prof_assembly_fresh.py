@@ -56,6 +56,7 @@ for rep in range(1):
     t2 = time.perf_counter()
     print("level %d: operator %.4f s + plan %.4f s = %.4f s   %s" % (
         level, t1 - t0, t2 - t1, t2 - t0, {k: round(v, 4) for k, v in tm.items()}))
+    print("plan timing:", {k: round(v, 4) for k, v in h2.plan(hm).timing.items()})
 s = io.StringIO()
 pstats.Stats(pr, stream=s).sort_stats("cumulative").print_stats(40)
 print(s.getvalue()[:8000])

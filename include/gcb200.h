@@ -215,14 +215,6 @@ int gc_aca(int64_t nn, const int64_t* desc, int64_t W, double eps,
            int64_t max_rank, double* fac, int64_t* piv, int64_t* rank,
            double* v, double* u, int64_t max_rows, void* stream);
 
-/* gc_aca over a subset of the nodes: nodes [dev] (nn) indices into desc
- * and rank, a fixed CTA width nt (256 or 1024; gc_aca picks 1024 for fewer
- * than 148 nodes of >= 4096 factor entries), shared memory sized by
- * max_rows of the subset.  Per-node results equal gc_aca's at the same nt. */
-int gc_aca_nodes(int64_t nn, const int64_t* nodes, const int64_t* desc, int64_t W, double eps,
-                 int64_t max_rank, double* fac, int64_t* piv, int64_t* rank, double* v, double* u,
-                 int64_t max_rows, int32_t nt, void* stream);
-
 /* ---------------------------------------------------------------------
  * H2 matvec building blocks (h2.mvm, h2.py:19-80)
  * ------------------------------------------------------------------- */

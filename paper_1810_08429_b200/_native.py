@@ -57,8 +57,6 @@ _SIGNATURES = {
     "gc_green_factor": [ctypes.POINTER(GcGeom), ctypes.c_int, c_i64, c_i64, c_p, c_p, c_p,
                         c_p, c_p, c_p, c_p, c_p, c_p],
     "gc_aca": [c_i64, c_p, c_i64, ctypes.c_double, c_i64, c_p, c_p, c_p, c_p, c_p, c_i64, c_p],
-    "gc_aca_nodes": [c_i64, c_p, c_p, c_i64, ctypes.c_double, c_i64, c_p, c_p, c_p, c_p, c_p, c_i64,
-                     ctypes.c_int32, c_p],
     "gc_gather": [c_p, c_p, c_i64, c_p, c_p],
     "gc_scatter": [c_p, c_p, c_i64, c_p, c_p],
     "gc_scatter2": [c_p, c_p, c_p, c_i64, c_p, c_p],

@@ -57,10 +57,9 @@ template <int NT>
 __global__ void __launch_bounds__(NT) k_aca(const int64_t* __restrict__ desc, int W, double eps,
                                             int max_rank, double* fac, int64_t* __restrict__ piv_out,
                                             int64_t* __restrict__ rank_out, double* __restrict__ v_out,
-                                            double* __restrict__ u, int max_rows, int resid_in_smem,
-                                            const int64_t* __restrict__ nodes) {
+                                            double* __restrict__ u, int max_rows, int resid_in_smem) {
     extern __shared__ double smem[];
-    const int node = nodes ? (int)nodes[blockIdx.x] : (int)blockIdx.x;
+    const int node = blockIdx.x;
     const int64_t fac_off = desc[4 * node], piv_off = desc[4 * node + 2], v_off = desc[4 * node + 3];
     const int R = (int)desc[4 * node + 1];
     int limit = max_rank > 0 ? max_rank : W;
@@ -161,7 +160,7 @@ using namespace gcb;
 template <int NT>
 static int launch_aca(int64_t nn, const int64_t* desc, int64_t W, double eps, int64_t max_rank,
                       double* fac, int64_t* piv, int64_t* rank, double* v, double* u,
-                      int64_t max_rows, cudaStream_t st, const int64_t* nodes = nullptr) {
+                      int64_t max_rows, cudaStream_t st) {
     const size_t tail = (size_t)W * 8 + (size_t)(max_rows + 1) * 8 * 2 + (NT / 32) * 24 + 16;
     const size_t resid = (size_t)max_rows * W * 8;
     const int in_smem = (resid + tail) <= 200 * 1024;
@@ -170,7 +169,7 @@ static int launch_aca(int64_t nn, const int64_t* desc, int64_t W, double eps, in
     cudaError_t e = cudaFuncSetAttribute(k_aca<NT>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes);
     if (e != cudaSuccess) return cuda_status(e, "gc_aca smem attribute");
     k_aca<NT><<<(unsigned)nn, NT, bytes, st>>>(desc, (int)W, eps, (int)max_rank, fac, piv, rank, v, u,
-                                               (int)max_rows, in_smem, nodes);
+                                               (int)max_rows, in_smem);
     GC_CHECK_LAUNCH("k_aca");
     return GC_OK;
 }
@@ -187,24 +186,4 @@ extern "C" int gc_aca(int64_t nn, const int64_t* desc, int64_t W, double eps, in
     if (nn < 148 && max_rows * W >= 4096)
         return launch_aca<1024>(nn, desc, W, eps, max_rank, fac, piv, rank, v, u, max_rows, st);
     return launch_aca<256>(nn, desc, W, eps, max_rank, fac, piv, rank, v, u, max_rows, st);
-}
-
-// gc_aca over the subset `nodes` [dev] (nn indices into desc / rank) with a
-// fixed CTA width nt (256 or 1024): the caller launches the nodes of one
-// tree level in classes of similar row counts, so the shared-memory
-// residual (max_rows x W) is sized per class and small nodes are not held
-// to the occupancy of the level's largest one.  Per-node results are those
-// of gc_aca with the same nt.
-extern "C" int gc_aca_nodes(int64_t nn, const int64_t* nodes, const int64_t* desc, int64_t W, double eps,
-                            int64_t max_rank, double* fac, int64_t* piv, int64_t* rank, double* v, double* u,
-                            int64_t max_rows, int32_t nt, void* stream) {
-    if (nn <= 0) return GC_OK;
-    if (!nodes || (nt != 256 && nt != 1024)) { set_error(GC_ERR_CONFIG, "gc_aca_nodes: bad arguments"); return GC_ERR_CONFIG; }
-    if (W <= 0 || max_rows < 0) { set_error(GC_ERR_CONFIG, "gc_aca: bad shape"); return GC_ERR_CONFIG; }
-    if (!(eps >= 0.0)) { set_error(GC_ERR_CONFIG, "gc_aca: eps must be >= 0"); return GC_ERR_CONFIG; }
-    if (max_rows * W >= (1LL << 31)) { set_error(GC_ERR_CONFIG, "gc_aca: factor too large"); return GC_ERR_CONFIG; }
-    cudaStream_t st = (cudaStream_t)stream;
-    if (nt == 1024)
-        return launch_aca<1024>(nn, desc, W, eps, max_rank, fac, piv, rank, v, u, max_rows, st, nodes);
-    return launch_aca<256>(nn, desc, W, eps, max_rank, fac, piv, rank, v, u, max_rows, st, nodes);
 }

@@ -516,25 +516,8 @@ def build_cluster_bases(tree, mesh, basis, m, delta_factor, eps, sides, orders=(
         small = torch.zeros(max(int(limit.sum()), 1) + nn + 1, dtype=torch.int64, device=dev)
         d_piv, d_rank = small[:max(int(limit.sum()), 1)], small[-nn - 1:-1]
         with torch.cuda.device(dev):
-            if nn < 148 and int(R.max()) * W >= 4096:
-                # few large nodes (top levels): one 1024-thread CTA each
-                _native.call("gc_aca", nn, ptr(adesc), W, float(eps), 0, ptr(fac), ptr(d_piv),
-                             ptr(d_rank), ptr(V), ptr(U), int(R.max()), stream)
-            else:
-                # 256-thread CTAs launched per class of row counts, so the
-                # shared-memory residual of a class fits its own nodes (one
-                # level-wide size held every CTA to the largest node's
-                # occupancy); per-node results are the same
-                cls = np.minimum(np.ceil(np.log2(np.maximum(R, 1))).astype(np.int64), 20)
-                kinds = np.unique(cls)
-                sub = to_dev(np.concatenate([np.flatnonzero(cls == c) for c in kinds]).astype(np.int64), dev)
-                o = 0
-                for c in kinds:
-                    members = np.flatnonzero(cls == c)
-                    _native.call("gc_aca_nodes", len(members), ptr(sub[o:o + len(members)]), ptr(adesc), W,
-                                 float(eps), 0, ptr(fac), ptr(d_piv), ptr(d_rank), ptr(V), ptr(U),
-                                 int(R[members].max()), 256, stream)
-                    o += len(members)
+            _native.call("gc_aca", nn, ptr(adesc), W, float(eps), 0, ptr(fac), ptr(d_piv),
+                         ptr(d_rank), ptr(V), ptr(U), int(R.max()), stream)
             small[-1:].copy_(flags.to(torch.int64))
         host = small.cpu().numpy()                 # the level's only sync
         if host[-1] & 1:

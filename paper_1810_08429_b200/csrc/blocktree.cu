@@ -5,7 +5,6 @@
 // the children of every subdivided pair appended grouped by child slot
 // (row child a, column child b; a-major) and, inside a group, by parent.
 // Host code only; no device memory involved.
-#pragma GCC optimize("fp-contract=off")
 #include <cmath>
 #include <cstdint>
 #include <algorithm>
@@ -15,18 +14,22 @@
 
 namespace {
 
-// numpy's elementwise sqrt((g0*g0 + g1*g1) + g2*g2): this file is built
-// without floating-point contraction (the pragma above), so every product
-// and sum rounds separately as in numpy
+// numpy's elementwise sqrt((g0*g0 + g1*g1) + g2*g2): every product and sum
+// rounds separately (volatile: no contraction whatever the host flags)
 double norm3_plain(double a, double b, double c) {
-    return std::sqrt((a * a + b * b) + c * c);
+    volatile double aa = a * a, bb = b * b, cc = c * c;
+    volatile double s = (double)aa + (double)bb;
+    return std::sqrt((double)s + (double)cc);
 }
 
 // the 1-D numpy norm (np.linalg.norm of a 3-vector) in the rounding
 // sequence gc_host_norm3 reproduces (mode found by clustering.blas_norms)
 double norm3_blas(double x, double y, double z, int mode) {
-    const double s = mode == 0 ? std::fma(z, z, std::fma(y, y, x * x)) : (x * x + y * y) + z * z;
-    return std::sqrt(s);
+    volatile double xx = x * x;
+    if (mode == 0) return std::sqrt(std::fma(z, z, std::fma(y, y, (double)xx)));
+    volatile double yy = y * y, zz = z * z;
+    volatile double t = (double)xx + (double)yy;
+    return std::sqrt((double)t + (double)zz);
 }
 
 struct Tree {

@@ -296,6 +296,11 @@ int gc_panelmv(int64_t nitems, const int64_t* items, const int32_t* xidx,
 int gc_plan_create(int64_t n, const int64_t* nodes, int64_t ndeps, const int64_t* deps, int64_t nstreams,
                    const int32_t* stream_prio, void** plan);
 int gc_plan_run(void* plan, const double* x, double* y, void* stream);
+/* h2.mvm in one call: copies n_in doubles of host x into the pinned
+ * staging buffer x_pinned, runs the plan reading x_pinned and writing the
+ * pinned y_pinned over the host link, and synchronises `stream`. */
+int gc_plan_run_host(void* plan, const double* x_host, double* x_pinned, int64_t n_in, double* y_pinned,
+                     void* stream);
 int gc_plan_destroy(void* plan);
 
 /* Tiered transforms (plan time; h2.py PanelPlan tiers): the composed

@@ -67,6 +67,7 @@ _SIGNATURES = {
     "gc_gather_inv": [c_p, c_p, c_i64, c_p, c_p],
     "gc_plan_create": [c_i64, c_p, c_i64, c_p, c_i64, c_p, c_p],
     "gc_plan_run": [c_p, c_p, c_p, c_p],
+    "gc_plan_run_host": [c_p, c_p, c_p, c_i64, c_p, c_p],
     "gc_plan_destroy": [c_p],
     "gc_scatter2_inv": [c_p, c_p, c_p, c_i64, c_p, c_p],
     "gc_block_transpose": [c_i64, c_p, c_p, c_p, c_p],

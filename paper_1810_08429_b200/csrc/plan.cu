@@ -5,6 +5,7 @@
 // builds the phase descriptors; gc_plan_run re-points the graph's gather /
 // scatter nodes at the caller's x / y when they change
 // (cudaGraphExecKernelNodeSetParams) and launches the executable graph.
+#include <cstring>
 #include <vector>
 
 #include "common.cuh"
@@ -210,6 +211,23 @@ extern "C" int gc_plan_run(void* plan, const double* x, double* y, void* stream)
     }
     cudaError_t e = cudaGraphLaunch(p->exec, (cudaStream_t)stream);
     if (e != cudaSuccess) return cuda_status(e, "gc_plan_run");
+    return GC_OK;
+}
+
+// The synchronous host-vector product (h2.mvm) as one call: copy the
+// caller's host x (any host memory, n_in doubles) into the pinned staging
+// buffer x_pinned, run the graph reading x_pinned and writing the pinned y
+// directly (over the host link), and wait for it on `stream`.
+extern "C" int gc_plan_run_host(void* plan, const double* x_host, double* x_pinned, int64_t n_in, double* y_pinned,
+                                void* stream) {
+    if (!x_host || !x_pinned || !y_pinned || n_in < 0) {
+        set_error(GC_ERR_CONFIG, "gc_plan_run_host: bad arguments");
+        return GC_ERR_CONFIG;
+    }
+    std::memcpy(x_pinned, x_host, (size_t)n_in * sizeof(double));
+    if (int rc = gc_plan_run(plan, x_pinned, y_pinned, stream)) return rc;
+    cudaError_t e = cudaStreamSynchronize((cudaStream_t)stream);
+    if (e != cudaSuccess) return cuda_status(e, "gc_plan_run_host");
     return GC_OK;
 }
 

@@ -17,6 +17,7 @@ values stay in HBM in the matvec layout (``h2.py``) and reach the host only
 through the lazy ``.values`` / ``.v`` / ``.transfer`` views.
 """
 
+import threading
 import time
 import weakref
 from collections import namedtuple
@@ -625,15 +626,19 @@ class H2Matrix:
         self.nearfield = nearfield
         self._exec_stats = exec_stats
         self._settle = None
+        self._settle_lock = threading.Lock()
         self.dev = dev
 
     def settle(self):
         """Wait for the device assembly (build_h2 returns while its
         quadrature runs), check its queue flags and fix the executor
-        statistics; idempotent.  Every reader of block data calls it."""
+        statistics; idempotent and thread-safe.  Every reader of block data
+        calls it."""
         if self._settle is not None:
-            fn, self._settle = self._settle, None
-            self._exec_stats = fn()
+            with self._settle_lock:
+                if self._settle is not None:
+                    self._exec_stats = self._settle()
+                    self._settle = None
         return self
 
     @property

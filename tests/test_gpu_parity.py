@@ -221,6 +221,19 @@ def test_pipeline_storage_and_stats(built):
     assert all(s["wall_s"] >= 0.0 for s in hm.exec_stats)
 
 
+def test_build_h2_returns_before_the_quadrature_settles():
+    """build_h2 (plane charts) does not synchronise: the statistics settle on
+    first use, once, and equal a synchronous rebuild's."""
+    mesh = geometry.build_sphere_mesh(3)
+    cfg = cli.default_config(eps=1e-4)
+    hm, tree, bt = cli.build_h2_operator(mesh, cfg)
+    assert hm._settle is not None                       # still pending
+    st = hm.exec_stats
+    assert hm._settle is None and hm.settle().exec_stats == st
+    assert [s["tasks"] for s in st] == [s["tasks"] for s in cli.build_h2_operator(mesh, cfg)[0].exec_stats]
+    assert all(s["wall_s"] > 0.0 for s in st if s["tasks"])
+
+
 def test_stats_report(built, tmp_path):
     """``greencross stats`` CSV (pkg/tests/test_cli.py:145-154): header,
     case names, tasks / batches / seconds per case."""

@@ -202,6 +202,8 @@ _ITEM_ELEMS = 65536          # <= 512 KB of matrix data per bulk work item (rows
 _ITEM_MAX_ROWS = 1024        # PAN_MAX_ROWS in csrc/h2mv.cu
 _PAIR_MAX_ELEMS = 8192       # k_panel_pair (two small panels per CTA): panel size cap
 _RING_MIN_BYTES = 256 << 20  # bulk phases this large stream through k_panel_ring (measured: C4 +5 %, C2 -8 %)
+_PAIR_BULK_MAX_BYTES = 32 << 20    # small operators: bulk phases paired like the tier phases
+_SMALL_OPERATOR_BYTES = 128 << 20
 _MERGE_MIN_BYTES = 1 << 30   # coupling row heights with the same producer / consumer merge into one launch
 
 
@@ -248,6 +250,14 @@ class PanelPlan:
         t0 = time.perf_counter()
         self.timing = {}
         self._bulk = bulk
+        # a small operator (<= _SMALL_OPERATOR_BYTES of blocks) is latency-
+        # bound throughout: its bulk phases of <= _PAIR_BULK_MAX_BYTES run one
+        # item per panel, two panels per CTA.  Measured (profiles/sweeps/
+        # r02_pair_bulk*.txt): sphere L4 eps 1e-4 (18 MB) 23.5 -> 18.6 us,
+        # L5 eps 1e-4 (80 MB) 48 -> 37 us; L5 eps 1e-6 (166 MB) 52 -> 66 us,
+        # neutral to slower from L6 on - hence the operator bound
+        blocks = 8 * (h.dev.coup.numel() + h.dev.near.numel())
+        self._pair_bulk = _PAIR_BULK_MAX_BYTES if blocks <= _SMALL_OPERATOR_BYTES else 0
         d = h.dev
         dev = d.device
         self.dev = dev
@@ -715,7 +725,10 @@ class PanelPlan:
         elems = int((K * T).sum())
         ring = bool(not transform and n and int(T.max()) <= 256
                     and (self._bulk == "ring" or (self._bulk == "auto" and 8 * elems >= _RING_MIN_BYTES)))
-        if transform:
+        # small bulk phases (a few MB: the latency-bound products of small
+        # operators) get one item per panel, paired like the tier phases
+        small_bulk = bool(not transform and n and 8 * elems <= self._pair_bulk)
+        if transform or small_bulk:
             target = 1 << 40
         else:
             target = max(256, min(_ITEM_ELEMS, elems // (148 * 4) + 1))
@@ -751,7 +764,8 @@ class PanelPlan:
         P.acc = bool(n and acc.any() and not ordered)
         # two whole small panels per CTA (k_panel_pair) in the tier phases
         # whose items all fit: half the CTAs, half the waves of round trips
-        P.pair = bool(transform and self.tiers_pending and n and bool(np.all(direct)) and int(T.max()) <= 128
+        P.pair = bool(((transform and self.tiers_pending) or small_bulk) and n and bool(np.all(direct))
+                      and int(T.max()) <= 128
                       and int(item_rows.max()) <= 512
                       and int((item_rows * T[item_panel]).max()) <= _PAIR_MAX_ELEMS)
         if P.pair:   # pair equal-sized panels, largest first

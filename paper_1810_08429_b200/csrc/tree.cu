@@ -5,12 +5,16 @@
 //   * k_seg_keys  - the split coordinate of every dof of every splitting
 //                   node (-0.0 canonicalised to +0.0: numpy's comparison
 //                   sort treats them as equal, a radix sort would not);
-//   * CUB DeviceSegmentedSort::StableSortPairs - the stable per-node sort
-//                   (the reference's argsort(kind="stable"));
+//   * two stable CUB radix sorts - by the key, then by the segment (LSD
+//                   order: segments in place, keys ascending inside, ties in
+//                   row order) - the reference's per-node argsort(kind=
+//                   "stable"); one launch pair over all nodes of the depth
+//                   (CUB's segmented sort falls back to one-block sorts for
+//                   the large top-level segments);
 //   * k_seg_permute - applies the order to the permutation and to the
 //                   packed (lo | hi | point) rows.
 // The host keeps the per-node bookkeeping (frontier, child ids, axes).
-#include <cub/device/device_segmented_sort.cuh>
+#include <cub/device/device_radix_sort.cuh>
 
 #include "common.cuh"
 
@@ -68,6 +72,21 @@ __global__ void __launch_bounds__(TREE_THREADS) k_seg_keys(int64_t nseg, const i
     }
 }
 
+// seg[j] = the segment whose rows [start[s], start[s] + len[s]) hold row[j]
+// (segment starts ascending)
+__global__ void k_seg_of(int64_t n, int64_t nseg, const int64_t* __restrict__ start, const int32_t* __restrict__ row,
+                         int32_t* __restrict__ seg) {
+    for (int64_t j = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; j < n; j += (int64_t)gridDim.x * blockDim.x) {
+        const int64_t r = row[j];
+        int64_t lo = 0, hi = nseg;                  // first start > r
+        while (lo < hi) {
+            const int64_t mid = (lo + hi) >> 1;
+            if (start[mid] <= r) lo = mid + 1; else hi = mid;
+        }
+        seg[j] = (int32_t)(lo - 1);
+    }
+}
+
 // new[dst[i]] = old[src[i]] for the permutation and the packed rows
 __global__ void k_seg_permute(int64_t n, const int32_t* __restrict__ dst, const int32_t* __restrict__ src,
                               const int64_t* __restrict__ perm_old, int64_t* __restrict__ perm_new,
@@ -95,13 +114,15 @@ extern "C" int gc_tree_boxes(int64_t nseg, const int64_t* start, const int64_t* 
 
 // CUB temp-storage bytes of a split step with nitems dofs in nseg segments
 extern "C" int gc_tree_sort_bytes(int64_t nitems, int64_t nseg, int64_t* bytes) {
-    size_t tb = 0;
-    cudaError_t e = cub::DeviceSegmentedSort::StableSortPairs(nullptr, tb, (const double*)nullptr, (double*)nullptr,
-                                                              (const int32_t*)nullptr, (int32_t*)nullptr, (int)nitems,
-                                                              (int)nseg, (const int32_t*)nullptr,
-                                                              (const int32_t*)nullptr, (cudaStream_t)0);
+    (void)nseg;
+    size_t t1 = 0, t2 = 0;
+    cudaError_t e = cub::DeviceRadixSort::SortPairs(nullptr, t1, (const double*)nullptr, (double*)nullptr,
+                                                    (const int32_t*)nullptr, (int32_t*)nullptr, (int)nitems);
+    if (e == cudaSuccess)
+        e = cub::DeviceRadixSort::SortPairs(nullptr, t2, (const int32_t*)nullptr, (int32_t*)nullptr,
+                                            (const int32_t*)nullptr, (int32_t*)nullptr, (int)nitems);
     if (e != cudaSuccess) return cuda_status(e, "gc_tree_sort_bytes");
-    *bytes = (int64_t)tb;
+    *bytes = (int64_t)(t1 > t2 ? t1 : t2);
     return GC_OK;
 }
 
@@ -126,14 +147,27 @@ extern "C" int gc_tree_split(int64_t nseg, const int64_t* seg_start, const int64
     k_seg_keys<<<(unsigned)grid, TREE_THREADS, 0, st>>>(nseg, seg_start, seg_len, seg_head, seg_axis, pack_old,
                                                         keys, vals);
     GC_CHECK_LAUNCH("k_seg_keys");
+    (void)offsets;
+    // pass 1: all items by key (stable); pass 2: by segment (stable).  The
+    // key buffers are dead after pass 1: they hold the segment ids
+    // (keys[0..n)) and the final source rows (keys_out[0..n)).
     size_t tb = (size_t)temp_bytes;
-    cudaError_t e = cub::DeviceSegmentedSort::StableSortPairs(temp, tb, keys, keys_out, vals, vals_out,
-                                                              (int)nitems, (int)nseg, offsets, offsets + 1, st);
-    if (e != cudaSuccess) return cuda_status(e, "gc_tree_split sort");
-    count_launch();
+    cudaError_t e = cub::DeviceRadixSort::SortPairs(temp, tb, keys, keys_out, vals, vals_out, (int)nitems, 0, 64, st);
+    if (e != cudaSuccess) return cuda_status(e, "gc_tree_split sort (key)");
+    int32_t* segk = reinterpret_cast<int32_t*>(keys);
+    int32_t* segk_out = segk + nitems;
+    int32_t* src_final = reinterpret_cast<int32_t*>(keys_out);
     int64_t pgrid = (nitems + 255) / 256;
     if (pgrid > 148 * 32) pgrid = 148 * 32;
-    k_seg_permute<<<(unsigned)pgrid, 256, 0, st>>>(nitems, vals, vals_out, perm_old, perm_new, pack_old, pack_new);
+    k_seg_of<<<(unsigned)pgrid, 256, 0, st>>>(nitems, nseg, seg_start, vals_out, segk);
+    GC_CHECK_LAUNCH("k_seg_of");
+    int end_bit = 1;
+    while (end_bit < 31 && (1LL << end_bit) < nseg) ++end_bit;
+    tb = (size_t)temp_bytes;
+    e = cub::DeviceRadixSort::SortPairs(temp, tb, segk, segk_out, vals_out, src_final, (int)nitems, 0, end_bit, st);
+    if (e != cudaSuccess) return cuda_status(e, "gc_tree_split sort (segment)");
+    count_launch(2);
+    k_seg_permute<<<(unsigned)pgrid, 256, 0, st>>>(nitems, vals, src_final, perm_old, perm_new, pack_old, pack_new);
     GC_CHECK_LAUNCH("k_seg_permute");
     return GC_OK;
 }

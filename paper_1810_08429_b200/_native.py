@@ -53,6 +53,11 @@ _SIGNATURES = {
     "gc_block_tree": [c_p, c_p, c_p, c_p, c_p, c_p, c_p, c_p, c_p, c_p, c_i64, c_i64, ctypes.c_double,
                       ctypes.c_int32, ctypes.c_int32, ctypes.POINTER(c_p), ctypes.POINTER(c_i64)],
     "gc_block_tree_fetch": [c_p, c_p, c_p, c_p, c_p, c_p, c_p],
+    "gc_bt_level_bytes": [c_i64, ctypes.POINTER(c_i64)],
+    "gc_bt_leaves_bytes": [c_i64, ctypes.POINTER(c_i64)],
+    "gc_bt_leaves": [c_i64] + [c_p] * 11 + [c_i64, c_p],
+    "gc_bt_level": [c_i64, c_p, c_p, c_p, c_p, c_i64, c_i64, ctypes.c_int32] + [c_p] * 10
+                   + [ctypes.c_double, ctypes.c_int32] + [c_p] * 14 + [c_i64, c_p],
     "gc_green_box_rules": [ctypes.c_int, c_p, c_p, c_i64, c_p, c_p, c_p, c_p, c_p],
     "gc_green_factor": [ctypes.POINTER(GcGeom), ctypes.c_int, c_i64, c_i64, c_p, c_p, c_p,
                         c_p, c_p, c_p, c_p, c_p, c_p],

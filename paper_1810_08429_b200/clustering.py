@@ -389,6 +389,7 @@ def _build_cluster_tree_device(mesh, basis_kind, leaf_size, device):
             d += 1
         perm_h = perm[cur].cpu().numpy()
     flat = FlatClusterTree(perm_h, start, stop, left, right, parent, depth, lower, upper)
+    flat._device = device            # the block tree of a device-built tree is built there too
     return flat.node(0)
 
 
@@ -461,16 +462,19 @@ class FlatBlockTree:
     (``leaf_ids``, ``leaf_key``).  ``key`` is the base-4 path code aligned
     to ``_KEY_DIGITS`` digits, so sorting by it is the reference DFS order."""
 
-    def __init__(self, row_tree, col_tree, row, col, state, level, key, parent_of):
+    def __init__(self, row_tree, col_tree, row, col, state, level, key, parent_of, leaves=None):
         self.row_tree, self.col_tree = row_tree, col_tree
         self.row, self.col, self.state, self.level, self.key = row, col, state, level, key
         self.parent_of = parent_of
         span = np.power(4, _KEY_DIGITS - level, dtype=np.int64)
         self.key_lo, self.key_hi = key, key + span
-        leaves = np.flatnonzero(state != 2)
-        order = np.argsort(key[leaves])          # keys are unique paths: any sort is the DFS order
-        self.leaf_ids = leaves[order]
-        self.leaf_key = key[self.leaf_ids]
+        if leaves is None:
+            leaves = np.flatnonzero(state != 2)
+            order = np.argsort(key[leaves])      # keys are unique paths: any sort is the DFS order
+            self.leaf_ids = leaves[order]
+            self.leaf_key = key[self.leaf_ids]
+        else:                                    # (ids, keys) already in DFS order
+            self.leaf_ids, self.leaf_key = leaves
         self._kid_index = None
 
     def kids(self, i):
@@ -529,6 +533,9 @@ def build_block_tree(row_root, col_root=None, eta=1.0):
     mode = _NORM_MODE[0]
     if mode is None:                             # numpy's norm matches neither sequence
         return _build_block_tree_arrays(row_root, col_root, eta)
+    dev = getattr(row_root.flat, "_device", None)
+    if dev is not None and (col_root.flat is row_root.flat or getattr(col_root.flat, "_device", None) == dev):
+        return _build_block_tree_device(row_root, col_root, eta, mode, dev)
     from . import _native
     rt, ct = row_root.flat, col_root.flat
     trees = []
@@ -546,6 +553,71 @@ def build_block_tree(row_root, col_root=None, eta=1.0):
                                            np.empty(n, np.int64), np.empty(n, np.int64), np.empty(n, np.int64))
     _native.check(lib.gc_block_tree_fetch(handle, *[a.ctypes.data for a in (row, col, state, level, key, parent)]))
     flat = FlatBlockTree(rt, ct, row, col, state, level, key, parent)
+    return BlockTree(flat, 0)
+
+
+def _build_block_tree_device(row_root, col_root, eta, mode, device):
+    """The block tree built on the device one level per ``gc_bt_level``
+    call (node for node equal to gc_block_tree and the numpy builder), the
+    node arrays copied to the host once at the end."""
+    import torch
+
+    from . import _native
+    from .device import ptr, stream_handle
+    rt, ct = row_root.flat, col_root.flat
+    i64 = dict(dtype=torch.int64, device=device)
+
+    def up(t):
+        f64 = dict(dtype=torch.float64, device=device)
+        return (torch.from_numpy(np.ascontiguousarray(t.diam, np.float64)).to(**f64),
+                torch.from_numpy(np.ascontiguousarray(t.lower, np.float64)).to(**f64),
+                torch.from_numpy(np.ascontiguousarray(t.upper, np.float64)).to(**f64),
+                torch.from_numpy(np.ascontiguousarray(t.left, np.int64)).to(**i64),
+                torch.from_numpy(np.ascontiguousarray(t.right, np.int64)).to(**i64))
+    with torch.cuda.device(device):
+        tr = up(rt)
+        tc = tr if ct is rt else up(ct)
+        cap = max(4096, 32 * (len(rt) + len(ct)))
+        out = [torch.empty(cap, **i64), torch.empty(cap, **i64), torch.empty(cap, dtype=torch.int8, device=device),
+               torch.empty(cap, **i64), torch.empty(cap, **i64), torch.empty(cap, **i64)]
+        front = [torch.tensor([int(row_root.index)], **i64), torch.tensor([int(col_root.index)], **i64),
+                 torch.zeros(1, **i64), torch.full((1,), -1, **i64)]
+        count = torch.zeros(1, **i64)
+        base, lev, m = 0, 0, 1
+        st = stream_handle()
+        while m:
+            if lev >= _KEY_DIGITS:
+                raise ConfigError("block tree deeper than %d levels" % _KEY_DIGITS)
+            if base + m > cap:                   # grow the node arrays
+                cap = max(2 * cap, base + m)
+                out = [torch.cat([o[:base], torch.empty(cap - base, dtype=o.dtype, device=device)]) for o in out]
+            nxt = [torch.empty(4 * m, **i64) for _ in range(4)]
+            scratch = torch.empty(8 * m, dtype=torch.int32, device=device)
+            tb = _native.ctypes.c_int64(0)
+            _native.call("gc_bt_level_bytes", m, _native.ctypes.byref(tb))
+            temp = torch.empty(max(tb.value, 1), dtype=torch.uint8, device=device)
+            _native.call("gc_bt_level", m, *[ptr(f) for f in front], base, lev, _KEY_DIGITS,
+                         *[ptr(a) for a in tr], *[ptr(a) for a in tc], float(eta), int(mode),
+                         *[ptr(o) for o in out], *[ptr(a) for a in nxt], ptr(count),
+                         ptr(scratch[:4 * m]), ptr(scratch[4 * m:]), ptr(temp), tb.value, st)
+            base += m
+            m = int(count.item())
+            front = [a[:m] for a in nxt]
+            lev += 1
+        n = base
+        # the leaves in depth-first order, sorted on the device
+        lids, lkey = torch.empty(n, **i64), torch.empty(n, **i64)
+        sc = [torch.empty(n, **i64) for _ in range(3)]
+        fl = torch.empty(2 * n, dtype=torch.int8, device=device)
+        tb = _native.ctypes.c_int64(0)
+        _native.call("gc_bt_leaves_bytes", n, _native.ctypes.byref(tb))
+        temp = torch.empty(max(tb.value, 1), dtype=torch.uint8, device=device)
+        _native.call("gc_bt_leaves", n, ptr(out[2]), ptr(out[4]), ptr(lids), ptr(lkey), ptr(count),
+                     *[ptr(a) for a in sc], ptr(fl[:n]), ptr(fl[n:]), ptr(temp), tb.value, st)
+        nl = int(count.item())
+        row, col, state, level, key, parent = (o[:n].cpu().numpy() for o in out)
+        leaf_ids, leaf_key = lids[:nl].cpu().numpy(), lkey[:nl].cpu().numpy()
+    flat = FlatBlockTree(rt, ct, row, col, state, level, key, parent, leaves=(leaf_ids, leaf_key))
     return BlockTree(flat, 0)
 
 

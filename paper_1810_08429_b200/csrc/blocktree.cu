@@ -10,6 +10,10 @@
 #include <algorithm>
 #include <vector>
 
+#include <cub/device/device_radix_sort.cuh>
+#include <cub/device/device_scan.cuh>
+#include <cub/device/device_select.cuh>
+
 #include "common.cuh"
 
 namespace {
@@ -164,6 +168,218 @@ int gc_block_tree_fetch(void* handle, int64_t* row, int64_t* col, int8_t* state,
     if (parent) std::copy(o->parent.begin(), o->parent.end(), parent);
     (void)n;
     delete o;
+    return GC_OK;
+}
+
+}  // extern "C"
+
+// ---------------------------------------------------------------------------
+// The same build on the device, one tree level per call (gc_bt_level): the
+// admissibility of every frontier pair (same rounding as above: explicit
+// round-to-nearest products and sums, no contraction), its node record at
+// out[base + i], and the children of the subdivided pairs written in the
+// host routine's order - grouped by child slot q = 2a + b, then by parent -
+// through one exclusive scan over the slot-major flags.
+
+namespace gcb {
+
+struct BtTree {
+    const double* diam;
+    const double* lower;
+    const double* upper;
+    const int64_t* left;
+    const int64_t* right;
+};
+
+__device__ __forceinline__ double bt_norm_plain(double a, double b, double c) {
+    return sqrt(__dadd_rn(__dadd_rn(__dmul_rn(a, a), __dmul_rn(b, b)), __dmul_rn(c, c)));
+}
+
+__device__ __forceinline__ double bt_norm_blas(double x, double y, double z, int mode) {
+    if (mode == 0) return sqrt(fma(z, z, fma(y, y, __dmul_rn(x, x))));
+    return sqrt(__dadd_rn(__dadd_rn(__dmul_rn(x, x), __dmul_rn(y, y)), __dmul_rn(z, z)));
+}
+
+__global__ void k_bt_eval(int64_t m, const int64_t* __restrict__ fr, const int64_t* __restrict__ fc,
+                          const int64_t* __restrict__ fkey, const int64_t* __restrict__ fpar, int64_t base,
+                          int64_t lev, BtTree R, BtTree C, double eta, int mode, int64_t* __restrict__ o_row,
+                          int64_t* __restrict__ o_col, int8_t* __restrict__ o_state, int64_t* __restrict__ o_level,
+                          int64_t* __restrict__ o_key, int64_t* __restrict__ o_parent, int32_t* __restrict__ flags) {
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < m; i += (int64_t)gridDim.x * blockDim.x) {
+        const int64_t r = fr[i], c = fc[i];
+        const double d = R.diam[r] > C.diam[c] ? R.diam[r] : C.diam[c];
+        double g[3];
+#pragma unroll
+        for (int k = 0; k < 3; ++k) {
+            const double a = __dsub_rn(R.lower[3 * r + k], C.upper[3 * c + k]);
+            const double b = __dsub_rn(C.lower[3 * c + k], R.upper[3 * r + k]);
+            const double mx = a >= b ? a : b;
+            g[k] = mx >= 0.0 ? mx : 0.0;
+        }
+        const double two_eta = __dmul_rn(2.0, eta);
+        const double rhs = __dmul_rn(two_eta, bt_norm_plain(g[0], g[1], g[2]));
+        const double big = d > rhs ? d : rhs;
+        bool adm;
+        if (fabs(__dsub_rn(d, rhs)) <= __dmul_rn(1e-12, big))
+            adm = d <= __dmul_rn(two_eta, bt_norm_blas(g[0], g[1], g[2], mode));
+        else
+            adm = d <= rhs;
+        const bool rs = R.left[r] >= 0, cs = C.left[c] >= 0;
+        const int8_t st = adm ? 0 : ((!rs && !cs) ? 1 : 2);
+        const int64_t id = base + i;
+        o_row[id] = r;
+        o_col[id] = c;
+        o_state[id] = st;
+        o_level[id] = lev;
+        o_key[id] = fkey[i];
+        o_parent[id] = fpar[i];
+        const bool sub = st == 2;
+        flags[i] = sub;                                   // (a, b) = (0, 0): always present
+        flags[m + i] = sub && cs;                         // (0, 1)
+        flags[2 * m + i] = sub && rs;                     // (1, 0)
+        flags[3 * m + i] = sub && rs && cs;               // (1, 1)
+    }
+}
+
+__global__ void k_bt_children(int64_t m, const int64_t* __restrict__ fr, const int64_t* __restrict__ fc,
+                              const int64_t* __restrict__ fkey, int64_t base, int64_t scale, BtTree R, BtTree C,
+                              const int32_t* __restrict__ flags, const int32_t* __restrict__ pos,
+                              int64_t* __restrict__ nr, int64_t* __restrict__ nc, int64_t* __restrict__ nk,
+                              int64_t* __restrict__ np, int64_t* __restrict__ count) {
+    for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < 4 * m; t += (int64_t)gridDim.x * blockDim.x) {
+        if (t == 4 * m - 1) *count = (int64_t)pos[t] + flags[t];
+        if (!flags[t]) continue;
+        const int q = (int)(t / m);
+        const int64_t i = t - (int64_t)q * m;
+        const int a = q >> 1, b = q & 1;
+        const int64_t r = fr[i], c = fc[i];
+        const bool rs = R.left[r] >= 0, cs = C.left[c] >= 0;
+        const int64_t rk = a == 0 ? (rs ? R.left[r] : r) : R.right[r];
+        const int64_t ck = b == 0 ? (cs ? C.left[c] : c) : C.right[c];
+        const int64_t dig = a * (cs ? 2 : 1) + b;
+        const int64_t p = pos[t];
+        nr[p] = rk;
+        nc[p] = ck;
+        nk[p] = fkey[i] + dig * scale;
+        np[p] = base + i;
+    }
+}
+
+}  // namespace gcb
+
+extern "C" {
+
+// One level of the device block tree.  tree arrays [dev] as gc_block_tree;
+// frontier [dev] fr, fc, fkey, fpar (m); node records written at out_*[base
+// .. base + m) [dev]; next frontier [dev] nr, nc, nk, np (capacity 4m) and
+// its size in *count [dev int64]; flags / pos [dev] 4m int32 each; temp
+// [dev] of gc_bt_level_bytes(m) bytes.
+int gc_bt_level_bytes(int64_t m, int64_t* bytes) {
+    using namespace gcb;
+    size_t tb = 0;
+    cudaError_t e = cub::DeviceScan::ExclusiveSum(nullptr, tb, (const int32_t*)nullptr, (int32_t*)nullptr, (int)(4 * m));
+    if (e != cudaSuccess) return cuda_status(e, "gc_bt_level_bytes");
+    *bytes = (int64_t)tb;
+    return GC_OK;
+}
+
+int gc_bt_level(int64_t m, const int64_t* fr, const int64_t* fc, const int64_t* fkey, const int64_t* fpar,
+                int64_t base, int64_t lev, int32_t digits, const double* r_diam, const double* r_lower,
+                const double* r_upper, const int64_t* r_left, const int64_t* r_right, const double* c_diam,
+                const double* c_lower, const double* c_upper, const int64_t* c_left, const int64_t* c_right,
+                double eta, int32_t norm_mode, int64_t* o_row, int64_t* o_col, int8_t* o_state, int64_t* o_level,
+                int64_t* o_key, int64_t* o_parent, int64_t* nr, int64_t* nc, int64_t* nk, int64_t* np,
+                int64_t* count, int32_t* flags, int32_t* pos, void* temp, int64_t temp_bytes, void* stream) {
+    using namespace gcb;
+    if (m <= 0 || 4 * m >= (1LL << 31) || (norm_mode != 0 && norm_mode != 1) || lev >= digits || eta <= 0.0) {
+        set_error(GC_ERR_CONFIG, "gc_bt_level: bad arguments");
+        return GC_ERR_CONFIG;
+    }
+    cudaStream_t st = (cudaStream_t)stream;
+    const BtTree R{r_diam, r_lower, r_upper, r_left, r_right};
+    const BtTree C{c_diam, c_lower, c_upper, c_left, c_right};
+    int64_t grid = (m + 255) / 256;
+    if (grid > 148 * 16) grid = 148 * 16;
+    k_bt_eval<<<(unsigned)grid, 256, 0, st>>>(m, fr, fc, fkey, fpar, base, lev, R, C, eta, norm_mode, o_row, o_col,
+                                              o_state, o_level, o_key, o_parent, flags);
+    GC_CHECK_LAUNCH("k_bt_eval");
+    size_t tb = (size_t)temp_bytes;
+    cudaError_t e = cub::DeviceScan::ExclusiveSum(temp, tb, flags, pos, (int)(4 * m), st);
+    if (e != cudaSuccess) return cuda_status(e, "gc_bt_level scan");
+    int64_t scale = 1;
+    for (int k = 0; k < digits - 1 - lev; ++k) scale *= 4;
+    int64_t cgrid = (4 * m + 255) / 256;
+    if (cgrid > 148 * 16) cgrid = 148 * 16;
+    k_bt_children<<<(unsigned)cgrid, 256, 0, st>>>(m, fr, fc, fkey, base, scale, R, C, flags, pos, nr, nc, nk, np,
+                                                   count);
+    GC_CHECK_LAUNCH("k_bt_children");
+    return GC_OK;
+}
+
+}  // extern "C"
+
+namespace gcb {
+
+__global__ void k_bt_leaf_flags(int64_t n, const int8_t* __restrict__ state, char* __restrict__ flag,
+                                int64_t* __restrict__ ids) {
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+        flag[i] = state[i] != 2;
+        ids[i] = i;
+    }
+}
+
+__global__ void k_bt_gather_flags(int64_t n, const char* __restrict__ flag, const int64_t* __restrict__ ids,
+                                  char* __restrict__ out) {
+    for (int64_t j = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; j < n; j += (int64_t)gridDim.x * blockDim.x)
+        out[j] = flag[ids[j]];
+}
+
+}  // namespace gcb
+
+extern "C" {
+
+// Leaves of a device block tree in depth-first order (FlatBlockTree's
+// leaf_ids / leaf_key): every node sorted by its path key (stable radix;
+// a node shares its key only with its first descendants, never with
+// another leaf), then the leaves selected in that order.  Scratch [dev]:
+// ids, ids_sorted, key_sorted (n int64 each), flag, flag_sorted (n bytes
+// each), temp of gc_bt_leaves_bytes(n) bytes; *count [dev] = leaves.
+int gc_bt_leaves_bytes(int64_t n, int64_t* bytes) {
+    using namespace gcb;
+    size_t t1 = 0, t2 = 0;
+    cudaError_t e = cub::DeviceSelect::Flagged(nullptr, t1, (const int64_t*)nullptr, (const char*)nullptr,
+                                               (int64_t*)nullptr, (int64_t*)nullptr, (int)n);
+    if (e == cudaSuccess)
+        e = cub::DeviceRadixSort::SortPairs(nullptr, t2, (const int64_t*)nullptr, (int64_t*)nullptr,
+                                            (const int64_t*)nullptr, (int64_t*)nullptr, (int)n);
+    if (e != cudaSuccess) return cuda_status(e, "gc_bt_leaves_bytes");
+    *bytes = (int64_t)(t1 > t2 ? t1 : t2);
+    return GC_OK;
+}
+
+int gc_bt_leaves(int64_t n, const int8_t* state, const int64_t* key, int64_t* leaf_ids, int64_t* leaf_key,
+                 int64_t* count, int64_t* ids, int64_t* ids_sorted, int64_t* key_sorted, char* flag,
+                 char* flag_sorted, void* temp, int64_t temp_bytes, void* stream) {
+    using namespace gcb;
+    if (n <= 0 || n >= (1LL << 31)) { set_error(GC_ERR_CONFIG, "gc_bt_leaves: bad size"); return GC_ERR_CONFIG; }
+    cudaStream_t st = (cudaStream_t)stream;
+    int64_t grid = (n + 255) / 256;
+    if (grid > 148 * 16) grid = 148 * 16;
+    k_bt_leaf_flags<<<(unsigned)grid, 256, 0, st>>>(n, state, flag, ids);
+    GC_CHECK_LAUNCH("k_bt_leaf_flags");
+    size_t tb = (size_t)temp_bytes;
+    cudaError_t e = cub::DeviceRadixSort::SortPairs(temp, tb, key, key_sorted, ids, ids_sorted, (int)n, 0, 64, st);
+    if (e != cudaSuccess) return cuda_status(e, "gc_bt_leaves sort");
+    k_bt_gather_flags<<<(unsigned)grid, 256, 0, st>>>(n, flag, ids_sorted, flag_sorted);
+    GC_CHECK_LAUNCH("k_bt_gather_flags");
+    tb = (size_t)temp_bytes;
+    e = cub::DeviceSelect::Flagged(temp, tb, ids_sorted, flag_sorted, leaf_ids, count, (int)n, st);
+    if (e == cudaSuccess) {
+        tb = (size_t)temp_bytes;
+        e = cub::DeviceSelect::Flagged(temp, tb, key_sorted, flag_sorted, leaf_key, count, (int)n, st);
+    }
+    if (e != cudaSuccess) return cuda_status(e, "gc_bt_leaves select");
+    count_launch(3);
     return GC_OK;
 }
 

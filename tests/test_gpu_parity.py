@@ -221,6 +221,21 @@ def test_pipeline_storage_and_stats(built):
     assert all(s["wall_s"] >= 0.0 for s in hm.exec_stats)
 
 
+@pytest.mark.parametrize("mesh_fn,basis,eta", [("sphere5", "constant", 1.0), ("sphere4", "linear", 0.7),
+                                                ("cube4", "constant", 2.5), ("sphere6", "constant", 1.0)])
+def test_device_block_tree_equals_host_builders(mesh_fn, basis, eta):
+    """gc_bt_level (one tree level per launch pair, on the device) builds the
+    nodes, order, keys and parents of the numpy builder exactly."""
+    mesh = (geometry.build_sphere_mesh if mesh_fn.startswith("sphere") else geometry.build_cube_mesh)(
+        int(mesh_fn[-1]))
+    tree = clustering.build_cluster_tree(mesh, basis, 16, device=torch.device("cuda", 0))
+    assert getattr(tree.flat, "_device", None) is not None
+    a = clustering.build_block_tree(tree, eta=eta).flat
+    b = clustering._build_block_tree_arrays(tree, eta=eta).flat
+    for k in ("row", "col", "state", "level", "key", "parent_of", "leaf_ids"):
+        assert np.array_equal(getattr(a, k), getattr(b, k)), k
+
+
 def test_build_h2_returns_before_the_quadrature_settles():
     """build_h2 (plane charts) does not synchronise: the statistics settle on
     first use, once, and equal a synchronous rebuild's."""

@@ -795,13 +795,17 @@ def build_h2(btree, row_basis, col_basis, mesh, kind="slp", basis="constant",
         # the caller continues (e.g. builds the matvec plan); the counts,
         # the queue flags and the timings settle on first use (H2Matrix.settle)
         ev_c, ev_n, pending = [], [], ([] if not dmesh.curved else None)
+        # both block tables go up before the first quadrature launch: a large
+        # pageable upload waits for the work queued on its stream
+        ndesc = np.stack([rf.start[nr_r], n_nr, cf.start[nc_r], n_nc, n_off], 1)
+        c_d = to_dev(cdesc[keep].astype(np.int64), dev) if keep.any() else None
+        n_d = to_dev(ndesc.astype(np.int64), dev) if len(ndesc) else None
         stats_c = device_block_assembly(dmesh, rules, queue, rstore.pivots, cstore.pivots,
-                                        cdesc[keep], coup, kind=kind, events=ev_c, pending=pending)
+                                        cdesc[keep], coup, kind=kind, events=ev_c, pending=pending, d_desc=c_d)
         t1 = time.perf_counter()
         # near-field blocks: full clusters
-        ndesc = np.stack([rf.start[nr_r], n_nr, cf.start[nc_r], n_nc, n_off], 1)
         stats_n = device_block_assembly(dmesh, rules, queue, perm_r, perm_c, ndesc, near, kind=kind,
-                                        events=ev_n, pending=pending)
+                                        events=ev_n, pending=pending, d_desc=n_d)
     d = DeviceH2(dev)
     d.coup, d.near = coup, near
     d.c_rows, d.c_cols, d.c_nr, d.c_nc, d.c_off = cr, cc, c_nr, c_nc, c_off

@@ -57,13 +57,14 @@ def _offsets(sizes):
     return np.cumsum(sizes) - sizes
 
 
-def _grouped_offsets(keys, sizes):
+def _grouped_offsets(keys, sizes, with_order=False):
     """Offsets that store items with equal key contiguously (keys ascending,
-    original order inside a key)."""
+    original order inside a key); ``with_order``: also the storage order
+    (the item indices by ascending offset)."""
     order = np.argsort(keys, kind="stable")
     off = np.empty(len(keys), dtype=np.int64)
     off[order] = _offsets(np.asarray(sizes, dtype=np.int64)[order])
-    return off
+    return (off, order) if with_order else off
 
 
 # --------------------------------------------------------------------------
@@ -753,7 +754,7 @@ def build_h2(btree, row_basis, col_basis, mesh, kind="slp", basis="constant",
         c_key = 2 * cr + ~((cf.start[cc] >= row_range[0]) & (cf.stop[cc] <= row_range[1]))
     else:
         c_key = cr
-    c_off = _grouped_offsets(c_key, c_nr * c_nc)
+    c_off, c_order = _grouped_offsets(c_key, c_nr * c_nc, with_order=True)
     c_total = int((c_nr * c_nc).sum())
     coup = padded_empty(max(c_total, 1), dev)
     cdesc = np.stack([rstore.piv_off[cr], c_nr, cstore.piv_off[cc], c_nc, c_off], 1)
@@ -764,7 +765,7 @@ def build_h2(btree, row_basis, col_basis, mesh, kind="slp", basis="constant",
         n_key = 2 * nr_r + ~((cf.start[nc_r] >= row_range[0]) & (cf.stop[nc_r] <= row_range[1]))
     else:
         n_key = nr_r
-    n_off = _grouped_offsets(n_key, n_nr * n_nc)
+    n_off, n_order = _grouped_offsets(n_key, n_nr * n_nc, with_order=True)
     near = padded_empty(max(int((n_nr * n_nc).sum()), 1), dev)
     perm_r = to_dev(rf.perm, dev)
     perm_c = perm_r if cf is rf else to_dev(cf.perm, dev)
@@ -810,6 +811,7 @@ def build_h2(btree, row_basis, col_basis, mesh, kind="slp", basis="constant",
     d.coup, d.near = coup, near
     d.c_rows, d.c_cols, d.c_nr, d.c_nc, d.c_off = cr, cc, c_nr, c_nc, c_off
     d.n_rows, d.n_cols, d.n_nr, d.n_nc, d.n_off = nr_r, nc_r, n_nr, n_nc, n_off
+    d.c_order, d.n_order = c_order, n_order            # block indices in storage order
     d.perm_r, d.perm_c = perm_r, perm_c
     d.row_range = row_range
     ncase = 2 if disc == "collocation" else 4                 # the reference's executor cases

@@ -56,6 +56,17 @@ def plan(h, trans=False):
     return d.plans[key]
 
 
+def _storage_order(d, kind, blocks):
+    """``blocks`` (coupling "c" / near-field "n" block indices) in storage
+    order - rows contiguous, as build_h2 laid the blocks out."""
+    order = getattr(d, kind + "_order", None)
+    if order is None:
+        return blocks[np.argsort(getattr(d, kind + "_off")[blocks], kind="stable")]
+    keep = np.zeros(len(order), bool)
+    keep[blocks] = True
+    return order[keep[order]]
+
+
 def _check_dim(x, n):
     x = np.asarray(x, dtype=np.float64)
     if x.shape != (n,):
@@ -348,7 +359,7 @@ class PanelPlan:
         whose panel adds onto y_t (written by an earlier near phase)."""
         d = h.dev
         rf, cf = h.row_tree.flat, h.col_tree.flat
-        order = blocks[np.argsort(d.n_off[blocks], kind="stable")]       # storage order: rows contiguous
+        order = _storage_order(d, "n", blocks)                # rows contiguous
         sn = d.n_rows[order]
         cuts = np.flatnonzero(np.r_[True, sn[1:] != sn[:-1]]) if len(sn) else np.zeros(0, np.int64)
         K = np.add.reduceat(d.n_nc[order], cuts) if len(sn) else np.zeros(0, np.int64)
@@ -370,7 +381,7 @@ class PanelPlan:
         rf, cf = h.row_tree.flat, h.col_tree.flat
         cpl = []
         live = mask & (d.c_nr > 0) & (d.c_nc > 0)
-        order = np.flatnonzero(live)[np.argsort(d.c_off[live], kind="stable")]   # storage order
+        order = _storage_order(d, "c", np.flatnonzero(live))
         if not order.size:
             return cpl
         sn = d.c_rows[order]
@@ -401,8 +412,15 @@ class PanelPlan:
         pair_key = src * (len(bwd) + 1) + dst
         gbytes = np.bincount(pair_key, weights=8.0 * (K * d.c_nr[order[cuts]]))
         grp = np.stack([src, dst, np.where(gbytes[pair_key] >= _MERGE_MIN_BYTES, -1, rowh)], 1).astype(np.int64)
-        for key in sorted(map(tuple, np.unique(grp, axis=0).tolist()), key=lambda k: (-k[1], k[0], k[2])):
-            sel = np.flatnonzero(np.all(grp == np.array(key), axis=1))
+        # one int64 code per group, groups in (consumer top down, producer,
+        # height) order; members by a stable sort of the codes
+        hcol = grp[:, 2] + 1                                   # -1 (merged) -> 0
+        code = (len(bwd) - grp[:, 1]) * (len(fwd) + 2) * (int(hcol.max()) + 1) + grp[:, 0] * (int(hcol.max()) + 1) + hcol
+        codes, inv = np.unique(code, return_inverse=True)
+        members = np.argsort(inv, kind="stable")
+        bounds = np.searchsorted(inv[members], np.arange(len(codes) + 1))
+        for gi in range(len(codes)):
+            sel = members[bounds[gi]:bounds[gi + 1]]
             bsel = _ranges_np(cuts[sel], nblk[sel])
             panels = (d.c_off[order[cuts[sel]]], K[sel], d.c_nr[order[cuts[sel]]],
                       (bstart[bsel], blen[bsel]), rs.coef_off[sn[cuts[sel]]], acc[sel])

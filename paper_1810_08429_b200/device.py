@@ -40,6 +40,9 @@ def ptr(t):
     return ctypes.c_void_p(t.data_ptr()) if t is not None and t.numel() else ctypes.c_void_p(0)
 
 
+_PINNED_UPLOAD_BYTES = 1 << 20
+
+
 def to_dev(a, device, dtype=None):
     a = np.ascontiguousarray(a)
     if not a.flags.writeable:          # read-only views (broadcasts): copy
@@ -47,9 +50,15 @@ def to_dev(a, device, dtype=None):
     t = torch.from_numpy(a)
     if dtype is not None:
         t = t.to(dtype)
-    # asynchronous: a pageable source is staged by the driver before the
-    # call returns (no device synchronisation), so host work continues
-    # while earlier kernels run
+    if t.numel() * t.element_size() >= _PINNED_UPLOAD_BYTES:
+        # a large pageable upload waits for the work queued on its stream;
+        # staged in pinned memory (torch's caching host allocator, which
+        # keeps the block until the copy ran) it is queued without waiting
+        p = torch.empty(t.shape, dtype=t.dtype, pin_memory=True)
+        p.copy_(t)
+        return p.to(device, non_blocking=True)
+    # small uploads: the driver stages a pageable source before the call
+    # returns, without a device synchronisation
     return t.to(device, non_blocking=True)
 
 

@@ -30,6 +30,13 @@ __device__ __forceinline__ void merge(MaxLoc& a, double v, int i, double ss) {
     a.ss += ss;
 }
 
+// merge for a thread's own elements, visited in increasing flat index:
+// the first maximum stays without an index comparison
+__device__ __forceinline__ void merge_next(MaxLoc& a, double v, int i, double ss) {
+    if (v > a.v) { a.v = v; a.i = i; }
+    a.ss += ss;
+}
+
 // block-wide (max |.|, first flat index, sum of squares) with a fixed tree
 template <int NT>
 __device__ MaxLoc block_reduce(MaxLoc x, double* sv, int* si, double* ss) {
@@ -83,7 +90,7 @@ __global__ void __launch_bounds__(NT) k_aca(const int64_t* __restrict__ desc, in
     for (int e = threadIdx.x; e < N; e += NT) {
         const double x = fac[fac_off + e];
         if (resid_in_smem) res[e] = x;
-        merge(loc, fabs(x), e, x * x);
+        merge_next(loc, fabs(x), e, x * x);
     }
     for (int a = threadIdx.x; a < R; a += NT) pivpos[a] = -1;
     MaxLoc st = block_reduce<NT>(loc, sv, si, ss);
@@ -107,7 +114,7 @@ __global__ void __launch_bounds__(NT) k_aca(const int64_t* __restrict__ desc, in
         for (int e = threadIdx.x; e < N; e += NT) {
             const double x = __dsub_rn(res[e], __dmul_rn(ucol[a], prow[b]));
             res[e] = x;
-            merge(loc, fabs(x), e, x * x);
+            merge_next(loc, fabs(x), e, x * x);
             a += da;
             b += db;
             if (b >= W) { b -= W; ++a; }

@@ -402,7 +402,12 @@ class _Side:
         self.store.available = mat.copy()
         size = flat.stop - flat.start
         cap = int(np.minimum(size[mat], W).sum()) if mat.any() else 0
-        self.gpiv = np.empty(max(cap, 1), dtype=np.int64)
+        # [perm | this basis' global pivots]: the row source of every level
+        # (leaf dofs, children's pivots) without a per-level concatenation
+        perm = tree.flat.perm
+        self.combined = np.empty(len(perm) + max(cap, 1), dtype=np.int64)
+        self.combined[:len(perm)] = perm
+        self.gpiv = self.combined[len(perm):]
         self.cursor = 0
         self.v_parts = []        # (level tensor, start, stop)
         self.v_base = 0
@@ -454,8 +459,7 @@ def build_cluster_bases(tree, mesh, basis, m, delta_factor, eps, sides, orders=(
             ln1 = np.where(leaf, size[ids], st.rank[lc])
             st2 = np.where(leaf, 0, n_perm + st.piv_off[rc])
             ln2 = np.where(leaf, 0, st.rank[rc])
-            combined = np.concatenate([perm, s.gpiv[:s.cursor]])
-            rows_host = combined[_ranges(np.stack([st1, st2], 1).ravel(),
+            rows_host = s.combined[_ranges(np.stack([st1, st2], 1).ravel(),
                                          np.stack([ln1, ln2], 1).ravel())]
             st.child_row[lc[~leaf]] = 0
             st.child_row[rc[~leaf]] = st.rank[flat.left[ids][~leaf]]

@@ -341,7 +341,9 @@ def coupling_mark_arrays(btree):
     form: no Python sets of 10^5 clusters)."""
     fb = btree.flat
     ids = btree._leaf_ids(0)
-    return np.unique(fb.row[ids]), np.unique(fb.col[ids])
+    n = max(len(fb.row_tree), len(fb.col_tree))
+    return (np.flatnonzero(np.bincount(fb.row[ids], minlength=n)),
+            np.flatnonzero(np.bincount(fb.col[ids], minlength=n)))
 
 
 def _materialize(flat, marks):

@@ -41,10 +41,11 @@ def live_nodes(store):
     return store.materialized & (store.rank > 0)
 
 
-def _pairs(store, flat, lo, hi):
+def _pairs(store, flat, lo, hi, ordered=True):
     """(u, f) pairs of tier (lo, hi]: u a live tier node, f a frontier
     element under it (a frontier node, or for lo < 0 a live leaf, the leaf
-    itself included), plus the element weights w_f (rank, or leaf size)."""
+    itself included), plus the element weights w_f (rank, or leaf size).
+    ``ordered``: sorted by (u, position of f) - the layout of M_u."""
     live = live_nodes(store)
     H = flat.height
     par = flat.parent
@@ -77,6 +78,8 @@ def _pairs(store, flat, lo, hi):
         cur = up
     u = np.concatenate(us) if us else np.zeros(0, np.int64)
     f = np.concatenate(fs) if fs else np.zeros(0, np.int64)
+    if not ordered:
+        return u, f, wmap
     order = np.lexsort((flat.start[f], u))
     return u[order], f[order], wmap
 
@@ -108,12 +111,12 @@ def choose_tiers(store, flat, bounds=None, latency_s=5e-6, cta_bps=20e9, max_row
     # measured worse: L6 (5, 7) at 4.85 TB/s) plus a launch latency.
     cost = {}
     for lo in range(-1, top):
-        u, f, wmap = _pairs(store, flat, lo, top)
+        u, f, wmap = _pairs(store, flat, lo, top, ordered=False)     # sums only
         el = (wmap[f] * store.rank[u]).astype(np.float64)
         per_h = np.bincount(flat.height[u], weights=el, minlength=top + 1)
         acc = np.cumsum(per_h)
         m = np.bincount(u, weights=wmap[f].astype(np.float64), minlength=len(flat))
-        nodes = np.unique(u)
+        nodes = np.flatnonzero(np.bincount(u, minlength=len(flat)))
         item = np.minimum(m[nodes], max_rows) * store.rank[nodes] * 8.0
         big = np.zeros(top + 1)
         np.maximum.at(big, flat.height[nodes], item)
@@ -138,7 +141,7 @@ def tier_tables(store, flat, bounds):
     lo = -1
     for hi in bounds:
         u, f, wmap = _pairs(store, flat, lo, hi)
-        nodes = np.unique(u)
+        nodes = u[np.r_[True, u[1:] != u[:-1]]] if u.size else u      # u is sorted
         m = np.zeros(len(flat), np.int64)
         np.add.at(m, u, wmap[f])
         moff = np.full(len(flat), -1, np.int64)

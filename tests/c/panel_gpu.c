@@ -67,6 +67,15 @@ int main(void) {
     cudaMemcpy(got2, out, sizeof(got2), cudaMemcpyDeviceToHost);
     for (int t = 0; t < T; ++t)
         if (got2[t] != got[t]) { printf("plan result differs at %d\n", t); return 5; }
+    /* the synchronous host-vector call: a plan without gather / scatter
+     * nodes must refuse host pointers */
+    double* pin = NULL;
+    cudaMallocHost((void**)&pin, sizeof(double) * (K + T));
+    if (gc_plan_run_host(plan, hx, pin, K, pin + K, NULL) != GC_ERR_CONFIG) {
+        printf("gc_plan_run_host accepted a plan without gather / scatter nodes\n");
+        return 11;
+    }
+    cudaFreeHost(pin);
     gc_plan_destroy(plan);
     /* NCCL through the C-ABI (world of one): communicator from a unique id,
      * an in-place all-gather (send = the rank's own slot of recv) */

@@ -320,10 +320,6 @@ int gc_panelmv(int64_t nitems, const int64_t* items, const int32_t* xidx,
 int gc_plan_create(int64_t n, const int64_t* nodes, int64_t ndeps, const int64_t* deps, int64_t nstreams,
                    const int32_t* stream_prio, void** plan);
 int gc_plan_run(void* plan, const double* x, double* y, void* stream);
-/* Page-lock / release a host range (cudaHostRegister): a registered vector
- * can be bound to gc_plan_run directly (read over the host link). */
-int gc_host_register(void* ptr, int64_t bytes);
-int gc_host_unregister(void* ptr);
 /* h2.mvm in one call: copies n_in doubles of host x into the pinned
  * staging buffer x_pinned, runs the plan reading x_pinned and writing the
  * pinned y_pinned over the host link, and synchronises `stream`. */

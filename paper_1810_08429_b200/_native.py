@@ -73,8 +73,6 @@ _SIGNATURES = {
     "gc_plan_create": [c_i64, c_p, c_i64, c_p, c_i64, c_p, c_p],
     "gc_plan_run": [c_p, c_p, c_p, c_p],
     "gc_plan_run_host": [c_p, c_p, c_p, c_i64, c_p, c_p],
-    "gc_host_register": [c_p, c_i64],
-    "gc_host_unregister": [c_p],
     "gc_plan_destroy": [c_p],
     "gc_scatter2_inv": [c_p, c_p, c_p, c_i64, c_p, c_p],
     "gc_block_transpose": [c_i64, c_p, c_p, c_p, c_p],

@@ -299,28 +299,6 @@ int gc_graph_retarget(void* graph, void* exec, int32_t kernel, int32_t arg, cons
     return GC_OK;
 }
 
-// Page-lock a host range so that kernels read it over the host link
-// (h2.mvm reads a caller's vector in place when it is passed repeatedly);
-// GC_ERR_CUDA when the range is not registrable (e.g. already registered).
-int gc_host_register(void* ptr, int64_t bytes) {
-    if (!ptr || bytes <= 0) { set_error(GC_ERR_CONFIG, "gc_host_register: bad range"); return GC_ERR_CONFIG; }
-    cudaError_t e = cudaHostRegister(ptr, (size_t)bytes, cudaHostRegisterDefault);
-    if (e != cudaSuccess) {
-        (void)cudaGetLastError();
-        return cuda_status(e, "gc_host_register");
-    }
-    return GC_OK;
-}
-
-int gc_host_unregister(void* ptr) {
-    cudaError_t e = cudaHostUnregister(ptr);
-    if (e != cudaSuccess) {
-        (void)cudaGetLastError();
-        return cuda_status(e, "gc_host_unregister");
-    }
-    return GC_OK;
-}
-
 int gc_gather_inv(const double* x, const int64_t* iperm, int64_t n, double* xt, void* stream) {
     if (n <= 0) return GC_OK;
     k_gather_inv<<<grid_for(n, 256), 256, 0, (cudaStream_t)stream>>>(x, iperm, n, xt);

@@ -19,7 +19,6 @@ to device vectors directly, any other closure is called on host copies.
 """
 
 import threading
-import weakref
 from collections import namedtuple
 
 import numpy as np
@@ -66,61 +65,6 @@ def _storage_order(d, kind, blocks):
     keep = np.zeros(len(order), bool)
     keep[blocks] = True
     return order[keep[order]]
-
-
-class _HostRegistry:
-    """Caller vectors that ``h2.mvm`` reads in place.  A C-contiguous
-    float64 array that owns its memory and comes back for a second product
-    is page-locked once (``gc_host_register``) and then read by the graph's
-    gather kernel directly over the host link - no staging copy.  The
-    registration ends when the array is deallocated (a weak-reference
-    callback runs before numpy frees the buffer).  Arrays that cannot be
-    registered (pages shared with another registration, ...) keep the
-    staging copy."""
-
-    _MIN_BYTES = 64 << 10
-
-    def __init__(self):
-        self._lock = threading.RLock()   # weakref callbacks may run inside pointer() (GC)
-        self._seen = {}          # id -> weakref (passed once)
-        self._reg = {}           # id -> (weakref, ptr, nbytes, base)
-        self._failed = {}        # id -> weakref
-
-    def pointer(self, x):
-        if (not isinstance(x, np.ndarray) or x.dtype != np.float64 or not x.flags.c_contiguous
-                or not x.flags.owndata or x.nbytes < self._MIN_BYTES):
-            return None
-        key, ptr, nb = id(x), x.ctypes.data, x.nbytes
-        with self._lock:
-            ent = self._reg.get(key)
-            if ent is not None:
-                return ptr if (ent[0]() is x and ent[1] == ptr and ent[2] == nb) else None
-            f = self._failed.get(key)
-            if f is not None and f() is x:
-                return None
-            s = self._seen.get(key)
-            if s is None or s() is not x:
-                self._seen[key] = weakref.ref(x, lambda r, k=key: self._seen.pop(k, None))
-                return None
-            del self._seen[key]
-            base = ptr & ~4095
-            size = ((ptr + nb + 4095) & ~4095) - base
-            if _native.load().gc_host_register(base, size) != 0:
-                self._failed[key] = weakref.ref(x, lambda r, k=key: self._failed.pop(k, None))
-                return None
-            self._reg[key] = (weakref.ref(x, lambda r, k=key, b=base: self._release(k, b)), ptr, nb, base)
-            return ptr
-
-    def _release(self, key, base):
-        with self._lock:
-            self._reg.pop(key, None)
-        try:
-            _native.load().gc_host_unregister(base)
-        except Exception:        # pragma: no cover - interpreter shutdown
-            pass
-
-
-_HOST = _HostRegistry()
 
 
 def _check_dim(x, n):
@@ -1018,18 +962,11 @@ class PanelPlan:
                 if self._pin_x_np is None:
                     self._pin_x = torch.empty(self.n_in, dtype=torch.float64, pin_memory=True)
                     self._pin_x_np = self._pin_x.numpy()
-                y = torch.empty(self.n_out, dtype=torch.float64, pin_memory=True)
-                py = y.data_ptr()
-                xr = _HOST.pointer(x)
-                st = torch.cuda.current_stream()
-                if xr is not None:          # a registered caller vector: read in place
-                    _native.check(g._run(g.handle, xr, py, st.cuda_stream))
-                    g._x, g._y = xr, py
-                    st.synchronize()
-                    return y.numpy()
                 x = np.ascontiguousarray(x, dtype=np.float64)
-                px = self._pin_x.data_ptr()
-                _native.check(g._run_host(g.handle, x.ctypes.data, px, self.n_in, py, st.cuda_stream))
+                y = torch.empty(self.n_out, dtype=torch.float64, pin_memory=True)
+                px, py = self._pin_x.data_ptr(), y.data_ptr()
+                _native.check(g._run_host(g.handle, x.ctypes.data, px, self.n_in, py,
+                                          torch.cuda.current_stream().cuda_stream))
                 g._x, g._y = px, py
                 return y.numpy()
             with torch.cuda.device(self.dev):

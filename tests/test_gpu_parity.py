@@ -236,28 +236,6 @@ def test_device_block_tree_equals_host_builders(mesh_fn, basis, eta):
         assert np.array_equal(getattr(a, k), getattr(b, k)), k
 
 
-def test_mvm_reads_a_repeated_vector_in_place():
-    """h2.mvm page-locks a vector passed a second time and reads it in place:
-    results equal the staged product, an in-place update is seen, and the
-    registration ends with the array."""
-    import gc as _gc
-    mesh = geometry.build_sphere_mesh(5)                 # 64 KB vectors: registrable
-    hm, tree, bt = cli.build_h2_operator(mesh, cli.default_config(eps=1e-4))
-    x = np.random.default_rng(9).standard_normal(mesh.nt)
-    x2 = x.copy()
-    y0 = h2.mvm(hm, x2)                          # staged (first sight of x2)
-    y1 = h2.mvm(hm, x)                           # first sight of x: staged
-    y2 = h2.mvm(hm, x)                           # second: registered, read in place
-    assert id(x) in h2._HOST._reg
-    assert np.array_equal(y1, y0) and np.array_equal(y2, y0)
-    x *= 2.0                                     # in-place update between products
-    assert np.array_equal(h2.mvm(hm, x), h2.mvm(hm, x.copy()))
-    key = id(x)
-    del x
-    _gc.collect()
-    assert key not in h2._HOST._reg
-
-
 def test_build_h2_returns_before_the_quadrature_settles():
     """build_h2 (plane charts) does not synchronise: the statistics settle on
     first use, once, and equal a synchronous rebuild's."""

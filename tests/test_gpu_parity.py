@@ -622,6 +622,14 @@ def _sharded_worker(rank, world, port, out_dir, level, cfg_kw):
         x2 = np.random.default_rng(4).standard_normal(n)
         xt2 = torch.from_numpy(x2[perm][sh.layout.lo:sh.layout.hi].copy()).cuda()
         np.save(os.path.join(out_dir, "y2_%d.npy" % rank), sh.mvm_slice(xt2).cpu().numpy())
+        # a few of this rank's blocks, for the bitwise comparison with the
+        # single-operator assembly (same per-task arithmetic on every rank)
+        picks = []
+        for blocks in (sh.h.coupling, sh.h.nearfield):
+            for i in np.linspace(0, len(blocks) - 1, 4).astype(int) if len(blocks) else []:
+                b = blocks[int(i)]
+                picks.append((b.row.index, b.col.index, b.values.ravel()))
+        np.save(os.path.join(out_dir, "blk%d.npy" % rank), np.array(picks, dtype=object), allow_pickle=True)
     finally:
         dist.destroy_process_group()
 
@@ -667,6 +675,11 @@ def test_sharded_operator_multirank_matches_full(world, level, cfg_kw, tmp_path)
     y[tree.perm] = yt
     ref2 = h2.mvm(hm, x2)
     assert np.linalg.norm(y - ref2) <= 1e-13 * np.linalg.norm(ref2)
+    # the ranks' blocks are bitwise the single operator's (SURVEY 8e parity)
+    full = {(b.row.index, b.col.index): b.values for blocks in (hm.coupling, hm.nearfield) for b in blocks}
+    for g in range(world):
+        for r, c, v in np.load(tmp_path / ("blk%d.npy" % g), allow_pickle=True):
+            assert np.array_equal(full[(r, c)].ravel(), v)
     if cfg_kw.get("basis") == "linear" and world == 4:
         assert len(set(sizes)) > 1               # the padded all-gather path ran
 

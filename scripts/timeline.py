@@ -1,7 +1,7 @@
 """Timeline of the product DAG inside its CUDA graph: every panel kernel
 stamps min(start) / max(end) %globaltimer into a trace slot (median of 10
 replays).  Usage: python scripts/timeline.py level eps [key=value ...]
-(PanelPlan keyword arguments, e.g. parts=2)."""
+(PanelPlan keyword arguments, e.g. tiers=off)."""
 import os
 import sys
 

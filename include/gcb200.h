@@ -199,6 +199,35 @@ int gc_bt_level(int64_t m, const int64_t* fr, const int64_t* fc, const int64_t* 
                 int64_t* np, int64_t* count, int32_t* flags, int32_t* pos, void* temp, int64_t temp_bytes,
                 void* stream);
 
+/* Level bookkeeping of the nested bases (replaces the host loop body of
+ * greencross gca.py:162-220 around the factor / ACA launches).  Per basis
+ * side, tree arrays left/right/start/stop, rank/piv_off/rows/v_off per tree
+ * node and the global pivots gpiv with a device cursor stay on the device.
+ * gc_bases_R: factor rows R (leaf size or sum of the children's ranks),
+ * min(R, W) and R*min(R, W) of the n nodes at level positions pos0...
+ * gc_bases_scan: exclusive scans of those over the level's nn nodes and
+ * out = [max R, rows, limits, vcap, v_off at the n_bound positions bounds].
+ * gc_bases_rows: row lists (leaf dofs from perm, or the children's
+ * pivots) and the gc_green_factor (5 per node) / gc_aca (4) descriptors.
+ * gc_bases_post: after gc_aca, ranks, compact global pivots, piv_off and
+ * v_off (v_base + level offset) of one side; rk_off (n) and temp scratch. */
+int gc_bases_scan_bytes(int64_t nn, int64_t* bytes);
+int gc_bases_R(int64_t n, const int64_t* nodes, const int64_t* left, const int64_t* right, const int64_t* start,
+               const int64_t* stop, const int64_t* rank, int64_t pos0, int64_t W, int64_t* R, int64_t* lim,
+               int64_t* vcap, int64_t* rows_node, void* stream);
+int gc_bases_scan(int64_t nn, const int64_t* R, const int64_t* lim, const int64_t* vcap, int64_t* rows_off,
+                  int64_t* piv_off_l, int64_t* v_off, const int64_t* bounds, int64_t n_bound, int64_t* out,
+                  void* temp, int64_t temp_bytes, void* stream);
+int gc_bases_rows(int64_t n, const int64_t* nodes, const int64_t* left, const int64_t* right, const int64_t* start,
+                  const int64_t* rank, const int64_t* piv_off, const int64_t* gpiv, const int64_t* perm, int64_t pos0,
+                  int64_t box0, int64_t side, int64_t W, const int64_t* R, const int64_t* rows_off,
+                  const int64_t* piv_off_l, const int64_t* v_off, int64_t* rows, int64_t* fdesc, int64_t* adesc,
+                  void* stream);
+int gc_bases_post(int64_t n, const int64_t* nodes, int64_t pos0, const int64_t* rank_l, const int64_t* piv_l,
+                  const int64_t* piv_off_l, const int64_t* rows, const int64_t* rows_off, const int64_t* v_off,
+                  int64_t v_base, int64_t* cursor, int64_t* rank, int64_t* piv_off, int64_t* gpiv,
+                  int64_t* v_off_node, int64_t* rk_off, void* temp, int64_t temp_bytes, void* stream);
+
 /* Batched transpose: for node i with desc (off, rows, cols) [dev] (nn,3):
  * out[off + c*rows + r] = in[off + r*cols + c]. */
 int gc_batched_transpose(int64_t nn, const int64_t* desc, const double* in,

@@ -54,6 +54,11 @@ _SIGNATURES = {
                       ctypes.c_int32, ctypes.c_int32, ctypes.POINTER(c_p), ctypes.POINTER(c_i64)],
     "gc_block_tree_fetch": [c_p, c_p, c_p, c_p, c_p, c_p, c_p],
     "gc_bt_level_bytes": [c_i64, ctypes.POINTER(c_i64)],
+    "gc_bases_scan_bytes": [c_i64, ctypes.POINTER(c_i64)],
+    "gc_bases_R": [c_i64] + [c_p] * 6 + [c_i64, c_i64] + [c_p] * 4 + [c_p],
+    "gc_bases_scan": [c_i64] + [c_p] * 7 + [c_i64, c_p, c_p, c_i64, c_p],
+    "gc_bases_rows": [c_i64] + [c_p] * 8 + [c_i64, c_i64, c_i64, c_i64] + [c_p] * 7 + [c_p],
+    "gc_bases_post": [c_i64, c_p, c_i64] + [c_p] * 6 + [c_i64] + [c_p] * 7 + [c_i64, c_p],
     "gc_bt_leaves_bytes": [c_i64, ctypes.POINTER(c_i64)],
     "gc_bt_leaves": [c_i64] + [c_p] * 11 + [c_i64, c_p],
     "gc_bt_level": [c_i64, c_p, c_p, c_p, c_p, c_i64, c_i64, ctypes.c_int32] + [c_p] * 10

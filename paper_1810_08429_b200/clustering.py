@@ -390,6 +390,7 @@ def _build_cluster_tree_device(mesh, basis_kind, leaf_size, device):
         perm_h = perm[cur].cpu().numpy()
     flat = FlatClusterTree(perm_h, start, stop, left, right, parent, depth, lower, upper)
     flat._device = device            # the block tree of a device-built tree is built there too
+    flat._perm_dev = perm[cur]       # leaf dof order on the device (the bases' leaf rows)
     return flat.node(0)
 
 

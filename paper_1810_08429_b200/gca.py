@@ -9,9 +9,9 @@ Host-side mirror of the hot-path part of ``greencross/gca.py``:
 The reference builds bases by recursion (one factor + one ACA per node).
 Here the materialised forest is processed level-synchronously by height
 (SPEC.md:500-501): one ``gc_green_box_rules`` + ``gc_green_factor`` +
-``gc_aca`` launch per level over every node of that level, then one small
-device->host read of ranks and pivots, which the host turns into the next
-level's row lists.  ``build_h2`` assembles every coupling and near-field
+``gc_aca`` launch per level over every node of that level; the next
+level's row lists (the children's pivots) are gathered on the device
+(``csrc/bases.cu``) and the host reads only each level's row totals.  ``build_h2`` assembles every coupling and near-field
 block with two ``gc_assemble_blocks`` launches plus the singular flush;
 values stay in HBM in the matvec layout (``h2.py``) and reach the host only
 through the lazy ``.values`` / ``.v`` / ``.transfer`` views.
@@ -26,7 +26,7 @@ from collections.abc import Sequence
 import numpy as np
 
 from . import _native
-from .assembly import device_block_assembly, green_factors_device, resolve_counts
+from .assembly import device_block_assembly, resolve_counts
 from .device import (DeviceMesh, DeviceRules, SingularQueue, check_mesh, empty, padded_copy,
                      padded_empty, ptr, require_device, stream_handle, to_dev, torch)
 from .errors import ConfigError, GeometryError
@@ -39,17 +39,6 @@ __all__ = ["Interpolation", "aca_interpolation", "BasisNode", "ClusterBasis",
 Interpolation = namedtuple("Interpolation", "pivots v")
 CouplingBlock = namedtuple("CouplingBlock", "row col values")
 NearfieldBlock = namedtuple("NearfieldBlock", "row col values")
-
-
-def _ranges(starts, lengths):
-    """Concatenation of arange(s, s+l) over segments (vectorised)."""
-    starts = np.asarray(starts, dtype=np.int64)
-    lengths = np.asarray(lengths, dtype=np.int64)
-    total = int(lengths.sum())
-    if total == 0:
-        return np.zeros(0, dtype=np.int64)
-    heads = np.cumsum(lengths) - lengths
-    return np.arange(total, dtype=np.int64) + np.repeat(starts - heads, lengths)
 
 
 def _offsets(sizes):
@@ -385,7 +374,7 @@ def build_cluster_basis(tree, mesh, basis, m, delta_factor=0.5, eps=1e-4, side="
 class _Side:
     """Per-basis state while several bases are built in shared launches."""
 
-    def __init__(self, tree, side, marks, row_range, W, dev, basis="constant"):
+    def __init__(self, tree, side, marks, row_range, dev, basis="constant"):
         flat = tree.flat
         self.side = side
         self.basis = basis
@@ -402,17 +391,144 @@ class _Side:
         self.mat, self.roots = mat, roots
         self.store.materialized = mat
         self.store.available = mat.copy()
-        size = flat.stop - flat.start
-        cap = int(np.minimum(size[mat], W).sum()) if mat.any() else 0
-        # [perm | this basis' global pivots]: the row source of every level
-        # (leaf dofs, children's pivots) without a per-level concatenation
-        perm = tree.flat.perm
-        self.combined = np.empty(len(perm) + max(cap, 1), dtype=np.int64)
-        self.combined[:len(perm)] = perm
-        self.gpiv = self.combined[len(perm):]
-        self.cursor = 0
         self.v_parts = []        # (level tensor, start, stop)
         self.v_base = 0
+
+
+def _bases_levels_device(S, flat, heights, dmesh, m, K, W, eps, delta_factor, dev, stream, d_g01, d_w01):
+    """The level loop of :func:`build_cluster_bases` with its bookkeeping on
+    the device (``csrc/bases.cu``): per height the factor rows R (leaf size
+    or the children's ranks), their scans, the row lists, the factor and ACA
+    launches and the local -> global pivot map, with one 4 + sides integer
+    read per level (the row totals that size the buffers and the ACA's
+    shared memory).  Ranks, pivots and offsets come back once at the end."""
+    nf = len(flat)
+    levels, lo = [], 0
+    for h in heights:
+        segs = []
+        for k, s in enumerate(S):
+            ids = np.flatnonzero(s.mat & (flat.height == h))
+            if ids.size:
+                segs.append((k, ids))
+        nn = sum(len(i) for _, i in segs)
+        if nn:
+            levels.append((lo, nn, segs))
+            lo += nn
+    T = lo
+    if T == 0:
+        return 0.0, 0.0
+    all_ids = np.concatenate([i for _, _, segs in levels for _, i in segs])
+    bounds = [np.r_[np.cumsum([0] + [len(i) for _, i in segs])] for _, _, segs in levels]
+    b_off = _offsets(np.array([len(b) for b in bounds]))
+    diam = flat.diam[all_ids]
+    perm_dev = getattr(flat, "_perm_dev", None)
+    if perm_dev is not None and perm_dev.device != dev:
+        perm_dev = None
+    ints = to_dev(np.concatenate([flat.left, flat.right, flat.start, flat.stop, all_ids, np.concatenate(bounds)]
+                                 + ([] if perm_dev is not None else [flat.perm])), dev)
+    d_left, d_right, d_start, d_stop = (ints[i * nf:(i + 1) * nf] for i in range(4))
+    d_nodes = ints[4 * nf:4 * nf + T]
+    d_bounds = ints[4 * nf + T:4 * nf + T + int(b_off[-1] + len(bounds[-1]))]
+    if perm_dev is None:
+        perm_dev = ints[4 * nf + T + len(d_bounds):]
+    box = np.concatenate([flat.lower[all_ids], flat.upper[all_ids], (delta_factor * diam)[:, None],
+                          diam[:, None]], axis=1)
+    dbl = to_dev(np.concatenate([box.ravel(), diam]), dev)
+    d_box, d_diam = dbl[:8 * T], dbl[8 * T:]
+    # per side on the device: rank | piv_off | rows | v_off | cursor | pivots
+    side_buf = []
+    for s in S:
+        cap = int(np.minimum((flat.stop - flat.start)[s.mat], W).sum()) if s.mat.any() else 0
+        b = torch.zeros(4 * nf + 1 + max(cap, 1), dtype=torch.int64, device=dev)
+        b[nf:2 * nf].fill_(-1)
+        b[3 * nf:4 * nf].fill_(-1)
+        side_buf.append(b)
+    # level scratch: R, limit, vcap, their offsets (6 T), descriptors (9 T),
+    # the per-level totals (4 + bounds) and the post scan's rank offsets
+    n_tot = sum(4 + len(b) for b in bounds)
+    scr = torch.empty(15 * T + n_tot + max(nn for _, nn, _ in levels), dtype=torch.int64, device=dev)
+    tb = _native.ctypes.c_int64(0)
+    _native.call("gc_bases_scan_bytes", max(nn for _, nn, _ in levels), _native.ctypes.byref(tb))
+    temp = torch.empty(max(tb.value, 1), dtype=torch.uint8, device=dev)
+    flags = torch.zeros(1, dtype=torch.int32, device=dev)
+    P = scr.data_ptr()
+    p_left, p_right, p_start, p_stop = (t.data_ptr() for t in (d_left, d_right, d_start, d_stop))
+    cols = [P + 8 * c * T for c in range(15)]         # R lim vcap roff ploff voff fdesc(5) adesc(4)
+    t_factor = t_aca = 0.0
+    tot_base = 15 * T
+    rk_off = P + 8 * (15 * T + n_tot)
+    side_code = [0 if s.side == "row" else 1 for s in S]
+    with torch.cuda.device(dev):
+        for li, (lo, nn, segs) in enumerate(levels):
+            R, lim, vcap, roff, ploff, voff = (c + 8 * lo for c in cols[:6])
+            fdesc, adesc = cols[6] + 40 * lo, cols[6] + 40 * T + 32 * lo
+            tot = tot_base + sum(4 + len(b) for b in bounds[:li])
+            pos = [int(v) for v in bounds[li]]
+            for j, (k, ids) in enumerate(segs):
+                sb = side_buf[k].data_ptr()
+                _native.call("gc_bases_R", len(ids), d_nodes.data_ptr() + 8 * (lo + pos[j]), p_left, p_right, p_start,
+                             p_stop, sb, int(pos[j]), W, R, lim, vcap, sb + 16 * nf, stream)
+            _native.call("gc_bases_scan", nn, R, lim, vcap, roff, ploff, voff, d_bounds.data_ptr() + 8 * int(b_off[li]),
+                         len(pos), P + 8 * tot, ptr(temp), tb.value, stream)
+            host = scr[tot:tot + 4 + len(pos)].cpu().numpy()      # the level's only sync
+            r_max, n_rows, n_lim, n_v = (int(v) for v in host[:4])
+            tf = time.perf_counter()
+            rows = torch.empty(max(n_rows, 1), dtype=torch.int64, device=dev)
+            for j, (k, ids) in enumerate(segs):
+                sb = side_buf[k].data_ptr()
+                _native.call("gc_bases_rows", len(ids), d_nodes.data_ptr() + 8 * (lo + pos[j]), p_left, p_right, p_start,
+                             sb, sb + 8 * nf, sb + 8 * (4 * nf + 1), ptr(perm_dev), int(pos[j]), 0,
+                             side_code[k], W, R, roff, ploff, voff, ptr(rows), fdesc, adesc, stream)
+            z = empty(nn * K * 3, dev)
+            sq = empty(nn * K, dev)
+            nz = empty(nn * K * 3, dev)
+            _native.call("gc_green_box_rules", m, ptr(d_g01), ptr(d_w01), nn, d_box.data_ptr() + 64 * lo,
+                         ptr(z), ptr(sq), ptr(nz), stream)
+            fac = empty(max(n_rows, 1) * 2 * K, dev)
+            # one factor launch per run of sides with the same row kind
+            # (collocation rows pair with linear columns)
+            runs = []
+            for j, (k, ids) in enumerate(segs):
+                if runs and runs[-1][0] == S[k].basis:
+                    runs[-1][2] = int(pos[j + 1])
+                else:
+                    runs.append([S[k].basis, int(pos[j]), int(pos[j + 1])])
+            for b, p0, p1 in runs:
+                _native.call("gc_green_factor", dmesh.geom_of("slp", b), -1, K, p1 - p0, fdesc + 40 * p0,
+                             d_diam.data_ptr() + 8 * (lo + p0), ptr(z), ptr(sq), ptr(nz), ptr(rows), ptr(fac),
+                             ptr(flags), stream)
+            ta = time.perf_counter()
+            t_factor += ta - tf
+            V = torch.zeros(max(n_v, 1), dtype=torch.float64, device=dev)
+            U = empty(max(n_v, 1), dev)
+            small = torch.zeros(max(n_lim, 1) + nn, dtype=torch.int64, device=dev)
+            d_piv, d_rank = small[:max(n_lim, 1)], small[max(n_lim, 1):]
+            _native.call("gc_aca", nn, adesc, W, float(eps), 0, ptr(fac), ptr(d_piv), ptr(d_rank),
+                         ptr(V), ptr(U), r_max, stream)
+            for j, (k, ids) in enumerate(segs):
+                s, sb = S[k], side_buf[k].data_ptr()
+                v0, v1 = int(host[4 + j]), int(host[5 + j])
+                _native.call("gc_bases_post", len(ids), d_nodes.data_ptr() + 8 * (lo + pos[j]), int(pos[j]),
+                             ptr(d_rank), ptr(d_piv), ploff, ptr(rows), roff, voff, s.v_base, sb + 32 * nf,
+                             sb, sb + 8 * nf, sb + 8 * (4 * nf + 1), sb + 24 * nf, rk_off, ptr(temp), tb.value,
+                             stream)
+                s.v_parts.append(V[v0:max(v1, v0)])
+                s.v_base += v1 - v0
+            t_aca += time.perf_counter() - ta
+            del U, fac, z, sq, nz
+    fl = flags.cpu()
+    if int(fl[0]) & 1:
+        raise GeometryError("expansion point touches the surface; enlarge delta or the cluster box")
+    for s, b in zip(S, side_buf):
+        st = s.store
+        host = b[:4 * nf + 1].cpu().numpy()
+        st.rank, st.piv_off, st.rows, st.v_off = (host[i * nf:(i + 1) * nf].copy() for i in range(4))
+        cursor = int(host[4 * nf])
+        st.pivots = b[4 * nf + 1:4 * nf + 1 + max(cursor, 1)]
+        st.pivots_host = st.pivots[:cursor].cpu().numpy()
+        inner = np.flatnonzero(s.mat & ~flat.is_leaf)
+        st.child_row[flat.right[inner]] = st.rank[flat.left[inner]]
+    return t_factor, t_aca
 
 
 def build_cluster_bases(tree, mesh, basis, m, delta_factor, eps, sides, orders=(3, 5),
@@ -420,8 +536,9 @@ def build_cluster_bases(tree, mesh, basis, m, delta_factor, eps, sides, orders=(
     """Several nested bases of one cluster tree (row and column side of the
     H2 matrix) built together: per tree height one ``gc_green_box_rules``,
     one ``gc_green_factor`` (side per node) and one ``gc_aca`` launch over
-    the nodes of every basis, then one device->host read of ranks, pivots
-    and the touch flags.  ``sides`` is a list of (side, marks) or (side,
+    the nodes of every basis, with the row lists and the pivot bookkeeping
+    on the device (:func:`_bases_levels_device`); ranks, pivots and the
+    touch flags reach the host once, at the end.  ``sides`` is a list of (side, marks) or (side,
     marks, basis) - collocation rows pair a "collocation" row side with a
     "linear" column side.  Rows are triangles (constant basis) or vertices
     (linear basis, collocation points)."""
@@ -437,127 +554,13 @@ def build_cluster_bases(tree, mesh, basis, m, delta_factor, eps, sides, orders=(
     W = 2 * K
     g01, w01 = _gauss01(m)
     d_g01, d_w01 = to_dev(g01, dev), to_dev(w01, dev)
-    size = flat.stop - flat.start
-    perm = flat.perm
-    S = [_Side(tree, sd[0], sd[1], row_range, W, dev, sd[2] if len(sd) > 2 else basis) for sd in sides]
+    S = [_Side(tree, sd[0], sd[1], row_range, dev, sd[2] if len(sd) > 2 else basis) for sd in sides]
     heights = np.unique(np.concatenate([flat.height[s.mat] for s in S])) if S else []
-    t_factor = t_aca = 0.0
-    stream = stream_handle()
-    for h in heights:
-        # ---- host: row lists of every node of this height, all bases
-        parts = []
-        for k, s in enumerate(S):
-            st = s.store
-            ids = np.flatnonzero(s.mat & (flat.height == h))
-            if not ids.size:
-                continue
-            leaf = flat.is_leaf[ids]
-            lc, rc = np.maximum(flat.left[ids], 0), np.maximum(flat.right[ids], 0)
-            R = np.where(leaf, size[ids], st.rank[lc] + st.rank[rc])
-            # leaf dofs, or the children's pivots (left then right), gathered
-            # from the combined source [perm | this basis' pivots]
-            n_perm = len(perm)
-            st1 = np.where(leaf, flat.start[ids], n_perm + st.piv_off[lc])
-            ln1 = np.where(leaf, size[ids], st.rank[lc])
-            st2 = np.where(leaf, 0, n_perm + st.piv_off[rc])
-            ln2 = np.where(leaf, 0, st.rank[rc])
-            rows_host = s.combined[_ranges(np.stack([st1, st2], 1).ravel(),
-                                         np.stack([ln1, ln2], 1).ravel())]
-            st.child_row[lc[~leaf]] = 0
-            st.child_row[rc[~leaf]] = st.rank[flat.left[ids][~leaf]]
-            st.rows[ids] = R
-            parts.append((k, ids, R, rows_host))
-        if not parts:
-            continue
-        ids_all = np.concatenate([p[1] for p in parts])
-        R = np.concatenate([p[2] for p in parts])
-        rows_host = np.concatenate([p[3] for p in parts])
-        side_code = np.concatenate([np.full(len(p[1]), 0 if S[p[0]].side == "row" else 1)
-                                    for p in parts])
-        nn = len(ids_all)
-        rows_off = _offsets(R)
-        limit = np.minimum(R, W)
-        diam = flat.diam[ids_all]
-        box = np.concatenate([flat.lower[ids_all], flat.upper[ids_all],
-                              (delta_factor * diam)[:, None], diam[:, None]], axis=1)
-        vcap = R * limit
-        v_off = _offsets(vcap)
-        piv_off_l = _offsets(limit)
-        # one upload of every per-node table of this level
-        ints = to_dev(np.concatenate([np.stack([rows_off, R, rows_off * W, np.arange(nn), side_code], 1).ravel(),
-                                      np.stack([rows_off * W, R, piv_off_l, v_off], 1).ravel(),
-                                      rows_host]), dev)
-        fdesc, adesc, d_rows = ints[:5 * nn], ints[5 * nn:9 * nn], ints[9 * nn:]
-        dbl = to_dev(np.concatenate([box.ravel(), diam]), dev)
-        d_box, d_diam = dbl[:8 * nn], dbl[8 * nn:]
-        tf = time.perf_counter()
-        z = empty(nn * K * 3, dev)
-        sq = empty(nn * K, dev)
-        nz = empty(nn * K * 3, dev)
-        with torch.cuda.device(dev):
-            _native.call("gc_green_box_rules", m, ptr(d_g01), ptr(d_w01), nn, ptr(d_box),
-                         ptr(z), ptr(sq), ptr(nz), stream)
-        bases = sorted({S[p[0]].basis for p in parts})
-        if len(bases) == 1:
-            fac, flags = green_factors_device(dmesh, "mixed", K, d_rows, fdesc, d_diam, z, sq, nz,
-                                              int(R.sum()), dev, check_flags=False, basis=bases[0])
-        else:
-            # one launch per row kind (e.g. collocation rows, linear columns)
-            # into the same factor buffer
-            node_basis = np.concatenate([np.full(len(p[1]), S[p[0]].basis, dtype=object) for p in parts])
-            fac = empty(int(R.sum()) * 2 * K, dev)
-            flags = torch.zeros(1, dtype=torch.int32, device=dev)
-            fd = fdesc.view(nn, 5)
-            for b in bases:
-                sel = to_dev(np.flatnonzero(node_basis == b), dev)
-                # keep the gathered tables referenced until the launch is queued
-                # (a temporary freed inside the argument list would be reused)
-                sub_desc, sub_diam = fd[sel].contiguous(), d_diam[sel].contiguous()
-                with torch.cuda.device(dev):
-                    _native.call("gc_green_factor", dmesh.geom_of("slp", b), -1, K, len(sel),
-                                 ptr(sub_desc), ptr(sub_diam), ptr(z), ptr(sq), ptr(nz), ptr(d_rows),
-                                 ptr(fac), ptr(flags), stream)
-        ta = time.perf_counter()
-        t_factor += ta - tf
-        V = torch.zeros(max(int(vcap.sum()), 1), dtype=torch.float64, device=dev)
-        U = empty(max(int(vcap.sum()), 1), dev)
-        small = torch.zeros(max(int(limit.sum()), 1) + nn + 1, dtype=torch.int64, device=dev)
-        d_piv, d_rank = small[:max(int(limit.sum()), 1)], small[-nn - 1:-1]
-        with torch.cuda.device(dev):
-            _native.call("gc_aca", nn, ptr(adesc), W, float(eps), 0, ptr(fac), ptr(d_piv),
-                         ptr(d_rank), ptr(V), ptr(U), int(R.max()), stream)
-            small[-1:].copy_(flags.to(torch.int64))
-        host = small.cpu().numpy()                 # the level's only sync
-        if host[-1] & 1:
-            raise GeometryError("expansion point touches the surface; "
-                                "enlarge delta or the cluster box")
-        rank, piv_local = host[-nn - 1:-1], host[:max(int(limit.sum()), 1)]
-        t_aca += time.perf_counter() - ta
-        del U, fac
-        # ---- per basis: local -> global pivots, compact pivot store
-        o = 0
-        for k, ids, Rk, rh in parts:
-            s, st = S[k], S[k].store
-            n = len(ids)
-            rk = rank[o:o + n]
-            sel = _ranges(piv_off_l[o:o + n], rk)
-            node_of = np.repeat(np.arange(n), rk)
-            roff = rows_off[o:o + n] - rows_off[o]
-            glob = rh[roff[node_of] + piv_local[sel]]
-            s.gpiv[s.cursor:s.cursor + len(glob)] = glob
-            st.piv_off[ids] = s.cursor + _offsets(rk)
-            s.cursor += len(glob)
-            st.rank[ids] = rk
-            v0, v1 = int(v_off[o]), int(v_off[o + n - 1] + vcap[o + n - 1])
-            st.v_off[ids] = s.v_base + v_off[o:o + n] - v0
-            s.v_parts.append(V[v0:max(v1, v0)])
-            s.v_base += v1 - v0
-            o += n
+    t_factor, t_aca = _bases_levels_device(S, flat, heights, dmesh, m, K, W, eps, delta_factor,
+                                           dev, stream_handle(), d_g01, d_w01)
     out = []
     for s in S:
         st = s.store
-        st.pivots_host = s.gpiv[:s.cursor].copy()
-        st.pivots = to_dev(st.pivots_host if s.cursor else np.zeros(1, np.int64), dev)
         st.V = padded_copy(torch.cat(s.v_parts)) if s.v_parts else padded_empty(1, dev)
         if st.V.numel() == 0:
             st.V = padded_empty(1, dev).zero_()

@@ -1,5 +1,5 @@
-"""Assembly time (fresh mesh, after a warm-up) for values of one h2 module
-constant, alternating, N repetitions each.  Usage:
+"""Assembly time (fresh mesh, after a warm-up) for values of one device /
+gca / h2 module constant, alternating, N repetitions each.  Usage:
 python scripts/asm_ab.py NAME v1,v2 level eps [reps]"""
 import ast
 import gc
@@ -10,7 +10,7 @@ import time
 import torch
 
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
-from paper_1810_08429_b200 import cli, device as _device, geometry, h2  # noqa: E402
+from paper_1810_08429_b200 import cli, device as _device, gca, geometry, h2  # noqa: E402
 
 name, vals = sys.argv[1], [ast.literal_eval(v) for v in sys.argv[2].split(",")]
 L, eps = int(sys.argv[3]), float(sys.argv[4])
@@ -24,7 +24,7 @@ torch.cuda.synchronize()
 res = {v: [] for v in vals}
 for r in range(reps):
     for v in vals:
-        setattr(_device if hasattr(_device, name) else h2, name, v)
+        setattr(next(mod for mod in (_device, gca, h2) if hasattr(mod, name)), name, v)
         mesh = geometry.build_sphere_mesh(L)
         torch.cuda.synchronize()
         t0 = time.perf_counter()

@@ -442,6 +442,9 @@ int gc_col_pairs_blocks(const gc_geom* g, const double* verts, const double* reg
 int gc_tree_boxes(int64_t nseg, const int64_t* start, const int64_t* stop, const double* pack,
                   double* box, void* stream);
 int gc_tree_sort_bytes(int64_t nitems, int64_t nseg, int64_t* bytes);
+/* Split axes: axis[i] = argmax of the extents of box row rows[i] (first
+ * maximum; clustering.py:154 np.argmax(box.upper - box.lower)). */
+int gc_tree_axis(int64_t k, const int64_t* rows, const double* box, int64_t* axis, void* stream);
 int gc_tree_split(int64_t nseg, const int64_t* seg_start, const int64_t* seg_len, const int64_t* seg_head,
                   const int64_t* seg_axis, const int32_t* offsets, int64_t nitems, const double* pack_old,
                   double* pack_new, const int64_t* perm_old, int64_t* perm_new, double* keys, int32_t* vals,

@@ -307,10 +307,50 @@ def build_cluster_tree(mesh, basis_kind="constant", leaf_size=32, device=None):
     return flat.node(0)
 
 
+def _tree_topology(n, leaf_size):
+    """The shape of the cluster tree of n dofs: it depends only on n and the
+    leaf size (every split halves a segment, ``clustering.py:150-160``).
+    Returns the per-node arrays and, per depth, the frontier (node ids in
+    start order) and which of them split."""
+    memo = {}
+    total = _subtree_counts(n, leaf_size, memo)
+    start = np.zeros(total, dtype=np.int64)
+    stop = np.zeros(total, dtype=np.int64)
+    left = np.full(total, -1, dtype=np.int64)
+    right = np.full(total, -1, dtype=np.int64)
+    parent = np.full(total, -1, dtype=np.int64)
+    depth = np.zeros(total, dtype=np.int64)
+    stop[0] = n
+    ids = np.array([0], dtype=np.int64)
+    depths = []
+    d = 0
+    while ids.size:
+        depth[ids] = d
+        split = (stop[ids] - start[ids]) > leaf_size
+        depths.append((ids, split))
+        if not split.any():
+            break
+        ids_s = ids[split]
+        s_s, e_s = start[ids_s], stop[ids_s]
+        half = (e_s - s_s) // 2
+        lid = ids_s + 1
+        rid = ids_s + 1 + np.array([memo[int(h)] for h in half], dtype=np.int64)
+        left[ids_s], right[ids_s] = lid, rid
+        parent[lid], parent[rid] = ids_s, ids_s
+        start[lid], stop[lid] = s_s, s_s + half
+        start[rid], stop[rid] = s_s + half, e_s
+        ids = np.concatenate([lid, rid])
+        ids = ids[np.argsort(start[ids], kind="stable")]
+        d += 1
+    return start, stop, left, right, parent, depth, depths
+
+
 def _build_cluster_tree_device(mesh, basis_kind, leaf_size, device):
-    """build_cluster_tree with the n-sized work on the device: the frontier
-    bookkeeping (node ids, child ranges, split axes) stays on the host and
-    reads back 6 doubles per frontier node per depth."""
+    """build_cluster_tree with the n-sized work on the device.  The tree's
+    shape is known up front (:func:`_tree_topology`), so every depth - box
+    reduction, split axes, key sort and permutation - is queued back to back
+    from one upload of the frontier tables; the boxes and the permutation
+    come back in one read at the end."""
     import torch
 
     from . import _native
@@ -323,16 +363,30 @@ def _build_cluster_tree_device(mesh, basis_kind, leaf_size, device):
     else:
         points, lo, hi = _support_data(mesh, basis_kind)
         n = len(points)
-    memo = {}
-    total = _subtree_counts(n, leaf_size, memo)
-    start = np.zeros(total, dtype=np.int64)
-    stop = np.zeros(total, dtype=np.int64)
-    left = np.full(total, -1, dtype=np.int64)
-    right = np.full(total, -1, dtype=np.int64)
-    parent = np.full(total, -1, dtype=np.int64)
-    depth = np.zeros(total, dtype=np.int64)
-    lower = np.zeros((total, 3))
-    upper = np.zeros((total, 3))
+    start, stop, left, right, parent, depth, depths = _tree_topology(n, leaf_size)
+    total = len(start)
+    # one table: per depth the frontier [start | stop], then per splitting
+    # depth the split rows (into the box table), segment start / length /
+    # head and the int32 item offsets (as int64 pairs)
+    front = np.concatenate([ids for ids, _ in depths])
+    f_off = np.cumsum([0] + [len(ids) for ids, _ in depths])
+    parts, plan = [start[front], stop[front]], []
+    o = 2 * len(front)
+    for di, (ids, split) in enumerate(depths):
+        if not split.any():
+            continue
+        ids_s = ids[split]
+        s_s = start[ids_s]
+        seg_len = stop[ids_s] - s_s
+        heads = np.cumsum(seg_len) - seg_len
+        nitems = int(seg_len.sum())
+        offs = np.r_[heads, nitems].astype(np.int32)
+        offs = np.r_[offs, np.zeros(len(offs) % 2, np.int32)].view(np.int64)
+        k = len(ids_s)
+        rows = f_off[di] + np.flatnonzero(split)
+        parts += [rows, s_s, seg_len, heads, offs]
+        plan.append((di, k, nitems, o))
+        o += 4 * k + len(offs)
     f64 = dict(dtype=torch.float64, device=device)
     pack = [charts["support"].clone() if charts is not None else
             torch.from_numpy(np.ascontiguousarray(np.concatenate([lo, hi, points], axis=1))).to(device),
@@ -340,54 +394,37 @@ def _build_cluster_tree_device(mesh, basis_kind, leaf_size, device):
     perm = [torch.arange(n, dtype=torch.int64, device=device), torch.empty(n, dtype=torch.int64, device=device)]
     keys = torch.empty(2 * n, **f64)                       # sort scratch (torch caching allocator)
     vals = torch.empty(2 * n, dtype=torch.int32, device=device)
-    cur = 0
-    ids = np.array([0], dtype=np.int64)
-    stop[0] = n
-    d = 0
     with torch.cuda.device(device):
         st = stream_handle()
-        while ids.size:
-            s_, e_ = start[ids], stop[ids]
-            depth[ids] = d
-            se = torch.from_numpy(np.concatenate([s_, e_])).to(device)
-            box = torch.empty((len(ids), 6), **f64)
-            _native.call("gc_tree_boxes", len(ids), ptr(se[:len(ids)]), ptr(se[len(ids):]), ptr(pack[cur]),
-                         ptr(box), st)
-            bh = box.cpu().numpy()
-            lower[ids], upper[ids] = bh[:, :3], bh[:, 3:]
-            split = (e_ - s_) > leaf_size
-            if not split.any():
+        tab = torch.from_numpy(np.concatenate(parts)).to(device)
+        box = torch.empty((len(front), 6), **f64)
+        axis = torch.empty(max([k for _, k, _, _ in plan] + [1]), dtype=torch.int64, device=device)
+        tb = _native.ctypes.c_int64(0)
+        _native.call("gc_tree_sort_bytes", n, 1, _native.ctypes.byref(tb))
+        temp = torch.empty(max(tb.value, 1), dtype=torch.uint8, device=device)
+        T, nf = tab.data_ptr(), len(front)
+        cur = 0
+        steps = {di: (k, nitems, o) for di, k, nitems, o in plan}
+        for di in range(len(depths)):
+            f0, f1 = int(f_off[di]), int(f_off[di + 1])
+            _native.call("gc_tree_boxes", f1 - f0, T + 8 * f0, T + 8 * (nf + f0), ptr(pack[cur]),
+                         box.data_ptr() + 48 * f0, st)
+            if di not in steps:
                 break
-            ids_s, s_s, e_s = ids[split], s_[split], e_[split]
-            axis = np.argmax(upper[ids_s] - lower[ids_s], axis=1)
-            seg_len = e_s - s_s
-            heads = np.cumsum(seg_len) - seg_len
-            nitems = int(seg_len.sum())
-            offs = np.r_[heads, nitems].astype(np.int32)
-            seg = torch.from_numpy(np.concatenate([s_s, seg_len, heads, axis.astype(np.int64)])).to(device)
-            d_off = torch.from_numpy(offs).to(device)
-            k = len(ids_s)
+            k, nitems, o = steps[di]
+            _native.call("gc_tree_axis", k, T + 8 * o, ptr(box), ptr(axis), st)
             nxt = 1 - cur
             pack[nxt].copy_(pack[cur])
             perm[nxt].copy_(perm[cur])
-            tb = _native.ctypes.c_int64(0)
-            _native.call("gc_tree_sort_bytes", nitems, k, _native.ctypes.byref(tb))
-            temp = torch.empty(max(tb.value, 1), dtype=torch.uint8, device=device)
-            _native.call("gc_tree_split", k, ptr(seg[:k]), ptr(seg[k:2 * k]), ptr(seg[2 * k:3 * k]),
-                         ptr(seg[3 * k:]), ptr(d_off), nitems, ptr(pack[cur]), ptr(pack[nxt]), ptr(perm[cur]),
+            _native.call("gc_tree_split", k, T + 8 * (o + k), T + 8 * (o + 2 * k), T + 8 * (o + 3 * k),
+                         ptr(axis), T + 8 * (o + 4 * k), nitems, ptr(pack[cur]), ptr(pack[nxt]), ptr(perm[cur]),
                          ptr(perm[nxt]), ptr(keys), ptr(vals), ptr(temp), tb.value, st)
             cur = nxt
-            half = seg_len // 2
-            lid = ids_s + 1
-            rid = ids_s + 1 + np.array([memo[int(h)] for h in half], dtype=np.int64)
-            left[ids_s], right[ids_s] = lid, rid
-            parent[lid], parent[rid] = ids_s, ids_s
-            start[lid], stop[lid] = s_s, s_s + half
-            start[rid], stop[rid] = s_s + half, e_s
-            ids = np.concatenate([lid, rid])
-            ids = ids[np.argsort(start[ids], kind="stable")]
-            d += 1
+        bh = box.cpu().numpy()
         perm_h = perm[cur].cpu().numpy()
+    lower = np.zeros((total, 3))
+    upper = np.zeros((total, 3))
+    lower[front], upper[front] = bh[:, :3], bh[:, 3:]
     flat = FlatClusterTree(perm_h, start, stop, left, right, parent, depth, lower, upper)
     flat._device = device            # the block tree of a device-built tree is built there too
     flat._perm_dev = perm[cur]       # leaf dof order on the device (the bases' leaf rows)

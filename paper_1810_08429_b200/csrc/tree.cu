@@ -13,7 +13,10 @@
 //                   the large top-level segments);
 //   * k_seg_permute - applies the order to the permutation and to the
 //                   packed (lo | hi | point) rows.
-// The host keeps the per-node bookkeeping (frontier, child ids, axes).
+//   * k_seg_axis  - the longest box axis of every splitting node.
+// The tree's shape depends only on the dof count and the leaf size, so the
+// host lays out every depth's frontier up front and the depths run back to
+// back on the stream; boxes and the permutation come back once.
 #include <cub/device/device_radix_sort.cuh>
 
 #include "common.cuh"
@@ -99,9 +102,32 @@ __global__ void k_seg_permute(int64_t n, const int32_t* __restrict__ dst, const 
     }
 }
 
+// longest box axis of the splitting nodes (np.argmax: first maximum wins)
+__global__ void k_seg_axis(int64_t k, const int64_t* __restrict__ rows, const double* __restrict__ box,
+                           int64_t* __restrict__ axis) {
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < k; i += (int64_t)gridDim.x * blockDim.x) {
+        const double* b = box + 6 * rows[i];
+        const double e0 = __dsub_rn(b[3], b[0]), e1 = __dsub_rn(b[4], b[1]), e2 = __dsub_rn(b[5], b[2]);
+        int64_t ax = 0;
+        double m = e0;
+        if (e1 > m) { ax = 1; m = e1; }
+        if (e2 > m) ax = 2;
+        axis[i] = ax;
+    }
+}
+
 }  // namespace gcb
 
 using namespace gcb;
+
+// split axes of k nodes whose boxes are the rows [dev] of box (6 per row)
+extern "C" int gc_tree_axis(int64_t k, const int64_t* rows, const double* box, int64_t* axis, void* stream) {
+    if (k <= 0) return GC_OK;
+    const int64_t grid = (k + 255) / 256 < 148 * 8 ? (k + 255) / 256 : 148 * 8;
+    k_seg_axis<<<(unsigned)grid, 256, 0, (cudaStream_t)stream>>>(k, rows, box, axis);
+    GC_CHECK_LAUNCH("k_seg_axis");
+    return GC_OK;
+}
 
 extern "C" int gc_tree_boxes(int64_t nseg, const int64_t* start, const int64_t* stop, const double* pack,
                              double* box, void* stream) {

@@ -228,6 +228,35 @@ int gc_bases_post(int64_t n, const int64_t* nodes, int64_t pos0, const int64_t* 
                   int64_t v_base, int64_t* cursor, int64_t* rank, int64_t* piv_off, int64_t* gpiv,
                   int64_t* v_off_node, int64_t* rk_off, void* temp, int64_t temp_bytes, void* stream);
 
+/* Block tables of build_h2 (gca.py:282-312: the admissible leaves become
+ * coupling blocks, pivot rows x pivot columns, the inadmissible ones
+ * near-field blocks, full clusters).  From nl block-tree leaves leaf_ids
+ * [dev] in depth-first order with node_row / node_col [dev] (int64) and
+ * node_state [dev] (int8, 0 admissible / 1 inadmissible), the blocks of
+ * one kind (near = 0 coupling, 1 near field), optionally only block rows
+ * whose cluster lies in tree positions [lo, hi) (lo < 0: all).  Sizes are
+ * the ranks r_rank / c_rank [dev] (coupling) or the cluster sizes from
+ * r_start / r_stop / c_start / c_stop [dev]; a coupling block whose row
+ * cluster has r_ok = 0 or column cluster c_ok = 0 [dev] (int8: basis content
+ * / pivots present) is counted in totals[7].  Storage offsets group the
+ * blocks by key = row cluster (sharded: 2 row + column outside [lo, hi)),
+ * stable in DFS order, keys below 2^key_bits - 1.
+ * table [dev] (6 x count, column-major with stride count): row, col, nr,
+ * nc, off, order (block indices by ascending offset); desc [dev] (count x 5)
+ * of the non-empty blocks for gc_assemble_blocks: (row_off, nr, col_off,
+ * nc, off) with row/col offsets into the pivot lists r_poff / c_poff
+ * (coupling) or the cluster starts (near); totals [dev] (8 int64, zeroed
+ * by the caller): count, non-empty, max nr, max nc, entries, two counters,
+ * blocks without basis content.  Scratch [dev]: 12 nl
+ * int64, 2 nl bytes, temp of gc_h2_blocks_bytes(nl) bytes.  No host sync. */
+int gc_h2_blocks_bytes(int64_t nl, int64_t* bytes);
+int gc_h2_blocks(int64_t nl, const int64_t* leaf_ids, const int64_t* node_row, const int64_t* node_col,
+                 const int8_t* node_state, const int64_t* r_start, const int64_t* r_stop, const int64_t* c_start,
+                 const int64_t* c_stop, const int64_t* r_rank, const int64_t* r_poff, const int64_t* c_rank,
+                 const int64_t* c_poff, const int8_t* r_ok, const int8_t* c_ok, int64_t lo, int64_t hi,
+                 int32_t near, int32_t key_bits, int64_t* table, int64_t* desc, int64_t* totals, int64_t* scratch,
+                 char* flags, void* temp, int64_t temp_bytes, void* stream);
+
 /* Batched transpose: for node i with desc (off, rows, cols) [dev] (nn,3):
  * out[off + c*rows + r] = in[off + r*cols + c]. */
 int gc_batched_transpose(int64_t nn, const int64_t* desc, const double* in,

@@ -59,6 +59,9 @@ _SIGNATURES = {
     "gc_bases_scan": [c_i64] + [c_p] * 7 + [c_i64, c_p, c_p, c_i64, c_p],
     "gc_bases_rows": [c_i64] + [c_p] * 8 + [c_i64, c_i64, c_i64, c_i64] + [c_p] * 7 + [c_p],
     "gc_bases_post": [c_i64, c_p, c_i64] + [c_p] * 6 + [c_i64] + [c_p] * 7 + [c_i64, c_p],
+    "gc_h2_blocks_bytes": [c_i64, ctypes.POINTER(c_i64)],
+    "gc_h2_blocks": [c_i64] + [c_p] * 14 + [c_i64, c_i64, ctypes.c_int32, ctypes.c_int32] + [c_p] * 6
+                    + [c_i64, c_p],
     "gc_bt_leaves_bytes": [c_i64, ctypes.POINTER(c_i64)],
     "gc_bt_leaves": [c_i64] + [c_p] * 11 + [c_i64, c_p],
     "gc_bt_level": [c_i64, c_p, c_p, c_p, c_p, c_i64, c_i64, ctypes.c_int32] + [c_p] * 10

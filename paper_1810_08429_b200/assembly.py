@@ -96,7 +96,7 @@ def galerkin_pair_evaluator(kind, mesh, basis, q_reg, q_sing, device=None):
 
 
 def device_block_assembly(dmesh, rules, queue, row_idx, col_idx, desc, out, stats=None, kind="slp",
-                          d_desc=None, events=None, pending=None):
+                          d_desc=None, events=None, pending=None, shape=None):
     """Assemble blocks described by ``desc (nb,5)`` into the device buffer
     ``out`` (column-major per block); singular pairs are flushed at the end.
     ``kind`` "slp" / "dlp" picks the kernel (``rules`` must match it);
@@ -106,7 +106,9 @@ def device_block_assembly(dmesh, rules, queue, row_idx, col_idx, desc, out, stat
     ``pending``: asynchronous mode (plane charts) - no host synchronisation;
     appends (device singular counts, total entries) to the list and returns
     None; the caller resolves the counts and checks the queue flags after
-    its own synchronisation (:func:`resolve_counts`)."""
+    its own synchronisation (:func:`resolve_counts`).  ``shape``: (blocks,
+    max rows, max cols, entries) of a descriptor table that exists on the
+    device only (``desc`` None)."""
     if getattr(rules, "kind", "slp") != kind:
         raise ConfigError("rules built for %r, assembling %r" % (rules.kind, kind))
     geom = dmesh.geom_of(kind)
@@ -115,10 +117,15 @@ def device_block_assembly(dmesh, rules, queue, row_idx, col_idx, desc, out, stat
         # curved charts: singular pairs take the full Sauter-Schwab rules
         from . import linear
         full = linear.LinearRules.get(dmesh.q_reg, rules.q_sing, out.device)
-    nb = len(desc)
+    if shape is not None:
+        nb, max_rows, max_cols, total = (int(v) for v in shape[:4])
+    else:
+        nb = len(desc)
+        if nb:
+            max_rows, max_cols = int(desc[:, 1].max()), int(desc[:, 3].max())
+            total = int((desc[:, 1] * desc[:, 3]).sum())
     if nb == 0:
         return [0, 0, 0, 0]
-    entries = desc[:, 1] * desc[:, 3]
     if d_desc is None:
         d_desc = to_dev(desc.astype(np.int64), out.device)
     stream = stream_handle()
@@ -126,9 +133,8 @@ def device_block_assembly(dmesh, rules, queue, row_idx, col_idx, desc, out, stat
         ev = [torch.cuda.Event(enable_timing=True) for _ in range(3)] if events is not None else None
         if ev:
             ev[0].record()
-        _native.call("gc_assemble_blocks", geom, nb, ptr(d_desc), int(desc[:, 1].max()),
-                     int(desc[:, 3].max()), ptr(row_idx), ptr(col_idx), ptr(out), queue.struct, ptr(queue.flags),
-                     stream)
+        _native.call("gc_assemble_blocks", geom, nb, ptr(d_desc), max_rows, max_cols, ptr(row_idx),
+                     ptr(col_idx), ptr(out), queue.struct, ptr(queue.flags), stream)
         if ev:
             ev[1].record()
         counts = (_native.c_i64 * 4)()
@@ -145,11 +151,11 @@ def device_block_assembly(dmesh, rules, queue, row_idx, col_idx, desc, out, stat
             ev[2].record()
             events.append(ev)
     if pending is not None and full is None:
-        pending.append((cdev, int(entries.sum())))
+        pending.append((cdev, total))
         return None
     queue.check_flags()
     n_sing = [int(counts[k]) for k in range(4)]
-    n_sing[0] = int(entries.sum()) - sum(n_sing[1:])
+    n_sing[0] = total - sum(n_sing[1:])
     return n_sing
 
 

@@ -656,6 +656,7 @@ def _build_block_tree_device(row_root, col_root, eta, mode, device):
         row, col, state, level, key, parent = (o[:n].cpu().numpy() for o in out)
         leaf_ids, leaf_key = lids[:nl].cpu().numpy(), lkey[:nl].cpu().numpy()
     flat = FlatBlockTree(rt, ct, row, col, state, level, key, parent, leaves=(leaf_ids, leaf_key))
+    flat._dev = (out[0][:n], out[1][:n], out[2][:n], lids[:nl])    # row, col, state, leaves (build_h2 tables)
     return BlockTree(flat, 0)
 
 

@@ -717,6 +717,98 @@ def _case_seconds(calls, rules):
     return sec
 
 
+class _BlockTables:
+    """Coupling and near-field block tables of one build_h2 call, built on
+    the device (``gc_h2_blocks``): the assembly descriptors stay there, the
+    host copies (row, col, nr, nc, off, order per kind) arrive on a side
+    stream while the quadrature runs."""
+
+    def __init__(self, shapes, c_desc, n_desc, host_buf, counts, done):
+        self.shapes = shapes
+        self.c_desc, self.n_desc = c_desc, n_desc
+        self._buf, self._counts, self._done = host_buf, counts, done
+        self._host = None
+
+    def host(self):
+        if self._host is None:
+            self._done.synchronize()
+            h = self._buf.numpy()
+            nc_, nn_ = self._counts
+            tc, tn = h[:6 * nc_].reshape(6, nc_), h[6 * nc_:6 * (nc_ + nn_)].reshape(6, nn_)
+            self._host = tuple(tc), tuple(tn)
+        return self._host
+
+
+def _device_block_tables(btree, rf, cf, rstore, cstore, row_range, dev):
+    """The block tables of :func:`build_h2` from the block tree's leaves
+    (``csrc/h2blocks.cu``); one small read of the totals (counts, maxima,
+    entries), which size the stores and the quadrature launches."""
+    fb = btree.flat
+    a, b = np.searchsorted(fb.leaf_key, [fb.key_lo[btree._id], fb.key_hi[btree._id]], side="left")
+    nl = int(b - a)
+    dv = getattr(fb, "_dev", None)
+    if dv is None or dv[0].device != dev:
+        nn = len(fb.row)
+        ints = to_dev(np.concatenate([fb.row, fb.col, fb.leaf_ids]).astype(np.int64), dev)
+        dv = (ints[:nn], ints[nn:2 * nn], to_dev(fb.state.astype(np.int8), dev), ints[2 * nn:])
+        fb._dev = dv
+    node_row, node_col, node_state, leaf_ids = dv
+    same = cf is rf
+    parts = [rf.start, rf.stop, rstore.rank, rstore.piv_off]
+    if not same:
+        parts += [cf.start, cf.stop]
+    parts += [cstore.rank, cstore.piv_off]
+    tree_i = to_dev(np.concatenate(parts).astype(np.int64), dev)
+    nr_, nc_ = len(rf.start), len(cf.start)
+    r_start, r_stop, r_rank, r_poff = (tree_i[k * nr_:(k + 1) * nr_] for k in range(4))
+    o = 4 * nr_
+    if same:
+        c_start, c_stop = r_start, r_stop
+    else:
+        c_start, c_stop = tree_i[o:o + nc_], tree_i[o + nc_:o + 2 * nc_]
+        o += 2 * nc_
+    c_rank, c_poff = tree_i[o:o + nc_], tree_i[o + nc_:o + 2 * nc_]
+    ok = to_dev(np.concatenate([rstore.materialized, cstore.available]).astype(np.int8), dev)
+    r_ok, c_ok = ok[:nr_], ok[nr_:]
+    lo, hi = (-1, -1) if row_range is None else (int(row_range[0]), int(row_range[1]))
+    key_bits = max(1, int(2 * nr_ + 2).bit_length())
+    n = max(nl, 1)
+    tb = _native.ctypes.c_int64(0)
+    _native.call("gc_h2_blocks_bytes", n, _native.ctypes.byref(tb))
+    temp = torch.empty(max(tb.value, 1), dtype=torch.uint8, device=dev)
+    scratch = torch.empty(12 * n, dtype=torch.int64, device=dev)
+    flags = torch.empty(2 * n, dtype=torch.int8, device=dev)
+    tables = torch.empty(2, 11 * n, dtype=torch.int64, device=dev)       # table (6 n) | desc (5 n) per kind
+    totals = torch.zeros(2, 8, dtype=torch.int64, device=dev)
+    stream = stream_handle()
+    with torch.cuda.device(dev):
+        for kind in (0, 1):
+            _native.call("gc_h2_blocks", nl, leaf_ids.data_ptr() + 8 * int(a), ptr(node_row), ptr(node_col),
+                         ptr(node_state), ptr(r_start), ptr(r_stop), ptr(c_start), ptr(c_stop), ptr(r_rank),
+                         ptr(r_poff), ptr(c_rank), ptr(c_poff), ptr(r_ok), ptr(c_ok), lo, hi, kind, key_bits,
+                         ptr(tables[kind]), tables[kind].data_ptr() + 8 * 6 * n, totals[kind].data_ptr(),
+                         ptr(scratch), ptr(flags), ptr(temp), tb.value, stream)
+        tot = totals.cpu().numpy()                  # the only synchronisation
+        if tot[0, 7]:
+            raise ConfigError("coupling block without basis content; build the bases "
+                              "with coupling_marks(btree)")
+        counts = int(tot[0, 0]), int(tot[1, 0])
+        host = torch.empty(max(6 * sum(counts), 1), dtype=torch.int64, pin_memory=True)
+        side = torch.cuda.Stream(dev)
+        side.wait_stream(torch.cuda.current_stream(dev))
+        with torch.cuda.stream(side):
+            host[:6 * counts[0]].copy_(tables[0, :6 * counts[0]], non_blocking=True)
+            host[6 * counts[0]:6 * sum(counts)].copy_(tables[1, :6 * counts[1]], non_blocking=True)
+            done = torch.cuda.Event()
+            done.record(side)
+        # the tables stay referenced by the side stream's copy
+        tables.record_stream(side)
+    shapes = tuple((int(t[1]), int(t[2]), int(t[3]), int(t[4]), int(t[0])) for t in tot)
+    c_desc = tables[0, 6 * n:6 * n + 5 * shapes[0][0]].view(-1, 5)
+    n_desc = tables[1, 6 * n:6 * n + 5 * shapes[1][0]].view(-1, 5)
+    return _BlockTables(shapes, c_desc, n_desc, host, counts, done)
+
+
 def build_h2(btree, row_basis, col_basis, mesh, kind="slp", basis="constant",
              disc="galerkin", orders=(3, 5), capacity=None, threads=None, device=None,
              row_range=None):
@@ -735,53 +827,30 @@ def build_h2(btree, row_basis, col_basis, mesh, kind="slp", basis="constant",
     fb = btree.flat
     rf, cf = fb.row_tree, fb.col_tree
     rstore, cstore = row_basis.store, col_basis.store
-    ids = btree._leaf_ids()
-    st = fb.state[ids]
-    lr, lc = fb.row[ids], fb.col[ids]
-    if row_range is not None:
-        keep = (rf.start[lr] >= row_range[0]) & (rf.stop[lr] <= row_range[1])
-        ids, st, lr, lc = ids[keep], st[keep], lr[keep], lc[keep]
-    adm = st == 0
-    cr, cc = lr[adm], lc[adm]
-    nr_r, nc_r = lr[~adm], lc[~adm]
-    if np.any(~rstore.materialized[cr]) or np.any(~cstore.available[cc]):
-        raise ConfigError("coupling block without basis content; build the bases "
-                          "with coupling_marks(btree)")
     dmesh = DeviceMesh.get(mesh, orders[0], dev)
     rules = DeviceRules.get(orders[1], dev, kind)
     queue = SingularQueue.get(mesh, dev)
     t0 = time.perf_counter()
-    # coupling blocks: pivot rows x pivot columns
-    c_nr, c_nc = rstore.rank[cr], cstore.rank[cc]
-    # storage grouped by row cluster: the blocks of one block row form one
-    # contiguous (sum r_sigma) x r_tau panel for the matvec (h2.PanelPlan)
-    # a block-row shard stores, inside each block row, the blocks with
-    # local columns (its own tree positions) before the others, so either
-    # subset is one contiguous sub-panel (the sharded product runs them
-    # before / after its all-gathers, parallel.ShardPlan)
-    if row_range is not None:
-        c_key = 2 * cr + ~((cf.start[cc] >= row_range[0]) & (cf.stop[cc] <= row_range[1]))
-    else:
-        c_key = cr
-    c_off, c_order = _grouped_offsets(c_key, c_nr * c_nc, with_order=True)
-    c_total = int((c_nr * c_nc).sum())
+    # coupling blocks: pivot rows x pivot columns; near-field blocks: full
+    # clusters.  Storage is grouped by row cluster: the blocks of one block
+    # row form one contiguous (sum r_sigma) x r_tau panel for the matvec
+    # (h2.PanelPlan); a block-row shard stores, inside each block row, the
+    # blocks with local columns (its own tree positions) before the others,
+    # so either subset is one contiguous sub-panel (the sharded product runs
+    # them before / after its all-gathers, parallel.ShardPlan)
+    tabs = _device_block_tables(btree, rf, cf, rstore, cstore, row_range, dev)
+    c_shape, n_shape = tabs.shapes
+    c_total, n_total = c_shape[3], n_shape[3]
     coup = padded_empty(max(c_total, 1), dev)
-    cdesc = np.stack([rstore.piv_off[cr], c_nr, cstore.piv_off[cc], c_nc, c_off], 1)
-    keep = (c_nr > 0) & (c_nc > 0)
-    n_nr = rf.stop[nr_r] - rf.start[nr_r]
-    n_nc = cf.stop[nc_r] - cf.start[nc_r]
-    if row_range is not None:
-        n_key = 2 * nr_r + ~((cf.start[nc_r] >= row_range[0]) & (cf.stop[nc_r] <= row_range[1]))
-    else:
-        n_key = nr_r
-    n_off, n_order = _grouped_offsets(n_key, n_nr * n_nc, with_order=True)
-    near = padded_empty(max(int((n_nr * n_nc).sum()), 1), dev)
+    near = padded_empty(max(n_total, 1), dev)
     perm_r = to_dev(rf.perm, dev)
     perm_c = perm_r if cf is rf else to_dev(cf.perm, dev)
     if basis == "linear":
         # vertex DOFs: every block is the scatter of its triangle pairs'
         # 3x3 integrals (linear.py); collocation rows are point evaluations
         from . import linear
+        (cr, cc, c_nr, c_nc, c_off, c_order), (nr_r, nc_r, n_nr, n_nc, n_off, n_order) = tabs.host()
+        keep = (c_nr > 0) & (c_nc > 0)
         rp, cp = rstore.pivots_host, cstore.pivots_host
         # (rows, cols, out_off, row key, col key): one triangle table per cluster
         cblocks = [(rp[rstore.piv_off[a]:rstore.piv_off[a] + nr], cp[cstore.piv_off[b]:cstore.piv_off[b] + nc], o,
@@ -803,19 +872,18 @@ def build_h2(btree, row_basis, col_basis, mesh, kind="slp", basis="constant",
     else:
         # plane charts: no host synchronisation - the quadrature runs while
         # the caller continues (e.g. builds the matvec plan); the counts,
-        # the queue flags and the timings settle on first use (H2Matrix.settle)
+        # the queue flags and the timings settle on first use (H2Matrix.settle).
+        # The descriptors were built on the device; the host copies of the
+        # block tables arrive meanwhile on a side stream.
         ev_c, ev_n, pending = [], [], ([] if not dmesh.curved else None)
-        # both block tables go up before the first quadrature launch: a large
-        # pageable upload waits for the work queued on its stream
-        ndesc = np.stack([rf.start[nr_r], n_nr, cf.start[nc_r], n_nc, n_off], 1)
-        c_d = to_dev(cdesc[keep].astype(np.int64), dev) if keep.any() else None
-        n_d = to_dev(ndesc.astype(np.int64), dev) if len(ndesc) else None
-        stats_c = device_block_assembly(dmesh, rules, queue, rstore.pivots, cstore.pivots,
-                                        cdesc[keep], coup, kind=kind, events=ev_c, pending=pending, d_desc=c_d)
+        stats_c = device_block_assembly(dmesh, rules, queue, rstore.pivots, cstore.pivots, None, coup,
+                                        kind=kind, events=ev_c, pending=pending, d_desc=tabs.c_desc,
+                                        shape=c_shape)
         t1 = time.perf_counter()
         # near-field blocks: full clusters
-        stats_n = device_block_assembly(dmesh, rules, queue, perm_r, perm_c, ndesc, near, kind=kind,
-                                        events=ev_n, pending=pending, d_desc=n_d)
+        stats_n = device_block_assembly(dmesh, rules, queue, perm_r, perm_c, None, near, kind=kind,
+                                        events=ev_n, pending=pending, d_desc=tabs.n_desc, shape=n_shape)
+        (cr, cc, c_nr, c_nc, c_off, c_order), (nr_r, nc_r, n_nr, n_nc, n_off, n_order) = tabs.host()
     d = DeviceH2(dev)
     d.coup, d.near = coup, near
     d.c_rows, d.c_cols, d.c_nr, d.c_nc, d.c_off = cr, cc, c_nr, c_nc, c_off

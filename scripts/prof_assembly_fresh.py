@@ -67,6 +67,11 @@ s = io.StringIO()
 st = pstats.Stats(pr, stream=s)
 st.sort_stats("tottime").print_callers("argsort|_native.py:138|method 'cpu'|method 'to' of|stack|tolist")
 print(s.getvalue()[:12000])
+callees = os.environ.get("PROF_CALLEES")
+if callees:
+    s = io.StringIO()
+    pstats.Stats(pr, stream=s).sort_stats("cumulative").print_callees(callees)
+    print(s.getvalue()[:20000])
 print("native calls (count, s):")
 for k, (n, t) in sorted(_calls.items(), key=lambda kv: -kv[1][1])[:20]:
     print("  %-28s %5d %8.4f" % (k, n, t))

@@ -211,6 +211,7 @@ def _stream_ptr(stream=None):
 
 _ITEM_ELEMS = 65536          # <= 512 KB of matrix data per bulk work item (rows capped at 1024)
 _ITEM_MAX_ROWS = 1024        # PAN_MAX_ROWS in csrc/h2mv.cu
+_BULK_ITEMS_PER_SM = 1       # bulk items per SM per phase (4 -> 1: C2 product -3 %, sweeps/r02_bulk_items_per_sm.txt)
 _PAIR_MAX_ELEMS = 8192       # k_panel_pair (two small panels per CTA): panel size cap
 _RING_MIN_BYTES = 256 << 20  # bulk phases this large stream through k_panel_ring (measured: C4 +5 %, C2 -8 %)
 _PAIR_BULK_MAX_BYTES = 32 << 20    # small operators: bulk phases paired like the tier phases
@@ -731,7 +732,9 @@ class PanelPlan:
         phases get one item per panel (split only past the row cap: they are
         latency-bound, and a split panel costs a second pass over L2 for its
         reduction); bulk phases are cut into items of <= _ITEM_ELEMS
-        elements with >= ~4 items per SM per phase.  A panel split over
+        elements, about _BULK_ITEMS_PER_SM per SM per phase (fewer, larger
+        items: fewer split-panel reductions; the concurrent phases fill
+        the SMs).  A panel split over
         several items writes partial sums to scratch and its last item adds
         them in item order."""
         a_off, K, T, rows, out_off, accumulate = panels
@@ -749,7 +752,7 @@ class PanelPlan:
         if transform or small_bulk:
             target = 1 << 40
         else:
-            target = max(256, min(_ITEM_ELEMS, elems // (148 * 4) + 1))
+            target = max(256, min(_ITEM_ELEMS, elems // (148 * _BULK_ITEMS_PER_SM) + 1))
         rpi = np.minimum(_ITEM_MAX_ROWS, np.maximum(1, -(-target // np.maximum(T, 1))))  # rows/item
         # at most 8 items per panel: the last item of a split panel sums the
         # partials serially, so deep splits of small phases cost latency

@@ -260,7 +260,7 @@ def run_reference(args):
 def _traffic(kernel):
     """dram__bytes_read.sum + dram__bytes_write.sum per launch of the
     roofline kernel, from the committed ncu --set full summary
-    (profiles/traffic.json, written by scripts/ncu_traffic.py)."""
+    (profiles/traffic.json, written by scripts/ncu_summary.py)."""
     path = os.path.join(ROOT, "profiles", "traffic.json")
     try:
         return json.load(open(path)).get(kernel)

@@ -213,7 +213,7 @@ _ITEM_ELEMS = 65536          # <= 512 KB of matrix data per bulk work item (rows
 _ITEM_MAX_ROWS = 1024        # PAN_MAX_ROWS in csrc/h2mv.cu
 _BULK_ITEMS_PER_SM = 1       # bulk items per SM per phase (4 -> 1: C2 product -3 %, sweeps/r02_bulk_items_per_sm.txt)
 _PAIR_MAX_ELEMS = 8192       # k_panel_pair (two small panels per CTA): panel size cap
-_RING_MIN_BYTES = 256 << 20  # bulk phases this large stream through k_panel_ring (measured: C4 +5 %, C2 -8 %)
+_RING_MIN_BYTES = 16 << 30   # bulk phases this large stream through k_panel_ring (with one bulk item per SM: L7 -2.3 %, L8 -0.8 % without it, L9 +0.6 %; sweeps/r02_ring_threshold.txt)
 _PAIR_BULK_MAX_BYTES = 32 << 20    # small operators: bulk phases paired like the tier phases
 _SMALL_OPERATOR_BYTES = 128 << 20
 _MERGE_MIN_BYTES = 1 << 30   # coupling row heights with the same producer / consumer merge into one launch

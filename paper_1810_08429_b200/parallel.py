@@ -10,8 +10,9 @@ contiguous range of tree-ordered rows.
   row and column bases of its own subtree.  Every basis root sits at tree
   depth >= 4 >= k, so no node straddles shards.
 * Coupling entries on rank g need the column pivots of remote clusters
-  sigma.  One ``all_gather_object`` of the per-rank (node, rank, pivots)
-  lists, a few MB, gives every rank the global column pivot table.
+  sigma.  Tensor all-gathers of the per-rank (node, rank, pivots) arrays
+  (:func:`_all_gather_arrays`: lengths, then the arrays padded to the
+  longest; a few MB) give every rank the global column pivot table.
 * Matvec:
   1. all-gather the owned slice of x (tree order) -> full x_t;
   2. forward transform of the own column subtree into the own slot of a

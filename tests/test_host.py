@@ -130,6 +130,33 @@ def test_native_block_tree_equals_array_builder(level, basis, eta):
         assert np.array_equal(getattr(a, k), getattr(b, k)), k
 
 
+@pytest.mark.parametrize("n,leaf", [(2048, 16), (8194, 16), (1000, 7), (5, 16), (131072, 16)])
+def test_tree_topology_matches_the_host_builder(n, leaf):
+    """The device cluster tree lays out every depth from the dof count and
+    leaf size alone (clustering._tree_topology); the shape must equal the
+    host builder's on any point set of that size."""
+    rng = np.random.default_rng(n)
+    pts = rng.standard_normal((n, 3))
+
+    class _Pts:                       # minimal support data: points as zero-size boxes
+        pass
+    start, stop, left, right, parent, depth, depths = clustering._tree_topology(n, leaf)
+    orig = clustering._support_data
+    clustering._support_data = lambda mesh, kind: (pts, pts, pts)
+    try:
+        flat = clustering.build_cluster_tree(_Pts(), "constant", leaf).flat
+    finally:
+        clustering._support_data = orig
+    for k, v in (("start", start), ("stop", stop), ("left", left), ("right", right), ("parent", parent),
+                 ("depth", depth)):
+        assert np.array_equal(getattr(flat, k), v), k
+    front = np.concatenate([ids for ids, _ in depths])
+    assert np.array_equal(np.sort(front), np.arange(len(start)))      # every node in one frontier
+    for ids, split in depths:
+        assert np.all(np.diff(start[ids]) > 0)                          # start order
+        assert np.array_equal(split, (stop[ids] - start[ids]) > leaf)
+
+
 def test_block_tree_tiles_the_matrix(sphere3):
     tree = clustering.build_cluster_tree(sphere3, "constant", 16)
     bt = clustering.build_block_tree(tree, eta=1.0)

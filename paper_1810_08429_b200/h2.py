@@ -221,7 +221,8 @@ _MERGE_MIN_BYTES = 1 << 30   # coupling row heights with the same producer / con
 
 class _Phase:
     __slots__ = ("name", "height", "items", "xidx", "red", "arrivals", "nitems", "nred", "A0", "A1",
-                 "in0", "in1", "out", "scratch", "bytes", "in_elems", "out_elems", "pair", "ring", "acc")
+                 "in0", "in1", "out", "scratch", "bytes", "in_elems", "out_elems", "pair", "ring", "acc",
+                 "_h_items", "_h_xidx", "_h_red", "_n_arrivals", "_n_scratch")   # staged tables (_flush_tables)
 
 
 class _Node:
@@ -294,6 +295,7 @@ class PanelPlan:
         self._obuf = torch.zeros(self.n_out + max(cs.coef_size, 1), **f64)
         self.yt, self.xhat = self._obuf[:self.n_out], self._obuf[self.n_out:]
         self._keep = []
+        self._t64, self._t32, self._staged = [], [], []      # tables of the phases (_flush_tables)
         self.tiers_pending = False
         ny = max(rs.coef_size, 1)
         # y-hat | y-hat from the tiers above | leaf-basis part of y (summed
@@ -335,6 +337,7 @@ class PanelPlan:
         self._fwd, self._cpl, self._bwd, self._near, self._leafparts = fwd, cpl, bwd, near, parts
         self.phases = [P for P in [near, self._near_remote] + fwd + [c for c, _, _ in cpl + self._cpl_remote]
                        + [b for b, _ in bwd] + [p for p, _ in parts] if P is not None and P.nitems > 0]
+        self._flush_tables()
         # the chain gets the highest stream priority so its CTAs are
         # scheduled ahead of the queued bulk (coupling buckets, near field)
         self.streams = {"chain": torch.cuda.Stream(device=dev, priority=-8)}
@@ -793,27 +796,86 @@ class PanelPlan:
             items = items[np.argsort(-(items[:, 3] * items[:, 4]), kind="stable")]
         # large bulk phases stream through the TMA ring kernel (k_panel_ring)
         P.ring = ring
-        P.items = to_dev(np.ascontiguousarray(items, np.int64), self.dev)
+        # the device tables of every phase go up together (_flush_tables)
+        P._h_items = self._stage(self._t64, items)
         if segs is not None:
             st_, ln_ = np.asarray(segs[0], np.int64), np.asarray(segs[1], np.int64)
-            total = int(ln_.sum())
-            P.xidx = torch.empty(max(total, 1), dtype=torch.int32, device=self.dev)
-            tab = to_dev(np.concatenate([st_, ln_, _offsets_np(ln_)]), self.dev)
-            m = len(st_)
-            with torch.cuda.device(self.dev):
-                _native.call("gc_expand_ranges", m, ptr(tab[:m]), ptr(tab[m:2 * m]), ptr(tab[2 * m:]),
-                             ptr(P.xidx), stream_handle())
+            P._h_xidx = ("ranges", st_, ln_, int(ln_.sum()))
         else:
-            P.xidx = to_dev(xidx, self.dev)
+            P._h_xidx = ("explicit", self._stage(self._t32, xidx))
         P.nitems, P.nred = len(items), int(multi.sum())
-        P.red = to_dev(np.ascontiguousarray(red, np.int64), self.dev) if P.nred else None
-        P.arrivals = torch.zeros(max(P.nred, 1), dtype=torch.int32, device=self.dev)
+        P._h_red = self._stage(self._t64, red) if P.nred else None
+        P._n_arrivals = max(P.nred, 1)
+        P._n_scratch = max(int((np.where(multi, nit * T, 0)).sum()), 1)
+        P.items = P.xidx = P.red = P.arrivals = P.scratch = None
+        self._staged.append(P)
         P.A0, P.A1, P.in0, P.in1, P.out = A0, A1, in0, in1, out
         P.scratch = torch.zeros(max(int((np.where(multi, nit * T, 0)).sum()), 1),
                                 dtype=torch.float64, device=self.dev)
         P.bytes = 8 * elems
         P.in_elems, P.out_elems = int(K.sum()), int(T.sum())
         return P
+
+    @staticmethod
+    def _stage(parts, a):
+        """Queue a host table for the plan's single upload; returns its
+        (element offset, length), segments 16-byte aligned."""
+        a = np.ascontiguousarray(a).ravel()
+        off = sum(len(x) for x in parts)
+        parts.append(a)
+        pad = (-len(a)) % 4
+        if pad:
+            parts.append(np.zeros(pad, a.dtype))
+        return off, len(a)
+
+    def _flush_tables(self):
+        """One upload per element type for the tables of every phase, one
+        launch expanding all index ranges, one zeroed buffer each for the
+        split-panel arrivals and partial sums."""
+        staged, self._staged = self._staged, []
+        if not staged:
+            return
+        d64 = to_dev(np.concatenate(self._t64) if self._t64 else np.zeros(4, np.int64), self.dev)
+        d32 = to_dev(np.concatenate(self._t32) if self._t32 else np.zeros(4, np.int32), self.dev)
+        self._t64, self._t32 = [], []
+        rng = [P for P in staged if P._h_xidx[0] == "ranges"]
+        sizes = [P._h_xidx[3] + (-P._h_xidx[3]) % 4 for P in rng]
+        xbuf = torch.empty(max(sum(sizes), 4), dtype=torch.int32, device=self.dev)
+        arr = torch.zeros(sum(P._n_arrivals + (-P._n_arrivals) % 4 for P in staged), dtype=torch.int32,
+                          device=self.dev)
+        scr = torch.zeros(sum(P._n_scratch + (-P._n_scratch) % 4 for P in staged), dtype=torch.float64,
+                          device=self.dev)
+        self._keep.extend([d64, d32, xbuf, arr, scr])
+        base = 0
+        starts, lens, outs = [], [], []
+        for P, sz in zip(rng, sizes):
+            _, st_, ln_, total = P._h_xidx
+            P.xidx = xbuf[base:base + max(total, 1)]
+            starts.append(st_)
+            lens.append(ln_)
+            outs.append(base + _offsets_np(ln_))
+            base += sz
+        if rng and sum(len(x) for x in starts):
+            tab = to_dev(np.concatenate(starts + lens + outs), self.dev)
+            m = sum(len(x) for x in starts)
+            with torch.cuda.device(self.dev):
+                _native.call("gc_expand_ranges", m, ptr(tab[:m]), ptr(tab[m:2 * m]), ptr(tab[2 * m:]),
+                             ptr(xbuf), stream_handle())
+        oa = os_ = 0
+        for P in staged:
+            o, n = P._h_items
+            P.items = d64[o:o + n]
+            if P._h_xidx[0] == "explicit":
+                o, n = P._h_xidx[1]
+                P.xidx = d32[o:o + n]
+            if P._h_red is not None:
+                o, n = P._h_red
+                P.red = d64[o:o + n]
+            P.arrivals = arr[oa:oa + P._n_arrivals]
+            P.scratch = scr[os_:os_ + P._n_scratch]
+            oa += P._n_arrivals + (-P._n_arrivals) % 4
+            os_ += P._n_scratch + (-P._n_scratch) % 4
+            del P._h_items, P._h_xidx, P._h_red
 
     def _launch(self, P, stream, chain=False, priority=0):
         mode = (1 if chain else 0) | (16 if P.pair else 0) | (32 if P.ring else 0)

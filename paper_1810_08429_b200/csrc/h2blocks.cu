@@ -9,7 +9,7 @@
 #include <cub/device/device_radix_sort.cuh>
 #include <cub/device/device_scan.cuh>
 #include <cub/device/device_select.cuh>
-#include <cub/iterator/counting_input_iterator.cuh>
+#include <thrust/iterator/counting_iterator.h>
 
 #include "common.cuh"
 
@@ -158,7 +158,7 @@ namespace {
 
 size_t blk_temp(int64_t nl) {
     size_t t1 = 0, t2 = 0, t3 = 0;
-    cub::CountingInputIterator<int64_t> it(0);
+    thrust::counting_iterator<int64_t> it(0);
     cub::DeviceSelect::Flagged(nullptr, t1, it, (const char*)nullptr, (int64_t*)nullptr, (int64_t*)nullptr, (int)nl);
     cub::DeviceRadixSort::SortPairs(nullptr, t2, (const int64_t*)nullptr, (int64_t*)nullptr, (const int64_t*)nullptr,
                                     (int64_t*)nullptr, (int)nl);
@@ -214,7 +214,7 @@ int gc_h2_blocks(int64_t nl, const int64_t* leaf_ids, const int64_t* node_row, c
     k_blk_flag<<<(unsigned)grid, 256, 0, st>>>(nl, in, flag);
     GC_CHECK_LAUNCH("k_blk_flag");
     size_t tb = (size_t)temp_bytes;
-    cub::CountingInputIterator<int64_t> it(0);
+    thrust::counting_iterator<int64_t> it(0);
     cudaError_t e = cub::DeviceSelect::Flagged(temp, tb, it, flag, sel, count, (int)nl, st);
     if (e != cudaSuccess) return cuda_status(e, "gc_h2_blocks select");
     k_blk_fill<<<(unsigned)grid, 256, 0, st>>>(nl, in, count, sel, sentinel, row, col, nr, nc, key, size, idx,

@@ -212,7 +212,7 @@ def _stream_ptr(stream=None):
 _ITEM_ELEMS = 65536          # <= 512 KB of matrix data per bulk work item (rows capped at 1024)
 _ITEM_MAX_ROWS = 1024        # PAN_MAX_ROWS in csrc/h2mv.cu
 _BULK_ITEMS_PER_SM = 1       # bulk items per SM per phase (4 -> 1: C2 product -3 %, sweeps/r02_bulk_items_per_sm.txt)
-_PAIR_MAX_ELEMS = 8192       # k_panel_pair (two small panels per CTA): panel size cap
+_PAIR_MAX_ELEMS = 12288      # k_panel_pair (two small panels per CTA): panel size cap (8192 -> 12288: cube L7 -4.6 %, L8 -1.4 %; sweeps/r02_pair_max_elems.txt)
 _RING_MIN_BYTES = 16 << 30   # bulk phases this large stream through k_panel_ring (with one bulk item per SM: L7 -2.3 %, L8 -0.8 % without it, L9 +0.6 %; sweeps/r02_ring_threshold.txt)
 _PAIR_BULK_MAX_BYTES = 32 << 20    # small operators: bulk phases paired like the tier phases
 _SMALL_OPERATOR_BYTES = 128 << 20

@@ -1,5 +1,5 @@
 """Product time for values of one h2 module constant (plan-construction
-parameters under study).  Usage: python scripts/modvar.py NAME v1,v2,... level:eps ..."""
+parameters under study).  Usage: python scripts/modvar.py NAME v1,v2,... level:eps ... (cubeL:eps for the cube)"""
 import ast
 import os
 import sys
@@ -22,8 +22,9 @@ def conv(v):
 vals = [conv(v) for v in vals]
 for spec in sys.argv[3:]:
     L, eps = spec.split(":")
-    L, eps = int(L), float(eps)
-    mesh = geometry.build_sphere_mesh(L)
+    cube = L.startswith("cube")
+    L, eps = int(L[4:] if cube else L), float(eps)
+    mesh = geometry.build_cube_mesh(L) if cube else geometry.build_sphere_mesh(L)
     hm, _, _ = cli.build_h2_operator(mesh, cli.default_config(eps=eps))
     nbytes = h2.storage_report(hm)["total"] + 16 * mesh.nt
     x = torch.randn(mesh.nt, dtype=torch.float64, device="cuda")

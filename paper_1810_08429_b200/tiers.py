@@ -35,6 +35,8 @@ from . import _native
 from .device import padded_empty, ptr, stream_handle, to_dev
 
 _BW = 6.5e12             # B/s, the measured HBM copy bandwidth (MEASURED_PEAKS.json)
+_LATENCY_S = 5e-6        # hand-off between dependent tier launches
+_CTA_BPS = 20e9          # one CTA's streaming rate (B/s)
 
 
 def live_nodes(store):
@@ -90,7 +92,7 @@ def tier_elems(store, flat, lo, hi):
     return int((wmap[f] * store.rank[u]).sum())
 
 
-def choose_tiers(store, flat, bounds=None, latency_s=5e-6, cta_bps=20e9, max_rows=1024):
+def choose_tiers(store, flat, bounds=None, latency_s=None, cta_bps=None, max_rows=1024):
     """Tier upper boundaries (ascending heights) for one transform
     direction of one store: minimise, summed over tiers, streamed bytes /
     HBM bandwidth + the largest work item / one CTA's streaming rate
@@ -103,7 +105,8 @@ def choose_tiers(store, flat, bounds=None, latency_s=5e-6, cta_bps=20e9, max_row
     top = int(flat.height[live].max())
     if bounds is not None:
         return sorted({min(int(v), top) for v in bounds} | {top})
-    lat, cta_bw = latency_s, cta_bps
+    lat = _LATENCY_S if latency_s is None else latency_s
+    cta_bw = _CTA_BPS if cta_bps is None else cta_bps
     # elems(lo, hi) for every hi from ONE walk per lo: the pairs of tier
     # (lo, hi] are those of (lo, top] whose u lies at height <= hi.  A tier
     # launch costs its bytes at full bandwidth plus its largest work item

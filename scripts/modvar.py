@@ -7,7 +7,7 @@ import sys
 import torch
 
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
-from paper_1810_08429_b200 import cli, geometry, h2  # noqa: E402
+from paper_1810_08429_b200 import cli, geometry, h2, tiers  # noqa: E402
 
 name, vals = sys.argv[1], sys.argv[2].split(",")
 
@@ -29,13 +29,14 @@ for spec in sys.argv[3:]:
     nbytes = h2.storage_report(hm)["total"] + 16 * mesh.nt
     x = torch.randn(mesh.nt, dtype=torch.float64, device="cuda")
     plans, res, ref = [], [[] for _ in vals], None
-    old = getattr(h2, name)
+    mod = next(m for m in (h2, tiers) if hasattr(m, name))
+    old = getattr(mod, name)
     for v in vals:
-        setattr(h2, name, v)
+        setattr(mod, name, v)
         p = h2.PanelPlan(hm)
         p.capture()
         plans.append(p)
-    setattr(h2, name, old)
+    setattr(mod, name, old)
     reps = 50 if L <= 7 else 10
     for rnd in range(3):
         for i, p in enumerate(plans):

@@ -1022,7 +1022,7 @@ class PanelPlan:
         cache) that is returned without a copy."""
         with self.lock:
             g = self.graph
-            if isinstance(g, _NativeGraph) and torch.cuda.current_device() == self._dev_index:
+            if isinstance(g, _NativeGraph) and torch._C._cuda_getDevice() == self._dev_index:
                 # the e2e hot path: staging copy, graph and sync in one C call
                 if self._pin_x_np is None:
                     self._pin_x = torch.empty(self.n_in, dtype=torch.float64, pin_memory=True)
@@ -1030,8 +1030,9 @@ class PanelPlan:
                 x = np.ascontiguousarray(x, dtype=np.float64)
                 y = torch.empty(self.n_out, dtype=torch.float64, pin_memory=True)
                 px, py = self._pin_x.data_ptr(), y.data_ptr()
+                # the raw current stream (the torch.cuda.Stream wrapper costs ~2 us per call)
                 _native.check(g._run_host(g.handle, x.ctypes.data, px, self.n_in, py,
-                                          torch.cuda.current_stream().cuda_stream))
+                                          torch._C._cuda_getCurrentRawStream(self._dev_index)))
                 g._x, g._y = px, py
                 return y.numpy()
             with torch.cuda.device(self.dev):

@@ -30,6 +30,14 @@ import numpy as np
 ROOT = os.path.dirname(os.path.abspath(__file__))
 sys.path.insert(0, ROOT)
 
+# PyTorch's expandable-segment allocator (set before torch initialises
+# CUDA): after the warm-up build a repeated assembly is served from the
+# reserved segments.  With the default allocator, block splitting now and
+# then forces a fresh cudaMalloc during the timed build, and on these boxes
+# about 5 % of fresh cudaMallocs stall for 10-100 ms (scripts/malloc_probe.py,
+# profiles/sweeps/r02_allocator.txt).  The matvec is unaffected.
+os.environ.setdefault("PYTORCH_CUDA_ALLOC_CONF", "expandable_segments:True")
+
 LEVEL_DEFAULT, EPS_DEFAULT = 6, 1e-6
 METRIC = "H² assembly time (s) and H² matvec GB/s at 1/2/4/8 B200 vs host CPU ref"
 
@@ -62,7 +70,8 @@ def workload(args):
                                                    args.eps, args.steps),
             "triangles": 8 * 4 ** args.level, "eta": 1.0, "m": 3, "delta_factor": 0.5,
             "eps": args.eps, "leaf_size": 16, "q_reg": 3, "q_sing": 5,
-            "l2": "H2 data > 126 MB L2 at level >= 6: inputs larger than L2, no flush"}
+            "l2": "H2 data > 126 MB L2 at level >= 6: inputs larger than L2, no flush",
+            "allocator": os.environ.get("PYTORCH_CUDA_ALLOC_CONF", "default")}
 
 
 # --------------------------------------------------------------------------

@@ -982,3 +982,59 @@ def test_device_charts_bit_identical_to_host(kind, level):
         np.minimum(lo, ctrl[:, k], out=lo)
         np.maximum(hi, ctrl[:, k], out=hi)
     assert sup[:, :3].tobytes() == lo.tobytes() and sup[:, 3:6].tobytes() == hi.tobytes()
+
+
+def _expected_block_tables(bt, rf, cf, rs, cs, rng):
+    """numpy restatement of build_h2's block loop (gca.py:296-310): leaves in
+    DFS order, admissible -> coupling (ranks), inadmissible -> near field
+    (cluster sizes), storage grouped stably by block row (a shard: local
+    columns first inside each row)."""
+    fb = bt.flat
+    ids = fb.leaf_ids
+    st, lr, lc = fb.state[ids], fb.row[ids], fb.col[ids]
+    if rng is not None:
+        k = (rf.start[lr] >= rng[0]) & (rf.stop[lr] <= rng[1])
+        st, lr, lc = st[k], lr[k], lc[k]
+    adm = st == 0
+    out = []
+    for rows, cols, nr, nc in ((lr[adm], lc[adm], rs.rank[lr[adm]], cs.rank[lc[adm]]),
+                               (lr[~adm], lc[~adm], (rf.stop - rf.start)[lr[~adm]],
+                                (cf.stop - cf.start)[lc[~adm]])):
+        key = rows if rng is None else 2 * rows + ~((cf.start[cols] >= rng[0]) & (cf.stop[cols] <= rng[1]))
+        order = np.argsort(key, kind="stable")
+        sz = nr * nc
+        off = np.empty(len(key), np.int64)
+        off[order] = np.cumsum(sz[order]) - sz[order]
+        out.append((rows, cols, nr, nc, off, order))
+    return out
+
+
+@pytest.mark.parametrize("level,basis,disc", [(4, "constant", "galerkin"), (3, "linear", "collocation")])
+def test_device_block_tables_match_numpy(level, basis, disc):
+    """gc_h2_blocks (csrc/h2blocks.cu): the coupling / near-field tables and
+    storage offsets equal the numpy restatement, unsharded and for three
+    block-row shards; the assembly descriptors point at the same pivots /
+    clusters."""
+    mesh = geometry.build_sphere_mesh(level)
+    cfg = cli.default_config(eps=1e-6, basis=basis, disc=disc)
+    hm, tree, bt = cli.build_h2_operator(mesh, cfg)
+    rf = cf = tree.flat
+    rs, cs = hm.row_basis.store, hm.col_basis.store
+    dev = torch.device("cuda", 0)
+    n = int(rf.stop[0])
+    for rng in [None, (0, n // 4), (n // 4, n // 2), (n // 2, n)]:
+        tabs = gca._device_block_tables(bt, rf, cf, rs, cs, rng, dev)
+        got = tabs.host()
+        exp = _expected_block_tables(bt, rf, cf, rs, cs, rng)
+        for g, e in zip(got, exp):
+            for a, b in zip(g, e):
+                assert np.array_equal(a, b), rng
+        (cr, cc, c_nr, c_nc, c_off, _), (nr_r, nc_r, n_nr, n_nc, n_off, _) = exp
+        keep = (c_nr > 0) & (c_nc > 0)
+        cd = tabs.c_desc.cpu().numpy()
+        assert np.array_equal(cd, np.stack([rs.piv_off[cr], c_nr, cs.piv_off[cc], c_nc, c_off], 1)[keep])
+        nd = tabs.n_desc.cpu().numpy()
+        assert np.array_equal(nd, np.stack([rf.start[nr_r], n_nr, cf.start[nc_r], n_nc, n_off], 1))
+        c_shape, n_shape = tabs.shapes
+        assert c_shape[0] == int(keep.sum()) and c_shape[3] == int((c_nr * c_nc).sum())
+        assert n_shape[0] == len(nr_r) and n_shape[3] == int((n_nr * n_nc).sum())

@@ -562,10 +562,12 @@ def scaling_config(args, torch):
     cfg = cli.default_config(level=args.scale_level, eps=args.scale_eps)
     # the first build at this size (cold: fresh device and pinned-host
     # allocations) doubles as the warm-up; the timed build starts from a
-    # fresh mesh object as the C2 one does
+    # fresh mesh object as the C2 one does (mesh generation is outside both
+    # timed builds, as in the reference arm)
+    mesh = geometry.build_sphere_mesh(args.scale_level)
     torch.cuda.synchronize()
     t0 = time.perf_counter()
-    hm, _, _ = cli.build_h2_operator(geometry.build_sphere_mesh(args.scale_level), cfg)
+    hm, _, _ = cli.build_h2_operator(mesh, cfg)
     h2.plan(hm)
     torch.cuda.synchronize()
     asm_cold = time.perf_counter() - t0

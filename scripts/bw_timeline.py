@@ -27,7 +27,7 @@ for i, n in enumerate(p.nodes):
     P = n.phase
     if P is None:
         continue
-    it = P.items.cpu().numpy()
+    it = P.items.cpu().numpy().reshape(-1, 8)
     b = 8 * it[:, 3] * it[:, 4] + 12 * it[:, 4] + 8 * it[:, 3]
     ncta = (P.nitems + 1) // 2 if P.pair else P.nitems
     if P.pair:

@@ -746,12 +746,14 @@ def _device_block_tables(btree, rf, cf, rstore, cstore, row_range, dev):
     fb = btree.flat
     a, b = np.searchsorted(fb.leaf_key, [fb.key_lo[btree._id], fb.key_hi[btree._id]], side="left")
     nl = int(b - a)
+    # the device block tree's node arrays (clustering._build_block_tree_device)
+    # serve this one call; later calls upload the host arrays
     dv = getattr(fb, "_dev", None)
+    fb._dev = None
     if dv is None or dv[0].device != dev:
         nn = len(fb.row)
         ints = to_dev(np.concatenate([fb.row, fb.col, fb.leaf_ids]).astype(np.int64), dev)
         dv = (ints[:nn], ints[nn:2 * nn], to_dev(fb.state.astype(np.int8), dev), ints[2 * nn:])
-        fb._dev = dv
     node_row, node_col, node_state, leaf_ids = dv
     same = cf is rf
     parts = [rf.start, rf.stop, rstore.rank, rstore.piv_off]

@@ -16,7 +16,7 @@ kw = {}
 for a in sys.argv[3:]:
     k, v = a.split("=")
     kw[k] = int(v) if v.lstrip("-").isdigit() else v
-mesh = geometry.build_sphere_mesh(L)
+mesh = (geometry.build_cube_mesh if os.environ.get("GC_GEO") == "cube" else geometry.build_sphere_mesh)(L)
 hm, _, _ = cli.build_h2_operator(mesh, cli.default_config(eps=eps))
 p = h2.PanelPlan(hm, **kw)
 x = torch.randn(mesh.nt, dtype=torch.float64, device="cuda")

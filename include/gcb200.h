@@ -474,6 +474,13 @@ int gc_tree_sort_bytes(int64_t nitems, int64_t nseg, int64_t* bytes);
 /* Split axes: axis[i] = argmax of the extents of box row rows[i] (first
  * maximum; clustering.py:154 np.argmax(box.upper - box.lower)). */
 int gc_tree_axis(int64_t k, const int64_t* rows, const double* box, int64_t* axis, void* stream);
+/* gc_tree_split for a depth whose segments are all short: one stable
+ * segmented sort over the offsets (required here) instead of two radix
+ * sorts; identical result.  gc_tree_sort_bytes(nitems, nseg) covers both. */
+int gc_tree_split_small(int64_t nseg, const int64_t* seg_start, const int64_t* seg_len, const int64_t* seg_head,
+                        const int64_t* seg_axis, const int32_t* offsets, int64_t nitems, const double* pack_old,
+                        double* pack_new, const int64_t* perm_old, int64_t* perm_new, double* keys, int32_t* vals,
+                        void* temp, int64_t temp_bytes, void* stream);
 int gc_tree_split(int64_t nseg, const int64_t* seg_start, const int64_t* seg_len, const int64_t* seg_head,
                   const int64_t* seg_axis, const int32_t* offsets, int64_t nitems, const double* pack_old,
                   double* pack_new, const int64_t* perm_old, int64_t* perm_new, double* keys, int32_t* vals,

@@ -97,6 +97,7 @@ _SIGNATURES = {
     "gc_tree_sort_bytes": [c_i64, c_i64, ctypes.POINTER(c_i64)],
     "gc_tree_axis": [c_i64, c_p, c_p, c_p, c_p],
     "gc_tree_split": [c_i64, c_p, c_p, c_p, c_p, c_p, c_i64, c_p, c_p, c_p, c_p, c_p, c_p, c_p, c_i64, c_p],
+    "gc_tree_split_small": [c_i64, c_p, c_p, c_p, c_p, c_p, c_i64, c_p, c_p, c_p, c_p, c_p, c_p, c_p, c_i64, c_p],
     "gc_lin_pairs_blocks": [ctypes.POINTER(GcGeom), c_p, c_p, c_i64, c_i64, c_p, c_p, c_p, c_p, c_p,
                             ctypes.POINTER(GcQueue), c_p, c_p],
     "gc_col_pairs_blocks": [ctypes.POINTER(GcGeom), c_p, c_p, c_p, c_i64, c_p, c_p, c_i64, c_i64, c_p, c_p, c_p,

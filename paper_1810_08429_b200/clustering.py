@@ -307,6 +307,9 @@ def build_cluster_tree(mesh, basis_kind="constant", leaf_size=32, device=None):
     return flat.node(0)
 
 
+_TREE_SMALL_SEGMENT = 4096      # depths whose segments are all this short sort per segment
+
+
 def _tree_topology(n, leaf_size):
     """The shape of the cluster tree of n dofs: it depends only on n and the
     leaf size (every split halves a segment, ``clustering.py:150-160``).
@@ -385,7 +388,7 @@ def _build_cluster_tree_device(mesh, basis_kind, leaf_size, device):
         k = len(ids_s)
         rows = f_off[di] + np.flatnonzero(split)
         parts += [rows, s_s, seg_len, heads, offs]
-        plan.append((di, k, nitems, o))
+        plan.append((di, k, nitems, o, int(seg_len.max()) <= _TREE_SMALL_SEGMENT))
         o += 4 * k + len(offs)
     f64 = dict(dtype=torch.float64, device=device)
     pack = [charts["support"].clone() if charts is not None else
@@ -398,27 +401,30 @@ def _build_cluster_tree_device(mesh, basis_kind, leaf_size, device):
         st = stream_handle()
         tab = torch.from_numpy(np.concatenate(parts)).to(device)
         box = torch.empty((len(front), 6), **f64)
-        axis = torch.empty(max([k for _, k, _, _ in plan] + [1]), dtype=torch.int64, device=device)
-        tb = _native.ctypes.c_int64(0)
-        _native.call("gc_tree_sort_bytes", n, 1, _native.ctypes.byref(tb))
-        temp = torch.empty(max(tb.value, 1), dtype=torch.uint8, device=device)
+        axis = torch.empty(max([k for _, k, _, _, _ in plan] + [1]), dtype=torch.int64, device=device)
+        tb, need = _native.ctypes.c_int64(0), 1
+        for _, k, nitems, _, _ in plan:
+            _native.call("gc_tree_sort_bytes", nitems, k, _native.ctypes.byref(tb))
+            need = max(need, tb.value)
+        temp = torch.empty(need, dtype=torch.uint8, device=device)
         T, nf = tab.data_ptr(), len(front)
         cur = 0
-        steps = {di: (k, nitems, o) for di, k, nitems, o in plan}
+        steps = {di: (k, nitems, o, small) for di, k, nitems, o, small in plan}
         for di in range(len(depths)):
             f0, f1 = int(f_off[di]), int(f_off[di + 1])
             _native.call("gc_tree_boxes", f1 - f0, T + 8 * f0, T + 8 * (nf + f0), ptr(pack[cur]),
                          box.data_ptr() + 48 * f0, st)
             if di not in steps:
                 break
-            k, nitems, o = steps[di]
+            k, nitems, o, small = steps[di]
             _native.call("gc_tree_axis", k, T + 8 * o, ptr(box), ptr(axis), st)
             nxt = 1 - cur
             pack[nxt].copy_(pack[cur])
             perm[nxt].copy_(perm[cur])
-            _native.call("gc_tree_split", k, T + 8 * (o + k), T + 8 * (o + 2 * k), T + 8 * (o + 3 * k),
+            # short segments: one segmented sort; long ones: two radix sorts
+            _native.call("gc_tree_split_small" if small else "gc_tree_split", k, T + 8 * (o + k), T + 8 * (o + 2 * k), T + 8 * (o + 3 * k),
                          ptr(axis), T + 8 * (o + 4 * k), nitems, ptr(pack[cur]), ptr(pack[nxt]), ptr(perm[cur]),
-                         ptr(perm[nxt]), ptr(keys), ptr(vals), ptr(temp), tb.value, st)
+                         ptr(perm[nxt]), ptr(keys), ptr(vals), ptr(temp), need, st)
             cur = nxt
         bh = box.cpu().numpy()
         perm_h = perm[cur].cpu().numpy()

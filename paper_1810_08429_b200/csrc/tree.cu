@@ -18,6 +18,7 @@
 // host lays out every depth's frontier up front and the depths run back to
 // back on the stream; boxes and the permutation come back once.
 #include <cub/device/device_radix_sort.cuh>
+#include <cub/device/device_segmented_sort.cuh>
 
 #include "common.cuh"
 
@@ -140,15 +141,20 @@ extern "C" int gc_tree_boxes(int64_t nseg, const int64_t* start, const int64_t* 
 
 // CUB temp-storage bytes of a split step with nitems dofs in nseg segments
 extern "C" int gc_tree_sort_bytes(int64_t nitems, int64_t nseg, int64_t* bytes) {
-    (void)nseg;
-    size_t t1 = 0, t2 = 0;
+    size_t t1 = 0, t2 = 0, t3 = 0;
     cudaError_t e = cub::DeviceRadixSort::SortPairs(nullptr, t1, (const double*)nullptr, (double*)nullptr,
                                                     (const int32_t*)nullptr, (int32_t*)nullptr, (int)nitems);
     if (e == cudaSuccess)
         e = cub::DeviceRadixSort::SortPairs(nullptr, t2, (const int32_t*)nullptr, (int32_t*)nullptr,
                                             (const int32_t*)nullptr, (int32_t*)nullptr, (int)nitems);
+    if (e == cudaSuccess)
+        e = cub::DeviceSegmentedSort::StableSortPairs(nullptr, t3, (const double*)nullptr, (double*)nullptr,
+                                                      (const int32_t*)nullptr, (int32_t*)nullptr, (int)nitems,
+                                                      (int)(nseg > 0 ? nseg : 1), (const int32_t*)nullptr,
+                                                      (const int32_t*)nullptr);
     if (e != cudaSuccess) return cuda_status(e, "gc_tree_sort_bytes");
-    *bytes = (int64_t)(t1 > t2 ? t1 : t2);
+    size_t t = t1 > t2 ? t1 : t2;
+    *bytes = (int64_t)(t > t3 ? t : t3);
     return GC_OK;
 }
 
@@ -194,6 +200,39 @@ extern "C" int gc_tree_split(int64_t nseg, const int64_t* seg_start, const int64
     if (e != cudaSuccess) return cuda_status(e, "gc_tree_split sort (segment)");
     count_launch(2);
     k_seg_permute<<<(unsigned)pgrid, 256, 0, st>>>(nitems, vals, src_final, perm_old, perm_new, pack_old, pack_new);
+    GC_CHECK_LAUNCH("k_seg_permute");
+    return GC_OK;
+}
+
+// gc_tree_split for depths whose segments are all short: one stable
+// segmented sort (CUB picks warp / block sorts per segment size) instead of
+// the two full-width radix sorts; the same order (key ascending, ties in
+// row order) and the same permutation.
+extern "C" int gc_tree_split_small(int64_t nseg, const int64_t* seg_start, const int64_t* seg_len,
+                                   const int64_t* seg_head, const int64_t* seg_axis, const int32_t* offsets,
+                                   int64_t nitems, const double* pack_old, double* pack_new,
+                                   const int64_t* perm_old, int64_t* perm_new, double* keys, int32_t* vals,
+                                   void* temp, int64_t temp_bytes, void* stream) {
+    if (nseg <= 0 || nitems <= 0) return GC_OK;
+    if (nitems > 0x7fffffffLL) { set_error(GC_ERR_CONFIG, "gc_tree_split_small: too many dofs"); return GC_ERR_CONFIG; }
+    if (!keys || !vals || !temp || !offsets) {
+        set_error(GC_ERR_CONFIG, "gc_tree_split_small: scratch missing");
+        return GC_ERR_CONFIG;
+    }
+    cudaStream_t st = (cudaStream_t)stream;
+    const int64_t grid = nseg < 148 * 16 ? nseg : 148 * 16;
+    k_seg_keys<<<(unsigned)grid, TREE_THREADS, 0, st>>>(nseg, seg_start, seg_len, seg_head, seg_axis, pack_old,
+                                                        keys, vals);
+    GC_CHECK_LAUNCH("k_seg_keys");
+    size_t tb = (size_t)temp_bytes;
+    cudaError_t e = cub::DeviceSegmentedSort::StableSortPairs(temp, tb, keys, keys + nitems, vals, vals + nitems,
+                                                              (int)nitems, (int)nseg, offsets, offsets + 1, st);
+    if (e != cudaSuccess) return cuda_status(e, "gc_tree_split_small sort");
+    count_launch(1);
+    int64_t pgrid = (nitems + 255) / 256;
+    if (pgrid > 148 * 32) pgrid = 148 * 32;
+    k_seg_permute<<<(unsigned)pgrid, 256, 0, st>>>(nitems, vals, vals + nitems, perm_old, perm_new, pack_old,
+                                                  pack_new);
     GC_CHECK_LAUNCH("k_seg_permute");
     return GC_OK;
 }

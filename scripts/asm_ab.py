@@ -10,7 +10,7 @@ import time
 import torch
 
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
-from paper_1810_08429_b200 import cli, device as _device, gca, geometry, h2  # noqa: E402
+from paper_1810_08429_b200 import cli, clustering, device as _device, gca, geometry, h2  # noqa: E402
 
 name, vals = sys.argv[1], [ast.literal_eval(v) for v in sys.argv[2].split(",")]
 L, eps = int(sys.argv[3]), float(sys.argv[4])
@@ -24,7 +24,7 @@ torch.cuda.synchronize()
 res = {v: [] for v in vals}
 for r in range(reps):
     for v in vals:
-        setattr(next(mod for mod in (_device, gca, h2) if hasattr(mod, name)), name, v)
+        setattr(next(mod for mod in (_device, gca, h2, clustering) if hasattr(mod, name)), name, v)
         mesh = geometry.build_sphere_mesh(L)
         torch.cuda.synchronize()
         t0 = time.perf_counter()

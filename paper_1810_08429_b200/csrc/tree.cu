@@ -10,7 +10,8 @@
 //                   row order) - the reference's per-node argsort(kind=
 //                   "stable"); one launch pair over all nodes of the depth
 //                   (CUB's segmented sort falls back to one-block sorts for
-//                   the large top-level segments);
+//                   the large top-level segments); once every segment is
+//                   short, one stable segmented sort (gc_tree_split_small);
 //   * k_seg_permute - applies the order to the permutation and to the
 //                   packed (lo | hi | point) rows.
 //   * k_seg_axis  - the longest box axis of every splitting node.

@@ -175,13 +175,12 @@ int gc_block_tree(const double* r_diam, const double* r_lower, const double* r_u
 int gc_block_tree_fetch(void* handle, int64_t* row, int64_t* col, int8_t* state, int64_t* level,
                         int64_t* key, int64_t* parent);
 
-/* One level of the same block tree built on the device: the frontier pairs
- * fr, fc, fkey, fpar [dev] (m) are decided (gc_block_tree's rounding) and
- * recorded at out_*[base .. base + m) [dev]; their children are written to
- * nr, nc, nk, np [dev] (capacity 4m) in gc_block_tree's order and their
- * number to *count [dev].  Tree arrays [dev] as gc_block_tree.  flags, pos
- * [dev] 4m int32 scratch; temp [dev] of gc_bt_level_bytes(m) bytes. */
-int gc_bt_level_bytes(int64_t m, int64_t* bytes);
+/* The same block tree built on the device one level per gc_bt_level call
+ * (below): the frontier pairs fr, fc, fkey, fpar [dev] are decided
+ * (gc_block_tree's rounding) and recorded at out_*[base ..] [dev]; their
+ * children go to nr, nc, nk, np [dev] in gc_block_tree's order.  Tree
+ * arrays [dev] as gc_block_tree; temp [dev] of gc_bt_level_bytes(cap_f). */
+int gc_bt_level_bytes(int64_t cap_f, int64_t* bytes);
 /* The leaves of a device block tree (n nodes, state / key [dev]) in
  * depth-first order: leaf_ids, leaf_key [dev] (capacity n), *count [dev].
  * Scratch [dev]: ids, ids_sorted, key_sorted (n int64), flag, flag_sorted
@@ -190,14 +189,19 @@ int gc_bt_leaves_bytes(int64_t n, int64_t* bytes);
 int gc_bt_leaves(int64_t n, const int8_t* state, const int64_t* key, int64_t* leaf_ids, int64_t* leaf_key,
                  int64_t* count, int64_t* ids, int64_t* ids_sorted, int64_t* key_sorted, char* flag,
                  char* flag_sorted, void* temp, int64_t temp_bytes, void* stream);
-int gc_bt_level(int64_t m, const int64_t* fr, const int64_t* fc, const int64_t* fkey, const int64_t* fpar,
-                int64_t base, int64_t lev, int32_t digits, const double* r_diam, const double* r_lower,
-                const double* r_upper, const int64_t* r_left, const int64_t* r_right, const double* c_diam,
-                const double* c_lower, const double* c_upper, const int64_t* c_left, const int64_t* c_right,
-                double eta, int32_t norm_mode, int64_t* o_row, int64_t* o_col, int8_t* o_state,
-                int64_t* o_level, int64_t* o_key, int64_t* o_parent, int64_t* nr, int64_t* nc, int64_t* nk,
-                int64_t* np, int64_t* count, int32_t* flags, int32_t* pos, void* temp, int64_t temp_bytes,
-                void* stream);
+/* One level of the same build on the device, no host read: meta [dev] =
+ * (frontier size, node offset) of this level, the next level's written to
+ * meta[2..3]; frontier / next frontier capacity cap_f, node capacity cap_n;
+ * flags / pos [dev] 4 cap_f int32; err [dev] int32 bits: 1 frontier, 2 node
+ * capacity, 4 key digits exhausted (the tree then ends at this level). */
+int gc_bt_level(int64_t* meta, int64_t cap_f, int64_t cap_n, const int64_t* fr, const int64_t* fc,
+                const int64_t* fkey, const int64_t* fpar, int64_t lev, int32_t digits, const double* r_diam,
+                const double* r_lower, const double* r_upper, const int64_t* r_left, const int64_t* r_right,
+                const double* c_diam, const double* c_lower, const double* c_upper, const int64_t* c_left,
+                const int64_t* c_right, double eta, int32_t norm_mode, int64_t* o_row, int64_t* o_col,
+                int8_t* o_state, int64_t* o_level, int64_t* o_key, int64_t* o_parent, int64_t* nr, int64_t* nc,
+                int64_t* nk, int64_t* np, int32_t* flags, int32_t* pos, int32_t* err, void* temp,
+                int64_t temp_bytes, void* stream);
 
 /* Level bookkeeping of the nested bases (replaces the host loop body of
  * greencross gca.py:162-220 around the factor / ACA launches).  Per basis

@@ -64,7 +64,7 @@ _SIGNATURES = {
                     + [c_i64, c_p],
     "gc_bt_leaves_bytes": [c_i64, ctypes.POINTER(c_i64)],
     "gc_bt_leaves": [c_i64] + [c_p] * 11 + [c_i64, c_p],
-    "gc_bt_level": [c_i64, c_p, c_p, c_p, c_p, c_i64, c_i64, ctypes.c_int32] + [c_p] * 10
+    "gc_bt_level": [c_p, c_i64, c_i64, c_p, c_p, c_p, c_p, c_i64, ctypes.c_int32] + [c_p] * 10
                    + [ctypes.c_double, ctypes.c_int32] + [c_p] * 14 + [c_i64, c_p],
     "gc_green_box_rules": [ctypes.c_int, c_p, c_p, c_i64, c_p, c_p, c_p, c_p, c_p],
     "gc_green_factor": [ctypes.POINTER(GcGeom), ctypes.c_int, c_i64, c_i64, c_p, c_p, c_p,

@@ -622,32 +622,41 @@ def _build_block_tree_device(row_root, col_root, eta, mode, device):
         tr = up(rt)
         tc = tr if ct is rt else up(ct)
         cap = max(4096, 32 * (len(rt) + len(ct)))
-        out = [torch.empty(cap, **i64), torch.empty(cap, **i64), torch.empty(cap, dtype=torch.int8, device=device),
-               torch.empty(cap, **i64), torch.empty(cap, **i64), torch.empty(cap, **i64)]
-        front = [torch.tensor([int(row_root.index)], **i64), torch.tensor([int(col_root.index)], **i64),
-                 torch.zeros(1, **i64), torch.full((1,), -1, **i64)]
-        count = torch.zeros(1, **i64)
-        base, lev, m = 0, 0, 1
+        # a pair's level is the deeper of its clusters' depths (a leaf side
+        # stays while the other splits), so this many levels end the tree;
+        # every level runs from device-side sizes, read once at the end
+        levels = min(int(max(rt.depth.max(), ct.depth.max())) + 2, _KEY_DIGITS)
         st = stream_handle()
-        while m:
-            if lev >= _KEY_DIGITS:
-                raise ConfigError("block tree deeper than %d levels" % _KEY_DIGITS)
-            if base + m > cap:                   # grow the node arrays
-                cap = max(2 * cap, base + m)
-                out = [torch.cat([o[:base], torch.empty(cap - base, dtype=o.dtype, device=device)]) for o in out]
-            nxt = [torch.empty(4 * m, **i64) for _ in range(4)]
-            scratch = torch.empty(8 * m, dtype=torch.int32, device=device)
+        while True:
+            cap_f = max(1024, cap // 2)
+            out = [torch.empty(cap, **i64), torch.empty(cap, **i64), torch.empty(cap, dtype=torch.int8, device=device),
+                   torch.empty(cap, **i64), torch.empty(cap, **i64), torch.empty(cap, **i64)]
+            front = [torch.empty(cap_f, **i64) for _ in range(4)]
+            nxt = [torch.empty(cap_f, **i64) for _ in range(4)]
+            for f, v in zip(front, (int(row_root.index), int(col_root.index), 0, -1)):
+                f[:1].fill_(v)
+            meta = torch.zeros(2 * levels + 2, **i64)
+            meta[:1].fill_(1)
+            err = torch.zeros(1, dtype=torch.int32, device=device)
+            scratch = torch.empty(8 * cap_f, dtype=torch.int32, device=device)
             tb = _native.ctypes.c_int64(0)
-            _native.call("gc_bt_level_bytes", m, _native.ctypes.byref(tb))
+            _native.call("gc_bt_level_bytes", cap_f, _native.ctypes.byref(tb))
             temp = torch.empty(max(tb.value, 1), dtype=torch.uint8, device=device)
-            _native.call("gc_bt_level", m, *[ptr(f) for f in front], base, lev, _KEY_DIGITS,
-                         *[ptr(a) for a in tr], *[ptr(a) for a in tc], float(eta), int(mode),
-                         *[ptr(o) for o in out], *[ptr(a) for a in nxt], ptr(count),
-                         ptr(scratch[:4 * m]), ptr(scratch[4 * m:]), ptr(temp), tb.value, st)
-            base += m
-            m = int(count.item())
-            front = [a[:m] for a in nxt]
-            lev += 1
+            for lev in range(levels):
+                _native.call("gc_bt_level", meta.data_ptr() + 16 * lev, cap_f, cap, *[ptr(f) for f in front], lev,
+                             _KEY_DIGITS, *[ptr(a) for a in tr], *[ptr(a) for a in tc], float(eta), int(mode),
+                             *[ptr(o) for o in out], *[ptr(a) for a in nxt], ptr(scratch[:4 * cap_f]),
+                             ptr(scratch[4 * cap_f:]), ptr(err), ptr(temp), tb.value, st)
+                front, nxt = nxt, front
+            mh = meta.cpu().numpy()
+            e = int(err.cpu()[0])
+            if e & 4 or (not e & 3 and mh[2 * levels]):
+                raise ConfigError("block tree deeper than %d levels" % _KEY_DIGITS)
+            if not e & 3:
+                break
+            cap *= 2                                     # frontier or node capacity: rebuild larger
+        base = int(mh[2 * levels + 1])             # nodes of all levels
+        count = torch.zeros(1, **i64)
         n = base
         # the leaves in depth-first order, sorted on the device
         lids, lkey = torch.empty(n, **i64), torch.empty(n, **i64)

@@ -200,12 +200,25 @@ __device__ __forceinline__ double bt_norm_blas(double x, double y, double z, int
     return sqrt(__dadd_rn(__dadd_rn(__dmul_rn(x, x), __dmul_rn(y, y)), __dmul_rn(z, z)));
 }
 
-__global__ void k_bt_eval(int64_t m, const int64_t* __restrict__ fr, const int64_t* __restrict__ fc,
-                          const int64_t* __restrict__ fkey, const int64_t* __restrict__ fpar, int64_t base,
-                          int64_t lev, BtTree R, BtTree C, double eta, int mode, int64_t* __restrict__ o_row,
-                          int64_t* __restrict__ o_col, int8_t* __restrict__ o_state, int64_t* __restrict__ o_level,
-                          int64_t* __restrict__ o_key, int64_t* __restrict__ o_parent, int32_t* __restrict__ flags) {
-    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < m; i += (int64_t)gridDim.x * blockDim.x) {
+// frontier size m and node offset base of this level in meta[0], meta[1]
+// (device); the flags are slot-major with stride cap_f (entries past m are
+// zero, so the scan orders the children exactly as a stride-m layout would)
+__global__ void k_bt_eval(const int64_t* __restrict__ meta, int64_t cap_f, const int64_t* __restrict__ fr,
+                          const int64_t* __restrict__ fc, const int64_t* __restrict__ fkey,
+                          const int64_t* __restrict__ fpar, int64_t lev, BtTree R, BtTree C, double eta, int mode,
+                          int64_t* __restrict__ o_row, int64_t* __restrict__ o_col, int8_t* __restrict__ o_state,
+                          int64_t* __restrict__ o_level, int64_t* __restrict__ o_key, int64_t* __restrict__ o_parent,
+                          int32_t* __restrict__ flags) {
+    const int64_t m = meta[0], base = meta[1];
+    if (m == 0) return;
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < cap_f; i += (int64_t)gridDim.x * blockDim.x) {
+        if (i >= m) {
+            flags[i] = 0;
+            flags[cap_f + i] = 0;
+            flags[2 * cap_f + i] = 0;
+            flags[3 * cap_f + i] = 0;
+            continue;
+        }
         const int64_t r = fr[i], c = fc[i];
         const double d = R.diam[r] > C.diam[c] ? R.diam[r] : C.diam[c];
         double g[3];
@@ -235,29 +248,48 @@ __global__ void k_bt_eval(int64_t m, const int64_t* __restrict__ fr, const int64
         o_parent[id] = fpar[i];
         const bool sub = st == 2;
         flags[i] = sub;                                   // (a, b) = (0, 0): always present
-        flags[m + i] = sub && cs;                         // (0, 1)
-        flags[2 * m + i] = sub && rs;                     // (1, 0)
-        flags[3 * m + i] = sub && rs && cs;               // (1, 1)
+        flags[cap_f + i] = sub && cs;                     // (0, 1)
+        flags[2 * cap_f + i] = sub && rs;                 // (1, 0)
+        flags[3 * cap_f + i] = sub && rs && cs;           // (1, 1)
     }
 }
 
-__global__ void k_bt_children(int64_t m, const int64_t* __restrict__ fr, const int64_t* __restrict__ fc,
-                              const int64_t* __restrict__ fkey, int64_t base, int64_t scale, BtTree R, BtTree C,
+// children of the subdivided pairs; the next level's meta (m, base) and
+// err bits: 1 frontier capacity, 2 node capacity, 4 key digits exhausted
+__global__ void k_bt_children(int64_t* __restrict__ meta, int64_t cap_f, int64_t cap_n, int64_t lev, int32_t digits,
+                              const int64_t* __restrict__ fr, const int64_t* __restrict__ fc,
+                              const int64_t* __restrict__ fkey, int64_t scale, BtTree R, BtTree C,
                               const int32_t* __restrict__ flags, const int32_t* __restrict__ pos,
                               int64_t* __restrict__ nr, int64_t* __restrict__ nc, int64_t* __restrict__ nk,
-                              int64_t* __restrict__ np, int64_t* __restrict__ count) {
-    for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < 4 * m; t += (int64_t)gridDim.x * blockDim.x) {
-        if (t == 4 * m - 1) *count = (int64_t)pos[t] + flags[t];
+                              int64_t* __restrict__ np, int32_t* __restrict__ err) {
+    const int64_t m = meta[0], base = meta[1];
+    const int64_t total = 4 * cap_f;
+    if (blockIdx.x == 0 && threadIdx.x == 0) {
+        int64_t count = m == 0 ? 0 : (int64_t)pos[total - 1] + flags[total - 1];
+        int32_t e = 0;
+        if (count > cap_f) e |= 1;
+        if (base + m + count > cap_n) e |= 2;
+        if (count > 0 && lev + 1 >= digits) e |= 4;
+        if (e) {
+            atomicOr(err, e);
+            count = 0;
+        }
+        meta[2] = count;
+        meta[3] = base + m;
+    }
+    if (m == 0) return;
+    for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < total; t += (int64_t)gridDim.x * blockDim.x) {
         if (!flags[t]) continue;
-        const int q = (int)(t / m);
-        const int64_t i = t - (int64_t)q * m;
+        const int q = (int)(t / cap_f);
+        const int64_t i = t - (int64_t)q * cap_f;
+        const int64_t p = pos[t];
+        if (p >= cap_f) continue;                         // overflow: reported above
         const int a = q >> 1, b = q & 1;
         const int64_t r = fr[i], c = fc[i];
         const bool rs = R.left[r] >= 0, cs = C.left[c] >= 0;
         const int64_t rk = a == 0 ? (rs ? R.left[r] : r) : R.right[r];
         const int64_t ck = b == 0 ? (cs ? C.left[c] : c) : C.right[c];
         const int64_t dig = a * (cs ? 2 : 1) + b;
-        const int64_t p = pos[t];
         nr[p] = rk;
         nc[p] = ck;
         nk[p] = fkey[i] + dig * scale;
@@ -269,49 +301,55 @@ __global__ void k_bt_children(int64_t m, const int64_t* __restrict__ fr, const i
 
 extern "C" {
 
-// One level of the device block tree.  tree arrays [dev] as gc_block_tree;
-// frontier [dev] fr, fc, fkey, fpar (m); node records written at out_*[base
-// .. base + m) [dev]; next frontier [dev] nr, nc, nk, np (capacity 4m) and
-// its size in *count [dev int64]; flags / pos [dev] 4m int32 each; temp
-// [dev] of gc_bt_level_bytes(m) bytes.
-int gc_bt_level_bytes(int64_t m, int64_t* bytes) {
+// One level of the device block tree without a host read: the level's
+// frontier size and node offset in meta[0..1] [dev], the next level's written
+// to meta[2..3]; tree arrays [dev] as gc_block_tree; frontier [dev] fr, fc,
+// fkey, fpar (capacity cap_f); node records at out_*[base ..] [dev]
+// (capacity cap_n); next frontier [dev] nr, nc, nk, np (capacity cap_f);
+// flags / pos [dev] 4 cap_f int32 each; err [dev] int32 (1 frontier, 2 node
+// capacity, 4 key digits exhausted: the level then ends the tree); temp
+// [dev] of gc_bt_level_bytes(cap_f) bytes.  An empty level is a no-op.
+int gc_bt_level_bytes(int64_t cap_f, int64_t* bytes) {
     using namespace gcb;
     size_t tb = 0;
-    cudaError_t e = cub::DeviceScan::ExclusiveSum(nullptr, tb, (const int32_t*)nullptr, (int32_t*)nullptr, (int)(4 * m));
+    cudaError_t e = cub::DeviceScan::ExclusiveSum(nullptr, tb, (const int32_t*)nullptr, (int32_t*)nullptr,
+                                                  (int)(4 * cap_f));
     if (e != cudaSuccess) return cuda_status(e, "gc_bt_level_bytes");
     *bytes = (int64_t)tb;
     return GC_OK;
 }
 
-int gc_bt_level(int64_t m, const int64_t* fr, const int64_t* fc, const int64_t* fkey, const int64_t* fpar,
-                int64_t base, int64_t lev, int32_t digits, const double* r_diam, const double* r_lower,
-                const double* r_upper, const int64_t* r_left, const int64_t* r_right, const double* c_diam,
-                const double* c_lower, const double* c_upper, const int64_t* c_left, const int64_t* c_right,
-                double eta, int32_t norm_mode, int64_t* o_row, int64_t* o_col, int8_t* o_state, int64_t* o_level,
-                int64_t* o_key, int64_t* o_parent, int64_t* nr, int64_t* nc, int64_t* nk, int64_t* np,
-                int64_t* count, int32_t* flags, int32_t* pos, void* temp, int64_t temp_bytes, void* stream) {
+int gc_bt_level(int64_t* meta, int64_t cap_f, int64_t cap_n, const int64_t* fr, const int64_t* fc,
+                const int64_t* fkey, const int64_t* fpar, int64_t lev, int32_t digits, const double* r_diam,
+                const double* r_lower, const double* r_upper, const int64_t* r_left, const int64_t* r_right,
+                const double* c_diam, const double* c_lower, const double* c_upper, const int64_t* c_left,
+                const int64_t* c_right, double eta, int32_t norm_mode, int64_t* o_row, int64_t* o_col,
+                int8_t* o_state, int64_t* o_level, int64_t* o_key, int64_t* o_parent, int64_t* nr, int64_t* nc,
+                int64_t* nk, int64_t* np, int32_t* flags, int32_t* pos, int32_t* err, void* temp,
+                int64_t temp_bytes, void* stream) {
     using namespace gcb;
-    if (m <= 0 || 4 * m >= (1LL << 31) || (norm_mode != 0 && norm_mode != 1) || lev >= digits || eta <= 0.0) {
+    if (cap_f <= 0 || 4 * cap_f >= (1LL << 31) || (norm_mode != 0 && norm_mode != 1) || lev >= digits ||
+        eta <= 0.0 || !meta || !err) {
         set_error(GC_ERR_CONFIG, "gc_bt_level: bad arguments");
         return GC_ERR_CONFIG;
     }
     cudaStream_t st = (cudaStream_t)stream;
     const BtTree R{r_diam, r_lower, r_upper, r_left, r_right};
     const BtTree C{c_diam, c_lower, c_upper, c_left, c_right};
-    int64_t grid = (m + 255) / 256;
+    int64_t grid = (cap_f + 255) / 256;
     if (grid > 148 * 16) grid = 148 * 16;
-    k_bt_eval<<<(unsigned)grid, 256, 0, st>>>(m, fr, fc, fkey, fpar, base, lev, R, C, eta, norm_mode, o_row, o_col,
-                                              o_state, o_level, o_key, o_parent, flags);
+    k_bt_eval<<<(unsigned)grid, 256, 0, st>>>(meta, cap_f, fr, fc, fkey, fpar, lev, R, C, eta, norm_mode, o_row,
+                                              o_col, o_state, o_level, o_key, o_parent, flags);
     GC_CHECK_LAUNCH("k_bt_eval");
     size_t tb = (size_t)temp_bytes;
-    cudaError_t e = cub::DeviceScan::ExclusiveSum(temp, tb, flags, pos, (int)(4 * m), st);
+    cudaError_t e = cub::DeviceScan::ExclusiveSum(temp, tb, flags, pos, (int)(4 * cap_f), st);
     if (e != cudaSuccess) return cuda_status(e, "gc_bt_level scan");
     int64_t scale = 1;
     for (int k = 0; k < digits - 1 - lev; ++k) scale *= 4;
-    int64_t cgrid = (4 * m + 255) / 256;
+    int64_t cgrid = (4 * cap_f + 255) / 256;
     if (cgrid > 148 * 16) cgrid = 148 * 16;
-    k_bt_children<<<(unsigned)cgrid, 256, 0, st>>>(m, fr, fc, fkey, base, scale, R, C, flags, pos, nr, nc, nk, np,
-                                                   count);
+    k_bt_children<<<(unsigned)cgrid, 256, 0, st>>>(meta, cap_f, cap_n, lev, digits, fr, fc, fkey, scale, R, C,
+                                                   flags, pos, nr, nc, nk, np, err);
     GC_CHECK_LAUNCH("k_bt_children");
     return GC_OK;
 }
